@@ -1,0 +1,149 @@
+/*
+ * tsmpc.h — C ABI of the B200-native scenario-tree APG solver (libtsmpc.so).
+ *
+ * This is the drop-in boundary for the reference's accelerated dual proximal
+ * gradient path.  The reference (`treesmpc`, pure Python) has no FFI layer; the
+ * entry points below replace its Python solver functions one for one and are
+ * bound from Python with ctypes by `paper_1604_01074_b200/_native.py`
+ * (see INTEGRATION.md for the binding a reference maintainer would add):
+ *
+ *   tsmpc_plan_create     replaces the per-(model, tree) setup that the reference
+ *                         does inside SolveContext.__init__
+ *                         (pkg/src/treesmpc/factor.py:86-128) plus the upload of
+ *                         factor_step outputs (factor.py:67-76) and the dual
+ *                         scaling (engine.py:120-143, 239-277).
+ *   tsmpc_set_cache       uploads one StageCache (elimination.py:54-65,114-158).
+ *   tsmpc_solve           engine.solve (engine.py:485-601): fixed-iteration APG
+ *                         loop, ergodic averages, residual, duality gap.
+ *   tsmpc_solve_step      factor.solve_step / SolveContext.solve
+ *                         (factor.py:174-217).
+ *   tsmpc_prox            engine.prox_g (engine.py:157-183).
+ *   tsmpc_dual_operator   one application of the scaled dual-gradient operator used
+ *                         by engine.compute_lambda (engine.py:286-337).
+ *
+ * Conventions: every array is host memory, float64, C-contiguous row-major,
+ * with the reference's shapes (points.py:17-57): per-node arrays have n_nodes
+ * rows, per-edge arrays n_edges = n_nodes-1 rows, row e <-> node e+1.  Device
+ * memory is owned by the plan.  A plan is not thread-safe; use one host thread
+ * per plan.  Functions return TSMPC_OK (0) or a negative status; the message of
+ * the last failure on the calling thread is returned by tsmpc_last_error().
+ */
+#ifndef TSMPC_H
+#define TSMPC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSMPC_OK               0
+#define TSMPC_ERR_DIMENSION   -1   /* -> DimensionError  */
+#define TSMPC_ERR_VALIDATION  -2   /* -> ValidationError */
+#define TSMPC_ERR_CUDA        -3   /* -> DeviceError     */
+#define TSMPC_ERR_NCCL        -4   /* -> DeviceError     */
+#define TSMPC_ERR_ARGUMENT    -5   /* NULL / out-of-range argument */
+
+typedef struct tsmpc_plan tsmpc_plan;
+
+/* Model, factor matrices, scaling and tree of one plan (all host pointers). */
+typedef struct tsmpc_problem {
+  int32_t n_x, n_u, n_v, n_d, n_e; /* states, inputs, reduced inputs, demands, junctions */
+  int32_t N;                       /* horizon (stages 0..N)                            */
+  int32_t n_nodes;
+  /* model / factor (factor.py:38-76, elimination.py:34-103) */
+  const double* A;        /* n_x*n_x                                   */
+  const double* B;        /* n_x*n_u                                   */
+  const double* L;        /* n_u*n_v  orthonormal basis of ker(E)      */
+  const double* Bbar;     /* n_x*n_v  = B L                            */
+  const double* Phi;      /* n_v*n_x  = -Rbar^{-1} Bbar'               */
+  const double* Psi;      /* n_v*n_u  = -Rbar^{-1} L'                  */
+  const double* Wu;       /* n_u*n_u  control-increment weight         */
+  const double* E;        /* n_e*n_u  junction matrix                  */
+  const double* E_pinvT;  /* n_e*n_u  = ((E')(E E')^{-1})'  (gap)      */
+  const double* u_min; const double* u_max;   /* n_u */
+  const double* x_min; const double* x_max;   /* n_x */
+  const double* x_s;                          /* n_x */
+  double W_alpha, Wx, gamma_d;
+  /* dual scaling (engine.py:120-143); NULL -> identity */
+  const double* sig_stage;   /* N      */
+  const double* zeta_stage;  /* N      */
+  const double* psi_stage;   /* N*n_u  */
+  /* tree (tree.py:31-94) */
+  const int64_t* stage_starts; /* N+2     */
+  const int64_t* anc;          /* n_nodes */
+  const int64_t* child_start;  /* n_nodes */
+  const int64_t* child_stop;   /* n_nodes */
+  const double* prob;          /* n_nodes */
+} tsmpc_problem;
+
+/* Host buffers filled by tsmpc_solve; any pointer may be NULL to skip it. */
+typedef struct tsmpc_result {
+  double* u0;          /* n_u             = u_avg[0]                          */
+  double* x;           /* n_nodes*n_x     last primal iterate                 */
+  double* u;           /* n_edges*n_u                                          */
+  double* x_avg;       /* n_nodes*n_x     ergodic states                       */
+  double* u_avg;       /* n_edges*n_u     ergodic controls                     */
+  double* dual_sig;    /* n_edges*n_x     final dual, scaled coordinates       */
+  double* dual_zeta;   /* n_edges*n_x                                          */
+  double* dual_psi;    /* n_edges*n_u                                          */
+  double* resid_trace; /* iters (only with TSMPC_RECORD_RESIDUALS)             */
+  double residual_inf; /* out */
+  double gap;          /* out (NaN when TSMPC_SKIP_GAP)                        */
+  double device_ms;    /* out: CUDA-event time of the on-device iteration loop */
+  int32_t iterations;  /* out: iterations actually run                         */
+} tsmpc_result;
+
+#define TSMPC_RECORD_RESIDUALS 1   /* residual_inf of every iteration -> resid_trace */
+#define TSMPC_SKIP_GAP         2   /* do not evaluate the duality gap               */
+#define TSMPC_KEEP_DEVICE      4   /* leave results on the device (no D2H)          */
+
+/* Problem / tree geometry and device planning.  Returns NULL on failure. */
+tsmpc_plan* tsmpc_plan_create(const tsmpc_problem* prob, int device);
+void tsmpc_plan_destroy(tsmpc_plan* plan);
+
+/* Per-forecast stage cache (elimination.py:114-158).
+ * beta n_edges*n_v, uhat n_edges*n_u, evec n_edges*n_x, q n_u,
+ * prices N*n_u (alpha1 + alpha2(k+j) per stage), jrhs n_edges*n_e (= -Ed d per
+ * edge) and gdd n_edges*n_x (= Gd d per edge) are only read by the duality gap
+ * (engine.py:347-480) and may be NULL when TSMPC_SKIP_GAP is always used. */
+int tsmpc_set_cache(tsmpc_plan* plan, const double* beta, const double* uhat,
+                    const double* evec, const double* q, const double* prices,
+                    const double* jrhs, const double* gdd);
+
+/* engine.solve: `iters` APG iterations at step size `lam` from y0 = y_-1 = warm
+ * (three blocks, scaled coordinates) or zero when warm_sig == NULL.
+ * theta / coef: optional momentum tables of length iters (NULL -> computed). */
+int tsmpc_solve(tsmpc_plan* plan, const double* p, int32_t iters, double lam,
+                const double* warm_sig, const double* warm_zeta, const double* warm_psi,
+                const double* theta, const double* coef, int32_t flags,
+                tsmpc_result* out);
+
+/* factor.solve_step: z = argmin <z, H'w> + f(z) for an unscaled dual w. */
+int tsmpc_solve_step(tsmpc_plan* plan, const double* w_sig, const double* w_zeta,
+                     const double* w_psi, const double* p, double* x_out, double* u_out);
+
+/* engine.prox_g on n_rows rows with prox parameter `lam`; scaling rows per edge
+ * are taken from the plan when use_scaling != 0 (rows must then equal n_edges). */
+int tsmpc_prox(tsmpc_plan* plan, int32_t n_rows, const double* t_sig,
+               const double* t_zeta, const double* t_psi, double lam, int32_t use_scaling,
+               double* o_sig, double* o_zeta, double* o_psi);
+
+/* Power-iteration support for compute_lambda: for the dual vector y resident on
+ * the device (set by tsmpc_dual_operator_set), computes Dy = S H (z(0) - z(S y))
+ * with a zero-demand cache built from beta0, stores Dy as the next y and returns
+ * <y, Dy> and <Dy, Dy>.  Used by `compute_lambda` in engine.py of the package. */
+int tsmpc_dual_operator_begin(tsmpc_plan* plan, const double* beta0);
+int tsmpc_dual_operator_set_ones(tsmpc_plan* plan);
+int tsmpc_dual_operator_step(tsmpc_plan* plan, double* y_dot_dy, double* dy_dot_dy,
+                             double* y_dot_y);
+
+/* Introspection (tests / bench). */
+int tsmpc_plan_info(const tsmpc_plan* plan, int64_t* info, int32_t n_info);
+const char* tsmpc_last_error(void);
+int tsmpc_device_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSMPC_H */

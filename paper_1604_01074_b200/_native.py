@@ -1,0 +1,151 @@
+"""ctypes binding of ``libtsmpc.so`` (C ABI declared in ``include/tsmpc.h``).
+
+The shared library is built in-tree by :func:`build_library` (nvcc, sm_100a)
+and loaded from this package directory.  There is deliberately no fallback: if
+the library or a CUDA device is missing, every solver entry point raises
+:class:`~.errors.DeviceError`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import pathlib
+import subprocess
+
+import numpy as np
+
+from .errors import DeviceError, DimensionError, TreeSmpcError, ValidationError
+
+PKG_DIR = pathlib.Path(__file__).resolve().parent
+LIB_PATH = PKG_DIR / "libtsmpc.so"
+CSRC = PKG_DIR / "csrc"
+SOURCES = ["tsmpc_apg.cu", "tsmpc_aux.cu", "tsmpc_capi.cu"]
+
+OK, ERR_DIMENSION, ERR_VALIDATION, ERR_CUDA, ERR_NCCL, ERR_ARGUMENT = 0, -1, -2, -3, -4, -5
+RECORD_RESIDUALS, SKIP_GAP, KEEP_DEVICE = 1, 2, 4
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_ip = ctypes.POINTER(ctypes.c_int64)
+
+
+class Problem(ctypes.Structure):
+    _fields_ = [
+        ("n_x", ctypes.c_int32), ("n_u", ctypes.c_int32), ("n_v", ctypes.c_int32),
+        ("n_d", ctypes.c_int32), ("n_e", ctypes.c_int32), ("N", ctypes.c_int32),
+        ("n_nodes", ctypes.c_int32),
+        ("A", _dp), ("B", _dp), ("L", _dp), ("Bbar", _dp), ("Phi", _dp), ("Psi", _dp),
+        ("Wu", _dp), ("E", _dp), ("E_pinvT", _dp),
+        ("u_min", _dp), ("u_max", _dp), ("x_min", _dp), ("x_max", _dp), ("x_s", _dp),
+        ("W_alpha", ctypes.c_double), ("Wx", ctypes.c_double), ("gamma_d", ctypes.c_double),
+        ("sig_stage", _dp), ("zeta_stage", _dp), ("psi_stage", _dp),
+        ("stage_starts", _ip), ("anc", _ip), ("child_start", _ip), ("child_stop", _ip),
+        ("prob", _dp),
+    ]
+
+
+class Result(ctypes.Structure):
+    _fields_ = [
+        ("u0", _dp), ("x", _dp), ("u", _dp), ("x_avg", _dp), ("u_avg", _dp),
+        ("dual_sig", _dp), ("dual_zeta", _dp), ("dual_psi", _dp), ("resid_trace", _dp),
+        ("residual_inf", ctypes.c_double), ("gap", ctypes.c_double),
+        ("device_ms", ctypes.c_double), ("iterations", ctypes.c_int32),
+    ]
+
+
+# name -> (restype, argtypes); the exported symbol set of include/tsmpc.h
+SIGNATURES = {
+    "tsmpc_plan_create": (ctypes.c_void_p, [ctypes.POINTER(Problem), ctypes.c_int]),
+    "tsmpc_plan_destroy": (None, [ctypes.c_void_p]),
+    "tsmpc_set_cache": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, _dp, _dp, _dp, _dp, _dp]),
+    "tsmpc_solve": (ctypes.c_int, [ctypes.c_void_p, _dp, ctypes.c_int32, ctypes.c_double,
+                                   _dp, _dp, _dp, _dp, _dp, ctypes.c_int32,
+                                   ctypes.POINTER(Result)]),
+    "tsmpc_solve_step": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, _dp, _dp, _dp, _dp]),
+    "tsmpc_prox": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, _dp, _dp, _dp,
+                                  ctypes.c_double, ctypes.c_int32, _dp, _dp, _dp]),
+    "tsmpc_dual_operator_begin": (ctypes.c_int, [ctypes.c_void_p, _dp]),
+    "tsmpc_dual_operator_set_ones": (ctypes.c_int, [ctypes.c_void_p]),
+    "tsmpc_dual_operator_step": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, _dp]),
+    "tsmpc_plan_info": (ctypes.c_int, [ctypes.c_void_p, _ip, ctypes.c_int32]),
+    "tsmpc_last_error": (ctypes.c_char_p, []),
+    "tsmpc_device_count": (ctypes.c_int, []),
+}
+
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC", "-shared"]
+
+
+def build_library(force: bool = False, verbose: bool = False) -> pathlib.Path:
+    """Compile ``libtsmpc.so`` in-tree for sm_100a (cross-compiles without a GPU)."""
+    srcs = [CSRC / s for s in SOURCES]
+    deps = srcs + list(CSRC.glob("*.cuh")) + [PKG_DIR.parent / "include" / "tsmpc.h"]
+    if not force and LIB_PATH.exists():
+        newest = max(p.stat().st_mtime for p in deps)
+        if LIB_PATH.stat().st_mtime >= newest:
+            return LIB_PATH
+    nvcc = os.environ.get("NVCC", "nvcc")
+    cmd = [nvcc, *NVCC_FLAGS, "-o", str(LIB_PATH), *map(str, srcs)]
+    res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise DeviceError(f"nvcc failed ({' '.join(cmd)}):\n{res.stderr[-4000:]}")
+    if verbose and res.stderr:
+        print(res.stderr)
+    return LIB_PATH
+
+
+_LIB = None
+
+
+def load_library() -> ctypes.CDLL:
+    """Load (never silently skip) the native library and bind its signatures."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not LIB_PATH.exists():
+        raise DeviceError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                          "(or paper_1604_01074_b200._native.build_library())")
+    lib = ctypes.CDLL(str(LIB_PATH))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _LIB = lib
+    return lib
+
+
+def last_error() -> str:
+    msg = load_library().tsmpc_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == OK:
+        return
+    msg = f"{what}: {last_error()}" if what else last_error()
+    if rc == ERR_DIMENSION:
+        raise DimensionError(msg)
+    if rc == ERR_VALIDATION:
+        raise ValidationError(msg)
+    if rc in (ERR_CUDA, ERR_NCCL):
+        raise DeviceError(msg)
+    raise TreeSmpcError(msg)
+
+
+def device_count() -> int:
+    return int(load_library().tsmpc_device_count())
+
+
+def dptr(a) -> "ctypes._Pointer | None":
+    """float64 C-contiguous pointer (None passes NULL)."""
+    if a is None:
+        return None
+    if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous):
+        raise TypeError("expected a C-contiguous float64 array")
+    return a.ctypes.data_as(_dp)
+
+
+def iptr(a):
+    if not (isinstance(a, np.ndarray) and a.dtype == np.int64 and a.flags.c_contiguous):
+        raise TypeError("expected a C-contiguous int64 array")
+    return a.ctypes.data_as(_ip)

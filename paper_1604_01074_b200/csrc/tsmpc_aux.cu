@@ -1,0 +1,424 @@
+// tsmpc_aux.cu — per-edge kernels around the persistent APG loop:
+//   prox_g as a standalone operator        (engine.py:146-183)
+//   dual-gradient operator for compute_lambda's power iteration (engine.py:286-337)
+//   duality gap                            (engine.py:347-480)
+//   deterministic fixed-order reductions (bitwise run-to-run reproducible sums)
+// All kernels use one warp per edge row; rows are at most 128 wide (4 per lane).
+#include "tsmpc_aux.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace tsmpc {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
+  return v;
+}
+__device__ __forceinline__ double clip(double v, double lo, double hi) { return fmin(fmax(v, lo), hi); }
+
+// ---------------------------------------------------------------- reductions
+// out[c] = sum_i vals[i * ncols + c], fixed order (one block, 1024 threads).
+__global__ void __launch_bounds__(1024) reduce_cols_kernel(const double* __restrict__ vals, int n,
+                                                           int ncols, double* __restrict__ out) {
+  __shared__ double red[1024];
+  for (int c = 0; c < ncols; ++c) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += 1024) s += vals[(size_t)i * ncols + c];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 512; w > 0; w >>= 1) {
+      if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[c] = red[0];
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- prox_g
+__global__ void prox_kernel(ProxArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int r = gw; r < a.rows; r += nw) {
+    const int st = a.edge_stage ? a.edge_stage[r] : 0;
+    const double ds = a.sig_stage ? a.sig_stage[st] : 1.0;
+    const double dz = a.zeta_stage ? a.zeta_stage[st] : 1.0;
+    double ss = 0.0, sz = 0.0;
+    for (int i = lane; i < a.nx; i += 32) {
+      const double ts = a.t_sig[(size_t)r * a.nx + i], tz = a.t_zeta[(size_t)r * a.nx + i];
+      const double gs = fmax(ts, ds * a.x_s[i]) - ts;
+      const double gz = clip(tz, dz * a.x_min[i], dz * a.x_max[i]) - tz;
+      ss = fma(gs, gs, ss);
+      sz = fma(gz, gz, sz);
+    }
+    ss = warp_sum(ss);
+    sz = warp_sum(sz);
+    const double ws = a.lam * a.Wx / ds, wz = a.lam * a.gamma_d / dz;
+    const double ds_ = sqrt(ss), dz_ = sqrt(sz);
+    const double fs = ds_ > ws ? ws / ds_ : 1.0, fz = dz_ > wz ? wz / dz_ : 1.0;
+    for (int i = lane; i < a.nx; i += 32) {
+      const size_t o = (size_t)r * a.nx + i;
+      const double ts = a.t_sig[o], tz = a.t_zeta[o];
+      a.o_sig[o] = ts + fs * (fmax(ts, ds * a.x_s[i]) - ts);
+      a.o_zeta[o] = tz + fz * (clip(tz, dz * a.x_min[i], dz * a.x_max[i]) - tz);
+    }
+    for (int j = lane; j < a.nu; j += 32) {
+      const size_t o = (size_t)r * a.nu + j;
+      const double dp = a.psi_stage ? a.psi_stage[(size_t)st * a.nu + j] : 1.0;
+      a.o_psi[o] = clip(a.t_psi[o], dp * a.u_min[j], dp * a.u_max[j]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- power iteration
+// rows[e] = (sum y_sig^2, sum y_zeta^2, sum y_psi^2)
+__global__ void dual_sq_rows_kernel(EdgeCtx c, const double* __restrict__ y, double* rows) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const size_t zoff = (size_t)c.E * c.NXP, poff = 2 * zoff;
+  for (int e = gw; e < c.E; e += nw) {
+    double s = 0, z = 0, p = 0;
+    for (int i = lane; i < c.nx; i += 32) {
+      const double a = y[(size_t)e * c.NXP + i], b = y[zoff + (size_t)e * c.NXP + i];
+      s = fma(a, a, s);
+      z = fma(b, b, z);
+    }
+    for (int j = lane; j < c.nu; j += 32) {
+      const double a = y[poff + (size_t)e * c.NUP + j];
+      p = fma(a, a, p);
+    }
+    s = warp_sum(s); z = warp_sum(z); p = warp_sum(p);
+    if (lane == 0) { rows[3 * e] = s; rows[3 * e + 1] = z; rows[3 * e + 2] = p; }
+  }
+}
+
+// y /= sqrt(sq[0] + sq[1] + sq[2])
+__global__ void dual_normalize_kernel(EdgeCtx c, double* y, const double* sq) {
+  const double norm = sqrt((sq[0] + sq[1]) + sq[2]);
+  const size_t n = 2 * (size_t)c.E * c.NXP + (size_t)c.E * c.NUP;
+  for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n; k += (size_t)gridDim.x * blockDim.x)
+    y[k] = y[k] / norm;
+}
+
+// Dy = S (z0 - H z);  rows[e] = (<y,Dy> by block, <Dy,Dy> by block); y <- Dy
+__global__ void dual_apply_kernel(EdgeCtx c, double* y, const double* __restrict__ X,
+                                  const double* __restrict__ U, const double* __restrict__ Z0X,
+                                  const double* __restrict__ Z0U, double* rows) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const size_t zoff = (size_t)c.E * c.NXP, poff = 2 * zoff;
+  for (int e = gw; e < c.E; e += nw) {
+    const int st = c.edge_stage[e];
+    const double ds = c.sig_stage ? c.sig_stage[st] : 1.0;
+    const double dz = c.zeta_stage ? c.zeta_stage[st] : 1.0;
+    double a[6] = {0, 0, 0, 0, 0, 0};
+    for (int i = lane; i < c.nx; i += 32) {
+      const size_t ox = (size_t)(e + 1) * c.NXP + i, o = (size_t)e * c.NXP + i;
+      const double d = Z0X[ox] - X[ox];
+      const double dsg = d * ds, dzt = d * dz;
+      a[0] = fma(y[o], dsg, a[0]);
+      a[1] = fma(y[zoff + o], dzt, a[1]);
+      a[3] = fma(dsg, dsg, a[3]);
+      a[4] = fma(dzt, dzt, a[4]);
+      y[o] = dsg;
+      y[zoff + o] = dzt;
+    }
+    for (int j = lane; j < c.nu; j += 32) {
+      const size_t o = (size_t)e * c.NUP + j;
+      const double dp = c.psi_stage ? c.psi_stage[(size_t)st * c.NUP + j] : 1.0;
+      const double d = (Z0U[o] - U[o]) * dp;
+      a[2] = fma(y[poff + o], d, a[2]);
+      a[5] = fma(d, d, a[5]);
+      y[poff + o] = d;
+    }
+#pragma unroll
+    for (int k = 0; k < 6; ++k) a[k] = warp_sum(a[k]);
+    if (lane == 0)
+      for (int k = 0; k < 6; ++k) rows[6 * (size_t)e + k] = a[k];
+  }
+}
+
+// ---------------------------------------------------------------- duality gap
+// Dual side, part 1: y_hat = projection of the unscaled dual onto dom g*, plus
+// the conjugate terms (engine.py:435-455).  cols[e*10 + 7..9].
+__global__ void gap_dual_project_kernel(EdgeCtx c, const double* __restrict__ y, double* what,
+                                        double* cols) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const size_t zoff = (size_t)c.E * c.NXP, poff = 2 * zoff;
+  for (int e = gw; e < c.E; e += nw) {
+    const int st = c.edge_stage[e];
+    const double ds = c.sig_stage ? c.sig_stage[st] : 1.0;
+    const double dz = c.zeta_stage ? c.zeta_stage[st] : 1.0;
+    double ns = 0, nz = 0;
+    for (int i = lane; i < c.nx; i += 32) {
+      const size_t o = (size_t)e * c.NXP + i;
+      const double s = fmin(y[o] * ds, 0.0), z = y[zoff + o] * dz;
+      ns = fma(s, s, ns);
+      nz = fma(z, z, nz);
+    }
+    ns = sqrt(warp_sum(ns));
+    nz = sqrt(warp_sum(nz));
+    const double fs = ns > c.Wx ? c.Wx / ns : 1.0;
+    const double fz = nz > c.gamma_d ? c.gamma_d / nz : 1.0;
+    const bool os = ns > c.Wx, oz = nz > c.gamma_d;
+    double k7 = 0, k8 = 0, k9 = 0;
+    for (int i = lane; i < c.nx; i += 32) {
+      const size_t o = (size_t)e * c.NXP + i;
+      double s = fmin(y[o] * ds, 0.0), z = y[zoff + o] * dz;
+      if (os) s *= fs;
+      if (oz) z *= fz;
+      what[o] = s;
+      what[zoff + o] = z;
+      k7 = fma(s, c.x_s[i], k7);
+      k8 += z > 0 ? z * c.x_max[i] : z * c.x_min[i];
+    }
+    for (int j = lane; j < c.nu; j += 32) {
+      const size_t o = (size_t)e * c.NUP + j;
+      const double dp = c.psi_stage ? c.psi_stage[(size_t)st * c.NUP + j] : 1.0;
+      const double p = y[poff + o] * dp;
+      what[poff + o] = p;
+      k9 += p > 0 ? p * c.u_max[j] : p * c.u_min[j];
+    }
+    k7 = warp_sum(k7); k8 = warp_sum(k8); k9 = warp_sum(k9);
+    if (lane == 0) {
+      cols[10 * (size_t)e + 7] = k7;
+      cols[10 * (size_t)e + 8] = k8;
+      cols[10 * (size_t)e + 9] = k9;
+    }
+  }
+}
+
+// p_e (W_alpha price_stage . u_e + du' Wu du), du = u_e - u_parent (or q).
+__device__ double smooth_term(const EdgeCtx& c, int e, const double* U, int ldu, double* sh) {
+  const int lane = threadIdx.x & 31;
+  const int st = c.edge_stage[e];
+  const int pa = c.anc[e + 1] - 1;
+  double econ = 0.0;
+  for (int j = lane; j < c.nu; j += 32) {
+    const double u = U[(size_t)e * ldu + j];
+    const double up = pa >= 0 ? U[(size_t)pa * ldu + j] : c.q[j];
+    sh[j] = u - up;
+    econ = fma(c.prices[(size_t)st * c.nu + j], u, econ);
+  }
+  __syncwarp();
+  double quad = 0.0;
+  for (int j = lane; j < c.nu; j += 32) {
+    double wd = 0.0;
+    for (int k = 0; k < c.nu; ++k) wd = fma(c.Wu[(size_t)j * c.nu + k], sh[k], wd);
+    quad = fma(sh[j], wd, quad);
+  }
+  __syncwarp();
+  econ = warp_sum(econ);
+  quad = warp_sum(quad);
+  return c.prob_edge[e] * (c.W_alpha * econ + quad);
+}
+
+// Dual side, part 2 (after the solve step at y_hat): pairing <H z, y_hat> and the
+// smooth cost of z_hat.u (engine.py:474-479).  cols[e*10 + 3..6].
+__global__ void gap_dual_terms_kernel(EdgeCtx c, const double* __restrict__ what,
+                                      const double* __restrict__ X, const double* __restrict__ U,
+                                      double* cols) {
+  __shared__ double shm[8][128];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const size_t zoff = (size_t)c.E * c.NXP, poff = 2 * zoff;
+  for (int e = gw; e < c.E; e += nw) {
+    double k3 = 0, k4 = 0, k5 = 0;
+    for (int i = lane; i < c.nx; i += 32) {
+      const double x = X[(size_t)(e + 1) * c.NXP + i];
+      k3 = fma(x, what[(size_t)e * c.NXP + i], k3);
+      k4 = fma(x, what[zoff + (size_t)e * c.NXP + i], k4);
+    }
+    for (int j = lane; j < c.nu; j += 32) k5 = fma(U[(size_t)e * c.NUP + j], what[poff + (size_t)e * c.NUP + j], k5);
+    k3 = warp_sum(k3); k4 = warp_sum(k4); k5 = warp_sum(k5);
+    const double k6 = smooth_term(c, e, U, c.NUP, shm[wl]);
+    if (lane == 0) {
+      cols[10 * (size_t)e + 3] = k3;
+      cols[10 * (size_t)e + 4] = k4;
+      cols[10 * (size_t)e + 5] = k5;
+      cols[10 * (size_t)e + 6] = k6;
+    }
+  }
+}
+
+// Primal side, part 1 (n_e == 1): exact multiplier bisection (engine.py:383-405).
+__device__ __forceinline__ double balance1(const EdgeCtx& c, const double* u, double mu) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int j = lane; j < c.nu; j += 32) {
+    const double a = c.Ej[j];
+    s = fma(clip(u[j] - mu * a, c.u_min[j], c.u_max[j]), a, s);
+  }
+  return warp_sum(s);
+}
+
+__global__ void gap_project_bisect_kernel(EdgeCtx c, const double* __restrict__ uavg, double* uf) {
+  __shared__ double shm[8][128];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  double* u = shm[wl];
+  for (int e = gw; e < c.E; e += nw) {
+    for (int j = lane; j < c.nu; j += 32) u[j] = uavg[(size_t)e * c.NUP + j];
+    __syncwarp();
+    const double b = c.jrhs[(size_t)e * c.ne];
+    double lo = -1.0, hi = 1.0;
+    for (int it = 0; it < 60; ++it) {
+      const bool need = balance1(c, u, lo) < b;
+      const bool high = balance1(c, u, hi) > b;
+      if (!need && !high) break;
+      if (need) lo *= 2.0;
+      if (high) hi *= 2.0;
+    }
+    for (int it = 0; it < 80; ++it) {
+      const double mid = 0.5 * (lo + hi);
+      const bool th = balance1(c, u, mid) > b;
+      lo = th ? mid : lo;
+      hi = th ? hi : mid;
+    }
+    const double mu = 0.5 * (lo + hi);
+    for (int j = lane; j < c.nu; j += 32)
+      uf[(size_t)e * c.NUP + j] = clip(u[j] - mu * c.Ej[j], c.u_min[j], c.u_max[j]);
+    __syncwarp();
+  }
+}
+
+// ya = x - (x E' - target) pinv'   (per warp; r in shared scratch)
+__device__ __forceinline__ void affine_project(const EdgeCtx& c, const double* x, const double* tgt,
+                                               double* r, double* ya) {
+  const int lane = threadIdx.x & 31;
+  for (int k = 0; k < c.ne; ++k) {
+    double s = 0.0;
+    for (int j = lane; j < c.nu; j += 32) s = fma(x[j], c.Emat[(size_t)k * c.nu + j], s);
+    s = warp_sum(s);
+    if (lane == 0) r[k] = s - tgt[k];
+  }
+  __syncwarp();
+  for (int j = lane; j < c.nu; j += 32) {
+    double s = 0.0;
+    for (int k = 0; k < c.ne; ++k) s = fma(r[k], c.EpinvT[(size_t)k * c.nu + j], s);
+    ya[j] = x[j] - s;
+  }
+  __syncwarp();
+}
+
+// Primal side, part 1 (n_e > 1): Dykstra between the junction plane and the box
+// (engine.py:407-419).  Cooperative: the stopping test is a max over every edge.
+__global__ void __launch_bounds__(256) gap_project_dykstra_kernel(EdgeCtx c, double* xit, double* inc,
+                                                                  double* uf,
+                                                                  unsigned long long* slots) {
+  __shared__ double sx[8][128], sy[8][128], sr[8][64];
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int it = 0; it < 200; ++it) {
+    double mx = 0.0;
+    for (int e = gw; e < c.E; e += nw) {
+      double* x = sx[wl];
+      for (int j = lane; j < c.nu; j += 32) x[j] = xit[(size_t)e * c.NUP + j];
+      __syncwarp();
+      affine_project(c, x, c.jrhs + (size_t)e * c.ne, sr[wl], sy[wl]);
+      for (int j = lane; j < c.nu; j += 32) {
+        const size_t o = (size_t)e * c.NUP + j;
+        const double t = sy[wl][j] + inc[o];
+        const double xn = clip(t, c.u_min[j], c.u_max[j]);
+        inc[o] = t - xn;
+        mx = fmax(mx, fabs(xn - x[j]));
+        xit[o] = xn;
+      }
+      __syncwarp();
+    }
+    mx = warp_max(mx);
+    if (lane == 0 && mx > 0.0) atomicMax(slots + it, (unsigned long long)__double_as_longlong(mx));
+    grid.sync();
+    const double gmax = __longlong_as_double((long long)*((volatile unsigned long long*)(slots + it)));
+    if (gmax < 1e-13) break;
+  }
+  for (int e = gw; e < c.E; e += nw) {
+    double* x = sx[wl];
+    for (int j = lane; j < c.nu; j += 32) x[j] = xit[(size_t)e * c.NUP + j];
+    __syncwarp();
+    affine_project(c, x, c.jrhs + (size_t)e * c.ne, sr[wl], sy[wl]);
+    for (int j = lane; j < c.nu; j += 32) uf[(size_t)e * c.NUP + j] = sy[wl][j];
+    __syncwarp();
+  }
+}
+
+// ub_e = u_feas_e B'   (E x NXP)
+__global__ void gap_ub_kernel(EdgeCtx c, const double* __restrict__ uf, double* ub) {
+  __shared__ double shm[8][128];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int e = gw; e < c.E; e += nw) {
+    for (int j = lane; j < c.nu; j += 32) shm[wl][j] = uf[(size_t)e * c.NUP + j];
+    __syncwarp();
+    for (int i = lane; i < c.nx; i += 32) {
+      double s = 0.0;
+      for (int j = 0; j < c.nu; ++j) s = fma(shm[wl][j], c.B[(size_t)i * c.nu + j], s);
+      ub[(size_t)e * c.NXP + i] = s;
+    }
+    __syncwarp();
+  }
+}
+
+// one stage of x_feas propagation (engine.py:422-432): x = (x_anc A' + u B') + Gd d
+__global__ void gap_propagate_stage_kernel(EdgeCtx c, int n0, int n1, double* xf,
+                                           const double* __restrict__ ub) {
+  const int total = (n1 - n0) * c.nx;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
+    const int n = n0 + k / c.nx, i = k % c.nx;
+    const int an = c.anc[n];
+    double s;
+    if (c.a_diag) {
+      s = xf[(size_t)an * c.NXP + i] * c.a_diag[i];
+    } else {
+      s = 0.0;
+      for (int j = 0; j < c.nx; ++j) s = fma(xf[(size_t)an * c.NXP + j], c.A[(size_t)i * c.nx + j], s);
+    }
+    const size_t oe = (size_t)(n - 1) * c.NXP + i;
+    xf[(size_t)n * c.NXP + i] = (s + ub[oe]) + c.gdd[oe];
+  }
+}
+
+// Primal side, part 2: smooth cost of u_feas and soft state cost (engine.py:347-364).
+__global__ void gap_primal_terms_kernel(EdgeCtx c, const double* __restrict__ uf,
+                                        const double* __restrict__ xf, double* cols) {
+  __shared__ double shm[8][128];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int e = gw; e < c.E; e += nw) {
+    const double k0 = smooth_term(c, e, uf, c.NUP, shm[wl]);
+    double b = 0, o = 0;
+    for (int i = lane; i < c.nx; i += 32) {
+      const double x = xf[(size_t)(e + 1) * c.NXP + i];
+      const double below = fmax(c.x_s[i] - x, 0.0);
+      const double out = x - clip(x, c.x_min[i], c.x_max[i]);
+      b = fma(below, below, b);
+      o = fma(out, out, o);
+    }
+    b = sqrt(warp_sum(b));
+    o = sqrt(warp_sum(o));
+    if (lane == 0) {
+      cols[10 * (size_t)e + 0] = k0;
+      cols[10 * (size_t)e + 1] = b;
+      cols[10 * (size_t)e + 2] = o;
+    }
+  }
+}
+
+}  // namespace tsmpc

@@ -1,0 +1,58 @@
+// tsmpc_aux.cuh — declarations of the per-edge helper kernels (tsmpc_aux.cu).
+#pragma once
+#include "tsmpc_kernels.cuh"
+
+namespace tsmpc {
+
+// Read-only per-edge context shared by the helper kernels.
+struct EdgeCtx {
+  int nx, nu, ne, E, NXP, NUP;
+  double Wx, gamma_d, W_alpha;
+  const int* edge_stage;
+  const int* anc;
+  const double *sig_stage, *zeta_stage, *psi_stage;  // null -> identity
+  const double *x_s, *x_min, *x_max, *u_min, *u_max;
+  const double* prob_edge;  // E
+  const double* prices;     // N*nu
+  const double* q;          // nu
+  const double* Wu;         // nu*nu
+  const double* Emat;       // ne*nu (junction matrix)
+  const double* Ej;         // row 0 of E (ne == 1)
+  const double* EpinvT;     // ne*nu
+  const double* jrhs;       // E*ne
+  const double* gdd;        // E*NXP
+  const double* B;          // nx*nu
+  const double* a_diag;     // NXP or null
+  const double* A;          // nx*nx
+};
+
+struct ProxArgs {
+  int rows, nx, nu;
+  double lam, Wx, gamma_d;
+  const int* edge_stage;  // null -> unscaled
+  const double *sig_stage, *zeta_stage, *psi_stage;  // compact (N, N, N*nu) or null
+  const double *x_s, *x_min, *x_max, *u_min, *u_max;
+  const double *t_sig, *t_zeta, *t_psi;
+  double *o_sig, *o_zeta, *o_psi;
+};
+
+__global__ void reduce_cols_kernel(const double* vals, int n, int ncols, double* out);
+__global__ void prox_kernel(ProxArgs a);
+__global__ void dual_sq_rows_kernel(EdgeCtx c, const double* y, double* rows);
+__global__ void dual_normalize_kernel(EdgeCtx c, double* y, const double* sq);
+__global__ void dual_apply_kernel(EdgeCtx c, double* y, const double* X, const double* U,
+                                  const double* Z0X, const double* Z0U, double* rows);
+__global__ void gap_dual_project_kernel(EdgeCtx c, const double* y, double* what, double* cols);
+__global__ void gap_dual_terms_kernel(EdgeCtx c, const double* what, const double* X,
+                                      const double* U, double* cols);
+__global__ void gap_project_bisect_kernel(EdgeCtx c, const double* uavg, double* uf);
+__global__ void gap_project_dykstra_kernel(EdgeCtx c, double* xit, double* inc, double* uf,
+                                           unsigned long long* slots);
+__global__ void gap_ub_kernel(EdgeCtx c, const double* uf, double* ub);
+__global__ void gap_propagate_stage_kernel(EdgeCtx c, int n0, int n1, double* xf, const double* ub);
+__global__ void gap_primal_terms_kernel(EdgeCtx c, const double* uf, const double* xf, double* cols);
+
+__global__ void apg_persistent_kernel(Params P);
+size_t smem_bytes(int LDA, int LDB);
+
+}  // namespace tsmpc

@@ -1,0 +1,816 @@
+// tsmpc_capi.cu — host runtime behind include/tsmpc.h: tree planning (segments,
+// levels, tiles), HBM layout, uploads, launches and the C ABI.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tsmpc.h"
+#include "tsmpc_aux.cuh"
+
+using namespace tsmpc;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CU(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(TSMPC_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+
+inline int r4(int v) { return (v + 3) / 4 * 4; }
+inline int r8(int v) { return (v + 7) / 8 * 8; }
+
+}  // namespace
+
+struct tsmpc_plan {
+  int device = 0;
+  int nx, nu, nv, nd, ne, N, n_nodes, E;
+  int NXP, NUP, NVP;
+  int sm_count = 0;
+  size_t smem = 0;
+  Params base{};
+  EdgeCtx ctx{};
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<void*> allocs;
+  std::vector<int64_t> stage_starts;
+  bool has_cache = false;
+  bool has_op = false;
+  // device buffers
+  double *Y0, *Y1, *WB, *PY;
+  double *XAVG, *UAVG, *X, *U, *XL, *UL, *T, *GG, *XIQG;
+  double *BETA, *BETA0, *UHAT, *EVEC, *GDD, *JRHS, *PRICES, *Q, *P;
+  double *Z0X, *Z0U, *UF, *XIT, *INC, *UB, *XF, *COLS, *ROWS, *RED;
+  double *THETA, *COEF;
+  int theta_cap = 0;
+  unsigned long long* RESID = nullptr;
+  int resid_cap = 0;
+  unsigned long long* DYK = nullptr;
+  // compact scaling copies for tsmpc_prox
+  double *sig_c = nullptr, *zeta_c = nullptr, *psi_c = nullptr;
+  // plan stats
+  int n_levels = 0, n_tiles = 0, n_segs = 0, n_ctas = 0;
+  int dyk_blocks = 0;
+
+  template <class T>
+  int alloc(T** p, size_t count) {
+    void* d = nullptr;
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc(&d, count * sizeof(T));
+    if (e != cudaSuccess)
+      return fail(TSMPC_ERR_CUDA, "cudaMalloc(%zu bytes): %s", count * sizeof(T), cudaGetErrorString(e));
+    allocs.push_back(d);
+    *p = static_cast<T*>(d);
+    e = cudaMemsetAsync(d, 0, count * sizeof(T), stream);
+    if (e != cudaSuccess) return fail(TSMPC_ERR_CUDA, "cudaMemset: %s", cudaGetErrorString(e));
+    return TSMPC_OK;
+  }
+  template <class T>
+  int upload(T** p, const T* host, size_t count) {
+    int rc = alloc(p, count);
+    if (rc) return rc;
+    CU(cudaMemcpyAsync(*p, host, count * sizeof(T), cudaMemcpyHostToDevice, stream));
+    return TSMPC_OK;
+  }
+  // host rows of `w` doubles -> device rows of pitch `ld` doubles
+  int put_rows(double* dst, int ld, const double* src, int w, int rows) {
+    if (rows == 0 || w == 0) return TSMPC_OK;
+    CU(cudaMemcpy2DAsync(dst, ld * sizeof(double), src, w * sizeof(double), w * sizeof(double), rows,
+                         cudaMemcpyHostToDevice, stream));
+    return TSMPC_OK;
+  }
+  int get_rows(double* dst, int w, const double* src, int ld, int rows) {
+    if (rows == 0 || w == 0 || dst == nullptr) return TSMPC_OK;
+    CU(cudaMemcpy2DAsync(dst, w * sizeof(double), src, ld * sizeof(double), w * sizeof(double), rows,
+                         cudaMemcpyDeviceToHost, stream));
+    return TSMPC_OK;
+  }
+  ~tsmpc_plan() {
+    if (stream) cudaStreamSynchronize(stream);
+    for (void* p : allocs) cudaFree(p);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+// ---------------------------------------------------------------- planning
+struct Decomposition {
+  int n_levels = 0;
+  std::vector<int> lvl_tiles, tile_seg, seg_row, row_edge;
+  int n_ctas = 0;
+};
+
+// Cut the tree into segments (maximal only-child chains of <= kMaxSeg edges),
+// group them by segment depth, balance each level's rows over the CTAs and pack
+// every CTA's share into tiles of <= kTileM rows.
+int decompose(const tsmpc_problem* pb, int max_ctas, Decomposition& out) {
+  const int n_nodes = pb->n_nodes, E = n_nodes - 1;
+  std::vector<int> nch(n_nodes);
+  for (int n = 0; n < n_nodes; ++n) nch[n] = (int)(pb->child_stop[n] - pb->child_start[n]);
+  std::vector<char> head(E, 0);
+  for (int e = 0; e < E; ++e) {
+    const int p = (int)pb->anc[e + 1];
+    head[e] = (p == 0 || nch[p] != 1) ? 1 : 0;
+  }
+  std::vector<std::vector<int>> segs;
+  std::vector<int> seg_of(E, -1);
+  for (int e = 0; e < E; ++e) {
+    if (!head[e] || seg_of[e] >= 0) continue;
+    int cur = e;
+    while (cur >= 0) {  // one segment per pass; long chains continue in a new segment
+      std::vector<int> s{cur};
+      seg_of[cur] = (int)segs.size();
+      int x = cur;
+      int next = -1;
+      while (nch[x + 1] == 1) {
+        const int c = (int)pb->child_start[x + 1] - 1;
+        if ((int)s.size() == kMaxSeg) { next = c; break; }
+        s.push_back(c);
+        seg_of[c] = (int)segs.size();
+        x = c;
+      }
+      segs.push_back(std::move(s));
+      cur = next;
+    }
+  }
+  for (int e = 0; e < E; ++e)
+    if (seg_of[e] < 0) return fail(TSMPC_ERR_VALIDATION, "tree decomposition missed edge %d", e);
+  // segment order by head edge id => parents before children
+  std::vector<int> order(segs.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return segs[a][0] < segs[b][0]; });
+  std::vector<int> level(segs.size(), 0);
+  int D = 0;
+  for (int s : order) {
+    const int h = segs[s][0];
+    const int pn = (int)pb->anc[h + 1];
+    level[s] = pn == 0 ? 0 : level[seg_of[pn - 1]] + 1;
+    D = std::max(D, level[s] + 1);
+  }
+  std::vector<std::vector<int>> by_level(D);
+  for (int s : order) by_level[level[s]].push_back(s);
+  size_t widest = 0;
+  for (auto& v : by_level) widest = std::max(widest, v.size());
+  const int C = std::max(1, std::min<int>(max_ctas, (int)widest));
+
+  out.n_levels = D;
+  out.n_ctas = C;
+  out.lvl_tiles.assign((size_t)D * C + 1, 0);
+  out.tile_seg.clear();
+  out.seg_row.clear();
+  out.row_edge.clear();
+  int tiles = 0;
+  for (int l = 0; l < D; ++l) {
+    const auto& v = by_level[l];
+    long long R = 0;
+    for (int s : v) R += (long long)segs[s].size();
+    std::vector<std::vector<int>> share(C);
+    long long pre = 0;
+    for (int s : v) {
+      const long long mid2 = 2 * pre + (long long)segs[s].size();  // 2 x segment midpoint
+      int c = (int)((mid2 * C) / (2 * std::max<long long>(R, 1)));
+      c = std::min(std::max(c, 0), C - 1);
+      share[c].push_back(s);
+      pre += (long long)segs[s].size();
+    }
+    for (int c = 0; c < C; ++c) {
+      out.lvl_tiles[(size_t)l * C + c] = tiles;
+      int rows_in_tile = kTileM + 1;
+      for (int s : share[c]) {
+        const int len = (int)segs[s].size();
+        if (rows_in_tile + len > kTileM) {  // open a new tile
+          out.tile_seg.push_back((int)out.seg_row.size());
+          ++tiles;
+          rows_in_tile = 0;
+        }
+        out.seg_row.push_back((int)out.row_edge.size());
+        for (int e : segs[s]) out.row_edge.push_back(e);
+        rows_in_tile += len;
+      }
+    }
+  }
+  out.lvl_tiles[(size_t)D * C] = tiles;
+  out.tile_seg.push_back((int)out.seg_row.size());
+  out.seg_row.push_back((int)out.row_edge.size());
+  return TSMPC_OK;
+}
+
+int launch_apg(tsmpc_plan* pl, const Params& P) {
+  void* args[] = {const_cast<Params*>(&P)};
+  CU(cudaLaunchCooperativeKernel((void*)apg_persistent_kernel, dim3(pl->n_ctas), dim3(kThreads), args,
+                                 pl->smem, pl->stream));
+  return TSMPC_OK;
+}
+
+int grid_for(int E) {  // warp-per-edge helper kernels, 256 threads = 8 warps per block
+  return std::max(1, std::min((E + 7) / 8, 148 * 16));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tsmpc_last_error(void) { return g_err.c_str(); }
+
+int tsmpc_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+tsmpc_plan* tsmpc_plan_create(const tsmpc_problem* pb, int device) {
+  if (!pb) { fail(TSMPC_ERR_ARGUMENT, "null problem"); return nullptr; }
+  const int nx = pb->n_x, nu = pb->n_u, nv = pb->n_v, ne = pb->n_e, N = pb->N, n_nodes = pb->n_nodes;
+  if (nx < 1 || nu < 1 || nv < 1 || ne < 1 || N < 1 || n_nodes < 2) {
+    fail(TSMPC_ERR_DIMENSION, "invalid dimensions n_x=%d n_u=%d n_v=%d n_e=%d N=%d n_nodes=%d", nx, nu, nv, ne,
+         N, n_nodes);
+    return nullptr;
+  }
+  if (nx > 128 || nu > 128 || ne > 64) {
+    fail(TSMPC_ERR_DIMENSION, "dimension above the supported limit (n_x, n_u <= 128, n_e <= 64)");
+    return nullptr;
+  }
+  if (!pb->A || !pb->B || !pb->L || !pb->Bbar || !pb->Phi || !pb->Psi || !pb->Wu || !pb->E ||
+      !pb->E_pinvT || !pb->u_min || !pb->u_max || !pb->x_min || !pb->x_max || !pb->x_s ||
+      !pb->stage_starts || !pb->anc || !pb->child_start || !pb->child_stop || !pb->prob) {
+    fail(TSMPC_ERR_ARGUMENT, "null array in tsmpc_problem");
+    return nullptr;
+  }
+  if (pb->stage_starts[0] != 0 || pb->stage_starts[N + 1] != n_nodes || pb->stage_starts[1] != 1) {
+    fail(TSMPC_ERR_VALIDATION, "stage offsets do not cover the node arrays");
+    return nullptr;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    fail(TSMPC_ERR_CUDA, "no CUDA device available");
+    return nullptr;
+  }
+  if (device < 0 || device >= ndev) {
+    fail(TSMPC_ERR_ARGUMENT, "device %d out of range (%d devices)", device, ndev);
+    return nullptr;
+  }
+  auto* pl = new tsmpc_plan();
+  auto bail = [&](int) -> tsmpc_plan* { delete pl; return nullptr; };
+  pl->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) { fail(TSMPC_ERR_CUDA, "cudaSetDevice failed"); return bail(0); }
+  if (cudaStreamCreateWithFlags(&pl->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&pl->ev0) != cudaSuccess || cudaEventCreate(&pl->ev1) != cudaSuccess) {
+    fail(TSMPC_ERR_CUDA, "stream/event creation failed");
+    return bail(0);
+  }
+  cudaDeviceProp prop{};
+  cudaGetDeviceProperties(&prop, device);
+  pl->sm_count = prop.multiProcessorCount;
+
+  const int E = n_nodes - 1;
+  pl->nx = nx; pl->nu = nu; pl->nv = nv; pl->nd = pb->n_d; pl->ne = ne; pl->N = N;
+  pl->n_nodes = n_nodes; pl->E = E;
+  const int NXP = r4(nx), NUP = r4(nu), NVP = r4(nv);
+  pl->NXP = NXP; pl->NUP = NUP; pl->NVP = NVP;
+  pl->stage_starts.assign(pb->stage_starts, pb->stage_starts + N + 2);
+
+  Params& P = pl->base;
+  P.nx = nx; P.nu = nu; P.nv = nv; P.N = N; P.n_nodes = n_nodes; P.n_edges = E;
+  P.NXP = NXP; P.NUP = NUP; P.NVP = NVP;
+  const int K1 = NXP + NUP;
+  P.KS1 = K1 / 4;
+  P.NT1 = (nv + 7) / 8;
+  P.KS2 = NVP / 4;
+  P.NU8 = r8(nu);
+  P.NT2 = (P.NU8 + r8(nx)) / 8;
+  int lda = std::max(std::max(K1, NVP), NXP);
+  while (lda % 16 != 4) ++lda;
+  P.LDA = lda;
+  P.LDB = std::max(P.NT1 * 8, P.NT2 * 8);
+  P.Wx = pb->Wx; P.gamma_d = pb->gamma_d;
+  pl->smem = smem_bytes(P.LDA, P.LDB);
+  if (pl->smem > (size_t)prop.sharedMemPerBlockOptin) {
+    fail(TSMPC_ERR_DIMENSION, "tile needs %zu bytes of shared memory (limit %zu)", pl->smem,
+         (size_t)prop.sharedMemPerBlockOptin);
+    return bail(0);
+  }
+  if (cudaFuncSetAttribute(apg_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)pl->smem) != cudaSuccess) {
+    fail(TSMPC_ERR_CUDA, "cannot reserve %zu bytes of shared memory", pl->smem);
+    return bail(0);
+  }
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, apg_persistent_kernel, kThreads, pl->smem);
+  if (occ < 1) { fail(TSMPC_ERR_CUDA, "persistent kernel does not fit on an SM"); return bail(0); }
+
+  Decomposition dec;
+  if (decompose(pb, pl->sm_count * std::min(occ, 1), dec)) return bail(0);
+  pl->n_levels = dec.n_levels;
+  pl->n_ctas = dec.n_ctas;
+  pl->n_tiles = (int)dec.tile_seg.size() - 1;
+  pl->n_segs = (int)dec.seg_row.size() - 1;
+  P.n_levels = dec.n_levels;
+  P.n_ctas = dec.n_ctas;
+
+  // ---- operator blocks in DMMA fragment order
+  std::vector<double> W1((size_t)K1 * P.NT1 * 8, 0.0), W2((size_t)P.KS2 * 4 * P.NT2 * 8, 0.0);
+  const int n1 = P.NT1 * 8, n2 = P.NT2 * 8;
+  for (int i = 0; i < nx; ++i)
+    for (int n = 0; n < nv; ++n) W1[(size_t)i * n1 + n] = pb->Bbar[(size_t)i * nv + n];
+  for (int j = 0; j < nu; ++j)
+    for (int n = 0; n < nv; ++n) W1[(size_t)(NXP + j) * n1 + n] = pb->L[(size_t)j * nv + n];
+  for (int k = 0; k < nv; ++k) {
+    for (int j = 0; j < nu; ++j) W2[(size_t)k * n2 + j] = pb->Psi[(size_t)k * nu + j];
+    for (int i = 0; i < nx; ++i) W2[(size_t)k * n2 + P.NU8 + i] = pb->Phi[(size_t)k * nx + i];
+  }
+  auto frag = [](const std::vector<double>& W, int KS, int NT) {
+    std::vector<double> f((size_t)NT * KS * 32);
+    const int ld = NT * 8;
+    for (int nt = 0; nt < NT; ++nt)
+      for (int ks = 0; ks < KS; ++ks)
+        for (int l = 0; l < 32; ++l)
+          f[((size_t)nt * KS + ks) * 32 + l] = W[(size_t)(4 * ks + (l & 3)) * ld + nt * 8 + (l >> 2)];
+    return f;
+  };
+  const auto W1f = frag(W1, P.KS1, P.NT1), W2f = frag(W2, P.KS2, P.NT2);
+
+  // ---- model vectors (padded)
+  auto padv = [](const double* v, int n, int np) {
+    std::vector<double> o(np, 0.0);
+    std::copy(v, v + n, o.begin());
+    return o;
+  };
+  bool diag = true;
+  for (int i = 0; i < nx && diag; ++i)
+    for (int j = 0; j < nx; ++j)
+      if (i != j && pb->A[(size_t)i * nx + j] != 0.0) { diag = false; break; }
+  std::vector<double> adiag(NXP, 0.0);
+  for (int i = 0; i < nx; ++i) adiag[i] = pb->A[(size_t)i * nx + i];
+  P.diagA = diag ? 1 : 0;
+
+  // ---- tree arrays
+  std::vector<int> anc(n_nodes), cs(n_nodes), ce(n_nodes), est(E);
+  std::vector<double> inv2p(E), pe(E);
+  for (int n = 0; n < n_nodes; ++n) {
+    anc[n] = (int)pb->anc[n];
+    cs[n] = (int)pb->child_start[n];
+    ce[n] = (int)pb->child_stop[n];
+  }
+  for (int j = 0; j < N; ++j)
+    for (int64_t n = pb->stage_starts[j + 1]; n < pb->stage_starts[j + 2]; ++n) est[n - 1] = j;
+  for (int e = 0; e < E; ++e) {
+    pe[e] = pb->prob[e + 1];
+    inv2p[e] = 1.0 / (2.0 * pb->prob[e + 1]);
+  }
+
+  // ---- scaling
+  const bool scaled = pb->sig_stage && pb->zeta_stage && pb->psi_stage;
+  std::vector<double> sig(N, 1.0), zeta(N, 1.0), psi((size_t)N * NUP, 1.0), psi_c((size_t)N * nu, 1.0);
+  if (scaled) {
+    for (int j = 0; j < N; ++j) {
+      sig[j] = pb->sig_stage[j];
+      zeta[j] = pb->zeta_stage[j];
+      for (int k = 0; k < nu; ++k) psi[(size_t)j * NUP + k] = psi_c[(size_t)j * nu + k] = pb->psi_stage[(size_t)j * nu + k];
+    }
+  }
+  P.scaled = scaled ? 1 : 0;
+
+  int rc = 0;
+  const double* d_c = nullptr;
+  double *d_W1f, *d_W2f, *d_adiag, *d_A, *d_xs, *d_xmin, *d_xmax, *d_umin, *d_umax, *d_sig, *d_zeta, *d_psi,
+      *d_inv2p, *d_pe, *d_Wu, *d_E, *d_EpinvT, *d_B;
+  int *d_anc, *d_cs, *d_ce, *d_est, *d_lt, *d_ts, *d_sr, *d_re;
+  (void)d_c;
+  rc |= pl->upload(&d_W1f, W1f.data(), W1f.size());
+  rc |= pl->upload(&d_W2f, W2f.data(), W2f.size());
+  rc |= pl->upload(&d_adiag, adiag.data(), adiag.size());
+  rc |= pl->upload(&d_A, pb->A, (size_t)nx * nx);
+  rc |= pl->upload(&d_B, pb->B, (size_t)nx * nu);
+  const auto xs = padv(pb->x_s, nx, NXP), xmn = padv(pb->x_min, nx, NXP), xmx = padv(pb->x_max, nx, NXP);
+  const auto umn = padv(pb->u_min, nu, NUP), umx = padv(pb->u_max, nu, NUP);
+  rc |= pl->upload(&d_xs, xs.data(), xs.size());
+  rc |= pl->upload(&d_xmin, xmn.data(), xmn.size());
+  rc |= pl->upload(&d_xmax, xmx.data(), xmx.size());
+  rc |= pl->upload(&d_umin, umn.data(), umn.size());
+  rc |= pl->upload(&d_umax, umx.data(), umx.size());
+  rc |= pl->upload(&d_sig, sig.data(), sig.size());
+  rc |= pl->upload(&d_zeta, zeta.data(), zeta.size());
+  rc |= pl->upload(&d_psi, psi.data(), psi.size());
+  rc |= pl->upload(&pl->psi_c, psi_c.data(), psi_c.size());
+  pl->sig_c = d_sig;
+  pl->zeta_c = d_zeta;
+  rc |= pl->upload(&d_inv2p, inv2p.data(), inv2p.size());
+  rc |= pl->upload(&d_pe, pe.data(), pe.size());
+  rc |= pl->upload(&d_Wu, pb->Wu, (size_t)nu * nu);
+  rc |= pl->upload(&d_E, pb->E, (size_t)ne * nu);
+  rc |= pl->upload(&d_EpinvT, pb->E_pinvT, (size_t)ne * nu);
+  rc |= pl->upload(&d_anc, anc.data(), anc.size());
+  rc |= pl->upload(&d_cs, cs.data(), cs.size());
+  rc |= pl->upload(&d_ce, ce.data(), ce.size());
+  rc |= pl->upload(&d_est, est.data(), est.size());
+  rc |= pl->upload(&d_lt, dec.lvl_tiles.data(), dec.lvl_tiles.size());
+  rc |= pl->upload(&d_ts, dec.tile_seg.data(), dec.tile_seg.size());
+  rc |= pl->upload(&d_sr, dec.seg_row.data(), dec.seg_row.size());
+  rc |= pl->upload(&d_re, dec.row_edge.data(), dec.row_edge.size());
+  // state
+  const size_t yblk = 2 * (size_t)E * NXP + (size_t)E * NUP;
+  rc |= pl->alloc(&pl->Y0, yblk);
+  rc |= pl->alloc(&pl->Y1, yblk);
+  rc |= pl->alloc(&pl->WB, yblk);
+  rc |= pl->alloc(&pl->PY, yblk);
+  rc |= pl->alloc(&pl->XAVG, (size_t)n_nodes * NXP);
+  rc |= pl->alloc(&pl->X, (size_t)n_nodes * NXP);
+  rc |= pl->alloc(&pl->XL, (size_t)n_nodes * NXP);
+  rc |= pl->alloc(&pl->XF, (size_t)n_nodes * NXP);
+  rc |= pl->alloc(&pl->Z0X, (size_t)n_nodes * NXP);
+  rc |= pl->alloc(&pl->UAVG, (size_t)E * NUP);
+  rc |= pl->alloc(&pl->U, (size_t)E * NUP);
+  rc |= pl->alloc(&pl->UL, (size_t)E * NUP);
+  rc |= pl->alloc(&pl->Z0U, (size_t)E * NUP);
+  rc |= pl->alloc(&pl->UF, (size_t)E * NUP);
+  rc |= pl->alloc(&pl->XIT, (size_t)E * NUP);
+  rc |= pl->alloc(&pl->INC, (size_t)E * NUP);
+  rc |= pl->alloc(&pl->UHAT, (size_t)E * NUP);
+  rc |= pl->alloc(&pl->T, (size_t)E * NVP);
+  rc |= pl->alloc(&pl->GG, (size_t)E * NVP);
+  rc |= pl->alloc(&pl->BETA, (size_t)E * NVP);
+  rc |= pl->alloc(&pl->BETA0, (size_t)E * NVP);
+  rc |= pl->alloc(&pl->XIQG, (size_t)E * NXP);
+  rc |= pl->alloc(&pl->EVEC, (size_t)E * NXP);
+  rc |= pl->alloc(&pl->GDD, (size_t)E * NXP);
+  rc |= pl->alloc(&pl->UB, (size_t)E * NXP);
+  rc |= pl->alloc(&pl->JRHS, (size_t)E * ne);
+  rc |= pl->alloc(&pl->PRICES, (size_t)N * nu);
+  rc |= pl->alloc(&pl->Q, (size_t)nu);
+  rc |= pl->alloc(&pl->P, (size_t)NXP);
+  rc |= pl->alloc(&pl->COLS, (size_t)E * 10);
+  rc |= pl->alloc(&pl->ROWS, (size_t)E * 6);
+  rc |= pl->alloc(&pl->RED, 16);
+  rc |= pl->alloc(&pl->DYK, 256);
+  if (rc) return bail(0);
+
+  P.a_diag = d_adiag; P.A = d_A; P.W1f = d_W1f; P.W2f = d_W2f;
+  P.x_s = d_xs; P.x_min = d_xmin; P.x_max = d_xmax; P.u_min = d_umin; P.u_max = d_umax;
+  P.sig_stage = d_sig; P.zeta_stage = d_zeta; P.psi_stage = d_psi;
+  P.anc = d_anc; P.child_start = d_cs; P.child_stop = d_ce; P.edge_stage = d_est; P.inv2p = d_inv2p;
+  P.lvl_tiles = d_lt; P.tile_seg = d_ts; P.seg_row = d_sr; P.row_edge = d_re;
+  P.xavg = pl->XAVG; P.uavg = pl->UAVG; P.X = pl->X; P.U = pl->U; P.T = pl->T;
+  P.XIQG = pl->XIQG; P.GG = pl->GG; P.p = pl->P;
+
+  EdgeCtx& c = pl->ctx;
+  c.nx = nx; c.nu = nu; c.ne = ne; c.E = E; c.NXP = NXP; c.NUP = NUP;
+  c.Wx = pb->Wx; c.gamma_d = pb->gamma_d; c.W_alpha = pb->W_alpha;
+  c.edge_stage = d_est; c.anc = d_anc;
+  c.sig_stage = scaled ? d_sig : nullptr;
+  c.zeta_stage = scaled ? d_zeta : nullptr;
+  c.psi_stage = scaled ? d_psi : nullptr;
+  c.x_s = d_xs; c.x_min = d_xmin; c.x_max = d_xmax; c.u_min = d_umin; c.u_max = d_umax;
+  c.prob_edge = d_pe; c.prices = pl->PRICES; c.q = pl->Q; c.Wu = d_Wu; c.Emat = d_E; c.Ej = d_E;
+  c.EpinvT = d_EpinvT; c.jrhs = pl->JRHS; c.gdd = pl->GDD; c.B = d_B;
+  c.a_diag = diag ? d_adiag : nullptr; c.A = d_A;
+
+  int occ_d = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_d, gap_project_dykstra_kernel, 256, 0);
+  pl->dyk_blocks = std::max(1, std::min(occ_d, 4)) * pl->sm_count;
+  if (cudaStreamSynchronize(pl->stream) != cudaSuccess) {
+    fail(TSMPC_ERR_CUDA, "plan upload failed: %s", cudaGetErrorString(cudaGetLastError()));
+    return bail(0);
+  }
+  return pl;
+}
+
+void tsmpc_plan_destroy(tsmpc_plan* plan) { delete plan; }
+
+int tsmpc_plan_info(const tsmpc_plan* pl, int64_t* info, int32_t n) {
+  if (!pl || !info) return fail(TSMPC_ERR_ARGUMENT, "null argument");
+  const int64_t vals[] = {pl->n_levels, pl->n_ctas, pl->n_tiles, pl->n_segs, (int64_t)pl->smem,
+                          pl->base.diagA, kThreads, kTileM, pl->sm_count};
+  for (int i = 0; i < n && i < (int)(sizeof(vals) / sizeof(vals[0])); ++i) info[i] = vals[i];
+  return TSMPC_OK;
+}
+
+int tsmpc_set_cache(tsmpc_plan* pl, const double* beta, const double* uhat, const double* evec,
+                    const double* q, const double* prices, const double* jrhs, const double* gdd) {
+  if (!pl || !beta || !uhat || !evec || !q) return fail(TSMPC_ERR_ARGUMENT, "null cache array");
+  CU(cudaSetDevice(pl->device));
+  const int E = pl->E;
+  int rc = 0;
+  rc |= pl->put_rows(pl->BETA, pl->NVP, beta, pl->nv, E);
+  rc |= pl->put_rows(pl->UHAT, pl->NUP, uhat, pl->nu, E);
+  rc |= pl->put_rows(pl->EVEC, pl->NXP, evec, pl->nx, E);
+  if (rc) return rc;
+  CU(cudaMemcpyAsync(pl->Q, q, sizeof(double) * pl->nu, cudaMemcpyHostToDevice, pl->stream));
+  if (prices)
+    CU(cudaMemcpyAsync(pl->PRICES, prices, sizeof(double) * pl->N * pl->nu, cudaMemcpyHostToDevice, pl->stream));
+  if (jrhs)
+    CU(cudaMemcpyAsync(pl->JRHS, jrhs, sizeof(double) * (size_t)E * pl->ne, cudaMemcpyHostToDevice, pl->stream));
+  if (gdd && pl->put_rows(pl->GDD, pl->NXP, gdd, pl->nx, E)) return TSMPC_ERR_CUDA;
+  CU(cudaStreamSynchronize(pl->stream));
+  pl->has_cache = true;
+  return TSMPC_OK;
+}
+
+static int set_root(tsmpc_plan* pl, const double* p) {
+  std::vector<double> pp(pl->NXP, 0.0);
+  if (p) std::copy(p, p + pl->nx, pp.begin());
+  CU(cudaMemcpyAsync(pl->P, pp.data(), sizeof(double) * pl->NXP, cudaMemcpyHostToDevice, pl->stream));
+  CU(cudaMemcpyAsync(pl->X, pl->P, sizeof(double) * pl->NXP, cudaMemcpyDeviceToDevice, pl->stream));
+  CU(cudaStreamSynchronize(pl->stream));  // pp is a stack buffer
+  return TSMPC_OK;
+}
+
+// One solve step (mode STEP) on the dual stored in `w` (three blocks).
+static int run_step(tsmpc_plan* pl, double* w, int scaled, const double* beta, const double* uhat,
+                    const double* evec) {
+  Params P = pl->base;
+  P.mode = kModeStep;
+  P.iters = 1;
+  P.scaled = scaled && pl->base.scaled;
+  P.slot0 = 0;
+  P.ybuf[0] = P.ybuf[1] = w;
+  P.beta = beta;
+  P.uhat = uhat;
+  P.evec = evec;
+  P.record_all = 0;
+  P.lam = 1.0;
+  P.theta = P.coef = nullptr;
+  P.resid = nullptr;
+  return launch_apg(pl, P);
+}
+
+static int compute_gap(tsmpc_plan* pl, const double* yfinal, double* gap) {
+  EdgeCtx c = pl->ctx;
+  const int E = pl->E, G = grid_for(E);
+  CU(cudaMemsetAsync(pl->COLS, 0, sizeof(double) * (size_t)E * 10, pl->stream));
+  gap_dual_project_kernel<<<G, 256, 0, pl->stream>>>(c, yfinal, pl->WB, pl->COLS);
+  CU(cudaGetLastError());
+  if (run_step(pl, pl->WB, 0, pl->BETA, pl->UHAT, pl->EVEC)) return TSMPC_ERR_CUDA;
+  gap_dual_terms_kernel<<<G, 256, 0, pl->stream>>>(c, pl->WB, pl->X, pl->U, pl->COLS);
+  CU(cudaGetLastError());
+  if (pl->ne == 1) {
+    gap_project_bisect_kernel<<<G, 256, 0, pl->stream>>>(c, pl->UAVG, pl->UF);
+    CU(cudaGetLastError());
+  } else {
+    CU(cudaMemcpyAsync(pl->XIT, pl->UAVG, sizeof(double) * (size_t)E * pl->NUP, cudaMemcpyDeviceToDevice,
+                       pl->stream));
+    CU(cudaMemsetAsync(pl->INC, 0, sizeof(double) * (size_t)E * pl->NUP, pl->stream));
+    CU(cudaMemsetAsync(pl->DYK, 0, sizeof(unsigned long long) * 256, pl->stream));
+    void* args[] = {&c, &pl->XIT, &pl->INC, &pl->UF, &pl->DYK};
+    CU(cudaLaunchCooperativeKernel((void*)gap_project_dykstra_kernel, dim3(pl->dyk_blocks), dim3(256), args, 0,
+                                   pl->stream));
+  }
+  gap_ub_kernel<<<G, 256, 0, pl->stream>>>(c, pl->UF, pl->UB);
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(pl->XF, pl->P, sizeof(double) * pl->NXP, cudaMemcpyDeviceToDevice, pl->stream));
+  for (int j = 0; j < pl->N; ++j) {
+    const int n0 = (int)pl->stage_starts[j + 1], n1 = (int)pl->stage_starts[j + 2];
+    const int total = (n1 - n0) * pl->nx;
+    gap_propagate_stage_kernel<<<std::max(1, std::min((total + 255) / 256, 4096)), 256, 0, pl->stream>>>(
+        c, n0, n1, pl->XF, pl->UB);
+  }
+  CU(cudaGetLastError());
+  gap_primal_terms_kernel<<<G, 256, 0, pl->stream>>>(c, pl->UF, pl->XF, pl->COLS);
+  CU(cudaGetLastError());
+  reduce_cols_kernel<<<1, 1024, 0, pl->stream>>>(pl->COLS, E, 10, pl->RED);
+  CU(cudaGetLastError());
+  double k[10];
+  CU(cudaMemcpyAsync(k, pl->RED, sizeof(k), cudaMemcpyDeviceToHost, pl->stream));
+  CU(cudaStreamSynchronize(pl->stream));
+  const double primal = k[0] + (pl->ctx.Wx * k[1] + pl->ctx.gamma_d * k[2]);
+  const double pairing = (k[3] + k[4]) + k[5];
+  const double conj = (k[7] + k[8]) + k[9];
+  *gap = primal - ((pairing + k[6]) - conj);
+  return TSMPC_OK;
+}
+
+int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, const double* warm_sig,
+                const double* warm_zeta, const double* warm_psi, const double* theta, const double* coef,
+                int32_t flags, tsmpc_result* out) {
+  if (!pl || !p || !out) return fail(TSMPC_ERR_ARGUMENT, "null argument");
+  if (iters < 1) return fail(TSMPC_ERR_VALIDATION, "max_iters must be >= 1");
+  if (!(lam > 0.0)) return fail(TSMPC_ERR_VALIDATION, "step size must be positive");
+  if (!pl->has_cache) return fail(TSMPC_ERR_VALIDATION, "no stage cache uploaded (tsmpc_set_cache)");
+  CU(cudaSetDevice(pl->device));
+  const int E = pl->E, NXP = pl->NXP, NUP = pl->NUP, nx = pl->nx, nu = pl->nu;
+  const bool record = flags & TSMPC_RECORD_RESIDUALS;
+  // momentum tables
+  if (pl->theta_cap < iters) {
+    int rc = pl->alloc(&pl->THETA, iters) | pl->alloc(&pl->COEF, iters);
+    if (rc) return rc;
+    pl->theta_cap = iters;
+  }
+  std::vector<double> th(iters), cf(iters);
+  if (theta && coef) {
+    std::copy(theta, theta + iters, th.begin());
+    std::copy(coef, coef + iters, cf.begin());
+  } else {
+    double t = 1.0, tp = 1.0;
+    for (int k = 0; k < iters; ++k) {
+      th[k] = t;
+      cf[k] = t * (1.0 / tp - 1.0);
+      tp = t;
+      t = 0.5 * (std::sqrt(std::pow(t, 4.0) + 4.0 * (t * t)) - t * t);
+    }
+  }
+  CU(cudaMemcpyAsync(pl->THETA, th.data(), sizeof(double) * iters, cudaMemcpyHostToDevice, pl->stream));
+  CU(cudaMemcpyAsync(pl->COEF, cf.data(), sizeof(double) * iters, cudaMemcpyHostToDevice, pl->stream));
+  const int nres = record ? iters : 1;
+  if (pl->resid_cap < nres) {
+    if (pl->alloc(&pl->RESID, nres)) return TSMPC_ERR_CUDA;
+    pl->resid_cap = nres;
+  }
+  CU(cudaMemsetAsync(pl->RESID, 0, sizeof(unsigned long long) * nres, pl->stream));
+  // dual start
+  const size_t yblk = 2 * (size_t)E * NXP + (size_t)E * NUP;
+  if (warm_sig && warm_zeta && warm_psi) {
+    if (pl->put_rows(pl->Y0, NXP, warm_sig, nx, E) || pl->put_rows(pl->Y0 + (size_t)E * NXP, NXP, warm_zeta, nx, E) ||
+        pl->put_rows(pl->Y0 + 2 * (size_t)E * NXP, NUP, warm_psi, nu, E))
+      return TSMPC_ERR_CUDA;
+    CU(cudaMemcpyAsync(pl->Y1, pl->Y0, sizeof(double) * yblk, cudaMemcpyDeviceToDevice, pl->stream));
+  } else {
+    CU(cudaMemsetAsync(pl->Y0, 0, sizeof(double) * yblk, pl->stream));
+    CU(cudaMemsetAsync(pl->Y1, 0, sizeof(double) * yblk, pl->stream));
+  }
+  CU(cudaMemsetAsync(pl->XAVG, 0, sizeof(double) * (size_t)pl->n_nodes * NXP, pl->stream));
+  CU(cudaMemsetAsync(pl->UAVG, 0, sizeof(double) * (size_t)E * NUP, pl->stream));
+  if (set_root(pl, p)) return TSMPC_ERR_CUDA;
+
+  Params P = pl->base;
+  P.mode = kModeApg;
+  P.iters = iters;
+  P.slot0 = 0;
+  P.ybuf[0] = pl->Y0;
+  P.ybuf[1] = pl->Y1;
+  P.beta = pl->BETA;
+  P.uhat = pl->UHAT;
+  P.evec = pl->EVEC;
+  P.lam = lam;
+  P.theta = pl->THETA;
+  P.coef = pl->COEF;
+  P.record_all = record ? 1 : 0;
+  P.resid = pl->RESID;
+  CU(cudaEventRecord(pl->ev0, pl->stream));
+  if (launch_apg(pl, P)) return TSMPC_ERR_CUDA;
+  CU(cudaEventRecord(pl->ev1, pl->stream));
+  double* yfin = ((iters & 1) == 0) ? pl->Y0 : pl->Y1;
+  // keep the last iterate before the gap's solve step reuses X / U
+  CU(cudaMemcpyAsync(pl->XL, pl->X, sizeof(double) * (size_t)pl->n_nodes * NXP, cudaMemcpyDeviceToDevice, pl->stream));
+  CU(cudaMemcpyAsync(pl->UL, pl->U, sizeof(double) * (size_t)E * NUP, cudaMemcpyDeviceToDevice, pl->stream));
+  double gap = NAN;
+  if (!(flags & TSMPC_SKIP_GAP)) {
+    int rc = compute_gap(pl, yfin, &gap);
+    if (rc) return rc;
+  }
+  out->gap = gap;
+  out->iterations = iters;
+  std::vector<unsigned long long> rbits(nres);
+  CU(cudaMemcpyAsync(rbits.data(), pl->RESID, sizeof(unsigned long long) * nres, cudaMemcpyDeviceToHost, pl->stream));
+  if (!(flags & TSMPC_KEEP_DEVICE)) {
+    int rc = 0;
+    rc |= pl->get_rows(out->x, nx, pl->XL, NXP, pl->n_nodes);
+    rc |= pl->get_rows(out->u, nu, pl->UL, NUP, E);
+    rc |= pl->get_rows(out->x_avg, nx, pl->XAVG, NXP, pl->n_nodes);
+    rc |= pl->get_rows(out->u_avg, nu, pl->UAVG, NUP, E);
+    rc |= pl->get_rows(out->u0, nu, pl->UAVG, NUP, 1);
+    rc |= pl->get_rows(out->dual_sig, nx, yfin, NXP, E);
+    rc |= pl->get_rows(out->dual_zeta, nx, yfin + (size_t)E * NXP, NXP, E);
+    rc |= pl->get_rows(out->dual_psi, nu, yfin + 2 * (size_t)E * NXP, NUP, E);
+    if (rc) return rc;
+  }
+  CU(cudaStreamSynchronize(pl->stream));
+  float ms = 0.f;
+  CU(cudaEventElapsedTime(&ms, pl->ev0, pl->ev1));
+  out->device_ms = ms;
+  auto as_d = [](unsigned long long b) { double d; std::memcpy(&d, &b, sizeof d); return d; };
+  out->residual_inf = as_d(rbits[nres - 1]);
+  if (record && out->resid_trace)
+    for (int k = 0; k < iters; ++k) out->resid_trace[k] = as_d(rbits[k]);
+  return TSMPC_OK;
+}
+
+int tsmpc_solve_step(tsmpc_plan* pl, const double* w_sig, const double* w_zeta, const double* w_psi,
+                     const double* p, double* x_out, double* u_out) {
+  if (!pl || !w_sig || !w_zeta || !w_psi || !p) return fail(TSMPC_ERR_ARGUMENT, "null argument");
+  if (!pl->has_cache) return fail(TSMPC_ERR_VALIDATION, "no stage cache uploaded (tsmpc_set_cache)");
+  CU(cudaSetDevice(pl->device));
+  const int E = pl->E, NXP = pl->NXP, NUP = pl->NUP;
+  if (pl->put_rows(pl->WB, NXP, w_sig, pl->nx, E) || pl->put_rows(pl->WB + (size_t)E * NXP, NXP, w_zeta, pl->nx, E) ||
+      pl->put_rows(pl->WB + 2 * (size_t)E * NXP, NUP, w_psi, pl->nu, E))
+    return TSMPC_ERR_CUDA;
+  if (set_root(pl, p)) return TSMPC_ERR_CUDA;
+  if (run_step(pl, pl->WB, 0, pl->BETA, pl->UHAT, pl->EVEC)) return TSMPC_ERR_CUDA;
+  if (pl->get_rows(x_out, pl->nx, pl->X, NXP, pl->n_nodes) || pl->get_rows(u_out, pl->nu, pl->U, NUP, E))
+    return TSMPC_ERR_CUDA;
+  CU(cudaStreamSynchronize(pl->stream));
+  return TSMPC_OK;
+}
+
+int tsmpc_prox(tsmpc_plan* pl, int32_t rows, const double* t_sig, const double* t_zeta, const double* t_psi,
+               double lam, int32_t use_scaling, double* o_sig, double* o_zeta, double* o_psi) {
+  if (!pl || !t_sig || !t_zeta || !t_psi || !o_sig || !o_zeta || !o_psi) return fail(TSMPC_ERR_ARGUMENT, "null argument");
+  if (!(lam > 0.0)) return fail(TSMPC_ERR_VALIDATION, "prox parameter must be positive");
+  if (use_scaling && rows != pl->E) return fail(TSMPC_ERR_DIMENSION, "scaled prox needs one row per edge");
+  if (rows < 1) return TSMPC_OK;
+  CU(cudaSetDevice(pl->device));
+  const int nx = pl->nx, nu = pl->nu;
+  double *d_ts, *d_tz, *d_tp, *d_os, *d_oz, *d_op;
+  const size_t nxr = (size_t)rows * nx, nur = (size_t)rows * nu;
+  CU(cudaMallocAsync((void**)&d_ts, sizeof(double) * (4 * nxr + 2 * nur), pl->stream));
+  d_tz = d_ts + nxr; d_os = d_tz + nxr; d_oz = d_os + nxr; d_tp = d_oz + nxr; d_op = d_tp + nur;
+  CU(cudaMemcpyAsync(d_ts, t_sig, sizeof(double) * nxr, cudaMemcpyHostToDevice, pl->stream));
+  CU(cudaMemcpyAsync(d_tz, t_zeta, sizeof(double) * nxr, cudaMemcpyHostToDevice, pl->stream));
+  CU(cudaMemcpyAsync(d_tp, t_psi, sizeof(double) * nur, cudaMemcpyHostToDevice, pl->stream));
+  ProxArgs a{};
+  a.rows = rows; a.nx = nx; a.nu = nu; a.lam = lam; a.Wx = pl->ctx.Wx; a.gamma_d = pl->ctx.gamma_d;
+  const bool sc = use_scaling && pl->base.scaled;
+  a.edge_stage = sc ? pl->base.edge_stage : nullptr;
+  a.sig_stage = sc ? pl->sig_c : nullptr;
+  a.zeta_stage = sc ? pl->zeta_c : nullptr;
+  a.psi_stage = sc ? pl->psi_c : nullptr;
+  a.x_s = pl->base.x_s; a.x_min = pl->base.x_min; a.x_max = pl->base.x_max;
+  a.u_min = pl->base.u_min; a.u_max = pl->base.u_max;
+  a.t_sig = d_ts; a.t_zeta = d_tz; a.t_psi = d_tp; a.o_sig = d_os; a.o_zeta = d_oz; a.o_psi = d_op;
+  prox_kernel<<<grid_for(rows), 256, 0, pl->stream>>>(a);
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(o_sig, d_os, sizeof(double) * nxr, cudaMemcpyDeviceToHost, pl->stream));
+  CU(cudaMemcpyAsync(o_zeta, d_oz, sizeof(double) * nxr, cudaMemcpyDeviceToHost, pl->stream));
+  CU(cudaMemcpyAsync(o_psi, d_op, sizeof(double) * nur, cudaMemcpyDeviceToHost, pl->stream));
+  CU(cudaFreeAsync(d_ts, pl->stream));
+  CU(cudaStreamSynchronize(pl->stream));
+  return TSMPC_OK;
+}
+
+int tsmpc_dual_operator_begin(tsmpc_plan* pl, const double* beta0) {
+  if (!pl || !beta0) return fail(TSMPC_ERR_ARGUMENT, "null argument");
+  CU(cudaSetDevice(pl->device));
+  const int E = pl->E;
+  if (pl->put_rows(pl->BETA0, pl->NVP, beta0, pl->nv, E)) return TSMPC_ERR_CUDA;
+  const size_t yblk = 2 * (size_t)E * pl->NXP + (size_t)E * pl->NUP;
+  CU(cudaMemsetAsync(pl->PY, 0, sizeof(double) * yblk, pl->stream));
+  if (set_root(pl, nullptr)) return TSMPC_ERR_CUDA;
+  if (run_step(pl, pl->PY, 1, pl->BETA0, nullptr, nullptr)) return TSMPC_ERR_CUDA;
+  CU(cudaMemcpyAsync(pl->Z0X, pl->X, sizeof(double) * (size_t)pl->n_nodes * pl->NXP, cudaMemcpyDeviceToDevice, pl->stream));
+  CU(cudaMemcpyAsync(pl->Z0U, pl->U, sizeof(double) * (size_t)E * pl->NUP, cudaMemcpyDeviceToDevice, pl->stream));
+  CU(cudaStreamSynchronize(pl->stream));
+  pl->has_op = true;
+  return TSMPC_OK;
+}
+
+int tsmpc_dual_operator_set_ones(tsmpc_plan* pl) {
+  if (!pl || !pl->has_op) return fail(TSMPC_ERR_ARGUMENT, "dual operator not initialised");
+  const int E = pl->E;
+  std::vector<double> ones((size_t)E * std::max(pl->nx, pl->nu), 1.0);
+  if (pl->put_rows(pl->PY, pl->NXP, ones.data(), pl->nx, E) ||
+      pl->put_rows(pl->PY + (size_t)E * pl->NXP, pl->NXP, ones.data(), pl->nx, E) ||
+      pl->put_rows(pl->PY + 2 * (size_t)E * pl->NXP, pl->NUP, ones.data(), pl->nu, E))
+    return TSMPC_ERR_CUDA;
+  CU(cudaStreamSynchronize(pl->stream));
+  return TSMPC_OK;
+}
+
+int tsmpc_dual_operator_step(tsmpc_plan* pl, double* y_dot_dy, double* dy_dot_dy, double* y_dot_y) {
+  if (!pl || !pl->has_op) return fail(TSMPC_ERR_ARGUMENT, "dual operator not initialised");
+  CU(cudaSetDevice(pl->device));
+  EdgeCtx c = pl->ctx;
+  if (!pl->base.scaled) { c.sig_stage = c.zeta_stage = c.psi_stage = nullptr; }
+  const int E = pl->E, G = grid_for(E);
+  dual_sq_rows_kernel<<<G, 256, 0, pl->stream>>>(c, pl->PY, pl->ROWS);
+  reduce_cols_kernel<<<1, 1024, 0, pl->stream>>>(pl->ROWS, E, 3, pl->RED);
+  double sq[3];
+  CU(cudaMemcpyAsync(sq, pl->RED, sizeof(sq), cudaMemcpyDeviceToHost, pl->stream));
+  CU(cudaStreamSynchronize(pl->stream));
+  const double yy = (sq[0] + sq[1]) + sq[2];
+  if (y_dot_y) *y_dot_y = yy;
+  if (!(yy > 0.0)) return fail(TSMPC_ERR_VALIDATION, "dual operator vanished during power iteration");
+  dual_normalize_kernel<<<G, 256, 0, pl->stream>>>(c, pl->PY, pl->RED);
+  CU(cudaGetLastError());
+  if (set_root(pl, nullptr)) return TSMPC_ERR_CUDA;
+  if (run_step(pl, pl->PY, 1, pl->BETA0, nullptr, nullptr)) return TSMPC_ERR_CUDA;
+  dual_apply_kernel<<<G, 256, 0, pl->stream>>>(c, pl->PY, pl->X, pl->U, pl->Z0X, pl->Z0U, pl->ROWS);
+  reduce_cols_kernel<<<1, 1024, 0, pl->stream>>>(pl->ROWS, E, 6, pl->RED);
+  CU(cudaGetLastError());
+  double d[6];
+  CU(cudaMemcpyAsync(d, pl->RED, sizeof(d), cudaMemcpyDeviceToHost, pl->stream));
+  CU(cudaStreamSynchronize(pl->stream));
+  if (y_dot_dy) *y_dot_dy = (d[0] + d[1]) + d[2];
+  if (dy_dot_dy) *dy_dot_dy = (d[3] + d[4]) + d[5];
+  return TSMPC_OK;
+}
+
+}  // extern "C"

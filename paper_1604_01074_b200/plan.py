@@ -1,0 +1,184 @@
+"""Device plan: one (model, tree, factor, scaling) resident in HBM.
+
+A :class:`DevicePlan` owns a native ``tsmpc_plan`` (``include/tsmpc.h``).
+Creating it uploads the fused operator blocks, bounds, scaling and tree arrays
+once and lets the native runtime cut the tree into segments / levels / tiles
+(``csrc/tsmpc_capi.cu:decompose``).  Per forecast only the stage cache moves
+(``set_cache``); per solve only p (and an optional warm dual) go up and the
+report comes down.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import weakref
+
+import numpy as np
+
+from . import _native as nat
+from .errors import DeviceError, DimensionError
+from .points import DualPoint, PrimalPoint
+
+__all__ = ["DevicePlan", "plan_for"]
+
+
+def _c(a, dtype=np.float64):
+    return np.ascontiguousarray(np.asarray(a, dtype=dtype))
+
+
+class DevicePlan:
+    def __init__(self, model, tree, factor, scaling=None, device: int = 0):
+        lib = nat.load_library()
+        n_x, n_u, n_v = factor.n_x, factor.n_u, factor.n_v
+        E = np.asarray(model.E, dtype=float)
+        n_e = E.shape[0]
+        pinv = E.T @ np.linalg.inv(E @ E.T)
+        keep = {
+            "A": _c(factor.A), "B": _c(model.B), "L": _c(factor.L), "Bbar": _c(factor.Bbar),
+            "Phi": _c(factor.Phi), "Psi": _c(factor.Psi), "Wu": _c(model.Wu), "E": _c(E),
+            "E_pinvT": _c(pinv.T), "u_min": _c(model.u_min), "u_max": _c(model.u_max),
+            "x_min": _c(model.x_min), "x_max": _c(model.x_max), "x_s": _c(model.x_s),
+            "stage_starts": _c(tree.stage_starts, np.int64), "anc": _c(tree.anc, np.int64),
+            "child_start": _c(tree.child_start, np.int64),
+            "child_stop": _c(tree.child_stop, np.int64), "prob": _c(tree.prob),
+        }
+        if scaling is not None:
+            keep["sig_stage"] = _c(scaling.sig_stage)
+            keep["zeta_stage"] = _c(scaling.zeta_stage)
+            keep["psi_stage"] = _c(scaling.psi_stage)
+        pb = nat.Problem()
+        pb.n_x, pb.n_u, pb.n_v = n_x, n_u, n_v
+        pb.n_d, pb.n_e, pb.N, pb.n_nodes = int(model.Gd.shape[1]), n_e, int(tree.N), int(tree.n_nodes)
+        pb.W_alpha, pb.Wx, pb.gamma_d = float(model.W_alpha), float(model.Wx), float(model.gamma_d)
+        for name, arr in keep.items():
+            setattr(pb, name, nat.iptr(arr) if arr.dtype == np.int64 else nat.dptr(arr))
+        handle = lib.tsmpc_plan_create(ctypes.byref(pb), int(device))
+        if not handle:
+            nat.check(nat.ERR_CUDA if "CUDA" in nat.last_error() or "device" in nat.last_error()
+                      else nat.ERR_VALIDATION, "tsmpc_plan_create")
+        self._lib = lib
+        self._h = ctypes.c_void_p(handle)
+        self._fin = weakref.finalize(self, lib.tsmpc_plan_destroy, ctypes.c_void_p(handle))
+        self.model, self.tree, self.factor, self.scaling = model, tree, factor, scaling
+        self.n_x, self.n_u, self.n_v = n_x, n_u, n_v
+        self.n_nodes, self.n_edges = int(tree.n_nodes), int(tree.n_edges)
+        self._cache_key = None
+
+    # -- introspection -------------------------------------------------------
+    def info(self) -> dict:
+        buf = np.zeros(9, dtype=np.int64)
+        nat.check(self._lib.tsmpc_plan_info(self._h, nat.iptr(buf), 9), "tsmpc_plan_info")
+        keys = ("levels", "ctas", "tiles", "segments", "smem_bytes", "diag_A", "threads",
+                "tile_rows", "sms")
+        return dict(zip(keys, (int(v) for v in buf)))
+
+    # -- uploads -------------------------------------------------------------
+    def set_cache(self, cache, model=None):
+        """Upload a StageCache (+ the gap's prices / junction rhs / Gd d terms)."""
+        key = (id(cache), id(cache.beta), id(cache.uhat), id(cache.evec))
+        if key == self._cache_key:
+            return
+        E, m = self.n_edges, model if model is not None else self.model
+        if cache.beta.shape != (E, self.n_v):
+            raise DimensionError("stage cache does not match the tree shape")
+        prices = jrhs = gdd = None
+        demands = np.asarray(cache.demands, dtype=float)
+        if getattr(m, "gap_inputs", True):
+            prices = _c(np.stack([m.price(cache.k + j) for j in range(self.tree.N)]))
+            jrhs = _c(-(demands @ np.asarray(m.Ed, dtype=float).T))
+            gdd = _c(demands @ np.asarray(m.Gd, dtype=float).T)
+        arrs = [_c(cache.beta), _c(cache.uhat), _c(cache.evec), _c(cache.q), prices, jrhs, gdd]
+        nat.check(self._lib.tsmpc_set_cache(self._h, *map(nat.dptr, arrs)), "tsmpc_set_cache")
+        self._cache_key = key
+        self._cache_ref = cache
+
+    # -- solver entry points ---------------------------------------------------
+    def solve(self, p, iters: int, lam: float, warm: DualPoint | None = None,
+              theta=None, coef=None, record_residuals: bool = False,
+              skip_gap: bool = False, keep_device: bool = False) -> dict:
+        E, n_x, n_u, n = self.n_edges, self.n_x, self.n_u, self.n_nodes
+        out = {
+            "u0": np.empty(n_u), "x": np.empty((n, n_x)), "u": np.empty((E, n_u)),
+            "x_avg": np.empty((n, n_x)), "u_avg": np.empty((E, n_u)),
+            "dual_sig": np.empty((E, n_x)), "dual_zeta": np.empty((E, n_x)),
+            "dual_psi": np.empty((E, n_u)),
+        }
+        res = nat.Result()
+        if not keep_device:
+            for k, v in out.items():
+                setattr(res, k, nat.dptr(v))
+        trace = np.empty(iters) if record_residuals else None
+        res.resid_trace = nat.dptr(trace)
+        flags = ((nat.RECORD_RESIDUALS if record_residuals else 0)
+                 | (nat.SKIP_GAP if skip_gap else 0) | (nat.KEEP_DEVICE if keep_device else 0))
+        ws = wz = wp = None
+        if warm is not None:
+            ws, wz, wp = _c(warm.sig), _c(warm.zeta), _c(warm.psi)
+        th = _c(theta) if theta is not None else None
+        cf = _c(coef) if coef is not None else None
+        pv = _c(p)
+        rc = self._lib.tsmpc_solve(self._h, nat.dptr(pv), int(iters), float(lam),
+                                   nat.dptr(ws), nat.dptr(wz), nat.dptr(wp),
+                                   nat.dptr(th), nat.dptr(cf), flags, ctypes.byref(res))
+        nat.check(rc, "tsmpc_solve")
+        out.update(residual_inf=float(res.residual_inf), gap=float(res.gap),
+                   device_ms=float(res.device_ms), iterations=int(res.iterations),
+                   resid_trace=trace)
+        return out
+
+    def solve_step(self, w: DualPoint, p) -> PrimalPoint:
+        x = np.empty((self.n_nodes, self.n_x))
+        u = np.empty((self.n_edges, self.n_u))
+        args = [_c(w.sig), _c(w.zeta), _c(w.psi), _c(p)]
+        nat.check(self._lib.tsmpc_solve_step(self._h, *map(nat.dptr, args), nat.dptr(x),
+                                             nat.dptr(u)), "tsmpc_solve_step")
+        return PrimalPoint(x, u)
+
+    def prox(self, t, lam: float, scaled: bool):
+        rows = t.sig.shape[0]
+        o = [np.empty_like(_c(t.sig)), np.empty_like(_c(t.zeta)), np.empty_like(_c(t.psi))]
+        args = [_c(t.sig), _c(t.zeta), _c(t.psi)]
+        nat.check(self._lib.tsmpc_prox(self._h, int(rows), *map(nat.dptr, args), float(lam),
+                                       1 if scaled else 0, *map(nat.dptr, o)), "tsmpc_prox")
+        return o
+
+    def dual_operator_begin(self, beta0):
+        nat.check(self._lib.tsmpc_dual_operator_begin(self._h, nat.dptr(_c(beta0))),
+                  "tsmpc_dual_operator_begin")
+        nat.check(self._lib.tsmpc_dual_operator_set_ones(self._h), "tsmpc_dual_operator_set_ones")
+
+    def dual_operator_step(self):
+        v = [ctypes.c_double(), ctypes.c_double(), ctypes.c_double()]
+        rc = self._lib.tsmpc_dual_operator_step(self._h, *(ctypes.byref(x) for x in v))
+        if rc != nat.OK and v[2].value == 0.0:
+            nat.check(nat.ERR_VALIDATION, "power iteration")
+        nat.check(rc, "tsmpc_dual_operator_step")
+        return v[0].value, v[1].value, v[2].value
+
+
+_PLANS: dict = {}
+_MAX_PLANS = 6
+
+
+def plan_for(model, tree, factor, scaling=None, device: int = 0) -> DevicePlan:
+    """Cached plan per (model, tree, factor, scaling) object identity."""
+    key = (id(model), id(tree), id(factor), id(scaling), device)
+    hit = _PLANS.get(key)
+    if hit is not None and hit.model is model and hit.tree is tree and hit.factor is factor \
+            and hit.scaling is scaling:
+        _PLANS[key] = _PLANS.pop(key)  # LRU touch
+        return hit
+    if len(_PLANS) >= _MAX_PLANS:
+        _PLANS.pop(next(iter(_PLANS)))
+    plan = DevicePlan(model, tree, factor, scaling, device)
+    _PLANS[key] = plan
+    return plan
+
+
+def release_plans():
+    _PLANS.clear()
+
+
+def require_device():
+    if nat.device_count() < 1:
+        raise DeviceError("no CUDA device visible to libtsmpc")

@@ -1,0 +1,127 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+vectors and the pinned CPU oracle.
+
+Tolerances: solve step and prox are single-pass fp64 contractions (rel 1e-11);
+APG outputs after the fixed iteration count use 10x the reference's own
+ulp-perturbation deviation for that case and field (stored in the
+fixture by make_golden.py), floored at 1e-11.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import ALL_CASES, SMALL_CASES, has_gpu, load_case, rel_err
+
+pytestmark = pytest.mark.gpu
+
+if not has_gpu():  # pragma: no cover - CPU container
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1604_01074_b200 import DualPoint, SplitPoint, engine, factor  # noqa: E402
+from paper_1604_01074_b200.plan import DevicePlan  # noqa: E402
+from oracle import tsmpc_oracle as O  # noqa: E402
+
+
+def _plan(c, scaled=True):
+    plan = DevicePlan(c.model, c.tree, c.factor, c.scaling if scaled else None)
+    plan.set_cache(c.cache, c.model)
+    return plan
+
+
+@pytest.mark.parametrize("name", ALL_CASES)
+def test_solve_step_matches_reference(name):
+    c = load_case(name)
+    z = c.z
+    out = factor.solve_step(c.factor, c.cache, c.tree,
+                            DualPoint(z["w_sig"], z["w_zeta"], z["w_psi"]), c.p)
+    assert rel_err(out.x, z["s_x"]) <= 1e-11
+    assert rel_err(out.u, z["s_u"]) <= 1e-11
+
+
+@pytest.mark.parametrize("name", ALL_CASES)
+def test_apg_solve_matches_reference(name):
+    c = load_case(name)
+    z = c.z
+    plan = _plan(c)
+    th, cf = engine.theta_schedule(c.iters)
+    out = plan.solve(c.p, c.iters, c.lam, theta=th, coef=cf)
+    for f in ("u0", "x", "u", "x_avg", "u_avg"):
+        assert rel_err(out[f], z[f"r_{f}"]) <= c.tol(f), (f, rel_err(out[f], z[f"r_{f}"]), c.tol(f))
+    for k in ("sig", "zeta", "psi"):
+        assert rel_err(out[f"dual_{k}"], z[f"r_dual_{k}"]) <= c.tol("dual"), k
+    r_ref = float(z["r_residual_inf"])
+    assert abs(out["residual_inf"] - r_ref) <= c.tol("residual_inf") * max(1.0, abs(r_ref))
+    g_ref = float(z["r_gap"])
+    assert abs(out["gap"] - g_ref) <= max(1e-8, c.tol("gap")) * max(1.0, abs(g_ref))
+
+
+@pytest.mark.parametrize("name", ALL_CASES)
+def test_prox_matches_reference(name):
+    c = load_case(name)
+    z = c.z
+    t = SplitPoint(z["t_sig"], z["t_zeta"], z["t_psi"])
+    out = engine.prox_g(t, 0.7, c.model)
+    np.testing.assert_array_equal(out.psi, z["pr_psi"])
+    assert rel_err(out.sig, z["pr_sig"]) <= 1e-13
+    assert rel_err(out.zeta, z["pr_zeta"]) <= 1e-13
+    if c.scaling is not None:
+        out = engine.prox_g(t, 0.7, c.model, scaling_edges=c.scaling.expand(c.tree))
+        assert rel_err(out.sig, z["prs_sig"]) <= 1e-13
+        assert rel_err(out.zeta, z["prs_zeta"]) <= 1e-13
+        np.testing.assert_array_equal(out.psi, z["prs_psi"])
+
+
+@pytest.mark.parametrize("name", ["tank3_tree_6_N8", "small_s0", "small_s4", "small_denseA",
+                                  "bcn63_CE_N24", "bcn63_SMPC1_N24"])
+def test_lambda_power_iteration_matches_reference(name):
+    c = load_case(name)
+    lam = engine.compute_lambda(c.basis, c.factor, c.model, c.tree, scaling=c.scaling)
+    assert lam == pytest.approx(c.lam, rel=1e-7)
+    lam0 = engine.compute_lambda(c.basis, c.factor, c.model, c.tree, scaling=None)
+    assert lam0 == pytest.approx(float(c.z["lam_plain"]), rel=1e-7)
+
+
+@pytest.mark.parametrize("name", SMALL_CASES)
+def test_dropin_solve_end_to_end(name):
+    """Public ``solve`` with nothing precomputed: host setup + device lambda + loop."""
+    c = load_case(name)
+    z = c.z
+    cfg = engine.SolverConfig(max_iters=c.iters, precondition=bool(z["precondition"]))
+    rep = engine.solve(c.model, c.tree, c.forecast, c.p, c.q, cfg)
+    assert rep.lam == pytest.approx(c.lam, rel=1e-7)
+    # lambda differs at ~1e-9: allow the corresponding perturbation of the iterates
+    for f in ("u0", "u_avg", "x_avg"):
+        assert rel_err(getattr(rep, f), z[f"r_{f}"]) <= max(1e-6, c.tol(f)), f
+
+
+def test_residual_trace_and_determinism():
+    c = load_case("tank3_tree_30_N8")
+    plan = _plan(c)
+    th, cf = engine.theta_schedule(c.iters)
+    a = plan.solve(c.p, c.iters, c.lam, theta=th, coef=cf, record_residuals=True)
+    b = plan.solve(c.p, c.iters, c.lam, theta=th, coef=cf, record_residuals=True)
+    for k in ("x_avg", "u_avg", "x", "u", "dual_sig", "dual_psi"):
+        assert np.array_equal(a[k], b[k]), k          # bitwise run-to-run
+    assert a["gap"] == b["gap"] and a["residual_inf"] == b["residual_inf"]
+    tr = a["resid_trace"]
+    assert tr.shape == (c.iters,) and tr[-1] == a["residual_inf"]
+    fac, cache, tree, mdl = (O.factor_dict(c.factor), O.cache_dict(c.cache, c.model, c.tree),
+                             O.tree_dict(c.tree), O.model_dict(c.model))
+    ref = O.apg(fac, cache, tree, mdl, c.p, c.lam, c.iters, O.scaling_tuple(c.scaling), record=True)
+    np.testing.assert_allclose(tr, ref["residual_trace"], rtol=1e-9, atol=1e-12)
+
+
+def test_warm_start_matches_oracle():
+    c = load_case("tank3_tree_6_N8")
+    z = c.z
+    warm = DualPoint(z["r_dual_sig"], z["r_dual_zeta"], z["r_dual_psi"])
+    plan = _plan(c)
+    th, cf = engine.theta_schedule(100)
+    out = plan.solve(c.p, 100, c.lam, warm=warm, theta=th, coef=cf)
+    fac, cache, tree, mdl = (O.factor_dict(c.factor), O.cache_dict(c.cache, c.model, c.tree),
+                             O.tree_dict(c.tree), O.model_dict(c.model))
+    ref = O.solve(fac, cache, tree, mdl, c.p, c.lam, 100, O.scaling_tuple(c.scaling),
+                  warm=[warm.sig, warm.zeta, warm.psi])
+    for f in ("u0", "u_avg", "x_avg"):
+        assert rel_err(out[f], ref[f]) <= 1e-10, f
+    assert abs(out["gap"] - ref["gap"]) <= 1e-8 * max(1.0, abs(ref["gap"]))
