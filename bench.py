@@ -1,0 +1,362 @@
+"""Benchmark: SMPC solve time & APG iterations/s on Barcelona-dimension trees (N=24).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--tree SMPC3] [--iters 500] [--no-sweep] [--no-cpu]
+
+One *step* = one full ``engine.solve`` of the workload: ``--iters`` (default 500,
+the paper's fixed count) APG iterations plus the final
+duality gap.  Headline workload: BASELINE.json configs[1], the ~100-scenario
+paper tree SMPC3 (114 scenarios, 2,431 edges) on the synthetic bcn63 network
+(Barcelona data is not shipped).  ``value`` = APG iterations/s of
+the whole job with inputs resident in HBM (device-event time of loop + gap);
+``e2e`` = the same metric through the public ``engine.solve`` call with host
+buffers (stage-cache H2D and full-report D2H inside the timed region).
+``--impl reference`` times the reference algorithm's CPU restatement
+(oracle/, the reference itself is pure Python and cannot travel) on the same
+workload, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+BYTES_PER_EDGE = 10_784        # compulsory fp64 bytes per edge per iteration
+FLOPS_PER_EDGE_REF = 108_170   # reference formulation flops per edge per iteration
+DMMA_PEAK_TFLOPS = 36.9        # measured DMMA m8n8k4 fp64 peak (tools/microbench, gpurun_out/mb.log)
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in getattr(self, "lines", []):
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def build_workload(tree_name: str, seed_offset: int = 0):
+    from paper_1604_01074_b200 import (build_stage_cache, compute_basis, compute_preconditioner,
+                                       factor_step, node_demands, synth)
+    model = synth.bcn63_network()
+    tree = synth.paper_tree(*synth.PAPER_TREES[tree_name], seed=seed_offset)
+    basis = compute_basis(model)
+    fac = factor_step(basis, model)
+    scaling = compute_preconditioner(basis, model, tree.N, tree=tree)
+    p, q = synth.initial_state(model)
+    fcs = [synth.forecast_for(tree, k=k) for k in (0, 1)]
+    caches = [build_stage_cache(basis, model, tree, node_demands(tree, f), k=f.k, q=q) for f in fcs]
+    return dict(model=model, tree=tree, basis=basis, factor=fac, scaling=scaling, p=p, q=q,
+                forecasts=fcs, caches=caches)
+
+
+def flush_l2(torch, dev):
+    buf = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    buf.fill_(1.0)
+    torch.cuda.synchronize(dev)
+
+
+def run_ours(args, ws, rank, local):
+    import torch
+    from paper_1604_01074_b200 import engine, theta_schedule
+    from paper_1604_01074_b200.plan import DevicePlan
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    W = build_workload(args.tree, seed_offset=rank)
+    tree, model = W["tree"], W["model"]
+    E = tree.n_edges
+    plan = DevicePlan(model, tree, W["factor"], W["scaling"], device=local)
+    plan.set_cache(W["caches"][0], model)
+    lam = engine.compute_lambda(W["basis"], W["factor"], model, tree, scaling=W["scaling"],
+                                device=local)
+    th, cf = theta_schedule(args.iters)
+    info = plan.info()
+
+    def step():
+        return plan.solve(W["p"], args.iters, lam, theta=th, coef=cf, keep_device=True)
+
+    for _ in range(args.warmup):
+        step()
+    # timed region: K steps, L2 flushed before each (the state of SMPC3 fits in L2)
+    per_loop, per_total, launches = [], [], 0
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush_l2(torch, dev)
+            r = step()
+            per_loop.append(r["device_ms"])
+            per_total.append(r["device_total_ms"])
+            launches += r["kernel_launches"]
+    torch.cuda.synchronize(dev)
+    total_ms = float(sum(per_total))
+    loop_ms = float(sum(per_loop))
+    if dist is not None:
+        t = torch.tensor([total_ms, loop_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, loop_ms = float(t[0]), float(t[1])
+    ms_per_step = total_ms / args.steps
+    value = ws * args.steps * args.iters / (total_ms / 1e3)
+
+    # ---- e2e through the public API (host buffers: cache H2D + report D2H per step)
+    e2e_ms = []
+    for k in range(args.warmup + args.steps):
+        cache = W["caches"][k % 2]
+        t0 = time.perf_counter()
+        rep = engine.solve(model, tree, W["forecasts"][k % 2], W["p"], W["q"],
+                           engine.SolverConfig(max_iters=args.iters), basis=W["basis"],
+                           factor=W["factor"], cache=cache, scaling=W["scaling"], lam=lam)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_ms = e2e_ms[args.warmup:]
+    e2e_total = float(sum(e2e_ms))
+    if dist is not None:
+        t = torch.tensor([e2e_total], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t[0])
+    e2e_value = ws * args.steps * args.iters / (e2e_total / 1e3)
+    n_x, n_u, n_v, n_e = model.n_x, model.n_u, 97, model.n_e
+    h2d = 8 * (E * (n_v + n_u + n_x + n_e + n_x) + n_u + tree.N * n_u + n_x)
+    d2h = 8 * (n_u + 2 * tree.n_nodes * n_x + 2 * E * n_u + E * (2 * n_x + n_u) + 1)
+
+    hbm_peak, peak_kind = peaks()
+    loop_s = (loop_ms / args.steps) / 1e3
+    achieved = E * BYTES_PER_EDGE * args.iters / loop_s / 1e9
+    fp64_tf = E * FLOPS_PER_EDGE_REF * args.iters / loop_s / 1e12
+    line = {
+        "metric": "SMPC solve time (ms) & APG iters/s vs scenario count, Barcelona DWN N=24",
+        "value": value, "unit": "APG iter/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"bcn63 {args.tree} N=24 ({tree.n_s} scenarios, {E} edges), "
+                               f"{args.iters}-iteration APG solve + duality gap",
+                   "tree": args.tree, "edges": E, "scenarios": tree.n_s, "iters": args.iters,
+                   "parallelism": "replicas" if ws > 1 else "single",
+                   "l2": "flushed (256 MB write) before every timed step",
+                   "plan": info},
+        "e2e": {"value": e2e_value, "unit": "APG iter/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / args.steps,
+                "call": "paper_1604_01074_b200.engine.solve (precomputed basis/factor/scaling/lam)"},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": None,
+                     "kernel": "tsmpc::apg_persistent_kernel",
+                     "peak_source": peak_kind,
+                     "fp64": {"achieved_tflops_ref_formulation": fp64_tf,
+                              "dmma_peak_tflops": DMMA_PEAK_TFLOPS,
+                              "frac": fp64_tf / DMMA_PEAK_TFLOPS}},
+        "solve_ms": {"loop": loop_ms / args.steps, "loop_plus_gap": ms_per_step},
+        "clocks": clk.summary(),
+    }
+    if not args.no_sweep and rank == 0:
+        line["sweep"] = sweep(args, lam_cache={args.tree: lam}, local=local)
+    if rank == 0 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(W, lam, args)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line))
+
+
+def sweep(args, lam_cache, local):
+    from paper_1604_01074_b200 import engine, theta_schedule
+    from paper_1604_01074_b200.plan import DevicePlan
+    out = {}
+    hbm_peak, _ = peaks()
+    for name in ("CE", "SMPC1", "SMPC3", "SMPC8"):
+        W = build_workload(name)
+        plan = DevicePlan(W["model"], W["tree"], W["factor"], W["scaling"], device=local)
+        plan.set_cache(W["caches"][0], W["model"])
+        lam = lam_cache.get(name) or engine.compute_lambda(W["basis"], W["factor"], W["model"],
+                                                           W["tree"], scaling=W["scaling"],
+                                                           device=local)
+        th, cf = theta_schedule(args.iters)
+        for _ in range(2):
+            plan.solve(W["p"], args.iters, lam, theta=th, coef=cf, keep_device=True)
+        rs = [plan.solve(W["p"], args.iters, lam, theta=th, coef=cf, keep_device=True)
+              for _ in range(3)]
+        loop = statistics.median(r["device_ms"] for r in rs)
+        tot = statistics.median(r["device_total_ms"] for r in rs)
+        E = W["tree"].n_edges
+        out[name] = {"edges": E, "scenarios": W["tree"].n_s, "solve_ms": tot, "loop_ms": loop,
+                     "iters_per_s": args.iters / (tot / 1e3),
+                     "us_per_iter": loop * 1e3 / args.iters,
+                     "hbm_frac": E * BYTES_PER_EDGE * args.iters / (loop / 1e3) / 1e9 / hbm_peak,
+                     "levels": plan.info()["levels"], "ctas": plan.info()["ctas"]}
+    return out
+
+
+def cpu_baseline(W, lam, args, iters_sample: int | None = None):
+    """Reference algorithm (oracle port, BLAS pinned to 1 thread as engine.py:535 does)."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import tsmpc_oracle as O
+    it = iters_sample or args.cpu_iters
+    fac = O.factor_dict(W["factor"])
+    cache = O.cache_dict(W["caches"][0], W["model"], W["tree"])
+    tree = O.tree_dict(W["tree"])
+    mdl = O.model_dict(W["model"])
+    scal = O.scaling_tuple(W["scaling"])
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        O.apg(fac, cache, tree, mdl, W["p"], lam, it, scal)
+        dt = time.perf_counter() - t0
+    return {"value": it / dt, "unit": "APG iter/s", "cores": 1, "kind": "port",
+            "sample": f"{it} APG iterations of bcn63 {args.tree} (oracle/tsmpc_oracle.py.apg, "
+                      f"numpy/scipy, BLAS pinned to 1 thread like engine.py:535), {dt:.2f} s",
+            "host": _cpu_model(), "nproc": os.cpu_count()}
+
+
+def _cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    W = build_workload(args.tree)
+    # The step size changes the iterates, not the work per iteration; the bcn63 value
+    # (tests/golden/bcn63_*: lam = 0.4797) keeps this arm free of any GPU code.
+    lam = 0.4797
+    from threadpoolctl import threadpool_limits
+
+    from oracle import tsmpc_oracle as O
+    fac = O.factor_dict(W["factor"])
+    cache = O.cache_dict(W["caches"][0], W["model"], W["tree"])
+    tree = O.tree_dict(W["tree"])
+    mdl = O.model_dict(W["model"])
+    scal = O.scaling_tuple(W["scaling"])
+    it = args.ref_iters
+    times = []
+    with threadpool_limits(limits=1):
+        for k in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            O.apg(fac, cache, tree, mdl, W["p"], lam, it, scal)
+            if k >= args.warmup:
+                times.append(time.perf_counter() - t0)
+    total = float(sum(times))
+    value = args.steps * it / total
+    line = {
+        "impl": "reference",
+        "metric": "SMPC solve time (ms) & APG iters/s vs scenario count, Barcelona DWN N=24",
+        "value": value, "unit": "APG iter/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3 * args.iters / it,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"bcn63 {args.tree} N=24 ({W['tree'].n_s} scenarios, "
+                               f"{W['tree'].n_edges} edges), {args.iters}-iteration APG solve",
+                   "tree": args.tree, "edges": W["tree"].n_edges, "iters": args.iters,
+                   "sample_iters_per_step": it},
+        "cpu_baseline": {"value": value, "unit": "APG iter/s", "cores": 1, "kind": "port",
+                         "sample": f"{it} APG iterations per step (reference algorithm restated "
+                                   "in oracle/tsmpc_oracle.py; BLAS pinned to 1 thread as the "
+                                   "reference does, engine.py:535)",
+                         "host": _cpu_model(), "nproc": os.cpu_count()},
+        "e2e": {"value": value, "unit": "APG iter/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--tree", default="SMPC3", choices=("CE", "SMPC1", "SMPC3", "SMPC8", "W4k"))
+    ap.add_argument("--iters", type=int, default=500)
+    ap.add_argument("--cpu-iters", type=int, default=200)
+    ap.add_argument("--ref-iters", type=int, default=40)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_ours(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -92,6 +92,8 @@ typedef struct tsmpc_result {
   double gap;          /* out (NaN when TSMPC_SKIP_GAP)                        */
   double device_ms;    /* out: CUDA-event time of the on-device iteration loop */
   int32_t iterations;  /* out: iterations actually run                         */
+  double device_total_ms;   /* out: CUDA-event time of loop + duality gap        */
+  int64_t kernel_launches;  /* out: libtsmpc kernels launched by this call       */
 } tsmpc_result;
 
 #define TSMPC_RECORD_RESIDUALS 1   /* residual_inf of every iteration -> resid_trace */
@@ -141,6 +143,8 @@ int tsmpc_dual_operator_step(tsmpc_plan* plan, double* y_dot_dy, double* dy_dot_
 /* Introspection (tests / bench). */
 int tsmpc_plan_info(const tsmpc_plan* plan, int64_t* info, int32_t n_info);
 const char* tsmpc_last_error(void);
+/* Phase cycle counters of CTA 0 (non-zero only in -DTSMPC_TIMERS builds); reset on read. */
+int tsmpc_debug_timers(tsmpc_plan* plan, uint64_t* out, int32_t n);
 int tsmpc_device_count(void);
 
 #ifdef __cplusplus

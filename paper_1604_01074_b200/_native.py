@@ -50,6 +50,7 @@ class Result(ctypes.Structure):
         ("dual_sig", _dp), ("dual_zeta", _dp), ("dual_psi", _dp), ("resid_trace", _dp),
         ("residual_inf", ctypes.c_double), ("gap", ctypes.c_double),
         ("device_ms", ctypes.c_double), ("iterations", ctypes.c_int32),
+        ("device_total_ms", ctypes.c_double), ("kernel_launches", ctypes.c_int64),
     ]
 
 
@@ -70,15 +71,29 @@ SIGNATURES = {
     "tsmpc_plan_info": (ctypes.c_int, [ctypes.c_void_p, _ip, ctypes.c_int32]),
     "tsmpc_last_error": (ctypes.c_char_p, []),
     "tsmpc_device_count": (ctypes.c_int, []),
+    "tsmpc_debug_timers": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64),
+                                          ctypes.c_int32]),
 }
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]
 
 
-def build_library(force: bool = False, verbose: bool = False) -> pathlib.Path:
-    """Compile ``libtsmpc.so`` in-tree for sm_100a (cross-compiles without a GPU)."""
+def build_library(force: bool = False, verbose: bool = False, timers: bool = False) -> pathlib.Path:
+    """Compile ``libtsmpc.so`` in-tree for sm_100a (cross-compiles without a GPU).
+
+    ``timers=True`` builds the phase-timer profiling variant ``libtsmpc_timers.so``
+    (load it with ``TSMPC_LIB=.../libtsmpc_timers.so``).
+    """
     srcs = [CSRC / s for s in SOURCES]
+    if timers:
+        out = PKG_DIR / "libtsmpc_timers.so"
+        cmd = [os.environ.get("NVCC", "nvcc"), *NVCC_FLAGS, "-DTSMPC_TIMERS", "-o", str(out),
+               *map(str, srcs)]
+        res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise DeviceError(f"nvcc failed:\n{res.stderr[-4000:]}")
+        return out
     deps = srcs + list(CSRC.glob("*.cuh")) + [PKG_DIR.parent / "include" / "tsmpc.h"]
     if not force and LIB_PATH.exists():
         newest = max(p.stat().st_mtime for p in deps)
@@ -102,10 +117,11 @@ def load_library() -> ctypes.CDLL:
     global _LIB
     if _LIB is not None:
         return _LIB
-    if not LIB_PATH.exists():
-        raise DeviceError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+    path = pathlib.Path(os.environ.get("TSMPC_LIB", str(LIB_PATH)))
+    if not path.exists():
+        raise DeviceError(f"{path} is missing: run __graft_entry__.build() "
                           "(or paper_1604_01074_b200._native.build_library())")
-    lib = ctypes.CDLL(str(LIB_PATH))
+    lib = ctypes.CDLL(str(path))
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.restype = res

@@ -1,11 +1,24 @@
 // tsmpc_apg.cu — persistent cooperative APG kernel for sm_100a.
 // See tsmpc_kernels.cuh for the algorithm outline and DESIGN.md for the
 // derivation, data layout and roofline.
+//
+// Shared memory is one dynamic array (g_smem) addressed by per-phase offsets so
+// that every tile access compiles to LDS/STS (a generic pointer passed across a
+// call would turn them into generic loads).  A tile of <= kTileM edge rows uses
+//   backward: A = [xiq | psi^] (LDA1 = 180 cols), C = h (LDB1 = 104 cols)
+//   forward:  A = S then x     (LDA2 = 100 cols), C = [u | bv + e] (LDB2 = 184)
+// i.e. 284 doubles per row in both sweeps.  Every global read of a phase is
+// issued up front (one warp per edge row), per-row bias terms are folded into
+// the GEMM epilogues and the sequential stage scans touch shared memory only.
 #include "tsmpc_kernels.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace tsmpc {
+
+extern __shared__ __align__(16) double g_smem[];
+
+constexpr int kChunks = 4;  // n_x, n_u <= 128: a row is at most 4 x 32 lanes
 
 __device__ __forceinline__ void dmma8x8x4(double (&c)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -13,17 +26,28 @@ __device__ __forceinline__ void dmma8x8x4(double (&c)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-// C[rows, nt*8 .. nt*8+7] = A[rows, 0:4*KS] * B for every n-tile owned by this
-// warp.  A is a shared-memory tile (row-major, lda = 4 mod 16 for conflict-free
-// fragment loads), B is global memory in fragment order [NT][KS][32] so each
-// warp-wide B load is one coalesced 256-byte transaction; B fragments are
-// register-prefetched 8 k-steps ahead and reused across all MT m-tiles.
+// Tile metadata ints after the double region: edge[kTileM], lo[kTileM], hi[kTileM], misc[4]
+__device__ __forceinline__ int* meta_base(const Params& P) {
+  return reinterpret_cast<int*>(g_smem + P.META_OFF);
+}
+#define SM_EDGE(P) (meta_base(P))
+#define SM_LO(P) (meta_base(P) + kTileM)
+#define SM_HI(P) (meta_base(P) + 2 * kTileM)
+#define SM_MISC(P) (meta_base(P) + 3 * kTileM)
+
+// C[rows, nt*8 .. nt*8+7] = A[rows, 0:4*KS] * B + C for every n-tile owned by
+// this warp (C holds the per-row bias, staged by the caller's load phase; rows
+// >= nrows are overwritten, not accumulated).  A = g_smem[a_off ...] row-major
+// with lda = 4 mod 16 (conflict-free fragment loads), B in global memory in
+// fragment order [NT][KS][32] (one coalesced 256-byte load per warp and k-step),
+// register-prefetched 8 k-steps ahead and reused across the MT m-tiles.
 template <int MT>
-__device__ __forceinline__ void gemm_tile(const double* __restrict__ As, int lda, int KS, int NT,
-                                          const double* __restrict__ Bf, double* __restrict__ Cs,
-                                          int ldc) {
+__device__ __forceinline__ void gemm_tile(const Params& P, int a_off, int lda, int KS, int NT,
+                                          const double* __restrict__ Bf, int c_off, int ldc,
+                                          int nrows) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ar = lane >> 2, ac = lane & 3;
+  const double* As = g_smem + a_off + ar * lda + ac;
   for (int nt = warp; nt < NT; nt += kWarps) {
     double acc[MT][2];
 #pragma unroll
@@ -32,66 +56,75 @@ __device__ __forceinline__ void gemm_tile(const double* __restrict__ As, int lda
     double bq[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) bq[q] = (q < KS) ? __ldg(bp + q * 32) : 0.0;
-    const double* ap = As + ar * lda + ac;
     for (int ks0 = 0; ks0 < KS; ks0 += 8) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const int ks = ks0 + q;
         if (ks < KS) {
-          const double b = bq[q];
-          if (ks + 8 < KS) bq[q] = __ldg(bp + (ks + 8) * 32);
+          // all A fragments of the k-step in distinct registers, then the DMMAs read
+          // the ring slot directly; the slot is refilled (8 k-steps ahead) only after
+          // its last use, so no move ever waits on an in-flight load
+          double af[MT];
 #pragma unroll
-          for (int m = 0; m < MT; ++m) dmma8x8x4(acc[m], ap[m * 8 * lda + ks * 4], b);
+          for (int m = 0; m < MT; ++m) af[m] = As[m * 8 * lda + ks * 4];
+#pragma unroll
+          for (int m = 0; m < MT; ++m) dmma8x8x4(acc[m], af[m], bq[q]);
+          if (ks + 8 < KS) bq[q] = __ldg(bp + (ks + 8) * 32);
         }
       }
     }
+    const int c0 = nt * 8 + 2 * ac;
 #pragma unroll
     for (int m = 0; m < MT; ++m) {
-      double* cp = Cs + (m * 8 + ar) * ldc + nt * 8 + 2 * ac;
-      cp[0] = acc[m][0];
-      cp[1] = acc[m][1];
+      const int r = m * 8 + ar;
+      double* cp = g_smem + c_off + r * ldc + c0;
+      if (r < nrows) {
+        cp[0] = __dadd_rn(acc[m][0], cp[0]);
+        cp[1] = __dadd_rn(acc[m][1], cp[1]);
+      } else {
+        cp[0] = acc[m][0];
+        cp[1] = acc[m][1];
+      }
     }
   }
 }
 
-__device__ __noinline__ void gemm_dispatch(int mt, const double* As, int lda, int KS, int NT,
-                                           const double* Bf, double* Cs, int ldc) {
+__device__ __noinline__ void gemm_dispatch(const Params& P, int mt, int a_off, int lda, int KS, int NT,
+                                           const double* Bf, int c_off, int ldc, int nrows) {
   switch (mt) {
-    case 1: gemm_tile<1>(As, lda, KS, NT, Bf, Cs, ldc); break;
-    case 2: gemm_tile<2>(As, lda, KS, NT, Bf, Cs, ldc); break;
-    case 3: gemm_tile<3>(As, lda, KS, NT, Bf, Cs, ldc); break;
-    case 4: gemm_tile<4>(As, lda, KS, NT, Bf, Cs, ldc); break;
-    case 5: gemm_tile<5>(As, lda, KS, NT, Bf, Cs, ldc); break;
-    case 6: gemm_tile<6>(As, lda, KS, NT, Bf, Cs, ldc); break;
-    case 7: gemm_tile<7>(As, lda, KS, NT, Bf, Cs, ldc); break;
-    default: gemm_tile<8>(As, lda, KS, NT, Bf, Cs, ldc); break;
+    case 1: gemm_tile<1>(P, a_off, lda, KS, NT, Bf, c_off, ldc, nrows); break;
+    case 2: gemm_tile<2>(P, a_off, lda, KS, NT, Bf, c_off, ldc, nrows); break;
+    case 3: gemm_tile<3>(P, a_off, lda, KS, NT, Bf, c_off, ldc, nrows); break;
+    case 4: gemm_tile<4>(P, a_off, lda, KS, NT, Bf, c_off, ldc, nrows); break;
+    case 5: gemm_tile<5>(P, a_off, lda, KS, NT, Bf, c_off, ldc, nrows); break;
+    case 6: gemm_tile<6>(P, a_off, lda, KS, NT, Bf, c_off, ldc, nrows); break;
+    case 7: gemm_tile<7>(P, a_off, lda, KS, NT, Bf, c_off, ldc, nrows); break;
+    case 8: gemm_tile<8>(P, a_off, lda, KS, NT, Bf, c_off, ldc, nrows); break;
+    case 9: gemm_tile<9>(P, a_off, lda, KS, NT, Bf, c_off, ldc, nrows); break;
+    case 10: gemm_tile<10>(P, a_off, lda, KS, NT, Bf, c_off, ldc, nrows); break;
+    case 11: gemm_tile<11>(P, a_off, lda, KS, NT, Bf, c_off, ldc, nrows); break;
+    default: gemm_tile<12>(P, a_off, lda, KS, NT, Bf, c_off, ldc, nrows); break;
   }
 }
 
-struct Smem {
-  double* A;   // kTileM x LDA
-  double* B;   // kTileM x LDB
-  int* edge;   // kTileM
-  int* lo;     // kTileM
-  int* hi;     // kTileM
-  int* misc;   // [0] = longest segment of the tile
-};
-
-__device__ __forceinline__ void load_tile(const Params& P, int tile, const Smem& sm, int& nrows,
-                                          int& nsegs) {
+__device__ __forceinline__ void load_tile(const Params& P, int tile, int& nrows, int& nsegs) {
   const int sg0 = P.tile_seg[tile], sg1 = P.tile_seg[tile + 1];
   const int rbase = P.seg_row[sg0];
   nrows = P.seg_row[sg1] - rbase;
   nsegs = sg1 - sg0;
+  int* edge = SM_EDGE(P);
+  int* lo = SM_LO(P);
+  int* hi = SM_HI(P);
+  int* misc = SM_MISC(P);
   __syncthreads();  // the previous tile is done with shared memory
-  for (int i = threadIdx.x; i < nrows; i += kThreads) sm.edge[i] = P.row_edge[rbase + i];
-  if (threadIdx.x == 0) sm.misc[0] = 0;
+  for (int i = threadIdx.x; i < nrows; i += kThreads) edge[i] = P.row_edge[rbase + i];
+  if (threadIdx.x == 0) misc[0] = 0;
   __syncthreads();
   for (int i = threadIdx.x; i < nsegs; i += kThreads) {
-    const int lo = P.seg_row[sg0 + i] - rbase, hi = P.seg_row[sg0 + i + 1] - rbase;
-    sm.lo[i] = lo;
-    sm.hi[i] = hi;
-    atomicMax(sm.misc, hi - lo);
+    const int l = P.seg_row[sg0 + i] - rbase, h = P.seg_row[sg0 + i + 1] - rbase;
+    lo[i] = l;
+    hi[i] = h;
+    atomicMax(misc, h - l);
   }
   __syncthreads();
 }
@@ -106,216 +139,306 @@ __device__ __forceinline__ double extrap(double y, double yp, double c) {
   return __dadd_rn(y, __dmul_rn(c, __dsub_rn(y, yp)));
 }
 
+// sum_{c in children(node)} buf[c-1][i] for the edges below `node`
+__device__ __forceinline__ double child_sum(const Params& P, const double* buf, int ld, int node, int i) {
+  const int c0 = P.child_start[node] - 1, c1 = P.child_stop[node] - 1;
+  double acc = 0.0;
+  for (int ch = c0; ch < c1; ++ch) acc = __dadd_rn(acc, buf[(size_t)ch * ld + i]);
+  return acc;
+}
+
+// S of the parent edge of a segment head: the trunk GEMM output (collapsed mode)
+// or the parent segment's tail S left in T (level mode).
+__device__ __forceinline__ double head_parent_S(const Params& P, int pa, int j) {
+  if (pa < 0) return 0.0;
+  if (P.collapsed) return P.OUT[(size_t)P.trunk_pos[pa] * P.OUT_LD + j];
+  return P.T[(size_t)pa * P.NVP + j];
+}
+
+// x_i at the node below trunk position tp: x = a x + (bv + e) down the trunk path.
+__device__ __forceinline__ double trunk_x(const Params& P, int tp, int i) {
+  double x = P.p[i];
+  const double a = P.a_diag[i];
+  const int k0 = P.path_ptr[tp], k1 = P.path_ptr[tp + 1];
+  for (int k = k0; k < k1; ++k)
+    x = __dadd_rn(__dmul_rn(x, a), P.OUT[(size_t)P.path_list[k] * P.OUT_LD + P.X_OFF + i]);
+  return x;
+}
+
+__device__ void rows_epilogue(const Params& P, int nu, int nrows);
+
 // ---------------------------------------------------------------------------
 // backward sweep of one tile
 // ---------------------------------------------------------------------------
-__device__ void bwd_tile(const Params& P, int tile, int nu, const Smem& sm) {
+__device__ __noinline__ void bwd_tile(const Params& P, int tile, int nu) {
   int nrows, nsegs;
-  load_tile(P, tile, sm, nrows, nsegs);
-  const int tid = threadIdx.x;
+  load_tile(P, tile, nrows, nsegs);
+  long long tm_ = clock64();
+  (void)tm_;
+  const int LDA = P.LDA1, LDB = P.LDB1;
+  double* const SA = g_smem;
+  double* const SB = g_smem + kTileM * LDA;
+  const int* const edge = SM_EDGE(P);
+  const int* const slo = SM_LO(P);
+  const int* const shi = SM_HI(P);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int E = P.n_edges;
   const int cur = (P.slot0 + nu) & 1;
-  const double* Y = P.ybuf[cur];
-  const double* Yp = P.ybuf[cur ^ 1];
+  const double* __restrict__ Y = P.ybuf[cur];
+  const double* __restrict__ Yp = P.ybuf[cur ^ 1];
   const bool apg = P.mode == kModeApg;
   const double c = apg ? P.coef[nu] : 0.0;
-  const int K1 = P.KS1 * 4;
   const size_t zoff = (size_t)E * P.NXP, poff = 2 * (size_t)E * P.NXP;
 
-  // (1) operand rows [s | psi^] in shared memory
-  for (int idx = tid; idx < nrows * K1; idx += kThreads) {
-    const int r = idx / K1, k = idx - r * K1;
-    const int e = sm.edge[r];
+  // (1) operand rows [s | psi^]; a warp owns a row and issues all its loads first
+  for (int r = warp; r < nrows; r += kWarps) {
+    const int e = edge[r];
     const int st = P.edge_stage[e];
-    double v = 0.0;
-    if (k < P.NXP) {
-      if (k < P.nx) {
-        const size_t o = (size_t)e * P.NXP + k;
-        const double ws = apg ? extrap(Y[o], Yp[o], c) : Y[o];
-        const double wz = apg ? extrap(Y[zoff + o], Yp[zoff + o], c) : Y[zoff + o];
-        v = __dadd_rn(__dmul_rn(ws, stage_scale(P.sig_stage, st, P.scaled)),
-                      __dmul_rn(wz, stage_scale(P.zeta_stage, st, P.scaled)));
+    const double ds = stage_scale(P.sig_stage, st, P.scaled);
+    const double dz = stage_scale(P.zeta_stage, st, P.scaled);
+    const double* ys = Y + (size_t)e * P.NXP;
+    const double* yps = Yp + (size_t)e * P.NXP;
+    const double* yp_ = Y + poff + (size_t)e * P.NUP;
+    const double* ypp = Yp + poff + (size_t)e * P.NUP;
+    const double* bt = P.beta + (size_t)e * P.NVP;
+    double a[kChunks], b[kChunks], g[kChunks], h[kChunks], pv[kChunks], pp[kChunks], bb[kChunks];
+#pragma unroll
+    for (int q = 0; q < kChunks; ++q) {
+      const int i = lane + 32 * q;
+      const bool okx = i < P.nx, oku = i < P.nu;
+      a[q] = okx ? ys[i] : 0.0;
+      g[q] = okx ? ys[zoff + i] : 0.0;
+      pv[q] = oku ? yp_[i] : 0.0;
+      b[q] = (apg && okx) ? yps[i] : 0.0;
+      h[q] = (apg && okx) ? yps[zoff + i] : 0.0;
+      pp[q] = (apg && oku) ? ypp[i] : 0.0;
+      bb[q] = i < P.nv ? bt[i] : 0.0;
+    }
+    // GEMM 1 accumulates onto its C tile: stage beta there (zero pad columns)
+#pragma unroll
+    for (int q = 0; q < kChunks; ++q) {
+      const int j = lane + 32 * q;
+      if (j < P.NT1 * 8) SB[r * LDB + j] = bb[q];
+    }
+    double* row = SA + r * LDA;
+#pragma unroll
+    for (int q = 0; q < kChunks; ++q) {
+      const int i = lane + 32 * q;
+      if (i < P.NXP) {
+        double v = 0.0;
+        if (i < P.nx) {
+          const double ws = apg ? extrap(a[q], b[q], c) : a[q];
+          const double wz = apg ? extrap(g[q], h[q], c) : g[q];
+          v = __dadd_rn(__dmul_rn(ws, ds), __dmul_rn(wz, dz));
+        }
+        row[i] = v;
       }
-    } else {
-      const int j = k - P.NXP;
-      if (j < P.nu) {
-        const size_t o = poff + (size_t)e * P.NUP + j;
-        const double wp = apg ? extrap(Y[o], Yp[o], c) : Y[o];
-        v = P.scaled ? __dmul_rn(wp, P.psi_stage[(size_t)st * P.NUP + j]) : wp;
+      if (i < P.NUP) {
+        double v = 0.0;
+        if (i < P.nu) {
+          const double wp = apg ? extrap(pv[q], pp[q], c) : pv[q];
+          v = P.scaled ? __dmul_rn(wp, P.psi_stage[(size_t)st * P.NUP + i]) : wp;
+        }
+        row[P.NXP + i] = v;
       }
     }
-    sm.A[r * P.LDA + k] = v;
   }
   __syncthreads();
+  TSMPC_MARK(P, 0, tm_);
 
   // (2) xiq scan, tail -> head:  xiq_e = s_e + A' sum_{children} xiq_c
   if (P.diagA) {
     for (int idx = tid; idx < nsegs * P.nx; idx += kThreads) {
       const int s = idx / P.nx, i = idx - s * P.nx;
-      const int lo = sm.lo[s], hi = sm.hi[s];
-      const int tail_node = sm.edge[hi - 1] + 1;
-      const int c0 = P.child_start[tail_node] - 1, c1 = P.child_stop[tail_node] - 1;
-      double acc = 0.0;
-      for (int ch = c0; ch < c1; ++ch) acc = __dadd_rn(acc, P.XIQG[(size_t)ch * P.NXP + i]);
+      const int lo = slo[s], hi = shi[s];
+      const double acc = child_sum(P, P.XIQG, P.NXP, edge[hi - 1] + 1, i);
       const double a = P.a_diag[i];
-      double x = __dadd_rn(sm.A[(hi - 1) * P.LDA + i], __dmul_rn(acc, a));
-      sm.A[(hi - 1) * P.LDA + i] = x;
+      double x = __dadd_rn(SA[(hi - 1) * LDA + i], __dmul_rn(acc, a));
+      SA[(hi - 1) * LDA + i] = x;
       for (int r = hi - 2; r >= lo; --r) {
-        x = __dadd_rn(sm.A[r * P.LDA + i], __dmul_rn(x, a));
-        sm.A[r * P.LDA + i] = x;
+        x = __dadd_rn(SA[r * LDA + i], __dmul_rn(x, a));
+        SA[r * LDA + i] = x;
       }
-      P.XIQG[(size_t)sm.edge[lo] * P.NXP + i] = x;
+      P.XIQG[(size_t)edge[lo] * P.NXP + i] = x;
     }
   } else {
-    // dense A: children sums into B scratch, then depth-synchronous GEMV steps
-    for (int idx = tid; idx < nsegs * P.nx; idx += kThreads) {
-      const int s = idx / P.nx, i = idx - s * P.nx;
-      const int tail_node = sm.edge[sm.hi[s] - 1] + 1;
-      const int c0 = P.child_start[tail_node] - 1, c1 = P.child_stop[tail_node] - 1;
-      double acc = 0.0;
-      for (int ch = c0; ch < c1; ++ch) acc = __dadd_rn(acc, P.XIQG[(size_t)ch * P.NXP + i]);
-      sm.B[s * P.LDB + i] = acc;
-    }
-    __syncthreads();
-    const int maxlen = sm.misc[0];
+    // dense A (level mode only): depth-synchronous GEMV steps; step 0 reads the
+    // children sums straight from global memory (the C tile already holds beta)
+    const int maxlen = SM_MISC(P)[0];
     for (int d = 0; d < maxlen; ++d) {
       for (int idx = tid; idx < nsegs * P.nx; idx += kThreads) {
         const int s = idx / P.nx, i = idx - s * P.nx;
-        const int lo = sm.lo[s], hi = sm.hi[s];
+        const int lo = slo[s], hi = shi[s];
         const int r = hi - 1 - d;
         if (r < lo) continue;
-        // step d writes row r and reads only row r+1 (or the children sum): no hazard
-        const double* prev = (d == 0) ? (sm.B + s * P.LDB) : (sm.A + (r + 1) * P.LDA);
+        // step d writes row r and reads only row r+1 (or the children sums): no hazard
         double q = 0.0;
-        for (int j = 0; j < P.nx; ++j) q = fma(prev[j], P.A[(size_t)j * P.nx + i], q);
-        sm.A[r * P.LDA + i] = __dadd_rn(sm.A[r * P.LDA + i], q);
+        if (d == 0) {
+          const int tail_node = edge[hi - 1] + 1;
+          for (int j = 0; j < P.nx; ++j)
+            q = fma(child_sum(P, P.XIQG, P.NXP, tail_node, j), P.A[(size_t)j * P.nx + i], q);
+        } else {
+          const double* prev = SA + (r + 1) * LDA;
+          for (int j = 0; j < P.nx; ++j) q = fma(prev[j], P.A[(size_t)j * P.nx + i], q);
+        }
+        SA[r * LDA + i] = __dadd_rn(SA[r * LDA + i], q);
       }
       __syncthreads();
     }
     for (int idx = tid; idx < nsegs * P.nx; idx += kThreads) {
       const int s = idx / P.nx, i = idx - s * P.nx;
-      const int lo = sm.lo[s];
-      P.XIQG[(size_t)sm.edge[lo] * P.NXP + i] = sm.A[lo * P.LDA + i];
+      const int lo = slo[s];
+      P.XIQG[(size_t)edge[lo] * P.NXP + i] = SA[lo * LDA + i];
     }
   }
   __syncthreads();
+  TSMPC_MARK(P, 1, tm_);
 
-  // (3) GEMM 1: h = [xiq | psi^] [Bbar ; L]
-  gemm_dispatch((nrows + 7) >> 3, sm.A, P.LDA, P.KS1, P.NT1, P.W1f, sm.B, P.LDB);
+  // (3) GEMM 1: h = [xiq | psi^] [Bbar ; L] + beta
+  gemm_dispatch(P, (nrows + 7) >> 3, 0, LDA, P.KS1, P.NT1, P.W1f, kTileM * LDA, LDB, nrows);
   __syncthreads();
+  TSMPC_MARK(P, 2, tm_);
 
-  // (4) g scan, tail -> head: g_e = (beta_e + sum_children g_c) + h_e ; t_e = g_e / (2 p_e)
+  // (4) g scan, tail -> head: g_e = (beta_e + h_e) + sum_children g_c ; t_e = g_e / (2 p_e)
   for (int idx = tid; idx < nsegs * P.nv; idx += kThreads) {
     const int s = idx / P.nv, j = idx - s * P.nv;
-    const int lo = sm.lo[s], hi = sm.hi[s];
-    const int tail_node = sm.edge[hi - 1] + 1;
-    const int c0 = P.child_start[tail_node] - 1, c1 = P.child_stop[tail_node] - 1;
-    double acc = 0.0;
-    for (int ch = c0; ch < c1; ++ch) acc = __dadd_rn(acc, P.GG[(size_t)ch * P.NVP + j]);
-    double g = 0.0;
+    const int lo = slo[s], hi = shi[s];
+    double g = child_sum(P, P.GG, P.NVP, edge[hi - 1] + 1, j);
     for (int r = hi - 1; r >= lo; --r) {
-      const int e = sm.edge[r];
-      g = __dadd_rn(__dadd_rn(P.beta[(size_t)e * P.NVP + j], acc), sm.B[r * P.LDB + j]);
-      acc = g;
+      const int e = edge[r];
+      g = __dadd_rn(SB[r * LDB + j], g);
       P.T[(size_t)e * P.NVP + j] = __dmul_rn(g, P.inv2p[e]);
     }
-    P.GG[(size_t)sm.edge[lo] * P.NVP + j] = g;
+    P.GG[(size_t)edge[lo] * P.NVP + j] = g;
   }
+  TSMPC_MARK(P, 3, tm_);
 }
 
 // ---------------------------------------------------------------------------
 // forward sweep of one tile (+ prox / dual update epilogue in APG mode)
 // ---------------------------------------------------------------------------
-__device__ void fwd_tile(const Params& P, int tile, int nu, const Smem& sm) {
+__device__ __noinline__ void fwd_tile(const Params& P, int tile, int nu) {
   int nrows, nsegs;
-  load_tile(P, tile, sm, nrows, nsegs);
-  const int tid = threadIdx.x;
+  load_tile(P, tile, nrows, nsegs);
+  long long tm_ = clock64();
+  (void)tm_;
+  const int LDA = P.LDA2, LDB = P.LDB2;
+  double* const SA = g_smem;
+  double* const SB = g_smem + kTileM * LDA;
+  const int* const edge = SM_EDGE(P);
+  const int* const slo = SM_LO(P);
+  const int* const shi = SM_HI(P);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int K2 = P.KS2 * 4;
-  const bool apg = P.mode == kModeApg;
-  const bool last = (nu == P.iters - 1) || !apg;
 
-  // (1) S scan, head -> tail: S_e = t_e + S_parent
-  for (int idx = tid; idx < nsegs * K2; idx += kThreads) {
-    const int s = idx / K2, j = idx - s * K2;
-    const int lo = sm.lo[s], hi = sm.hi[s];
-    if (j >= P.nv) {
-      for (int r = lo; r < hi; ++r) sm.A[r * P.LDA + j] = 0.0;
-      continue;
+  // (1a) stage t rows (zero-padded to K2 columns) and GEMM 2's bias [uhat | e]
+  for (int r = warp; r < nrows; r += kWarps) {
+    const int e = edge[r];
+    const double* tr = P.T + (size_t)e * P.NVP;
+    double v[kChunks], uh[kChunks], ev[kChunks];
+#pragma unroll
+    for (int q = 0; q < kChunks; ++q) {
+      const int j = lane + 32 * q;
+      v[q] = j < P.nv ? tr[j] : 0.0;
+      uh[q] = (P.uhat && j < P.nu) ? P.uhat[(size_t)e * P.NUP + j] : 0.0;
+      ev[q] = (P.evec && j < P.nx) ? P.evec[(size_t)e * P.NXP + j] : 0.0;
     }
-    const int head = sm.edge[lo];
-    const int pa = P.anc[head + 1] - 1;
-    double S = (pa >= 0) ? P.T[(size_t)pa * P.NVP + j] : 0.0;
-    for (int r = lo; r < hi; ++r) {
-      S = __dadd_rn(P.T[(size_t)sm.edge[r] * P.NVP + j], S);
-      sm.A[r * P.LDA + j] = S;
+#pragma unroll
+    for (int q = 0; q < kChunks; ++q) {
+      const int j = lane + 32 * q;
+      if (j < K2) SA[r * LDA + j] = v[q];
+      if (j < P.NU8) SB[r * LDB + j] = uh[q];
+      if (j < LDB - P.NU8) SB[r * LDB + P.NU8 + j] = ev[q];
     }
-    P.T[(size_t)sm.edge[hi - 1] * P.NVP + j] = S;  // the children's heads read it
   }
   __syncthreads();
-
-  // (2) GEMM 2: [du | bv] = S [Psi | Phi]
-  gemm_dispatch((nrows + 7) >> 3, sm.A, P.LDA, P.KS2, P.NT2, P.W2f, sm.B, P.LDB);
+  TSMPC_MARK(P, 4, tm_);
+  // (1b) S scan, head -> tail: S_e = t_e + S_parent  (in shared memory)
+  for (int idx = tid; idx < nsegs * P.nv; idx += kThreads) {
+    const int s = idx / P.nv, j = idx - s * P.nv;
+    const int lo = slo[s], hi = shi[s];
+    const int pa = P.anc[edge[lo] + 1] - 1;
+    double S = head_parent_S(P, pa, j);
+    for (int r = lo; r < hi; ++r) {
+      S = __dadd_rn(SA[r * LDA + j], S);
+      SA[r * LDA + j] = S;
+    }
+    if (!P.collapsed) P.T[(size_t)edge[hi - 1] * P.NVP + j] = S;  // the children's heads read it
+  }
   __syncthreads();
+  TSMPC_MARK(P, 5, tm_);
 
-  // (3) x scan, head -> tail: x = A x_anc + bv + e   (x kept in sm.A)
+  // (2) GEMM 2: [u | bv + e] = S [Psi | Phi] + [uhat | e]
+  gemm_dispatch(P, (nrows + 7) >> 3, 0, LDA, P.KS2, P.NT2, P.W2f, kTileM * LDA, LDB, nrows);
+  __syncthreads();
+  TSMPC_MARK(P, 6, tm_);
+
+  // (3) x scan, head -> tail: x = A x_anc + (bv + e)   (x kept in the A region)
   if (P.diagA) {
     for (int idx = tid; idx < nsegs * P.nx; idx += kThreads) {
       const int s = idx / P.nx, i = idx - s * P.nx;
-      const int lo = sm.lo[s], hi = sm.hi[s];
-      const int an = P.anc[sm.edge[lo] + 1];
-      double xa = P.X[(size_t)an * P.NXP + i];
+      const int lo = slo[s], hi = shi[s];
+      const int an = P.anc[edge[lo] + 1];
+      double xa = P.collapsed ? (an == 0 ? P.p[i] : trunk_x(P, P.trunk_pos[an - 1], i))
+                              : P.X[(size_t)an * P.NXP + i];
       const double a = P.a_diag[i];
       for (int r = lo; r < hi; ++r) {
-        const int e = sm.edge[r];
-        const double ev = P.evec ? P.evec[(size_t)e * P.NXP + i] : 0.0;
-        const double x = __dadd_rn(__dadd_rn(__dmul_rn(xa, a), sm.B[r * P.LDB + P.NU8 + i]), ev);
-        sm.A[r * P.LDA + i] = x;
-        if (last) P.X[(size_t)(e + 1) * P.NXP + i] = x;
-        xa = x;
+        xa = __dadd_rn(__dmul_rn(xa, a), SB[r * LDB + P.NU8 + i]);
+        SA[r * LDA + i] = xa;
       }
-      if (!last) P.X[(size_t)(sm.edge[hi - 1] + 1) * P.NXP + i] = xa;
+      if (!P.collapsed) P.X[(size_t)(edge[hi - 1] + 1) * P.NXP + i] = xa;
     }
   } else {
-    const int maxlen = sm.misc[0];
+    const int maxlen = SM_MISC(P)[0];
     for (int d = 0; d < maxlen; ++d) {
       for (int idx = tid; idx < nsegs * P.nx; idx += kThreads) {
         const int s = idx / P.nx, i = idx - s * P.nx;
-        const int lo = sm.lo[s], hi = sm.hi[s];
+        const int lo = slo[s], hi = shi[s];
         const int r = lo + d;
         if (r >= hi) continue;
-        const int e = sm.edge[r];
-        const double* prev = (d == 0) ? (P.X + (size_t)P.anc[e + 1] * P.NXP) : (sm.A + (r - 1) * P.LDA);
+        const int e = edge[r];
+        const double* prev = (d == 0) ? (P.X + (size_t)P.anc[e + 1] * P.NXP) : (SA + (r - 1) * LDA);
         double q = 0.0;
         for (int j = 0; j < P.nx; ++j) q = fma(P.A[(size_t)i * P.nx + j], prev[j], q);
-        const double ev = P.evec ? P.evec[(size_t)e * P.NXP + i] : 0.0;
-        sm.A[r * P.LDA + i] = __dadd_rn(__dadd_rn(q, sm.B[r * P.LDB + P.NU8 + i]), ev);
+        SA[r * LDA + i] = __dadd_rn(q, SB[r * LDB + P.NU8 + i]);
       }
       __syncthreads();
     }
     for (int idx = tid; idx < nsegs * P.nx; idx += kThreads) {
       const int s = idx / P.nx, i = idx - s * P.nx;
-      const int lo = sm.lo[s], hi = sm.hi[s];
-      for (int r = lo; r < hi; ++r) {
-        if (last || r == hi - 1) P.X[(size_t)(sm.edge[r] + 1) * P.NXP + i] = sm.A[r * P.LDA + i];
-      }
+      const int hi = shi[s];
+      P.X[(size_t)(edge[hi - 1] + 1) * P.NXP + i] = SA[(hi - 1) * LDA + i];
     }
   }
   __syncthreads();
+  TSMPC_MARK(P, 7, tm_);
+  rows_epilogue(P, nu, nrows);
+  TSMPC_MARK(P, 8, tm_);
+}
 
-  // (4) per-row epilogue: one warp per edge row
-  const int warp = tid >> 5, lane = tid & 31;
+// Per-row epilogue of the forward sweep, one warp per edge row: x in the A
+// region rows, u in the C region rows (forward layout), edge ids in SM_EDGE.
+// APG mode: prox_g, dual update, ergodic averages, residual (engine.py:546-575);
+// STEP mode: store x, u.
+__device__ __noinline__ void rows_epilogue(const Params& P, int nu, int nrows) {
+  const int LDA = P.LDA2, LDB = P.LDB2;
+  const double* const SA = g_smem;
+  const double* const SB = g_smem + kTileM * LDA;
+  const int* const edge = SM_EDGE(P);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool apg = P.mode == kModeApg;
+  const bool last = (nu == P.iters - 1) || !apg;
   if (!apg) {
-    for (int idx = tid; idx < nrows * P.nu; idx += kThreads) {
-      const int r = idx / P.nu, j = idx - r * P.nu;
-      const int e = sm.edge[r];
-      const double uh = P.uhat ? P.uhat[(size_t)e * P.NUP + j] : 0.0;
-      P.U[(size_t)e * P.NUP + j] = __dadd_rn(sm.B[r * P.LDB + j], uh);
+    for (int r = warp; r < nrows; r += kWarps) {
+      const int e = edge[r];
+      for (int j = lane; j < P.nu; j += 32) P.U[(size_t)e * P.NUP + j] = SB[r * LDB + j];
+      for (int i = lane; i < P.nx; i += 32) P.X[(size_t)(e + 1) * P.NXP + i] = SA[r * LDA + i];
     }
     return;
   }
   const int E = P.n_edges;
   const int cur = (P.slot0 + nu) & 1;
-  const double* Y = P.ybuf[cur];
+  const double* __restrict__ Y = P.ybuf[cur];
   double* Yn = P.ybuf[cur ^ 1];  // y_prev slot receives y_next
   const double c = P.coef[nu];
   const double th = P.theta[nu];
@@ -323,25 +446,38 @@ __device__ void fwd_tile(const Params& P, int tile, int nu, const Smem& sm) {
   const double lam = P.lam;
   const double lam_p = 1.0 / lam;  // prox parameter (engine.py:555)
   const size_t zoff = (size_t)E * P.NXP, poff = 2 * (size_t)E * P.NXP;
+  const bool want_resid = last || P.record_all;
   double rmax = 0.0;
   for (int r = warp; r < nrows; r += kWarps) {
-    const int e = sm.edge[r];
+    const int e = edge[r];
     const int node = e + 1;
     const int st = P.edge_stage[e];
     const double ds = stage_scale(P.sig_stage, st, P.scaled);
     const double dz = stage_scale(P.zeta_stage, st, P.scaled);
+    const size_t ox = (size_t)e * P.NXP, oa = (size_t)node * P.NXP, ou = (size_t)e * P.NUP;
+    // issue every global read of the state-copy part first
+    double ys[kChunks], yps[kChunks], yz[kChunks], ypz[kChunks], xa[kChunks];
+#pragma unroll
+    for (int q = 0; q < kChunks; ++q) {
+      const int i = lane + 32 * q;
+      const bool okx = i < P.nx;
+      ys[q] = okx ? Y[ox + i] : 0.0;
+      yps[q] = okx ? Yn[ox + i] : 0.0;
+      yz[q] = okx ? Y[zoff + ox + i] : 0.0;
+      ypz[q] = okx ? Yn[zoff + ox + i] : 0.0;
+      xa[q] = okx ? P.xavg[oa + i] : 0.0;
+    }
     // --- state copies: two weighted-distance prox blocks (engine.py:146-180)
-    double xs[4], ws[4], wz[4], ts[4], tz[4];
+    double xs[kChunks], ws[kChunks], wz[kChunks], ts[kChunks], tz[kChunks];
     double ss = 0.0, sz = 0.0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < kChunks; ++q) {
       const int i = lane + 32 * q;
       if (i < P.nx) {
-        const size_t o = (size_t)e * P.NXP + i;
-        const double x = sm.A[r * P.LDA + i];
+        const double x = SA[r * LDA + i];
         xs[q] = x;
-        ws[q] = extrap(Y[o], Yn[o], c);
-        wz[q] = extrap(Y[zoff + o], Yn[zoff + o], c);
+        ws[q] = extrap(ys[q], yps[q], c);
+        wz[q] = extrap(yz[q], ypz[q], c);
         // t_arg = w / lam + D Hz   (engine.py:552-554)
         ts[q] = __dadd_rn(__ddiv_rn(ws[q], lam), __dmul_rn(x, ds));
         tz[q] = __dadd_rn(__ddiv_rn(wz[q], lam), __dmul_rn(x, dz));
@@ -363,44 +499,53 @@ __device__ void fwd_tile(const Params& P, int tile, int nu, const Smem& sm) {
     const double fs = dist_s > wgt_s ? __ddiv_rn(wgt_s, dist_s) : 1.0;
     const double fz = dist_z > wgt_z ? __ddiv_rn(wgt_z, dist_z) : 1.0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < kChunks; ++q) {
       const int i = lane + 32 * q;
       if (i < P.nx) {
-        const size_t o = (size_t)e * P.NXP + i;
         const double x = xs[q];
         const double hs = __dmul_rn(x, ds), hz = __dmul_rn(x, dz);
         const double ps = fmax(ts[q], __dmul_rn(ds, P.x_s[i]));
         const double pz = fmin(fmax(tz[q], __dmul_rn(dz, P.x_min[i])), __dmul_rn(dz, P.x_max[i]));
         const double t_s = __dadd_rn(ts[q], __dmul_rn(fs, __dsub_rn(ps, ts[q])));
         const double t_z = __dadd_rn(tz[q], __dmul_rn(fz, __dsub_rn(pz, tz[q])));
-        Yn[o] = __dadd_rn(ws[q], __dmul_rn(lam, __dsub_rn(hs, t_s)));
-        Yn[zoff + o] = __dadd_rn(wz[q], __dmul_rn(lam, __dsub_rn(hz, t_z)));
-        if (last || P.record_all) {
+        Yn[ox + i] = __dadd_rn(ws[q], __dmul_rn(lam, __dsub_rn(hs, t_s)));
+        Yn[zoff + ox + i] = __dadd_rn(wz[q], __dmul_rn(lam, __dsub_rn(hz, t_z)));
+        if (want_resid) {
           rmax = fmax(rmax, fabs(__dsub_rn(x, __ddiv_rn(t_s, ds))));
           rmax = fmax(rmax, fabs(__dsub_rn(x, __ddiv_rn(t_z, dz))));
         }
-        const size_t oa = (size_t)node * P.NXP + i;
-        P.xavg[oa] = __dadd_rn(__dmul_rn(P.xavg[oa], om), __dmul_rn(th, x));
+        P.xavg[oa + i] = __dadd_rn(__dmul_rn(xa[q], om), __dmul_rn(th, x));
+        if (last) P.X[oa + i] = x;
       }
     }
     // --- input copy: box projection (engine.py:182)
-    for (int j = lane; j < P.nu; j += 32) {
-      const size_t o = poff + (size_t)e * P.NUP + j;
-      const size_t ou = (size_t)e * P.NUP + j;
-      const double uh = P.uhat ? P.uhat[ou] : 0.0;
-      const double u = __dadd_rn(sm.B[r * P.LDB + j], uh);
-      const double dp = P.scaled ? P.psi_stage[(size_t)st * P.NUP + j] : 1.0;
-      const double w = extrap(Y[o], Yn[o], c);
-      const double hp = __dmul_rn(u, dp);
-      const double a = __dadd_rn(__ddiv_rn(w, lam), hp);
-      const double t = fmin(fmax(a, __dmul_rn(dp, P.u_min[j])), __dmul_rn(dp, P.u_max[j]));
-      Yn[o] = __dadd_rn(w, __dmul_rn(lam, __dsub_rn(hp, t)));
-      if (last || P.record_all) rmax = fmax(rmax, fabs(__dsub_rn(u, __ddiv_rn(t, dp))));
-      P.uavg[ou] = __dadd_rn(__dmul_rn(P.uavg[ou], om), __dmul_rn(th, u));
-      if (last) P.U[ou] = u;
+    double yp[kChunks], ypp[kChunks], ua[kChunks];
+#pragma unroll
+    for (int q = 0; q < kChunks; ++q) {
+      const int j = lane + 32 * q;
+      const bool oku = j < P.nu;
+      yp[q] = oku ? Y[poff + ou + j] : 0.0;
+      ypp[q] = oku ? Yn[poff + ou + j] : 0.0;
+      ua[q] = oku ? P.uavg[ou + j] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < kChunks; ++q) {
+      const int j = lane + 32 * q;
+      if (j < P.nu) {
+        const double u = SB[r * LDB + j];
+        const double dp = P.scaled ? P.psi_stage[(size_t)st * P.NUP + j] : 1.0;
+        const double w = extrap(yp[q], ypp[q], c);
+        const double hp = __dmul_rn(u, dp);
+        const double a = __dadd_rn(__ddiv_rn(w, lam), hp);
+        const double t = fmin(fmax(a, __dmul_rn(dp, P.u_min[j])), __dmul_rn(dp, P.u_max[j]));
+        Yn[poff + ou + j] = __dadd_rn(w, __dmul_rn(lam, __dsub_rn(hp, t)));
+        if (want_resid) rmax = fmax(rmax, fabs(__dsub_rn(u, __ddiv_rn(t, dp))));
+        P.uavg[ou + j] = __dadd_rn(__dmul_rn(ua[q], om), __dmul_rn(th, u));
+        if (last) P.U[ou + j] = u;
+      }
     }
   }
-  if (last || P.record_all) {
+  if (want_resid) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, off));
     if (lane == 0 && rmax > 0.0)
@@ -408,23 +553,246 @@ __device__ void fwd_tile(const Params& P, int tile, int nu, const Smem& sm) {
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) apg_persistent_kernel(Params P) {
-  extern __shared__ __align__(16) double smem[];
-  Smem sm;
-  sm.A = smem;
-  sm.B = sm.A + kTileM * P.LDA;
-  sm.edge = reinterpret_cast<int*>(sm.B + kTileM * P.LDB);
-  sm.lo = sm.edge + kTileM;
-  sm.hi = sm.lo + kTileM;
-  sm.misc = sm.hi + kTileM;
+// ---------------------------------------------------------------------------
+// collapsed trunk (diagonal A).  With g_a = sum over the trunk subtree of a of
+// (beta_k + [xiq_k | psi^_k] W1) plus the chain-head sums G_c below it, linearity
+// gives, per trunk edge a (b runs over the trunk path root .. a):
+//   K_a = sum_b inv2p_b (sum_{k in sub(b)} beta_k + sum_{heads c in sub(b)} G_c)
+//   Y_a = sum_b inv2p_b  sum_{k in sub(b)} [xiq_k | psi^_k]
+//   S_a = K_a + Y_a W1,   [u_a - uhat_a | bv_a] = S_a W2 = K_a W2 + Y_a (W1 W2)
+// The first two are per-component tree recursions (one CTA per component slice,
+// no cross-component coupling because A is diagonal); the last is one GEMM of the
+// T trunk rows against the fused [[I, W2], [W1, W1 W2]] operator.
+// ---------------------------------------------------------------------------
+
+// v + sum over the children ch of trunk row tp: trunk children contribute
+// KY[child][col], chain-head children hb[ch][hcol] (skipped when hb is null).
+// Children of a node are contiguous edges, hence contiguous trunk positions.
+__device__ __forceinline__ double child_acc(const Params& P, int tp, int ch0, int ch1, int col,
+                                            const double* hb, int hld, int hcol, double v) {
+  const int tc = P.trunk_child0[tp];
+  const int n = ch1 - ch0;
+  if (tc >= 0) {
+#pragma unroll 4
+    for (int k = 0; k < n; ++k) v = __dadd_rn(v, P.KY[(size_t)(tc + k) * P.KY_LD + col]);
+  } else if (tc == -1) {
+    if (hb) {
+#pragma unroll 4
+      for (int ch = ch0; ch < ch1; ++ch) v = __dadd_rn(v, hb[(size_t)ch * hld + hcol]);
+    }
+  } else {
+    for (int ch = ch0; ch < ch1; ++ch) {
+      const int cp = P.trunk_pos[ch];
+      if (cp >= 0) v = __dadd_rn(v, P.KY[(size_t)cp * P.KY_LD + col]);
+      else if (hb) v = __dadd_rn(v, hb[(size_t)ch * hld + hcol]);
+    }
+  }
+  return v;
+}
+
+// Phase B: component-sliced trunk recursion -> KY = [K | Yx | Ypsi] (and XIQG for
+// trunk edges).
+__device__ __noinline__ void trunk_sweep(const Params& P, int nu) {
+  const int ncomp = P.nv + P.nx + P.nu;
+  const int c_lo = (int)((long long)ncomp * blockIdx.x / gridDim.x);
+  const int c_hi = (int)((long long)ncomp * (blockIdx.x + 1) / gridDim.x);
+  const int nc = c_hi - c_lo;
+  if (nc <= 0) return;
+  const int E = P.n_edges;
+  const bool apg = P.mode == kModeApg;
+  const int cur = (P.slot0 + nu) & 1;
+  const double* __restrict__ Y = P.ybuf[cur];
+  const double* __restrict__ Yp = P.ybuf[cur ^ 1];
+  const double c = apg ? P.coef[nu] : 0.0;
+  const size_t zoff = (size_t)E * P.NXP, poff = 2 * zoff;
+  // bottom-up over edge stages (children live in later stages)
+  for (int st = P.N - 1; st >= 0; --st) {
+    const int t0 = P.trunk_stage_ptr[st], t1 = P.trunk_stage_ptr[st + 1];
+    if (t0 == t1) continue;  // block-uniform
+    for (int idx = threadIdx.x; idx < (t1 - t0) * nc; idx += kThreads) {
+      const int tp = t0 + idx / nc, q = c_lo + idx % nc;
+      const int a = P.trunk_edge[tp];
+      const int node = a + 1;
+      const int ch0 = P.child_start[node] - 1, ch1 = P.child_stop[node] - 1;
+      double* ky = P.KY + (size_t)tp * P.KY_LD;
+      if (q < P.nv) {  // K part: beta sums (+ chain heads' G)
+        const int j = q;
+        ky[j] = child_acc(P, tp, ch0, ch1, j, P.GG, P.NVP, j, P.beta[(size_t)a * P.NVP + j]);
+      } else if (q < P.nv + P.nx) {  // xiq and its subtree sum
+        const int i = q - P.nv;
+        const int es = P.edge_stage[a];
+        const size_t o = (size_t)a * P.NXP + i;
+        const double ws = apg ? extrap(Y[o], Yp[o], c) : Y[o];
+        const double wz = apg ? extrap(Y[zoff + o], Yp[zoff + o], c) : Y[zoff + o];
+        const double s = __dadd_rn(__dmul_rn(ws, stage_scale(P.sig_stage, es, P.scaled)),
+                                   __dmul_rn(wz, stage_scale(P.zeta_stage, es, P.scaled)));
+        double xs = 0.0;
+#pragma unroll 4
+        for (int ch = ch0; ch < ch1; ++ch) xs = __dadd_rn(xs, P.XIQG[(size_t)ch * P.NXP + i]);
+        const double zs = child_acc(P, tp, ch0, ch1, P.NVP + i, nullptr, 0, 0, 0.0);
+        const double xiq = __dadd_rn(s, __dmul_rn(xs, P.a_diag[i]));
+        P.XIQG[o] = xiq;
+        ky[P.NVP + i] = __dadd_rn(xiq, zs);
+      } else {  // psi^ subtree sum
+        const int j = q - P.nv - P.nx;
+        const int es = P.edge_stage[a];
+        const size_t o = poff + (size_t)a * P.NUP + j;
+        const double wp = apg ? extrap(Y[o], Yp[o], c) : Y[o];
+        const double v = P.scaled ? __dmul_rn(wp, P.psi_stage[(size_t)es * P.NUP + j]) : wp;
+        ky[P.NVP + P.NXP + j] = child_acc(P, tp, ch0, ch1, P.NVP + P.NXP + j, nullptr, 0, 0, v);
+      }
+    }
+    __syncthreads();
+  }
+  // top-down: K_a, Y_a = own * inv2p_a + parent's
+  for (int st = 0; st < P.N; ++st) {
+    const int t0 = P.trunk_stage_ptr[st], t1 = P.trunk_stage_ptr[st + 1];
+    if (t0 == t1) continue;
+    for (int idx = threadIdx.x; idx < (t1 - t0) * nc; idx += kThreads) {
+      const int tp = t0 + idx / nc, q = c_lo + idx % nc;
+      const int a = P.trunk_edge[tp];
+      const int col = q < P.nv ? q : (q < P.nv + P.nx ? P.NVP + (q - P.nv) : P.NVP + P.NXP + (q - P.nv - P.nx));
+      const int pa = P.anc[a + 1] - 1;
+      double v = __dmul_rn(P.KY[(size_t)tp * P.KY_LD + col], P.inv2p[a]);
+      if (pa >= 0) v = __dadd_rn(v, P.KY[(size_t)P.trunk_pos[pa] * P.KY_LD + col]);
+      P.KY[(size_t)tp * P.KY_LD + col] = v;
+    }
+    __syncthreads();
+  }
+}
+
+// Phase C: OUT = KY * MT + [0 | uhat | e] for all trunk rows.  Work item = (n-tile,
+// block of 4 m-tiles); the 13 warps of a CTA split the k-steps and reduce their
+// partial tiles through shared memory in a fixed order (deterministic).
+__device__ __noinline__ void trunk_gemm(const Params& P) {
+  const int T = P.n_trunk;
+  constexpr int MTB = 4;
+  const int mblocks = (T + 8 * MTB - 1) / (8 * MTB);
+  const int items = P.NTT * mblocks;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ar = lane >> 2, ac = lane & 3;
+  double* const red = g_smem;  // [kWarps][MTB][32][2]
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    const int nt = it % P.NTT, mb = it / P.NTT;
+    const int k0 = (int)((long long)P.KSK * warp / kWarps), k1 = (int)((long long)P.KSK * (warp + 1) / kWarps);
+    double acc[MTB][2];
+#pragma unroll
+    for (int m = 0; m < MTB; ++m) acc[m][0] = acc[m][1] = 0.0;
+    const double* bp = P.MTf + (size_t)nt * P.KSK * 32 + lane;
+#pragma unroll 2
+    for (int ks = k0; ks < k1; ++ks) {
+      const double b = __ldg(bp + (size_t)ks * 32);
+#pragma unroll
+      for (int m = 0; m < MTB; ++m) {
+        const int row = (mb * MTB + m) * 8 + ar;
+        const double a = row < T ? P.KY[(size_t)row * P.KY_LD + ks * 4 + ac] : 0.0;
+        dmma8x8x4(acc[m], a, b);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < MTB; ++m) {
+      red[((warp * MTB + m) * 32 + lane) * 2] = acc[m][0];
+      red[((warp * MTB + m) * 32 + lane) * 2 + 1] = acc[m][1];
+    }
+    __syncthreads();
+    if (warp < MTB) {
+      const int m = warp;
+      double v0 = 0.0, v1 = 0.0;
+      for (int w = 0; w < kWarps; ++w) {
+        v0 = __dadd_rn(v0, red[((w * MTB + m) * 32 + lane) * 2]);
+        v1 = __dadd_rn(v1, red[((w * MTB + m) * 32 + lane) * 2 + 1]);
+      }
+      const int row = (mb * MTB + m) * 8 + ar;
+      if (row < T) {
+        const int e = P.trunk_edge[row];
+        const int col = nt * 8 + 2 * ac;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int cc = col + h;
+          double bias = 0.0;
+          if (cc >= P.U_OFF && cc < P.U_OFF + P.nu && P.uhat) bias = P.uhat[(size_t)e * P.NUP + cc - P.U_OFF];
+          if (cc >= P.X_OFF && cc < P.X_OFF + P.nx && P.evec) bias = P.evec[(size_t)e * P.NXP + cc - P.X_OFF];
+          P.OUT[(size_t)row * P.OUT_LD + cc] = __dadd_rn(h ? v1 : v0, bias);
+        }
+      }
+    }
+  }
+}
+
+// Phase D (trunk part): x by the trunk path recursion, u from OUT, then the
+// standard row epilogue, for the trunk rows owned by this CTA.
+__device__ __noinline__ void trunk_rows(const Params& P, int nu) {
+  const int T = P.n_trunk;
+  const int LDA = P.LDA2, LDB = P.LDB2;
+  double* const SA = g_smem;
+  double* const SB = g_smem + kTileM * LDA;
+  int* const edge = SM_EDGE(P);
+  // trunk row tp goes to CTA C-1-(tp mod C): round-robin from the last CTA, which
+  // the balanced chain assignment leaves with the fewest chain rows
+  const int C = gridDim.x;
+  const int first = C - 1 - (int)blockIdx.x;
+  const int mine = first < T ? (T - 1 - first) / C + 1 : 0;
+  for (int k0 = 0; k0 < mine; k0 += kTileM) {
+    const int nrows = min(kTileM, mine - k0);
+    __syncthreads();
+    for (int r = threadIdx.x; r < nrows; r += kThreads) edge[r] = P.trunk_edge[first + (k0 + r) * C];
+    for (int idx = threadIdx.x; idx < nrows * P.nx; idx += kThreads) {
+      const int r = idx / P.nx, i = idx - r * P.nx;
+      SA[r * LDA + i] = trunk_x(P, first + (k0 + r) * C, i);
+    }
+    for (int idx = threadIdx.x; idx < nrows * P.nu; idx += kThreads) {
+      const int r = idx / P.nu, j = idx - r * P.nu;
+      SB[r * LDB + j] = P.OUT[(size_t)(first + (k0 + r) * C) * P.OUT_LD + P.U_OFF + j];
+    }
+    __syncthreads();
+    rows_epilogue(P, nu, nrows);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) apg_persistent_kernel(const __grid_constant__ Params P) {
   cg::grid_group grid = cg::this_grid();
   const int cta = blockIdx.x;
   const int D = P.n_levels;
+  if (P.collapsed) {
+    // leaf segments = level-0 tiles; trunk collapsed: 3 grid barriers / iteration
+    const int* lt = P.lvl_tiles + cta;
+    const bool trunk = P.n_trunk > 0;
+    for (int nu = 0; nu < P.iters; ++nu) {
+      for (int t = lt[0]; t < lt[1]; ++t) bwd_tile(P, t, nu);
+      if (trunk) {
+        long long tb_ = clock64();
+        grid.sync();
+        TSMPC_MARK(P, 9, tb_);
+        trunk_sweep(P, nu);
+        TSMPC_MARK(P, 10, tb_);
+        grid.sync();
+        TSMPC_MARK(P, 9, tb_);
+        trunk_gemm(P);
+        TSMPC_MARK(P, 11, tb_);
+        grid.sync();
+        TSMPC_MARK(P, 9, tb_);
+      }
+      if (P.mode == kModeApg && cta == 0) {
+        const double th = P.theta[nu];
+        const double om = __dsub_rn(1.0, th);
+        for (int i = threadIdx.x; i < P.nx; i += kThreads)
+          P.xavg[i] = __dadd_rn(__dmul_rn(P.xavg[i], om), __dmul_rn(th, P.p[i]));
+      }
+      if (trunk) {
+        long long tr_ = clock64();
+        trunk_rows(P, nu);
+        TSMPC_MARK(P, 12, tr_);
+      }
+      for (int t = lt[0]; t < lt[1]; ++t) fwd_tile(P, t, nu);
+    }
+    return;
+  }
   for (int nu = 0; nu < P.iters; ++nu) {
     for (int l = D - 1; l >= 0; --l) {
       const int* lt = P.lvl_tiles + l * P.n_ctas + cta;
-      for (int t = lt[0]; t < lt[1]; ++t) bwd_tile(P, t, nu, sm);
-      if (l > 0) grid.sync();
+      for (int t = lt[0]; t < lt[1]; ++t) bwd_tile(P, t, nu);
+      if (l > 0) { long long tb_ = clock64(); grid.sync(); TSMPC_MARK(P, 9, tb_); }
     }
     if (P.mode == kModeApg && cta == 0) {
       const double th = P.theta[nu];
@@ -434,14 +802,10 @@ __global__ void __launch_bounds__(kThreads, 1) apg_persistent_kernel(Params P) {
     }
     for (int l = 0; l < D; ++l) {
       const int* lt = P.lvl_tiles + l * P.n_ctas + cta;
-      for (int t = lt[0]; t < lt[1]; ++t) fwd_tile(P, t, nu, sm);
-      if (l < D - 1) grid.sync();
+      for (int t = lt[0]; t < lt[1]; ++t) fwd_tile(P, t, nu);
+      if (l < D - 1) { long long tb_ = clock64(); grid.sync(); TSMPC_MARK(P, 9, tb_); }
     }
   }
-}
-
-size_t smem_bytes(int LDA, int LDB) {
-  return sizeof(double) * (size_t)kTileM * (LDA + LDB) + sizeof(int) * (3 * kTileM + 4);
 }
 
 }  // namespace tsmpc

@@ -52,7 +52,6 @@ __global__ void gap_ub_kernel(EdgeCtx c, const double* uf, double* ub);
 __global__ void gap_propagate_stage_kernel(EdgeCtx c, int n0, int n1, double* xf, const double* ub);
 __global__ void gap_primal_terms_kernel(EdgeCtx c, const double* uf, const double* xf, double* cols);
 
-__global__ void apg_persistent_kernel(Params P);
-size_t smem_bytes(int LDA, int LDB);
+__global__ void apg_persistent_kernel(const __grid_constant__ Params P);
 
 }  // namespace tsmpc

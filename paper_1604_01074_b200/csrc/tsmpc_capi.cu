@@ -49,7 +49,8 @@ struct tsmpc_plan {
   Params base{};
   EdgeCtx ctx{};
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
+  long long launches = 0;  // kernels launched by the current API call
   std::vector<void*> allocs;
   std::vector<int64_t> stage_starts;
   bool has_cache = false;
@@ -64,10 +65,11 @@ struct tsmpc_plan {
   unsigned long long* RESID = nullptr;
   int resid_cap = 0;
   unsigned long long* DYK = nullptr;
+  unsigned long long* TIMERS = nullptr;
   // compact scaling copies for tsmpc_prox
   double *sig_c = nullptr, *zeta_c = nullptr, *psi_c = nullptr;
   // plan stats
-  int n_levels = 0, n_tiles = 0, n_segs = 0, n_ctas = 0;
+  int n_levels = 0, n_tiles = 0, n_segs = 0, n_ctas = 0, n_trunk = 0;
   int dyk_blocks = 0;
 
   template <class T>
@@ -108,6 +110,7 @@ struct tsmpc_plan {
     for (void* p : allocs) cudaFree(p);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    if (ev2) cudaEventDestroy(ev2);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -119,12 +122,15 @@ struct Decomposition {
   int n_levels = 0;
   std::vector<int> lvl_tiles, tile_seg, seg_row, row_edge;
   int n_ctas = 0;
+  // collapsed-trunk mode
+  bool collapsed = false;
+  std::vector<int> trunk_edge, trunk_stage_ptr, trunk_pos, path_ptr, path_list, trunk_child0;
 };
 
 // Cut the tree into segments (maximal only-child chains of <= kMaxSeg edges),
 // group them by segment depth, balance each level's rows over the CTAs and pack
 // every CTA's share into tiles of <= kTileM rows.
-int decompose(const tsmpc_problem* pb, int max_ctas, Decomposition& out) {
+int decompose(const tsmpc_problem* pb, int max_ctas, bool collapse, Decomposition& out) {
   const int n_nodes = pb->n_nodes, E = n_nodes - 1;
   std::vector<int> nch(n_nodes);
   for (int n = 0; n < n_nodes; ++n) nch[n] = (int)(pb->child_stop[n] - pb->child_start[n]);
@@ -170,9 +176,59 @@ int decompose(const tsmpc_problem* pb, int max_ctas, Decomposition& out) {
   }
   std::vector<std::vector<int>> by_level(D);
   for (int s : order) by_level[level[s]].push_back(s);
+  out.collapsed = collapse;
+  if (collapse) {
+    // leaf segments (tail is a leaf) form the single tile level; every other edge
+    // is a trunk edge handled by the collapsed sweep + GEMM
+    std::vector<int> leaf_segs;
+    std::vector<char> in_leaf(E, 0);
+    for (int s : order) {
+      if (nch[segs[s].back() + 1] == 0) {
+        leaf_segs.push_back(s);
+        for (int e : segs[s]) in_leaf[e] = 1;
+      }
+    }
+    out.trunk_pos.assign(E, -1);
+    out.trunk_edge.clear();
+    for (int e = 0; e < E; ++e)
+      if (!in_leaf[e]) {
+        out.trunk_pos[e] = (int)out.trunk_edge.size();
+        out.trunk_edge.push_back(e);
+      }
+    const int N = pb->N;
+    out.trunk_stage_ptr.assign(N + 1, 0);
+    {
+      int k = 0;
+      for (int st = 0; st < N; ++st) {
+        out.trunk_stage_ptr[st] = k;
+        const int e_end = (int)pb->stage_starts[st + 2] - 1;  // edges into stage st+1
+        while (k < (int)out.trunk_edge.size() && out.trunk_edge[k] < e_end) ++k;
+      }
+      out.trunk_stage_ptr[N] = k;
+    }
+    out.trunk_child0.assign(out.trunk_edge.size(), -1);
+    for (size_t t = 0; t < out.trunk_edge.size(); ++t) {
+      const int node = out.trunk_edge[t] + 1;
+      int n_tr = 0, n = 0;
+      for (int64_t ch = pb->child_start[node] - 1; ch < pb->child_stop[node] - 1; ++ch, ++n)
+        n_tr += out.trunk_pos[ch] >= 0;
+      out.trunk_child0[t] = n_tr == 0 ? -1 : (n_tr == n ? out.trunk_pos[pb->child_start[node] - 1] : -2);
+    }
+    out.path_ptr.assign(out.trunk_edge.size() + 1, 0);
+    out.path_list.clear();
+    for (size_t t = 0; t < out.trunk_edge.size(); ++t) {
+      std::vector<int> path;
+      for (int e = out.trunk_edge[t]; e >= 0; e = (int)pb->anc[e + 1] - 1) path.push_back(out.trunk_pos[e]);
+      for (auto it = path.rbegin(); it != path.rend(); ++it) out.path_list.push_back(*it);
+      out.path_ptr[t + 1] = (int)out.path_list.size();
+    }
+    by_level.assign(1, leaf_segs);
+    D = 1;
+  }
   size_t widest = 0;
   for (auto& v : by_level) widest = std::max(widest, v.size());
-  const int C = std::max(1, std::min<int>(max_ctas, (int)widest));
+  int C = std::max(1, std::min<int>(max_ctas, (int)widest));
+  if (collapse && !out.trunk_edge.empty()) C = std::max(1, max_ctas);
 
   out.n_levels = D;
   out.n_ctas = C;
@@ -220,6 +276,7 @@ int launch_apg(tsmpc_plan* pl, const Params& P) {
   void* args[] = {const_cast<Params*>(&P)};
   CU(cudaLaunchCooperativeKernel((void*)apg_persistent_kernel, dim3(pl->n_ctas), dim3(kThreads), args,
                                  pl->smem, pl->stream));
+  ++pl->launches;
   return TSMPC_OK;
 }
 
@@ -275,7 +332,8 @@ tsmpc_plan* tsmpc_plan_create(const tsmpc_problem* pb, int device) {
   pl->device = device;
   if (cudaSetDevice(device) != cudaSuccess) { fail(TSMPC_ERR_CUDA, "cudaSetDevice failed"); return bail(0); }
   if (cudaStreamCreateWithFlags(&pl->stream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaEventCreate(&pl->ev0) != cudaSuccess || cudaEventCreate(&pl->ev1) != cudaSuccess) {
+      cudaEventCreate(&pl->ev0) != cudaSuccess || cudaEventCreate(&pl->ev1) != cudaSuccess ||
+      cudaEventCreate(&pl->ev2) != cudaSuccess) {
     fail(TSMPC_ERR_CUDA, "stream/event creation failed");
     return bail(0);
   }
@@ -299,12 +357,18 @@ tsmpc_plan* tsmpc_plan_create(const tsmpc_problem* pb, int device) {
   P.KS2 = NVP / 4;
   P.NU8 = r8(nu);
   P.NT2 = (P.NU8 + r8(nx)) / 8;
-  int lda = std::max(std::max(K1, NVP), NXP);
-  while (lda % 16 != 4) ++lda;
-  P.LDA = lda;
-  P.LDB = std::max(P.NT1 * 8, P.NT2 * 8);
+  // shared-memory tile layout: A leading dims = 4 mod 16 doubles (conflict-free
+  // DMMA fragment loads); C holds h (backward) / [u | bv + e] (forward)
+  auto lda_of = [](int k) { while (k % 16 != 4) ++k; return k; };
+  P.LDA1 = lda_of(K1);
+  P.LDB1 = std::max(P.NT1 * 8, r8(nx));          // dense-A child sums reuse C
+  P.LDA2 = lda_of(std::max(NVP, NXP));           // S, then x
+  P.LDB2 = P.NT2 * 8;
+  // the trunk GEMM reduces kWarps x 4 m-tile partials through the tile region
+  const int region = std::max({kTileM * (P.LDA1 + P.LDB1), kTileM * (P.LDA2 + P.LDB2), kWarps * 4 * 64});
+  P.META_OFF = region;
   P.Wx = pb->Wx; P.gamma_d = pb->gamma_d;
-  pl->smem = smem_bytes(P.LDA, P.LDB);
+  pl->smem = sizeof(double) * (size_t)region + sizeof(int) * (3 * kTileM + 4);
   if (pl->smem > (size_t)prop.sharedMemPerBlockOptin) {
     fail(TSMPC_ERR_DIMENSION, "tile needs %zu bytes of shared memory (limit %zu)", pl->smem,
          (size_t)prop.sharedMemPerBlockOptin);
@@ -319,14 +383,24 @@ tsmpc_plan* tsmpc_plan_create(const tsmpc_problem* pb, int device) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, apg_persistent_kernel, kThreads, pl->smem);
   if (occ < 1) { fail(TSMPC_ERR_CUDA, "persistent kernel does not fit on an SM"); return bail(0); }
 
+  bool diag = true;
+  for (int i = 0; i < nx && diag; ++i)
+    for (int j = 0; j < nx; ++j)
+      if (i != j && pb->A[(size_t)i * nx + j] != 0.0) { diag = false; break; }
+  const char* env_mode = getenv("TSMPC_LEVEL_MODE");  // force the level-synchronous path
+  const bool collapse = diag && !(env_mode && env_mode[0] == '1');
+
   Decomposition dec;
-  if (decompose(pb, pl->sm_count * std::min(occ, 1), dec)) return bail(0);
+  if (decompose(pb, pl->sm_count * std::min(occ, 1), collapse, dec)) return bail(0);
   pl->n_levels = dec.n_levels;
   pl->n_ctas = dec.n_ctas;
   pl->n_tiles = (int)dec.tile_seg.size() - 1;
   pl->n_segs = (int)dec.seg_row.size() - 1;
+  pl->n_trunk = (int)dec.trunk_edge.size();
   P.n_levels = dec.n_levels;
   P.n_ctas = dec.n_ctas;
+  P.collapsed = dec.collapsed ? 1 : 0;
+  P.n_trunk = pl->n_trunk;
 
   // ---- operator blocks in DMMA fragment order
   std::vector<double> W1((size_t)K1 * P.NT1 * 8, 0.0), W2((size_t)P.KS2 * 4 * P.NT2 * 8, 0.0);
@@ -350,16 +424,52 @@ tsmpc_plan* tsmpc_plan_create(const tsmpc_problem* pb, int device) {
   };
   const auto W1f = frag(W1, P.KS1, P.NT1), W2f = frag(W2, P.KS2, P.NT2);
 
+  // ---- fused trunk operator MT = [[I, W2], [W1, W1 W2]] (rows [K | Yx | Ypsi],
+  //      columns [S | u | bv]) for the collapsed trunk GEMM
+  const int NTS = P.NT1;                 // S column tiles
+  P.KY_LD = NVP + NXP + NUP;
+  P.KSK = P.KY_LD / 4;
+  P.U_OFF = NTS * 8;
+  P.X_OFF = P.U_OFF + P.NU8;
+  P.OUT_LD = P.X_OFF + r8(nx);
+  P.NTT = P.OUT_LD / 8;
+  std::vector<double> MTf;
+  if (dec.collapsed && pl->n_trunk > 0) {
+    const int ld = P.OUT_LD;
+    std::vector<double> MT((size_t)P.KY_LD * ld, 0.0);
+    // W1 rows: r < nx -> Bbar[r], NXP + j -> L[j] (row index into the Y block)
+    auto w1 = [&](int yr, int v) -> double {
+      if (yr < NXP) return yr < nx ? pb->Bbar[(size_t)yr * nv + v] : 0.0;
+      const int j = yr - NXP;
+      return j < nu ? pb->L[(size_t)j * nv + v] : 0.0;
+    };
+    auto w2 = [&](int v, int col) -> double {  // col in [U_OFF, OUT_LD)
+      if (col < P.X_OFF) { const int j = col - P.U_OFF; return j < nu ? pb->Psi[(size_t)v * nu + j] : 0.0; }
+      const int i = col - P.X_OFF;
+      return i < nx ? pb->Phi[(size_t)v * nx + i] : 0.0;
+    };
+    for (int k = 0; k < nv; ++k) {           // K block: identity on S, W2 on [u | bv]
+      MT[(size_t)k * ld + k] = 1.0;
+      for (int col = P.U_OFF; col < ld; ++col) MT[(size_t)k * ld + col] = w2(k, col);
+    }
+    for (int yr = 0; yr < NXP + NUP; ++yr) {  // Y block: W1 on S, W1 W2 on [u | bv]
+      double* row = &MT[(size_t)(NVP + yr) * ld];
+      for (int v = 0; v < nv; ++v) row[v] = w1(yr, v);
+      for (int col = P.U_OFF; col < ld; ++col) {
+        double s = 0.0;
+        for (int v = 0; v < nv; ++v) s += w1(yr, v) * w2(v, col);
+        row[col] = s;
+      }
+    }
+    MTf = frag(MT, P.KSK, P.NTT);
+  }
+
   // ---- model vectors (padded)
   auto padv = [](const double* v, int n, int np) {
     std::vector<double> o(np, 0.0);
     std::copy(v, v + n, o.begin());
     return o;
   };
-  bool diag = true;
-  for (int i = 0; i < nx && diag; ++i)
-    for (int j = 0; j < nx; ++j)
-      if (i != j && pb->A[(size_t)i * nx + j] != 0.0) { diag = false; break; }
   std::vector<double> adiag(NXP, 0.0);
   for (int i = 0; i < nx; ++i) adiag[i] = pb->A[(size_t)i * nx + i];
   P.diagA = diag ? 1 : 0;
@@ -463,7 +573,27 @@ tsmpc_plan* tsmpc_plan_create(const tsmpc_problem* pb, int device) {
   rc |= pl->alloc(&pl->ROWS, (size_t)E * 6);
   rc |= pl->alloc(&pl->RED, 16);
   rc |= pl->alloc(&pl->DYK, 256);
+  rc |= pl->alloc(&pl->TIMERS, 16);
+  int *d_te = nullptr, *d_tsp = nullptr, *d_tpos = nullptr, *d_pp = nullptr, *d_pl = nullptr,
+      *d_tc0 = nullptr;
+  double *d_MTf = nullptr, *d_KY = nullptr, *d_OUT = nullptr;
+  if (dec.collapsed) {
+    const size_t T = std::max<size_t>(1, dec.trunk_edge.size());
+    rc |= pl->upload(&d_tpos, dec.trunk_pos.data(), dec.trunk_pos.size());
+    rc |= pl->upload(&d_tsp, dec.trunk_stage_ptr.data(), dec.trunk_stage_ptr.size());
+    if (!dec.trunk_edge.empty()) {
+      rc |= pl->upload(&d_te, dec.trunk_edge.data(), dec.trunk_edge.size());
+      rc |= pl->upload(&d_tc0, dec.trunk_child0.data(), dec.trunk_child0.size());
+      rc |= pl->upload(&d_pp, dec.path_ptr.data(), dec.path_ptr.size());
+      rc |= pl->upload(&d_pl, dec.path_list.data(), dec.path_list.size());
+      rc |= pl->upload(&d_MTf, MTf.data(), MTf.size());
+    }
+    rc |= pl->alloc(&d_KY, T * P.KY_LD);
+    rc |= pl->alloc(&d_OUT, T * P.OUT_LD);
+  }
   if (rc) return bail(0);
+  P.trunk_edge = d_te; P.trunk_stage_ptr = d_tsp; P.trunk_pos = d_tpos; P.trunk_child0 = d_tc0;
+  P.path_ptr = d_pp; P.path_list = d_pl; P.MTf = d_MTf; P.KY = d_KY; P.OUT = d_OUT;
 
   P.a_diag = d_adiag; P.A = d_A; P.W1f = d_W1f; P.W2f = d_W2f;
   P.x_s = d_xs; P.x_min = d_xmin; P.x_max = d_xmax; P.u_min = d_umin; P.u_max = d_umax;
@@ -472,6 +602,7 @@ tsmpc_plan* tsmpc_plan_create(const tsmpc_problem* pb, int device) {
   P.lvl_tiles = d_lt; P.tile_seg = d_ts; P.seg_row = d_sr; P.row_edge = d_re;
   P.xavg = pl->XAVG; P.uavg = pl->UAVG; P.X = pl->X; P.U = pl->U; P.T = pl->T;
   P.XIQG = pl->XIQG; P.GG = pl->GG; P.p = pl->P;
+  P.timers = pl->TIMERS;
 
   EdgeCtx& c = pl->ctx;
   c.nx = nx; c.nu = nu; c.ne = ne; c.E = E; c.NXP = NXP; c.NUP = NUP;
@@ -500,8 +631,18 @@ void tsmpc_plan_destroy(tsmpc_plan* plan) { delete plan; }
 int tsmpc_plan_info(const tsmpc_plan* pl, int64_t* info, int32_t n) {
   if (!pl || !info) return fail(TSMPC_ERR_ARGUMENT, "null argument");
   const int64_t vals[] = {pl->n_levels, pl->n_ctas, pl->n_tiles, pl->n_segs, (int64_t)pl->smem,
-                          pl->base.diagA, kThreads, kTileM, pl->sm_count};
+                          pl->base.diagA, kThreads, kTileM, pl->sm_count, pl->base.collapsed,
+                          pl->n_trunk};
   for (int i = 0; i < n && i < (int)(sizeof(vals) / sizeof(vals[0])); ++i) info[i] = vals[i];
+  return TSMPC_OK;
+}
+
+int tsmpc_debug_timers(tsmpc_plan* pl, uint64_t* out, int32_t n) {
+  if (!pl || !out) return fail(TSMPC_ERR_ARGUMENT, "null argument");
+  unsigned long long t[16];
+  CU(cudaMemcpy(t, pl->TIMERS, sizeof(t), cudaMemcpyDeviceToHost));
+  CU(cudaMemset(pl->TIMERS, 0, sizeof(t)));
+  for (int i = 0; i < n && i < 16; ++i) out[i] = t[i];
   return TSMPC_OK;
 }
 
@@ -560,6 +701,7 @@ static int compute_gap(tsmpc_plan* pl, const double* yfinal, double* gap) {
   CU(cudaMemsetAsync(pl->COLS, 0, sizeof(double) * (size_t)E * 10, pl->stream));
   gap_dual_project_kernel<<<G, 256, 0, pl->stream>>>(c, yfinal, pl->WB, pl->COLS);
   CU(cudaGetLastError());
+  pl->launches += 6 + pl->N;  // project, terms, projection, ub, N stages, primal terms, reduce (+ step)
   if (run_step(pl, pl->WB, 0, pl->BETA, pl->UHAT, pl->EVEC)) return TSMPC_ERR_CUDA;
   gap_dual_terms_kernel<<<G, 256, 0, pl->stream>>>(c, pl->WB, pl->X, pl->U, pl->COLS);
   CU(cudaGetLastError());
@@ -607,6 +749,7 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
   if (!(lam > 0.0)) return fail(TSMPC_ERR_VALIDATION, "step size must be positive");
   if (!pl->has_cache) return fail(TSMPC_ERR_VALIDATION, "no stage cache uploaded (tsmpc_set_cache)");
   CU(cudaSetDevice(pl->device));
+  pl->launches = 0;
   const int E = pl->E, NXP = pl->NXP, NUP = pl->NUP, nx = pl->nx, nu = pl->nu;
   const bool record = flags & TSMPC_RECORD_RESIDUALS;
   // momentum tables
@@ -677,6 +820,7 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
     int rc = compute_gap(pl, yfin, &gap);
     if (rc) return rc;
   }
+  CU(cudaEventRecord(pl->ev2, pl->stream));
   out->gap = gap;
   out->iterations = iters;
   std::vector<unsigned long long> rbits(nres);
@@ -697,6 +841,9 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
   float ms = 0.f;
   CU(cudaEventElapsedTime(&ms, pl->ev0, pl->ev1));
   out->device_ms = ms;
+  CU(cudaEventElapsedTime(&ms, pl->ev0, pl->ev2));
+  out->device_total_ms = ms;
+  out->kernel_launches = pl->launches;
   auto as_d = [](unsigned long long b) { double d; std::memcpy(&d, &b, sizeof d); return d; };
   out->residual_inf = as_d(rbits[nres - 1]);
   if (record && out->resid_trace)

@@ -30,7 +30,7 @@ namespace tsmpc {
 
 constexpr int kThreads = 416;      // 13 warps: one warp per n-tile of GEMM 1 at n_v = 97
 constexpr int kWarps = kThreads / 32;
-constexpr int kTileM = 64;         // edge rows per shared-memory tile
+constexpr int kTileM = 96;         // edge rows per shared-memory tile (<= 12 m-tiles)
 constexpr int kMaxSeg = 32;        // longest segment (longer chains are split into levels)
 
 enum Mode : int { kModeApg = 0, kModeStep = 1 };
@@ -41,7 +41,9 @@ struct Params {
   int NXP, NUP, NVP;            // global row pitches (multiples of 4 doubles)
   int KS1, NT1;                 // GEMM 1: k-steps (K1 = NXP+NUP), n-tiles (ceil(nv/8))
   int KS2, NT2, NU8;            // GEMM 2: k-steps (ceil(nv/4)), n-tiles, du columns
-  int LDA, LDB;                 // shared-memory leading dimensions
+  int LDA1, LDB1;               // shared-memory leading dims, backward sweep (A | C)
+  int LDA2, LDB2;               // shared-memory leading dims, forward sweep (A | C)
+  int META_OFF;                 // offset (doubles) of the tile metadata ints
   int diagA;
   double Wx, gamma_d;
   // model
@@ -60,6 +62,22 @@ struct Params {
   const int* tile_seg;          // n_tiles + 1
   const int* seg_row;           // n_segs + 1
   const int* row_edge;          // n_rows
+  // collapsed trunk (diagonal A): every non-leaf segment edge is a "trunk" edge,
+  // handled by one component-sliced sweep + one distributed GEMM per iteration
+  int collapsed;                // 1: leaf segments are level 0 tiles, trunk collapsed
+  int n_trunk;                  // trunk edges T
+  const int* trunk_edge;        // T, ascending edge id (stage-major)
+  const int* trunk_stage_ptr;   // N+1 offsets into trunk_edge per edge stage
+  const int* trunk_pos;         // E, position in trunk_edge or -1
+  const int* trunk_child0;      // T: trunk pos of the first child if all children are trunk,
+                                //    -1 if none is (chain heads only), -2 if mixed
+  const int* path_ptr;          // T+1 offsets into path_list
+  const int* path_list;         // trunk positions root .. t for every trunk edge t
+  int KY_LD, KSK, NTT;          // KY pitch (NVP + NXP + NUP), GEMM k-steps, n-tiles
+  int OUT_LD, U_OFF, X_OFF;     // OUT pitch and column offsets of u and bv + e
+  double* KY;                   // T x KY_LD  [K | Yx | Ypsi]
+  double* OUT;                  // T x OUT_LD [S | u | bv + e]
+  const double* MTf;            // fragment-ordered [NTT][KSK][32] trunk operator
   // state
   double* ybuf[2];              // slot -> [sig | zeta | psi] blocks
   double *xavg, *uavg, *X, *U, *T, *XIQG, *GG;
@@ -70,6 +88,23 @@ struct Params {
   double lam;
   const double *theta, *coef;
   unsigned long long* resid;    // iters (record_all) or 1 slot, bit pattern of a double >= 0
+  unsigned long long* timers;   // phase cycle counters of CTA 0 (TSMPC_TIMERS builds only)
 };
+
+// Phase timers (profiling builds: -DTSMPC_TIMERS).  Slot k accumulates the cycles
+// CTA 0 spends between consecutive marks.
+#ifdef TSMPC_TIMERS
+#define TSMPC_MARK(P, k, t)                                                   \
+  do {                                                                        \
+    __syncthreads();                                                          \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (P).timers) {                  \
+      const long long now_ = clock64();                                       \
+      atomicAdd((P).timers + (k), (unsigned long long)(now_ - (t)));          \
+      (t) = now_;                                                             \
+    }                                                                         \
+  } while (0)
+#else
+#define TSMPC_MARK(P, k, t) do { } while (0)
+#endif
 
 }  // namespace tsmpc

@@ -66,11 +66,17 @@ class DevicePlan:
 
     # -- introspection -------------------------------------------------------
     def info(self) -> dict:
-        buf = np.zeros(9, dtype=np.int64)
-        nat.check(self._lib.tsmpc_plan_info(self._h, nat.iptr(buf), 9), "tsmpc_plan_info")
+        buf = np.zeros(11, dtype=np.int64)
+        nat.check(self._lib.tsmpc_plan_info(self._h, nat.iptr(buf), 11), "tsmpc_plan_info")
         keys = ("levels", "ctas", "tiles", "segments", "smem_bytes", "diag_A", "threads",
-                "tile_rows", "sms")
+                "tile_rows", "sms", "collapsed", "trunk_edges")
         return dict(zip(keys, (int(v) for v in buf)))
+
+    def debug_timers(self) -> np.ndarray:
+        """Phase cycle counters of CTA 0 since the last call (timer builds only)."""
+        buf = (ctypes.c_uint64 * 16)()
+        nat.check(self._lib.tsmpc_debug_timers(self._h, buf, 16), "tsmpc_debug_timers")
+        return np.array(buf[:], dtype=np.uint64)
 
     # -- uploads -------------------------------------------------------------
     def set_cache(self, cache, model=None):
@@ -123,6 +129,8 @@ class DevicePlan:
         nat.check(rc, "tsmpc_solve")
         out.update(residual_inf=float(res.residual_inf), gap=float(res.gap),
                    device_ms=float(res.device_ms), iterations=int(res.iterations),
+                   device_total_ms=float(res.device_total_ms),
+                   kernel_launches=int(res.kernel_launches),
                    resid_trace=trace)
         return out
 
