@@ -34,6 +34,17 @@ __device__ __forceinline__ int* meta_base(const Params& P) {
 #define SM_LO(P) (meta_base(P) + kTileM)
 #define SM_HI(P) (meta_base(P) + 2 * kTileM)
 #define SM_MISC(P) (meta_base(P) + 3 * kTileM)
+// per-row 1/(2 p_e) of the current tile (doubles after the metadata ints)
+#define SM_INV2P(P) (g_smem + (P).META_OFF + 160)
+// model bound vectors, staged once per launch: x_s, x_min, x_max (NXP each), u_min, u_max (NUP)
+#define SM_BOUNDS(P) (g_smem + (P).META_OFF + 160 + kTileM)
+
+// Explicit global-space accesses: the state pointers reach the device code through
+// kernel parameters, so plain dereferences would compile to generic LD/ST.  The .cg
+// variants cache in L2 only, which keeps them coherent with the other CTAs' writes
+// (every cross-CTA dependency of the kernel crosses a grid barrier).
+__device__ __forceinline__ double gld(const double* p) { return __ldcg(p); }
+__device__ __forceinline__ void gst(double* p, double v) { __stcg(p, v); }
 
 // C[rows, nt*8 .. nt*8+7] = A[rows, 0:4*KS] * B + C for every n-tile owned by
 // this warp (C holds the per-row bias, staged by the caller's load phase; rows
@@ -53,23 +64,24 @@ __device__ __forceinline__ void gemm_tile(const Params& P, int a_off, int lda, i
 #pragma unroll
     for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = 0.0;
     const double* bp = Bf + (size_t)nt * KS * 32 + lane;
-    double bq[8];
+    constexpr int R = MT <= 6 ? 16 : 12;  // B-fragment ring depth (k-steps in flight)
+    double bq[R];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) bq[q] = (q < KS) ? __ldg(bp + q * 32) : 0.0;
-    for (int ks0 = 0; ks0 < KS; ks0 += 8) {
+    for (int q = 0; q < R; ++q) bq[q] = (q < KS) ? __ldg(bp + q * 32) : 0.0;
+    for (int ks0 = 0; ks0 < KS; ks0 += R) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < R; ++q) {
         const int ks = ks0 + q;
         if (ks < KS) {
           // all A fragments of the k-step in distinct registers, then the DMMAs read
-          // the ring slot directly; the slot is refilled (8 k-steps ahead) only after
+          // the ring slot directly; the slot is refilled (R k-steps ahead) only after
           // its last use, so no move ever waits on an in-flight load
           double af[MT];
 #pragma unroll
           for (int m = 0; m < MT; ++m) af[m] = As[m * 8 * lda + ks * 4];
 #pragma unroll
           for (int m = 0; m < MT; ++m) dmma8x8x4(acc[m], af[m], bq[q]);
-          if (ks + 8 < KS) bq[q] = __ldg(bp + (ks + 8) * 32);
+          if (ks + R < KS) bq[q] = __ldg(bp + (ks + R) * 32);
         }
       }
     }
@@ -117,7 +129,12 @@ __device__ __forceinline__ void load_tile(const Params& P, int tile, int& nrows,
   int* hi = SM_HI(P);
   int* misc = SM_MISC(P);
   __syncthreads();  // the previous tile is done with shared memory
-  for (int i = threadIdx.x; i < nrows; i += kThreads) edge[i] = P.row_edge[rbase + i];
+  double* inv2p = SM_INV2P(P);
+  for (int i = threadIdx.x; i < nrows; i += kThreads) {
+    const int e = P.row_edge[rbase + i];
+    edge[i] = e;
+    inv2p[i] = P.inv2p[e];
+  }
   if (threadIdx.x == 0) misc[0] = 0;
   __syncthreads();
   for (int i = threadIdx.x; i < nsegs; i += kThreads) {
@@ -193,26 +210,35 @@ __device__ __noinline__ void bwd_tile(const Params& P, int tile, int nu) {
   // (1) operand rows [s | psi^]; a warp owns a row and issues all its loads first
   for (int r = warp; r < nrows; r += kWarps) {
     const int e = edge[r];
-    const int st = P.edge_stage[e];
+    const int st = __ldg(P.edge_stage + e);
     const double ds = stage_scale(P.sig_stage, st, P.scaled);
     const double dz = stage_scale(P.zeta_stage, st, P.scaled);
-    const double* ys = Y + (size_t)e * P.NXP;
-    const double* yps = Yp + (size_t)e * P.NXP;
-    const double* yp_ = Y + poff + (size_t)e * P.NUP;
-    const double* ypp = Yp + poff + (size_t)e * P.NUP;
-    const double* bt = P.beta + (size_t)e * P.NVP;
-    double a[kChunks], b[kChunks], g[kChunks], h[kChunks], pv[kChunks], pp[kChunks], bb[kChunks];
+    // per-row base pointers (lane folded in) so every access is base + immediate
+    const double* ys = Y + (size_t)e * P.NXP + lane;
+    const double* yps = Yp + (size_t)e * P.NXP + lane;
+    const double* yp_ = Y + poff + (size_t)e * P.NUP + lane;
+    const double* ypp = Yp + poff + (size_t)e * P.NUP + lane;
+    const double* bt = P.beta + (size_t)e * P.NVP + lane;
+    const double* pst = P.psi_stage + (size_t)st * P.NUP + lane;
+    double a[kChunks] = {}, b[kChunks] = {}, g[kChunks] = {}, h[kChunks] = {};
+    double pv[kChunks] = {}, pp[kChunks] = {}, bb[kChunks] = {}, ps[kChunks] = {};
 #pragma unroll
     for (int q = 0; q < kChunks; ++q) {
       const int i = lane + 32 * q;
-      const bool okx = i < P.nx, oku = i < P.nu;
-      a[q] = okx ? ys[i] : 0.0;
-      g[q] = okx ? ys[zoff + i] : 0.0;
-      pv[q] = oku ? yp_[i] : 0.0;
-      b[q] = (apg && okx) ? yps[i] : 0.0;
-      h[q] = (apg && okx) ? yps[zoff + i] : 0.0;
-      pp[q] = (apg && oku) ? ypp[i] : 0.0;
-      bb[q] = i < P.nv ? bt[i] : 0.0;
+      if (i < P.nx) {
+        a[q] = gld(ys + 32 * q);
+        g[q] = gld(ys + zoff + 32 * q);
+        if (apg) {
+          b[q] = gld(yps + 32 * q);
+          h[q] = gld(yps + zoff + 32 * q);
+        }
+      }
+      if (i < P.nu) {
+        pv[q] = gld(yp_ + 32 * q);
+        if (apg) pp[q] = gld(ypp + 32 * q);
+        ps[q] = P.scaled ? __ldg(pst + 32 * q) : 1.0;
+      }
+      if (i < P.nv) bb[q] = __ldg(bt + 32 * q);
     }
     // GEMM 1 accumulates onto its C tile: stage beta there (zero pad columns)
 #pragma unroll
@@ -237,7 +263,7 @@ __device__ __noinline__ void bwd_tile(const Params& P, int tile, int nu) {
         double v = 0.0;
         if (i < P.nu) {
           const double wp = apg ? extrap(pv[q], pp[q], c) : pv[q];
-          v = P.scaled ? __dmul_rn(wp, P.psi_stage[(size_t)st * P.NUP + i]) : wp;
+          v = P.scaled ? __dmul_rn(wp, ps[q]) : wp;
         }
         row[P.NXP + i] = v;
       }
@@ -307,7 +333,7 @@ __device__ __noinline__ void bwd_tile(const Params& P, int tile, int nu) {
     for (int r = hi - 1; r >= lo; --r) {
       const int e = edge[r];
       g = __dadd_rn(SB[r * LDB + j], g);
-      P.T[(size_t)e * P.NVP + j] = __dmul_rn(g, P.inv2p[e]);
+      P.T[(size_t)e * P.NVP + j] = __dmul_rn(g, SM_INV2P(P)[r]);
     }
     P.GG[(size_t)edge[lo] * P.NVP + j] = g;
   }
@@ -334,14 +360,16 @@ __device__ __noinline__ void fwd_tile(const Params& P, int tile, int nu) {
   // (1a) stage t rows (zero-padded to K2 columns) and GEMM 2's bias [uhat | e]
   for (int r = warp; r < nrows; r += kWarps) {
     const int e = edge[r];
-    const double* tr = P.T + (size_t)e * P.NVP;
-    double v[kChunks], uh[kChunks], ev[kChunks];
+    const double* tr = P.T + (size_t)e * P.NVP + lane;
+    const double* uhp = P.uhat + (size_t)e * P.NUP + lane;
+    const double* evp = P.evec + (size_t)e * P.NXP + lane;
+    double v[kChunks] = {}, uh[kChunks] = {}, ev[kChunks] = {};
 #pragma unroll
     for (int q = 0; q < kChunks; ++q) {
       const int j = lane + 32 * q;
-      v[q] = j < P.nv ? tr[j] : 0.0;
-      uh[q] = (P.uhat && j < P.nu) ? P.uhat[(size_t)e * P.NUP + j] : 0.0;
-      ev[q] = (P.evec && j < P.nx) ? P.evec[(size_t)e * P.NXP + j] : 0.0;
+      if (j < P.nv) v[q] = gld(tr + 32 * q);
+      if (P.uhat && j < P.nu) uh[q] = __ldg(uhp + 32 * q);
+      if (P.evec && j < P.nx) ev[q] = __ldg(evp + 32 * q);
     }
 #pragma unroll
     for (int q = 0; q < kChunks; ++q) {
@@ -416,19 +444,15 @@ __device__ __noinline__ void fwd_tile(const Params& P, int tile, int nu) {
   TSMPC_MARK(P, 8, tm_);
 }
 
-// Per-row epilogue of the forward sweep, one warp per edge row: x in the A
-// region rows, u in the C region rows (forward layout), edge ids in SM_EDGE.
-// APG mode: prox_g, dual update, ergodic averages, residual (engine.py:546-575);
-// STEP mode: store x, u.
+#include "tsmpc_epilogue.cuh"
+
 __device__ __noinline__ void rows_epilogue(const Params& P, int nu, int nrows) {
-  const int LDA = P.LDA2, LDB = P.LDB2;
-  const double* const SA = g_smem;
-  const double* const SB = g_smem + kTileM * LDA;
-  const int* const edge = SM_EDGE(P);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const bool apg = P.mode == kModeApg;
-  const bool last = (nu == P.iters - 1) || !apg;
-  if (!apg) {
+  if (P.mode != kModeApg) {  // STEP: store x, u
+    const int LDA = P.LDA2, LDB = P.LDB2;
+    const double* const SA = g_smem;
+    const double* const SB = g_smem + kTileM * LDA;
+    const int* const edge = SM_EDGE(P);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int r = warp; r < nrows; r += kWarps) {
       const int e = edge[r];
       for (int j = lane; j < P.nu; j += 32) P.U[(size_t)e * P.NUP + j] = SB[r * LDB + j];
@@ -436,121 +460,16 @@ __device__ __noinline__ void rows_epilogue(const Params& P, int nu, int nrows) {
     }
     return;
   }
-  const int E = P.n_edges;
-  const int cur = (P.slot0 + nu) & 1;
-  const double* __restrict__ Y = P.ybuf[cur];
-  double* Yn = P.ybuf[cur ^ 1];  // y_prev slot receives y_next
-  const double c = P.coef[nu];
-  const double th = P.theta[nu];
-  const double om = __dsub_rn(1.0, th);
-  const double lam = P.lam;
-  const double lam_p = 1.0 / lam;  // prox parameter (engine.py:555)
-  const size_t zoff = (size_t)E * P.NXP, poff = 2 * (size_t)E * P.NXP;
-  const bool want_resid = last || P.record_all;
-  double rmax = 0.0;
-  for (int r = warp; r < nrows; r += kWarps) {
-    const int e = edge[r];
-    const int node = e + 1;
-    const int st = P.edge_stage[e];
-    const double ds = stage_scale(P.sig_stage, st, P.scaled);
-    const double dz = stage_scale(P.zeta_stage, st, P.scaled);
-    const size_t ox = (size_t)e * P.NXP, oa = (size_t)node * P.NXP, ou = (size_t)e * P.NUP;
-    // issue every global read of the state-copy part first
-    double ys[kChunks], yps[kChunks], yz[kChunks], ypz[kChunks], xa[kChunks];
-#pragma unroll
-    for (int q = 0; q < kChunks; ++q) {
-      const int i = lane + 32 * q;
-      const bool okx = i < P.nx;
-      ys[q] = okx ? Y[ox + i] : 0.0;
-      yps[q] = okx ? Yn[ox + i] : 0.0;
-      yz[q] = okx ? Y[zoff + ox + i] : 0.0;
-      ypz[q] = okx ? Yn[zoff + ox + i] : 0.0;
-      xa[q] = okx ? P.xavg[oa + i] : 0.0;
-    }
-    // --- state copies: two weighted-distance prox blocks (engine.py:146-180)
-    double xs[kChunks], ws[kChunks], wz[kChunks], ts[kChunks], tz[kChunks];
-    double ss = 0.0, sz = 0.0;
-#pragma unroll
-    for (int q = 0; q < kChunks; ++q) {
-      const int i = lane + 32 * q;
-      if (i < P.nx) {
-        const double x = SA[r * LDA + i];
-        xs[q] = x;
-        ws[q] = extrap(ys[q], yps[q], c);
-        wz[q] = extrap(yz[q], ypz[q], c);
-        // t_arg = w / lam + D Hz   (engine.py:552-554)
-        ts[q] = __dadd_rn(__ddiv_rn(ws[q], lam), __dmul_rn(x, ds));
-        tz[q] = __dadd_rn(__ddiv_rn(wz[q], lam), __dmul_rn(x, dz));
-        const double ps = fmax(ts[q], __dmul_rn(ds, P.x_s[i]));
-        const double pz = fmin(fmax(tz[q], __dmul_rn(dz, P.x_min[i])), __dmul_rn(dz, P.x_max[i]));
-        const double gs = __dsub_rn(ps, ts[q]), gz = __dsub_rn(pz, tz[q]);
-        ss = fma(gs, gs, ss);
-        sz = fma(gz, gz, sz);
-      }
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      ss += __shfl_xor_sync(0xffffffffu, ss, off);
-      sz += __shfl_xor_sync(0xffffffffu, sz, off);
-    }
-    const double dist_s = sqrt(ss), dist_z = sqrt(sz);
-    const double wgt_s = __ddiv_rn(__dmul_rn(lam_p, P.Wx), ds);
-    const double wgt_z = __ddiv_rn(__dmul_rn(lam_p, P.gamma_d), dz);
-    const double fs = dist_s > wgt_s ? __ddiv_rn(wgt_s, dist_s) : 1.0;
-    const double fz = dist_z > wgt_z ? __ddiv_rn(wgt_z, dist_z) : 1.0;
-#pragma unroll
-    for (int q = 0; q < kChunks; ++q) {
-      const int i = lane + 32 * q;
-      if (i < P.nx) {
-        const double x = xs[q];
-        const double hs = __dmul_rn(x, ds), hz = __dmul_rn(x, dz);
-        const double ps = fmax(ts[q], __dmul_rn(ds, P.x_s[i]));
-        const double pz = fmin(fmax(tz[q], __dmul_rn(dz, P.x_min[i])), __dmul_rn(dz, P.x_max[i]));
-        const double t_s = __dadd_rn(ts[q], __dmul_rn(fs, __dsub_rn(ps, ts[q])));
-        const double t_z = __dadd_rn(tz[q], __dmul_rn(fz, __dsub_rn(pz, tz[q])));
-        Yn[ox + i] = __dadd_rn(ws[q], __dmul_rn(lam, __dsub_rn(hs, t_s)));
-        Yn[zoff + ox + i] = __dadd_rn(wz[q], __dmul_rn(lam, __dsub_rn(hz, t_z)));
-        if (want_resid) {
-          rmax = fmax(rmax, fabs(__dsub_rn(x, __ddiv_rn(t_s, ds))));
-          rmax = fmax(rmax, fabs(__dsub_rn(x, __ddiv_rn(t_z, dz))));
-        }
-        P.xavg[oa + i] = __dadd_rn(__dmul_rn(xa[q], om), __dmul_rn(th, x));
-        if (last) P.X[oa + i] = x;
-      }
-    }
-    // --- input copy: box projection (engine.py:182)
-    double yp[kChunks], ypp[kChunks], ua[kChunks];
-#pragma unroll
-    for (int q = 0; q < kChunks; ++q) {
-      const int j = lane + 32 * q;
-      const bool oku = j < P.nu;
-      yp[q] = oku ? Y[poff + ou + j] : 0.0;
-      ypp[q] = oku ? Yn[poff + ou + j] : 0.0;
-      ua[q] = oku ? P.uavg[ou + j] : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < kChunks; ++q) {
-      const int j = lane + 32 * q;
-      if (j < P.nu) {
-        const double u = SB[r * LDB + j];
-        const double dp = P.scaled ? P.psi_stage[(size_t)st * P.NUP + j] : 1.0;
-        const double w = extrap(yp[q], ypp[q], c);
-        const double hp = __dmul_rn(u, dp);
-        const double a = __dadd_rn(__ddiv_rn(w, lam), hp);
-        const double t = fmin(fmax(a, __dmul_rn(dp, P.u_min[j])), __dmul_rn(dp, P.u_max[j]));
-        Yn[poff + ou + j] = __dadd_rn(w, __dmul_rn(lam, __dsub_rn(hp, t)));
-        if (want_resid) rmax = fmax(rmax, fabs(__dsub_rn(u, __ddiv_rn(t, dp))));
-        P.uavg[ou + j] = __dadd_rn(__dmul_rn(ua[q], om), __dmul_rn(th, u));
-        if (last) P.U[ou + j] = u;
-      }
-    }
+  const int xc = (P.nx + 31) >> 5, uc = (P.nu + 31) >> 5;
+#define TSMPC_EPI(X, U) case (X) * 8 + (U): rows_epilogue_t<X, U>(P, nu, nrows); break;
+  switch (xc * 8 + uc) {
+    TSMPC_EPI(1, 1) TSMPC_EPI(1, 2) TSMPC_EPI(1, 3) TSMPC_EPI(1, 4)
+    TSMPC_EPI(2, 1) TSMPC_EPI(2, 2) TSMPC_EPI(2, 3) TSMPC_EPI(2, 4)
+    TSMPC_EPI(3, 1) TSMPC_EPI(3, 2) TSMPC_EPI(3, 3) TSMPC_EPI(3, 4)
+    TSMPC_EPI(4, 1) TSMPC_EPI(4, 2) TSMPC_EPI(4, 3) TSMPC_EPI(4, 4)
+    default: break;
   }
-  if (want_resid) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, off));
-    if (lane == 0 && rmax > 0.0)
-      atomicMax(P.resid + (P.record_all ? nu : 0), (unsigned long long)__double_as_longlong(rmax));
-  }
+#undef TSMPC_EPI
 }
 
 // ---------------------------------------------------------------------------
@@ -754,6 +673,19 @@ __global__ void __launch_bounds__(kThreads, 1) apg_persistent_kernel(const __gri
   cg::grid_group grid = cg::this_grid();
   const int cta = blockIdx.x;
   const int D = P.n_levels;
+  {  // model bound vectors for the epilogue, once per launch
+    double* bnd = SM_BOUNDS(P);
+    for (int i = threadIdx.x; i < P.NXP; i += kThreads) {
+      bnd[i] = P.x_s[i];
+      bnd[P.NXP + i] = P.x_min[i];
+      bnd[2 * P.NXP + i] = P.x_max[i];
+    }
+    for (int j = threadIdx.x; j < P.NUP; j += kThreads) {
+      bnd[3 * P.NXP + j] = P.u_min[j];
+      bnd[3 * P.NXP + P.NUP + j] = P.u_max[j];
+    }
+    __syncthreads();
+  }
   if (P.collapsed) {
     // leaf segments = level-0 tiles; trunk collapsed: 3 grid barriers / iteration
     const int* lt = P.lvl_tiles + cta;

@@ -368,7 +368,8 @@ tsmpc_plan* tsmpc_plan_create(const tsmpc_problem* pb, int device) {
   const int region = std::max({kTileM * (P.LDA1 + P.LDB1), kTileM * (P.LDA2 + P.LDB2), kWarps * 4 * 64});
   P.META_OFF = region;
   P.Wx = pb->Wx; P.gamma_d = pb->gamma_d;
-  pl->smem = sizeof(double) * (size_t)region + sizeof(int) * (3 * kTileM + 4);
+  // + metadata ints (<= 160 doubles) + per-row inv2p (kTileM doubles) + model bounds
+  pl->smem = sizeof(double) * ((size_t)region + 160 + kTileM + 3 * NXP + 2 * NUP);
   if (pl->smem > (size_t)prop.sharedMemPerBlockOptin) {
     fail(TSMPC_ERR_DIMENSION, "tile needs %zu bytes of shared memory (limit %zu)", pl->smem,
          (size_t)prop.sharedMemPerBlockOptin);
@@ -525,6 +526,16 @@ tsmpc_plan* tsmpc_plan_create(const tsmpc_problem* pb, int device) {
   rc |= pl->upload(&pl->psi_c, psi_c.data(), psi_c.size());
   pl->sig_c = d_sig;
   pl->zeta_c = d_zeta;
+  {  // reciprocal scaling tables for the epilogue's quotients
+    std::vector<double> rs(N), rz(N), rp(psi.size());
+    for (int j = 0; j < N; ++j) { rs[j] = 1.0 / sig[j]; rz[j] = 1.0 / zeta[j]; }
+    for (size_t k = 0; k < psi.size(); ++k) rp[k] = 1.0 / psi[k];
+    double *d_rs, *d_rz, *d_rp;
+    rc |= pl->upload(&d_rs, rs.data(), rs.size());
+    rc |= pl->upload(&d_rz, rz.data(), rz.size());
+    rc |= pl->upload(&d_rp, rp.data(), rp.size());
+    P.sig_rcp = d_rs; P.zeta_rcp = d_rz; P.psi_rcp = d_rp;
+  }
   rc |= pl->upload(&d_inv2p, inv2p.data(), inv2p.size());
   rc |= pl->upload(&d_pe, pe.data(), pe.size());
   rc |= pl->upload(&d_Wu, pb->Wu, (size_t)nu * nu);
@@ -804,6 +815,7 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
   P.uhat = pl->UHAT;
   P.evec = pl->EVEC;
   P.lam = lam;
+  P.inv_lam = 1.0 / lam;
   P.theta = pl->THETA;
   P.coef = pl->COEF;
   P.record_all = record ? 1 : 0;

@@ -53,6 +53,8 @@ struct Params {
   const double* W2f;            // fragment-ordered [NT2][KS2][32]
   const double *x_s, *x_min, *x_max, *u_min, *u_max;
   const double *sig_stage, *zeta_stage, *psi_stage;  // N, N, N*NUP
+  const double *sig_rcp, *zeta_rcp, *psi_rcp;        // reciprocals of the above
+  double inv_lam;                                    // 1 / lam
   // tree
   const int *anc, *child_start, *child_stop, *edge_stage;
   const double* inv2p;
