@@ -580,6 +580,118 @@ __device__ __noinline__ void trunk_sweep(const Params& P, int nu) {
   }
 }
 
+// Phase B with the CTA's component slice staged in shared memory (the tile region
+// is free between the sweeps): one parallel round of global loads (own terms and
+// chain-head contributions, which do not depend on the recursion), then the
+// bottom-up / top-down recursions touch shared memory only, then one store round.
+// Zs[tp][k]: beta sums (K) or subtree sums Z (Yx, Ypsi); Xs[tp][k]: xiq (Yx).
+__device__ __noinline__ void trunk_sweep_smem(const Params& P, int nu) {
+  const int T = P.n_trunk;
+  const int ncomp = P.nv + P.nx + P.nu;
+  const int c_lo = (int)((long long)ncomp * blockIdx.x / gridDim.x);
+  const int c_hi = (int)((long long)ncomp * (blockIdx.x + 1) / gridDim.x);
+  const int nc = c_hi - c_lo;
+  if (nc <= 0) return;
+  double* const Zs = g_smem;
+  double* const Xs = g_smem + (size_t)T * nc;
+  const int E = P.n_edges;
+  const bool apg = P.mode == kModeApg;
+  const int cur = (P.slot0 + nu) & 1;
+  const double* __restrict__ Y = P.ybuf[cur];
+  const double* __restrict__ Yp = P.ybuf[cur ^ 1];
+  const double c = apg ? P.coef[nu] : 0.0;
+  const size_t zoff = (size_t)E * P.NXP, poff = 2 * zoff;
+  __syncthreads();  // shared memory is free
+  // (1) own terms + chain-head children (independent of the recursion)
+  for (int idx = threadIdx.x; idx < T * nc; idx += kThreads) {
+    const int tp = idx / nc, k = idx - tp * nc, q = c_lo + k;
+    const int a = P.trunk_edge[tp];
+    const int node = a + 1;
+    const int ch0 = P.child_start[node] - 1, ch1 = P.child_stop[node] - 1;
+    const int tc = P.trunk_child0[tp];  // >= 0: no chain-head children
+    double z = 0.0, x = 0.0;
+    if (q < P.nv) {
+      z = __ldg(P.beta + (size_t)a * P.NVP + q);
+      if (tc < 0)
+        for (int ch = ch0; ch < ch1; ++ch)
+          if (tc == -1 || P.trunk_pos[ch] < 0) z = __dadd_rn(z, gld(P.GG + (size_t)ch * P.NVP + q));
+    } else if (q < P.nv + P.nx) {
+      const int i = q - P.nv;
+      const int es = __ldg(P.edge_stage + a);
+      const size_t o = (size_t)a * P.NXP + i;
+      const double ws = apg ? extrap(gld(Y + o), gld(Yp + o), c) : gld(Y + o);
+      const double wz = apg ? extrap(gld(Y + zoff + o), gld(Yp + zoff + o), c) : gld(Y + zoff + o);
+      const double s = __dadd_rn(__dmul_rn(ws, stage_scale(P.sig_stage, es, P.scaled)),
+                                 __dmul_rn(wz, stage_scale(P.zeta_stage, es, P.scaled)));
+      double h = 0.0;
+      if (tc < 0)
+        for (int ch = ch0; ch < ch1; ++ch)
+          if (tc == -1 || P.trunk_pos[ch] < 0) h = __dadd_rn(h, gld(P.XIQG + (size_t)ch * P.NXP + i));
+      x = __dadd_rn(s, __dmul_rn(h, P.a_diag[i]));  // s + a * (head-children xiq)
+    } else {
+      const int j = q - P.nv - P.nx;
+      const int es = __ldg(P.edge_stage + a);
+      const size_t o = poff + (size_t)a * P.NUP + j;
+      const double wp = apg ? extrap(gld(Y + o), gld(Yp + o), c) : gld(Y + o);
+      z = P.scaled ? __dmul_rn(wp, __ldg(P.psi_stage + (size_t)es * P.NUP + j)) : wp;
+    }
+    Zs[idx] = z;
+    Xs[idx] = x;
+  }
+  __syncthreads();
+  // (2) bottom-up: add the trunk children (shared memory only)
+  for (int st = P.N - 1; st >= 0; --st) {
+    const int t0 = P.trunk_stage_ptr[st], t1 = P.trunk_stage_ptr[st + 1];
+    if (t0 == t1) continue;  // block-uniform
+    for (int idx = t0 * nc + threadIdx.x; idx < t1 * nc; idx += kThreads) {
+      const int tp = idx / nc, k = idx - tp * nc, q = c_lo + k;
+      const int tc = P.trunk_child0[tp];
+      if (tc == -1) {
+        if (q >= P.nv && q < P.nv + P.nx) Zs[idx] = Xs[idx];  // leaf of the trunk: Z = xiq
+        continue;
+      }
+      const int a = P.trunk_edge[tp];
+      const int node = a + 1;
+      const int n = P.child_stop[node] - P.child_start[node];
+      double zs = 0.0, xs = 0.0;
+      for (int m = 0; m < n; ++m) {
+        const int cp = tc >= 0 ? tc + m : P.trunk_pos[P.child_start[node] - 1 + m];
+        if (cp < 0) continue;
+        zs = __dadd_rn(zs, Zs[cp * nc + k]);
+        xs = __dadd_rn(xs, Xs[cp * nc + k]);
+      }
+      if (q >= P.nv && q < P.nv + P.nx) {
+        const double xiq = __dadd_rn(Xs[idx], __dmul_rn(xs, P.a_diag[q - P.nv]));
+        Xs[idx] = xiq;
+        Zs[idx] = __dadd_rn(xiq, zs);
+      } else {
+        Zs[idx] = __dadd_rn(Zs[idx], zs);
+      }
+    }
+    __syncthreads();
+  }
+  // (3) top-down: K_a, Y_a = own * inv2p_a + parent's
+  for (int st = 0; st < P.N; ++st) {
+    const int t0 = P.trunk_stage_ptr[st], t1 = P.trunk_stage_ptr[st + 1];
+    if (t0 == t1) continue;
+    for (int idx = t0 * nc + threadIdx.x; idx < t1 * nc; idx += kThreads) {
+      const int tp = idx / nc, k = idx - tp * nc;
+      const int pp = P.trunk_parent[tp];
+      double v = __dmul_rn(Zs[idx], __ldg(P.inv2p + P.trunk_edge[tp]));
+      if (pp >= 0) v = __dadd_rn(v, Zs[pp * nc + k]);
+      Zs[idx] = v;
+    }
+    __syncthreads();
+  }
+  // (4) results: KY columns of the slice, xiq of the trunk edges
+  for (int idx = threadIdx.x; idx < T * nc; idx += kThreads) {
+    const int tp = idx / nc, k = idx - tp * nc, q = c_lo + k;
+    const int col = q < P.nv ? q : (q < P.nv + P.nx ? P.NVP + (q - P.nv) : P.NVP + P.NXP + (q - P.nv - P.nx));
+    gst(P.KY + (size_t)tp * P.KY_LD + col, Zs[idx]);
+    if (q >= P.nv && q < P.nv + P.nx) gst(P.XIQG + (size_t)P.trunk_edge[tp] * P.NXP + (q - P.nv), Xs[idx]);
+  }
+}
+
 // Phase C: OUT = KY * MT + [0 | uhat | e] for all trunk rows.  Work item = (n-tile,
 // block of 4 m-tiles); the 13 warps of a CTA split the k-steps and reduce their
 // partial tiles through shared memory in a fixed order (deterministic).
@@ -696,7 +808,8 @@ __global__ void __launch_bounds__(kThreads, 1) apg_persistent_kernel(const __gri
         long long tb_ = clock64();
         grid.sync();
         TSMPC_MARK(P, 9, tb_);
-        trunk_sweep(P, nu);
+        if (P.trunk_smem) trunk_sweep_smem(P, nu);
+        else trunk_sweep(P, nu);
         TSMPC_MARK(P, 10, tb_);
         grid.sync();
         TSMPC_MARK(P, 9, tb_);

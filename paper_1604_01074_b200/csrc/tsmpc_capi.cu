@@ -124,7 +124,8 @@ struct Decomposition {
   int n_ctas = 0;
   // collapsed-trunk mode
   bool collapsed = false;
-  std::vector<int> trunk_edge, trunk_stage_ptr, trunk_pos, path_ptr, path_list, trunk_child0;
+  std::vector<int> trunk_edge, trunk_stage_ptr, trunk_pos, path_ptr, path_list, trunk_child0,
+      trunk_parent;
 };
 
 // Cut the tree into segments (maximal only-child chains of <= kMaxSeg edges),
@@ -205,6 +206,11 @@ int decompose(const tsmpc_problem* pb, int max_ctas, bool collapse, Decompositio
         while (k < (int)out.trunk_edge.size() && out.trunk_edge[k] < e_end) ++k;
       }
       out.trunk_stage_ptr[N] = k;
+    }
+    out.trunk_parent.assign(out.trunk_edge.size(), -1);
+    for (size_t t = 0; t < out.trunk_edge.size(); ++t) {
+      const int pa = (int)pb->anc[out.trunk_edge[t] + 1] - 1;
+      out.trunk_parent[t] = pa >= 0 ? out.trunk_pos[pa] : -1;
     }
     out.trunk_child0.assign(out.trunk_edge.size(), -1);
     for (size_t t = 0; t < out.trunk_edge.size(); ++t) {
@@ -586,7 +592,7 @@ tsmpc_plan* tsmpc_plan_create(const tsmpc_problem* pb, int device) {
   rc |= pl->alloc(&pl->DYK, 256);
   rc |= pl->alloc(&pl->TIMERS, 16);
   int *d_te = nullptr, *d_tsp = nullptr, *d_tpos = nullptr, *d_pp = nullptr, *d_pl = nullptr,
-      *d_tc0 = nullptr;
+      *d_tc0 = nullptr, *d_tpar = nullptr;
   double *d_MTf = nullptr, *d_KY = nullptr, *d_OUT = nullptr;
   if (dec.collapsed) {
     const size_t T = std::max<size_t>(1, dec.trunk_edge.size());
@@ -595,6 +601,7 @@ tsmpc_plan* tsmpc_plan_create(const tsmpc_problem* pb, int device) {
     if (!dec.trunk_edge.empty()) {
       rc |= pl->upload(&d_te, dec.trunk_edge.data(), dec.trunk_edge.size());
       rc |= pl->upload(&d_tc0, dec.trunk_child0.data(), dec.trunk_child0.size());
+      rc |= pl->upload(&d_tpar, dec.trunk_parent.data(), dec.trunk_parent.size());
       rc |= pl->upload(&d_pp, dec.path_ptr.data(), dec.path_ptr.size());
       rc |= pl->upload(&d_pl, dec.path_list.data(), dec.path_list.size());
       rc |= pl->upload(&d_MTf, MTf.data(), MTf.size());
@@ -604,6 +611,11 @@ tsmpc_plan* tsmpc_plan_create(const tsmpc_problem* pb, int device) {
   }
   if (rc) return bail(0);
   P.trunk_edge = d_te; P.trunk_stage_ptr = d_tsp; P.trunk_pos = d_tpos; P.trunk_child0 = d_tc0;
+  P.trunk_parent = d_tpar;
+  {  // the component sweep stages 2 x T x (components per CTA) doubles in the tile region
+    const long long per_cta = (nv + nx + nu + dec.n_ctas - 1) / dec.n_ctas;
+    P.trunk_smem = (2LL * pl->n_trunk * per_cta <= (long long)P.META_OFF) ? 1 : 0;
+  }
   P.path_ptr = d_pp; P.path_list = d_pl; P.MTf = d_MTf; P.KY = d_KY; P.OUT = d_OUT;
 
   P.a_diag = d_adiag; P.A = d_A; P.W1f = d_W1f; P.W2f = d_W2f;

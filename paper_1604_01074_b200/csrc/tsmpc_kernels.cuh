@@ -71,6 +71,8 @@ struct Params {
   const int* trunk_edge;        // T, ascending edge id (stage-major)
   const int* trunk_stage_ptr;   // N+1 offsets into trunk_edge per edge stage
   const int* trunk_pos;         // E, position in trunk_edge or -1
+  const int* trunk_parent;      // T: trunk position of the parent edge, -1 below the root
+  int trunk_smem;               // 1: the component sweep fits its slice in shared memory
   const int* trunk_child0;      // T: trunk pos of the first child if all children are trunk,
                                 //    -1 if none is (chain heads only), -2 if mixed
   const int* path_ptr;          // T+1 offsets into path_list
