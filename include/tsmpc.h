@@ -142,6 +142,13 @@ int tsmpc_dual_operator_step(tsmpc_plan* plan, double* y_dot_dy, double* dy_dot_
 
 /* Introspection (tests / bench). */
 int tsmpc_plan_info(const tsmpc_plan* plan, int64_t* info, int32_t n_info);
+
+/* Host-only planning (no device needed): the segment / level / tile / trunk
+ * decomposition tsmpc_plan_create would build for this tree with `max_ctas` CTAs.
+ * info = {levels, ctas, tiles, segments, rows, trunk_edges, max_rows_per_cta,
+ *         max_tiles_per_cta, max_trunk_path}. */
+int tsmpc_describe_tree(const tsmpc_problem* prob, int32_t max_ctas, int32_t collapse,
+                        int64_t* info, int32_t n_info);
 const char* tsmpc_last_error(void);
 /* Phase cycle counters of CTA 0 (non-zero only in -DTSMPC_TIMERS builds); reset on read. */
 int tsmpc_debug_timers(tsmpc_plan* plan, uint64_t* out, int32_t n);

@@ -73,6 +73,8 @@ SIGNATURES = {
     "tsmpc_device_count": (ctypes.c_int, []),
     "tsmpc_debug_timers": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64),
                                           ctypes.c_int32]),
+    "tsmpc_describe_tree": (ctypes.c_int, [ctypes.POINTER(Problem), ctypes.c_int32, ctypes.c_int32,
+                                           _ip, ctypes.c_int32]),
 }
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

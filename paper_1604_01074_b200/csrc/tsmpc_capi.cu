@@ -651,6 +651,35 @@ tsmpc_plan* tsmpc_plan_create(const tsmpc_problem* pb, int device) {
 
 void tsmpc_plan_destroy(tsmpc_plan* plan) { delete plan; }
 
+int tsmpc_describe_tree(const tsmpc_problem* pb, int32_t max_ctas, int32_t collapse, int64_t* info,
+                        int32_t n) {
+  if (!pb || !info || !pb->anc || !pb->child_start || !pb->child_stop || !pb->stage_starts)
+    return fail(TSMPC_ERR_ARGUMENT, "null argument");
+  if (pb->n_nodes < 2 || pb->N < 1) return fail(TSMPC_ERR_DIMENSION, "tree too small");
+  Decomposition dec;
+  const int rc = decompose(pb, std::max(1, (int)max_ctas), collapse != 0, dec);
+  if (rc) return rc;
+  int64_t max_rows = 0, max_tiles = 0;
+  for (int c = 0; c < dec.n_ctas; ++c) {
+    int64_t rows = 0, tiles = 0;
+    for (int l = 0; l < dec.n_levels; ++l)
+      for (int t = dec.lvl_tiles[(size_t)l * dec.n_ctas + c]; t < dec.lvl_tiles[(size_t)l * dec.n_ctas + c + 1]; ++t) {
+        rows += dec.seg_row[dec.tile_seg[t + 1]] - dec.seg_row[dec.tile_seg[t]];
+        ++tiles;
+      }
+    max_rows = std::max(max_rows, rows);
+    max_tiles = std::max(max_tiles, tiles);
+  }
+  int64_t max_path = 0;
+  for (size_t t = 0; t + 1 < dec.path_ptr.size(); ++t)
+    max_path = std::max<int64_t>(max_path, dec.path_ptr[t + 1] - dec.path_ptr[t]);
+  const int64_t vals[] = {dec.n_levels, dec.n_ctas, (int64_t)dec.tile_seg.size() - 1,
+                          (int64_t)dec.seg_row.size() - 1, (int64_t)dec.row_edge.size(),
+                          (int64_t)dec.trunk_edge.size(), max_rows, max_tiles, max_path};
+  for (int i = 0; i < n && i < (int)(sizeof(vals) / sizeof(vals[0])); ++i) info[i] = vals[i];
+  return TSMPC_OK;
+}
+
 int tsmpc_plan_info(const tsmpc_plan* pl, int64_t* info, int32_t n) {
   if (!pl || !info) return fail(TSMPC_ERR_ARGUMENT, "null argument");
   const int64_t vals[] = {pl->n_levels, pl->n_ctas, pl->n_tiles, pl->n_segs, (int64_t)pl->smem,

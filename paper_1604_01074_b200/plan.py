@@ -168,6 +168,29 @@ _PLANS: dict = {}
 _MAX_PLANS = 6
 
 
+def describe_tree(tree, max_ctas: int = 148, collapse: bool = True) -> dict:
+    """Host-only view of the device decomposition of ``tree`` (no GPU needed).
+
+    Returns levels, ctas, tiles, segments, rows, trunk_edges, max_rows_per_cta,
+    max_tiles_per_cta and max_trunk_path as ``tsmpc_plan_create`` would build
+    them with ``max_ctas`` CTAs (``collapse``: diagonal-A collapsed-trunk mode).
+    """
+    lib = nat.load_library()
+    keep = {"stage_starts": _c(tree.stage_starts, np.int64), "anc": _c(tree.anc, np.int64),
+            "child_start": _c(tree.child_start, np.int64),
+            "child_stop": _c(tree.child_stop, np.int64), "prob": _c(tree.prob)}
+    pb = nat.Problem()
+    pb.N, pb.n_nodes = int(tree.N), int(tree.n_nodes)
+    for name, arr in keep.items():
+        setattr(pb, name, nat.iptr(arr) if arr.dtype == np.int64 else nat.dptr(arr))
+    buf = np.zeros(9, dtype=np.int64)
+    nat.check(lib.tsmpc_describe_tree(ctypes.byref(pb), int(max_ctas), 1 if collapse else 0,
+                                      nat.iptr(buf), 9), "tsmpc_describe_tree")
+    keys = ("levels", "ctas", "tiles", "segments", "rows", "trunk_edges", "max_rows_per_cta",
+            "max_tiles_per_cta", "max_trunk_path")
+    return dict(zip(keys, (int(v) for v in buf)))
+
+
 def plan_for(model, tree, factor, scaling=None, device: int = 0) -> DevicePlan:
     """Cached plan per (model, tree, factor, scaling) object identity."""
     key = (id(model), id(tree), id(factor), id(scaling), device)
