@@ -184,6 +184,105 @@ __device__ __forceinline__ double trunk_x(const Params& P, int tp, int i) {
 
 __device__ void rows_epilogue(const Params& P, int nu, int nrows);
 
+// Backward fill: operand rows [s | psi^] of GEMM 1 (A region) and its bias beta
+// (C region); a warp owns a row and issues each part's loads before using them.
+// Templated on the 32-lane chunk counts of x (XC) and u (UC >= chunks of n_v).
+template <int XC, int UC>
+__device__ __noinline__ void fill_rows_t(const Params& P, int nu, int nrows) {
+  const int LDA = P.LDA1, LDB = P.LDB1;
+  double* const SA = g_smem;
+  double* const SB = g_smem + kTileM * LDA;
+  const int* const edge = SM_EDGE(P);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int E = P.n_edges;
+  const int cur = (P.slot0 + nu) & 1;
+  const double* __restrict__ Y = P.ybuf[cur];
+  const double* __restrict__ Yp = P.ybuf[cur ^ 1];
+  const bool apg = P.mode == kModeApg;
+  const double c = apg ? P.coef[nu] : 0.0;
+  const size_t zoff = (size_t)E * P.NXP, poff = 2 * zoff;
+  for (int r = warp; r < nrows; r += kWarps) {
+    const int e = edge[r];
+    const int st = __ldg(P.edge_stage + e);
+    double* row = SA + r * LDA;
+    {  // s = D_sig w_sig + D_zeta w_zeta
+      const double* ys = Y + (size_t)e * P.NXP + lane;
+      const double* yps = Yp + (size_t)e * P.NXP + lane;
+      double a[XC] = {}, b[XC] = {}, g[XC] = {}, h[XC] = {};
+#pragma unroll
+      for (int q = 0; q < XC; ++q) {
+        if (lane + 32 * q < P.nx) {
+          a[q] = gld(ys + 32 * q);
+          g[q] = gld(ys + zoff + 32 * q);
+          if (apg) {
+            b[q] = gld(yps + 32 * q);
+            h[q] = gld(yps + zoff + 32 * q);
+          }
+        }
+      }
+      const double ds = stage_scale(P.sig_stage, st, P.scaled);
+      const double dz = stage_scale(P.zeta_stage, st, P.scaled);
+#pragma unroll
+      for (int q = 0; q < XC; ++q) {
+        const int i = lane + 32 * q;
+        if (i < P.NXP) {
+          double v = 0.0;
+          if (i < P.nx) {
+            const double ws = apg ? extrap(a[q], b[q], c) : a[q];
+            const double wz = apg ? extrap(g[q], h[q], c) : g[q];
+            v = __dadd_rn(__dmul_rn(ws, ds), __dmul_rn(wz, dz));
+          }
+          row[i] = v;
+        }
+      }
+    }
+    {  // psi^ = D_psi w_psi, and beta into the C tile (zero pad columns)
+      const double* yp_ = Y + poff + (size_t)e * P.NUP + lane;
+      const double* ypp = Yp + poff + (size_t)e * P.NUP + lane;
+      const double* bt = P.beta + (size_t)e * P.NVP + lane;
+      const double* pst = P.psi_stage + (size_t)st * P.NUP + lane;
+      double pv[UC] = {}, pp[UC] = {}, bb[UC] = {}, ps[UC];
+#pragma unroll
+      for (int q = 0; q < UC; ++q) {
+        const int j = lane + 32 * q;
+        ps[q] = 1.0;
+        if (j < P.nu) {
+          pv[q] = gld(yp_ + 32 * q);
+          if (apg) pp[q] = gld(ypp + 32 * q);
+          if (P.scaled) ps[q] = __ldg(pst + 32 * q);
+        }
+        if (j < P.nv) bb[q] = __ldg(bt + 32 * q);
+      }
+#pragma unroll
+      for (int q = 0; q < UC; ++q) {
+        const int j = lane + 32 * q;
+        if (j < P.NT1 * 8) SB[r * LDB + j] = bb[q];
+        if (j < P.NUP) {
+          double v = 0.0;
+          if (j < P.nu) {
+            const double wp = apg ? extrap(pv[q], pp[q], c) : pv[q];
+            v = P.scaled ? __dmul_rn(wp, ps[q]) : wp;
+          }
+          row[P.NXP + j] = v;
+        }
+      }
+    }
+  }
+}
+
+__device__ __noinline__ void fill_rows(const Params& P, int nu, int nrows) {
+  const int xc = (P.nx + 31) >> 5, uc = (P.nu + 31) >> 5;
+#define TSMPC_FILL(X, U) case (X) * 8 + (U): fill_rows_t<X, U>(P, nu, nrows); break;
+  switch (xc * 8 + uc) {
+    TSMPC_FILL(1, 1) TSMPC_FILL(1, 2) TSMPC_FILL(1, 3) TSMPC_FILL(1, 4)
+    TSMPC_FILL(2, 1) TSMPC_FILL(2, 2) TSMPC_FILL(2, 3) TSMPC_FILL(2, 4)
+    TSMPC_FILL(3, 1) TSMPC_FILL(3, 2) TSMPC_FILL(3, 3) TSMPC_FILL(3, 4)
+    TSMPC_FILL(4, 1) TSMPC_FILL(4, 2) TSMPC_FILL(4, 3) TSMPC_FILL(4, 4)
+    default: break;
+  }
+#undef TSMPC_FILL
+}
+
 // ---------------------------------------------------------------------------
 // backward sweep of one tile
 // ---------------------------------------------------------------------------
@@ -207,68 +306,8 @@ __device__ __noinline__ void bwd_tile(const Params& P, int tile, int nu) {
   const double c = apg ? P.coef[nu] : 0.0;
   const size_t zoff = (size_t)E * P.NXP, poff = 2 * (size_t)E * P.NXP;
 
-  // (1) operand rows [s | psi^]; a warp owns a row and issues all its loads first
-  for (int r = warp; r < nrows; r += kWarps) {
-    const int e = edge[r];
-    const int st = __ldg(P.edge_stage + e);
-    const double ds = stage_scale(P.sig_stage, st, P.scaled);
-    const double dz = stage_scale(P.zeta_stage, st, P.scaled);
-    // per-row base pointers (lane folded in) so every access is base + immediate
-    const double* ys = Y + (size_t)e * P.NXP + lane;
-    const double* yps = Yp + (size_t)e * P.NXP + lane;
-    const double* yp_ = Y + poff + (size_t)e * P.NUP + lane;
-    const double* ypp = Yp + poff + (size_t)e * P.NUP + lane;
-    const double* bt = P.beta + (size_t)e * P.NVP + lane;
-    const double* pst = P.psi_stage + (size_t)st * P.NUP + lane;
-    double a[kChunks] = {}, b[kChunks] = {}, g[kChunks] = {}, h[kChunks] = {};
-    double pv[kChunks] = {}, pp[kChunks] = {}, bb[kChunks] = {}, ps[kChunks] = {};
-#pragma unroll
-    for (int q = 0; q < kChunks; ++q) {
-      const int i = lane + 32 * q;
-      if (i < P.nx) {
-        a[q] = gld(ys + 32 * q);
-        g[q] = gld(ys + zoff + 32 * q);
-        if (apg) {
-          b[q] = gld(yps + 32 * q);
-          h[q] = gld(yps + zoff + 32 * q);
-        }
-      }
-      if (i < P.nu) {
-        pv[q] = gld(yp_ + 32 * q);
-        if (apg) pp[q] = gld(ypp + 32 * q);
-        ps[q] = P.scaled ? __ldg(pst + 32 * q) : 1.0;
-      }
-      if (i < P.nv) bb[q] = __ldg(bt + 32 * q);
-    }
-    // GEMM 1 accumulates onto its C tile: stage beta there (zero pad columns)
-#pragma unroll
-    for (int q = 0; q < kChunks; ++q) {
-      const int j = lane + 32 * q;
-      if (j < P.NT1 * 8) SB[r * LDB + j] = bb[q];
-    }
-    double* row = SA + r * LDA;
-#pragma unroll
-    for (int q = 0; q < kChunks; ++q) {
-      const int i = lane + 32 * q;
-      if (i < P.NXP) {
-        double v = 0.0;
-        if (i < P.nx) {
-          const double ws = apg ? extrap(a[q], b[q], c) : a[q];
-          const double wz = apg ? extrap(g[q], h[q], c) : g[q];
-          v = __dadd_rn(__dmul_rn(ws, ds), __dmul_rn(wz, dz));
-        }
-        row[i] = v;
-      }
-      if (i < P.NUP) {
-        double v = 0.0;
-        if (i < P.nu) {
-          const double wp = apg ? extrap(pv[q], pp[q], c) : pv[q];
-          v = P.scaled ? __dmul_rn(wp, ps[q]) : wp;
-        }
-        row[P.NXP + i] = v;
-      }
-    }
-  }
+  // (1) operand rows [s | psi^] + GEMM-1 bias beta (warp per row)
+  fill_rows(P, nu, nrows);
   __syncthreads();
   TSMPC_MARK(P, 0, tm_);
 

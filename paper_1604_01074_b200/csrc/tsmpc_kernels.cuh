@@ -28,7 +28,7 @@
 
 namespace tsmpc {
 
-constexpr int kThreads = 416;      // 13 warps: one warp per n-tile of GEMM 1 at n_v = 97
+constexpr int kThreads = 416;      // 13 warps (128 registers each); GEMM items = (n-tile, m-part)
 constexpr int kWarps = kThreads / 32;
 constexpr int kTileM = 96;         // edge rows per shared-memory tile (<= 12 m-tiles)
 constexpr int kMaxSeg = 32;        // longest segment (longer chains are split into levels)
