@@ -75,6 +75,13 @@ typedef struct tsmpc_problem {
   const int64_t* child_start;  /* n_nodes */
   const int64_t* child_stop;   /* n_nodes */
   const double* prob;          /* n_nodes */
+  /* optional block-structured kernel basis (precompute.structured_basis):
+   * Ls = L M spans ker(E) with Ls' Wu Ls = diag(lam_s).  When present, A is
+   * diagonal and every leaf chain fits a tile, tsmpc_solve runs the sparse
+   * persistent kernel; NULL -> dense fused-operator kernel only. */
+  const double* Ls;            /* n_u*n_v */
+  const double* lam_s;         /* n_v     */
+  const double* Ms;            /* n_v*n_v */
 } tsmpc_problem;
 
 /* Host buffers filled by tsmpc_solve; any pointer may be NULL to skip it. */
@@ -149,7 +156,14 @@ int tsmpc_plan_info(const tsmpc_plan* plan, int64_t* info, int32_t n_info);
  *         max_tiles_per_cta, max_trunk_path}. */
 int tsmpc_describe_tree(const tsmpc_problem* prob, int32_t max_ctas, int32_t collapse,
                         int64_t* info, int32_t n_info);
+/* Host-only planning of the sparse kernel: info = {ctas, tiles, chains,
+ * trunk_edges, resident_ctas, max_rows_per_cta, max_needs, smem_bytes}. */
+int tsmpc_describe_sparse(const tsmpc_problem* prob, int32_t max_ctas, int64_t smem_limit,
+                          int64_t* info, int32_t n_info);
 const char* tsmpc_last_error(void);
+/* Which persistent kernel tsmpc_solve runs: "sparse" (structured basis,
+ * tsmpc_sparse.cu) or "dense: <reason>" (fused-operator DMMA kernel). */
+const char* tsmpc_plan_path(const tsmpc_plan* plan);
 /* Phase cycle counters of CTA 0 (non-zero only in -DTSMPC_TIMERS builds); reset on read. */
 int tsmpc_debug_timers(tsmpc_plan* plan, uint64_t* out, int32_t n);
 int tsmpc_device_count(void);

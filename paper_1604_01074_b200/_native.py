@@ -20,7 +20,7 @@ from .errors import DeviceError, DimensionError, TreeSmpcError, ValidationError
 PKG_DIR = pathlib.Path(__file__).resolve().parent
 LIB_PATH = PKG_DIR / "libtsmpc.so"
 CSRC = PKG_DIR / "csrc"
-SOURCES = ["tsmpc_apg.cu", "tsmpc_aux.cu", "tsmpc_capi.cu"]
+SOURCES = ["tsmpc_apg.cu", "tsmpc_sparse.cu", "tsmpc_sparse_host.cu", "tsmpc_aux.cu", "tsmpc_capi.cu"]
 
 OK, ERR_DIMENSION, ERR_VALIDATION, ERR_CUDA, ERR_NCCL, ERR_ARGUMENT = 0, -1, -2, -3, -4, -5
 RECORD_RESIDUALS, SKIP_GAP, KEEP_DEVICE = 1, 2, 4
@@ -41,6 +41,7 @@ class Problem(ctypes.Structure):
         ("sig_stage", _dp), ("zeta_stage", _dp), ("psi_stage", _dp),
         ("stage_starts", _ip), ("anc", _ip), ("child_start", _ip), ("child_stop", _ip),
         ("prob", _dp),
+        ("Ls", _dp), ("lam_s", _dp), ("Ms", _dp),
     ]
 
 
@@ -70,6 +71,9 @@ SIGNATURES = {
     "tsmpc_dual_operator_step": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, _dp]),
     "tsmpc_plan_info": (ctypes.c_int, [ctypes.c_void_p, _ip, ctypes.c_int32]),
     "tsmpc_last_error": (ctypes.c_char_p, []),
+    "tsmpc_plan_path": (ctypes.c_char_p, [ctypes.c_void_p]),
+    "tsmpc_describe_sparse": (ctypes.c_int, [ctypes.POINTER(Problem), ctypes.c_int32, ctypes.c_int64,
+                                             _ip, ctypes.c_int32]),
     "tsmpc_device_count": (ctypes.c_int, []),
     "tsmpc_debug_timers": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64),
                                           ctypes.c_int32]),
@@ -96,7 +100,7 @@ def build_library(force: bool = False, verbose: bool = False, timers: bool = Fal
         if res.returncode != 0:
             raise DeviceError(f"nvcc failed:\n{res.stderr[-4000:]}")
         return out
-    deps = srcs + list(CSRC.glob("*.cuh")) + [PKG_DIR.parent / "include" / "tsmpc.h"]
+    deps = srcs + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [PKG_DIR.parent / "include" / "tsmpc.h"]
     if not force and LIB_PATH.exists():
         newest = max(p.stat().st_mtime for p in deps)
         if LIB_PATH.stat().st_mtime >= newest:

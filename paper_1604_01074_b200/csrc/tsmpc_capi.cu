@@ -10,6 +10,7 @@
 
 #include "../../include/tsmpc.h"
 #include "tsmpc_aux.cuh"
+#include "tsmpc_sparse_host.h"
 
 using namespace tsmpc;
 
@@ -68,6 +69,13 @@ struct tsmpc_plan {
   unsigned long long* TIMERS = nullptr;
   // compact scaling copies for tsmpc_prox
   double *sig_c = nullptr, *zeta_c = nullptr, *psi_c = nullptr;
+  // structured-basis kernel (tsmpc_sparse.cu); used by tsmpc_solve when available
+  bool use_sparse = false;
+  SParams sbase{};
+  int sp_ctas = 0, sp_resident = 0, sp_tiles = 0, sp_trunk = 0;
+  size_t sp_smem = 0;
+  double *BETA_S = nullptr, *TG = nullptr, *KY_S = nullptr, *MS = nullptr;
+  std::string sp_why;
   // plan stats
   int n_levels = 0, n_tiles = 0, n_segs = 0, n_ctas = 0, n_trunk = 0;
   int dyk_blocks = 0;
@@ -295,6 +303,13 @@ int grid_for(int E) {  // warp-per-edge helper kernels, 256 threads = 8 warps pe
 extern "C" {
 
 const char* tsmpc_last_error(void) { return g_err.c_str(); }
+
+const char* tsmpc_plan_path(const tsmpc_plan* pl) {
+  if (!pl) return "";
+  static thread_local std::string s;
+  s = pl->use_sparse ? "sparse" : ("dense: " + pl->sp_why);
+  return s.c_str();
+}
 
 int tsmpc_device_count(void) {
   int n = 0;
@@ -639,6 +654,57 @@ tsmpc_plan* tsmpc_plan_create(const tsmpc_problem* pb, int device) {
   c.EpinvT = d_EpinvT; c.jrhs = pl->JRHS; c.gdd = pl->GDD; c.B = d_B;
   c.a_diag = diag ? d_adiag : nullptr; c.A = d_A;
 
+  // ---- structured-basis (sparse) kernel plan
+  {
+    const char* force = getenv("TSMPC_FORCE_DENSE");
+    if (!diag) pl->sp_why = "A is not diagonal";
+    else if (!pb->Ls || !pb->lam_s || !pb->Ms) pl->sp_why = "no structured basis supplied";
+    else if (force && force[0] == '1') pl->sp_why = "disabled by TSMPC_FORCE_DENSE";
+    else {
+      SparseTreeIn ti{N, n_nodes, pb->stage_starts, pb->anc, pb->child_start, pb->child_stop, pb->prob};
+      SparseOpsIn oi{nx, nu, nv, pb->B, pb->Ls, pb->lam_s};
+      SparseHostPlan hp = plan_sparse(ti, oi, NXP, NUP, NVP, pl->sm_count, (size_t)prop.sharedMemPerBlockOptin);
+      int occ_s = 0;
+      if (hp.ok) {
+        if (cudaFuncSetAttribute(apg_sparse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hp.smem) !=
+            cudaSuccess) {
+          hp.ok = false;
+          hp.why = "cannot reserve shared memory for the sparse kernel";
+          cudaGetLastError();
+        } else {
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, apg_sparse_kernel, kThreadsS, hp.smem);
+          if (occ_s < 1) { hp.ok = false; hp.why = "sparse kernel does not fit on an SM"; }
+        }
+      }
+      if (hp.ok) {
+        int *d_meta, *d_mptr, *d_ts, *d_spi;
+        double* d_spv;
+        rc |= pl->upload(&d_meta, hp.meta.data(), hp.meta.size());
+        rc |= pl->upload(&d_mptr, hp.meta_ptr.data(), hp.meta_ptr.size());
+        rc |= pl->upload(&d_ts, hp.tsched.data(), hp.tsched.size());
+        rc |= pl->upload(&d_spi, hp.spi.data(), hp.spi.size());
+        rc |= pl->upload(&d_spv, hp.spv.data(), hp.spv.size());
+        rc |= pl->upload(&pl->MS, pb->Ms, (size_t)nv * nv);
+        rc |= pl->alloc(&pl->BETA_S, (size_t)E * NVP);
+        rc |= pl->alloc(&pl->TG, (size_t)E * NVP);
+        rc |= pl->alloc(&pl->KY_S, (size_t)std::max(1, hp.n_trunk) * P.KY_LD);
+        if (rc) return bail(0);
+        SParams& S = pl->sbase;
+        S = hp.S;
+        S.spi = d_spi; S.spv = d_spv; S.meta = d_meta; S.meta_ptr = d_mptr; S.tsched = d_ts;
+        S.beta_s = pl->BETA_S; S.TG = pl->TG;
+        pl->use_sparse = true;
+        pl->sp_ctas = hp.n_ctas;
+        pl->sp_smem = hp.smem;
+        pl->sp_resident = hp.resident_ctas;
+        pl->sp_tiles = hp.n_tiles;
+        pl->sp_trunk = hp.n_trunk;
+      } else {
+        pl->sp_why = hp.why;
+      }
+    }
+  }
+
   int occ_d = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_d, gap_project_dykstra_kernel, 256, 0);
   pl->dyk_blocks = std::max(1, std::min(occ_d, 4)) * pl->sm_count;
@@ -680,11 +746,29 @@ int tsmpc_describe_tree(const tsmpc_problem* pb, int32_t max_ctas, int32_t colla
   return TSMPC_OK;
 }
 
+int tsmpc_describe_sparse(const tsmpc_problem* pb, int32_t max_ctas, int64_t smem_limit, int64_t* info,
+                          int32_t n) {
+  if (!pb || !info || !pb->anc || !pb->child_start || !pb->child_stop || !pb->stage_starts || !pb->prob ||
+      !pb->B || !pb->Ls || !pb->lam_s)
+    return fail(TSMPC_ERR_ARGUMENT, "null argument");
+  SparseTreeIn ti{pb->N, pb->n_nodes, pb->stage_starts, pb->anc, pb->child_start, pb->child_stop, pb->prob};
+  SparseOpsIn oi{pb->n_x, pb->n_u, pb->n_v, pb->B, pb->Ls, pb->lam_s};
+  SparseHostPlan hp = plan_sparse(ti, oi, r4(pb->n_x), r4(pb->n_u), r4(pb->n_v), std::max(1, (int)max_ctas),
+                                  (size_t)smem_limit);
+  if (!hp.ok) return fail(TSMPC_ERR_VALIDATION, "%s", hp.why.c_str());
+  const int64_t vals[] = {hp.n_ctas, hp.n_tiles, hp.n_chains, hp.n_trunk, hp.resident_ctas, hp.max_rows,
+                          hp.max_needs, (int64_t)hp.smem};
+  for (int i = 0; i < n && i < (int)(sizeof(vals) / sizeof(vals[0])); ++i) info[i] = vals[i];
+  return TSMPC_OK;
+}
+
 int tsmpc_plan_info(const tsmpc_plan* pl, int64_t* info, int32_t n) {
   if (!pl || !info) return fail(TSMPC_ERR_ARGUMENT, "null argument");
-  const int64_t vals[] = {pl->n_levels, pl->n_ctas, pl->n_tiles, pl->n_segs, (int64_t)pl->smem,
-                          pl->base.diagA, kThreads, kTileM, pl->sm_count, pl->base.collapsed,
-                          pl->n_trunk};
+  const bool sp = pl->use_sparse;
+  const int64_t vals[] = {pl->n_levels, sp ? pl->sp_ctas : pl->n_ctas, sp ? pl->sp_tiles : pl->n_tiles,
+                          pl->n_segs, (int64_t)(sp ? pl->sp_smem : pl->smem), pl->base.diagA,
+                          sp ? kThreadsS : kThreads, sp ? kTileS : kTileM, pl->sm_count, pl->base.collapsed,
+                          sp ? pl->sp_trunk : pl->n_trunk, sp ? 1 : 0, pl->sp_resident};
   for (int i = 0; i < n && i < (int)(sizeof(vals) / sizeof(vals[0])); ++i) info[i] = vals[i];
   return TSMPC_OK;
 }
@@ -708,6 +792,11 @@ int tsmpc_set_cache(tsmpc_plan* pl, const double* beta, const double* uhat, cons
   rc |= pl->put_rows(pl->UHAT, pl->NUP, uhat, pl->nu, E);
   rc |= pl->put_rows(pl->EVEC, pl->NXP, evec, pl->nx, E);
   if (rc) return rc;
+  if (pl->use_sparse) {
+    beta_rotate_kernel<<<std::max(1, std::min((E + 7) / 8, 148 * 8)), 256, 0, pl->stream>>>(pl->BETA, pl->MS,
+                                                                                         pl->BETA_S, E, pl->nv, pl->NVP);
+    CU(cudaGetLastError());
+  }
   CU(cudaMemcpyAsync(pl->Q, q, sizeof(double) * pl->nu, cudaMemcpyHostToDevice, pl->stream));
   if (prices)
     CU(cudaMemcpyAsync(pl->PRICES, prices, sizeof(double) * pl->N * pl->nu, cudaMemcpyHostToDevice, pl->stream));
@@ -862,7 +951,18 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
   P.record_all = record ? 1 : 0;
   P.resid = pl->RESID;
   CU(cudaEventRecord(pl->ev0, pl->stream));
-  if (launch_apg(pl, P)) return TSMPC_ERR_CUDA;
+  if (pl->use_sparse) {
+    SParams S = pl->sbase;
+    S.P = P;
+    S.P.KY = pl->KY_S;
+    S.P.n_trunk = pl->sp_trunk;
+    void* args[] = {&S};
+    CU(cudaLaunchCooperativeKernel((void*)apg_sparse_kernel, dim3(pl->sp_ctas), dim3(kThreadsS), args, pl->sp_smem,
+                                   pl->stream));
+    ++pl->launches;
+  } else if (launch_apg(pl, P)) {
+    return TSMPC_ERR_CUDA;
+  }
   CU(cudaEventRecord(pl->ev1, pl->stream));
   double* yfin = ((iters & 1) == 0) ? pl->Y0 : pl->Y1;
   // keep the last iterate before the gap's solve step reuses X / U

@@ -95,6 +95,48 @@ struct Params {
   unsigned long long* timers;   // phase cycle counters of CTA 0 (TSMPC_TIMERS builds only)
 };
 
+// ---------------------------------------------------------------------------
+// Structured-basis ("sparse") persistent kernel, tsmpc_sparse.cu.  Used by
+// tsmpc_solve when A is diagonal, the plan carries the block-structured kernel
+// basis Ls (precompute.structured_basis: Ls' Wu Ls = diag) and every leaf chain
+// fits a tile of kTileS rows.  The factor step then needs no dense contraction:
+//   h  = Ls' (B' xiq + psi^)          (two sparse products)
+//   du = -Ls diag(lam)^-1 S           (one sparse product), bv = B du
+// so the loop is bound by memory latency/bandwidth, and each CTA keeps the dual,
+// ergodic and t rows of its chains resident in shared memory across iterations
+// when they fit (otherwise one tile slot is streamed with cp.async).
+// ---------------------------------------------------------------------------
+constexpr int kThreadsS = 512;
+constexpr int kWarpsS = kThreadsS / 32;
+constexpr int kTileS = 24;         // rows per chain tile (a leaf chain never spans tiles)
+
+struct SParams {
+  Params P;                     // dims, model vectors, scaling, tree, state, loop control, KY
+  // sparse operators (int pool + double pool, staged in shared memory)
+  const int* spi;
+  const double* spv;
+  int n_spi, n_spv;
+  int Bc_ptr, Bc_idx, Br_ptr, Br_idx, Lc_ptr, Lc_idx, Lr_ptr, Lr_idx;  // int-pool offsets
+  int Bc_val, Br_val, Lc_val, Lr_val;                                  // double-pool offsets
+  // per-CTA plan (ints): see tsmpc_sparse.cu "meta layout"
+  const int* meta;
+  const int* meta_ptr;          // n_ctas + 1
+  int meta_max;
+  // trunk schedule (ints, shared by all CTAs): see "trunk schedule layout"
+  const int* tsched;
+  int n_tsched;
+  // shared-memory layout, offsets in doubles from the dynamic base
+  int O_BND, O_SPV, O_NEED, O_WORK, O_SLOT, O_INT;
+  int n_work;                   // doubles in the work region
+  int need_ld;                  // NVP + NXP + NUP  ([S | x | u] of one needed trunk edge)
+  int need_max;
+  int YW;                       // 2 NXP + NUP      ([sig | zeta | psi] of one dual row)
+  int slot_ld;                  // 2 YW + NXP + NUP + NVP
+  int slot_rows;                // resident capacity of the slot region (rows)
+  const double* beta_s;         // E x NVP  beta in the structured basis (beta M)
+  double* TG;                   // E x NVP  t rows of streamed CTAs
+};
+
 // Phase timers (profiling builds: -DTSMPC_TIMERS).  Slot k accumulates the cycles
 // CTA 0 spends between consecutive marks.
 #ifdef TSMPC_TIMERS

@@ -1,0 +1,352 @@
+// tsmpc_sparse_host.cpp — host planner of the structured-basis kernel.
+//
+// Tree terms follow the reference's layout (tree.py:31-94): stage-major nodes,
+// edge e <-> node e+1, children of a node contiguous.  A *leaf chain* is a
+// maximal only-child path ending at a leaf; its first edge is the chain head,
+// whose parent node has != 1 children (or is the root).  Every other edge is a
+// *trunk* edge.  For the paper's trees (branching in stages <= 3, then one
+// chain per scenario) the chains carry ~99% of the edges.
+#include "tsmpc_sparse_host.h"
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <queue>
+#include <set>
+
+namespace tsmpc {
+
+namespace {
+
+void csr(int rows, int cols, const std::vector<double>& dense, bool by_col, std::vector<int>& ptr,
+         std::vector<int>& idx, std::vector<double>& val) {
+  // dense is rows x cols row-major; by_col -> compressed columns
+  const int outer = by_col ? cols : rows, inner = by_col ? rows : cols;
+  ptr.assign(outer + 1, 0);
+  idx.clear();
+  val.clear();
+  for (int o = 0; o < outer; ++o) {
+    for (int i = 0; i < inner; ++i) {
+      const double v = by_col ? dense[(size_t)i * cols + o] : dense[(size_t)o * cols + i];
+      if (v != 0.0) {
+        idx.push_back(i);
+        val.push_back(v);
+      }
+    }
+    ptr[o + 1] = (int)idx.size();
+  }
+}
+
+}  // namespace
+
+SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NXP, int NUP, int NVP,
+                           int max_ctas, size_t smem_limit) {
+  SparseHostPlan out;
+  const int n_nodes = t.n_nodes, E = n_nodes - 1, N = t.N;
+  const int nx = ops.nx, nu = ops.nu, nv = ops.nv;
+  std::vector<int> nch(n_nodes), stage_of_edge(E);
+  for (int n = 0; n < n_nodes; ++n) nch[n] = (int)(t.child_stop[n] - t.child_start[n]);
+  for (int j = 0; j < N; ++j)
+    for (int64_t n = t.stage_starts[j + 1]; n < t.stage_starts[j + 2]; ++n) stage_of_edge[n - 1] = j;
+
+  // ---- leaf chains and trunk
+  std::vector<std::vector<int>> chains;
+  std::vector<char> in_chain(E, 0);
+  for (int e = 0; e < E; ++e) {
+    const int pn = (int)t.anc[e + 1];
+    const bool head = pn == 0 || nch[pn] != 1;
+    if (!head) continue;
+    std::vector<int> path{e};
+    int x = e;
+    while (nch[x + 1] == 1) {
+      x = (int)t.child_start[x + 1] - 1;
+      path.push_back(x);
+    }
+    if (nch[x + 1] == 0) {
+      if ((int)path.size() > kTileS) {
+        out.why = "leaf chain longer than a tile (" + std::to_string(path.size()) + " edges)";
+        return out;
+      }
+      for (int c : path) in_chain[c] = 1;
+      chains.push_back(std::move(path));
+    }
+  }
+  std::vector<int> tpos(E, -1);
+  for (int e = 0; e < E; ++e)
+    if (!in_chain[e]) {
+      tpos[e] = (int)out.trunk_edge.size();
+      out.trunk_edge.push_back(e);
+    }
+  const int T = (int)out.trunk_edge.size();
+  out.n_trunk = T;
+  out.n_chains = (int)chains.size();
+  std::sort(chains.begin(), chains.end(), [](const auto& a, const auto& b) { return a[0] < b[0]; });
+
+  // ---- CTA count and chain assignment (contiguous, balanced by rows)
+  long long R = 0;
+  for (auto& ch : chains) R += (long long)ch.size();
+  int C = T > 0 ? max_ctas : std::max(1, std::min(max_ctas, (int)chains.size()));
+  if (T > 0) C = std::max(1, std::min(max_ctas, (int)chains.size() + T));
+  std::vector<std::vector<int>> cta_chains(C);
+  {
+    long long pre = 0;
+    for (int i = 0; i < (int)chains.size(); ++i) {
+      const long long mid2 = 2 * pre + (long long)chains[i].size();
+      int c = (int)((mid2 * C) / (2 * std::max<long long>(R, 1)));
+      c = std::min(std::max(c, 0), C - 1);
+      cta_chains[c].push_back(i);
+      pre += (long long)chains[i].size();
+    }
+  }
+  // trunk rows -> least-loaded CTAs (deterministic: load, then CTA index)
+  std::vector<std::vector<int>> cta_own(C);
+  {
+    using Item = std::pair<long long, int>;
+    std::priority_queue<Item, std::vector<Item>, std::greater<Item>> pq;
+    for (int c = 0; c < C; ++c) {
+      long long rows = 0;
+      for (int i : cta_chains[c]) rows += (long long)chains[i].size();
+      pq.push({rows, c});
+    }
+    for (int tp = 0; tp < T; ++tp) {
+      auto [load, c] = pq.top();
+      pq.pop();
+      cta_own[c].push_back(tp);
+      pq.push({load + 1, c});
+    }
+  }
+
+  // ---- trunk schedule
+  {
+    std::vector<int> lev_ptr;  // trunk positions grouped by edge stage (ascending)
+    int last_stage = -1;
+    for (int tp = 0; tp < T; ++tp) {
+      const int st = stage_of_edge[out.trunk_edge[tp]];
+      if (st != last_stage) {
+        lev_ptr.push_back(tp);
+        last_stage = st;
+      }
+    }
+    lev_ptr.push_back(T);
+    const int nlev = (int)lev_ptr.size() - 1;
+    std::vector<int> pos(8 * (size_t)T, 0), tch, hch;
+    for (int tp = 0; tp < T; ++tp) {
+      const int a = out.trunk_edge[tp], node = a + 1;
+      const int pa = (int)t.anc[node] - 1;
+      int* p = &pos[8 * (size_t)tp];
+      p[0] = a;
+      p[1] = stage_of_edge[a];
+      p[2] = pa >= 0 ? tpos[pa] : -1;
+      p[3] = (int)tch.size();
+      p[5] = (int)hch.size();
+      std::vector<int> hc;
+      for (int64_t ch = t.child_start[node] - 1; ch < t.child_stop[node] - 1; ++ch) {
+        if (tpos[ch] >= 0) tch.push_back(tpos[ch]);
+        else hch.push_back((int)ch);
+      }
+      p[4] = (int)tch.size() - p[3];
+      p[6] = (int)hch.size() - p[5];
+    }
+    out.tsched = {T, nlev, (int)tch.size(), (int)hch.size()};
+    if (T == 0) out.tsched[1] = 0;
+    if (T > 0) out.tsched.insert(out.tsched.end(), lev_ptr.begin(), lev_ptr.end());
+    else out.tsched.push_back(0);
+    out.tsched.insert(out.tsched.end(), pos.begin(), pos.end());
+    out.tsched.insert(out.tsched.end(), tch.begin(), tch.end());
+    out.tsched.insert(out.tsched.end(), hch.begin(), hch.end());
+  }
+
+  // ---- per-CTA meta
+  std::vector<int> depth(T, 0);
+  for (int tp = 0; tp < T; ++tp) {
+    int d = 0;
+    for (int e = out.trunk_edge[tp]; e >= 0; e = (int)t.anc[e + 1] - 1) ++d;
+    depth[tp] = d;
+  }
+  std::vector<int> cta_rows(C, 0), cta_needs(C, 0);
+  std::vector<std::vector<int>> metas(C);
+  int total_tiles = 0;
+  for (int c = 0; c < C; ++c) {
+    // tiles: consecutive chains packed up to kTileS rows
+    std::vector<std::vector<int>> tiles;
+    int fill = kTileS + 1;
+    for (int i : cta_chains[c]) {
+      const int len = (int)chains[i].size();
+      if (fill + len > kTileS) {
+        tiles.emplace_back();
+        fill = 0;
+      }
+      tiles.back().push_back(i);
+      fill += len;
+    }
+    // needs: trunk paths of the chain heads' parents and of own trunk rows
+    std::set<std::pair<int, int>> need_set;  // (depth, tp)
+    auto add_path = [&](int e) {
+      for (; e >= 0; e = (int)t.anc[e + 1] - 1) need_set.insert({depth[tpos[e]], tpos[e]});
+    };
+    for (int i : cta_chains[c]) {
+      const int pa = (int)t.anc[chains[i][0] + 1] - 1;
+      if (pa >= 0) add_path(pa);
+    }
+    for (int tp : cta_own[c]) add_path(out.trunk_edge[tp]);
+    std::vector<int> need_tp;
+    std::map<int, int> need_idx;
+    std::vector<int> lev{0};
+    int last_d = -1;
+    for (auto& [d, tp] : need_set) {
+      if (d != last_d && last_d >= 0) lev.push_back((int)need_tp.size());
+      last_d = d;
+      need_idx[tp] = (int)need_tp.size();
+      need_tp.push_back(tp);
+    }
+    lev.push_back((int)need_tp.size());
+    if (need_tp.empty()) lev = {0};
+    const int nlev = (int)lev.size() - 1;
+    int nrows = 0, nsegs = 0;
+    for (auto& tl : tiles)
+      for (int i : tl) nrows += (int)chains[i].size(), ++nsegs;
+    std::vector<int>& m = metas[c];
+    m = {(int)tiles.size(), nrows, nsegs, (int)need_tp.size(), nlev, (int)cta_own[c].size(), 0, 0};
+    std::vector<int> rows, segs;
+    int row = 0, seg = 0;
+    for (auto& tl : tiles) {
+      const int row0 = row, seg0 = seg;
+      int lo = 0;
+      for (int i : tl) {
+        const auto& ch = chains[i];
+        const int pa = (int)t.anc[ch[0] + 1] - 1;
+        segs.insert(segs.end(), {lo, lo + (int)ch.size(), pa >= 0 ? need_idx[tpos[pa]] : -1, 0});
+        for (int e : ch) {
+          const double inv2p = 1.0 / (2.0 * t.prob[e + 1]);
+          int w[2];
+          std::memcpy(w, &inv2p, sizeof(w));
+          rows.insert(rows.end(), {e, stage_of_edge[e], w[0], w[1]});
+        }
+        lo += (int)ch.size();
+        ++seg;
+      }
+      row += lo;
+      m.insert(m.end(), {row0, lo, seg0, (int)tl.size()});
+    }
+    m.insert(m.end(), rows.begin(), rows.end());
+    m.insert(m.end(), segs.begin(), segs.end());
+    for (int tp : need_tp) {
+      const int a = out.trunk_edge[tp], pa = (int)t.anc[a + 1] - 1;
+      m.insert(m.end(), {tp, pa >= 0 ? need_idx[tpos[pa]] : -1, a, stage_of_edge[a]});
+    }
+    m.insert(m.end(), lev.begin(), lev.end());
+    for (int tp : cta_own[c]) m.push_back(need_idx[tp]);
+    cta_rows[c] = nrows;
+    cta_needs[c] = (int)need_tp.size();
+    total_tiles += (int)tiles.size();
+  }
+  out.n_tiles = total_tiles;
+  out.n_ctas = C;
+
+  // ---- sparse operators
+  {
+    std::vector<double> Bd(ops.B, ops.B + (size_t)nx * nu), Lsd(ops.Ls, ops.Ls + (size_t)nu * nv),
+        Lt((size_t)nu * nv);
+    for (int j = 0; j < nu; ++j)
+      for (int k = 0; k < nv; ++k) {
+        const double l = Lsd[(size_t)j * nv + k];
+        Lt[(size_t)j * nv + k] = l == 0.0 ? 0.0 : -(l / ops.lam[k]);
+      }
+    std::vector<int> p1, i1, p2, i2, p3, i3, p4, i4;
+    std::vector<double> v1, v2, v3, v4;
+    csr(nx, nu, Bd, true, p1, i1, v1);    // B by column j
+    csr(nx, nu, Bd, false, p2, i2, v2);   // B by row i
+    csr(nu, nv, Lsd, true, p3, i3, v3);   // Ls by column k
+    csr(nu, nv, Lt, false, p4, i4, v4);   // Lt by row j
+    SParams& S = out.S;
+    auto put = [&](const std::vector<int>& v) { int o = (int)out.spi.size(); out.spi.insert(out.spi.end(), v.begin(), v.end()); return o; };
+    auto putv = [&](const std::vector<double>& v) { int o = (int)out.spv.size(); out.spv.insert(out.spv.end(), v.begin(), v.end()); return o; };
+    S.Bc_ptr = put(p1); S.Bc_idx = put(i1); S.Bc_val = putv(v1);
+    S.Br_ptr = put(p2); S.Br_idx = put(i2); S.Br_val = putv(v2);
+    S.Lc_ptr = put(p3); S.Lc_idx = put(i3); S.Lc_val = putv(v3);
+    S.Lr_ptr = put(p4); S.Lr_idx = put(i4); S.Lr_val = putv(v4);
+    S.n_spi = (int)out.spi.size();
+    S.n_spv = (int)out.spv.size();
+  }
+
+  // ---- shared-memory layout (doubles)
+  SParams& S = out.S;
+  const int need_max = *std::max_element(cta_needs.begin(), cta_needs.end());
+  int meta_max = 0;
+  out.meta_ptr.assign(C + 1, 0);
+  for (int c = 0; c < C; ++c) {
+    meta_max = std::max(meta_max, (int)metas[c].size());
+    out.meta_ptr[c + 1] = out.meta_ptr[c] + (int)metas[c].size();
+  }
+  S.YW = 2 * NXP + NUP;
+  S.slot_ld = 2 * S.YW + NXP + NUP + NVP;
+  S.need_ld = NVP + NXP + NUP;
+  S.need_max = need_max;
+  auto even = [](long long v) { return (v + 1) / 2 * 2; };
+  long long off = 0;
+  S.O_BND = 0;
+  off += even(4LL * NXP + 2LL * NUP);
+  S.O_SPV = (int)off;
+  off += even(S.n_spv);
+  S.O_NEED = (int)off;
+  off += (long long)need_max * S.need_ld;
+  S.O_WORK = (int)off;
+  const int ncomp = nv + nx + nu;
+  const int nc_max = (ncomp + C - 1) / C;
+  long long work = (long long)kTileS * (NXP + NUP + NVP);
+  work = std::max(work, 2LL * need_max * NUP);
+  work = std::max(work, 2LL * T * nc_max + ((long long)out.tsched.size() + 1) / 2 + 2);
+  work = std::max(work, (long long)S.slot_ld);  // one own trunk row at a time at least
+  S.n_work = (int)even(work);
+  off += S.n_work;
+  S.O_SLOT = (int)off;
+  const long long ints_d = ((long long)meta_max + S.n_spi + 1) / 2 + 1;
+  const long long limit_d = (long long)(smem_limit / sizeof(double));
+  const long long slot_avail = limit_d - off - ints_d;
+  // resident rows carry their t row (slot_ld); a streamed tile slot does not
+  const long long stream_ld = 2LL * S.YW + NXP + NUP;
+  const long long slot_rows = slot_avail / S.slot_ld;
+  if (slot_avail / stream_ld < kTileS) {
+    out.why = "shared memory too small for one tile slot";
+    return out;
+  }
+  int max_rows = 0;
+  for (int c = 0; c < C; ++c) max_rows = std::max(max_rows, cta_rows[c]);
+  // size the slot region for the largest resident CTA (or one tile when streaming)
+  long long want_rows = 0;
+  int resident = 0;
+  for (int c = 0; c < C; ++c)
+    if (cta_rows[c] <= slot_rows) want_rows = std::max<long long>(want_rows, cta_rows[c]);
+  if (want_rows == 0) {
+    S.slot_ld = (int)stream_ld;
+    want_rows = kTileS;
+  } else if (want_rows < kTileS) {
+    want_rows = std::min<long long>(kTileS, slot_rows);
+  }
+  if (want_rows < kTileS && want_rows * S.slot_ld < kTileS * stream_ld) {
+    out.why = "shared memory too small for one tile slot";
+    return out;
+  }
+  for (int c = 0; c < C; ++c) {
+    const bool res = cta_rows[c] <= want_rows;
+    metas[c][6] = res ? 1 : 0;
+    resident += res;
+  }
+  S.slot_rows = (int)want_rows;
+  off += want_rows * S.slot_ld;
+  S.O_INT = (int)off;
+  off += ints_d;
+  S.meta_max = meta_max;
+  out.smem = (size_t)off * sizeof(double);
+  out.meta.clear();
+  for (int c = 0; c < C; ++c) out.meta.insert(out.meta.end(), metas[c].begin(), metas[c].end());
+  S.n_tsched = (int)out.tsched.size();
+  out.resident_ctas = resident;
+  out.max_rows = max_rows;
+  out.max_needs = need_max;
+  out.ok = true;
+  return out;
+}
+
+}  // namespace tsmpc

@@ -1,0 +1,49 @@
+// tsmpc_sparse_host.h — host planner of the structured-basis kernel
+// (tsmpc_sparse.cu): chain tiles, CTA assignment, trunk schedule, shared-memory
+// layout.  Pure host code; tsmpc_capi.cu owns the device buffers.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "tsmpc_kernels.cuh"
+
+namespace tsmpc {
+
+struct SparseTreeIn {
+  int N, n_nodes;
+  const int64_t* stage_starts;  // N + 2
+  const int64_t* anc;           // n_nodes
+  const int64_t* child_start;   // n_nodes
+  const int64_t* child_stop;    // n_nodes
+  const double* prob;           // n_nodes
+};
+
+struct SparseOpsIn {
+  int nx, nu, nv;
+  const double* B;    // nx * nu
+  const double* Ls;   // nu * nv
+  const double* lam;  // nv
+};
+
+struct SparseHostPlan {
+  bool ok = false;
+  std::string why;                  // reason when !ok
+  int n_ctas = 0, n_chains = 0, n_trunk = 0, n_tiles = 0;
+  int resident_ctas = 0, max_rows = 0, max_needs = 0;
+  size_t smem = 0;
+  std::vector<int> meta, meta_ptr;  // per-CTA plans
+  std::vector<int> tsched;          // trunk schedule
+  std::vector<int> trunk_edge;      // trunk position -> edge
+  std::vector<int> spi;             // sparse index pool
+  std::vector<double> spv;          // sparse value pool
+  // filled layout / pool offsets (device pointers are set by the caller)
+  SParams S{};
+};
+
+// Build the plan.  smem_limit: opt-in shared memory per block (bytes);
+// max_ctas: SMs available for the cooperative launch.
+SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NXP, int NUP, int NVP,
+                           int max_ctas, size_t smem_limit);
+
+}  // namespace tsmpc

@@ -42,6 +42,16 @@ class DevicePlan:
             "child_start": _c(tree.child_start, np.int64),
             "child_stop": _c(tree.child_stop, np.int64), "prob": _c(tree.prob),
         }
+        self.structured = None
+        if np.count_nonzero(np.asarray(factor.A) - np.diag(np.diag(factor.A))) == 0:
+            try:
+                from .precompute import structured_basis
+                basis = _BasisView(factor.L)
+                sb = structured_basis(model, basis)
+                keep["Ls"], keep["lam_s"], keep["Ms"] = _c(sb.Ls), _c(sb.lam), _c(sb.M)
+                self.structured = sb
+            except Exception:  # no structured basis -> dense fused-operator kernel
+                self.structured = None
         if scaling is not None:
             keep["sig_stage"] = _c(scaling.sig_stage)
             keep["zeta_stage"] = _c(scaling.zeta_stage)
@@ -66,11 +76,13 @@ class DevicePlan:
 
     # -- introspection -------------------------------------------------------
     def info(self) -> dict:
-        buf = np.zeros(11, dtype=np.int64)
-        nat.check(self._lib.tsmpc_plan_info(self._h, nat.iptr(buf), 11), "tsmpc_plan_info")
         keys = ("levels", "ctas", "tiles", "segments", "smem_bytes", "diag_A", "threads",
-                "tile_rows", "sms", "collapsed", "trunk_edges")
-        return dict(zip(keys, (int(v) for v in buf)))
+                "tile_rows", "sms", "collapsed", "trunk_edges", "sparse", "resident_ctas")
+        buf = np.zeros(len(keys), dtype=np.int64)
+        nat.check(self._lib.tsmpc_plan_info(self._h, nat.iptr(buf), len(keys)), "tsmpc_plan_info")
+        d = dict(zip(keys, (int(v) for v in buf)))
+        d["path"] = self._lib.tsmpc_plan_path(self._h).decode()
+        return d
 
     def debug_timers(self) -> np.ndarray:
         """Phase cycle counters of CTA 0 since the last call (timer builds only)."""
@@ -164,6 +176,14 @@ class DevicePlan:
         return v[0].value, v[1].value, v[2].value
 
 
+class _BasisView:
+    """The slice of EliminationBasis that structured_basis reads."""
+
+    def __init__(self, L):
+        self.L = np.asarray(L)
+        self.n_v = self.L.shape[1]
+
+
 _PLANS: dict = {}
 _MAX_PLANS = 6
 
@@ -188,6 +208,28 @@ def describe_tree(tree, max_ctas: int = 148, collapse: bool = True) -> dict:
                                       nat.iptr(buf), 9), "tsmpc_describe_tree")
     keys = ("levels", "ctas", "tiles", "segments", "rows", "trunk_edges", "max_rows_per_cta",
             "max_tiles_per_cta", "max_trunk_path")
+    return dict(zip(keys, (int(v) for v in buf)))
+
+
+def describe_sparse(model, tree, factor, max_ctas: int = 148, smem_limit: int = 232448) -> dict:
+    """Host-only view of the structured-basis kernel plan (no GPU needed)."""
+    from .precompute import structured_basis
+    lib = nat.load_library()
+    sb = structured_basis(model, _BasisView(factor.L))
+    keep = {"stage_starts": _c(tree.stage_starts, np.int64), "anc": _c(tree.anc, np.int64),
+            "child_start": _c(tree.child_start, np.int64),
+            "child_stop": _c(tree.child_stop, np.int64), "prob": _c(tree.prob),
+            "B": _c(model.B), "Ls": _c(sb.Ls), "lam_s": _c(sb.lam)}
+    pb = nat.Problem()
+    pb.n_x, pb.n_u, pb.n_v = factor.n_x, factor.n_u, factor.n_v
+    pb.N, pb.n_nodes = int(tree.N), int(tree.n_nodes)
+    for name, arr in keep.items():
+        setattr(pb, name, nat.iptr(arr) if arr.dtype == np.int64 else nat.dptr(arr))
+    keys = ("ctas", "tiles", "chains", "trunk_edges", "resident_ctas", "max_rows", "max_needs",
+            "smem_bytes")
+    buf = np.zeros(len(keys), dtype=np.int64)
+    nat.check(lib.tsmpc_describe_sparse(ctypes.byref(pb), int(max_ctas), int(smem_limit),
+                                        nat.iptr(buf), len(keys)), "tsmpc_describe_sparse")
     return dict(zip(keys, (int(v) for v in buf)))
 
 

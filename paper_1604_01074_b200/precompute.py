@@ -30,7 +30,8 @@ from .errors import DimensionError, ValidationError
 __all__ = ["EliminationBasis", "StageCache", "FactorCache", "DualScaling",
            "compute_basis", "particular_solution", "build_stage_cache",
            "lift_controls", "factor_step", "compute_preconditioner",
-           "dual_hessian_row_sums", "theta_update", "theta_schedule"]
+           "dual_hessian_row_sums", "theta_update", "theta_schedule",
+           "StructuredBasis", "structured_basis"]
 
 
 @dataclass(frozen=True)
@@ -176,6 +177,92 @@ def factor_step(basis, model) -> FactorCache:
     for arr in (Bbar, Phi, Psi):
         arr.setflags(write=False)
     return FactorCache(Bbar=Bbar, Phi=Phi, Psi=Psi, Rbar_chol=chol, A=model.A, L=basis.L)
+
+
+# -- block-structured elimination basis (device fast path) ------------------------
+
+@dataclass(frozen=True)
+class StructuredBasis:
+    """A second orthonormal basis ``Ls`` of ker(E) in which ``Ls' Wu Ls`` is diagonal.
+
+    Flows couple when they share a junction row of E or an off-diagonal entry of
+    Wu.  Each connected component of that graph gets its own orthonormal kernel
+    basis, rotated by the eigenvectors of its reduced weight block.  Hence Ls is
+    block-sparse (for a water network: identity columns for junction-free flows,
+    3 x 2 blocks for a junction with three flows) and ``Rbar_s = Ls' Wu Ls =
+    diag(lam)``.  ``Ls = L M`` with ``M = L' Ls`` orthogonal, so reduced
+    coordinates map as ``v = M v_s`` and ``beta_s = M' beta``.  The exact
+    minimiser of the solve step (``factor.py:142-170``) does not depend on the
+    basis of ker(E); the device uses this one so that the factor step becomes
+    sparse (``Rbar_s^{-1}`` diagonal, two sparse products per sweep).
+    """
+
+    Ls: np.ndarray    # (n_u, n_v)
+    lam: np.ndarray   # (n_v,) diagonal of Ls' Wu Ls
+    M: np.ndarray     # (n_v, n_v) = L' Ls (orthogonal)
+    blocks: int       # connected components
+    nnz: int          # structural non-zeros of Ls
+
+
+def structured_basis(model, basis) -> StructuredBasis:
+    E = np.asarray(model.E, dtype=float)
+    Wu = np.asarray(model.Wu, dtype=float)
+    n_e, n_u = E.shape
+    parent = list(range(n_u))
+
+    def find(a):
+        while parent[a] != a:
+            parent[a] = parent[parent[a]]
+            a = parent[a]
+        return a
+
+    def union(a, b):
+        ra, rb = find(a), find(b)
+        if ra != rb:
+            parent[max(ra, rb)] = min(ra, rb)
+
+    for row in E:
+        nz = np.flatnonzero(row)
+        for j in nz[1:]:
+            union(int(nz[0]), int(j))
+    ii, jj = np.nonzero(Wu)
+    for a, b in zip(ii, jj):
+        if a != b:
+            union(int(a), int(b))
+    comps: dict[int, list[int]] = {}
+    for j in range(n_u):
+        comps.setdefault(find(j), []).append(j)
+    cols, lams = [], []
+    for root in sorted(comps):
+        F = comps[root]
+        rows = [r for r in range(n_e) if np.any(E[r, F] != 0.0)]
+        if rows:
+            Ec = E[np.ix_(rows, F)]
+            _, s, vt = np.linalg.svd(Ec)
+            rank = int(np.sum(s > max(Ec.shape) * np.finfo(float).eps * s[0]))
+            K = vt[rank:].T
+        else:
+            K = np.eye(len(F))
+        if K.shape[1] == 0:
+            continue
+        Rc = K.T @ Wu[np.ix_(F, F)] @ K
+        w, Q = np.linalg.eigh(0.5 * (Rc + Rc.T))
+        Kc = K @ Q
+        for c in range(Kc.shape[1]):
+            col = np.zeros(n_u)
+            col[F] = Kc[:, c]
+            cols.append(col)
+            lams.append(w[c])
+    Ls = np.array(cols).T if cols else np.zeros((n_u, 0))
+    if Ls.shape[1] != basis.n_v:
+        raise ValidationError(f"structured kernel basis has {Ls.shape[1]} columns, expected {basis.n_v}")
+    lam = np.array(lams)
+    if not (lam > 0).all():
+        raise ValidationError("reduced weight matrix not positive definite")
+    M = basis.L.T @ Ls
+    nnz = int(sum(len(c) * len(c) for c in comps.values()))
+    return StructuredBasis(Ls=Ls, lam=lam, M=M, blocks=len(comps),
+                           nnz=int(np.count_nonzero(Ls)) if nnz else 0)
 
 
 # -- dual preconditioner ---------------------------------------------------------

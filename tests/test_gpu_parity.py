@@ -38,11 +38,18 @@ def test_solve_step_matches_reference(name):
     assert rel_err(out.u, z["s_u"]) <= 1e-11
 
 
+@pytest.mark.parametrize("path", ["sparse", "dense"])
 @pytest.mark.parametrize("name", ALL_CASES)
-def test_apg_solve_matches_reference(name):
+def test_apg_solve_matches_reference(name, path, monkeypatch):
+    """Both persistent kernels: the structured-basis sparse kernel (default when A
+    is diagonal) and the dense fused-operator DMMA kernel (TSMPC_FORCE_DENSE)."""
     c = load_case(name)
     z = c.z
+    monkeypatch.setenv("TSMPC_FORCE_DENSE", "1" if path == "dense" else "0")
     plan = _plan(c)
+    info = plan.info()
+    diag = np.count_nonzero(c.model.A - np.diag(np.diag(c.model.A))) == 0
+    assert info["sparse"] == (1 if (path == "sparse" and diag) else 0), info["path"]
     th, cf = engine.theta_schedule(c.iters)
     out = plan.solve(c.p, c.iters, c.lam, theta=th, coef=cf)
     for f in ("u0", "x", "u", "x_avg", "u_avg"):
