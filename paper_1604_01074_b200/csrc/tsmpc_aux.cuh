@@ -53,7 +53,9 @@ __global__ void gap_propagate_stage_kernel(EdgeCtx c, int n0, int n1, double* xf
 __global__ void gap_primal_terms_kernel(EdgeCtx c, const double* uf, const double* xf, double* cols);
 
 __global__ void apg_persistent_kernel(const __grid_constant__ Params P);
-__global__ void apg_sparse_kernel(const __grid_constant__ SParams S);
+__global__ void apg_sparse_kernel();
+// copies S to the kernel's constant parameter block and launches (cooperative)
+cudaError_t sparse_launch(const SParams& S, int ctas, size_t smem, cudaStream_t stream);
 __global__ void beta_rotate_kernel(const double* __restrict__ beta, const double* __restrict__ M, double* out,
                                    int E, int nv, int NVP);
 

@@ -956,9 +956,7 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
     S.P = P;
     S.P.KY = pl->KY_S;
     S.P.n_trunk = pl->sp_trunk;
-    void* args[] = {&S};
-    CU(cudaLaunchCooperativeKernel((void*)apg_sparse_kernel, dim3(pl->sp_ctas), dim3(kThreadsS), args, pl->sp_smem,
-                                   pl->stream));
+    CU(sparse_launch(S, pl->sp_ctas, pl->sp_smem, pl->stream));
     ++pl->launches;
   } else if (launch_apg(pl, P)) {
     return TSMPC_ERR_CUDA;

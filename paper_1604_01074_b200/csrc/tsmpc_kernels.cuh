@@ -126,7 +126,7 @@ struct SParams {
   const int* tsched;
   int n_tsched;
   // shared-memory layout, offsets in doubles from the dynamic base
-  int O_BND, O_SPV, O_NEED, O_WORK, O_SLOT, O_INT;
+  int O_BND, O_SCL, O_RED, O_SPV, O_NEED, O_WORK, O_SLOT, O_INT;
   int n_work;                   // doubles in the work region
   int need_ld;                  // NVP + NXP + NUP  ([S | x | u] of one needed trunk edge)
   int need_max;

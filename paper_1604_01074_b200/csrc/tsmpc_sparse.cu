@@ -42,6 +42,11 @@ namespace tsmpc {
 
 extern __shared__ __align__(16) double s_dyn[];
 
+// The launch parameters live in constant memory (set by sparse_launch on the
+// launching stream): every field access is a uniform constant-bank load that
+// the compiler may hoist freely, also inside the __noinline__ phase functions.
+__constant__ SParams g_sp;
+
 namespace {
 
 // ---- meta layout (ints, per CTA) -------------------------------------------
@@ -93,50 +98,121 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+
+// Element phases map threads component-major: thread = (row group g, component
+// k), g = tid / kKW, rows r = g, g + kGroups, ...  The per-component sparse
+// column range is read once per phase; no integer divisions.  Phase functions
+// are __noinline__ and rebuild their context from the __grid_constant__
+// parameters (the whole loop body stays within the instruction cache).
+constexpr int kKW = 128;                    // component lanes per row group (n_x, n_u <= 128)
+constexpr int kGroups = kThreadsS / kKW;    // 4 row groups
+constexpr int kRowsPT = kTileS / kGroups;   // rows per thread in a full tile
+
 struct Ctx {
   const SParams* S;
   const Params* P;
   Meta mt;
-  double* bnd;     // x_s, x_min, x_max (NXP each), u_min, u_max (NUP each)
+  double* bnd;     // x_s, x_min, x_max (NXP), u_min, u_max (NUP), a_diag (NXP), p (NXP)
+  double* scl;     // sig, zeta, 1/sig, 1/zeta per stage (N each)
+  double* red;     // epilogue partial norms, then row descriptors
   const int* spi;  // sparse index pool (shared)
   const double* spv;
   double* need;    // need rows [S | x | u]
   double* work;    // XI | Z | H  (backward),  XB | DU | H=S  (forward)
   double* slot;
-  int NXP, NUP, NVP, YW, SL;
+  int NXP, NUP, NVP, YW, SL, N;
   int nx, nu, nv, E;
   __device__ double* XI() const { return work; }
   __device__ double* Z() const { return work + kTileS * NXP; }
   __device__ double* H() const { return work + kTileS * (NXP + NUP); }
+  __device__ const double* adiag() const { return bnd + 3 * NXP + 2 * NUP; }
+  __device__ const double* proot() const { return bnd + 4 * NXP + 2 * NUP; }
+  __device__ int* rdesc() const { return reinterpret_cast<int*>(red + kGroups * kRowsPT * 8); }
 };
+
+__device__ __forceinline__ Ctx ctx_of() {
+  const SParams& S = g_sp;
+  const Params& P = S.P;
+  Ctx c;
+  c.S = &S;
+  c.P = &P;
+  c.NXP = P.NXP; c.NUP = P.NUP; c.NVP = P.NVP;
+  c.YW = S.YW; c.SL = S.slot_ld; c.N = P.N;
+  c.nx = P.nx; c.nu = P.nu; c.nv = P.nv; c.E = P.n_edges;
+  c.bnd = s_dyn + S.O_BND;
+  c.scl = s_dyn + S.O_SCL;
+  c.red = s_dyn + S.O_RED;
+  c.need = s_dyn + S.O_NEED;
+  c.work = s_dyn + S.O_WORK;
+  c.slot = s_dyn + S.O_SLOT;
+  const int* ints = reinterpret_cast<const int*>(s_dyn + S.O_INT);
+  c.mt.bind(ints);
+  c.spi = ints + S.meta_max;
+  c.spv = s_dyn + S.O_SPV;
+  return c;
+}
+
+// One compressed column (or row) of an operator; its first kNZ entries are
+// row-invariant and held in registers for the whole phase.
+constexpr int kNZ = 4;
+struct SpCol {
+  int q0, q1;
+  int idx[kNZ];
+  double val[kNZ];
+};
+__device__ __forceinline__ SpCol sp_col(const Ctx& c, int ptr_off, int idx_off, int val_off, int k) {
+  SpCol s;
+  s.q0 = c.spi[ptr_off + k];
+  s.q1 = c.spi[ptr_off + k + 1];
+#pragma unroll
+  for (int m = 0; m < kNZ; ++m) {
+    const bool v = s.q0 + m < s.q1;
+    s.idx[m] = v ? c.spi[idx_off + s.q0 + m] : 0;
+    s.val[m] = v ? c.spv[val_off + s.q0 + m] : 0.0;
+  }
+  return s;
+}
+// acc + sum_q val_q * row[idx_q], q ascending (fixed order)
+__device__ __forceinline__ double sp_dot(const Ctx& c, const SpCol& s, int idx_off, int val_off,
+                                         const double* row, double acc) {
+#pragma unroll
+  for (int m = 0; m < kNZ; ++m)
+    if (s.q0 + m < s.q1) acc = fma(s.val[m], row[s.idx[m]], acc);
+#pragma unroll 1
+  for (int q = s.q0 + kNZ; q < s.q1; ++q) acc = fma(c.spv[val_off + q], row[c.spi[idx_off + q]], acc);
+  return acc;
+}
 
 // slot row pointers: Y0 | Y1 | XA | UA | T
 __device__ __forceinline__ double* slot_row(const Ctx& c, int srow) { return c.slot + (size_t)srow * c.SL; }
 
-// Issue cp.async copies of one tile's slot rows.  parts: 1 = both dual rows,
+// Issue cp.async copies of rows into slot-format smem rows.  Row r of the batch
+// is edge edge_of(r) -> smem row dst + r * SL.  parts: 1 = both dual rows,
 // 2 = ergodic rows.  ysm = smem dual index that receives HBM slot `cur`.
-__device__ void load_slot(const Ctx& c, int row0, int nrows, int srow0, int parts, int cur, int ysm) {
-  const Params& P = *c.P;
+__device__ __noinline__ void load_rows(const int* edges, int estride, int nrows, double* dst,
+                                       int parts, int cur, int ysm) {
+  const SParams& S = g_sp;
+  const Ctx c = ctx_of();
+  const Params& P = S.P;
   const int hx = c.NXP / 2, hu = c.NUP / 2;
   const int per_y = 2 * hx + hu;               // 16-byte chunks of one dual row
   const int nch = ((parts & 1) ? 2 * per_y : 0) + ((parts & 2) ? hx + hu : 0);
   const size_t E = (size_t)c.E;
+  #pragma unroll 1
   for (int idx = threadIdx.x; idx < nrows * nch; idx += kThreadsS) {
     const int r = idx / nch;
     int k = idx - r * nch;
-    const int e = c.mt.edge(row0 + r);
-    double* srow = slot_row(c, srow0 + r);
+    const int e = edges[r * estride];
+    double* srow = dst + (size_t)r * c.SL;
     if (parts & 1) {
       if (k < 2 * per_y) {
         const int which = k < per_y ? 0 : 1;     // 0: HBM slot cur, 1: cur ^ 1
         const int kk = k - which * per_y;
         const double* Y = P.ybuf[cur ^ which];
-        double* dst = srow + (size_t)(ysm ^ which) * c.YW;
-        const double* src;
-        if (kk < hx) src = Y + (size_t)e * c.NXP + 2 * kk, dst += 2 * kk;
-        else if (kk < 2 * hx) src = Y + E * c.NXP + (size_t)e * c.NXP + 2 * (kk - hx), dst += c.NXP + 2 * (kk - hx);
-        else src = Y + 2 * E * c.NXP + (size_t)e * c.NUP + 2 * (kk - 2 * hx), dst += 2 * c.NXP + 2 * (kk - 2 * hx);
-        cp16(dst, src);
+        double* d = srow + (size_t)(ysm ^ which) * c.YW;
+        if (kk < hx) cp16(d + 2 * kk, Y + (size_t)e * c.NXP + 2 * kk);
+        else if (kk < 2 * hx) cp16(d + c.NXP + 2 * (kk - hx), Y + E * c.NXP + (size_t)e * c.NXP + 2 * (kk - hx));
+        else cp16(d + 2 * c.NXP + 2 * (kk - 2 * hx), Y + 2 * E * c.NXP + (size_t)e * c.NUP + 2 * (kk - 2 * hx));
         continue;
       }
       k -= 2 * per_y;
@@ -149,19 +225,23 @@ __device__ void load_slot(const Ctx& c, int row0, int nrows, int srow0, int part
 
 // ----------------------------------------------------------------------------
 // epilogue: prox_g (engine.py:146-183), dual update, ergodic averages, residual
-// (engine.py:546-575) for nrows rows.  Row r: edge ge(r), stage gs(r); x at
-// xrow(r), u at urow(r), dual rows (y at index ysm, y_prev at ysm ^ 1) and
-// ergodic rows in the slot-format row srow(r).  y+ replaces y_prev in place.
-// wt: also write y+ and the ergodic rows to HBM (slot `ncur` receives y+).
+// (engine.py:546-575) for nrows <= kTileS rows described by c.rdesc():
+// {edge, stage, x offset, u offset, slot-row offset} (offsets in doubles from
+// the dynamic shared-memory base).  Dual rows: y at index ysm, y_prev at ysm ^ 1;
+// y+ replaces y_prev in place.  wt: also write y+ and the ergodic rows to HBM
+// (slot `ncur` receives y+).  The two weighted-distance prox blocks need a norm
+// over the n_x components: per-warp shuffle sums combined across the group's
+// warps in a fixed order.
 // ----------------------------------------------------------------------------
-template <class EdgeOf, class StageOf, class XOf, class UOf, class SOf>
-__device__ void epilogue(const Ctx& c, int nu_it, int nrows, EdgeOf ge, StageOf gs, XOf xrow, UOf urow,
-                         SOf srow, int ysm, bool wt, int ncur, double& rmax) {
-  const Params& P = *c.P;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+__device__ __noinline__ void epilogue(int nu_it, double cf, double th, int nrows, int ysm,
+                                      bool wt, int ncur, double* rmax_io) {
+  const SParams& S = g_sp;
+  const Ctx c = ctx_of();
+  const Params& P = S.P;
+  const int k = threadIdx.x & (kKW - 1), g = threadIdx.x / kKW, lane = threadIdx.x & 31, w4 = k >> 5;
   const bool last = nu_it == P.iters - 1;
   const bool want = last || P.record_all;
-  const double cf = P.coef[nu_it], th = P.theta[nu_it], om = __dsub_rn(1.0, th);
+  const double om = __dsub_rn(1.0, th);
   const double lam = P.lam, ilam = P.inv_lam, lam_p = 1.0 / lam;
   const size_t E = (size_t)c.E;
   double* Yn = P.ybuf[ncur];
@@ -170,155 +250,186 @@ __device__ void epilogue(const Ctx& c, int nu_it, int nrows, EdgeOf ge, StageOf 
   const double* xmx_s = c.bnd + 2 * c.NXP;
   const double* umn_s = c.bnd + 3 * c.NXP;
   const double* umx_s = c.bnd + 3 * c.NXP + c.NUP;
-  // --- state copies: warp per row, two weighted-distance prox blocks
-  for (int r = warp; r < nrows; r += kWarpsS) {
-    const int e = ge(r), st = gs(r);
-    double* row = srow(r);
+  const int N = c.N;
+  const bool xk = k < c.nx, uk = k < c.nu;
+  const int* rd = c.rdesc();
+  double* red = c.red + (size_t)g * kRowsPT * 8;
+  double rmax = *rmax_io;
+  // psi scaling of this thread's component for its rows (all loads in flight at once)
+  double dpv[kRowsPT];
+#pragma unroll
+  for (int m = 0; m < kRowsPT; ++m) {
+    const int r = g + kGroups * m;
+    dpv[m] = 1.0;
+    if (P.scaled && uk && r < nrows) dpv[m] = __ldg(P.psi_stage + (size_t)rd[5 * r + 1] * c.NUP + k);
+  }
+  // pass 1: psi block (complete) and the partial squared distances of the state blocks
+  double ssv[kRowsPT], szv[kRowsPT];
+#pragma unroll
+  for (int m = 0; m < kRowsPT; ++m) {
+    const int r = g + kGroups * m;
+    ssv[m] = szv[m] = 0.0;
+    if (r >= nrows) continue;
+    const int* d = rd + 5 * r;
+    const int e = d[0], st = d[1];
+    double* row = s_dyn + d[4];
     double* yc = row + (size_t)ysm * c.YW;
     double* yp = row + (size_t)(ysm ^ 1) * c.YW;
-    double* xa = row + 2 * c.YW;
-    const double* x = xrow(r);
-    const double ds = P.scaled ? __ldg(P.sig_stage + st) : 1.0;
-    const double dz = P.scaled ? __ldg(P.zeta_stage + st) : 1.0;
-    const double rds = P.scaled ? __ldg(P.sig_rcp + st) : 1.0;
-    const double rdz = P.scaled ? __ldg(P.zeta_rcp + st) : 1.0;
-    double ts[4], tz[4], ws[4], wz[4];
-    double ss = 0.0, sz = 0.0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int i = lane + 32 * q;
-      ts[q] = tz[q] = ws[q] = wz[q] = 0.0;
-      if (i < c.nx) {
-        ws[q] = extrap(yc[i], yp[i], cf);
-        wz[q] = extrap(yc[c.NXP + i], yp[c.NXP + i], cf);
-        const double xi = x[i];
-        ts[q] = __dadd_rn(__dmul_rn(ws[q], ilam), __dmul_rn(xi, ds));
-        tz[q] = __dadd_rn(__dmul_rn(wz[q], ilam), __dmul_rn(xi, dz));
-        const double ps = fmax(ts[q], __dmul_rn(ds, xs_s[i]));
-        const double pz = fmin(fmax(tz[q], __dmul_rn(dz, xmn_s[i])), __dmul_rn(dz, xmx_s[i]));
-        const double gs_ = __dsub_rn(ps, ts[q]), gz = __dsub_rn(pz, tz[q]);
-        ss = fma(gs_, gs_, ss);
-        sz = fma(gz, gz, sz);
-      }
+    if (xk) {
+      const double ds = c.scl[st], dz = c.scl[N + st];
+      const double ws = extrap(yc[k], yp[k], cf);
+      const double wz = extrap(yc[c.NXP + k], yp[c.NXP + k], cf);
+      const double xi = s_dyn[d[2] + k];
+      const double ts = __dadd_rn(__dmul_rn(ws, ilam), __dmul_rn(xi, ds));
+      const double tz = __dadd_rn(__dmul_rn(wz, ilam), __dmul_rn(xi, dz));
+      const double gs_ = __dsub_rn(fmax(ts, __dmul_rn(ds, xs_s[k])), ts);
+      const double gz = __dsub_rn(fmin(fmax(tz, __dmul_rn(dz, xmn_s[k])), __dmul_rn(dz, xmx_s[k])), tz);
+      ssv[m] = __dmul_rn(gs_, gs_);
+      szv[m] = __dmul_rn(gz, gz);
     }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      ss += __shfl_xor_sync(0xffffffffu, ss, off);
-      sz += __shfl_xor_sync(0xffffffffu, sz, off);
-    }
-    const double dist_s = sqrt(ss), dist_z = sqrt(sz);
-    const double wgt_s = __dmul_rn(__dmul_rn(lam_p, P.Wx), rds);
-    const double wgt_z = __dmul_rn(__dmul_rn(lam_p, P.gamma_d), rdz);
-    const double fs = dist_s > wgt_s ? __ddiv_rn(wgt_s, dist_s) : 1.0;
-    const double fz = dist_z > wgt_z ? __ddiv_rn(wgt_z, dist_z) : 1.0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int i = lane + 32 * q;
-      if (i < c.nx) {
-        const double xi = x[i];
-        const double hs = __dmul_rn(xi, ds), hz = __dmul_rn(xi, dz);
-        const double ps = fmax(ts[q], __dmul_rn(ds, xs_s[i]));
-        const double pz = fmin(fmax(tz[q], __dmul_rn(dz, xmn_s[i])), __dmul_rn(dz, xmx_s[i]));
-        const double t_s = __dadd_rn(ts[q], __dmul_rn(fs, __dsub_rn(ps, ts[q])));
-        const double t_z = __dadd_rn(tz[q], __dmul_rn(fz, __dsub_rn(pz, tz[q])));
-        const double ns = __dadd_rn(ws[q], __dmul_rn(lam, __dsub_rn(hs, t_s)));
-        const double nz = __dadd_rn(wz[q], __dmul_rn(lam, __dsub_rn(hz, t_z)));
-        yp[i] = ns;
-        yp[c.NXP + i] = nz;
-        if (want) {
-          rmax = fmax(rmax, fabs(__dsub_rn(xi, __dmul_rn(t_s, rds))));
-          rmax = fmax(rmax, fabs(__dsub_rn(xi, __dmul_rn(t_z, rdz))));
-        }
-        const double na = __dadd_rn(__dmul_rn(xa[i], om), __dmul_rn(th, xi));
-        xa[i] = na;
-        if (wt) {
-          stcg(Yn + (size_t)e * c.NXP + i, ns);
-          stcg(Yn + E * c.NXP + (size_t)e * c.NXP + i, nz);
-          stcg(P.xavg + (size_t)(e + 1) * c.NXP + i, na);
-        }
-        if (last) stcg(P.X + (size_t)(e + 1) * c.NXP + i, xi);
+    if (uk) {
+      const double u = s_dyn[d[3] + k];
+      const double dp = dpv[m];
+      const double w = extrap(yc[2 * c.NXP + k], yp[2 * c.NXP + k], cf);
+      const double hp = __dmul_rn(u, dp);
+      const double a = __dadd_rn(__dmul_rn(w, ilam), hp);
+      const double t = fmin(fmax(a, __dmul_rn(dp, umn_s[k])), __dmul_rn(dp, umx_s[k]));
+      const double ny = __dadd_rn(w, __dmul_rn(lam, __dsub_rn(hp, t)));
+      yp[2 * c.NXP + k] = ny;
+      if (want) {
+        const double rdp = P.scaled ? __ldg(P.psi_rcp + (size_t)st * c.NUP + k) : 1.0;
+        rmax = fmax(rmax, fabs(__dsub_rn(u, __dmul_rn(t, rdp))));
       }
+      double* ua = row + 2 * c.YW + c.NXP;
+      const double na = __dadd_rn(__dmul_rn(ua[k], om), __dmul_rn(th, u));
+      ua[k] = na;
+      if (wt) {
+        stcg(Yn + 2 * E * c.NXP + (size_t)e * c.NUP + k, ny);
+        stcg(P.uavg + (size_t)e * c.NUP + k, na);
+      }
+      if (last) stcg(P.U + (size_t)e * c.NUP + k, u);
     }
   }
-  // --- input copy: box projection (engine.py:182), element-parallel
-  for (int idx = threadIdx.x; idx < nrows * c.nu; idx += kThreadsS) {
-    const int r = idx / c.nu, j = idx - r * c.nu;
-    const int e = ge(r), st = gs(r);
-    double* row = srow(r);
-    double* yc = row + (size_t)ysm * c.YW + 2 * c.NXP;
-    double* yp = row + (size_t)(ysm ^ 1) * c.YW + 2 * c.NXP;
-    double* ua = row + 2 * c.YW + c.NXP;
-    const double u = urow(r)[j];
-    const double dp = P.scaled ? __ldg(P.psi_stage + (size_t)st * c.NUP + j) : 1.0;
-    const double w = extrap(yc[j], yp[j], cf);
-    const double hp = __dmul_rn(u, dp);
-    const double a = __dadd_rn(__dmul_rn(w, ilam), hp);
-    const double t = fmin(fmax(a, __dmul_rn(dp, umn_s[j])), __dmul_rn(dp, umx_s[j]));
-    const double ny = __dadd_rn(w, __dmul_rn(lam, __dsub_rn(hp, t)));
-    yp[j] = ny;
-    if (want) {
-      const double rdp = P.scaled ? __ldg(P.psi_rcp + (size_t)st * c.NUP + j) : 1.0;
-      rmax = fmax(rmax, fabs(__dsub_rn(u, __dmul_rn(t, rdp))));
+  // warp sums of all rows at once (independent shuffle chains), fixed order
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+    for (int m = 0; m < kRowsPT; ++m) {
+      ssv[m] += __shfl_xor_sync(0xffffffffu, ssv[m], off);
+      szv[m] += __shfl_xor_sync(0xffffffffu, szv[m], off);
     }
-    const double na = __dadd_rn(__dmul_rn(ua[j], om), __dmul_rn(th, u));
-    ua[j] = na;
-    if (wt) {
-      stcg(Yn + 2 * E * c.NXP + (size_t)e * c.NUP + j, ny);
-      stcg(P.uavg + (size_t)e * c.NUP + j, na);
+  if (lane == 0) {
+#pragma unroll
+    for (int m = 0; m < kRowsPT; ++m) {
+      red[(m * 4 + w4) * 2] = ssv[m];
+      red[(m * 4 + w4) * 2 + 1] = szv[m];
     }
-    if (last) stcg(P.U + (size_t)e * c.NUP + j, u);
   }
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(kKW) : "memory");
+  // pass 2: the state blocks
+  if (xk) {
+#pragma unroll
+    for (int m = 0; m < kRowsPT; ++m) {
+      const int r = g + kGroups * m;
+      if (r >= nrows) continue;
+      const int* d = rd + 5 * r;
+      const int e = d[0], st = d[1];
+      double* row = s_dyn + d[4];
+      double* yc = row + (size_t)ysm * c.YW;
+      double* yp = row + (size_t)(ysm ^ 1) * c.YW;
+      double* xa = row + 2 * c.YW;
+      const double ss = ((red[m * 8] + red[m * 8 + 2]) + red[m * 8 + 4]) + red[m * 8 + 6];
+      const double sz = ((red[m * 8 + 1] + red[m * 8 + 3]) + red[m * 8 + 5]) + red[m * 8 + 7];
+      const double ds = c.scl[st], dz = c.scl[N + st];
+      const double rds = c.scl[2 * N + st], rdz = c.scl[3 * N + st];
+      const double dist_s = sqrt(ss), dist_z = sqrt(sz);
+      const double wgt_s = __dmul_rn(__dmul_rn(lam_p, P.Wx), rds);
+      const double wgt_z = __dmul_rn(__dmul_rn(lam_p, P.gamma_d), rdz);
+      const double fs = dist_s > wgt_s ? __ddiv_rn(wgt_s, dist_s) : 1.0;
+      const double fz = dist_z > wgt_z ? __ddiv_rn(wgt_z, dist_z) : 1.0;
+      const double ws = extrap(yc[k], yp[k], cf);
+      const double wz = extrap(yc[c.NXP + k], yp[c.NXP + k], cf);
+      const double xi = s_dyn[d[2] + k];
+      const double ts = __dadd_rn(__dmul_rn(ws, ilam), __dmul_rn(xi, ds));
+      const double tz = __dadd_rn(__dmul_rn(wz, ilam), __dmul_rn(xi, dz));
+      const double hs = __dmul_rn(xi, ds), hz = __dmul_rn(xi, dz);
+      const double ps = fmax(ts, __dmul_rn(ds, xs_s[k]));
+      const double pz = fmin(fmax(tz, __dmul_rn(dz, xmn_s[k])), __dmul_rn(dz, xmx_s[k]));
+      const double t_s = __dadd_rn(ts, __dmul_rn(fs, __dsub_rn(ps, ts)));
+      const double t_z = __dadd_rn(tz, __dmul_rn(fz, __dsub_rn(pz, tz)));
+      const double ns = __dadd_rn(ws, __dmul_rn(lam, __dsub_rn(hs, t_s)));
+      const double nz = __dadd_rn(wz, __dmul_rn(lam, __dsub_rn(hz, t_z)));
+      yp[k] = ns;
+      yp[c.NXP + k] = nz;
+      if (want) {
+        rmax = fmax(rmax, fabs(__dsub_rn(xi, __dmul_rn(t_s, rds))));
+        rmax = fmax(rmax, fabs(__dsub_rn(xi, __dmul_rn(t_z, rdz))));
+      }
+      const double na = __dadd_rn(__dmul_rn(xa[k], om), __dmul_rn(th, xi));
+      xa[k] = na;
+      if (wt) {
+        stcg(Yn + (size_t)e * c.NXP + k, ns);
+        stcg(Yn + E * c.NXP + (size_t)e * c.NXP + k, nz);
+        stcg(P.xavg + (size_t)(e + 1) * c.NXP + k, na);
+      }
+      if (last) stcg(P.X + (size_t)(e + 1) * c.NXP + k, xi);
+    }
+  }
+  *rmax_io = rmax;
 }
 
 // ----------------------------------------------------------------------------
 // backward sweep of tile ti (reference factor.py:142-156)
 // ----------------------------------------------------------------------------
-__device__ void bwd_tile(const Ctx& c, int ti, int nu_it, int ysm, int srow0, bool resident, int cur) {
-  const Params& P = *c.P;
-  const SParams& S = *c.S;
+__device__ __noinline__ void bwd_tile(int ti, double cf, int ysm, int srow0, bool resident,
+                                      int cur) {
+  const SParams& S = g_sp;
+  const Ctx c = ctx_of();
+  const Params& P = S.P;
   const int* td = c.mt.tiles + 4 * ti;
   const int row0 = td[0], nrows = td[1], seg0 = td[2], nsegs = td[3];
-  const int tid = threadIdx.x;
-  const int nx = c.nx, nu = c.nu, nv = c.nv;
-  const bool apg = true;
-  const double cf = P.coef[nu_it];
+  const int tid = threadIdx.x, k = tid & (kKW - 1), g = tid / kKW;
+  const int nx = c.nx, nu = c.nu, nv = c.nv, N = c.N;
   double* XI = c.XI();
   double* Z = c.Z();
   double* H = c.H();
   long long tm_ = clock64();
   (void)tm_;
-  // prefetch beta_s (the bias of h) for this thread's (row, k) elements
-  constexpr int kPer = (kTileS * 128 + kThreadsS - 1) / kThreadsS;
-  double bpre[kPer];
+  // prefetch beta_s (the bias of h) for this thread's rows
+  double bpre[kRowsPT];
 #pragma unroll
-  for (int m = 0; m < kPer; ++m) {
-    const int idx = tid + m * kThreadsS;
+  for (int m = 0; m < kRowsPT; ++m) {
+    const int r = g + kGroups * m;
     bpre[m] = 0.0;
-    if (idx < nrows * nv) {
-      const int r = idx / nv, k = idx - r * nv;
-      bpre[m] = ldcg(S.beta_s + (size_t)c.mt.edge(row0 + r) * c.NVP + k);
-    }
+    if (r < nrows && k < nv) bpre[m] = ldcg(S.beta_s + (size_t)c.mt.edge(row0 + r) * c.NVP + k);
   }
   if (!resident) {
     cp_wait<0>();
     __syncthreads();
   }
+  double dpv[kRowsPT];
+#pragma unroll
+  for (int m = 0; m < kRowsPT; ++m) {
+    const int r = g + kGroups * m;
+    dpv[m] = 1.0;
+    if (P.scaled && k < nu && r < nrows) dpv[m] = __ldg(P.psi_stage + (size_t)c.mt.stage(row0 + r) * c.NUP + k);
+  }
   // (1) fill: s = D_sig w_sig + D_zeta w_zeta ; psi^ = D_psi w_psi
-  for (int idx = tid; idx < nrows * (nx + nu); idx += kThreadsS) {
-    const int r = idx / (nx + nu), k = idx - r * (nx + nu);
-    const int st = c.mt.stage(row0 + r);
+#pragma unroll
+  for (int m = 0; m < kRowsPT; ++m) {
+    const int r = g + kGroups * m;
+    if (r >= nrows) break;
     const double* yc = slot_row(c, srow0 + r) + (size_t)ysm * c.YW;
     const double* yp = slot_row(c, srow0 + r) + (size_t)(ysm ^ 1) * c.YW;
+    const int st = c.mt.stage(row0 + r);
     if (k < nx) {
-      const double ws = apg ? extrap(yc[k], yp[k], cf) : yc[k];
-      const double wz = apg ? extrap(yc[c.NXP + k], yp[c.NXP + k], cf) : yc[c.NXP + k];
-      const double ds = P.scaled ? __ldg(P.sig_stage + st) : 1.0;
-      const double dz = P.scaled ? __ldg(P.zeta_stage + st) : 1.0;
-      XI[r * c.NXP + k] = __dadd_rn(__dmul_rn(ws, ds), __dmul_rn(wz, dz));
-    } else {
-      const int j = k - nx;
-      const double wp = apg ? extrap(yc[2 * c.NXP + j], yp[2 * c.NXP + j], cf) : yc[2 * c.NXP + j];
-      Z[r * c.NUP + j] = P.scaled ? __dmul_rn(wp, __ldg(P.psi_stage + (size_t)st * c.NUP + j)) : wp;
+      const double ws = extrap(yc[k], yp[k], cf);
+      const double wz = extrap(yc[c.NXP + k], yp[c.NXP + k], cf);
+      XI[r * c.NXP + k] = __dadd_rn(__dmul_rn(ws, c.scl[st]), __dmul_rn(wz, c.scl[N + st]));
+    }
+    if (k < nu) {
+      const double wp = extrap(yc[2 * c.NXP + k], yp[2 * c.NXP + k], cf);
+      Z[r * c.NUP + k] = P.scaled ? __dmul_rn(wp, dpv[m]) : wp;
     }
   }
   __syncthreads();
@@ -326,74 +437,74 @@ __device__ void bwd_tile(const Ctx& c, int ti, int nu_it, int ysm, int srow0, bo
   // streamed CTAs: the slot is free again -> prefetch the next tile's dual rows
   // (or, after the last backward tile, the ergodic rows the forward sweep needs)
   if (!resident) {
-    if (ti > 0) {
-      const int* tn = c.mt.tiles + 4 * (ti - 1);
-      load_slot(c, tn[0], tn[1], 0, 1, cur, ysm);
-    } else {
-      load_slot(c, row0, nrows, 0, 2, cur, ysm);
-    }
+    const int* tn = c.mt.tiles + 4 * (ti > 0 ? ti - 1 : 0);
+    load_rows(c.mt.rows + 4 * tn[0], 4, tn[1], c.slot, ti > 0 ? 1 : 2, cur, ysm);
     cp_commit();
   }
   // (2) xiq scan, tail -> head (leaf tails have no children)
-  const double* adiag = c.bnd + 3 * c.NXP + 2 * c.NUP;
+  const double* adiag = c.adiag();
+  #pragma unroll 1
   for (int idx = tid; idx < nsegs * nx; idx += kThreadsS) {
     const int s = idx / nx, i = idx - s * nx;
     const int* sg = c.mt.segs + 4 * (seg0 + s);
-    const int lo = sg[0], hi = sg[1];
+    const int lo = sg[0], n = sg[1] - lo;
     const double a = adiag[i];
-    double x = XI[(hi - 1) * c.NXP + i];
-    for (int r = hi - 2; r >= lo; --r) {
-      x = __dadd_rn(XI[r * c.NXP + i], __dmul_rn(x, a));
-      XI[r * c.NXP + i] = x;
+    double* col = XI + lo * c.NXP + i;
+    double x = 0.0;  // leaf tail: no children (s + a .* 0 = s exactly)
+#pragma unroll 1
+    for (int j = n - 1; j >= 0; --j) {
+      x = __dadd_rn(col[j * c.NXP], __dmul_rn(x, a));
+      col[j * c.NXP] = x;
     }
     if (sg[2] >= 0) stcg(P.XIQG + (size_t)c.mt.edge(row0 + lo) * c.NXP + i, x);
   }
   __syncthreads();
   TSMPC_MARK(P, 1, tm_);
-  // (3) z = psi^ + B' xiq   (CSC of B: column j -> rows i)
-  {
-    const int* cp = c.spi + S.Bc_ptr;
-    const int* ci = c.spi + S.Bc_idx;
-    const double* cv = c.spv + S.Bc_val;
-    for (int idx = tid; idx < nrows * nu; idx += kThreadsS) {
-      const int r = idx / nu, j = idx - r * nu;
-      double z = Z[r * c.NUP + j];
-      for (int q = cp[j]; q < cp[j + 1]; ++q) z = fma(cv[q], XI[r * c.NXP + ci[q]], z);
-      Z[r * c.NUP + j] = z;
+  // (3) z = psi^ + B' xiq   (column k of B)
+  if (k < nu) {
+    const SpCol col = sp_col(c, S.Bc_ptr, S.Bc_idx, S.Bc_val, k);
+#pragma unroll
+    for (int m = 0; m < kRowsPT; ++m) {
+      const int r = g + kGroups * m;
+      if (r < nrows) Z[r * c.NUP + k] = sp_dot(c, col, S.Bc_idx, S.Bc_val, XI + r * c.NXP, Z[r * c.NUP + k]);
     }
   }
   __syncthreads();
-  // (4) h = beta_s + Ls' z   (CSC of Ls: column k -> rows j)
-  {
-    const int* cp = c.spi + S.Lc_ptr;
-    const int* ci = c.spi + S.Lc_idx;
-    const double* cv = c.spv + S.Lc_val;
+  TSMPC_MARK(P, 5, tm_);
+  // (4) h = beta_s + Ls' z   (column k of Ls)
+  if (k < nv) {
+    const SpCol col = sp_col(c, S.Lc_ptr, S.Lc_idx, S.Lc_val, k);
 #pragma unroll
-    for (int m = 0; m < kPer; ++m) {
-      const int idx = tid + m * kThreadsS;
-      if (idx < nrows * nv) {
-        const int r = idx / nv, k = idx - r * nv;
-        double h = 0.0;
-        for (int q = cp[k]; q < cp[k + 1]; ++q) h = fma(cv[q], Z[r * c.NUP + ci[q]], h);
-        H[r * c.NVP + k] = __dadd_rn(bpre[m], h);
-      }
+    for (int m = 0; m < kRowsPT; ++m) {
+      const int r = g + kGroups * m;
+      if (r < nrows) H[r * c.NVP + k] = __dadd_rn(bpre[m], sp_dot(c, col, S.Lc_idx, S.Lc_val, Z + r * c.NUP, 0.0));
     }
   }
   __syncthreads();
   TSMPC_MARK(P, 2, tm_);
   // (5) g scan, tail -> head: g_e = h_e + g_child ; t_e = g_e / (2 p_e)
+  #pragma unroll 1
   for (int idx = tid; idx < nsegs * nv; idx += kThreadsS) {
-    const int s = idx / nv, k = idx - s * nv;
+    const int s = idx / nv, kk = idx - s * nv;
     const int* sg = c.mt.segs + 4 * (seg0 + s);
-    const int lo = sg[0], hi = sg[1];
-    double g = 0.0;
-    for (int r = hi - 1; r >= lo; --r) {
-      g = __dadd_rn(H[r * c.NVP + k], g);
-      const double t = __dmul_rn(g, c.mt.inv2p(row0 + r));
-      if (resident) slot_row(c, srow0 + r)[2 * c.YW + c.NXP + c.NUP + k] = t;
-      else stcg(S.TG + (size_t)c.mt.edge(row0 + r) * c.NVP + k, t);
+    const int lo = sg[0], n = sg[1] - lo;
+    const double* col = H + lo * c.NVP + kk;
+    double gv = 0.0;
+    if (resident) {
+      double* tcol = slot_row(c, srow0 + lo) + 2 * c.YW + c.NXP + c.NUP + kk;
+#pragma unroll 1
+      for (int j = n - 1; j >= 0; --j) {
+        gv = __dadd_rn(col[j * c.NVP], gv);
+        tcol[j * c.SL] = __dmul_rn(gv, c.mt.inv2p(row0 + lo + j));
+      }
+    } else {
+#pragma unroll 1
+      for (int j = n - 1; j >= 0; --j) {
+        gv = __dadd_rn(col[j * c.NVP], gv);
+        stcg(S.TG + (size_t)c.mt.edge(row0 + lo + j) * c.NVP + kk, __dmul_rn(gv, c.mt.inv2p(row0 + lo + j)));
+      }
     }
-    if (sg[2] >= 0) stcg(P.GG + (size_t)c.mt.edge(row0 + lo) * c.NVP + k, g);
+    if (sg[2] >= 0) stcg(P.GG + (size_t)c.mt.edge(row0 + lo) * c.NVP + kk, gv);
   }
   __syncthreads();
   TSMPC_MARK(P, 3, tm_);
@@ -402,13 +513,14 @@ __device__ void bwd_tile(const Ctx& c, int ti, int nu_it, int ysm, int srow0, bo
 // ----------------------------------------------------------------------------
 // forward sweep of tile ti (factor.py:158-170) + epilogue
 // ----------------------------------------------------------------------------
-__device__ void fwd_tile(const Ctx& c, int ti, int nu_it, int ysm, int srow0, bool resident, int cur,
-                         double& rmax) {
-  const Params& P = *c.P;
-  const SParams& S = *c.S;
+__device__ __noinline__ void fwd_tile(int ti, int nu_it, double cf, double th, int ysm,
+                                      int srow0, bool resident, int cur, double* rmax) {
+  const SParams& S = g_sp;
+  const Ctx c = ctx_of();
+  const Params& P = S.P;
   const int* td = c.mt.tiles + 4 * ti;
   const int row0 = td[0], nrows = td[1], seg0 = td[2], nsegs = td[3];
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, k = tid & (kKW - 1), g = tid / kKW;
   const int nx = c.nx, nu = c.nu, nv = c.nv;
   double* XB = c.XI();
   double* DU = c.Z();
@@ -418,28 +530,25 @@ __device__ void fwd_tile(const Ctx& c, int ti, int nu_it, int ysm, int srow0, bo
   if (!resident) {
     // t rows of this tile -> S region; then (after the previous epilogue) the slot
     const int hv = c.NVP / 2;
+    #pragma unroll 1
     for (int idx = tid; idx < nrows * hv; idx += kThreadsS) {
-      const int r = idx / hv, k = idx - r * hv;
-      cp16(SS + r * c.NVP + 2 * k, S.TG + (size_t)c.mt.edge(row0 + r) * c.NVP + 2 * k);
+      const int r = idx / hv, kk = idx - r * hv;
+      cp16(SS + r * c.NVP + 2 * kk, S.TG + (size_t)c.mt.edge(row0 + r) * c.NVP + 2 * kk);
     }
     cp_commit();
-    if (ti > 0) load_slot(c, row0, nrows, 0, 3, cur, ysm);
+    if (ti > 0) load_rows(c.mt.rows + 4 * row0, 4, nrows, c.slot, 3, cur, ysm);
     cp_commit();
   }
   // prefetch the static biases: uhat (u = uhat + du) and e (x recursion)
-  constexpr int kPerU = (kTileS * 128 + kThreadsS - 1) / kThreadsS;
-  double upre[kPerU], epre[kPerU];
+  double upre[kRowsPT], epre[kRowsPT];
 #pragma unroll
-  for (int m = 0; m < kPerU; ++m) {
-    const int idx = tid + m * kThreadsS;
+  for (int m = 0; m < kRowsPT; ++m) {
+    const int r = g + kGroups * m;
     upre[m] = epre[m] = 0.0;
-    if (idx < nrows * nu) {
-      const int r = idx / nu, j = idx - r * nu;
-      upre[m] = ldcg(P.uhat + (size_t)c.mt.edge(row0 + r) * c.NUP + j);
-    }
-    if (idx < nrows * nx) {
-      const int r = idx / nx, i = idx - r * nx;
-      epre[m] = ldcg(P.evec + (size_t)c.mt.edge(row0 + r) * c.NXP + i);
+    if (r < nrows) {
+      const int e = c.mt.edge(row0 + r);
+      if (k < nu) upre[m] = ldcg(P.uhat + (size_t)e * c.NUP + k);
+      if (k < nx) epre[m] = ldcg(P.evec + (size_t)e * c.NXP + k);
     }
   }
   if (!resident) {
@@ -447,82 +556,84 @@ __device__ void fwd_tile(const Ctx& c, int ti, int nu_it, int ysm, int srow0, bo
     __syncthreads();
   }
   // (1) S scan, head -> tail: S_e = t_e + S_parent
+  #pragma unroll 1
   for (int idx = tid; idx < nsegs * nv; idx += kThreadsS) {
-    const int s = idx / nv, k = idx - s * nv;
+    const int s = idx / nv, kk = idx - s * nv;
     const int* sg = c.mt.segs + 4 * (seg0 + s);
-    const int lo = sg[0], hi = sg[1], pn = sg[2];
-    double Sv = pn >= 0 ? c.need[(size_t)pn * c.S->need_ld + k] : 0.0;
-    for (int r = lo; r < hi; ++r) {
-      const double t = resident ? slot_row(c, srow0 + r)[2 * c.YW + c.NXP + c.NUP + k] : SS[r * c.NVP + k];
-      Sv = __dadd_rn(t, Sv);
-      SS[r * c.NVP + k] = Sv;
+    const int lo = sg[0], n = sg[1] - lo, pn = sg[2];
+    const double* tcol = resident ? slot_row(c, srow0 + lo) + 2 * c.YW + c.NXP + c.NUP + kk : SS + lo * c.NVP + kk;
+    const int tld = resident ? c.SL : c.NVP;
+    double* scol = SS + lo * c.NVP + kk;
+    double Sv = pn >= 0 ? c.need[(size_t)pn * S.need_ld + kk] : 0.0;
+#pragma unroll 1
+    for (int j = 0; j < n; ++j) {
+      Sv = __dadd_rn(tcol[j * tld], Sv);
+      scol[j * c.NVP] = Sv;
     }
   }
   __syncthreads();
   TSMPC_MARK(P, 4, tm_);
-  // (2) du = Lt S   (CSR of Lt: row j -> columns k)
-  {
-    const int* rp = c.spi + S.Lr_ptr;
-    const int* ri = c.spi + S.Lr_idx;
-    const double* rv = c.spv + S.Lr_val;
-    for (int idx = tid; idx < nrows * nu; idx += kThreadsS) {
-      const int r = idx / nu, j = idx - r * nu;
-      double d = 0.0;
-      for (int q = rp[j]; q < rp[j + 1]; ++q) d = fma(rv[q], SS[r * c.NVP + ri[q]], d);
-      DU[r * c.NUP + j] = d;
+  // (2) du = Lt S   (row k of Lt)
+  if (k < nu) {
+    const SpCol col = sp_col(c, S.Lr_ptr, S.Lr_idx, S.Lr_val, k);
+#pragma unroll
+    for (int m = 0; m < kRowsPT; ++m) {
+      const int r = g + kGroups * m;
+      if (r < nrows) DU[r * c.NUP + k] = sp_dot(c, col, S.Lr_idx, S.Lr_val, SS + r * c.NVP, 0.0);
     }
   }
   __syncthreads();
-  // (3) bv + e = B du + e   (CSR of B: row i -> columns j)
-  {
-    const int* rp = c.spi + S.Br_ptr;
-    const int* ri = c.spi + S.Br_idx;
-    const double* rv = c.spv + S.Br_val;
+  TSMPC_MARK(P, 11, tm_);
+  // (3) bv + e = B du + e   (row k of B)
+  if (k < nx) {
+    const SpCol col = sp_col(c, S.Br_ptr, S.Br_idx, S.Br_val, k);
 #pragma unroll
-    for (int m = 0; m < kPerU; ++m) {
-      const int idx = tid + m * kThreadsS;
-      if (idx < nrows * nx) {
-        const int r = idx / nx, i = idx - r * nx;
-        double b = 0.0;
-        for (int q = rp[i]; q < rp[i + 1]; ++q) b = fma(rv[q], DU[r * c.NUP + ri[q]], b);
-        XB[r * c.NXP + i] = __dadd_rn(b, epre[m]);
-      }
+    for (int m = 0; m < kRowsPT; ++m) {
+      const int r = g + kGroups * m;
+      if (r < nrows) XB[r * c.NXP + k] = __dadd_rn(sp_dot(c, col, S.Br_idx, S.Br_val, DU + r * c.NUP, 0.0), epre[m]);
     }
   }
   __syncthreads();
   TSMPC_MARK(P, 6, tm_);
-  // (4) u = uhat + du ; x scan, head -> tail: x = a .* x_anc + (bv + e)
+  // (4) u = uhat + du ; x scan, head -> tail: x = a .* x_anc + (bv + e) ; row descriptors
+  if (k < nu) {
 #pragma unroll
-  for (int m = 0; m < kPerU; ++m) {
-    const int idx = tid + m * kThreadsS;
-    if (idx < nrows * nu) {
-      const int r = idx / nu, j = idx - r * nu;
-      DU[r * c.NUP + j] = __dadd_rn(DU[r * c.NUP + j], upre[m]);
+    for (int m = 0; m < kRowsPT; ++m) {
+      const int r = g + kGroups * m;
+      if (r < nrows) DU[r * c.NUP + k] = __dadd_rn(DU[r * c.NUP + k], upre[m]);
     }
   }
   {
-    const double* adiag = c.bnd + 3 * c.NXP + 2 * c.NUP;
+    const double* adiag = c.adiag();
+    const double* pr = c.proot();
+    #pragma unroll 1
     for (int idx = tid; idx < nsegs * nx; idx += kThreadsS) {
       const int s = idx / nx, i = idx - s * nx;
       const int* sg = c.mt.segs + 4 * (seg0 + s);
-      const int lo = sg[0], hi = sg[1], pn = sg[2];
-      double x = pn >= 0 ? c.need[(size_t)pn * c.S->need_ld + c.NVP + i] : P.p[i];
+      const int lo = sg[0], n = sg[1] - lo, pn = sg[2];
+      double* col = XB + lo * c.NXP + i;
+      double x = pn >= 0 ? c.need[(size_t)pn * S.need_ld + c.NVP + i] : pr[i];
       const double a = adiag[i];
-      for (int r = lo; r < hi; ++r) {
-        x = __dadd_rn(__dmul_rn(x, a), XB[r * c.NXP + i]);
-        XB[r * c.NXP + i] = x;
+#pragma unroll 1
+      for (int j = 0; j < n; ++j) {
+        x = __dadd_rn(__dmul_rn(x, a), col[j * c.NXP]);
+        col[j * c.NXP] = x;
       }
     }
+  }
+  if (tid < nrows) {
+    int* d = c.rdesc() + 5 * tid;
+    d[0] = c.mt.edge(row0 + tid);
+    d[1] = c.mt.stage(row0 + tid);
+    d[2] = (int)(XB + tid * c.NXP - s_dyn);
+    d[3] = (int)(DU + tid * c.NUP - s_dyn);
+    d[4] = (int)(slot_row(c, srow0 + tid) - s_dyn);
   }
   if (!resident) cp_wait<0>();
   __syncthreads();
   TSMPC_MARK(P, 7, tm_);
   // (5) epilogue
-  const Meta& mt = c.mt;
-  epilogue(
-      c, nu_it, nrows, [&](int r) { return mt.edge(row0 + r); }, [&](int r) { return mt.stage(row0 + r); },
-      [&](int r) { return XB + r * c.NXP; }, [&](int r) { return DU + r * c.NUP; },
-      [&](int r) { return slot_row(c, srow0 + r); }, ysm, !resident || nu_it == P.iters - 1, cur ^ 1, rmax);
+  epilogue(nu_it, cf, th, nrows, ysm, !resident || nu_it == P.iters - 1, cur ^ 1, rmax);
   __syncthreads();
   TSMPC_MARK(P, 8, tm_);
 }
@@ -531,9 +642,10 @@ __device__ void fwd_tile(const Ctx& c, int ti, int nu_it, int ysm, int srow0, bo
 // phase B: component-sliced trunk sweep -> KY (see tsmpc_apg.cu trunk_sweep_smem
 // for the recursion; here the schedule is staged in shared memory first)
 // ----------------------------------------------------------------------------
-__device__ void trunk_sweep(const Ctx& c, int nu_it, int cur) {
-  const Params& P = *c.P;
-  const SParams& S = *c.S;
+__device__ __noinline__ void trunk_sweep(double cf, int cur) {
+  const SParams& S = g_sp;
+  const Ctx c = ctx_of();
+  const Params& P = S.P;
   const int ncomp = c.nv + c.nx + c.nu;
   const int c_lo = (int)((long long)ncomp * blockIdx.x / gridDim.x);
   const int c_hi = (int)((long long)ncomp * (blockIdx.x + 1) / gridDim.x);
@@ -544,6 +656,7 @@ __device__ void trunk_sweep(const Ctx& c, int nu_it, int cur) {
   double* Zs = c.work;
   double* Xs = Zs + (size_t)T * nc;
   int* sch = reinterpret_cast<int*>(Xs + (size_t)T * nc);
+  #pragma unroll 1
   for (int i = threadIdx.x; i < S.n_tsched; i += kThreadsS) sch[i] = __ldg(g + i);
   __syncthreads();
   const int* lev = sch + 4;
@@ -553,9 +666,9 @@ __device__ void trunk_sweep(const Ctx& c, int nu_it, int cur) {
   const size_t E = (size_t)c.E;
   const double* Y = P.ybuf[cur];
   const double* Yp = P.ybuf[cur ^ 1];
-  const double cf = P.coef[nu_it];
-  const double* adiag = c.bnd + 3 * c.NXP + 2 * c.NUP;
+  const double* adiag = c.adiag();
   // (1) own terms + chain-head children (one parallel round of loads)
+  #pragma unroll 1
   for (int idx = threadIdx.x; idx < T * nc; idx += kThreadsS) {
     const int tp = idx / nc, k = idx - tp * nc, q = c_lo + k;
     const int* ps = pos + 8 * tp;
@@ -563,16 +676,17 @@ __device__ void trunk_sweep(const Ctx& c, int nu_it, int cur) {
     double z = 0.0, x = 0.0;
     if (q < c.nv) {
       z = ldcg(S.beta_s + (size_t)a * c.NVP + q);
+      #pragma unroll 1
       for (int m = 0; m < nh; ++m) z = __dadd_rn(z, ldcg(P.GG + (size_t)hch[h0 + m] * c.NVP + q));
     } else if (q < c.nv + c.nx) {
       const int i = q - c.nv;
       const size_t o = (size_t)a * c.NXP + i;
       const double ws = extrap(ldcg(Y + o), ldcg(Yp + o), cf);
       const double wz = extrap(ldcg(Y + E * c.NXP + o), ldcg(Yp + E * c.NXP + o), cf);
-      const double ds = P.scaled ? __ldg(P.sig_stage + st) : 1.0;
-      const double dz = P.scaled ? __ldg(P.zeta_stage + st) : 1.0;
+      const double ds = c.scl[st], dz = c.scl[c.N + st];
       const double s = __dadd_rn(__dmul_rn(ws, ds), __dmul_rn(wz, dz));
       double h = 0.0;
+      #pragma unroll 1
       for (int m = 0; m < nh; ++m) h = __dadd_rn(h, ldcg(P.XIQG + (size_t)hch[h0 + m] * c.NXP + i));
       x = __dadd_rn(s, __dmul_rn(h, adiag[i]));
     } else {
@@ -586,12 +700,15 @@ __device__ void trunk_sweep(const Ctx& c, int nu_it, int cur) {
   }
   __syncthreads();
   // (2) bottom-up over edge-stage levels: add trunk children
+  #pragma unroll 1
   for (int l = nlev - 1; l >= 0; --l) {
+    #pragma unroll 1
     for (int idx = lev[l] * nc + threadIdx.x; idx < lev[l + 1] * nc; idx += kThreadsS) {
       const int tp = idx / nc, k = idx - tp * nc, q = c_lo + k;
       const int* ps = pos + 8 * tp;
       const int c0 = ps[3], n = ps[4];
       double zs = 0.0, xs = 0.0;
+      #pragma unroll 1
       for (int m = 0; m < n; ++m) {
         const int cp = tch[c0 + m];
         zs = __dadd_rn(zs, Zs[cp * nc + k]);
@@ -608,7 +725,9 @@ __device__ void trunk_sweep(const Ctx& c, int nu_it, int cur) {
     __syncthreads();
   }
   // (3) top-down: K_a, Y_a = own * inv2p_a + parent's
+  #pragma unroll 1
   for (int l = 0; l < nlev; ++l) {
+    #pragma unroll 1
     for (int idx = lev[l] * nc + threadIdx.x; idx < lev[l + 1] * nc; idx += kThreadsS) {
       const int tp = idx / nc, k = idx - tp * nc;
       const int* ps = pos + 8 * tp;
@@ -620,6 +739,7 @@ __device__ void trunk_sweep(const Ctx& c, int nu_it, int cur) {
     __syncthreads();
   }
   // (4) KY columns of this slice
+  #pragma unroll 1
   for (int idx = threadIdx.x; idx < T * nc; idx += kThreadsS) {
     const int tp = idx / nc, k = idx - tp * nc, q = c_lo + k;
     const int col = q < c.nv ? q : (q < c.nv + c.nx ? c.NVP + (q - c.nv) : c.NVP + c.NXP + (q - c.nv - c.nx));
@@ -631,9 +751,10 @@ __device__ void trunk_sweep(const Ctx& c, int nu_it, int cur) {
 // phase D (trunk part): S, x, u of the needed trunk edges from KY
 //   S = K + Ls'(B' Yx + Ypsi),  du = Lt S,  u = uhat + du,  x = a .* x_par + (B du + e)
 // ----------------------------------------------------------------------------
-__device__ void trunk_needs(const Ctx& c) {
-  const Params& P = *c.P;
-  const SParams& S = *c.S;
+__device__ __noinline__ void trunk_needs() {
+  const SParams& S = g_sp;
+  const Ctx c = ctx_of();
+  const Params& P = S.P;
   const int nn = c.mt.nneed;
   if (nn == 0) return;
   const int nx = c.nx, nu = c.nu, nv = c.nv;
@@ -646,10 +767,12 @@ __device__ void trunk_needs(const Ctx& c) {
     const int* cp = c.spi + S.Bc_ptr;
     const int* ci = c.spi + S.Bc_idx;
     const double* cv = c.spv + S.Bc_val;
+    #pragma unroll 1
     for (int idx = threadIdx.x; idx < nn * nu; idx += kThreadsS) {
       const int n = idx / nu, j = idx - n * nu;
       const double* ky = P.KY + (size_t)nd[4 * n] * P.KY_LD;
       double z = ldcg(ky + c.NVP + c.NXP + j);
+      #pragma unroll 1
       for (int q = cp[j]; q < cp[j + 1]; ++q) z = fma(cv[q], ldcg(ky + c.NVP + ci[q]), z);
       Yz[(size_t)n * c.NUP + j] = z;
     }
@@ -660,9 +783,11 @@ __device__ void trunk_needs(const Ctx& c) {
     const int* cp = c.spi + S.Lc_ptr;
     const int* ci = c.spi + S.Lc_idx;
     const double* cv = c.spv + S.Lc_val;
+    #pragma unroll 1
     for (int idx = threadIdx.x; idx < nn * nv; idx += kThreadsS) {
       const int n = idx / nv, k = idx - n * nv;
       double h = 0.0;
+      #pragma unroll 1
       for (int q = cp[k]; q < cp[k + 1]; ++q) h = fma(cv[q], Yz[(size_t)n * c.NUP + ci[q]], h);
       c.need[(size_t)n * LD + k] = __dadd_rn(ldcg(P.KY + (size_t)nd[4 * n] * P.KY_LD + k), h);
     }
@@ -673,9 +798,11 @@ __device__ void trunk_needs(const Ctx& c) {
     const int* rp = c.spi + S.Lr_ptr;
     const int* ri = c.spi + S.Lr_idx;
     const double* rv = c.spv + S.Lr_val;
+    #pragma unroll 1
     for (int idx = threadIdx.x; idx < nn * nu; idx += kThreadsS) {
       const int n = idx / nu, j = idx - n * nu;
       double d = 0.0;
+      #pragma unroll 1
       for (int q = rp[j]; q < rp[j + 1]; ++q) d = fma(rv[q], c.need[(size_t)n * LD + ri[q]], d);
       DU[(size_t)n * c.NUP + j] = d;
       c.need[(size_t)n * LD + c.NVP + c.NXP + j] = __dadd_rn(d, ldcg(P.uhat + (size_t)nd[4 * n + 2] * c.NUP + j));
@@ -687,20 +814,24 @@ __device__ void trunk_needs(const Ctx& c) {
     const int* rp = c.spi + S.Br_ptr;
     const int* ri = c.spi + S.Br_idx;
     const double* rv = c.spv + S.Br_val;
+    #pragma unroll 1
     for (int idx = threadIdx.x; idx < nn * nx; idx += kThreadsS) {
       const int n = idx / nx, i = idx - n * nx;
       double b = 0.0;
+      #pragma unroll 1
       for (int q = rp[i]; q < rp[i + 1]; ++q) b = fma(rv[q], DU[(size_t)n * c.NUP + ri[q]], b);
       c.need[(size_t)n * LD + c.NVP + i] = __dadd_rn(b, ldcg(P.evec + (size_t)nd[4 * n + 2] * c.NXP + i));
     }
     __syncthreads();
-    const double* adiag = c.bnd + 3 * c.NXP + 2 * c.NUP;
+    const double* adiag = c.adiag();
+    #pragma unroll 1
     for (int l = 0; l < c.mt.nlev; ++l) {
       const int n0 = c.mt.lev[l], n1 = c.mt.lev[l + 1];
+      #pragma unroll 1
       for (int idx = n0 * nx + threadIdx.x; idx < n1 * nx; idx += kThreadsS) {
         const int n = idx / nx, i = idx - n * nx;
         const int pn = nd[4 * n + 1];
-        const double xp = pn >= 0 ? c.need[(size_t)pn * LD + c.NVP + i] : P.p[i];
+        const double xp = pn >= 0 ? c.need[(size_t)pn * LD + c.NVP + i] : c.proot()[i];
         double* xv = c.need + (size_t)n * LD + c.NVP + i;
         *xv = __dadd_rn(__dmul_rn(xp, adiag[i]), *xv);
       }
@@ -709,148 +840,146 @@ __device__ void trunk_needs(const Ctx& c) {
   }
 }
 
+
 // epilogue of the CTA's own trunk rows (dual / ergodic rows live in HBM)
-__device__ void trunk_own_rows(const Ctx& c, int nu_it, int cur, double& rmax) {
-  const Params& P = *c.P;
-  const SParams& S = *c.S;
+__device__ __noinline__ void trunk_own_rows(int nu_it, double cf, double th, int cur,
+                                            double* rmax) {
+  const SParams& S = g_sp;
+  const Ctx c = ctx_of();
   const int no = c.mt.nown;
   if (no == 0) return;
-  const int cap = max(1, c.S->n_work / c.SL);
+  const int cap = max(1, min(kTileS, S.n_work / c.SL));
+  const int LD = S.need_ld;
   for (int b0 = 0; b0 < no; b0 += cap) {
     const int nb = min(cap, no - b0);
-    // stage the rows into the work region in slot format (dual at index 0 = HBM cur)
-    const int hx = c.NXP / 2, hu = c.NUP / 2, per_y = 2 * hx + hu, nch = 2 * per_y + hx + hu;
-    const size_t E = (size_t)c.E;
-    for (int idx = threadIdx.x; idx < nb * nch; idx += kThreadsS) {
-      const int r = idx / nch;
-      int k = idx - r * nch;
-      const int e = c.mt.needs[4 * c.mt.own[b0 + r] + 2];
-      double* srow = c.work + (size_t)r * c.SL;
-      if (k < 2 * per_y) {
-        const int which = k < per_y ? 0 : 1;
-        const int kk = k - which * per_y;
-        const double* Y = P.ybuf[cur ^ which];
-        double* dst = srow + (size_t)which * c.YW;
-        if (kk < hx) cp16(dst + 2 * kk, Y + (size_t)e * c.NXP + 2 * kk);
-        else if (kk < 2 * hx) cp16(dst + c.NXP + 2 * (kk - hx), Y + E * c.NXP + (size_t)e * c.NXP + 2 * (kk - hx));
-        else cp16(dst + 2 * c.NXP + 2 * (kk - 2 * hx), Y + 2 * E * c.NXP + (size_t)e * c.NUP + 2 * (kk - 2 * hx));
-      } else {
-        k -= 2 * per_y;
-        double* xa = srow + 2 * c.YW;
-        if (k < hx) cp16(xa + 2 * k, P.xavg + (size_t)(e + 1) * c.NXP + 2 * k);
-        else cp16(xa + c.NXP + 2 * (k - hx), P.uavg + (size_t)e * c.NUP + 2 * (k - hx));
-      }
+    const int* own = c.mt.own + b0;
+    if (threadIdx.x < nb) {
+      const int n = own[threadIdx.x];
+      int* d = c.rdesc() + 5 * threadIdx.x;
+      d[0] = c.mt.needs[4 * n + 2];
+      d[1] = c.mt.needs[4 * n + 3];
+      d[2] = (int)(c.need + (size_t)n * LD + c.NVP - s_dyn);
+      d[3] = (int)(c.need + (size_t)n * LD + c.NVP + c.NXP - s_dyn);
+      d[4] = (int)(c.work + (size_t)threadIdx.x * c.SL - s_dyn);
     }
+    __syncthreads();
+    // stage the rows into the work region in slot format (dual at index 0 = HBM cur)
+    load_rows(c.rdesc(), 5, nb, c.work, 3, cur, 0);
     cp_commit();
     cp_wait<0>();
     __syncthreads();
-    const Meta& mt = c.mt;
-    const int LD = S.need_ld;
-    const int* own = mt.own + b0;
-    epilogue(
-        c, nu_it, nb, [&](int r) { return mt.needs[4 * own[r] + 2]; }, [&](int r) { return mt.needs[4 * own[r] + 3]; },
-        [&](int r) { return c.need + (size_t)own[r] * LD + c.NVP; },
-        [&](int r) { return c.need + (size_t)own[r] * LD + c.NVP + c.NXP; },
-        [&](int r) { return c.work + (size_t)r * c.SL; }, 0, true, cur ^ 1, rmax);
+    epilogue(nu_it, cf, th, nb, 0, true, cur ^ 1, rmax);
     __syncthreads();
   }
 }
 
 }  // namespace
 
-__global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel(const __grid_constant__ SParams S) {
+__global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
   cg::grid_group grid = cg::this_grid();
+  const SParams& S = g_sp;
   const Params& P = S.P;
-  Ctx c;
-  c.S = &S;
-  c.P = &P;
-  c.NXP = P.NXP; c.NUP = P.NUP; c.NVP = P.NVP;
-  c.YW = S.YW; c.SL = S.slot_ld;
-  c.nx = P.nx; c.nu = P.nu; c.nv = P.nv; c.E = P.n_edges;
-  c.bnd = s_dyn + S.O_BND;
-  c.need = s_dyn + S.O_NEED;
-  c.work = s_dyn + S.O_WORK;
-  c.slot = s_dyn + S.O_SLOT;
-  int* ints = reinterpret_cast<int*>(s_dyn + S.O_INT);
-  int* smeta = ints;
-  int* sspi = ints + S.meta_max;
-  double* sspv = s_dyn + S.O_SPV;
-  {  // stage model vectors, sparse operators and this CTA's plan
-    double* bnd = c.bnd;
-    for (int i = threadIdx.x; i < c.NXP; i += kThreadsS) {
+  {  // stage model vectors, scaling, sparse operators and this CTA's plan
+    double* bnd = s_dyn + S.O_BND;
+    double* scl = s_dyn + S.O_SCL;
+    const int NXP = P.NXP, NUP = P.NUP, N = P.N;
+    #pragma unroll 1
+    for (int i = threadIdx.x; i < NXP; i += kThreadsS) {
       bnd[i] = P.x_s[i];
-      bnd[c.NXP + i] = P.x_min[i];
-      bnd[2 * c.NXP + i] = P.x_max[i];
-      bnd[3 * c.NXP + 2 * c.NUP + i] = P.a_diag[i];
+      bnd[NXP + i] = P.x_min[i];
+      bnd[2 * NXP + i] = P.x_max[i];
+      bnd[3 * NXP + 2 * NUP + i] = P.a_diag[i];
+      bnd[4 * NXP + 2 * NUP + i] = P.p[i];
     }
-    for (int j = threadIdx.x; j < c.NUP; j += kThreadsS) {
-      bnd[3 * c.NXP + j] = P.u_min[j];
-      bnd[3 * c.NXP + c.NUP + j] = P.u_max[j];
+    #pragma unroll 1
+    for (int j = threadIdx.x; j < NUP; j += kThreadsS) {
+      bnd[3 * NXP + j] = P.u_min[j];
+      bnd[3 * NXP + NUP + j] = P.u_max[j];
     }
+    #pragma unroll 1
+    for (int j = threadIdx.x; j < N; j += kThreadsS) {
+      scl[j] = P.scaled ? P.sig_stage[j] : 1.0;
+      scl[N + j] = P.scaled ? P.zeta_stage[j] : 1.0;
+      scl[2 * N + j] = P.scaled ? P.sig_rcp[j] : 1.0;
+      scl[3 * N + j] = P.scaled ? P.zeta_rcp[j] : 1.0;
+    }
+    int* ints = reinterpret_cast<int*>(s_dyn + S.O_INT);
     const int m0 = __ldg(S.meta_ptr + blockIdx.x), m1 = __ldg(S.meta_ptr + blockIdx.x + 1);
-    for (int i = threadIdx.x; i < m1 - m0; i += kThreadsS) smeta[i] = __ldg(S.meta + m0 + i);
-    for (int i = threadIdx.x; i < S.n_spi; i += kThreadsS) sspi[i] = __ldg(S.spi + i);
-    for (int i = threadIdx.x; i < S.n_spv; i += kThreadsS) sspv[i] = __ldg(S.spv + i);
+    #pragma unroll 1
+    for (int i = threadIdx.x; i < m1 - m0; i += kThreadsS) ints[i] = __ldg(S.meta + m0 + i);
+    #pragma unroll 1
+    for (int i = threadIdx.x; i < S.n_spi; i += kThreadsS) ints[S.meta_max + i] = __ldg(S.spi + i);
+    double* spv = s_dyn + S.O_SPV;
+    #pragma unroll 1
+    for (int i = threadIdx.x; i < S.n_spv; i += kThreadsS) spv[i] = __ldg(S.spv + i);
     __syncthreads();
   }
-  c.mt.bind(smeta);
-  c.spi = sspi;
-  c.spv = sspv;
+  const Ctx c = ctx_of();
   const bool resident = c.mt.resident != 0;
   const int nt = c.mt.ntiles;
   const bool trunk = P.n_trunk > 0;
-  // initial dual / ergodic rows
-  {
+  {  // initial dual / ergodic rows
     const int cur0 = P.slot0 & 1;
     if (resident) {
-      for (int t = 0; t < nt; ++t) {
-        const int* td = c.mt.tiles + 4 * t;
-        load_slot(c, td[0], td[1], td[0], 3, cur0, 0);
-      }
+      if (nt > 0) load_rows(c.mt.rows, 4, c.mt.nrows, c.slot, 3, cur0, 0);
     } else if (nt > 0) {
       const int* td = c.mt.tiles + 4 * (nt - 1);
-      load_slot(c, td[0], td[1], 0, 1, cur0, 0);
+      load_rows(c.mt.rows + 4 * td[0], 4, td[1], c.slot, 1, cur0, 0);
     }
     cp_commit();
     cp_wait<0>();
     __syncthreads();
   }
   double rmax = 0.0;
+  double cf = P.coef[0], th = P.theta[0];
   for (int nu = 0; nu < P.iters; ++nu) {
     const int cur = (P.slot0 + nu) & 1;
     const int ysm = nu & 1;
-    for (int t = nt - 1; t >= 0; --t) bwd_tile(c, t, nu, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur);
+    // momentum coefficients of the next iteration, loaded one iteration ahead
+    const int nn = nu + 1 < P.iters ? nu + 1 : nu;
+    const double cf_n = P.coef[nn], th_n = P.theta[nn];
+    for (int t = nt - 1; t >= 0; --t) bwd_tile(t, cf, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur);
     if (trunk) {
       long long tb_ = clock64();
       (void)tb_;
       grid.sync();
       TSMPC_MARK(P, 9, tb_);
-      trunk_sweep(c, nu, cur);
+      trunk_sweep(cf, cur);
       TSMPC_MARK(P, 10, tb_);
       grid.sync();
       TSMPC_MARK(P, 9, tb_);
-      trunk_needs(c);
-      trunk_own_rows(c, nu, cur, rmax);
+      trunk_needs();
+      trunk_own_rows(nu, cf, th, cur, &rmax);
       TSMPC_MARK(P, 12, tb_);
     }
     if (blockIdx.x == 0) {
-      const double th = P.theta[nu], om = __dsub_rn(1.0, th);
+      const double om = __dsub_rn(1.0, th);
+      #pragma unroll 1
       for (int i = threadIdx.x; i < c.nx; i += kThreadsS)
-        P.xavg[i] = __dadd_rn(__dmul_rn(P.xavg[i], om), __dmul_rn(th, P.p[i]));
+        P.xavg[i] = __dadd_rn(__dmul_rn(P.xavg[i], om), __dmul_rn(th, c.proot()[i]));
     }
-    for (int t = 0; t < nt; ++t) fwd_tile(c, t, nu, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur, rmax);
+    for (int t = 0; t < nt; ++t)
+      fwd_tile(t, nu, cf, th, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur, &rmax);
     if (nu == P.iters - 1 || P.record_all) {
       for (int off = 16; off > 0; off >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, off));
       if ((threadIdx.x & 31) == 0 && rmax > 0.0)
         atomicMax(P.resid + (P.record_all ? nu : 0), (unsigned long long)__double_as_longlong(rmax));
       rmax = 0.0;
     }
+    cf = cf_n;
+    th = th_n;
   }
 }
 
 }  // namespace tsmpc
 
 namespace tsmpc {
+
+cudaError_t sparse_launch(const SParams& S, int ctas, size_t smem, cudaStream_t stream) {
+  cudaError_t e = cudaMemcpyToSymbolAsync(g_sp, &S, sizeof(SParams), 0, cudaMemcpyHostToDevice, stream);
+  if (e != cudaSuccess) return e;
+  return cudaLaunchCooperativeKernel((void*)apg_sparse_kernel, dim3(ctas), dim3(kThreadsS), nullptr, smem, stream);
+}
 
 // beta_s = beta M (rows of the stage cache mapped to the structured basis,
 // elimination.py:156-157 with L replaced by Ls = L M).  One warp per edge row.
@@ -861,6 +990,7 @@ __global__ void beta_rotate_kernel(const double* __restrict__ beta, const double
     const double* b = beta + (size_t)e * NVP;
     for (int k = lane; k < nv; k += 32) {
       double s = 0.0;
+      #pragma unroll 1
       for (int j = 0; j < nv; ++j) s = fma(b[j], M[(size_t)j * nv + k], s);
       out[(size_t)e * NVP + k] = s;
     }

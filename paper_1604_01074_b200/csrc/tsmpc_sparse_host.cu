@@ -286,7 +286,11 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
   auto even = [](long long v) { return (v + 1) / 2 * 2; };
   long long off = 0;
   S.O_BND = 0;
-  off += even(4LL * NXP + 2LL * NUP);
+  off += even(5LL * NXP + 2LL * NUP);
+  S.O_SCL = (int)off;
+  off += even(4LL * N);
+  S.O_RED = (int)off;
+  off += 4 * 6 * 8 + (5 * kTileS + 1) / 2;  // epilogue partial norms + row descriptors
   S.O_SPV = (int)off;
   off += even(S.n_spv);
   S.O_NEED = (int)off;

@@ -30,9 +30,15 @@ for _ in range(a.reps):
     r = plan.solve(p, a.iters, 0.48, theta=th, coef=cf, keep_device=True, skip_gap=a.skip_gap)
 print(a.tree, plan.info(), f"loop {r['device_ms']:.3f} ms = {r['device_ms']*1e3/a.iters:.1f} us/iter")
 tm = plan.debug_timers()
-names = ["bwd fill", "bwd xiq scan", "bwd gemm1", "bwd g scan", "fwd t load", "fwd S scan",
-         "fwd gemm2", "fwd x scan", "fwd epilogue", "grid.sync", "trunk sweep", "trunk gemm",
-         "trunk rows"]
+import os
+if os.environ.get("TSMPC_DENSE_NAMES"):
+    names = ["bwd fill", "bwd xiq scan", "bwd gemm1", "bwd g scan", "fwd t load", "fwd S scan",
+             "fwd gemm2", "fwd x scan", "fwd epilogue", "grid.sync", "trunk sweep", "trunk gemm",
+             "trunk rows"]
+else:  # sparse kernel marks (tsmpc_sparse.cu)
+    names = ["bwd fill", "bwd xiq scan", "bwd h=Ls'z", "bwd g scan", "fwd S scan", "bwd z=B'xiq",
+             "fwd bv=B du", "fwd u, x scan", "fwd epilogue", "grid.sync", "trunk sweep", "fwd du=Lt S",
+             "trunk needs+own"]
 tot = float(tm.sum())
 if tot > 0:
     n = a.iters * a.reps
