@@ -126,12 +126,13 @@ struct SParams {
   const int* tsched;
   int n_tsched;
   // shared-memory layout, offsets in doubles from the dynamic base
-  int O_BND, O_SCL, O_RED, O_SPV, O_NEED, O_WORK, O_SLOT, O_INT;
+  int O_BND, O_SCL, O_RED, O_PSI, O_SPV, O_NEED, O_WORK, O_SLOT, O_INT;
+  int LA;                       // pitch of work region A: max(NXP, NVP)
   int n_work;                   // doubles in the work region
   int need_ld;                  // NVP + NXP + NUP  ([S | x | u] of one needed trunk edge)
   int need_max;
   int YW;                       // 2 NXP + NUP      ([sig | zeta | psi] of one dual row)
-  int slot_ld;                  // 2 YW + NXP + NUP + NVP
+  int slot_ld;                  // 2 YW + NXP + NUP (+ NVP when some CTA keeps t in its slot rows)
   int slot_rows;                // resident capacity of the slot region (rows)
   const double* beta_s;         // E x NVP  beta in the structured basis (beta M)
   double* TG;                   // E x NVP  t rows of streamed CTAs

@@ -50,7 +50,8 @@ __constant__ SParams g_sp;
 namespace {
 
 // ---- meta layout (ints, per CTA) -------------------------------------------
-//   [0] ntiles [1] nrows [2] nsegs [3] nneed [4] nlev [5] nown [6] resident [7] 0
+//   [0] ntiles [1] nrows [2] nsegs [3] nneed [4] nlev [5] nown [6] resident
+//   [7] tmode (where t rows live: 0 region A, 1 slot rows, 2 HBM)
 //   tiles : ntiles x {row0, nrows, seg0, nsegs}
 //   rows  : nrows  x {edge, stage, inv2p lo, inv2p hi}
 //   segs  : nsegs  x {lo, hi, pneed, 0}         (lo/hi relative to the tile)
@@ -59,11 +60,12 @@ namespace {
 //   own   : nown need indices (trunk rows whose epilogue this CTA runs)
 struct Meta {
   const int* m;
-  int ntiles, nrows, nsegs, nneed, nlev, nown, resident;
+  int ntiles, nrows, nsegs, nneed, nlev, nown, resident, tmode;
   const int *tiles, *rows, *segs, *needs, *lev, *own;
   __device__ void bind(const int* base) {
     m = base;
     ntiles = m[0]; nrows = m[1]; nsegs = m[2]; nneed = m[3]; nlev = m[4]; nown = m[5]; resident = m[6];
+    tmode = m[7];
     tiles = m + 8;
     rows = tiles + 4 * ntiles;
     segs = rows + 4 * nrows;
@@ -114,20 +116,23 @@ struct Ctx {
   Meta mt;
   double* bnd;     // x_s, x_min, x_max (NXP), u_min, u_max (NUP), a_diag (NXP), p (NXP)
   double* scl;     // sig, zeta, 1/sig, 1/zeta per stage (N each)
-  double* red;     // epilogue partial norms, then row descriptors
+  double* psi;     // psi_stage (N x NUP) or null (unscaled)
+  double* red;     // epilogue: partial norms [kTileS][4][2], factors [kTileS][2], row descriptors
   const int* spi;  // sparse index pool (shared)
   const double* spv;
   double* need;    // need rows [S | x | u]
-  double* work;    // XI | Z | H  (backward),  XB | DU | H=S  (forward)
+  double* work;    // region A (kTileS x LA) | region B (kTileS x NUP)
   double* slot;
-  int NXP, NUP, NVP, YW, SL, N;
+  int NXP, NUP, NVP, YW, SL, N, LA;
   int nx, nu, nv, E;
-  __device__ double* XI() const { return work; }
-  __device__ double* Z() const { return work + kTileS * NXP; }
-  __device__ double* H() const { return work + kTileS * (NXP + NUP); }
+  // region A: xiq -> h -> t (backward), S -> bv + e -> x (forward); region B: z / du -> u
+  __device__ double* A() const { return work; }
+  __device__ double* B() const { return work + kTileS * LA; }
   __device__ const double* adiag() const { return bnd + 3 * NXP + 2 * NUP; }
   __device__ const double* proot() const { return bnd + 4 * NXP + 2 * NUP; }
-  __device__ int* rdesc() const { return reinterpret_cast<int*>(red + kGroups * kRowsPT * 8); }
+  __device__ double* fac() const { return red + kTileS * 8; }
+  __device__ int* rdesc() const { return reinterpret_cast<int*>(red + kTileS * 10); }
+  __device__ double dpsi(int st, int k) const { return psi ? psi[st * NUP + k] : 1.0; }
 };
 
 __device__ __forceinline__ Ctx ctx_of() {
@@ -142,6 +147,8 @@ __device__ __forceinline__ Ctx ctx_of() {
   c.bnd = s_dyn + S.O_BND;
   c.scl = s_dyn + S.O_SCL;
   c.red = s_dyn + S.O_RED;
+  c.psi = P.scaled ? s_dyn + S.O_PSI : nullptr;
+  c.LA = S.LA;
   c.need = s_dyn + S.O_NEED;
   c.work = s_dyn + S.O_WORK;
   c.slot = s_dyn + S.O_SLOT;
@@ -253,28 +260,21 @@ __device__ __noinline__ void epilogue(int nu_it, double cf, double th, int nrows
   const int N = c.N;
   const bool xk = k < c.nx, uk = k < c.nu;
   const int* rd = c.rdesc();
-  double* red = c.red + (size_t)g * kRowsPT * 8;
   double rmax = *rmax_io;
-  // psi scaling of this thread's component for its rows (all loads in flight at once)
-  double dpv[kRowsPT];
-#pragma unroll
+  long long te_ = clock64();
+  (void)te_;
+  // pass 1: psi block (complete) and the warp sums of the squared distances of the
+  // state blocks
+#pragma unroll 2
   for (int m = 0; m < kRowsPT; ++m) {
     const int r = g + kGroups * m;
-    dpv[m] = 1.0;
-    if (P.scaled && uk && r < nrows) dpv[m] = __ldg(P.psi_stage + (size_t)rd[5 * r + 1] * c.NUP + k);
-  }
-  // pass 1: psi block (complete) and the partial squared distances of the state blocks
-  double ssv[kRowsPT], szv[kRowsPT];
-#pragma unroll
-  for (int m = 0; m < kRowsPT; ++m) {
-    const int r = g + kGroups * m;
-    ssv[m] = szv[m] = 0.0;
-    if (r >= nrows) continue;
+    if (r >= nrows) break;
     const int* d = rd + 5 * r;
     const int e = d[0], st = d[1];
     double* row = s_dyn + d[4];
     double* yc = row + (size_t)ysm * c.YW;
     double* yp = row + (size_t)(ysm ^ 1) * c.YW;
+    double ss = 0.0, sz = 0.0;
     if (xk) {
       const double ds = c.scl[st], dz = c.scl[N + st];
       const double ws = extrap(yc[k], yp[k], cf);
@@ -284,22 +284,19 @@ __device__ __noinline__ void epilogue(int nu_it, double cf, double th, int nrows
       const double tz = __dadd_rn(__dmul_rn(wz, ilam), __dmul_rn(xi, dz));
       const double gs_ = __dsub_rn(fmax(ts, __dmul_rn(ds, xs_s[k])), ts);
       const double gz = __dsub_rn(fmin(fmax(tz, __dmul_rn(dz, xmn_s[k])), __dmul_rn(dz, xmx_s[k])), tz);
-      ssv[m] = __dmul_rn(gs_, gs_);
-      szv[m] = __dmul_rn(gz, gz);
+      ss = __dmul_rn(gs_, gs_);
+      sz = __dmul_rn(gz, gz);
     }
     if (uk) {
       const double u = s_dyn[d[3] + k];
-      const double dp = dpv[m];
+      const double dp = c.dpsi(st, k);
       const double w = extrap(yc[2 * c.NXP + k], yp[2 * c.NXP + k], cf);
       const double hp = __dmul_rn(u, dp);
       const double a = __dadd_rn(__dmul_rn(w, ilam), hp);
       const double t = fmin(fmax(a, __dmul_rn(dp, umn_s[k])), __dmul_rn(dp, umx_s[k]));
       const double ny = __dadd_rn(w, __dmul_rn(lam, __dsub_rn(hp, t)));
       yp[2 * c.NXP + k] = ny;
-      if (want) {
-        const double rdp = P.scaled ? __ldg(P.psi_rcp + (size_t)st * c.NUP + k) : 1.0;
-        rmax = fmax(rmax, fabs(__dsub_rn(u, __dmul_rn(t, rdp))));
-      }
+      if (want) rmax = fmax(rmax, fabs(__dsub_rn(u, __ddiv_rn(t, dp))));
       double* ua = row + 2 * c.YW + c.NXP;
       const double na = __dadd_rn(__dmul_rn(ua[k], om), __dmul_rn(th, u));
       ua[k] = na;
@@ -309,44 +306,46 @@ __device__ __noinline__ void epilogue(int nu_it, double cf, double th, int nrows
       }
       if (last) stcg(P.U + (size_t)e * c.NUP + k, u);
     }
-  }
-  // warp sums of all rows at once (independent shuffle chains), fixed order
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1)
-#pragma unroll
-    for (int m = 0; m < kRowsPT; ++m) {
-      ssv[m] += __shfl_xor_sync(0xffffffffu, ssv[m], off);
-      szv[m] += __shfl_xor_sync(0xffffffffu, szv[m], off);
+    for (int off = 16; off > 0; off >>= 1) {
+      ss += __shfl_xor_sync(0xffffffffu, ss, off);
+      sz += __shfl_xor_sync(0xffffffffu, sz, off);
     }
-  if (lane == 0) {
-#pragma unroll
-    for (int m = 0; m < kRowsPT; ++m) {
-      red[(m * 4 + w4) * 2] = ssv[m];
-      red[(m * 4 + w4) * 2 + 1] = szv[m];
+    if (lane == 0) {
+      c.red[(r * 4 + w4) * 2] = ss;
+      c.red[(r * 4 + w4) * 2 + 1] = sz;
     }
   }
-  asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(kKW) : "memory");
+  __syncthreads();
+  TSMPC_MARK(P, 13, te_);
+  // pass 1.5: one thread per row -> the two prox factors min(1, weight / distance)
+  if (threadIdx.x < nrows) {
+    const int r = threadIdx.x, st = rd[5 * r + 1];
+    const double* q = c.red + r * 8;
+    const double ss = ((q[0] + q[2]) + q[4]) + q[6];
+    const double sz = ((q[1] + q[3]) + q[5]) + q[7];
+    const double dist_s = sqrt(ss), dist_z = sqrt(sz);
+    const double wgt_s = __dmul_rn(__dmul_rn(lam_p, P.Wx), c.scl[2 * N + st]);
+    const double wgt_z = __dmul_rn(__dmul_rn(lam_p, P.gamma_d), c.scl[3 * N + st]);
+    c.fac()[2 * r] = dist_s > wgt_s ? __ddiv_rn(wgt_s, dist_s) : 1.0;
+    c.fac()[2 * r + 1] = dist_z > wgt_z ? __ddiv_rn(wgt_z, dist_z) : 1.0;
+  }
+  __syncthreads();
+  TSMPC_MARK(P, 14, te_);
   // pass 2: the state blocks
   if (xk) {
-#pragma unroll
+#pragma unroll 2
     for (int m = 0; m < kRowsPT; ++m) {
       const int r = g + kGroups * m;
-      if (r >= nrows) continue;
+      if (r >= nrows) break;
       const int* d = rd + 5 * r;
       const int e = d[0], st = d[1];
       double* row = s_dyn + d[4];
       double* yc = row + (size_t)ysm * c.YW;
       double* yp = row + (size_t)(ysm ^ 1) * c.YW;
       double* xa = row + 2 * c.YW;
-      const double ss = ((red[m * 8] + red[m * 8 + 2]) + red[m * 8 + 4]) + red[m * 8 + 6];
-      const double sz = ((red[m * 8 + 1] + red[m * 8 + 3]) + red[m * 8 + 5]) + red[m * 8 + 7];
+      const double fs = c.fac()[2 * r], fz = c.fac()[2 * r + 1];
       const double ds = c.scl[st], dz = c.scl[N + st];
-      const double rds = c.scl[2 * N + st], rdz = c.scl[3 * N + st];
-      const double dist_s = sqrt(ss), dist_z = sqrt(sz);
-      const double wgt_s = __dmul_rn(__dmul_rn(lam_p, P.Wx), rds);
-      const double wgt_z = __dmul_rn(__dmul_rn(lam_p, P.gamma_d), rdz);
-      const double fs = dist_s > wgt_s ? __ddiv_rn(wgt_s, dist_s) : 1.0;
-      const double fz = dist_z > wgt_z ? __ddiv_rn(wgt_z, dist_z) : 1.0;
       const double ws = extrap(yc[k], yp[k], cf);
       const double wz = extrap(yc[c.NXP + k], yp[c.NXP + k], cf);
       const double xi = s_dyn[d[2] + k];
@@ -362,8 +361,8 @@ __device__ __noinline__ void epilogue(int nu_it, double cf, double th, int nrows
       yp[k] = ns;
       yp[c.NXP + k] = nz;
       if (want) {
-        rmax = fmax(rmax, fabs(__dsub_rn(xi, __dmul_rn(t_s, rds))));
-        rmax = fmax(rmax, fabs(__dsub_rn(xi, __dmul_rn(t_z, rdz))));
+        rmax = fmax(rmax, fabs(__dsub_rn(xi, __ddiv_rn(t_s, ds))));
+        rmax = fmax(rmax, fabs(__dsub_rn(xi, __ddiv_rn(t_z, dz))));
       }
       const double na = __dadd_rn(__dmul_rn(xa[k], om), __dmul_rn(th, xi));
       xa[k] = na;
@@ -375,24 +374,26 @@ __device__ __noinline__ void epilogue(int nu_it, double cf, double th, int nrows
       if (last) stcg(P.X + (size_t)(e + 1) * c.NXP + k, xi);
     }
   }
+  TSMPC_MARK(P, 15, te_);
   *rmax_io = rmax;
 }
 
 // ----------------------------------------------------------------------------
-// backward sweep of tile ti (reference factor.py:142-156)
+// backward sweep of tile ti (reference factor.py:142-156).  t rows go to region
+// A in place (tmode 0: the CTA's only tile stays in shared memory), to the
+// tile's slot rows (tmode 1) or to HBM (tmode 2, streamed CTAs).
 // ----------------------------------------------------------------------------
-__device__ __noinline__ void bwd_tile(int ti, double cf, int ysm, int srow0, bool resident,
-                                      int cur) {
+__device__ __noinline__ void bwd_tile(int ti, double cf, int ysm, int srow0, bool resident, int cur) {
   const SParams& S = g_sp;
   const Ctx c = ctx_of();
   const Params& P = S.P;
   const int* td = c.mt.tiles + 4 * ti;
   const int row0 = td[0], nrows = td[1], seg0 = td[2], nsegs = td[3];
   const int tid = threadIdx.x, k = tid & (kKW - 1), g = tid / kKW;
-  const int nx = c.nx, nu = c.nu, nv = c.nv, N = c.N;
-  double* XI = c.XI();
-  double* Z = c.Z();
-  double* H = c.H();
+  const int nx = c.nx, nu = c.nu, nv = c.nv, N = c.N, LA = c.LA;
+  const int tmode = c.mt.tmode;
+  double* RA = c.A();
+  double* RB = c.B();
   long long tm_ = clock64();
   (void)tm_;
   // prefetch beta_s (the bias of h) for this thread's rows
@@ -407,15 +408,8 @@ __device__ __noinline__ void bwd_tile(int ti, double cf, int ysm, int srow0, boo
     cp_wait<0>();
     __syncthreads();
   }
-  double dpv[kRowsPT];
-#pragma unroll
-  for (int m = 0; m < kRowsPT; ++m) {
-    const int r = g + kGroups * m;
-    dpv[m] = 1.0;
-    if (P.scaled && k < nu && r < nrows) dpv[m] = __ldg(P.psi_stage + (size_t)c.mt.stage(row0 + r) * c.NUP + k);
-  }
-  // (1) fill: s = D_sig w_sig + D_zeta w_zeta ; psi^ = D_psi w_psi
-#pragma unroll
+  // (1) fill: s = D_sig w_sig + D_zeta w_zeta -> A ; psi^ = D_psi w_psi -> B
+#pragma unroll 1
   for (int m = 0; m < kRowsPT; ++m) {
     const int r = g + kGroups * m;
     if (r >= nrows) break;
@@ -425,11 +419,11 @@ __device__ __noinline__ void bwd_tile(int ti, double cf, int ysm, int srow0, boo
     if (k < nx) {
       const double ws = extrap(yc[k], yp[k], cf);
       const double wz = extrap(yc[c.NXP + k], yp[c.NXP + k], cf);
-      XI[r * c.NXP + k] = __dadd_rn(__dmul_rn(ws, c.scl[st]), __dmul_rn(wz, c.scl[N + st]));
+      RA[r * LA + k] = __dadd_rn(__dmul_rn(ws, c.scl[st]), __dmul_rn(wz, c.scl[N + st]));
     }
     if (k < nu) {
       const double wp = extrap(yc[2 * c.NXP + k], yp[2 * c.NXP + k], cf);
-      Z[r * c.NUP + k] = P.scaled ? __dmul_rn(wp, dpv[m]) : wp;
+      RB[r * c.NUP + k] = c.psi ? __dmul_rn(wp, c.dpsi(st, k)) : wp;
     }
   }
   __syncthreads();
@@ -441,66 +435,72 @@ __device__ __noinline__ void bwd_tile(int ti, double cf, int ysm, int srow0, boo
     load_rows(c.mt.rows + 4 * tn[0], 4, tn[1], c.slot, ti > 0 ? 1 : 2, cur, ysm);
     cp_commit();
   }
-  // (2) xiq scan, tail -> head (leaf tails have no children)
+  // (2) xiq scan, tail -> head (leaf tails have no children: s + a .* 0 = s)
   const double* adiag = c.adiag();
-  #pragma unroll 1
+#pragma unroll 1
   for (int idx = tid; idx < nsegs * nx; idx += kThreadsS) {
     const int s = idx / nx, i = idx - s * nx;
     const int* sg = c.mt.segs + 4 * (seg0 + s);
     const int lo = sg[0], n = sg[1] - lo;
     const double a = adiag[i];
-    double* col = XI + lo * c.NXP + i;
-    double x = 0.0;  // leaf tail: no children (s + a .* 0 = s exactly)
+    double* col = RA + lo * LA + i;
+    double x = 0.0;
 #pragma unroll 1
     for (int j = n - 1; j >= 0; --j) {
-      x = __dadd_rn(col[j * c.NXP], __dmul_rn(x, a));
-      col[j * c.NXP] = x;
+      x = __dadd_rn(col[j * LA], __dmul_rn(x, a));
+      col[j * LA] = x;
     }
     if (sg[2] >= 0) stcg(P.XIQG + (size_t)c.mt.edge(row0 + lo) * c.NXP + i, x);
   }
   __syncthreads();
   TSMPC_MARK(P, 1, tm_);
-  // (3) z = psi^ + B' xiq   (column k of B)
+  // (3) z = psi^ + B' xiq   (column k of B)  B <- B + B' A
   if (k < nu) {
     const SpCol col = sp_col(c, S.Bc_ptr, S.Bc_idx, S.Bc_val, k);
 #pragma unroll
     for (int m = 0; m < kRowsPT; ++m) {
       const int r = g + kGroups * m;
-      if (r < nrows) Z[r * c.NUP + k] = sp_dot(c, col, S.Bc_idx, S.Bc_val, XI + r * c.NXP, Z[r * c.NUP + k]);
+      if (r < nrows) RB[r * c.NUP + k] = sp_dot(c, col, S.Bc_idx, S.Bc_val, RA + r * LA, RB[r * c.NUP + k]);
     }
   }
   __syncthreads();
   TSMPC_MARK(P, 5, tm_);
-  // (4) h = beta_s + Ls' z   (column k of Ls)
+  // (4) h = beta_s + Ls' z   (column k of Ls)  A <- beta_s + Ls' B
   if (k < nv) {
     const SpCol col = sp_col(c, S.Lc_ptr, S.Lc_idx, S.Lc_val, k);
 #pragma unroll
     for (int m = 0; m < kRowsPT; ++m) {
       const int r = g + kGroups * m;
-      if (r < nrows) H[r * c.NVP + k] = __dadd_rn(bpre[m], sp_dot(c, col, S.Lc_idx, S.Lc_val, Z + r * c.NUP, 0.0));
+      if (r < nrows) RA[r * LA + k] = __dadd_rn(bpre[m], sp_dot(c, col, S.Lc_idx, S.Lc_val, RB + r * c.NUP, 0.0));
     }
   }
   __syncthreads();
   TSMPC_MARK(P, 2, tm_);
   // (5) g scan, tail -> head: g_e = h_e + g_child ; t_e = g_e / (2 p_e)
-  #pragma unroll 1
+#pragma unroll 1
   for (int idx = tid; idx < nsegs * nv; idx += kThreadsS) {
     const int s = idx / nv, kk = idx - s * nv;
     const int* sg = c.mt.segs + 4 * (seg0 + s);
     const int lo = sg[0], n = sg[1] - lo;
-    const double* col = H + lo * c.NVP + kk;
+    double* col = RA + lo * LA + kk;
     double gv = 0.0;
-    if (resident) {
+    if (tmode == 0) {
+#pragma unroll 1
+      for (int j = n - 1; j >= 0; --j) {
+        gv = __dadd_rn(col[j * LA], gv);
+        col[j * LA] = __dmul_rn(gv, c.mt.inv2p(row0 + lo + j));
+      }
+    } else if (tmode == 1) {
       double* tcol = slot_row(c, srow0 + lo) + 2 * c.YW + c.NXP + c.NUP + kk;
 #pragma unroll 1
       for (int j = n - 1; j >= 0; --j) {
-        gv = __dadd_rn(col[j * c.NVP], gv);
+        gv = __dadd_rn(col[j * LA], gv);
         tcol[j * c.SL] = __dmul_rn(gv, c.mt.inv2p(row0 + lo + j));
       }
     } else {
 #pragma unroll 1
       for (int j = n - 1; j >= 0; --j) {
-        gv = __dadd_rn(col[j * c.NVP], gv);
+        gv = __dadd_rn(col[j * LA], gv);
         stcg(S.TG + (size_t)c.mt.edge(row0 + lo + j) * c.NVP + kk, __dmul_rn(gv, c.mt.inv2p(row0 + lo + j)));
       }
     }
@@ -521,19 +521,19 @@ __device__ __noinline__ void fwd_tile(int ti, int nu_it, double cf, double th, i
   const int* td = c.mt.tiles + 4 * ti;
   const int row0 = td[0], nrows = td[1], seg0 = td[2], nsegs = td[3];
   const int tid = threadIdx.x, k = tid & (kKW - 1), g = tid / kKW;
-  const int nx = c.nx, nu = c.nu, nv = c.nv;
-  double* XB = c.XI();
-  double* DU = c.Z();
-  double* SS = c.H();
+  const int nx = c.nx, nu = c.nu, nv = c.nv, LA = c.LA;
+  const int tmode = c.mt.tmode;
+  double* RA = c.A();
+  double* RB = c.B();
   long long tm_ = clock64();
   (void)tm_;
   if (!resident) {
-    // t rows of this tile -> S region; then (after the previous epilogue) the slot
+    // t rows of this tile -> region A; then (after the previous epilogue) the slot
     const int hv = c.NVP / 2;
-    #pragma unroll 1
+#pragma unroll 1
     for (int idx = tid; idx < nrows * hv; idx += kThreadsS) {
       const int r = idx / hv, kk = idx - r * hv;
-      cp16(SS + r * c.NVP + 2 * kk, S.TG + (size_t)c.mt.edge(row0 + r) * c.NVP + 2 * kk);
+      cp16(RA + r * LA + 2 * kk, S.TG + (size_t)c.mt.edge(row0 + r) * c.NVP + 2 * kk);
     }
     cp_commit();
     if (ti > 0) load_rows(c.mt.rows + 4 * row0, 4, nrows, c.slot, 3, cur, ysm);
@@ -555,69 +555,69 @@ __device__ __noinline__ void fwd_tile(int ti, int nu_it, double cf, double th, i
     cp_wait<1>();
     __syncthreads();
   }
-  // (1) S scan, head -> tail: S_e = t_e + S_parent
-  #pragma unroll 1
+  // (1) S scan, head -> tail: S_e = t_e + S_parent  (A, in place unless tmode 1)
+#pragma unroll 1
   for (int idx = tid; idx < nsegs * nv; idx += kThreadsS) {
     const int s = idx / nv, kk = idx - s * nv;
     const int* sg = c.mt.segs + 4 * (seg0 + s);
     const int lo = sg[0], n = sg[1] - lo, pn = sg[2];
-    const double* tcol = resident ? slot_row(c, srow0 + lo) + 2 * c.YW + c.NXP + c.NUP + kk : SS + lo * c.NVP + kk;
-    const int tld = resident ? c.SL : c.NVP;
-    double* scol = SS + lo * c.NVP + kk;
+    double* scol = RA + lo * LA + kk;
+    const double* tcol = tmode == 1 ? slot_row(c, srow0 + lo) + 2 * c.YW + c.NXP + c.NUP + kk : scol;
+    const int tld = tmode == 1 ? c.SL : LA;
     double Sv = pn >= 0 ? c.need[(size_t)pn * S.need_ld + kk] : 0.0;
 #pragma unroll 1
     for (int j = 0; j < n; ++j) {
       Sv = __dadd_rn(tcol[j * tld], Sv);
-      scol[j * c.NVP] = Sv;
+      scol[j * LA] = Sv;
     }
   }
   __syncthreads();
   TSMPC_MARK(P, 4, tm_);
-  // (2) du = Lt S   (row k of Lt)
+  // (2) du = Lt S   (row k of Lt)  B <- Lt A
   if (k < nu) {
     const SpCol col = sp_col(c, S.Lr_ptr, S.Lr_idx, S.Lr_val, k);
 #pragma unroll
     for (int m = 0; m < kRowsPT; ++m) {
       const int r = g + kGroups * m;
-      if (r < nrows) DU[r * c.NUP + k] = sp_dot(c, col, S.Lr_idx, S.Lr_val, SS + r * c.NVP, 0.0);
+      if (r < nrows) RB[r * c.NUP + k] = sp_dot(c, col, S.Lr_idx, S.Lr_val, RA + r * LA, 0.0);
     }
   }
   __syncthreads();
   TSMPC_MARK(P, 11, tm_);
-  // (3) bv + e = B du + e   (row k of B)
+  // (3) bv + e = B du + e   (row k of B)  A <- B B + e
   if (k < nx) {
     const SpCol col = sp_col(c, S.Br_ptr, S.Br_idx, S.Br_val, k);
 #pragma unroll
     for (int m = 0; m < kRowsPT; ++m) {
       const int r = g + kGroups * m;
-      if (r < nrows) XB[r * c.NXP + k] = __dadd_rn(sp_dot(c, col, S.Br_idx, S.Br_val, DU + r * c.NUP, 0.0), epre[m]);
+      if (r < nrows) RA[r * LA + k] = __dadd_rn(sp_dot(c, col, S.Br_idx, S.Br_val, RB + r * c.NUP, 0.0), epre[m]);
     }
   }
   __syncthreads();
   TSMPC_MARK(P, 6, tm_);
-  // (4) u = uhat + du ; x scan, head -> tail: x = a .* x_anc + (bv + e) ; row descriptors
+  // (4) u = uhat + du (B) ; x scan, head -> tail: x = a .* x_anc + (bv + e) (A) ; row descriptors
   if (k < nu) {
 #pragma unroll
     for (int m = 0; m < kRowsPT; ++m) {
       const int r = g + kGroups * m;
-      if (r < nrows) DU[r * c.NUP + k] = __dadd_rn(DU[r * c.NUP + k], upre[m]);
+      if (r < nrows) RB[r * c.NUP + k] = __dadd_rn(RB[r * c.NUP + k], upre[m]);
     }
   }
   {
     const double* adiag = c.adiag();
     const double* pr = c.proot();
-    #pragma unroll 1
+#pragma unroll 1
     for (int idx = tid; idx < nsegs * nx; idx += kThreadsS) {
       const int s = idx / nx, i = idx - s * nx;
       const int* sg = c.mt.segs + 4 * (seg0 + s);
       const int lo = sg[0], n = sg[1] - lo, pn = sg[2];
-      double* col = XB + lo * c.NXP + i;
+      double* col = RA + lo * LA + i;
       double x = pn >= 0 ? c.need[(size_t)pn * S.need_ld + c.NVP + i] : pr[i];
       const double a = adiag[i];
 #pragma unroll 1
       for (int j = 0; j < n; ++j) {
-        x = __dadd_rn(__dmul_rn(x, a), col[j * c.NXP]);
-        col[j * c.NXP] = x;
+        x = __dadd_rn(__dmul_rn(x, a), col[j * LA]);
+        col[j * LA] = x;
       }
     }
   }
@@ -625,8 +625,8 @@ __device__ __noinline__ void fwd_tile(int ti, int nu_it, double cf, double th, i
     int* d = c.rdesc() + 5 * tid;
     d[0] = c.mt.edge(row0 + tid);
     d[1] = c.mt.stage(row0 + tid);
-    d[2] = (int)(XB + tid * c.NXP - s_dyn);
-    d[3] = (int)(DU + tid * c.NUP - s_dyn);
+    d[2] = (int)(RA + tid * LA - s_dyn);
+    d[3] = (int)(RB + tid * c.NUP - s_dyn);
     d[4] = (int)(slot_row(c, srow0 + tid) - s_dyn);
   }
   if (!resident) cp_wait<0>();
@@ -653,7 +653,7 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
   if (nc <= 0) return;
   const int* g = S.tsched;
   const int T = __ldg(g), nlev = __ldg(g + 1);
-  double* Zs = c.work;
+  double* Zs = c.B();
   double* Xs = Zs + (size_t)T * nc;
   int* sch = reinterpret_cast<int*>(Xs + (size_t)T * nc);
   #pragma unroll 1
@@ -693,7 +693,7 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
       const int j = q - c.nv - c.nx;
       const size_t o = 2 * E * c.NXP + (size_t)a * c.NUP + j;
       const double wp = extrap(ldcg(Y + o), ldcg(Yp + o), cf);
-      z = P.scaled ? __dmul_rn(wp, __ldg(P.psi_stage + (size_t)st * c.NUP + j)) : wp;
+      z = c.psi ? __dmul_rn(wp, c.dpsi(st, j)) : wp;
     }
     Zs[idx] = z;
     Xs[idx] = x;
@@ -759,8 +759,8 @@ __device__ __noinline__ void trunk_needs() {
   if (nn == 0) return;
   const int nx = c.nx, nu = c.nu, nv = c.nv;
   const int LD = S.need_ld;
-  double* Yz = c.work;                       // nn x NUP
-  double* DU = c.work + (size_t)nn * c.NUP;  // nn x NUP
+  double* Yz = c.B();                        // nn x NUP
+  double* DU = c.B() + (size_t)nn * c.NUP;   // nn x NUP
   const int* nd = c.mt.needs;
   // (1) Yz = Ypsi + B' Yx
   {
@@ -848,7 +848,7 @@ __device__ __noinline__ void trunk_own_rows(int nu_it, double cf, double th, int
   const Ctx c = ctx_of();
   const int no = c.mt.nown;
   if (no == 0) return;
-  const int cap = max(1, min(kTileS, S.n_work / c.SL));
+  const int cap = max(1, min(kTileS, (kTileS * c.NUP) / c.SL));
   const int LD = S.need_ld;
   for (int b0 = 0; b0 < no; b0 += cap) {
     const int nb = min(cap, no - b0);
@@ -860,11 +860,11 @@ __device__ __noinline__ void trunk_own_rows(int nu_it, double cf, double th, int
       d[1] = c.mt.needs[4 * n + 3];
       d[2] = (int)(c.need + (size_t)n * LD + c.NVP - s_dyn);
       d[3] = (int)(c.need + (size_t)n * LD + c.NVP + c.NXP - s_dyn);
-      d[4] = (int)(c.work + (size_t)threadIdx.x * c.SL - s_dyn);
+      d[4] = (int)(c.B() + (size_t)threadIdx.x * c.SL - s_dyn);
     }
     __syncthreads();
     // stage the rows into the work region in slot format (dual at index 0 = HBM cur)
-    load_rows(c.rdesc(), 5, nb, c.work, 3, cur, 0);
+    load_rows(c.rdesc(), 5, nb, c.B(), 3, cur, 0);
     cp_commit();
     cp_wait<0>();
     __syncthreads();
@@ -902,6 +902,11 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
       scl[N + j] = P.scaled ? P.zeta_stage[j] : 1.0;
       scl[2 * N + j] = P.scaled ? P.sig_rcp[j] : 1.0;
       scl[3 * N + j] = P.scaled ? P.zeta_rcp[j] : 1.0;
+    }
+    if (P.scaled) {
+      double* psi = s_dyn + S.O_PSI;
+#pragma unroll 1
+      for (int i = threadIdx.x; i < N * NUP; i += kThreadsS) psi[i] = P.psi_stage[i];
     }
     int* ints = reinterpret_cast<int*>(s_dyn + S.O_INT);
     const int m0 = __ldg(S.meta_ptr + blockIdx.x), m1 = __ldg(S.meta_ptr + blockIdx.x + 1);

@@ -279,66 +279,104 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
     meta_max = std::max(meta_max, (int)metas[c].size());
     out.meta_ptr[c + 1] = out.meta_ptr[c] + (int)metas[c].size();
   }
+  auto even = [](long long v) { return (v + 1) / 2 * 2; };
   S.YW = 2 * NXP + NUP;
-  S.slot_ld = 2 * S.YW + NXP + NUP + NVP;
   S.need_ld = NVP + NXP + NUP;
   S.need_max = need_max;
-  auto even = [](long long v) { return (v + 1) / 2 * 2; };
+  S.LA = (int)even(std::max(NXP, NVP));
   long long off = 0;
   S.O_BND = 0;
   off += even(5LL * NXP + 2LL * NUP);
   S.O_SCL = (int)off;
   off += even(4LL * N);
   S.O_RED = (int)off;
-  off += 4 * 6 * 8 + (5 * kTileS + 1) / 2;  // epilogue partial norms + row descriptors
+  off += 10LL * kTileS + (5 * kTileS + 1) / 2 + 1;  // partial norms, factors, row descriptors
+  off = even(off);
+  S.O_PSI = (int)off;
+  off += even((long long)N * NUP);
   S.O_SPV = (int)off;
   off += even(S.n_spv);
   S.O_NEED = (int)off;
   off += (long long)need_max * S.need_ld;
   S.O_WORK = (int)off;
-  const int ncomp = nv + nx + nu;
-  const int nc_max = (ncomp + C - 1) / C;
-  long long work = (long long)kTileS * (NXP + NUP + NVP);
-  work = std::max(work, 2LL * need_max * NUP);
-  work = std::max(work, 2LL * T * nc_max + ((long long)out.tsched.size() + 1) / 2 + 2);
-  work = std::max(work, (long long)S.slot_ld);  // one own trunk row at a time at least
-  S.n_work = (int)even(work);
+  S.n_work = (int)even((long long)kTileS * (S.LA + NUP));
   off += S.n_work;
+  // the trunk phases run in work region B (kTileS x NUP)
+  {
+    const int ncomp = nv + nx + nu;
+    const long long nc_max = (ncomp + C - 1) / C;
+    const long long regB = (long long)kTileS * NUP;
+    const long long sweep = 2LL * T * nc_max + ((long long)out.tsched.size() + 1) / 2 + 2;
+    const long long needs = 2LL * need_max * NUP;
+    const long long stage1 = 2LL * S.YW + NXP + NUP + NVP;
+    if (sweep > regB || needs > regB || stage1 > regB) {
+      out.why = "trunk too large for the work region";
+      return out;
+    }
+  }
   S.O_SLOT = (int)off;
   const long long ints_d = ((long long)meta_max + S.n_spi + 1) / 2 + 1;
   const long long limit_d = (long long)(smem_limit / sizeof(double));
   const long long slot_avail = limit_d - off - ints_d;
-  // resident rows carry their t row (slot_ld); a streamed tile slot does not
-  const long long stream_ld = 2LL * S.YW + NXP + NUP;
-  const long long slot_rows = slot_avail / S.slot_ld;
-  if (slot_avail / stream_ld < kTileS) {
+  // slot rows: both dual rows + ergodic rows; t rows join them only for resident
+  // CTAs with several tiles (tmode 1); a single resident tile keeps t in region A
+  const long long base_ld = 2LL * S.YW + NXP + NUP;
+  const long long t_ld = base_ld + NVP;
+  if (slot_avail / base_ld < kTileS) {
     out.why = "shared memory too small for one tile slot";
     return out;
   }
   int max_rows = 0;
   for (int c = 0; c < C; ++c) max_rows = std::max(max_rows, cta_rows[c]);
-  // size the slot region for the largest resident CTA (or one tile when streaming)
-  long long want_rows = 0;
-  int resident = 0;
-  for (int c = 0; c < C; ++c)
-    if (cta_rows[c] <= slot_rows) want_rows = std::max<long long>(want_rows, cta_rows[c]);
-  if (want_rows == 0) {
-    S.slot_ld = (int)stream_ld;
-    want_rows = kTileS;
-  } else if (want_rows < kTileS) {
-    want_rows = std::min<long long>(kTileS, slot_rows);
+  std::vector<int> ntiles_c(C);
+  for (int c = 0; c < C; ++c) ntiles_c[c] = metas[c][0];
+  // resident: all rows of the CTA fit; multi-tile residents need the t column
+  auto plan_ld = [&](long long ld, long long& rows_out, int& res_out, bool& need_t) {
+    const long long cap = slot_avail / ld;
+    rows_out = 0;
+    res_out = 0;
+    need_t = false;
+    for (int c = 0; c < C; ++c)
+      if (cta_rows[c] <= cap) {
+        rows_out = std::max<long long>(rows_out, cta_rows[c]);
+        ++res_out;
+        if (ntiles_c[c] > 1) need_t = true;
+      }
+  };
+  long long rows_b, rows_t;
+  int res_b, res_t;
+  bool nt_b, nt_t;
+  plan_ld(base_ld, rows_b, res_b, nt_b);
+  plan_ld(t_ld, rows_t, res_t, nt_t);
+  long long slot_ld, want_rows;
+  if (!nt_b) {  // no multi-tile resident CTA with the narrow pitch
+    slot_ld = base_ld;
+    want_rows = rows_b;
+  } else {      // multi-tile residents need t in the slot: use the wide pitch
+    slot_ld = t_ld;
+    want_rows = rows_t;
   }
-  if (want_rows < kTileS && want_rows * S.slot_ld < kTileS * stream_ld) {
+  const bool any_stream = (slot_ld == base_ld ? res_b : res_t) < C;
+  if (any_stream) want_rows = std::max<long long>(want_rows, kTileS);  // one streamed tile slot
+  if (want_rows * slot_ld > slot_avail) want_rows = slot_avail / slot_ld;
+  if (any_stream && want_rows < kTileS && want_rows * slot_ld < kTileS * base_ld) {
     out.why = "shared memory too small for one tile slot";
     return out;
   }
+  S.slot_ld = (int)slot_ld;
+  int resident = 0;
   for (int c = 0; c < C; ++c) {
     const bool res = cta_rows[c] <= want_rows;
     metas[c][6] = res ? 1 : 0;
+    metas[c][7] = !res ? 2 : (ntiles_c[c] <= 1 ? 0 : 1);
+    if (res && ntiles_c[c] > 1 && slot_ld != t_ld) {  // cannot happen by construction
+      out.why = "internal: multi-tile resident CTA without a t column";
+      return out;
+    }
     resident += res;
   }
   S.slot_rows = (int)want_rows;
-  off += want_rows * S.slot_ld;
+  off += want_rows * slot_ld;
   S.O_INT = (int)off;
   off += ints_d;
   S.meta_max = meta_max;

@@ -14,6 +14,7 @@ ap.add_argument("--tree", default="CE")
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--skip-gap", action="store_true")
+ap.add_argument("--plain", action="store_true", help="no dual preconditioner (identity scaling)")
 a = ap.parse_args()
 m = synth.bcn63_network()
 t = synth.paper_tree(*synth.PAPER_TREES[a.tree])
@@ -23,7 +24,7 @@ s = compute_preconditioner(b, m, t.N, tree=t)
 p, q = synth.initial_state(m)
 fc = synth.forecast_for(t)
 c = build_stage_cache(b, m, t, node_demands(t, fc), k=0, q=q)
-plan = DevicePlan(m, t, f, s)
+plan = DevicePlan(m, t, f, None if a.plain else s)
 plan.set_cache(c, m)
 th, cf = theta_schedule(a.iters)
 for _ in range(a.reps):
@@ -38,7 +39,7 @@ if os.environ.get("TSMPC_DENSE_NAMES"):
 else:  # sparse kernel marks (tsmpc_sparse.cu)
     names = ["bwd fill", "bwd xiq scan", "bwd h=Ls'z", "bwd g scan", "fwd S scan", "bwd z=B'xiq",
              "fwd bv=B du", "fwd u, x scan", "fwd epilogue", "grid.sync", "trunk sweep", "fwd du=Lt S",
-             "trunk needs+own"]
+             "trunk needs+own", " epi pass1", " epi bar", " epi pass2"]
 tot = float(tm.sum())
 if tot > 0:
     n = a.iters * a.reps
