@@ -111,6 +111,24 @@ typedef struct tsmpc_result {
 tsmpc_plan* tsmpc_plan_create(const tsmpc_problem* prob, int device);
 void tsmpc_plan_destroy(tsmpc_plan* plan);
 
+/* Subtree sharding across the GPUs of one node (one process per GPU).  Rank 0
+ * creates an NCCL unique id (128 bytes) with tsmpc_nccl_unique_id and shares it
+ * (e.g. torch.distributed broadcast); every rank then creates its shard plan.
+ * The trunk (edges above the leaf chains) is replicated; the leaf chains are
+ * split by the trunk node they hang from.  tsmpc_solve on a shard plan runs, per
+ * iteration, phase 1 -> ncclAllReduce of the per-trunk-node chain-head sums ->
+ * phase 2, and returns results for tsmpc_plan_edges(plan, 0, ...) only; the
+ * residual is the max over ranks; the duality gap is not evaluated (NaN).
+ * Replaces the reference's intra-stage thread pool (pkg/src/treesmpc/_parallel.py,
+ * factor.py:107-128) at the node level.  Requires the structured-basis kernel. */
+int tsmpc_nccl_unique_id(uint8_t* out128);
+tsmpc_plan* tsmpc_plan_create_shard(const tsmpc_problem* prob, int device, int32_t rank,
+                                    int32_t world, const uint8_t* nccl_id128);
+/* Edges whose rows a plan computes (which = 0: all for a single-GPU plan, owned
+ * chains + trunk for a shard plan; which = 1: trunk edges).  Writes up to cap
+ * edge ids to out (may be NULL) and returns the count (or a negative status). */
+int tsmpc_plan_edges(const tsmpc_plan* plan, int32_t which, int64_t* out, int64_t cap);
+
 /* Per-forecast stage cache (elimination.py:114-158).
  * beta n_edges*n_v, uhat n_edges*n_u, evec n_edges*n_x, q n_u,
  * prices N*n_u (alpha1 + alpha2(k+j) per stage), jrhs n_edges*n_e (= -Ed d per
@@ -160,6 +178,12 @@ int tsmpc_describe_tree(const tsmpc_problem* prob, int32_t max_ctas, int32_t col
  * trunk_edges, resident_ctas, max_rows_per_cta, max_needs, smem_bytes}. */
 int tsmpc_describe_sparse(const tsmpc_problem* prob, int32_t max_ctas, int64_t smem_limit,
                           int64_t* info, int32_t n_info);
+/* Host-only planning of one shard: info = {ctas, owned_chains, owned_rows,
+ * trunk_edges, total_chains, owned_trunk_nodes, smem_bytes}; the owned chain
+ * edges go to edges[0..cap) when edges != NULL. */
+int tsmpc_describe_shard(const tsmpc_problem* prob, int32_t max_ctas, int64_t smem_limit,
+                         int32_t rank, int32_t world, int64_t* info, int32_t n_info,
+                         int64_t* edges, int64_t cap);
 const char* tsmpc_last_error(void);
 /* Which persistent kernel tsmpc_solve runs: "sparse" (structured basis,
  * tsmpc_sparse.cu) or "dense: <reason>" (fused-operator DMMA kernel). */

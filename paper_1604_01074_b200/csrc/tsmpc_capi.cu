@@ -10,6 +10,7 @@
 
 #include "../../include/tsmpc.h"
 #include "tsmpc_aux.cuh"
+#include "tsmpc_nccl.h"
 #include "tsmpc_sparse_host.h"
 
 using namespace tsmpc;
@@ -76,6 +77,13 @@ struct tsmpc_plan {
   size_t sp_smem = 0;
   double *BETA_S = nullptr, *TG = nullptr, *KY_S = nullptr, *MS = nullptr;
   std::string sp_why;
+  // subtree sharding across GPUs (tsmpc_plan_create_shard)
+  bool sharded = false;
+  int rank = 0, world = 1, total_chains = 0;
+  const NcclApi* nccl = nullptr;
+  void* comm = nullptr;
+  double* HS = nullptr;
+  std::vector<int> owned_edges, trunk_edges;
   // plan stats
   int n_levels = 0, n_tiles = 0, n_segs = 0, n_ctas = 0, n_trunk = 0;
   int dyk_blocks = 0;
@@ -115,6 +123,7 @@ struct tsmpc_plan {
   }
   ~tsmpc_plan() {
     if (stream) cudaStreamSynchronize(stream);
+    if (comm && nccl) nccl->CommDestroy(comm);
     for (void* p : allocs) cudaFree(p);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -317,7 +326,9 @@ int tsmpc_device_count(void) {
   return n;
 }
 
-tsmpc_plan* tsmpc_plan_create(const tsmpc_problem* pb, int device) {
+static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int srank, int sworld,
+                                    const void* nccl_id) {
+  const bool shard = srank >= 0;
   if (!pb) { fail(TSMPC_ERR_ARGUMENT, "null problem"); return nullptr; }
   const int nx = pb->n_x, nu = pb->n_u, nv = pb->n_v, ne = pb->n_e, N = pb->N, n_nodes = pb->n_nodes;
   if (nx < 1 || nu < 1 || nv < 1 || ne < 1 || N < 1 || n_nodes < 2) {
@@ -663,7 +674,8 @@ tsmpc_plan* tsmpc_plan_create(const tsmpc_problem* pb, int device) {
     else {
       SparseTreeIn ti{N, n_nodes, pb->stage_starts, pb->anc, pb->child_start, pb->child_stop, pb->prob};
       SparseOpsIn oi{nx, nu, nv, pb->B, pb->Ls, pb->lam_s};
-      SparseHostPlan hp = plan_sparse(ti, oi, NXP, NUP, NVP, pl->sm_count, (size_t)prop.sharedMemPerBlockOptin);
+      SparseHostPlan hp = plan_sparse(ti, oi, NXP, NUP, NVP, pl->sm_count, (size_t)prop.sharedMemPerBlockOptin,
+                                      shard, shard ? srank : 0, shard ? sworld : 1);
       int occ_s = 0;
       if (hp.ok) {
         if (cudaFuncSetAttribute(apg_sparse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hp.smem) !=
@@ -693,6 +705,22 @@ tsmpc_plan* tsmpc_plan_create(const tsmpc_problem* pb, int device) {
         S = hp.S;
         S.spi = d_spi; S.spv = d_spv; S.meta = d_meta; S.meta_ptr = d_mptr; S.tsched = d_ts;
         S.beta_s = pl->BETA_S; S.TG = pl->TG;
+        S.HS_LD = NVP + NXP;
+        if (shard) {
+          unsigned char* d_tow;
+          rc |= pl->upload(&d_tow, hp.towned.data(), std::max<size_t>(1, hp.towned.size()));
+          rc |= pl->alloc(&pl->HS, (size_t)std::max(1, hp.n_trunk) * S.HS_LD);
+          if (rc) return bail(0);
+          S.sharded = 1;
+          S.HS = pl->HS;
+          S.towned = d_tow;
+          pl->sharded = true;
+          pl->rank = srank;
+          pl->world = sworld;
+          pl->total_chains = hp.total_chains;
+          pl->owned_edges = hp.owned_edges;
+          pl->trunk_edges = hp.trunk_edge;
+        }
         pl->use_sparse = true;
         pl->sp_ctas = hp.n_ctas;
         pl->sp_smem = hp.smem;
@@ -705,6 +733,24 @@ tsmpc_plan* tsmpc_plan_create(const tsmpc_problem* pb, int device) {
     }
   }
 
+  if (shard && !pl->use_sparse) {
+    fail(TSMPC_ERR_VALIDATION, "subtree sharding needs the structured-basis kernel (%s)", pl->sp_why.c_str());
+    return bail(0);
+  }
+  if (shard) {
+    std::string why;
+    pl->nccl = nccl_api(why);
+    if (!pl->nccl) { fail(TSMPC_ERR_NCCL, "%s", why.c_str()); return bail(0); }
+    NcclApi::UniqueId id;
+    std::memcpy(id.internal, nccl_id, sizeof(id.internal));
+    const int nr = pl->nccl->CommInitRank(&pl->comm, sworld, id, srank);
+    if (nr != 0) {
+      pl->comm = nullptr;
+      fail(TSMPC_ERR_NCCL, "ncclCommInitRank(rank %d of %d): %s", srank, sworld, pl->nccl->GetErrorString(nr));
+      return bail(0);
+    }
+  }
+
   int occ_d = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_d, gap_project_dykstra_kernel, 256, 0);
   pl->dyk_blocks = std::max(1, std::min(occ_d, 4)) * pl->sm_count;
@@ -713,6 +759,53 @@ tsmpc_plan* tsmpc_plan_create(const tsmpc_problem* pb, int device) {
     return bail(0);
   }
   return pl;
+}
+
+tsmpc_plan* tsmpc_plan_create(const tsmpc_problem* pb, int device) {
+  return plan_create_impl(pb, device, -1, 1, nullptr);
+}
+
+int tsmpc_nccl_unique_id(uint8_t* out) {
+  if (!out) return fail(TSMPC_ERR_ARGUMENT, "null argument");
+  std::string why;
+  const NcclApi* api = nccl_api(why);
+  if (!api) return fail(TSMPC_ERR_NCCL, "%s", why.c_str());
+  NcclApi::UniqueId id;
+  const int r = api->GetUniqueId(&id);
+  if (r != 0) return fail(TSMPC_ERR_NCCL, "ncclGetUniqueId: %s", api->GetErrorString(r));
+  std::memcpy(out, id.internal, sizeof(id.internal));
+  return TSMPC_OK;
+}
+
+tsmpc_plan* tsmpc_plan_create_shard(const tsmpc_problem* pb, int device, int32_t rank, int32_t world,
+                                    const uint8_t* nccl_id) {
+  if (!nccl_id || world < 1 || rank < 0 || rank >= world) {
+    fail(TSMPC_ERR_ARGUMENT, "invalid shard arguments (rank %d of %d)", rank, world);
+    return nullptr;
+  }
+  return plan_create_impl(pb, device, rank, world, nccl_id);
+}
+
+int tsmpc_plan_edges(const tsmpc_plan* pl, int32_t which, int64_t* out, int64_t cap) {
+  if (!pl) return fail(TSMPC_ERR_ARGUMENT, "null argument");
+  std::vector<int> all;
+  const std::vector<int>* v = &all;
+  if (which == 0) {  // edges whose results this plan computes
+    if (!pl->sharded) {
+      for (int e = 0; e < pl->E; ++e) all.push_back(e);
+    } else {
+      all = pl->owned_edges;
+      all.insert(all.end(), pl->trunk_edges.begin(), pl->trunk_edges.end());
+      std::sort(all.begin(), all.end());
+    }
+  } else if (which == 1) {
+    v = &pl->trunk_edges;
+  } else {
+    return fail(TSMPC_ERR_ARGUMENT, "which must be 0 (owned) or 1 (trunk)");
+  }
+  if (out)
+    for (int64_t i = 0; i < cap && i < (int64_t)v->size(); ++i) out[i] = (*v)[i];
+  return (int)v->size();
 }
 
 void tsmpc_plan_destroy(tsmpc_plan* plan) { delete plan; }
@@ -762,13 +855,35 @@ int tsmpc_describe_sparse(const tsmpc_problem* pb, int32_t max_ctas, int64_t sme
   return TSMPC_OK;
 }
 
+int tsmpc_describe_shard(const tsmpc_problem* pb, int32_t max_ctas, int64_t smem_limit, int32_t rank,
+                         int32_t world, int64_t* info, int32_t n, int64_t* edges, int64_t cap) {
+  if (!pb || !info || !pb->anc || !pb->child_start || !pb->child_stop || !pb->stage_starts || !pb->prob ||
+      !pb->B || !pb->Ls || !pb->lam_s)
+    return fail(TSMPC_ERR_ARGUMENT, "null argument");
+  SparseTreeIn ti{pb->N, pb->n_nodes, pb->stage_starts, pb->anc, pb->child_start, pb->child_stop, pb->prob};
+  SparseOpsIn oi{pb->n_x, pb->n_u, pb->n_v, pb->B, pb->Ls, pb->lam_s};
+  SparseHostPlan hp = plan_sparse(ti, oi, r4(pb->n_x), r4(pb->n_u), r4(pb->n_v), std::max(1, (int)max_ctas),
+                                  (size_t)smem_limit, true, rank, world);
+  if (!hp.ok) return fail(TSMPC_ERR_VALIDATION, "%s", hp.why.c_str());
+  int64_t owned_heads = 0;
+  for (unsigned char t : hp.towned) owned_heads += t;
+  const int64_t vals[] = {hp.n_ctas, hp.n_chains, hp.owned_rows, hp.n_trunk, hp.total_chains, owned_heads,
+                          (int64_t)hp.smem};
+  for (int i = 0; i < n && i < (int)(sizeof(vals) / sizeof(vals[0])); ++i) info[i] = vals[i];
+  if (edges)
+    for (int64_t i = 0; i < cap && i < (int64_t)hp.owned_edges.size(); ++i) edges[i] = hp.owned_edges[i];
+  return TSMPC_OK;
+}
+
 int tsmpc_plan_info(const tsmpc_plan* pl, int64_t* info, int32_t n) {
   if (!pl || !info) return fail(TSMPC_ERR_ARGUMENT, "null argument");
   const bool sp = pl->use_sparse;
   const int64_t vals[] = {pl->n_levels, sp ? pl->sp_ctas : pl->n_ctas, sp ? pl->sp_tiles : pl->n_tiles,
                           pl->n_segs, (int64_t)(sp ? pl->sp_smem : pl->smem), pl->base.diagA,
                           sp ? kThreadsS : kThreads, sp ? kTileS : kTileM, pl->sm_count, pl->base.collapsed,
-                          sp ? pl->sp_trunk : pl->n_trunk, sp ? 1 : 0, pl->sp_resident};
+                          sp ? pl->sp_trunk : pl->n_trunk, sp ? 1 : 0, pl->sp_resident,
+                          pl->sharded ? 1 : 0, pl->rank, pl->world, (int64_t)pl->owned_edges.size(),
+                          pl->total_chains};
   for (int i = 0; i < n && i < (int)(sizeof(vals) / sizeof(vals[0])); ++i) info[i] = vals[i];
   return TSMPC_OK;
 }
@@ -956,8 +1071,34 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
     S.P = P;
     S.P.KY = pl->KY_S;
     S.P.n_trunk = pl->sp_trunk;
-    CU(sparse_launch(S, pl->sp_ctas, pl->sp_smem, pl->stream));
-    ++pl->launches;
+    if (!pl->sharded) {
+      S.nu0 = 0;
+      S.nu1 = iters;
+      S.phase = 3;
+      CU(sparse_launch(S, pl->sp_ctas, pl->sp_smem, pl->stream));
+      ++pl->launches;
+    } else {
+      // per iteration: phase 1 (backward + head pre-reduction), the cross-GPU sum of
+      // the per-trunk-node head sums, phase 2 (trunk sweep, needs, forward, epilogue)
+      const size_t hs = (size_t)std::max(1, pl->sp_trunk) * S.HS_LD;
+      for (int nu = 0; nu < iters; ++nu) {
+        S.nu0 = nu;
+        S.nu1 = nu + 1;
+        S.phase = 1;
+        CU(sparse_launch(S, pl->sp_ctas, pl->sp_smem, pl->stream));
+        if (pl->sp_trunk > 0) {
+          const int nr = pl->nccl->AllReduce(pl->HS, pl->HS, hs, NcclApi::kFloat64, NcclApi::kSum, pl->comm, pl->stream);
+          if (nr != 0) return fail(TSMPC_ERR_NCCL, "ncclAllReduce: %s", pl->nccl->GetErrorString(nr));
+        }
+        S.phase = 2;
+        CU(sparse_launch(S, pl->sp_ctas, pl->sp_smem, pl->stream));
+        pl->launches += 2;
+      }
+      // residual: max over ranks (non-negative doubles order like their bit patterns)
+      const int nr = pl->nccl->AllReduce(pl->RESID, pl->RESID, (size_t)nres, NcclApi::kUint64, NcclApi::kMax,
+                                         pl->comm, pl->stream);
+      if (nr != 0) return fail(TSMPC_ERR_NCCL, "ncclAllReduce: %s", pl->nccl->GetErrorString(nr));
+    }
   } else if (launch_apg(pl, P)) {
     return TSMPC_ERR_CUDA;
   }
@@ -967,7 +1108,7 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
   CU(cudaMemcpyAsync(pl->XL, pl->X, sizeof(double) * (size_t)pl->n_nodes * NXP, cudaMemcpyDeviceToDevice, pl->stream));
   CU(cudaMemcpyAsync(pl->UL, pl->U, sizeof(double) * (size_t)E * NUP, cudaMemcpyDeviceToDevice, pl->stream));
   double gap = NAN;
-  if (!(flags & TSMPC_SKIP_GAP)) {
+  if (!(flags & TSMPC_SKIP_GAP) && !pl->sharded) {
     int rc = compute_gap(pl, yfin, &gap);
     if (rc) return rc;
   }

@@ -136,6 +136,19 @@ struct SParams {
   int slot_rows;                // resident capacity of the slot region (rows)
   const double* beta_s;         // E x NVP  beta in the structured basis (beta M)
   double* TG;                   // E x NVP  t rows of streamed CTAs
+  // launch window: iterations [nu0, nu1) and phases (1: backward (+ head pre-reduction
+  // when sharded), 2: trunk sweep, needs, forward + epilogue).  Single-GPU plans run
+  // every iteration with both phases in one launch.
+  int nu0, nu1, phase;
+  // subtree sharding across GPUs (one process per GPU): the trunk is replicated, the
+  // leaf chains are split by the trunk node they hang from; HS holds, per trunk
+  // position, [sum of the chain-head g | sum of the chain-head xiq] of the heads
+  // hanging from its node (non-zero on the owning rank only) and is summed across
+  // ranks between the two phases (ncclAllReduce; exact: one contributor per entry).
+  int sharded;
+  double* HS;                   // T x HS_LD
+  int HS_LD;                    // NVP + NXP
+  const unsigned char* towned;  // T: this rank owns the heads of the node below
 };
 
 // Phase timers (profiling builds: -DTSMPC_TIMERS).  Slot k accumulates the cycles

@@ -205,7 +205,7 @@ __device__ __noinline__ void load_rows(const int* edges, int estride, int nrows,
   const int per_y = 2 * hx + hu;               // 16-byte chunks of one dual row
   const int nch = ((parts & 1) ? 2 * per_y : 0) + ((parts & 2) ? hx + hu : 0);
   const size_t E = (size_t)c.E;
-  #pragma unroll 1
+#pragma unroll 1
   for (int idx = threadIdx.x; idx < nrows * nch; idx += kThreadsS) {
     const int r = idx / nch;
     int k = idx - r * nch;
@@ -656,7 +656,7 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
   double* Zs = c.B();
   double* Xs = Zs + (size_t)T * nc;
   int* sch = reinterpret_cast<int*>(Xs + (size_t)T * nc);
-  #pragma unroll 1
+#pragma unroll 1
   for (int i = threadIdx.x; i < S.n_tsched; i += kThreadsS) sch[i] = __ldg(g + i);
   __syncthreads();
   const int* lev = sch + 4;
@@ -668,7 +668,7 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
   const double* Yp = P.ybuf[cur ^ 1];
   const double* adiag = c.adiag();
   // (1) own terms + chain-head children (one parallel round of loads)
-  #pragma unroll 1
+#pragma unroll 1
   for (int idx = threadIdx.x; idx < T * nc; idx += kThreadsS) {
     const int tp = idx / nc, k = idx - tp * nc, q = c_lo + k;
     const int* ps = pos + 8 * tp;
@@ -676,8 +676,12 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
     double z = 0.0, x = 0.0;
     if (q < c.nv) {
       z = ldcg(S.beta_s + (size_t)a * c.NVP + q);
-      #pragma unroll 1
-      for (int m = 0; m < nh; ++m) z = __dadd_rn(z, ldcg(P.GG + (size_t)hch[h0 + m] * c.NVP + q));
+      if (S.sharded) {
+        if (nh > 0) z = __dadd_rn(z, ldcg(S.HS + (size_t)tp * S.HS_LD + q));
+      } else {
+#pragma unroll 1
+        for (int m = 0; m < nh; ++m) z = __dadd_rn(z, ldcg(P.GG + (size_t)hch[h0 + m] * c.NVP + q));
+      }
     } else if (q < c.nv + c.nx) {
       const int i = q - c.nv;
       const size_t o = (size_t)a * c.NXP + i;
@@ -686,8 +690,12 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
       const double ds = c.scl[st], dz = c.scl[c.N + st];
       const double s = __dadd_rn(__dmul_rn(ws, ds), __dmul_rn(wz, dz));
       double h = 0.0;
-      #pragma unroll 1
-      for (int m = 0; m < nh; ++m) h = __dadd_rn(h, ldcg(P.XIQG + (size_t)hch[h0 + m] * c.NXP + i));
+      if (S.sharded) {
+        if (nh > 0) h = ldcg(S.HS + (size_t)tp * S.HS_LD + c.NVP + i);
+      } else {
+#pragma unroll 1
+        for (int m = 0; m < nh; ++m) h = __dadd_rn(h, ldcg(P.XIQG + (size_t)hch[h0 + m] * c.NXP + i));
+      }
       x = __dadd_rn(s, __dmul_rn(h, adiag[i]));
     } else {
       const int j = q - c.nv - c.nx;
@@ -700,15 +708,15 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
   }
   __syncthreads();
   // (2) bottom-up over edge-stage levels: add trunk children
-  #pragma unroll 1
+#pragma unroll 1
   for (int l = nlev - 1; l >= 0; --l) {
-    #pragma unroll 1
+#pragma unroll 1
     for (int idx = lev[l] * nc + threadIdx.x; idx < lev[l + 1] * nc; idx += kThreadsS) {
       const int tp = idx / nc, k = idx - tp * nc, q = c_lo + k;
       const int* ps = pos + 8 * tp;
       const int c0 = ps[3], n = ps[4];
       double zs = 0.0, xs = 0.0;
-      #pragma unroll 1
+#pragma unroll 1
       for (int m = 0; m < n; ++m) {
         const int cp = tch[c0 + m];
         zs = __dadd_rn(zs, Zs[cp * nc + k]);
@@ -725,9 +733,9 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
     __syncthreads();
   }
   // (3) top-down: K_a, Y_a = own * inv2p_a + parent's
-  #pragma unroll 1
+#pragma unroll 1
   for (int l = 0; l < nlev; ++l) {
-    #pragma unroll 1
+#pragma unroll 1
     for (int idx = lev[l] * nc + threadIdx.x; idx < lev[l + 1] * nc; idx += kThreadsS) {
       const int tp = idx / nc, k = idx - tp * nc;
       const int* ps = pos + 8 * tp;
@@ -739,11 +747,44 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
     __syncthreads();
   }
   // (4) KY columns of this slice
-  #pragma unroll 1
+#pragma unroll 1
   for (int idx = threadIdx.x; idx < T * nc; idx += kThreadsS) {
     const int tp = idx / nc, k = idx - tp * nc, q = c_lo + k;
     const int col = q < c.nv ? q : (q < c.nv + c.nx ? c.NVP + (q - c.nv) : c.NVP + c.NXP + (q - c.nv - c.nx));
     stcg(P.KY + (size_t)tp * P.KY_LD + col, Zs[idx]);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// sharded plans, end of phase 1: per trunk position, the sums over the chain heads
+// hanging from its node (same order as the single-GPU sweep: children in node
+// order) -> HS; zero where another rank owns those heads.  Grid-strided.
+// ----------------------------------------------------------------------------
+__device__ __noinline__ void head_prereduce() {
+  const SParams& S = g_sp;
+  const Ctx c = ctx_of();
+  const Params& P = S.P;
+  const int* g = S.tsched;
+  const int T = __ldg(g), nlev = __ldg(g + 1);
+  const int* pos = g + 4 + nlev + 1;
+  const int* hch = pos + 8 * T + __ldg(g + 2);
+  const int ncomp = c.nv + c.nx;
+#pragma unroll 1
+  for (int idx = blockIdx.x * kThreadsS + threadIdx.x; idx < T * ncomp; idx += gridDim.x * kThreadsS) {
+    const int tp = idx / ncomp, q = idx - tp * ncomp;
+    const int h0 = __ldg(pos + 8 * tp + 5), nh = __ldg(pos + 8 * tp + 6);
+    double v = 0.0;
+    if (S.towned[tp]) {
+      if (q < c.nv) {
+#pragma unroll 1
+        for (int m = 0; m < nh; ++m) v = __dadd_rn(v, ldcg(P.GG + (size_t)__ldg(hch + h0 + m) * c.NVP + q));
+      } else {
+#pragma unroll 1
+        for (int m = 0; m < nh; ++m)
+          v = __dadd_rn(v, ldcg(P.XIQG + (size_t)__ldg(hch + h0 + m) * c.NXP + (q - c.nv)));
+      }
+    }
+    stcg(S.HS + (size_t)tp * S.HS_LD + (q < c.nv ? q : c.NVP + (q - c.nv)), v);
   }
 }
 
@@ -767,12 +808,12 @@ __device__ __noinline__ void trunk_needs() {
     const int* cp = c.spi + S.Bc_ptr;
     const int* ci = c.spi + S.Bc_idx;
     const double* cv = c.spv + S.Bc_val;
-    #pragma unroll 1
+#pragma unroll 1
     for (int idx = threadIdx.x; idx < nn * nu; idx += kThreadsS) {
       const int n = idx / nu, j = idx - n * nu;
       const double* ky = P.KY + (size_t)nd[4 * n] * P.KY_LD;
       double z = ldcg(ky + c.NVP + c.NXP + j);
-      #pragma unroll 1
+#pragma unroll 1
       for (int q = cp[j]; q < cp[j + 1]; ++q) z = fma(cv[q], ldcg(ky + c.NVP + ci[q]), z);
       Yz[(size_t)n * c.NUP + j] = z;
     }
@@ -783,11 +824,11 @@ __device__ __noinline__ void trunk_needs() {
     const int* cp = c.spi + S.Lc_ptr;
     const int* ci = c.spi + S.Lc_idx;
     const double* cv = c.spv + S.Lc_val;
-    #pragma unroll 1
+#pragma unroll 1
     for (int idx = threadIdx.x; idx < nn * nv; idx += kThreadsS) {
       const int n = idx / nv, k = idx - n * nv;
       double h = 0.0;
-      #pragma unroll 1
+#pragma unroll 1
       for (int q = cp[k]; q < cp[k + 1]; ++q) h = fma(cv[q], Yz[(size_t)n * c.NUP + ci[q]], h);
       c.need[(size_t)n * LD + k] = __dadd_rn(ldcg(P.KY + (size_t)nd[4 * n] * P.KY_LD + k), h);
     }
@@ -798,11 +839,11 @@ __device__ __noinline__ void trunk_needs() {
     const int* rp = c.spi + S.Lr_ptr;
     const int* ri = c.spi + S.Lr_idx;
     const double* rv = c.spv + S.Lr_val;
-    #pragma unroll 1
+#pragma unroll 1
     for (int idx = threadIdx.x; idx < nn * nu; idx += kThreadsS) {
       const int n = idx / nu, j = idx - n * nu;
       double d = 0.0;
-      #pragma unroll 1
+#pragma unroll 1
       for (int q = rp[j]; q < rp[j + 1]; ++q) d = fma(rv[q], c.need[(size_t)n * LD + ri[q]], d);
       DU[(size_t)n * c.NUP + j] = d;
       c.need[(size_t)n * LD + c.NVP + c.NXP + j] = __dadd_rn(d, ldcg(P.uhat + (size_t)nd[4 * n + 2] * c.NUP + j));
@@ -814,20 +855,20 @@ __device__ __noinline__ void trunk_needs() {
     const int* rp = c.spi + S.Br_ptr;
     const int* ri = c.spi + S.Br_idx;
     const double* rv = c.spv + S.Br_val;
-    #pragma unroll 1
+#pragma unroll 1
     for (int idx = threadIdx.x; idx < nn * nx; idx += kThreadsS) {
       const int n = idx / nx, i = idx - n * nx;
       double b = 0.0;
-      #pragma unroll 1
+#pragma unroll 1
       for (int q = rp[i]; q < rp[i + 1]; ++q) b = fma(rv[q], DU[(size_t)n * c.NUP + ri[q]], b);
       c.need[(size_t)n * LD + c.NVP + i] = __dadd_rn(b, ldcg(P.evec + (size_t)nd[4 * n + 2] * c.NXP + i));
     }
     __syncthreads();
     const double* adiag = c.adiag();
-    #pragma unroll 1
+#pragma unroll 1
     for (int l = 0; l < c.mt.nlev; ++l) {
       const int n0 = c.mt.lev[l], n1 = c.mt.lev[l + 1];
-      #pragma unroll 1
+#pragma unroll 1
       for (int idx = n0 * nx + threadIdx.x; idx < n1 * nx; idx += kThreadsS) {
         const int n = idx / nx, i = idx - n * nx;
         const int pn = nd[4 * n + 1];
@@ -883,7 +924,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
     double* bnd = s_dyn + S.O_BND;
     double* scl = s_dyn + S.O_SCL;
     const int NXP = P.NXP, NUP = P.NUP, N = P.N;
-    #pragma unroll 1
+#pragma unroll 1
     for (int i = threadIdx.x; i < NXP; i += kThreadsS) {
       bnd[i] = P.x_s[i];
       bnd[NXP + i] = P.x_min[i];
@@ -891,12 +932,12 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
       bnd[3 * NXP + 2 * NUP + i] = P.a_diag[i];
       bnd[4 * NXP + 2 * NUP + i] = P.p[i];
     }
-    #pragma unroll 1
+#pragma unroll 1
     for (int j = threadIdx.x; j < NUP; j += kThreadsS) {
       bnd[3 * NXP + j] = P.u_min[j];
       bnd[3 * NXP + NUP + j] = P.u_max[j];
     }
-    #pragma unroll 1
+#pragma unroll 1
     for (int j = threadIdx.x; j < N; j += kThreadsS) {
       scl[j] = P.scaled ? P.sig_stage[j] : 1.0;
       scl[N + j] = P.scaled ? P.zeta_stage[j] : 1.0;
@@ -910,12 +951,12 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
     }
     int* ints = reinterpret_cast<int*>(s_dyn + S.O_INT);
     const int m0 = __ldg(S.meta_ptr + blockIdx.x), m1 = __ldg(S.meta_ptr + blockIdx.x + 1);
-    #pragma unroll 1
+#pragma unroll 1
     for (int i = threadIdx.x; i < m1 - m0; i += kThreadsS) ints[i] = __ldg(S.meta + m0 + i);
-    #pragma unroll 1
+#pragma unroll 1
     for (int i = threadIdx.x; i < S.n_spi; i += kThreadsS) ints[S.meta_max + i] = __ldg(S.spi + i);
     double* spv = s_dyn + S.O_SPV;
-    #pragma unroll 1
+#pragma unroll 1
     for (int i = threadIdx.x; i < S.n_spv; i += kThreadsS) spv[i] = __ldg(S.spv + i);
     __syncthreads();
   }
@@ -923,53 +964,63 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
   const bool resident = c.mt.resident != 0;
   const int nt = c.mt.ntiles;
   const bool trunk = P.n_trunk > 0;
+  const bool do_a = S.phase & 1, do_b = S.phase & 2;
   {  // initial dual / ergodic rows
-    const int cur0 = P.slot0 & 1;
+    const int cur0 = (P.slot0 + S.nu0) & 1, ysm0 = S.nu0 & 1;
     if (resident) {
-      if (nt > 0) load_rows(c.mt.rows, 4, c.mt.nrows, c.slot, 3, cur0, 0);
+      if (nt > 0) load_rows(c.mt.rows, 4, c.mt.nrows, c.slot, 3, cur0, ysm0);
     } else if (nt > 0) {
-      const int* td = c.mt.tiles + 4 * (nt - 1);
-      load_rows(c.mt.rows + 4 * td[0], 4, td[1], c.slot, 1, cur0, 0);
+      // streamed: the first backward tile is the last one; a forward-only launch
+      // (sharded phase 2) starts with tile 0 and its ergodic rows
+      const int* td = c.mt.tiles + 4 * (do_a ? nt - 1 : 0);
+      load_rows(c.mt.rows + 4 * td[0], 4, td[1], c.slot, do_a ? 1 : 3, cur0, ysm0);
     }
     cp_commit();
     cp_wait<0>();
     __syncthreads();
   }
   double rmax = 0.0;
-  double cf = P.coef[0], th = P.theta[0];
-  for (int nu = 0; nu < P.iters; ++nu) {
+  double cf = P.coef[S.nu0], th = P.theta[S.nu0];
+  for (int nu = S.nu0; nu < S.nu1; ++nu) {
     const int cur = (P.slot0 + nu) & 1;
     const int ysm = nu & 1;
     // momentum coefficients of the next iteration, loaded one iteration ahead
     const int nn = nu + 1 < P.iters ? nu + 1 : nu;
     const double cf_n = P.coef[nn], th_n = P.theta[nn];
-    for (int t = nt - 1; t >= 0; --t) bwd_tile(t, cf, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur);
-    if (trunk) {
-      long long tb_ = clock64();
-      (void)tb_;
-      grid.sync();
-      TSMPC_MARK(P, 9, tb_);
-      trunk_sweep(cf, cur);
-      TSMPC_MARK(P, 10, tb_);
-      grid.sync();
-      TSMPC_MARK(P, 9, tb_);
-      trunk_needs();
-      trunk_own_rows(nu, cf, th, cur, &rmax);
-      TSMPC_MARK(P, 12, tb_);
+    if (do_a) {
+      for (int t = nt - 1; t >= 0; --t) bwd_tile(t, cf, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur);
+      if (S.sharded && trunk) {
+        grid.sync();
+        head_prereduce();
+      }
     }
-    if (blockIdx.x == 0) {
-      const double om = __dsub_rn(1.0, th);
-      #pragma unroll 1
-      for (int i = threadIdx.x; i < c.nx; i += kThreadsS)
-        P.xavg[i] = __dadd_rn(__dmul_rn(P.xavg[i], om), __dmul_rn(th, c.proot()[i]));
-    }
-    for (int t = 0; t < nt; ++t)
-      fwd_tile(t, nu, cf, th, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur, &rmax);
-    if (nu == P.iters - 1 || P.record_all) {
-      for (int off = 16; off > 0; off >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, off));
-      if ((threadIdx.x & 31) == 0 && rmax > 0.0)
-        atomicMax(P.resid + (P.record_all ? nu : 0), (unsigned long long)__double_as_longlong(rmax));
-      rmax = 0.0;
+    if (do_b) {
+      if (trunk) {
+        long long tb_ = clock64();
+        (void)tb_;
+        if (!S.sharded) grid.sync();
+        TSMPC_MARK(P, 9, tb_);
+        trunk_sweep(cf, cur);
+        TSMPC_MARK(P, 10, tb_);
+        grid.sync();
+        TSMPC_MARK(P, 9, tb_);
+        trunk_needs();
+        trunk_own_rows(nu, cf, th, cur, &rmax);
+        TSMPC_MARK(P, 12, tb_);
+      }
+      if (blockIdx.x == 0) {
+        const double om = __dsub_rn(1.0, th);
+        for (int i = threadIdx.x; i < c.nx; i += kThreadsS)
+          P.xavg[i] = __dadd_rn(__dmul_rn(P.xavg[i], om), __dmul_rn(th, c.proot()[i]));
+      }
+      for (int t = 0; t < nt; ++t)
+        fwd_tile(t, nu, cf, th, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur, &rmax);
+      if (nu == P.iters - 1 || P.record_all) {
+        for (int off = 16; off > 0; off >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, off));
+        if ((threadIdx.x & 31) == 0 && rmax > 0.0)
+          atomicMax(P.resid + (P.record_all ? nu : 0), (unsigned long long)__double_as_longlong(rmax));
+        rmax = 0.0;
+      }
     }
     cf = cf_n;
     th = th_n;
@@ -995,7 +1046,7 @@ __global__ void beta_rotate_kernel(const double* __restrict__ beta, const double
     const double* b = beta + (size_t)e * NVP;
     for (int k = lane; k < nv; k += 32) {
       double s = 0.0;
-      #pragma unroll 1
+#pragma unroll 1
       for (int j = 0; j < nv; ++j) s = fma(b[j], M[(size_t)j * nv + k], s);
       out[(size_t)e * NVP + k] = s;
     }

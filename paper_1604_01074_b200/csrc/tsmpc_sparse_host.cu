@@ -41,8 +41,14 @@ void csr(int rows, int cols, const std::vector<double>& dense, bool by_col, std:
 }  // namespace
 
 SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NXP, int NUP, int NVP,
-                           int max_ctas, size_t smem_limit) {
+                           int max_ctas, size_t smem_limit, bool sharded, int rank, int world) {
   SparseHostPlan out;
+  out.rank = rank;
+  out.world = world;
+  if (world < 1 || rank < 0 || rank >= world) {
+    out.why = "invalid shard rank/world";
+    return out;
+  }
   const int n_nodes = t.n_nodes, E = n_nodes - 1, N = t.N;
   const int nx = ops.nx, nu = ops.nu, nv = ops.nv;
   std::vector<int> nch(n_nodes), stage_of_edge(E);
@@ -82,6 +88,46 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
   out.n_trunk = T;
   out.n_chains = (int)chains.size();
   std::sort(chains.begin(), chains.end(), [](const auto& a, const auto& b) { return a[0] < b[0]; });
+  out.total_chains = (int)chains.size();
+  // ---- sharding: groups of chains hanging from the same node, split contiguously
+  out.towned.assign(T, 1);
+  if (sharded && world > 1) {
+    std::vector<int> gnode;             // group -> parent node
+    std::vector<long long> grows;       // group -> rows
+    std::vector<int> group_of(chains.size());
+    for (size_t i = 0; i < chains.size(); ++i) {
+      const int pn = (int)t.anc[chains[i][0] + 1];
+      if (gnode.empty() || gnode.back() != pn) {
+        // chains are sorted by head edge, and siblings are contiguous edges
+        gnode.push_back(pn);
+        grows.push_back(0);
+      }
+      group_of[i] = (int)gnode.size() - 1;
+      grows.back() += (long long)chains[i].size();
+    }
+    long long Rg = 0;
+    for (long long r : grows) Rg += r;
+    std::vector<int> gowner(gnode.size());
+    long long pre = 0;
+    for (size_t gi = 0; gi < gnode.size(); ++gi) {
+      const long long mid2 = 2 * pre + grows[gi];
+      gowner[gi] = std::min(world - 1, (int)((mid2 * world) / (2 * std::max<long long>(Rg, 1))));
+      pre += grows[gi];
+    }
+    std::vector<std::vector<int>> kept;
+    for (size_t i = 0; i < chains.size(); ++i)
+      if (gowner[group_of[i]] == rank) kept.push_back(chains[i]);
+    for (int tp = 0; tp < T; ++tp) out.towned[tp] = 0;
+    for (size_t gi = 0; gi < gnode.size(); ++gi)
+      if (gowner[gi] == rank && gnode[gi] > 0 && tpos[gnode[gi] - 1] >= 0) out.towned[tpos[gnode[gi] - 1]] = 1;
+    chains.swap(kept);
+  }
+  out.n_chains = (int)chains.size();
+  for (auto& ch : chains) {
+    out.owned_rows += (int)ch.size();
+    out.owned_edges.insert(out.owned_edges.end(), ch.begin(), ch.end());
+  }
+  std::sort(out.owned_edges.begin(), out.owned_edges.end());
 
   // ---- CTA count and chain assignment (contiguous, balanced by rows)
   long long R = 0;
@@ -356,7 +402,7 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
     slot_ld = t_ld;
     want_rows = rows_t;
   }
-  const bool any_stream = (slot_ld == base_ld ? res_b : res_t) < C;
+  const bool any_stream = sharded || (slot_ld == base_ld ? res_b : res_t) < C;
   if (any_stream) want_rows = std::max<long long>(want_rows, kTileS);  // one streamed tile slot
   if (want_rows * slot_ld > slot_avail) want_rows = slot_avail / slot_ld;
   if (any_stream && want_rows < kTileS && want_rows * slot_ld < kTileS * base_ld) {
@@ -366,7 +412,7 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
   S.slot_ld = (int)slot_ld;
   int resident = 0;
   for (int c = 0; c < C; ++c) {
-    const bool res = cta_rows[c] <= want_rows;
+    const bool res = !sharded && cta_rows[c] <= want_rows;
     metas[c][6] = res ? 1 : 0;
     metas[c][7] = !res ? 2 : (ntiles_c[c] <= 1 ? 0 : 1);
     if (res && ntiles_c[c] > 1 && slot_ld != t_ld) {  // cannot happen by construction

@@ -37,13 +37,21 @@ struct SparseHostPlan {
   std::vector<int> trunk_edge;      // trunk position -> edge
   std::vector<int> spi;             // sparse index pool
   std::vector<double> spv;          // sparse value pool
+  // sharding (rank of world): chains owned, per trunk position ownership of the heads
+  int rank = 0, world = 1, owned_rows = 0, total_chains = 0;
+  std::vector<unsigned char> towned;
+  std::vector<int> owned_edges;     // edges of the owned chains (ascending)
   // filled layout / pool offsets (device pointers are set by the caller)
   SParams S{};
 };
 
 // Build the plan.  smem_limit: opt-in shared memory per block (bytes);
 // max_ctas: SMs available for the cooperative launch.
+// sharded: split the leaf chains across `world` ranks by the trunk node they hang
+// from (all chain heads of a node go to one rank), keep this rank's share, stream
+// every tile (state lives in HBM between the two launches of an iteration).
 SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NXP, int NUP, int NVP,
-                           int max_ctas, size_t smem_limit);
+                           int max_ctas, size_t smem_limit, bool sharded = false, int rank = 0,
+                           int world = 1);
 
 }  // namespace tsmpc

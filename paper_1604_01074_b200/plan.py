@@ -27,7 +27,10 @@ def _c(a, dtype=np.float64):
 
 
 class DevicePlan:
-    def __init__(self, model, tree, factor, scaling=None, device: int = 0):
+    """``shard=(rank, world, nccl_id)`` creates one rank's plan of a tree split
+    across GPUs (see ``shard.py``); results then cover ``edges()`` only."""
+
+    def __init__(self, model, tree, factor, scaling=None, device: int = 0, shard=None):
         lib = nat.load_library()
         n_x, n_u, n_v = factor.n_x, factor.n_u, factor.n_v
         E = np.asarray(model.E, dtype=float)
@@ -62,7 +65,14 @@ class DevicePlan:
         pb.W_alpha, pb.Wx, pb.gamma_d = float(model.W_alpha), float(model.Wx), float(model.gamma_d)
         for name, arr in keep.items():
             setattr(pb, name, nat.iptr(arr) if arr.dtype == np.int64 else nat.dptr(arr))
-        handle = lib.tsmpc_plan_create(ctypes.byref(pb), int(device))
+        if shard is None:
+            handle = lib.tsmpc_plan_create(ctypes.byref(pb), int(device))
+        else:
+            rank, world, nid = shard
+            idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(bytes(nid))
+            handle = lib.tsmpc_plan_create_shard(ctypes.byref(pb), int(device), int(rank), int(world),
+                                                 idbuf)
+        self.shard = shard
         if not handle:
             nat.check(nat.ERR_CUDA if "CUDA" in nat.last_error() or "device" in nat.last_error()
                       else nat.ERR_VALIDATION, "tsmpc_plan_create")
@@ -77,12 +87,22 @@ class DevicePlan:
     # -- introspection -------------------------------------------------------
     def info(self) -> dict:
         keys = ("levels", "ctas", "tiles", "segments", "smem_bytes", "diag_A", "threads",
-                "tile_rows", "sms", "collapsed", "trunk_edges", "sparse", "resident_ctas")
+                "tile_rows", "sms", "collapsed", "trunk_edges", "sparse", "resident_ctas",
+                "sharded", "rank", "world", "owned_chain_edges", "total_chains")
         buf = np.zeros(len(keys), dtype=np.int64)
         nat.check(self._lib.tsmpc_plan_info(self._h, nat.iptr(buf), len(keys)), "tsmpc_plan_info")
         d = dict(zip(keys, (int(v) for v in buf)))
         d["path"] = self._lib.tsmpc_plan_path(self._h).decode()
         return d
+
+    def edges(self, which: int = 0) -> np.ndarray:
+        """Edge ids whose rows this plan computes (which=0) or the trunk edges (1)."""
+        n = self._lib.tsmpc_plan_edges(self._h, int(which), None, 0)
+        if n < 0:
+            nat.check(n, "tsmpc_plan_edges")
+        buf = np.zeros(max(n, 1), dtype=np.int64)
+        self._lib.tsmpc_plan_edges(self._h, int(which), nat.iptr(buf), n)
+        return buf[:n]
 
     def debug_timers(self) -> np.ndarray:
         """Phase cycle counters of CTA 0 since the last call (timer builds only)."""
@@ -231,6 +251,33 @@ def describe_sparse(model, tree, factor, max_ctas: int = 148, smem_limit: int = 
     nat.check(lib.tsmpc_describe_sparse(ctypes.byref(pb), int(max_ctas), int(smem_limit),
                                         nat.iptr(buf), len(keys)), "tsmpc_describe_sparse")
     return dict(zip(keys, (int(v) for v in buf)))
+
+
+def describe_shard(model, tree, factor, rank: int, world: int, max_ctas: int = 148,
+                   smem_limit: int = 232448) -> dict:
+    """Host-only view of one shard of the structured-basis plan (no GPU needed)."""
+    from .precompute import structured_basis
+    lib = nat.load_library()
+    sb = structured_basis(model, _BasisView(factor.L))
+    keep = {"stage_starts": _c(tree.stage_starts, np.int64), "anc": _c(tree.anc, np.int64),
+            "child_start": _c(tree.child_start, np.int64),
+            "child_stop": _c(tree.child_stop, np.int64), "prob": _c(tree.prob),
+            "B": _c(model.B), "Ls": _c(sb.Ls), "lam_s": _c(sb.lam)}
+    pb = nat.Problem()
+    pb.n_x, pb.n_u, pb.n_v = factor.n_x, factor.n_u, factor.n_v
+    pb.N, pb.n_nodes = int(tree.N), int(tree.n_nodes)
+    for name, arr in keep.items():
+        setattr(pb, name, nat.iptr(arr) if arr.dtype == np.int64 else nat.dptr(arr))
+    keys = ("ctas", "owned_chains", "owned_rows", "trunk_edges", "total_chains",
+            "owned_trunk_nodes", "smem_bytes")
+    buf = np.zeros(len(keys), dtype=np.int64)
+    edges = np.zeros(max(1, tree.n_edges), dtype=np.int64)
+    nat.check(lib.tsmpc_describe_shard(ctypes.byref(pb), int(max_ctas), int(smem_limit), int(rank),
+                                       int(world), nat.iptr(buf), len(keys), nat.iptr(edges),
+                                       tree.n_edges), "tsmpc_describe_shard")
+    d = dict(zip(keys, (int(v) for v in buf)))
+    d["edges"] = edges[:d["owned_rows"]]
+    return d
 
 
 def plan_for(model, tree, factor, scaling=None, device: int = 0) -> DevicePlan:
