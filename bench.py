@@ -230,6 +230,13 @@ def run_ours(args, ws, rank, local):
         "solve_ms": {"loop": loop_ms / args.steps, "loop_plus_gap": ms_per_step},
         "clocks": clk.summary(),
     }
+    if not args.no_shard:
+        try:
+            sh = sharded_measure(args, ws, rank, local, dist)
+        except Exception as exc:  # report, never hang the headline line on it
+            sh = {"error": f"{type(exc).__name__}: {exc}"}
+        if rank == 0:
+            line["sharded"] = sh
     if not args.no_sweep and rank == 0:
         line["sweep"] = sweep(args, lam_cache={args.tree: lam}, local=local)
     if rank == 0 and not args.no_cpu:
@@ -239,6 +246,46 @@ def run_ours(args, ws, rank, local):
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(line))
+
+
+def sharded_measure(args, ws, rank, local, dist):
+    """SURVEY §8e / BASELINE configs[3]: one tree split by subtree across the ws GPUs
+    (strong scaling; the trunk is replicated, one ncclAllReduce of the per-trunk-node
+    chain-head sums per iteration).  Device time of the loop, max over ranks."""
+    import torch
+    from paper_1604_01074_b200 import engine, theta_schedule
+    from paper_1604_01074_b200.plan import DevicePlan
+    from paper_1604_01074_b200.shard import _broadcast_id, nccl_unique_id
+    W = build_workload(args.shard_tree)
+    nid = _broadcast_id(rank) if dist is not None else nccl_unique_id()
+    plan = DevicePlan(W["model"], W["tree"], W["factor"], W["scaling"], device=local,
+                      shard=(rank, ws, nid))
+    plan.set_cache(W["caches"][0], W["model"])
+    th, cf = theta_schedule(args.iters)
+    lam = 0.4797  # bcn63 step size (tests/golden); the work per iteration does not depend on it
+    for _ in range(2):
+        plan.solve(W["p"], args.iters, lam, theta=th, coef=cf, skip_gap=True, keep_device=True)
+    if dist is not None:
+        dist.barrier()
+    ms = []
+    for _ in range(3):
+        r = plan.solve(W["p"], args.iters, lam, theta=th, coef=cf, skip_gap=True, keep_device=True)
+        ms.append(r["device_ms"])
+    loop = statistics.median(ms)
+    if dist is not None:
+        t = torch.tensor([loop], device=torch.device("cuda", local), dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        loop = float(t[0])
+    info = plan.info()
+    E = W["tree"].n_edges
+    return {"tree": args.shard_tree, "edges": E, "scenarios": W["tree"].n_s, "ranks": ws,
+            "scaling": "strong", "iters": args.iters, "loop_ms": loop,
+            "iters_per_s": args.iters / (loop / 1e3), "us_per_iter": loop * 1e3 / args.iters,
+            "owned_chain_edges_rank0": info["owned_chain_edges"], "trunk_edges": info["trunk_edges"],
+            "ctas": info["ctas"], "launches_per_iter": 2,
+            "exchange_bytes_per_iter": 8 * info["trunk_edges"] * (97 + 64),
+            "note": "per iteration: phase 1 (backward, head sums) -> ncclAllReduce -> phase 2; "
+                    "duality gap not evaluated on shard plans"}
 
 
 def ncu_traffic(kernel: str, tree: str, iters: int):
@@ -374,6 +421,8 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=40)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-shard", action="store_true")
+    ap.add_argument("--shard-tree", default="SMPC8", choices=("SMPC3", "SMPC8", "W4k"))
     args = ap.parse_args()
     ws, rank, local = dist_env()
     if args.impl == "reference":

@@ -128,6 +128,9 @@ struct SParams {
   // shared-memory layout, offsets in doubles from the dynamic base
   int O_BND, O_SCL, O_RED, O_PSI, O_SPV, O_NEED, O_WORK, O_SLOT, O_INT;
   int LA;                       // pitch of work region A: max(NXP, NVP)
+  int sweep_in_a;               // trunk sweep buffers start in region A (no CTA keeps t there)
+  int sched_smem;               // trunk schedule staged in shared memory during the sweep
+  int psi_smem;                 // psi_stage table staged in shared memory (else read via L1)
   int n_work;                   // doubles in the work region
   int need_ld;                  // NVP + NXP + NUP  ([S | x | u] of one needed trunk edge)
   int need_max;

@@ -132,7 +132,11 @@ struct Ctx {
   __device__ const double* proot() const { return bnd + 4 * NXP + 2 * NUP; }
   __device__ double* fac() const { return red + kTileS * 8; }
   __device__ int* rdesc() const { return reinterpret_cast<int*>(red + kTileS * 10); }
-  __device__ double dpsi(int st, int k) const { return psi ? psi[st * NUP + k] : 1.0; }
+  const double* psi_g;  // psi_stage in HBM when the table does not fit shared memory
+  __device__ double dpsi(int st, int k) const {
+    return psi ? psi[st * NUP + k] : (psi_g ? __ldg(psi_g + (size_t)st * NUP + k) : 1.0);
+  }
+  __device__ bool scaled() const { return psi || psi_g; }
 };
 
 __device__ __forceinline__ Ctx ctx_of() {
@@ -147,7 +151,8 @@ __device__ __forceinline__ Ctx ctx_of() {
   c.bnd = s_dyn + S.O_BND;
   c.scl = s_dyn + S.O_SCL;
   c.red = s_dyn + S.O_RED;
-  c.psi = P.scaled ? s_dyn + S.O_PSI : nullptr;
+  c.psi = P.scaled && S.psi_smem ? s_dyn + S.O_PSI : nullptr;
+  c.psi_g = P.scaled && !S.psi_smem ? P.psi_stage : nullptr;
   c.LA = S.LA;
   c.need = s_dyn + S.O_NEED;
   c.work = s_dyn + S.O_WORK;
@@ -423,7 +428,7 @@ __device__ __noinline__ void bwd_tile(int ti, double cf, int ysm, int srow0, boo
     }
     if (k < nu) {
       const double wp = extrap(yc[2 * c.NXP + k], yp[2 * c.NXP + k], cf);
-      RB[r * c.NUP + k] = c.psi ? __dmul_rn(wp, c.dpsi(st, k)) : wp;
+      RB[r * c.NUP + k] = c.scaled() ? __dmul_rn(wp, c.dpsi(st, k)) : wp;
     }
   }
   __syncthreads();
@@ -653,11 +658,15 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
   if (nc <= 0) return;
   const int* g = S.tsched;
   const int T = __ldg(g), nlev = __ldg(g + 1);
-  double* Zs = c.B();
+  double* Zs = S.sweep_in_a ? c.A() : c.B();
   double* Xs = Zs + (size_t)T * nc;
-  int* sch = reinterpret_cast<int*>(Xs + (size_t)T * nc);
+  const int* sch = g;  // schedule: staged in shared memory when it fits, else read through L1
+  if (S.sched_smem) {
+    int* ss = reinterpret_cast<int*>(Xs + (size_t)T * nc);
 #pragma unroll 1
-  for (int i = threadIdx.x; i < S.n_tsched; i += kThreadsS) sch[i] = __ldg(g + i);
+    for (int i = threadIdx.x; i < S.n_tsched; i += kThreadsS) ss[i] = __ldg(g + i);
+    sch = ss;
+  }
   __syncthreads();
   const int* lev = sch + 4;
   const int* pos = lev + nlev + 1;
@@ -701,7 +710,7 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
       const int j = q - c.nv - c.nx;
       const size_t o = 2 * E * c.NXP + (size_t)a * c.NUP + j;
       const double wp = extrap(ldcg(Y + o), ldcg(Yp + o), cf);
-      z = c.psi ? __dmul_rn(wp, c.dpsi(st, j)) : wp;
+      z = c.scaled() ? __dmul_rn(wp, c.dpsi(st, j)) : wp;
     }
     Zs[idx] = z;
     Xs[idx] = x;
@@ -800,9 +809,10 @@ __device__ __noinline__ void trunk_needs() {
   if (nn == 0) return;
   const int nx = c.nx, nu = c.nu, nv = c.nv;
   const int LD = S.need_ld;
-  double* Yz = c.B();                        // nn x NUP
-  double* DU = c.B() + (size_t)nn * c.NUP;   // nn x NUP
   const int* nd = c.mt.needs;
+  // the u column of each need row holds Yz, then du, then u (no other scratch)
+  double* const ND = c.need;
+  const int UO = c.NVP + c.NXP;
   // (1) Yz = Ypsi + B' Yx
   {
     const int* cp = c.spi + S.Bc_ptr;
@@ -815,7 +825,7 @@ __device__ __noinline__ void trunk_needs() {
       double z = ldcg(ky + c.NVP + c.NXP + j);
 #pragma unroll 1
       for (int q = cp[j]; q < cp[j + 1]; ++q) z = fma(cv[q], ldcg(ky + c.NVP + ci[q]), z);
-      Yz[(size_t)n * c.NUP + j] = z;
+      ND[(size_t)n * LD + UO + j] = z;
     }
   }
   __syncthreads();
@@ -829,12 +839,12 @@ __device__ __noinline__ void trunk_needs() {
       const int n = idx / nv, k = idx - n * nv;
       double h = 0.0;
 #pragma unroll 1
-      for (int q = cp[k]; q < cp[k + 1]; ++q) h = fma(cv[q], Yz[(size_t)n * c.NUP + ci[q]], h);
-      c.need[(size_t)n * LD + k] = __dadd_rn(ldcg(P.KY + (size_t)nd[4 * n] * P.KY_LD + k), h);
+      for (int q = cp[k]; q < cp[k + 1]; ++q) h = fma(cv[q], ND[(size_t)n * LD + UO + ci[q]], h);
+      ND[(size_t)n * LD + k] = __dadd_rn(ldcg(P.KY + (size_t)nd[4 * n] * P.KY_LD + k), h);
     }
   }
   __syncthreads();
-  // (3) du = Lt S ; u = uhat + du
+  // (3) du = Lt S
   {
     const int* rp = c.spi + S.Lr_ptr;
     const int* ri = c.spi + S.Lr_idx;
@@ -844,13 +854,12 @@ __device__ __noinline__ void trunk_needs() {
       const int n = idx / nu, j = idx - n * nu;
       double d = 0.0;
 #pragma unroll 1
-      for (int q = rp[j]; q < rp[j + 1]; ++q) d = fma(rv[q], c.need[(size_t)n * LD + ri[q]], d);
-      DU[(size_t)n * c.NUP + j] = d;
-      c.need[(size_t)n * LD + c.NVP + c.NXP + j] = __dadd_rn(d, ldcg(P.uhat + (size_t)nd[4 * n + 2] * c.NUP + j));
+      for (int q = rp[j]; q < rp[j + 1]; ++q) d = fma(rv[q], ND[(size_t)n * LD + ri[q]], d);
+      ND[(size_t)n * LD + UO + j] = d;
     }
   }
   __syncthreads();
-  // (4) bv + e, then x level by level (parents first)
+  // (4) bv + e ; then u = uhat + du ; then x level by level (parents first)
   {
     const int* rp = c.spi + S.Br_ptr;
     const int* ri = c.spi + S.Br_idx;
@@ -860,8 +869,15 @@ __device__ __noinline__ void trunk_needs() {
       const int n = idx / nx, i = idx - n * nx;
       double b = 0.0;
 #pragma unroll 1
-      for (int q = rp[i]; q < rp[i + 1]; ++q) b = fma(rv[q], DU[(size_t)n * c.NUP + ri[q]], b);
-      c.need[(size_t)n * LD + c.NVP + i] = __dadd_rn(b, ldcg(P.evec + (size_t)nd[4 * n + 2] * c.NXP + i));
+      for (int q = rp[i]; q < rp[i + 1]; ++q) b = fma(rv[q], ND[(size_t)n * LD + UO + ri[q]], b);
+      ND[(size_t)n * LD + c.NVP + i] = __dadd_rn(b, ldcg(P.evec + (size_t)nd[4 * n + 2] * c.NXP + i));
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int idx = threadIdx.x; idx < nn * nu; idx += kThreadsS) {
+      const int n = idx / nu, j = idx - n * nu;
+      double* u = ND + (size_t)n * LD + UO + j;
+      *u = __dadd_rn(*u, ldcg(P.uhat + (size_t)nd[4 * n + 2] * c.NUP + j));
     }
     __syncthreads();
     const double* adiag = c.adiag();
@@ -944,7 +960,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
       scl[2 * N + j] = P.scaled ? P.sig_rcp[j] : 1.0;
       scl[3 * N + j] = P.scaled ? P.zeta_rcp[j] : 1.0;
     }
-    if (P.scaled) {
+    if (P.scaled && S.psi_smem) {
       double* psi = s_dyn + S.O_PSI;
 #pragma unroll 1
       for (int i = threadIdx.x; i < N * NUP; i += kThreadsS) psi[i] = P.psi_stage[i];

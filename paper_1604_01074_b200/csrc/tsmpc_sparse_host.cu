@@ -9,6 +9,8 @@
 #include "tsmpc_sparse_host.h"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -41,7 +43,7 @@ void csr(int rows, int cols, const std::vector<double>& dense, bool by_col, std:
 }  // namespace
 
 SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NXP, int NUP, int NVP,
-                           int max_ctas, size_t smem_limit, bool sharded, int rank, int world) {
+                           int max_ctas, size_t smem_limit, bool sharded, int rank, int world, bool psi_in_smem) {
   SparseHostPlan out;
   out.rank = rank;
   out.world = world;
@@ -145,21 +147,41 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
       pre += (long long)chains[i].size();
     }
   }
-  // trunk rows -> least-loaded CTAs (deterministic: load, then CTA index)
+  // trunk rows -> the CTA minimising load + 4 x (new "needs": trunk edges on the
+  // row's root path the CTA does not evaluate yet; 0 when its chains hang below
+  // the edge); at most ceil(T / C) + 1 rows per CTA.
+  // This keeps each CTA's needs close to its chains' root paths (also on shards,
+  // where many trunk edges have no owned chains below them).
   std::vector<std::vector<int>> cta_own(C);
   {
-    using Item = std::pair<long long, int>;
-    std::priority_queue<Item, std::vector<Item>, std::greater<Item>> pq;
-    for (int c = 0; c < C; ++c) {
-      long long rows = 0;
-      for (int i : cta_chains[c]) rows += (long long)chains[i].size();
-      pq.push({rows, c});
-    }
+    std::vector<long long> load(C, 0);
+    std::vector<std::set<int>> need(C);
+    for (int c = 0; c < C; ++c)
+      for (int i : cta_chains[c]) {
+        load[c] += (long long)chains[i].size();
+        for (int e = (int)t.anc[chains[i][0] + 1] - 1; e >= 0; e = (int)t.anc[e + 1] - 1) need[c].insert(tpos[e]);
+      }
+    const int cap_rows = (T + C - 1) / std::max(C, 1) + 1;
+    std::vector<int> path;
     for (int tp = 0; tp < T; ++tp) {
-      auto [load, c] = pq.top();
-      pq.pop();
-      cta_own[c].push_back(tp);
-      pq.push({load + 1, c});
+      path.clear();
+      for (int e = out.trunk_edge[tp]; e >= 0; e = (int)t.anc[e + 1] - 1) path.push_back(tpos[e]);
+      int best = -1, best_add = 0;
+      for (int c = 0; c < C; ++c) {
+        if ((int)cta_own[c].size() >= cap_rows) continue;
+        int add = 0;
+        for (int q : path) add += need[c].count(q) ? 0 : 1;
+        // a new need costs ~4 rows of work (it is evaluated once per iteration)
+        const long long cost = load[c] + 4LL * add;
+        if (best < 0 || cost < load[best] + 4LL * best_add) {
+          best = c;
+          best_add = add;
+        }
+      }
+      if (best < 0) best = tp % C;
+      cta_own[best].push_back(tp);
+      load[best] += 1;
+      for (int q : path) need[best].insert(q);
     }
   }
 
@@ -339,7 +361,8 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
   off += 10LL * kTileS + (5 * kTileS + 1) / 2 + 1;  // partial norms, factors, row descriptors
   off = even(off);
   S.O_PSI = (int)off;
-  off += even((long long)N * NUP);
+  S.psi_smem = psi_in_smem ? 1 : 0;
+  if (psi_in_smem) off += even((long long)N * NUP);
   S.O_SPV = (int)off;
   off += even(S.n_spv);
   S.O_NEED = (int)off;
@@ -347,19 +370,6 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
   S.O_WORK = (int)off;
   S.n_work = (int)even((long long)kTileS * (S.LA + NUP));
   off += S.n_work;
-  // the trunk phases run in work region B (kTileS x NUP)
-  {
-    const int ncomp = nv + nx + nu;
-    const long long nc_max = (ncomp + C - 1) / C;
-    const long long regB = (long long)kTileS * NUP;
-    const long long sweep = 2LL * T * nc_max + ((long long)out.tsched.size() + 1) / 2 + 2;
-    const long long needs = 2LL * need_max * NUP;
-    const long long stage1 = 2LL * S.YW + NXP + NUP + NVP;
-    if (sweep > regB || needs > regB || stage1 > regB) {
-      out.why = "trunk too large for the work region";
-      return out;
-    }
-  }
   S.O_SLOT = (int)off;
   const long long ints_d = ((long long)meta_max + S.n_spi + 1) / 2 + 1;
   const long long limit_d = (long long)(smem_limit / sizeof(double));
@@ -368,7 +378,12 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
   // CTAs with several tiles (tmode 1); a single resident tile keeps t in region A
   const long long base_ld = 2LL * S.YW + NXP + NUP;
   const long long t_ld = base_ld + NVP;
+  if (std::getenv("TSMPC_PLAN_DEBUG"))
+    std::fprintf(stderr, "plan_sparse: rank %d/%d C=%d need_max=%d meta_max=%d n_spi=%d work=%d off=%lld ints_d=%lld "
+                 "slot_avail=%lld base_ld=%lld psi=%d\n", rank, world, C, need_max, meta_max, S.n_spi, S.n_work,
+                 off, ints_d, slot_avail, base_ld, (int)psi_in_smem);
   if (slot_avail / base_ld < kTileS) {
+    if (psi_in_smem) return plan_sparse(t, ops, NXP, NUP, NVP, max_ctas, smem_limit, sharded, rank, world, false);
     out.why = "shared memory too small for one tile slot";
     return out;
   }
@@ -420,6 +435,25 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
       return out;
     }
     resident += res;
+  }
+  // trunk phases: the sweep's component slices (+ its schedule when it fits) use
+  // work region B, or A + B when no CTA keeps t rows in region A; the own trunk
+  // rows are staged in region B one slot row at a time at least
+  {
+    bool any_t0 = false;
+    for (int c = 0; c < C; ++c) any_t0 |= metas[c][7] == 0;
+    const int ncomp = nv + nx + nu;
+    const long long nc_max = (ncomp + C - 1) / C;
+    const long long regB = (long long)kTileS * NUP;
+    const long long cap = any_t0 ? regB : (long long)S.n_work;
+    const long long zx = 2LL * T * nc_max;
+    const long long sched = ((long long)out.tsched.size() + 1) / 2 + 2;
+    S.sweep_in_a = any_t0 ? 0 : 1;
+    S.sched_smem = zx + sched <= cap ? 1 : 0;
+    if (zx > cap || slot_ld > regB) {
+      out.why = "trunk too large for the work region";
+      return out;
+    }
   }
   S.slot_rows = (int)want_rows;
   off += want_rows * slot_ld;

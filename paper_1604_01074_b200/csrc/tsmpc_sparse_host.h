@@ -52,6 +52,6 @@ struct SparseHostPlan {
 // every tile (state lives in HBM between the two launches of an iteration).
 SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NXP, int NUP, int NVP,
                            int max_ctas, size_t smem_limit, bool sharded = false, int rank = 0,
-                           int world = 1);
+                           int world = 1, bool psi_in_smem = true);
 
 }  // namespace tsmpc
