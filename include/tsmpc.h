@@ -105,7 +105,8 @@ typedef struct tsmpc_result {
 
 #define TSMPC_RECORD_RESIDUALS 1   /* residual_inf of every iteration -> resid_trace */
 #define TSMPC_SKIP_GAP         2   /* do not evaluate the duality gap               */
-#define TSMPC_KEEP_DEVICE      4   /* leave results on the device (no D2H)          */
+#define TSMPC_KEEP_DEVICE      4   /* leave results on the device (no D2H but u0)   */
+#define TSMPC_WARM_DEVICE      8   /* warm start from the last solve's final dual (HBM) */
 
 /* Problem / tree geometry and device planning.  Returns NULL on failure. */
 tsmpc_plan* tsmpc_plan_create(const tsmpc_problem* prob, int device);
@@ -137,6 +138,20 @@ int tsmpc_plan_edges(const tsmpc_plan* plan, int32_t which, int64_t* out, int64_
 int tsmpc_set_cache(tsmpc_plan* plan, const double* beta, const double* uhat,
                     const double* evec, const double* q, const double* prices,
                     const double* jrhs, const double* gdd);
+
+/* Device stage cache (elimination.py:114-158 build_stage_cache, tree.py:319-331
+ * node_demands).  Once per plan: part_map n_u*n_d, Gd n_x*n_d, Ed n_e*n_d,
+ * Rhat = Wu L n_u*n_v, eps_edge n_edges*n_d (eps of node e+1), pbar n_edges.
+ * Per forecast: dhat N*n_d, q n_u, prices N*n_u (alpha1 + alpha2(k+j)) and
+ * abar N*n_v (W_alpha L' price(k+j)); beta/uhat/evec and the gap inputs are then
+ * built in HBM (replaces tsmpc_set_cache's E*(n_v+n_u+n_x) upload).
+ * tsmpc_get_cache downloads beta/uhat/evec (any pointer may be NULL). */
+int tsmpc_set_cache_operators(tsmpc_plan* plan, int32_t n_d, const double* part_map,
+                              const double* Gd, const double* Ed, const double* Rhat,
+                              const double* eps_edge, const double* pbar);
+int tsmpc_set_forecast(tsmpc_plan* plan, const double* dhat, const double* q,
+                       const double* prices, const double* abar);
+int tsmpc_get_cache(tsmpc_plan* plan, double* beta, double* uhat, double* evec);
 
 /* engine.solve: `iters` APG iterations at step size `lam` from y0 = y_-1 = warm
  * (three blocks, scaled coordinates) or zero when warm_sig == NULL.

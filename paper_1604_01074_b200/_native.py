@@ -20,11 +20,11 @@ from .errors import DeviceError, DimensionError, TreeSmpcError, ValidationError
 PKG_DIR = pathlib.Path(__file__).resolve().parent
 LIB_PATH = PKG_DIR / "libtsmpc.so"
 CSRC = PKG_DIR / "csrc"
-SOURCES = ["tsmpc_apg.cu", "tsmpc_sparse.cu", "tsmpc_sparse_host.cu", "tsmpc_nccl.cu", "tsmpc_aux.cu",
-           "tsmpc_capi.cu"]
+SOURCES = ["tsmpc_apg.cu", "tsmpc_sparse.cu", "tsmpc_sparse_host.cu", "tsmpc_nccl.cu", "tsmpc_cache.cu",
+           "tsmpc_aux.cu", "tsmpc_capi.cu"]
 
 OK, ERR_DIMENSION, ERR_VALIDATION, ERR_CUDA, ERR_NCCL, ERR_ARGUMENT = 0, -1, -2, -3, -4, -5
-RECORD_RESIDUALS, SKIP_GAP, KEEP_DEVICE = 1, 2, 4
+RECORD_RESIDUALS, SKIP_GAP, KEEP_DEVICE, WARM_DEVICE = 1, 2, 4, 8
 
 _dp = ctypes.POINTER(ctypes.c_double)
 _ip = ctypes.POINTER(ctypes.c_int64)
@@ -73,6 +73,10 @@ SIGNATURES = {
     "tsmpc_plan_info": (ctypes.c_int, [ctypes.c_void_p, _ip, ctypes.c_int32]),
     "tsmpc_last_error": (ctypes.c_char_p, []),
     "tsmpc_plan_path": (ctypes.c_char_p, [ctypes.c_void_p]),
+    "tsmpc_set_cache_operators": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, _dp, _dp, _dp, _dp, _dp,
+                                                 _dp]),
+    "tsmpc_set_forecast": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, _dp, _dp]),
+    "tsmpc_get_cache": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, _dp]),
     "tsmpc_nccl_unique_id": (ctypes.c_int, [ctypes.POINTER(ctypes.c_uint8)]),
     "tsmpc_plan_create_shard": (ctypes.c_void_p, [ctypes.POINTER(Problem), ctypes.c_int, ctypes.c_int32,
                                                   ctypes.c_int32, ctypes.POINTER(ctypes.c_uint8)]),

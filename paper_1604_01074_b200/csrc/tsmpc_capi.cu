@@ -10,6 +10,7 @@
 
 #include "../../include/tsmpc.h"
 #include "tsmpc_aux.cuh"
+#include "tsmpc_cache.cuh"
 #include "tsmpc_nccl.h"
 #include "tsmpc_sparse_host.h"
 
@@ -77,6 +78,14 @@ struct tsmpc_plan {
   size_t sp_smem = 0;
   double *BETA_S = nullptr, *TG = nullptr, *KY_S = nullptr, *MS = nullptr;
   std::string sp_why;
+  // device stage cache (tsmpc_set_cache_operators / tsmpc_set_forecast)
+  bool has_cache_ops = false;
+  int nd_c = 0;
+  double *PART_MAP = nullptr, *GD = nullptr, *ED = nullptr, *RHAT = nullptr, *EPS = nullptr, *PBAR = nullptr;
+  double *DHAT = nullptr, *ABAR = nullptr;
+  double* last_y = nullptr;  // final dual of the last solve (device warm start)
+  int *d_est_c = nullptr, *d_anc_c = nullptr, *d_cs_c = nullptr, *d_ce_c = nullptr;
+  double *d_pe_c = nullptr, *d_B_c = nullptr;
   // subtree sharding across GPUs (tsmpc_plan_create_shard)
   bool sharded = false;
   int rank = 0, world = 1, total_chains = 0;
@@ -653,6 +662,8 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
   P.XIQG = pl->XIQG; P.GG = pl->GG; P.p = pl->P;
   P.timers = pl->TIMERS;
 
+  pl->d_est_c = d_est; pl->d_anc_c = d_anc; pl->d_cs_c = d_cs; pl->d_ce_c = d_ce;
+  pl->d_pe_c = d_pe; pl->d_B_c = d_B;
   EdgeCtx& c = pl->ctx;
   c.nx = nx; c.nu = nu; c.ne = ne; c.E = E; c.NXP = NXP; c.NUP = NUP;
   c.Wx = pb->Wx; c.gamma_d = pb->gamma_d; c.W_alpha = pb->W_alpha;
@@ -923,6 +934,85 @@ int tsmpc_set_cache(tsmpc_plan* pl, const double* beta, const double* uhat, cons
   return TSMPC_OK;
 }
 
+int tsmpc_set_cache_operators(tsmpc_plan* pl, int32_t n_d, const double* part_map, const double* Gd,
+                              const double* Ed, const double* Rhat, const double* eps_edge, const double* pbar) {
+  if (!pl || !part_map || !Gd || !Ed || !Rhat || !eps_edge || !pbar) return fail(TSMPC_ERR_ARGUMENT, "null argument");
+  if (n_d < 1) return fail(TSMPC_ERR_DIMENSION, "n_d must be >= 1");
+  CU(cudaSetDevice(pl->device));
+  if (pl->has_cache_ops) {
+    if (n_d != pl->nd_c) return fail(TSMPC_ERR_DIMENSION, "n_d changed (%d -> %d)", pl->nd_c, n_d);
+  } else {
+    int rc = 0;
+    rc |= pl->alloc(&pl->PART_MAP, (size_t)pl->nu * n_d);
+    rc |= pl->alloc(&pl->GD, (size_t)pl->nx * n_d);
+    rc |= pl->alloc(&pl->ED, (size_t)pl->ne * n_d);
+    rc |= pl->alloc(&pl->RHAT, (size_t)pl->nu * pl->nv);
+    rc |= pl->alloc(&pl->EPS, (size_t)pl->E * n_d);
+    rc |= pl->alloc(&pl->PBAR, (size_t)pl->E);
+    rc |= pl->alloc(&pl->DHAT, (size_t)pl->N * n_d);
+    rc |= pl->alloc(&pl->ABAR, (size_t)pl->N * pl->nv);
+    if (rc) return rc;
+  }
+  pl->nd_c = n_d;
+  auto up = [&](double* dst, const double* src, size_t n) {
+    return cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyHostToDevice, pl->stream);
+  };
+  CU(up(pl->PART_MAP, part_map, (size_t)pl->nu * n_d));
+  CU(up(pl->GD, Gd, (size_t)pl->nx * n_d));
+  CU(up(pl->ED, Ed, (size_t)pl->ne * n_d));
+  CU(up(pl->RHAT, Rhat, (size_t)pl->nu * pl->nv));
+  CU(up(pl->EPS, eps_edge, (size_t)pl->E * n_d));
+  CU(up(pl->PBAR, pbar, (size_t)pl->E));
+  CU(cudaStreamSynchronize(pl->stream));
+  pl->has_cache_ops = true;
+  return TSMPC_OK;
+}
+
+int tsmpc_set_forecast(tsmpc_plan* pl, const double* dhat, const double* q, const double* prices,
+                       const double* abar) {
+  if (!pl || !dhat || !q || !prices || !abar) return fail(TSMPC_ERR_ARGUMENT, "null argument");
+  if (!pl->has_cache_ops) return fail(TSMPC_ERR_VALIDATION, "no cache operators (tsmpc_set_cache_operators)");
+  CU(cudaSetDevice(pl->device));
+  const int N = pl->N, nd = pl->nd_c;
+  CU(cudaMemcpyAsync(pl->DHAT, dhat, sizeof(double) * N * nd, cudaMemcpyHostToDevice, pl->stream));
+  CU(cudaMemcpyAsync(pl->ABAR, abar, sizeof(double) * N * pl->nv, cudaMemcpyHostToDevice, pl->stream));
+  CU(cudaMemcpyAsync(pl->Q, q, sizeof(double) * pl->nu, cudaMemcpyHostToDevice, pl->stream));
+  CU(cudaMemcpyAsync(pl->PRICES, prices, sizeof(double) * N * pl->nu, cudaMemcpyHostToDevice, pl->stream));
+  CacheArgs a{};
+  a.E = pl->E; a.nx = pl->nx; a.nu = pl->nu; a.nv = pl->nv; a.nd = nd; a.ne = pl->ne;
+  a.NXP = pl->NXP; a.NUP = pl->NUP; a.NVP = pl->NVP;
+  a.edge_stage = pl->d_est_c; a.anc = pl->d_anc_c; a.child_start = pl->d_cs_c; a.child_stop = pl->d_ce_c;
+  a.prob_edge = pl->d_pe_c; a.pbar = pl->PBAR; a.eps = pl->EPS;
+  a.part_map = pl->PART_MAP; a.B = pl->d_B_c; a.Gd = pl->GD; a.Ed = pl->ED; a.Rhat = pl->RHAT;
+  a.dhat = pl->DHAT; a.abar = pl->ABAR; a.q = pl->Q;
+  a.uhat = pl->UHAT; a.evec = pl->EVEC; a.beta = pl->BETA; a.jrhs = pl->JRHS; a.gdd = pl->GDD;
+  const int grid = std::max(1, std::min(pl->E, pl->sm_count * 8));
+  cache_rows_kernel<<<grid, 128, sizeof(double) * (nd + pl->nu), pl->stream>>>(a);
+  CU(cudaGetLastError());
+  cache_beta_kernel<<<grid, 128, sizeof(double) * pl->nu, pl->stream>>>(a);
+  CU(cudaGetLastError());
+  if (pl->use_sparse) {
+    beta_rotate_kernel<<<std::max(1, std::min((pl->E + 7) / 8, 148 * 8)), 256, 0, pl->stream>>>(pl->BETA, pl->MS,
+                                                                                              pl->BETA_S, pl->E,
+                                                                                              pl->nv, pl->NVP);
+    CU(cudaGetLastError());
+  }
+  CU(cudaStreamSynchronize(pl->stream));
+  pl->has_cache = true;
+  return TSMPC_OK;
+}
+
+int tsmpc_get_cache(tsmpc_plan* pl, double* beta, double* uhat, double* evec) {
+  if (!pl) return fail(TSMPC_ERR_ARGUMENT, "null argument");
+  if (!pl->has_cache) return fail(TSMPC_ERR_VALIDATION, "no stage cache on the device");
+  CU(cudaSetDevice(pl->device));
+  if (pl->get_rows(beta, pl->nv, pl->BETA, pl->NVP, pl->E) || pl->get_rows(uhat, pl->nu, pl->UHAT, pl->NUP, pl->E) ||
+      pl->get_rows(evec, pl->nx, pl->EVEC, pl->NXP, pl->E))
+    return TSMPC_ERR_CUDA;
+  CU(cudaStreamSynchronize(pl->stream));
+  return TSMPC_OK;
+}
+
 static int set_root(tsmpc_plan* pl, const double* p) {
   std::vector<double> pp(pl->NXP, 0.0);
   if (p) std::copy(p, p + pl->nx, pp.begin());
@@ -1037,7 +1127,12 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
   CU(cudaMemsetAsync(pl->RESID, 0, sizeof(unsigned long long) * nres, pl->stream));
   // dual start
   const size_t yblk = 2 * (size_t)E * NXP + (size_t)E * NUP;
-  if (warm_sig && warm_zeta && warm_psi) {
+  if ((flags & TSMPC_WARM_DEVICE) && pl->last_y) {
+    // warm start from the previous solve's final dual, still resident in HBM
+    if (pl->last_y != pl->Y0)
+      CU(cudaMemcpyAsync(pl->Y0, pl->last_y, sizeof(double) * yblk, cudaMemcpyDeviceToDevice, pl->stream));
+    CU(cudaMemcpyAsync(pl->Y1, pl->Y0, sizeof(double) * yblk, cudaMemcpyDeviceToDevice, pl->stream));
+  } else if (warm_sig && warm_zeta && warm_psi) {
     if (pl->put_rows(pl->Y0, NXP, warm_sig, nx, E) || pl->put_rows(pl->Y0 + (size_t)E * NXP, NXP, warm_zeta, nx, E) ||
         pl->put_rows(pl->Y0 + 2 * (size_t)E * NXP, NUP, warm_psi, nu, E))
       return TSMPC_ERR_CUDA;
@@ -1104,6 +1199,7 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
   }
   CU(cudaEventRecord(pl->ev1, pl->stream));
   double* yfin = ((iters & 1) == 0) ? pl->Y0 : pl->Y1;
+  pl->last_y = yfin;
   // keep the last iterate before the gap's solve step reuses X / U
   CU(cudaMemcpyAsync(pl->XL, pl->X, sizeof(double) * (size_t)pl->n_nodes * NXP, cudaMemcpyDeviceToDevice, pl->stream));
   CU(cudaMemcpyAsync(pl->UL, pl->U, sizeof(double) * (size_t)E * NUP, cudaMemcpyDeviceToDevice, pl->stream));
@@ -1117,13 +1213,13 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
   out->iterations = iters;
   std::vector<unsigned long long> rbits(nres);
   CU(cudaMemcpyAsync(rbits.data(), pl->RESID, sizeof(unsigned long long) * nres, cudaMemcpyDeviceToHost, pl->stream));
+  if (pl->get_rows(out->u0, nu, pl->UAVG, NUP, 1)) return TSMPC_ERR_CUDA;
   if (!(flags & TSMPC_KEEP_DEVICE)) {
     int rc = 0;
     rc |= pl->get_rows(out->x, nx, pl->XL, NXP, pl->n_nodes);
     rc |= pl->get_rows(out->u, nu, pl->UL, NUP, E);
     rc |= pl->get_rows(out->x_avg, nx, pl->XAVG, NXP, pl->n_nodes);
     rc |= pl->get_rows(out->u_avg, nu, pl->UAVG, NUP, E);
-    rc |= pl->get_rows(out->u0, nu, pl->UAVG, NUP, 1);
     rc |= pl->get_rows(out->dual_sig, nx, yfin, NXP, E);
     rc |= pl->get_rows(out->dual_zeta, nx, yfin + (size_t)E * NXP, NXP, E);
     rc |= pl->get_rows(out->dual_psi, nu, yfin + 2 * (size_t)E * NXP, NUP, E);

@@ -25,7 +25,6 @@ from .points import DualPoint, PrimalPoint, SplitPoint
 from .precompute import (DualScaling, build_stage_cache, compute_basis,
                          compute_preconditioner, dual_hessian_row_sums, factor_step,
                          theta_schedule, theta_update)
-from .tree import node_demands
 
 __all__ = [
     "SolverConfig", "SolveReport", "DualScaling",
@@ -226,9 +225,6 @@ def solve(model, tree, forecast, p, q, config: SolverConfig | None = None, *,
         raise DimensionError(f"q: shape {q.shape}, expected ({model.n_u},)")
     basis = basis or compute_basis(model)
     factor = factor or factor_step(basis, model)
-    if cache is None:
-        cache = build_stage_cache(basis, model, tree, node_demands(tree, forecast),
-                                  k=forecast.k, q=q)
     if config.precondition and scaling is None:
         scaling = compute_preconditioner(basis, model, tree.N, tree=tree)
     if not config.precondition:
@@ -238,7 +234,14 @@ def solve(model, tree, forecast, p, q, config: SolverConfig | None = None, *,
         lam = compute_lambda(basis, factor, model, tree, scaling=scaling, device=config.device)
 
     plan = plan_for(model, tree, factor, scaling, config.device)
-    plan.set_cache(cache, model)
+    if cache is None:
+        # stage cache built on the device from the forecast
+        if forecast.dhat.shape[0] != tree.N:
+            raise DimensionError(
+                f"forecast horizon {forecast.dhat.shape[0]} does not match tree horizon {tree.N}")
+        plan.set_forecast(forecast, q, basis, model)
+    else:
+        plan.set_cache(cache, model)
     theta, coef = theta_schedule(config.max_iters)
     warm = warm_dual if (config.warm_start and warm_dual is not None) else None
     t0 = time.perf_counter()

@@ -130,10 +130,54 @@ class DevicePlan:
         self._cache_key = key
         self._cache_ref = cache
 
+    def set_forecast(self, forecast, q, basis, model=None):
+        """Build the stage cache of ``forecast`` on the device (reference
+        ``elimination.py:114-158`` / ``tree.py:319-331``): only dhat (N x n_d), the
+        stage prices, the reduced prices and q are uploaded."""
+        m = model if model is not None else self.model
+        tree = self.tree
+        N = tree.N
+        dhat = _c(forecast.dhat)
+        if dhat.shape != (N, m.n_d):
+            raise DimensionError(f"forecast dhat: shape {dhat.shape}, expected ({N}, {m.n_d})")
+        q = _c(q)
+        if q.shape != (self.n_u,):
+            raise DimensionError(f"q: shape {q.shape}, expected ({self.n_u},)")
+        if not getattr(self, "_cache_ops", False):
+            pe = np.asarray(tree.edge_prob, dtype=float)
+            pa = np.asarray(tree.parent_edge())
+            pbar = pe.copy()
+            inner = pa >= 0
+            np.add.at(pbar, pa[inner], pe[inner])
+            ops = [_c(basis.part_map), _c(m.Gd), _c(m.Ed), _c(basis.Rhat), _c(tree.edge_eps), _c(pbar)]
+            nat.check(self._lib.tsmpc_set_cache_operators(self._h, int(m.n_d), *map(nat.dptr, ops)),
+                      "tsmpc_set_cache_operators")
+            self._cache_ops = True
+            self._basis_L = np.asarray(basis.L)
+        k = int(forecast.k)
+        prices = _c(np.stack([m.price(k + j) for j in range(N)]))
+        abar = _c(m.W_alpha * (prices @ self._basis_L))
+        nat.check(self._lib.tsmpc_set_forecast(self._h, nat.dptr(dhat), nat.dptr(q), nat.dptr(prices),
+                                               nat.dptr(abar)), "tsmpc_set_forecast")
+        self._cache_key = ("forecast", id(forecast), k)
+        self._cache_ref = None
+
+    def get_cache(self):
+        """(beta, uhat, evec) currently on the device (tests)."""
+        E = self.n_edges
+        beta, uhat, evec = np.empty((E, self.n_v)), np.empty((E, self.n_u)), np.empty((E, self.n_x))
+        nat.check(self._lib.tsmpc_get_cache(self._h, nat.dptr(beta), nat.dptr(uhat), nat.dptr(evec)),
+                  "tsmpc_get_cache")
+        return beta, uhat, evec
+
     # -- solver entry points ---------------------------------------------------
     def solve(self, p, iters: int, lam: float, warm: DualPoint | None = None,
               theta=None, coef=None, record_residuals: bool = False,
-              skip_gap: bool = False, keep_device: bool = False) -> dict:
+              skip_gap: bool = False, keep_device: bool = False,
+              warm_device: bool = False) -> dict:
+        """One APG solve (engine.py:485-601).  ``keep_device``: leave the iterates in
+        HBM (only u0, residual and gap come back); ``warm_device``: start from the
+        previous solve's final dual, still in HBM (closed-loop warm start)."""
         E, n_x, n_u, n = self.n_edges, self.n_x, self.n_u, self.n_nodes
         out = {
             "u0": np.empty(n_u), "x": np.empty((n, n_x)), "u": np.empty((E, n_u)),
@@ -142,13 +186,15 @@ class DevicePlan:
             "dual_psi": np.empty((E, n_u)),
         }
         res = nat.Result()
+        res.u0 = nat.dptr(out["u0"])
         if not keep_device:
             for k, v in out.items():
                 setattr(res, k, nat.dptr(v))
         trace = np.empty(iters) if record_residuals else None
         res.resid_trace = nat.dptr(trace)
         flags = ((nat.RECORD_RESIDUALS if record_residuals else 0)
-                 | (nat.SKIP_GAP if skip_gap else 0) | (nat.KEEP_DEVICE if keep_device else 0))
+                 | (nat.SKIP_GAP if skip_gap else 0) | (nat.KEEP_DEVICE if keep_device else 0)
+                 | (nat.WARM_DEVICE if warm_device else 0))
         ws = wz = wp = None
         if warm is not None:
             ws, wz, wp = _c(warm.sig), _c(warm.zeta), _c(warm.psi)
