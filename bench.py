@@ -241,6 +241,8 @@ def run_ours(args, ws, rank, local):
         line["sweep"] = sweep(args, lam_cache={args.tree: lam}, local=local)
     if rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(W, lam, args)
+        if not args.no_closed_loop:
+            line["closed_loop"] = closed_loop_measure(args, local, line["cpu_baseline"], W)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
@@ -286,6 +288,45 @@ def sharded_measure(args, ws, rank, local, dist):
             "exchange_bytes_per_iter": 8 * info["trunk_edges"] * (97 + 64),
             "note": "per iteration: phase 1 (backward, head sums) -> ncclAllReduce -> phase 2; "
                     "duality gap not evaluated on shard plans"}
+
+
+def closed_loop_measure(args, local, cpu, W):
+    """BASELINE configs[4]: closed-loop SMPC (Algorithm 2) with warm-started duals;
+    per-step latency = forecast upload + device stage cache + 500-iteration solve +
+    duality gap + u0 read-back (wall clock on the host, median over the steps)."""
+    from paper_1604_01074_b200 import SolverConfig, synth
+    from paper_1604_01074_b200.closed_loop import SimulationConfig, run_closed_loop
+    tree = W["tree"]
+    h_s = args.cl_steps
+    base = synth.base_demand(W["model"].n_d)
+    nominal = np.stack([synth.forecast_profile(base, k, 1)[0] for k in range(h_s + tree.N)])
+    realized = nominal[:h_s] * (1.0 + 0.05 * np.random.default_rng(7).standard_normal(nominal[:h_s].shape))
+    lam = 0.4797
+    cfg = SimulationConfig(network=W["model"], tree=tree, demands=realized, forecast=nominal, h_s=h_s,
+                           x0=W["p"], u_prev=W["q"],
+                           solver=SolverConfig(max_iters=args.iters, lam=lam, warm_start=True,
+                                               device=local))
+    run_closed_loop(SimulationConfig(**{**cfg.__dict__, "h_s": 2}))  # warm-up (plan, caches)
+    res = run_closed_loop(cfg)
+    step_ms = res.wall_times["step_s_median"] * 1e3
+    out = {"tree": args.tree, "h_s": h_s, "iters_per_step": args.iters, "warm_start": True,
+           "per_step_ms_median": step_ms, "per_step_ms_mean": res.wall_times["per_step_s"] * 1e3,
+           "kpis": res.kpis.to_dict(), "max_residual": float(np.max(res.residuals)),
+           "upload_bytes_per_step": 8 * (tree.N * (W["model"].n_d + W["model"].n_u + 97)
+                                         + W["model"].n_u + W["model"].n_x)}
+    if cpu:
+        from paper_1604_01074_b200 import build_stage_cache, node_demands
+        from paper_1604_01074_b200.tree import DemandForecast
+        t0 = time.perf_counter()
+        build_stage_cache(W["basis"], W["model"], tree,
+                          node_demands(tree, DemandForecast(nominal[:tree.N], k=0)), k=0, q=W["q"])
+        t_cache = time.perf_counter() - t0
+        cpu_step = t_cache + args.iters / cpu["value"]
+        out["cpu_reference_per_step_ms"] = cpu_step * 1e3
+        out["cpu_reference_note"] = (f"host stage cache ({t_cache * 1e3:.1f} ms) + {args.iters} iterations "
+                                     f"at the cpu_baseline rate ({cpu['value']:.1f} iter/s, 1 core); "
+                                     "the reference's gap evaluation is not included")
+    return out
 
 
 def ncu_traffic(kernel: str, tree: str, iters: int):
@@ -422,6 +463,8 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-shard", action="store_true")
+    ap.add_argument("--no-closed-loop", action="store_true")
+    ap.add_argument("--cl-steps", type=int, default=24)
     ap.add_argument("--shard-tree", default="SMPC8", choices=("SMPC3", "SMPC8", "W4k"))
     args = ap.parse_args()
     ws, rank, local = dist_env()
