@@ -357,6 +357,92 @@ __global__ void __launch_bounds__(256) gap_project_dykstra_kernel(EdgeCtx c, dou
   }
 }
 
+// Dykstra without grid barriers (engine.py:407-419).  The reference stops every
+// edge at the first sweep whose change, maxed over ALL edges, is < 1e-13.  Each
+// edge's iterates do not depend on the others, so: pass 1 runs every edge's 200
+// sweeps in shared memory and records the per-sweep max change (atomicMax into
+// slots[it]); pass 2 finds the global stopping sweep K from slots and re-runs each
+// edge for exactly K + 1 sweeps (or 200), then applies the final affine projection.
+// The junction operators are sparse (a junction touches a few flows): E by row
+// and E_pinv^T by column are staged in shared memory; warp per edge.
+__global__ void __launch_bounds__(256) gap_dykstra_pass_kernel(EdgeCtx c, const double* __restrict__ u0,
+                                                               unsigned long long* slots, int pass,
+                                                               double* uf) {
+  extern __shared__ double dsm[];
+  // sparse E (rows) and E_pinv^T (columns) staged in shared memory
+  double* ev = dsm;                                   // er_nnz
+  double* pv = ev + c.er_nnz;                         // pc_nnz
+  double* wsm = pv + c.pc_nnz + (c.pc_nnz + c.er_nnz & 1);  // 16-byte aligned per-warp scratch
+  int* ei = reinterpret_cast<int*>(wsm + 8 * 448);    // er_ptr (ne+1) | er_idx | pc_ptr (nu+1) | pc_idx
+  int* ep = ei;
+  int* eix = ep + c.ne + 1;
+  int* pp = eix + c.er_nnz;
+  int* pix = pp + c.nu + 1;
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < c.er_nnz; i += blockDim.x) { ev[i] = c.er_val[i]; eix[i] = c.er_idx[i]; }
+  for (int i = threadIdx.x; i < c.pc_nnz; i += blockDim.x) { pv[i] = c.pc_val[i]; pix[i] = c.pc_idx[i]; }
+  for (int i = threadIdx.x; i <= c.ne; i += blockDim.x) ep[i] = c.er_ptr[i];
+  for (int i = threadIdx.x; i <= c.nu; i += blockDim.x) pp[i] = c.pc_ptr[i];
+  __syncthreads();
+  // ya = x - (x E' - target) pinv'  (engine.py:409), non-zeros only, ascending order
+  auto project = [&](const double* xx, const double* tgt, double* rr, double* ya) {
+    for (int k = lane; k < c.ne; k += 32) {
+      double s = 0.0;
+      for (int q = ep[k]; q < ep[k + 1]; ++q) s = fma(xx[eix[q]], ev[q], s);
+      rr[k] = s - tgt[k];
+    }
+    __syncwarp();
+    for (int jj = lane; jj < c.nu; jj += 32) {
+      double s = 0.0;
+      for (int q = pp[jj]; q < pp[jj + 1]; ++q) s = fma(rr[pix[q]], pv[q], s);
+      ya[jj] = xx[jj] - s;
+    }
+    __syncwarp();
+  };
+  double* x = wsm + (size_t)wl * 448;
+  double* y = x + 128;
+  double* r = y + 128;
+  double* inc = r + 64;
+  int n_it = 200;
+  if (pass == 2) {
+    for (int it = 0; it < 200; ++it) {
+      const double g = __longlong_as_double((long long)slots[it]);
+      if (g < 1e-13) { n_it = it + 1; break; }
+    }
+  }
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int e = gw; e < c.E; e += nw) {
+    for (int j = lane; j < c.nu; j += 32) {
+      x[j] = u0[(size_t)e * c.NUP + j];
+      inc[j] = 0.0;
+    }
+    __syncwarp();
+    const double* tgt = c.jrhs + (size_t)e * c.ne;
+    for (int it = 0; it < n_it; ++it) {
+      project(x, tgt, r, y);
+      double mx = 0.0;
+      for (int j = lane; j < c.nu; j += 32) {
+        const double t = y[j] + inc[j];
+        const double xn = clip(t, c.u_min[j], c.u_max[j]);
+        inc[j] = t - xn;
+        mx = fmax(mx, fabs(xn - x[j]));
+        x[j] = xn;
+      }
+      __syncwarp();
+      if (pass == 1) {
+        mx = warp_max(mx);
+        if (lane == 0 && mx > 0.0) atomicMax(slots + it, (unsigned long long)__double_as_longlong(mx));
+      }
+    }
+    if (pass == 2) {
+      project(x, tgt, r, y);
+      for (int j = lane; j < c.nu; j += 32) uf[(size_t)e * c.NUP + j] = y[j];
+      __syncwarp();
+    }
+  }
+}
+
 // ub_e = u_feas_e B'   (E x NXP)
 __global__ void gap_ub_kernel(EdgeCtx c, const double* __restrict__ uf, double* ub) {
   __shared__ double shm[8][128];

@@ -24,6 +24,11 @@ struct EdgeCtx {
   const double* B;          // nx*nu
   const double* a_diag;     // NXP or null
   const double* A;          // nx*nx
+  // sparse junction operators for the Dykstra projection: E by row (CSR) and
+  // E_pinv^T by column (CSC), ascending order = the dense summation order
+  const int *er_ptr, *er_idx, *pc_ptr, *pc_idx;
+  const double *er_val, *pc_val;
+  int er_nnz, pc_nnz;
 };
 
 struct ProxArgs {
@@ -48,6 +53,8 @@ __global__ void gap_dual_terms_kernel(EdgeCtx c, const double* what, const doubl
 __global__ void gap_project_bisect_kernel(EdgeCtx c, const double* uavg, double* uf);
 __global__ void gap_project_dykstra_kernel(EdgeCtx c, double* xit, double* inc, double* uf,
                                            unsigned long long* slots);
+__global__ void gap_dykstra_pass_kernel(EdgeCtx c, const double* __restrict__ u0,
+                                        unsigned long long* slots, int pass, double* uf);
 __global__ void gap_ub_kernel(EdgeCtx c, const double* uf, double* ub);
 __global__ void gap_propagate_stage_kernel(EdgeCtx c, int n0, int n1, double* xf, const double* ub);
 __global__ void gap_primal_terms_kernel(EdgeCtx c, const double* uf, const double* xf, double* cols);

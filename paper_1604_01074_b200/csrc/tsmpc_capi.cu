@@ -762,6 +762,34 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
     }
   }
 
+  cudaFuncSetAttribute(gap_dykstra_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(sizeof(double) * (2 * 64 * 128 + 8 * 448 + 1) + sizeof(int) * (2 * 64 * 128 + 200)));
+  {  // sparse junction operators for the gap's Dykstra projection
+    std::vector<int> erp{0}, eri, pcp{0}, pci;
+    std::vector<double> erv, pcv;
+    for (int k = 0; k < ne; ++k) {
+      for (int j = 0; j < nu; ++j)
+        if (pb->E[(size_t)k * nu + j] != 0.0) { eri.push_back(j); erv.push_back(pb->E[(size_t)k * nu + j]); }
+      erp.push_back((int)eri.size());
+    }
+    for (int j = 0; j < nu; ++j) {
+      for (int k = 0; k < ne; ++k)
+        if (pb->E_pinvT[(size_t)k * nu + j] != 0.0) { pci.push_back(k); pcv.push_back(pb->E_pinvT[(size_t)k * nu + j]); }
+      pcp.push_back((int)pci.size());
+    }
+    int *d_erp, *d_eri, *d_pcp, *d_pci;
+    double *d_erv, *d_pcv;
+    rc |= pl->upload(&d_erp, erp.data(), erp.size());
+    rc |= pl->upload(&d_eri, eri.data(), std::max<size_t>(1, eri.size()));
+    rc |= pl->upload(&d_erv, erv.data(), std::max<size_t>(1, erv.size()));
+    rc |= pl->upload(&d_pcp, pcp.data(), pcp.size());
+    rc |= pl->upload(&d_pci, pci.data(), std::max<size_t>(1, pci.size()));
+    rc |= pl->upload(&d_pcv, pcv.data(), std::max<size_t>(1, pcv.size()));
+    if (rc) return bail(0);
+    c.er_ptr = d_erp; c.er_idx = d_eri; c.er_val = d_erv; c.er_nnz = (int)eri.size();
+    c.pc_ptr = d_pcp; c.pc_idx = d_pci; c.pc_val = d_pcv; c.pc_nnz = (int)pci.size();
+  }
+
   int occ_d = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_d, gap_project_dykstra_kernel, 256, 0);
   pl->dyk_blocks = std::max(1, std::min(occ_d, 4)) * pl->sm_count;
@@ -1055,13 +1083,15 @@ static int compute_gap(tsmpc_plan* pl, const double* yfinal, double* gap) {
     gap_project_bisect_kernel<<<G, 256, 0, pl->stream>>>(c, pl->UAVG, pl->UF);
     CU(cudaGetLastError());
   } else {
-    CU(cudaMemcpyAsync(pl->XIT, pl->UAVG, sizeof(double) * (size_t)E * pl->NUP, cudaMemcpyDeviceToDevice,
-                       pl->stream));
-    CU(cudaMemsetAsync(pl->INC, 0, sizeof(double) * (size_t)E * pl->NUP, pl->stream));
     CU(cudaMemsetAsync(pl->DYK, 0, sizeof(unsigned long long) * 256, pl->stream));
-    void* args[] = {&c, &pl->XIT, &pl->INC, &pl->UF, &pl->DYK};
-    CU(cudaLaunchCooperativeKernel((void*)gap_project_dykstra_kernel, dim3(pl->dyk_blocks), dim3(256), args, 0,
-                                   pl->stream));
+    const size_t dsm = sizeof(double) * ((size_t)c.er_nnz + c.pc_nnz + 1 + 8 * 448) +
+                       sizeof(int) * ((size_t)pl->ne + 1 + c.er_nnz + pl->nu + 1 + c.pc_nnz);
+    const int gblk = std::max(1, std::min((E + 7) / 8, pl->sm_count * 8));
+    gap_dykstra_pass_kernel<<<gblk, 256, dsm, pl->stream>>>(c, pl->UAVG, pl->DYK, 1, pl->UF);
+    CU(cudaGetLastError());
+    gap_dykstra_pass_kernel<<<gblk, 256, dsm, pl->stream>>>(c, pl->UAVG, pl->DYK, 2, pl->UF);
+    CU(cudaGetLastError());
+    pl->launches += 1;
   }
   gap_ub_kernel<<<G, 256, 0, pl->stream>>>(c, pl->UF, pl->UB);
   CU(cudaGetLastError());
