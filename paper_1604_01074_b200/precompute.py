@@ -19,6 +19,7 @@ The device kernels consume two fused operator blocks derived here (see
 
 from __future__ import annotations
 
+import functools
 import warnings
 from dataclasses import dataclass
 
@@ -326,6 +327,7 @@ def theta_update(theta: float) -> float:
     return 0.5 * (np.sqrt(theta ** 4 + 4.0 * theta ** 2) - theta ** 2)
 
 
+@functools.lru_cache(maxsize=16)
 def theta_schedule(iters: int):
     """Per-iteration (theta_nu, extrapolation coefficient) tables, host fp64.
 
@@ -341,4 +343,6 @@ def theta_schedule(iters: int):
         theta[nu] = th
         coef[nu] = th * (1.0 / th_prev - 1.0)
         th_prev, th = th, theta_update(th)
+    theta.setflags(write=False)  # cached: shared by every solve with this iteration count
+    coef.setflags(write=False)
     return theta, coef
