@@ -237,149 +237,162 @@ __device__ __noinline__ void load_rows(const int* edges, int estride, int nrows,
 
 // ----------------------------------------------------------------------------
 // epilogue: prox_g (engine.py:146-183), dual update, ergodic averages, residual
-// (engine.py:546-575) for nrows <= kTileS rows described by c.rdesc():
-// {edge, stage, x offset, u offset, slot-row offset} (offsets in doubles from
-// the dynamic shared-memory base).  Dual rows: y at index ysm, y_prev at ysm ^ 1;
-// y+ replaces y_prev in place.  wt: also write y+ and the ergodic rows to HBM
-// (slot `ncur` receives y+).  The two weighted-distance prox blocks need a norm
-// over the n_x components: per-warp shuffle sums combined across the group's
-// warps in a fixed order.
+// (engine.py:546-575) for rows described by c.rdesc(): {edge, stage, x offset,
+// u offset, slot-row offset} (offsets in doubles from the dynamic shared-memory
+// base).  Dual rows: y at index ysm, y_prev at ysm ^ 1; y+ replaces y_prev in
+// place.  wt: also write y+ and the ergodic rows to HBM (slot `ncur` gets y+).
+//
+// psi block (box projection, elementwise): thread (g, k) for its rows, given u.
+// state blocks (two weighted-distance proxes): one warp per row — the row norm
+// is a warp reduction and the prox factor a warp-uniform scalar, so the block
+// needs no shared-memory exchange and no barrier.
 // ----------------------------------------------------------------------------
-__device__ __noinline__ void epilogue(int nu_it, double cf, double th, int nrows, int ysm,
-                                      bool wt, int ncur, double* rmax_io) {
+struct EpiConst {
+  double cf, th, om, lam, ilam, lam_p;
+  bool last, want, wt;
+  double* Yn;
+};
+
+__device__ __forceinline__ EpiConst epi_const(const Params& P, int nu_it, double cf, double th, bool wt, int ncur) {
+  EpiConst k;
+  k.cf = cf;
+  k.th = th;
+  k.om = __dsub_rn(1.0, th);
+  k.lam = P.lam;
+  k.ilam = P.inv_lam;
+  k.lam_p = 1.0 / P.lam;
+  k.last = nu_it == P.iters - 1;
+  k.want = k.last || P.record_all;
+  k.wt = wt;
+  k.Yn = P.ybuf[ncur];
+  return k;
+}
+
+// psi block of row r, component k (k < n_u); u = the row's control component
+__device__ __forceinline__ void epi_psi_elem(const Ctx& c, const Params& P, const EpiConst& q, const int* d,
+                                             int ysm, int k, double u, double& rmax) {
+  const int e = d[0], st = d[1];
+  double* row = s_dyn + d[4];
+  const double* yc = row + (size_t)ysm * c.YW + 2 * c.NXP;
+  double* yp = row + (size_t)(ysm ^ 1) * c.YW + 2 * c.NXP;
+  const double dp = c.dpsi(st, k);
+  const double w = extrap(yc[k], yp[k], q.cf);
+  const double hp = __dmul_rn(u, dp);
+  const double a = __dadd_rn(__dmul_rn(w, q.ilam), hp);
+  const double t = fmin(fmax(a, __dmul_rn(dp, c.bnd[3 * c.NXP + k])), __dmul_rn(dp, c.bnd[3 * c.NXP + c.NUP + k]));
+  const double ny = __dadd_rn(w, __dmul_rn(q.lam, __dsub_rn(hp, t)));
+  yp[k] = ny;
+  if (q.want) rmax = fmax(rmax, fabs(__dsub_rn(u, __ddiv_rn(t, dp))));
+  double* ua = row + 2 * c.YW + c.NXP;
+  const double na = __dadd_rn(__dmul_rn(ua[k], q.om), __dmul_rn(q.th, u));
+  ua[k] = na;
+  if (q.wt) {
+    stcg(q.Yn + 2 * (size_t)c.E * c.NXP + (size_t)e * c.NUP + k, ny);
+    stcg(P.uavg + (size_t)e * c.NUP + k, na);
+  }
+  if (q.last) stcg(P.U + (size_t)e * c.NUP + k, u);
+}
+
+// state blocks of rows described by rdesc, one warp per row
+__device__ __noinline__ void epi_state(int nu_it, double cf, double th, int nrows, int ysm, bool wt, int ncur,
+                                       double* rmax_io) {
   const SParams& S = g_sp;
   const Ctx c = ctx_of();
   const Params& P = S.P;
-  const int k = threadIdx.x & (kKW - 1), g = threadIdx.x / kKW, lane = threadIdx.x & 31, w4 = k >> 5;
-  const bool last = nu_it == P.iters - 1;
-  const bool want = last || P.record_all;
-  const double om = __dsub_rn(1.0, th);
-  const double lam = P.lam, ilam = P.inv_lam, lam_p = 1.0 / lam;
+  const EpiConst q = epi_const(P, nu_it, cf, th, wt, ncur);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const size_t E = (size_t)c.E;
-  double* Yn = P.ybuf[ncur];
   const double* xs_s = c.bnd;
   const double* xmn_s = c.bnd + c.NXP;
   const double* xmx_s = c.bnd + 2 * c.NXP;
-  const double* umn_s = c.bnd + 3 * c.NXP;
-  const double* umx_s = c.bnd + 3 * c.NXP + c.NUP;
   const int N = c.N;
-  const bool xk = k < c.nx, uk = k < c.nu;
-  const int* rd = c.rdesc();
   double rmax = *rmax_io;
-  long long te_ = clock64();
-  (void)te_;
-  // pass 1: psi block (complete) and the warp sums of the squared distances of the
-  // state blocks
-#pragma unroll 2
-  for (int m = 0; m < kRowsPT; ++m) {
-    const int r = g + kGroups * m;
-    if (r >= nrows) break;
-    const int* d = rd + 5 * r;
+#pragma unroll 1
+  for (int r = warp; r < nrows; r += kWarpsS) {
+    const int* d = c.rdesc() + 5 * r;
     const int e = d[0], st = d[1];
     double* row = s_dyn + d[4];
-    double* yc = row + (size_t)ysm * c.YW;
+    const double* yc = row + (size_t)ysm * c.YW;
     double* yp = row + (size_t)(ysm ^ 1) * c.YW;
+    double* xa = row + 2 * c.YW;
+    const double* x = s_dyn + d[2];
+    const double ds = c.scl[st], dz = c.scl[N + st];
+    double ws[4], wz[4], ts[4], tz[4];
     double ss = 0.0, sz = 0.0;
-    if (xk) {
-      const double ds = c.scl[st], dz = c.scl[N + st];
-      const double ws = extrap(yc[k], yp[k], cf);
-      const double wz = extrap(yc[c.NXP + k], yp[c.NXP + k], cf);
-      const double xi = s_dyn[d[2] + k];
-      const double ts = __dadd_rn(__dmul_rn(ws, ilam), __dmul_rn(xi, ds));
-      const double tz = __dadd_rn(__dmul_rn(wz, ilam), __dmul_rn(xi, dz));
-      const double gs_ = __dsub_rn(fmax(ts, __dmul_rn(ds, xs_s[k])), ts);
-      const double gz = __dsub_rn(fmin(fmax(tz, __dmul_rn(dz, xmn_s[k])), __dmul_rn(dz, xmx_s[k])), tz);
-      ss = __dmul_rn(gs_, gs_);
-      sz = __dmul_rn(gz, gz);
-    }
-    if (uk) {
-      const double u = s_dyn[d[3] + k];
-      const double dp = c.dpsi(st, k);
-      const double w = extrap(yc[2 * c.NXP + k], yp[2 * c.NXP + k], cf);
-      const double hp = __dmul_rn(u, dp);
-      const double a = __dadd_rn(__dmul_rn(w, ilam), hp);
-      const double t = fmin(fmax(a, __dmul_rn(dp, umn_s[k])), __dmul_rn(dp, umx_s[k]));
-      const double ny = __dadd_rn(w, __dmul_rn(lam, __dsub_rn(hp, t)));
-      yp[2 * c.NXP + k] = ny;
-      if (want) rmax = fmax(rmax, fabs(__dsub_rn(u, __ddiv_rn(t, dp))));
-      double* ua = row + 2 * c.YW + c.NXP;
-      const double na = __dadd_rn(__dmul_rn(ua[k], om), __dmul_rn(th, u));
-      ua[k] = na;
-      if (wt) {
-        stcg(Yn + 2 * E * c.NXP + (size_t)e * c.NUP + k, ny);
-        stcg(P.uavg + (size_t)e * c.NUP + k, na);
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int i = lane + 32 * m;
+      ws[m] = wz[m] = ts[m] = tz[m] = 0.0;
+      if (i < c.nx) {
+        ws[m] = extrap(yc[i], yp[i], q.cf);
+        wz[m] = extrap(yc[c.NXP + i], yp[c.NXP + i], q.cf);
+        const double xi = x[i];
+        ts[m] = __dadd_rn(__dmul_rn(ws[m], q.ilam), __dmul_rn(xi, ds));
+        tz[m] = __dadd_rn(__dmul_rn(wz[m], q.ilam), __dmul_rn(xi, dz));
+        const double gs_ = __dsub_rn(fmax(ts[m], __dmul_rn(ds, xs_s[i])), ts[m]);
+        const double gz = __dsub_rn(fmin(fmax(tz[m], __dmul_rn(dz, xmn_s[i])), __dmul_rn(dz, xmx_s[i])), tz[m]);
+        ss = fma(gs_, gs_, ss);
+        sz = fma(gz, gz, sz);
       }
-      if (last) stcg(P.U + (size_t)e * c.NUP + k, u);
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
       ss += __shfl_xor_sync(0xffffffffu, ss, off);
       sz += __shfl_xor_sync(0xffffffffu, sz, off);
     }
-    if (lane == 0) {
-      c.red[(r * 4 + w4) * 2] = ss;
-      c.red[(r * 4 + w4) * 2 + 1] = sz;
-    }
-  }
-  __syncthreads();
-  TSMPC_MARK(P, 13, te_);
-  // pass 1.5: one thread per row -> the two prox factors min(1, weight / distance)
-  if (threadIdx.x < nrows) {
-    const int r = threadIdx.x, st = rd[5 * r + 1];
-    const double* q = c.red + r * 8;
-    const double ss = ((q[0] + q[2]) + q[4]) + q[6];
-    const double sz = ((q[1] + q[3]) + q[5]) + q[7];
     const double dist_s = sqrt(ss), dist_z = sqrt(sz);
-    const double wgt_s = __dmul_rn(__dmul_rn(lam_p, P.Wx), c.scl[2 * N + st]);
-    const double wgt_z = __dmul_rn(__dmul_rn(lam_p, P.gamma_d), c.scl[3 * N + st]);
-    c.fac()[2 * r] = dist_s > wgt_s ? __ddiv_rn(wgt_s, dist_s) : 1.0;
-    c.fac()[2 * r + 1] = dist_z > wgt_z ? __ddiv_rn(wgt_z, dist_z) : 1.0;
-  }
-  __syncthreads();
-  TSMPC_MARK(P, 14, te_);
-  // pass 2: the state blocks
-  if (xk) {
-#pragma unroll 2
-    for (int m = 0; m < kRowsPT; ++m) {
-      const int r = g + kGroups * m;
-      if (r >= nrows) break;
-      const int* d = rd + 5 * r;
-      const int e = d[0], st = d[1];
-      double* row = s_dyn + d[4];
-      double* yc = row + (size_t)ysm * c.YW;
-      double* yp = row + (size_t)(ysm ^ 1) * c.YW;
-      double* xa = row + 2 * c.YW;
-      const double fs = c.fac()[2 * r], fz = c.fac()[2 * r + 1];
-      const double ds = c.scl[st], dz = c.scl[N + st];
-      const double ws = extrap(yc[k], yp[k], cf);
-      const double wz = extrap(yc[c.NXP + k], yp[c.NXP + k], cf);
-      const double xi = s_dyn[d[2] + k];
-      const double ts = __dadd_rn(__dmul_rn(ws, ilam), __dmul_rn(xi, ds));
-      const double tz = __dadd_rn(__dmul_rn(wz, ilam), __dmul_rn(xi, dz));
-      const double hs = __dmul_rn(xi, ds), hz = __dmul_rn(xi, dz);
-      const double ps = fmax(ts, __dmul_rn(ds, xs_s[k]));
-      const double pz = fmin(fmax(tz, __dmul_rn(dz, xmn_s[k])), __dmul_rn(dz, xmx_s[k]));
-      const double t_s = __dadd_rn(ts, __dmul_rn(fs, __dsub_rn(ps, ts)));
-      const double t_z = __dadd_rn(tz, __dmul_rn(fz, __dsub_rn(pz, tz)));
-      const double ns = __dadd_rn(ws, __dmul_rn(lam, __dsub_rn(hs, t_s)));
-      const double nz = __dadd_rn(wz, __dmul_rn(lam, __dsub_rn(hz, t_z)));
-      yp[k] = ns;
-      yp[c.NXP + k] = nz;
-      if (want) {
-        rmax = fmax(rmax, fabs(__dsub_rn(xi, __ddiv_rn(t_s, ds))));
-        rmax = fmax(rmax, fabs(__dsub_rn(xi, __ddiv_rn(t_z, dz))));
+    const double wgt_s = __dmul_rn(__dmul_rn(q.lam_p, P.Wx), c.scl[2 * N + st]);
+    const double wgt_z = __dmul_rn(__dmul_rn(q.lam_p, P.gamma_d), c.scl[3 * N + st]);
+    const double fs = dist_s > wgt_s ? __ddiv_rn(wgt_s, dist_s) : 1.0;
+    const double fz = dist_z > wgt_z ? __ddiv_rn(wgt_z, dist_z) : 1.0;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int i = lane + 32 * m;
+      if (i < c.nx) {
+        const double xi = x[i];
+        const double hs = __dmul_rn(xi, ds), hz = __dmul_rn(xi, dz);
+        const double ps = fmax(ts[m], __dmul_rn(ds, xs_s[i]));
+        const double pz = fmin(fmax(tz[m], __dmul_rn(dz, xmn_s[i])), __dmul_rn(dz, xmx_s[i]));
+        const double t_s = __dadd_rn(ts[m], __dmul_rn(fs, __dsub_rn(ps, ts[m])));
+        const double t_z = __dadd_rn(tz[m], __dmul_rn(fz, __dsub_rn(pz, tz[m])));
+        const double ns = __dadd_rn(ws[m], __dmul_rn(q.lam, __dsub_rn(hs, t_s)));
+        const double nz = __dadd_rn(wz[m], __dmul_rn(q.lam, __dsub_rn(hz, t_z)));
+        yp[i] = ns;
+        yp[c.NXP + i] = nz;
+        if (q.want) {
+          rmax = fmax(rmax, fabs(__dsub_rn(xi, __ddiv_rn(t_s, ds))));
+          rmax = fmax(rmax, fabs(__dsub_rn(xi, __ddiv_rn(t_z, dz))));
+        }
+        const double na = __dadd_rn(__dmul_rn(xa[i], q.om), __dmul_rn(q.th, xi));
+        xa[i] = na;
+        if (q.wt) {
+          stcg(q.Yn + (size_t)e * c.NXP + i, ns);
+          stcg(q.Yn + E * c.NXP + (size_t)e * c.NXP + i, nz);
+          stcg(P.xavg + (size_t)(e + 1) * c.NXP + i, na);
+        }
+        if (q.last) stcg(P.X + (size_t)(e + 1) * c.NXP + i, xi);
       }
-      const double na = __dadd_rn(__dmul_rn(xa[k], om), __dmul_rn(th, xi));
-      xa[k] = na;
-      if (wt) {
-        stcg(Yn + (size_t)e * c.NXP + k, ns);
-        stcg(Yn + E * c.NXP + (size_t)e * c.NXP + k, nz);
-        stcg(P.xavg + (size_t)(e + 1) * c.NXP + k, na);
-      }
-      if (last) stcg(P.X + (size_t)(e + 1) * c.NXP + k, xi);
     }
   }
-  TSMPC_MARK(P, 15, te_);
+  *rmax_io = rmax;
+}
+
+// psi block of rows described by rdesc (component-major), u read from the rows
+__device__ __noinline__ void epi_psi_rows(int nu_it, double cf, double th, int nrows, int ysm, bool wt, int ncur,
+                                          double* rmax_io) {
+  const SParams& S = g_sp;
+  const Ctx c = ctx_of();
+  const Params& P = S.P;
+  const EpiConst q = epi_const(P, nu_it, cf, th, wt, ncur);
+  const int k = threadIdx.x & (kKW - 1), g = threadIdx.x / kKW;
+  double rmax = *rmax_io;
+  if (k < c.nu) {
+#pragma unroll 1
+    for (int r = g; r < nrows; r += kGroups) {
+      const int* d = c.rdesc() + 5 * r;
+      epi_psi_elem(c, P, q, d, ysm, k, s_dyn[d[3] + k], rmax);
+    }
+  }
   *rmax_io = rmax;
 }
 
@@ -544,6 +557,14 @@ __device__ __noinline__ void fwd_tile(int ti, int nu_it, double cf, double th, i
     if (ti > 0) load_rows(c.mt.rows + 4 * row0, 4, nrows, c.slot, 3, cur, ysm);
     cp_commit();
   }
+  if (tid < nrows) {  // row descriptors of the epilogue
+    int* d = c.rdesc() + 5 * tid;
+    d[0] = c.mt.edge(row0 + tid);
+    d[1] = c.mt.stage(row0 + tid);
+    d[2] = (int)(RA + tid * LA - s_dyn);
+    d[3] = (int)(RB + tid * c.NUP - s_dyn);
+    d[4] = (int)(slot_row(c, srow0 + tid) - s_dyn);
+  }
   // prefetch the static biases: uhat (u = uhat + du) and e (x recursion)
   double upre[kRowsPT], epre[kRowsPT];
 #pragma unroll
@@ -600,7 +621,10 @@ __device__ __noinline__ void fwd_tile(int ti, int nu_it, double cf, double th, i
   }
   __syncthreads();
   TSMPC_MARK(P, 6, tm_);
-  // (4) u = uhat + du (B) ; x scan, head -> tail: x = a .* x_anc + (bv + e) (A) ; row descriptors
+  // (4) u = uhat + du (B) and the psi block of the epilogue (elementwise, u in a
+  // register) ; x scan, head -> tail: x = a .* x_anc + (bv + e) (A)
+  if (!resident) cp_wait<0>();  // the slot rows of a streamed tile
+  __syncthreads();
   if (k < nu) {
 #pragma unroll
     for (int m = 0; m < kRowsPT; ++m) {
@@ -608,6 +632,8 @@ __device__ __noinline__ void fwd_tile(int ti, int nu_it, double cf, double th, i
       if (r < nrows) RB[r * c.NUP + k] = __dadd_rn(RB[r * c.NUP + k], upre[m]);
     }
   }
+  // the thread reads back only its own u entries: no barrier needed
+  epi_psi_rows(nu_it, cf, th, nrows, ysm, !resident || nu_it == P.iters - 1, cur ^ 1, rmax);
   {
     const double* adiag = c.adiag();
     const double* pr = c.proot();
@@ -626,19 +652,10 @@ __device__ __noinline__ void fwd_tile(int ti, int nu_it, double cf, double th, i
       }
     }
   }
-  if (tid < nrows) {
-    int* d = c.rdesc() + 5 * tid;
-    d[0] = c.mt.edge(row0 + tid);
-    d[1] = c.mt.stage(row0 + tid);
-    d[2] = (int)(RA + tid * LA - s_dyn);
-    d[3] = (int)(RB + tid * c.NUP - s_dyn);
-    d[4] = (int)(slot_row(c, srow0 + tid) - s_dyn);
-  }
-  if (!resident) cp_wait<0>();
   __syncthreads();
   TSMPC_MARK(P, 7, tm_);
-  // (5) epilogue
-  epilogue(nu_it, cf, th, nrows, ysm, !resident || nu_it == P.iters - 1, cur ^ 1, rmax);
+  // (5) epilogue, state blocks (warp per row)
+  epi_state(nu_it, cf, th, nrows, ysm, !resident || nu_it == P.iters - 1, cur ^ 1, rmax);
   __syncthreads();
   TSMPC_MARK(P, 8, tm_);
 }
@@ -925,7 +942,8 @@ __device__ __noinline__ void trunk_own_rows(int nu_it, double cf, double th, int
     cp_commit();
     cp_wait<0>();
     __syncthreads();
-    epilogue(nu_it, cf, th, nb, 0, true, cur ^ 1, rmax);
+    epi_psi_rows(nu_it, cf, th, nb, 0, true, cur ^ 1, rmax);
+    epi_state(nu_it, cf, th, nb, 0, true, cur ^ 1, rmax);
     __syncthreads();
   }
 }
