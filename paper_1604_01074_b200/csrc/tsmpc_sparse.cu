@@ -109,6 +109,7 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 constexpr int kKW = 128;                    // component lanes per row group (n_x, n_u <= 128)
 constexpr int kGroups = kThreadsS / kKW;    // 4 row groups
 constexpr int kRowsPT = kTileS / kGroups;   // rows per thread in a full tile
+constexpr int kCh = 8;                      // rows per register chunk of the chain scans
 
 struct Ctx {
   const SParams* S;
@@ -463,10 +464,19 @@ __device__ __noinline__ void bwd_tile(int ti, double cf, int ysm, int srow0, boo
     const double a = adiag[i];
     double* col = RA + lo * LA + i;
     double x = 0.0;
+    // chunks of kCh rows: the loads of a chunk are in flight together, then the
+    // dependent recursion runs from registers
 #pragma unroll 1
-    for (int j = n - 1; j >= 0; --j) {
-      x = __dadd_rn(col[j * LA], __dmul_rn(x, a));
-      col[j * LA] = x;
+    for (int j1 = n; j1 > 0; j1 -= kCh) {
+      double v[kCh];
+#pragma unroll
+      for (int u = 0; u < kCh; ++u) v[u] = j1 - 1 - u >= 0 ? col[(j1 - 1 - u) * LA] : 0.0;
+#pragma unroll
+      for (int u = 0; u < kCh; ++u)
+        if (j1 - 1 - u >= 0) {
+          x = __dadd_rn(v[u], __dmul_rn(x, a));
+          col[(j1 - 1 - u) * LA] = x;
+        }
     }
     if (sg[2] >= 0) stcg(P.XIQG + (size_t)c.mt.edge(row0 + lo) * c.NXP + i, x);
   }
@@ -502,24 +512,26 @@ __device__ __noinline__ void bwd_tile(int ti, double cf, int ysm, int srow0, boo
     const int lo = sg[0], n = sg[1] - lo;
     double* col = RA + lo * LA + kk;
     double gv = 0.0;
-    if (tmode == 0) {
+    double* tcol = tmode == 0 ? col : slot_row(c, srow0 + lo) + 2 * c.YW + c.NXP + c.NUP + kk;
+    const int tld = tmode == 0 ? LA : c.SL;
 #pragma unroll 1
-      for (int j = n - 1; j >= 0; --j) {
-        gv = __dadd_rn(col[j * LA], gv);
-        col[j * LA] = __dmul_rn(gv, c.mt.inv2p(row0 + lo + j));
+    for (int j1 = n; j1 > 0; j1 -= kCh) {
+      double v[kCh], ip[kCh];
+#pragma unroll
+      for (int u = 0; u < kCh; ++u) {
+        const int j = j1 - 1 - u;
+        v[u] = j >= 0 ? col[j * LA] : 0.0;
+        ip[u] = j >= 0 ? c.mt.inv2p(row0 + lo + j) : 0.0;
       }
-    } else if (tmode == 1) {
-      double* tcol = slot_row(c, srow0 + lo) + 2 * c.YW + c.NXP + c.NUP + kk;
-#pragma unroll 1
-      for (int j = n - 1; j >= 0; --j) {
-        gv = __dadd_rn(col[j * LA], gv);
-        tcol[j * c.SL] = __dmul_rn(gv, c.mt.inv2p(row0 + lo + j));
-      }
-    } else {
-#pragma unroll 1
-      for (int j = n - 1; j >= 0; --j) {
-        gv = __dadd_rn(col[j * LA], gv);
-        stcg(S.TG + (size_t)c.mt.edge(row0 + lo + j) * c.NVP + kk, __dmul_rn(gv, c.mt.inv2p(row0 + lo + j)));
+#pragma unroll
+      for (int u = 0; u < kCh; ++u) {
+        const int j = j1 - 1 - u;
+        if (j >= 0) {
+          gv = __dadd_rn(v[u], gv);
+          const double t = __dmul_rn(gv, ip[u]);
+          if (tmode == 2) stcg(S.TG + (size_t)c.mt.edge(row0 + lo + j) * c.NVP + kk, t);
+          else tcol[j * tld] = t;
+        }
       }
     }
     if (sg[2] >= 0) stcg(P.GG + (size_t)c.mt.edge(row0 + lo) * c.NVP + kk, gv);
@@ -592,9 +604,16 @@ __device__ __noinline__ void fwd_tile(int ti, int nu_it, double cf, double th, i
     const int tld = tmode == 1 ? c.SL : LA;
     double Sv = pn >= 0 ? c.need[(size_t)pn * S.need_ld + kk] : 0.0;
 #pragma unroll 1
-    for (int j = 0; j < n; ++j) {
-      Sv = __dadd_rn(tcol[j * tld], Sv);
-      scol[j * LA] = Sv;
+    for (int j0 = 0; j0 < n; j0 += kCh) {
+      double v[kCh];
+#pragma unroll
+      for (int u = 0; u < kCh; ++u) v[u] = j0 + u < n ? tcol[(j0 + u) * tld] : 0.0;
+#pragma unroll
+      for (int u = 0; u < kCh; ++u)
+        if (j0 + u < n) {
+          Sv = __dadd_rn(v[u], Sv);
+          scol[(j0 + u) * LA] = Sv;
+        }
     }
   }
   __syncthreads();
@@ -646,9 +665,16 @@ __device__ __noinline__ void fwd_tile(int ti, int nu_it, double cf, double th, i
       double x = pn >= 0 ? c.need[(size_t)pn * S.need_ld + c.NVP + i] : pr[i];
       const double a = adiag[i];
 #pragma unroll 1
-      for (int j = 0; j < n; ++j) {
-        x = __dadd_rn(__dmul_rn(x, a), col[j * LA]);
-        col[j * LA] = x;
+      for (int j0 = 0; j0 < n; j0 += kCh) {
+        double v[kCh];
+#pragma unroll
+        for (int u = 0; u < kCh; ++u) v[u] = j0 + u < n ? col[(j0 + u) * LA] : 0.0;
+#pragma unroll
+        for (int u = 0; u < kCh; ++u)
+          if (j0 + u < n) {
+            x = __dadd_rn(__dmul_rn(x, a), v[u]);
+            col[(j0 + u) * LA] = x;
+          }
       }
     }
   }
