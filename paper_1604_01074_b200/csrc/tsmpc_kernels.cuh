@@ -131,6 +131,7 @@ struct SParams {
   int sweep_in_a;               // trunk sweep buffers start in region A (no CTA keeps t there)
   int sched_smem;               // trunk schedule staged in shared memory during the sweep
   int psi_smem;                 // psi_stage table staged in shared memory (else read via L1)
+  int sched_resident, O_SCHED;  // trunk schedule resident in shared memory for the launch
   int n_work;                   // doubles in the work region
   int need_ld;                  // NVP + NXP + NUP  ([S | x | u] of one needed trunk edge)
   int need_max;

@@ -703,8 +703,10 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
   const int T = __ldg(g), nlev = __ldg(g + 1);
   double* Zs = S.sweep_in_a ? c.A() : c.B();
   double* Xs = Zs + (size_t)T * nc;
-  const int* sch = g;  // schedule: staged in shared memory when it fits, else read through L1
-  if (S.sched_smem) {
+  const int* sch = g;  // schedule: resident / staged in shared memory when it fits, else via L1
+  if (S.sched_resident) {
+    sch = reinterpret_cast<const int*>(s_dyn + S.O_SCHED);
+  } else if (S.sched_smem) {
     int* ss = reinterpret_cast<int*>(Xs + (size_t)T * nc);
 #pragma unroll 1
     for (int i = threadIdx.x; i < S.n_tsched; i += kThreadsS) ss[i] = __ldg(g + i);
@@ -732,7 +734,14 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
         if (nh > 0) z = __dadd_rn(z, ldcg(S.HS + (size_t)tp * S.HS_LD + q));
       } else {
 #pragma unroll 1
-        for (int m = 0; m < nh; ++m) z = __dadd_rn(z, ldcg(P.GG + (size_t)hch[h0 + m] * c.NVP + q));
+        for (int m0 = 0; m0 < nh; m0 += kCh) {  // loads of a chunk in flight together
+          double v[kCh];
+#pragma unroll
+          for (int u = 0; u < kCh; ++u) v[u] = m0 + u < nh ? ldcg(P.GG + (size_t)hch[h0 + m0 + u] * c.NVP + q) : 0.0;
+#pragma unroll
+          for (int u = 0; u < kCh; ++u)
+            if (m0 + u < nh) z = __dadd_rn(z, v[u]);
+        }
       }
     } else if (q < c.nv + c.nx) {
       const int i = q - c.nv;
@@ -746,7 +755,14 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
         if (nh > 0) h = ldcg(S.HS + (size_t)tp * S.HS_LD + c.NVP + i);
       } else {
 #pragma unroll 1
-        for (int m = 0; m < nh; ++m) h = __dadd_rn(h, ldcg(P.XIQG + (size_t)hch[h0 + m] * c.NXP + i));
+        for (int m0 = 0; m0 < nh; m0 += kCh) {
+          double v[kCh];
+#pragma unroll
+          for (int u = 0; u < kCh; ++u) v[u] = m0 + u < nh ? ldcg(P.XIQG + (size_t)hch[h0 + m0 + u] * c.NXP + i) : 0.0;
+#pragma unroll
+          for (int u = 0; u < kCh; ++u)
+            if (m0 + u < nh) h = __dadd_rn(h, v[u]);
+        }
       }
       x = __dadd_rn(s, __dmul_rn(h, adiag[i]));
     } else {
@@ -856,6 +872,34 @@ __device__ __noinline__ void trunk_needs() {
   // the u column of each need row holds Yz, then du, then u (no other scratch)
   double* const ND = c.need;
   const int UO = c.NVP + c.NXP;
+  // KY, uhat and e rows of the needs, staged in region B in one round of loads
+  // (else read through L2 where used)
+  const int SLD = P.KY_LD + c.NUP + c.NXP;
+  const bool staged = nn * SLD <= kTileS * c.NUP;
+  const double* KYs = c.B();
+  if (staged) {
+    const int hk = P.KY_LD / 2, hu = c.NUP / 2, hx = c.NXP / 2, per = hk + hu + hx;
+#pragma unroll 1
+    for (int idx = threadIdx.x; idx < nn * per; idx += kThreadsS) {
+      const int n = idx / per, q = idx - n * per;
+      double* dst = c.B() + (size_t)n * SLD;
+      if (q < hk) cp16(dst + 2 * q, P.KY + (size_t)nd[4 * n] * P.KY_LD + 2 * q);
+      else if (q < hk + hu) cp16(dst + P.KY_LD + 2 * (q - hk), P.uhat + (size_t)nd[4 * n + 2] * c.NUP + 2 * (q - hk));
+      else cp16(dst + P.KY_LD + c.NUP + 2 * (q - hk - hu), P.evec + (size_t)nd[4 * n + 2] * c.NXP + 2 * (q - hk - hu));
+    }
+    cp_commit();
+    cp_wait<0>();
+    __syncthreads();
+  }
+  auto ky = [&](int n, int col) -> double {
+    return staged ? KYs[(size_t)n * SLD + col] : ldcg(P.KY + (size_t)nd[4 * n] * P.KY_LD + col);
+  };
+  auto uhat_n = [&](int n, int j) -> double {
+    return staged ? KYs[(size_t)n * SLD + P.KY_LD + j] : ldcg(P.uhat + (size_t)nd[4 * n + 2] * c.NUP + j);
+  };
+  auto evec_n = [&](int n, int i) -> double {
+    return staged ? KYs[(size_t)n * SLD + P.KY_LD + c.NUP + i] : ldcg(P.evec + (size_t)nd[4 * n + 2] * c.NXP + i);
+  };
   // (1) Yz = Ypsi + B' Yx
   {
     const int* cp = c.spi + S.Bc_ptr;
@@ -864,10 +908,9 @@ __device__ __noinline__ void trunk_needs() {
 #pragma unroll 1
     for (int idx = threadIdx.x; idx < nn * nu; idx += kThreadsS) {
       const int n = idx / nu, j = idx - n * nu;
-      const double* ky = P.KY + (size_t)nd[4 * n] * P.KY_LD;
-      double z = ldcg(ky + c.NVP + c.NXP + j);
+      double z = ky(n, c.NVP + c.NXP + j);
 #pragma unroll 1
-      for (int q = cp[j]; q < cp[j + 1]; ++q) z = fma(cv[q], ldcg(ky + c.NVP + ci[q]), z);
+      for (int q = cp[j]; q < cp[j + 1]; ++q) z = fma(cv[q], ky(n, c.NVP + ci[q]), z);
       ND[(size_t)n * LD + UO + j] = z;
     }
   }
@@ -883,7 +926,7 @@ __device__ __noinline__ void trunk_needs() {
       double h = 0.0;
 #pragma unroll 1
       for (int q = cp[k]; q < cp[k + 1]; ++q) h = fma(cv[q], ND[(size_t)n * LD + UO + ci[q]], h);
-      ND[(size_t)n * LD + k] = __dadd_rn(ldcg(P.KY + (size_t)nd[4 * n] * P.KY_LD + k), h);
+      ND[(size_t)n * LD + k] = __dadd_rn(ky(n, k), h);
     }
   }
   __syncthreads();
@@ -913,14 +956,14 @@ __device__ __noinline__ void trunk_needs() {
       double b = 0.0;
 #pragma unroll 1
       for (int q = rp[i]; q < rp[i + 1]; ++q) b = fma(rv[q], ND[(size_t)n * LD + UO + ri[q]], b);
-      ND[(size_t)n * LD + c.NVP + i] = __dadd_rn(b, ldcg(P.evec + (size_t)nd[4 * n + 2] * c.NXP + i));
+      ND[(size_t)n * LD + c.NVP + i] = __dadd_rn(b, evec_n(n, i));
     }
     __syncthreads();
 #pragma unroll 1
     for (int idx = threadIdx.x; idx < nn * nu; idx += kThreadsS) {
       const int n = idx / nu, j = idx - n * nu;
       double* u = ND + (size_t)n * LD + UO + j;
-      *u = __dadd_rn(*u, ldcg(P.uhat + (size_t)nd[4 * n + 2] * c.NUP + j));
+      *u = __dadd_rn(*u, uhat_n(n, j));
     }
     __syncthreads();
     const double* adiag = c.adiag();
@@ -1008,6 +1051,11 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
       double* psi = s_dyn + S.O_PSI;
 #pragma unroll 1
       for (int i = threadIdx.x; i < N * NUP; i += kThreadsS) psi[i] = P.psi_stage[i];
+    }
+    if (S.sched_resident) {
+      int* ss = reinterpret_cast<int*>(s_dyn + S.O_SCHED);
+#pragma unroll 1
+      for (int i = threadIdx.x; i < S.n_tsched; i += kThreadsS) ss[i] = __ldg(S.tsched + i);
     }
     int* ints = reinterpret_cast<int*>(s_dyn + S.O_INT);
     const int m0 = __ldg(S.meta_ptr + blockIdx.x), m1 = __ldg(S.meta_ptr + blockIdx.x + 1);

@@ -457,6 +457,14 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
   }
   S.slot_rows = (int)want_rows;
   off += want_rows * slot_ld;
+  // the trunk schedule stays in shared memory for the launch when it fits
+  {
+    const long long sched_d = ((long long)out.tsched.size() + 1) / 2 + 1;
+    const long long limit_d2 = (long long)(smem_limit / sizeof(double));
+    S.sched_resident = (T > 0 && off + ints_d + sched_d <= limit_d2) ? 1 : 0;
+    S.O_SCHED = (int)off;
+    if (S.sched_resident) off += sched_d;
+  }
   S.O_INT = (int)off;
   off += ints_d;
   S.meta_max = meta_max;
