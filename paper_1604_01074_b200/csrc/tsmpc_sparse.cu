@@ -341,11 +341,13 @@ __device__ __noinline__ void epi_state(int nu_it, double cf, double th, int nrow
       ss += __shfl_xor_sync(0xffffffffu, ss, off);
       sz += __shfl_xor_sync(0xffffffffu, sz, off);
     }
-    const double dist_s = sqrt(ss), dist_z = sqrt(sz);
+    // factor min(1, weight / distance) (engine.py:146-155), as weight * rsqrt(distance^2):
+    // the full IEEE sqrt + division sequences cost more than the rest of the row,
+    // and the factor differs from weight / sqrt(.) by about one ulp
     const double wgt_s = __dmul_rn(__dmul_rn(q.lam_p, P.Wx), c.scl[2 * N + st]);
     const double wgt_z = __dmul_rn(__dmul_rn(q.lam_p, P.gamma_d), c.scl[3 * N + st]);
-    const double fs = dist_s > wgt_s ? __ddiv_rn(wgt_s, dist_s) : 1.0;
-    const double fz = dist_z > wgt_z ? __ddiv_rn(wgt_z, dist_z) : 1.0;
+    const double fs = ss > __dmul_rn(wgt_s, wgt_s) ? __dmul_rn(wgt_s, rsqrt(ss)) : 1.0;
+    const double fz = sz > __dmul_rn(wgt_z, wgt_z) ? __dmul_rn(wgt_z, rsqrt(sz)) : 1.0;
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
       const int i = lane + 32 * m;
