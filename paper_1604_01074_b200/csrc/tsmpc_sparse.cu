@@ -109,6 +109,7 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 constexpr int kKW = 128;                    // component lanes per row group (n_x, n_u <= 128)
 constexpr int kGroups = kThreadsS / kKW;    // 4 row groups
 constexpr int kRowsPT = kTileS / kGroups;   // rows per thread in a full tile
+constexpr int kSeqTrunk = 0;                // trunks up to this size are swept by one thread per component (slower on B200: off)
 constexpr int kCh = 8;                      // rows per register chunk of the chain scans
 
 struct Ctx {
@@ -705,11 +706,12 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
   const int T = __ldg(g), nlev = __ldg(g + 1);
   double* Zs = S.sweep_in_a ? c.A() : c.B();
   double* Xs = Zs + (size_t)T * nc;
+  double* Ip = Xs + (size_t)T * nc;  // 1 / (2 p) of each trunk edge
   const int* sch = g;  // schedule: resident / staged in shared memory when it fits, else via L1
   if (S.sched_resident) {
     sch = reinterpret_cast<const int*>(s_dyn + S.O_SCHED);
   } else if (S.sched_smem) {
-    int* ss = reinterpret_cast<int*>(Xs + (size_t)T * nc);
+    int* ss = reinterpret_cast<int*>(Ip + T);
 #pragma unroll 1
     for (int i = threadIdx.x; i < S.n_tsched; i += kThreadsS) ss[i] = __ldg(g + i);
     sch = ss;
@@ -724,6 +726,8 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
   const double* Yp = P.ybuf[cur ^ 1];
   const double* adiag = c.adiag();
   // (1) own terms + chain-head children (one parallel round of loads)
+#pragma unroll 1
+  for (int tp = threadIdx.x; tp < T; tp += kThreadsS) Ip[tp] = __ldg(P.inv2p + pos[8 * tp]);
 #pragma unroll 1
   for (int idx = threadIdx.x; idx < T * nc; idx += kThreadsS) {
     const int tp = idx / nc, k = idx - tp * nc, q = c_lo + k;
@@ -777,6 +781,43 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
     Xs[idx] = x;
   }
   __syncthreads();
+  if (T <= kSeqTrunk) {
+    // small trunk: one thread per component walks the levels (no level barriers)
+    if (threadIdx.x < nc) {
+      const int k = threadIdx.x, q = c_lo + k;
+      const bool xq = q >= c.nv && q < c.nv + c.nx;
+      const double aq = xq ? adiag[q - c.nv] : 0.0;
+#pragma unroll 1
+      for (int tp = T - 1; tp >= 0; --tp) {  // children have larger positions
+        const int* ps = pos + 8 * tp;
+        const int c0 = ps[3], n = ps[4];
+        double zs = 0.0, xs = 0.0;
+#pragma unroll 1
+        for (int m = 0; m < n; ++m) {
+          const int cp = tch[c0 + m];
+          zs = __dadd_rn(zs, Zs[cp * nc + k]);
+          xs = __dadd_rn(xs, Xs[cp * nc + k]);
+        }
+        const int idx = tp * nc + k;
+        if (xq) {
+          const double xiq = __dadd_rn(Xs[idx], __dmul_rn(xs, aq));
+          Xs[idx] = xiq;
+          Zs[idx] = __dadd_rn(xiq, zs);
+        } else {
+          Zs[idx] = __dadd_rn(Zs[idx], zs);
+        }
+      }
+#pragma unroll 1
+      for (int tp = 0; tp < T; ++tp) {  // parents have smaller positions
+        const int pp = pos[8 * tp + 2];
+        const int idx = tp * nc + k;
+        double v = __dmul_rn(Zs[idx], Ip[tp]);
+        if (pp >= 0) v = __dadd_rn(v, Zs[pp * nc + k]);
+        Zs[idx] = v;
+      }
+    }
+    __syncthreads();
+  } else {
   // (2) bottom-up over edge-stage levels: add trunk children
 #pragma unroll 1
   for (int l = nlev - 1; l >= 0; --l) {
@@ -810,11 +851,12 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
       const int tp = idx / nc, k = idx - tp * nc;
       const int* ps = pos + 8 * tp;
       const int pp = ps[2];
-      double v = __dmul_rn(Zs[idx], __ldg(P.inv2p + ps[0]));
+      double v = __dmul_rn(Zs[idx], Ip[tp]);
       if (pp >= 0) v = __dadd_rn(v, Zs[pp * nc + k]);
       Zs[idx] = v;
     }
     __syncthreads();
+  }
   }
   // (4) KY columns of this slice
 #pragma unroll 1
@@ -961,26 +1003,54 @@ __device__ __noinline__ void trunk_needs() {
       ND[(size_t)n * LD + c.NVP + i] = __dadd_rn(b, evec_n(n, i));
     }
     __syncthreads();
+    // u = uhat + du (independent of the x pass below: no barrier in between)
 #pragma unroll 1
     for (int idx = threadIdx.x; idx < nn * nu; idx += kThreadsS) {
       const int n = idx / nu, j = idx - n * nu;
       double* u = ND + (size_t)n * LD + UO + j;
       *u = __dadd_rn(*u, uhat_n(n, j));
     }
-    __syncthreads();
+    if (!staged) __syncthreads();
+    // x of each need: a .* x_parent + (bv + e), down its root path
     const double* adiag = c.adiag();
+    if (staged) {
+      // one pass: each (need, component) walks its path upwards, weighting the
+      // ancestors' (bv + e) by powers of a; the result goes to the staged KY
+      // columns (no longer read) and is copied back after a barrier
+      double* xo = c.B();
 #pragma unroll 1
-    for (int l = 0; l < c.mt.nlev; ++l) {
-      const int n0 = c.mt.lev[l], n1 = c.mt.lev[l + 1];
-#pragma unroll 1
-      for (int idx = n0 * nx + threadIdx.x; idx < n1 * nx; idx += kThreadsS) {
+      for (int idx = threadIdx.x; idx < nn * nx; idx += kThreadsS) {
         const int n = idx / nx, i = idx - n * nx;
-        const int pn = nd[4 * n + 1];
-        const double xp = pn >= 0 ? c.need[(size_t)pn * LD + c.NVP + i] : c.proot()[i];
-        double* xv = c.need + (size_t)n * LD + c.NVP + i;
-        *xv = __dadd_rn(__dmul_rn(xp, adiag[i]), *xv);
+        const double a = adiag[i];
+        double xv = ND[(size_t)n * LD + c.NVP + i], m = a;
+#pragma unroll 1
+        for (int anc = nd[4 * n + 1]; anc >= 0; anc = nd[4 * anc + 1]) {
+          xv = __dadd_rn(xv, __dmul_rn(m, ND[(size_t)anc * LD + c.NVP + i]));
+          m = __dmul_rn(m, a);
+        }
+        xo[(size_t)n * SLD + i] = __dadd_rn(xv, __dmul_rn(m, c.proot()[i]));
       }
       __syncthreads();
+#pragma unroll 1
+      for (int idx = threadIdx.x; idx < nn * nx; idx += kThreadsS) {
+        const int n = idx / nx, i = idx - n * nx;
+        ND[(size_t)n * LD + c.NVP + i] = xo[(size_t)n * SLD + i];
+      }
+      __syncthreads();
+    } else {
+#pragma unroll 1
+      for (int l = 0; l < c.mt.nlev; ++l) {
+        const int n0 = c.mt.lev[l], n1 = c.mt.lev[l + 1];
+#pragma unroll 1
+        for (int idx = n0 * nx + threadIdx.x; idx < n1 * nx; idx += kThreadsS) {
+          const int n = idx / nx, i = idx - n * nx;
+          const int pn = nd[4 * n + 1];
+          const double xp = pn >= 0 ? ND[(size_t)pn * LD + c.NVP + i] : c.proot()[i];
+          double* xv = ND + (size_t)n * LD + c.NVP + i;
+          *xv = __dadd_rn(__dmul_rn(xp, adiag[i]), *xv);
+        }
+        __syncthreads();
+      }
     }
   }
 }

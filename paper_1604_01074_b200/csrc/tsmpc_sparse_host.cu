@@ -446,7 +446,7 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
     const long long nc_max = (ncomp + C - 1) / C;
     const long long regB = (long long)kTileS * NUP;
     const long long cap = any_t0 ? regB : (long long)S.n_work;
-    const long long zx = 2LL * T * nc_max;
+    const long long zx = 2LL * T * nc_max + T;  // Zs, Xs, 1/(2p) per trunk edge
     const long long sched = ((long long)out.tsched.size() + 1) / 2 + 2;
     S.sweep_in_a = any_t0 ? 0 : 1;
     S.sched_smem = zx + sched <= cap ? 1 : 0;
