@@ -205,35 +205,38 @@ __device__ __forceinline__ double* slot_row(const Ctx& c, int srow) { return c.s
 // 2 = ergodic rows.  ysm = smem dual index that receives HBM slot `cur`.
 __device__ __noinline__ void load_rows(const int* edges, int estride, int nrows, double* dst,
                                        int parts, int cur, int ysm) {
+  // one (row, contiguous part) pair per warp pass; lanes stream 16-byte chunks
   const SParams& S = g_sp;
-  const Ctx c = ctx_of();
   const Params& P = S.P;
-  const int hx = c.NXP / 2, hu = c.NUP / 2;
-  const int per_y = 2 * hx + hu;               // 16-byte chunks of one dual row
-  const int nch = ((parts & 1) ? 2 * per_y : 0) + ((parts & 2) ? hx + hu : 0);
-  const size_t E = (size_t)c.E;
+  const int NXP = P.NXP, NUP = P.NUP, YW = S.YW, SL = S.slot_ld;
+  const size_t E = (size_t)P.n_edges;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int p0 = (parts & 1) ? 0 : 6, p1 = (parts & 2) ? 8 : 6;
+  const int np = p1 - p0;
 #pragma unroll 1
-  for (int idx = threadIdx.x; idx < nrows * nch; idx += kThreadsS) {
-    const int r = idx / nch;
-    int k = idx - r * nch;
+  for (int w = warp; w < nrows * np; w += kWarpsS) {
+    const int r = w / np, part = p0 + (w - r * np);
     const int e = edges[r * estride];
-    double* srow = dst + (size_t)r * c.SL;
-    if (parts & 1) {
-      if (k < 2 * per_y) {
-        const int which = k < per_y ? 0 : 1;     // 0: HBM slot cur, 1: cur ^ 1
-        const int kk = k - which * per_y;
-        const double* Y = P.ybuf[cur ^ which];
-        double* d = srow + (size_t)(ysm ^ which) * c.YW;
-        if (kk < hx) cp16(d + 2 * kk, Y + (size_t)e * c.NXP + 2 * kk);
-        else if (kk < 2 * hx) cp16(d + c.NXP + 2 * (kk - hx), Y + E * c.NXP + (size_t)e * c.NXP + 2 * (kk - hx));
-        else cp16(d + 2 * c.NXP + 2 * (kk - 2 * hx), Y + 2 * E * c.NXP + (size_t)e * c.NUP + 2 * (kk - 2 * hx));
-        continue;
-      }
-      k -= 2 * per_y;
+    double* srow = dst + (size_t)r * SL;
+    const double* src;
+    double* d;
+    int len;
+    if (part < 6) {  // dual rows: parts 0-2 from HBM slot cur, 3-5 from cur ^ 1
+      const int which = part / 3, blk = part - 3 * which;
+      const double* Y = P.ybuf[cur ^ which];
+      d = srow + (size_t)(ysm ^ which) * YW + blk * NXP;
+      src = blk < 2 ? Y + (size_t)blk * E * NXP + (size_t)e * NXP : Y + 2 * E * NXP + (size_t)e * NUP;
+      len = blk < 2 ? NXP : NUP;
+    } else if (part == 6) {
+      d = srow + 2 * YW;
+      src = P.xavg + (size_t)(e + 1) * NXP;
+      len = NXP;
+    } else {
+      d = srow + 2 * YW + NXP;
+      src = P.uavg + (size_t)e * NUP;
+      len = NUP;
     }
-    double* xa = srow + 2 * c.YW;
-    if (k < hx) cp16(xa + 2 * k, P.xavg + (size_t)(e + 1) * c.NXP + 2 * k);
-    else cp16(xa + c.NXP + 2 * (k - hx), P.uavg + (size_t)e * c.NUP + 2 * (k - hx));
+    for (int q = lane; q < len / 2; q += 32) cp16(d + 2 * q, src + 2 * q);
   }
 }
 
@@ -562,11 +565,13 @@ __device__ __noinline__ void fwd_tile(int ti, int nu_it, double cf, double th, i
   (void)tm_;
   if (!resident) {
     // t rows of this tile -> region A; then (after the previous epilogue) the slot
-    const int hv = c.NVP / 2;
+    {
+      const int lane = tid & 31;
 #pragma unroll 1
-    for (int idx = tid; idx < nrows * hv; idx += kThreadsS) {
-      const int r = idx / hv, kk = idx - r * hv;
-      cp16(RA + r * LA + 2 * kk, S.TG + (size_t)c.mt.edge(row0 + r) * c.NVP + 2 * kk);
+      for (int r = tid >> 5; r < nrows; r += kWarpsS) {
+        const double* src = S.TG + (size_t)c.mt.edge(row0 + r) * c.NVP;
+        for (int q = lane; q < c.NVP / 2; q += 32) cp16(RA + r * LA + 2 * q, src + 2 * q);
+      }
     }
     cp_commit();
     if (ti > 0) load_rows(c.mt.rows + 4 * row0, 4, nrows, c.slot, 3, cur, ysm);
