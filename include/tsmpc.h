@@ -161,6 +161,14 @@ int tsmpc_solve(tsmpc_plan* plan, const double* p, int32_t iters, double lam,
                 const double* theta, const double* coef, int32_t flags,
                 tsmpc_result* out);
 
+/* Residual stopping test for later tsmpc_solve calls (extension; the reference
+ * loop is fixed-iteration): every check_every iterations the residual_inf of
+ * that iteration is reduced on the device and the solve stops as soon as it is
+ * <= tol (tol <= 0 disables).  result.iterations reports the iterations run and
+ * result.residual_inf the stopping residual.  Honoured by the structured-basis
+ * kernel of single-GPU plans; other plans run max_iters. */
+int tsmpc_set_stopping(tsmpc_plan* plan, double tol, int32_t check_every);
+
 /* factor.solve_step: z = argmin <z, H'w> + f(z) for an unscaled dual w. */
 int tsmpc_solve_step(tsmpc_plan* plan, const double* w_sig, const double* w_zeta,
                      const double* w_psi, const double* p, double* x_out, double* u_out);

@@ -73,6 +73,7 @@ SIGNATURES = {
     "tsmpc_plan_info": (ctypes.c_int, [ctypes.c_void_p, _ip, ctypes.c_int32]),
     "tsmpc_last_error": (ctypes.c_char_p, []),
     "tsmpc_plan_path": (ctypes.c_char_p, [ctypes.c_void_p]),
+    "tsmpc_set_stopping": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, ctypes.c_int32]),
     "tsmpc_set_cache_operators": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, _dp, _dp, _dp, _dp, _dp,
                                                  _dp]),
     "tsmpc_set_forecast": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, _dp, _dp]),

@@ -68,6 +68,12 @@ struct tsmpc_plan {
   unsigned long long* RESID = nullptr;
   int resid_cap = 0;
   unsigned long long* DYK = nullptr;
+  // residual stopping test (tsmpc_set_stopping; sparse kernel only)
+  double tol = 0.0;
+  int check_every = 25;
+  unsigned long long* RCHK = nullptr;
+  int rchk_cap = 0;
+  int* ITERS = nullptr;
   unsigned long long* TIMERS = nullptr;
   // compact scaling copies for tsmpc_prox
   double *sig_c = nullptr, *zeta_c = nullptr, *psi_c = nullptr;
@@ -1175,9 +1181,23 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
   CU(cudaMemsetAsync(pl->UAVG, 0, sizeof(double) * (size_t)E * NUP, pl->stream));
   if (set_root(pl, p)) return TSMPC_ERR_CUDA;
 
+  const bool stopping = pl->tol > 0.0 && pl->use_sparse && !pl->sharded;
+  if (stopping) {
+    const int nchk = iters / std::max(1, pl->check_every) + 1;
+    if (pl->rchk_cap < nchk) {
+      if (pl->alloc(&pl->RCHK, nchk)) return TSMPC_ERR_CUDA;
+      pl->rchk_cap = nchk;
+    }
+    if (!pl->ITERS && pl->alloc(&pl->ITERS, 1)) return TSMPC_ERR_CUDA;
+    CU(cudaMemsetAsync(pl->RCHK, 0, sizeof(unsigned long long) * nchk, pl->stream));
+  }
   Params P = pl->base;
   P.mode = kModeApg;
   P.iters = iters;
+  P.tol = stopping ? pl->tol : 0.0;
+  P.check_every = std::max(1, pl->check_every);
+  P.resid_chk = pl->RCHK;
+  P.iters_done = pl->ITERS;
   P.slot0 = 0;
   P.ybuf[0] = pl->Y0;
   P.ybuf[1] = pl->Y1;
@@ -1228,7 +1248,21 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
     return TSMPC_ERR_CUDA;
   }
   CU(cudaEventRecord(pl->ev1, pl->stream));
-  double* yfin = ((iters & 1) == 0) ? pl->Y0 : pl->Y1;
+  int done = iters;
+  if (stopping) {
+    CU(cudaMemcpyAsync(&done, pl->ITERS, sizeof(int), cudaMemcpyDeviceToHost, pl->stream));
+    CU(cudaStreamSynchronize(pl->stream));
+    if (done < 1 || done > iters) done = iters;
+    if (done < iters) {  // the stopping residual becomes the reported one
+      unsigned long long b;
+      CU(cudaMemcpyAsync(&b, pl->RCHK + done / pl->check_every - 1, sizeof(b), cudaMemcpyDeviceToHost,
+                         pl->stream));
+      CU(cudaStreamSynchronize(pl->stream));
+      CU(cudaMemcpyAsync(pl->RESID, &b, sizeof(b), cudaMemcpyHostToDevice, pl->stream));
+      CU(cudaStreamSynchronize(pl->stream));
+    }
+  }
+  double* yfin = ((done & 1) == 0) ? pl->Y0 : pl->Y1;
   pl->last_y = yfin;
   // keep the last iterate before the gap's solve step reuses X / U
   CU(cudaMemcpyAsync(pl->XL, pl->X, sizeof(double) * (size_t)pl->n_nodes * NXP, cudaMemcpyDeviceToDevice, pl->stream));
@@ -1240,7 +1274,7 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
   }
   CU(cudaEventRecord(pl->ev2, pl->stream));
   out->gap = gap;
-  out->iterations = iters;
+  out->iterations = done;
   std::vector<unsigned long long> rbits(nres);
   CU(cudaMemcpyAsync(rbits.data(), pl->RESID, sizeof(unsigned long long) * nres, cudaMemcpyDeviceToHost, pl->stream));
   if (pl->get_rows(out->u0, nu, pl->UAVG, NUP, 1)) return TSMPC_ERR_CUDA;
@@ -1266,6 +1300,14 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
   out->residual_inf = as_d(rbits[nres - 1]);
   if (record && out->resid_trace)
     for (int k = 0; k < iters; ++k) out->resid_trace[k] = as_d(rbits[k]);
+  return TSMPC_OK;
+}
+
+int tsmpc_set_stopping(tsmpc_plan* pl, double tol, int32_t check_every) {
+  if (!pl) return fail(TSMPC_ERR_ARGUMENT, "null argument");
+  if (check_every < 1) return fail(TSMPC_ERR_VALIDATION, "check_every must be >= 1");
+  pl->tol = tol > 0.0 ? tol : 0.0;
+  pl->check_every = check_every;
   return TSMPC_OK;
 }
 

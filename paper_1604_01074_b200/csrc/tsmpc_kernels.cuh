@@ -92,6 +92,13 @@ struct Params {
   double lam;
   const double *theta, *coef;
   unsigned long long* resid;    // iters (record_all) or 1 slot, bit pattern of a double >= 0
+  // optional residual stopping test (sparse kernel): every check_every iterations
+  // the residual is reduced into resid_chk[k] and the solve stops as soon as it is
+  // <= tol; iters_done receives the number of iterations run
+  double tol;
+  int check_every;
+  unsigned long long* resid_chk;
+  int* iters_done;
   unsigned long long* timers;   // phase cycle counters of CTA 0 (TSMPC_TIMERS builds only)
 };
 

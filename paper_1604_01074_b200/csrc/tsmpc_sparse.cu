@@ -252,6 +252,11 @@ __device__ __noinline__ void load_rows(const int* edges, int estride, int nrows,
 // is a warp reduction and the prox factor a warp-uniform scalar, so the block
 // needs no shared-memory exchange and no barrier.
 // ----------------------------------------------------------------------------
+// iteration whose residual feeds the stopping test (its state is written back)
+__device__ __forceinline__ bool is_check(const Params& P, int nu) {
+  return P.tol > 0.0 && (nu + 1) % P.check_every == 0 && nu + 1 < P.iters;
+}
+
 struct EpiConst {
   double cf, th, om, lam, ilam, lam_p;
   bool last, want, wt;
@@ -266,7 +271,7 @@ __device__ __forceinline__ EpiConst epi_const(const Params& P, int nu_it, double
   k.lam = P.lam;
   k.ilam = P.inv_lam;
   k.lam_p = 1.0 / P.lam;
-  k.last = nu_it == P.iters - 1;
+  k.last = nu_it == P.iters - 1 || is_check(P, nu_it);
   k.want = k.last || P.record_all;
   k.wt = wt;
   k.Yn = P.ybuf[ncur];
@@ -660,7 +665,7 @@ __device__ __noinline__ void fwd_tile(int ti, int nu_it, double cf, double th, i
     }
   }
   // the thread reads back only its own u entries: no barrier needed
-  epi_psi_rows(nu_it, cf, th, nrows, ysm, !resident || nu_it == P.iters - 1, cur ^ 1, rmax);
+  epi_psi_rows(nu_it, cf, th, nrows, ysm, !resident || nu_it == P.iters - 1 || is_check(P, nu_it), cur ^ 1, rmax);
   {
     const double* adiag = c.adiag();
     const double* pr = c.proot();
@@ -689,7 +694,7 @@ __device__ __noinline__ void fwd_tile(int ti, int nu_it, double cf, double th, i
   __syncthreads();
   TSMPC_MARK(P, 7, tm_);
   // (5) epilogue, state blocks (warp per row)
-  epi_state(nu_it, cf, th, nrows, ysm, !resident || nu_it == P.iters - 1, cur ^ 1, rmax);
+  epi_state(nu_it, cf, th, nrows, ysm, !resident || nu_it == P.iters - 1 || is_check(P, nu_it), cur ^ 1, rmax);
   __syncthreads();
   TSMPC_MARK(P, 8, tm_);
 }
@@ -1169,6 +1174,16 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
   for (int nu = S.nu0; nu < S.nu1; ++nu) {
     const int cur = (P.slot0 + nu) & 1;
     const int ysm = nu & 1;
+    if (P.tol > 0.0 && nu > S.nu0 && nu % P.check_every == 0) {
+      // stopping test on the residual of iteration nu - 1 (its state is in HBM)
+      grid.sync();
+      const double r = __longlong_as_double(
+          (long long)*((volatile unsigned long long*)(P.resid_chk + nu / P.check_every - 1)));
+      if (r <= P.tol) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) *P.iters_done = nu;
+        return;
+      }
+    }
     // momentum coefficients of the next iteration, loaded one iteration ahead
     const int nn = nu + 1 < P.iters ? nu + 1 : nu;
     const double cf_n = P.coef[nn], th_n = P.theta[nn];
@@ -1200,16 +1215,20 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
       }
       for (int t = 0; t < nt; ++t)
         fwd_tile(t, nu, cf, th, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur, &rmax);
-      if (nu == P.iters - 1 || P.record_all) {
+      if (nu == P.iters - 1 || P.record_all || is_check(P, nu)) {
         for (int off = 16; off > 0; off >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, off));
-        if ((threadIdx.x & 31) == 0 && rmax > 0.0)
-          atomicMax(P.resid + (P.record_all ? nu : 0), (unsigned long long)__double_as_longlong(rmax));
+        if ((threadIdx.x & 31) == 0 && rmax > 0.0) {
+          const unsigned long long b = (unsigned long long)__double_as_longlong(rmax);
+          if (nu == P.iters - 1 || P.record_all) atomicMax(P.resid + (P.record_all ? nu : 0), b);
+          if (is_check(P, nu)) atomicMax(P.resid_chk + nu / P.check_every, b);
+        }
         rmax = 0.0;
       }
     }
     cf = cf_n;
     th = th_n;
   }
+  if (P.tol > 0.0 && blockIdx.x == 0 && threadIdx.x == 0) *P.iters_done = S.nu1;
 }
 
 }  // namespace tsmpc

@@ -46,6 +46,10 @@ class SolverConfig:
     record_residuals: bool = False
     warm_start: bool = False
     device: int = 0
+    # extension (the reference loop is fixed-iteration): stop as soon as the
+    # residual_inf checked every `check_every` iterations on the device is <= tol
+    tol: float | None = None
+    check_every: int = 25
 
     def __post_init__(self):
         if self.max_iters < 1:
@@ -246,7 +250,8 @@ def solve(model, tree, forecast, p, q, config: SolverConfig | None = None, *,
     warm = warm_dual if (config.warm_start and warm_dual is not None) else None
     t0 = time.perf_counter()
     out = plan.solve(p, config.max_iters, float(lam), warm=warm, theta=theta, coef=coef,
-                     record_residuals=config.record_residuals)
+                     record_residuals=config.record_residuals, tol=config.tol,
+                     check_every=config.check_every)
     wall = time.perf_counter() - t0
     gap_trace = None
     if config.record_residuals:

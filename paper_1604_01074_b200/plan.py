@@ -174,7 +174,8 @@ class DevicePlan:
     def solve(self, p, iters: int, lam: float, warm: DualPoint | None = None,
               theta=None, coef=None, record_residuals: bool = False,
               skip_gap: bool = False, keep_device: bool = False,
-              warm_device: bool = False) -> dict:
+              warm_device: bool = False, tol: float | None = None,
+              check_every: int = 25) -> dict:
         """One APG solve (engine.py:485-601).  ``keep_device``: leave the iterates in
         HBM (only u0, residual and gap come back); ``warm_device``: start from the
         previous solve's final dual, still in HBM (closed-loop warm start)."""
@@ -201,6 +202,8 @@ class DevicePlan:
         th = _c(theta) if theta is not None else None
         cf = _c(coef) if coef is not None else None
         pv = _c(p)
+        nat.check(self._lib.tsmpc_set_stopping(self._h, float(tol) if tol else 0.0, int(check_every)),
+                  "tsmpc_set_stopping")
         rc = self._lib.tsmpc_solve(self._h, nat.dptr(pv), int(iters), float(lam),
                                    nat.dptr(ws), nat.dptr(wz), nat.dptr(wp),
                                    nat.dptr(th), nat.dptr(cf), flags, ctypes.byref(res))

@@ -132,3 +132,25 @@ def test_warm_start_matches_oracle():
     for f in ("u0", "u_avg", "x_avg"):
         assert rel_err(out[f], ref[f]) <= 1e-10, f
     assert abs(out["gap"] - ref["gap"]) <= 1e-8 * max(1.0, abs(ref["gap"]))
+
+
+@pytest.mark.parametrize("name", ["bcn63_SMPC1_N24", "tank3_tree_30_N8"])
+def test_residual_stopping_matches_fixed_iteration_solve(name):
+    """SolverConfig(tol=...): the device checks residual_inf every 25 iterations and
+    stops at the first check <= tol; the result equals a fixed solve of that length."""
+    c = load_case(name)
+    plan = _plan(c)
+    n = 200
+    th, cf = engine.theta_schedule(n)
+    tr = plan.solve(c.p, n, c.lam, theta=th, coef=cf, record_residuals=True, skip_gap=True)["resid_trace"]
+    tol = float(tr[124])
+    want = next(j + 1 for j in range(n) if (j + 1) % 25 == 0 and j + 1 < n and tr[j] <= tol)
+    a = plan.solve(c.p, n, c.lam, theta=th, coef=cf, tol=tol, check_every=25)
+    assert a["iterations"] == want
+    assert a["residual_inf"] == tr[want - 1]
+    b = plan.solve(c.p, want, c.lam, theta=th[:want], coef=cf[:want])
+    for k in ("x_avg", "u_avg", "x", "u", "dual_sig", "dual_psi", "u0"):
+        assert np.array_equal(a[k], b[k]), k
+    assert a["gap"] == b["gap"]
+    never = plan.solve(c.p, n, c.lam, theta=th, coef=cf, tol=1e-300)
+    assert never["iterations"] == n
