@@ -125,6 +125,18 @@ void tsmpc_plan_destroy(tsmpc_plan* plan);
 int tsmpc_nccl_unique_id(uint8_t* out128);
 tsmpc_plan* tsmpc_plan_create_shard(const tsmpc_problem* prob, int device, int32_t rank,
                                     int32_t world, const uint8_t* nccl_id128);
+/* Several shard plans of one tree on ONE device, created with nccl_id128 = NULL
+ * (local shard plans, ranks 0..n-1 of world n, plans[r] = rank r), solved in
+ * lockstep in one process: per iteration, phase 1 of every shard, an in-place
+ * device sum of their head-sum buffers (the exchange ncclAllReduce performs
+ * across GPUs), phase 2 of every shard; residuals are max-reduced the same way.
+ * outs[r] receives rank r's rows, as tsmpc_solve on an NCCL shard plan would.
+ * Exercises the multi-rank split on a single GPU (the kernels of different
+ * shards never wait on each other).  n <= 8; warm starts from host arrays are
+ * not taken (TSMPC_WARM_DEVICE is). */
+int tsmpc_solve_group(tsmpc_plan* const* plans, int32_t n, const double* p, int32_t iters,
+                      double lam, const double* theta, const double* coef, int32_t flags,
+                      tsmpc_result* outs);
 /* Edges whose rows a plan computes (which = 0: all for a single-GPU plan, owned
  * chains + trunk for a shard plan; which = 1: trunk edges).  Writes up to cap
  * edge ids to out (may be NULL) and returns the count (or a negative status). */

@@ -81,6 +81,8 @@ SIGNATURES = {
     "tsmpc_nccl_unique_id": (ctypes.c_int, [ctypes.POINTER(ctypes.c_uint8)]),
     "tsmpc_plan_create_shard": (ctypes.c_void_p, [ctypes.POINTER(Problem), ctypes.c_int, ctypes.c_int32,
                                                   ctypes.c_int32, ctypes.POINTER(ctypes.c_uint8)]),
+    "tsmpc_solve_group": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32, _dp, ctypes.c_int32,
+                                         ctypes.c_double, _dp, _dp, ctypes.c_int32, ctypes.POINTER(Result)]),
     "tsmpc_plan_edges": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, _ip, ctypes.c_int64]),
     "tsmpc_describe_shard": (ctypes.c_int, [ctypes.POINTER(Problem), ctypes.c_int32, ctypes.c_int64,
                                             ctypes.c_int32, ctypes.c_int32, _ip, ctypes.c_int32, _ip,

@@ -754,7 +754,7 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
     fail(TSMPC_ERR_VALIDATION, "subtree sharding needs the structured-basis kernel (%s)", pl->sp_why.c_str());
     return bail(0);
   }
-  if (shard) {
+  if (shard && nccl_id) {  // without an id: a local shard plan for tsmpc_solve_group
     std::string why;
     pl->nccl = nccl_api(why);
     if (!pl->nccl) { fail(TSMPC_ERR_NCCL, "%s", why.c_str()); return bail(0); }
@@ -824,7 +824,7 @@ int tsmpc_nccl_unique_id(uint8_t* out) {
 
 tsmpc_plan* tsmpc_plan_create_shard(const tsmpc_problem* pb, int device, int32_t rank, int32_t world,
                                     const uint8_t* nccl_id) {
-  if (!nccl_id || world < 1 || rank < 0 || rank >= world) {
+  if (world < 1 || rank < 0 || rank >= world) {
     fail(TSMPC_ERR_ARGUMENT, "invalid shard arguments (rank %d of %d)", rank, world);
     return nullptr;
   }
@@ -1123,10 +1123,21 @@ static int compute_gap(tsmpc_plan* pl, const double* yfinal, double* gap) {
   return TSMPC_OK;
 }
 
-int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, const double* warm_sig,
-                const double* warm_zeta, const double* warm_psi, const double* theta, const double* coef,
-                int32_t flags, tsmpc_result* out) {
-  if (!pl || !p || !out) return fail(TSMPC_ERR_ARGUMENT, "null argument");
+namespace {
+
+// One solve split in three so that tsmpc_solve_group can interleave several
+// shard plans: prepare (tables, dual start, root), the launches, finish (stopping
+// bookkeeping, gap, read-back).
+struct SolveState {
+  int iters = 0, nres = 1;
+  bool record = false, stopping = false;
+  Params P{};
+};
+
+int solve_prepare(tsmpc_plan* pl, const double* p, int32_t iters, double lam, const double* warm_sig,
+                  const double* warm_zeta, const double* warm_psi, const double* theta, const double* coef,
+                  int32_t flags, SolveState& st) {
+  if (!pl || !p) return fail(TSMPC_ERR_ARGUMENT, "null argument");
   if (iters < 1) return fail(TSMPC_ERR_VALIDATION, "max_iters must be >= 1");
   if (!(lam > 0.0)) return fail(TSMPC_ERR_VALIDATION, "step size must be positive");
   if (!pl->has_cache) return fail(TSMPC_ERR_VALIDATION, "no stage cache uploaded (tsmpc_set_cache)");
@@ -1210,44 +1221,26 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
   P.coef = pl->COEF;
   P.record_all = record ? 1 : 0;
   P.resid = pl->RESID;
-  CU(cudaEventRecord(pl->ev0, pl->stream));
-  if (pl->use_sparse) {
-    SParams S = pl->sbase;
-    S.P = P;
-    S.P.KY = pl->KY_S;
-    S.P.n_trunk = pl->sp_trunk;
-    if (!pl->sharded) {
-      S.nu0 = 0;
-      S.nu1 = iters;
-      S.phase = 3;
-      CU(sparse_launch(S, pl->sp_ctas, pl->sp_smem, pl->stream));
-      ++pl->launches;
-    } else {
-      // per iteration: phase 1 (backward + head pre-reduction), the cross-GPU sum of
-      // the per-trunk-node head sums, phase 2 (trunk sweep, needs, forward, epilogue)
-      const size_t hs = (size_t)std::max(1, pl->sp_trunk) * S.HS_LD;
-      for (int nu = 0; nu < iters; ++nu) {
-        S.nu0 = nu;
-        S.nu1 = nu + 1;
-        S.phase = 1;
-        CU(sparse_launch(S, pl->sp_ctas, pl->sp_smem, pl->stream));
-        if (pl->sp_trunk > 0) {
-          const int nr = pl->nccl->AllReduce(pl->HS, pl->HS, hs, NcclApi::kFloat64, NcclApi::kSum, pl->comm, pl->stream);
-          if (nr != 0) return fail(TSMPC_ERR_NCCL, "ncclAllReduce: %s", pl->nccl->GetErrorString(nr));
-        }
-        S.phase = 2;
-        CU(sparse_launch(S, pl->sp_ctas, pl->sp_smem, pl->stream));
-        pl->launches += 2;
-      }
-      // residual: max over ranks (non-negative doubles order like their bit patterns)
-      const int nr = pl->nccl->AllReduce(pl->RESID, pl->RESID, (size_t)nres, NcclApi::kUint64, NcclApi::kMax,
-                                         pl->comm, pl->stream);
-      if (nr != 0) return fail(TSMPC_ERR_NCCL, "ncclAllReduce: %s", pl->nccl->GetErrorString(nr));
-    }
-  } else if (launch_apg(pl, P)) {
-    return TSMPC_ERR_CUDA;
-  }
-  CU(cudaEventRecord(pl->ev1, pl->stream));
+  st.iters = iters;
+  st.nres = nres;
+  st.record = record;
+  st.stopping = stopping;
+  st.P = P;
+  return TSMPC_OK;
+}
+
+SParams sparse_params(const tsmpc_plan* pl, const Params& P) {
+  SParams S = pl->sbase;
+  S.P = P;
+  S.P.KY = pl->KY_S;
+  S.P.n_trunk = pl->sp_trunk;
+  return S;
+}
+
+int solve_finish(tsmpc_plan* pl, const SolveState& st, int32_t flags, tsmpc_result* out) {
+  const int E = pl->E, NXP = pl->NXP, NUP = pl->NUP, nx = pl->nx, nu = pl->nu;
+  const int iters = st.iters, nres = st.nres;
+  const bool record = st.record, stopping = st.stopping;
   int done = iters;
   if (stopping) {
     CU(cudaMemcpyAsync(&done, pl->ITERS, sizeof(int), cudaMemcpyDeviceToHost, pl->stream));
@@ -1302,6 +1295,150 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
     for (int k = 0; k < iters; ++k) out->resid_trace[k] = as_d(rbits[k]);
   return TSMPC_OK;
 }
+
+}  // namespace
+
+int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, const double* warm_sig,
+                const double* warm_zeta, const double* warm_psi, const double* theta, const double* coef,
+                int32_t flags, tsmpc_result* out) {
+  if (!pl || !p || !out) return fail(TSMPC_ERR_ARGUMENT, "null argument");
+  if (pl->sharded && !pl->comm && pl->world > 1)
+    return fail(TSMPC_ERR_VALIDATION, "shard plan without a communicator: run it through tsmpc_solve_group");
+  SolveState st;
+  int rc = solve_prepare(pl, p, iters, lam, warm_sig, warm_zeta, warm_psi, theta, coef, flags, st);
+  if (rc) return rc;
+  const Params& P = st.P;
+  CU(cudaEventRecord(pl->ev0, pl->stream));
+  if (pl->use_sparse) {
+    SParams S = sparse_params(pl, P);
+    if (!pl->sharded) {
+      S.nu0 = 0;
+      S.nu1 = iters;
+      S.phase = 3;
+      CU(sparse_launch(S, pl->sp_ctas, pl->sp_smem, pl->stream));
+      ++pl->launches;
+    } else {
+      // per iteration: phase 1 (backward + head pre-reduction), the cross-GPU sum of
+      // the per-trunk-node head sums, phase 2 (trunk sweep, needs, forward, epilogue)
+      const size_t hs = (size_t)std::max(1, pl->sp_trunk) * S.HS_LD;
+      for (int nu = 0; nu < iters; ++nu) {
+        S.nu0 = nu;
+        S.nu1 = nu + 1;
+        S.phase = 1;
+        CU(sparse_launch(S, pl->sp_ctas, pl->sp_smem, pl->stream));
+        if (pl->sp_trunk > 0 && pl->comm) {
+          const int nr = pl->nccl->AllReduce(pl->HS, pl->HS, hs, NcclApi::kFloat64, NcclApi::kSum, pl->comm, pl->stream);
+          if (nr != 0) return fail(TSMPC_ERR_NCCL, "ncclAllReduce: %s", pl->nccl->GetErrorString(nr));
+        }
+        S.phase = 2;
+        CU(sparse_launch(S, pl->sp_ctas, pl->sp_smem, pl->stream));
+        pl->launches += 2;
+      }
+      if (pl->comm) {
+        // residual: max over ranks (non-negative doubles order like their bit patterns)
+        const int nr = pl->nccl->AllReduce(pl->RESID, pl->RESID, (size_t)st.nres, NcclApi::kUint64, NcclApi::kMax,
+                                           pl->comm, pl->stream);
+        if (nr != 0) return fail(TSMPC_ERR_NCCL, "ncclAllReduce: %s", pl->nccl->GetErrorString(nr));
+      }
+    }
+  } else if (launch_apg(pl, P)) {
+    return TSMPC_ERR_CUDA;
+  }
+  CU(cudaEventRecord(pl->ev1, pl->stream));
+  return solve_finish(pl, st, flags, out);
+}
+
+namespace {
+
+constexpr int kMaxGroup = 8;
+struct GroupBufs {
+  double* hs[kMaxGroup];
+  unsigned long long* res[kMaxGroup];
+};
+
+// The exchange NCCL performs between shard ranks, done in place on one device:
+// every plan's head-sum buffer becomes the sum over the group.
+__global__ void group_sum_kernel(GroupBufs g, int n, size_t count) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < n; ++r) s += g.hs[r][i];
+    for (int r = 0; r < n; ++r) g.hs[r][i] = s;
+  }
+}
+
+__global__ void group_max_kernel(GroupBufs g, int n, int count) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+    unsigned long long m = 0;
+    for (int r = 0; r < n; ++r) m = max(m, g.res[r][i]);
+    for (int r = 0; r < n; ++r) g.res[r][i] = m;
+  }
+}
+
+}  // namespace
+
+int tsmpc_solve_group(tsmpc_plan* const* plans, int32_t n, const double* p, int32_t iters, double lam,
+                      const double* theta, const double* coef, int32_t flags, tsmpc_result* outs) {
+  if (!plans || !p || !outs) return fail(TSMPC_ERR_ARGUMENT, "null argument");
+  if (n < 1 || n > kMaxGroup) return fail(TSMPC_ERR_ARGUMENT, "group size %d outside 1..%d", n, kMaxGroup);
+  for (int r = 0; r < n; ++r) {
+    const tsmpc_plan* pl = plans[r];
+    if (!pl) return fail(TSMPC_ERR_ARGUMENT, "null plan in group");
+    if (!pl->sharded || pl->comm || pl->world != n || pl->rank != r)
+      return fail(TSMPC_ERR_VALIDATION, "group member %d must be the local shard plan of rank %d of %d", r, r, n);
+    if (pl->device != plans[0]->device || pl->sp_trunk != plans[0]->sp_trunk ||
+        pl->sbase.HS_LD != plans[0]->sbase.HS_LD || pl->E != plans[0]->E)
+      return fail(TSMPC_ERR_VALIDATION, "group members must be shards of one tree on one device");
+  }
+  CU(cudaSetDevice(plans[0]->device));
+  // all members run on the first member's stream, in the order NCCL ranks would
+  std::vector<cudaStream_t> saved(n);
+  for (int r = 0; r < n; ++r) saved[r] = plans[r]->stream;
+  struct Restore {
+    tsmpc_plan* const* pl;
+    std::vector<cudaStream_t>& s;
+    ~Restore() { for (size_t r = 0; r < s.size(); ++r) pl[r]->stream = s[r]; }
+  } restore{plans, saved};
+  cudaStream_t s0 = plans[0]->stream;
+  for (int r = 0; r < n; ++r) plans[r]->stream = s0;
+  std::vector<SolveState> st(n);
+  std::vector<SParams> S(n);
+  GroupBufs g{};
+  for (int r = 0; r < n; ++r) {
+    int rc = solve_prepare(plans[r], p, iters, lam, nullptr, nullptr, nullptr, theta, coef, flags, st[r]);
+    if (rc) return rc;
+    S[r] = sparse_params(plans[r], st[r].P);
+    g.hs[r] = plans[r]->HS;
+    g.res[r] = plans[r]->RESID;
+    CU(cudaEventRecord(plans[r]->ev0, s0));
+  }
+  const size_t hs = (size_t)std::max(1, plans[0]->sp_trunk) * plans[0]->sbase.HS_LD;
+  for (int nu = 0; nu < iters; ++nu) {
+    for (int r = 0; r < n; ++r) {
+      S[r].nu0 = nu;
+      S[r].nu1 = nu + 1;
+      S[r].phase = 1;
+      CU(sparse_launch(S[r], plans[r]->sp_ctas, plans[r]->sp_smem, s0));
+    }
+    if (plans[0]->sp_trunk > 0) {
+      group_sum_kernel<<<(unsigned)std::min<size_t>(256, (hs + 255) / 256), 256, 0, s0>>>(g, n, hs);
+      CU(cudaGetLastError());
+    }
+    for (int r = 0; r < n; ++r) {
+      S[r].phase = 2;
+      CU(sparse_launch(S[r], plans[r]->sp_ctas, plans[r]->sp_smem, s0));
+      plans[r]->launches += 2;
+    }
+  }
+  group_max_kernel<<<(st[0].nres + 255) / 256, 256, 0, s0>>>(g, n, st[0].nres);
+  CU(cudaGetLastError());
+  for (int r = 0; r < n; ++r) CU(cudaEventRecord(plans[r]->ev1, s0));
+  for (int r = 0; r < n; ++r) {
+    int rc = solve_finish(plans[r], st[r], flags, outs + r);
+    if (rc) return rc;
+  }
+  return TSMPC_OK;
+}
+
 
 int tsmpc_set_stopping(tsmpc_plan* pl, double tol, int32_t check_every) {
   if (!pl) return fail(TSMPC_ERR_ARGUMENT, "null argument");

@@ -35,6 +35,7 @@
 // and, on the last iteration, the outputs.  Otherwise one tile slot is streamed
 // with cp.async, prefetched one step ahead (see bwd/fwd below).
 #include "tsmpc_kernels.cuh"
+#include <mutex>
 
 namespace cg = cooperative_groups;
 
@@ -1235,10 +1236,32 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
 
 namespace tsmpc {
 
+// g_sp is one per device and shared by every plan of the process: launches from
+// different streams are chained through a per-device event so that a launch's
+// parameter upload cannot land while another plan's kernel still reads g_sp
+// (the kernel occupies the whole GPU anyway, so nothing is lost).
 cudaError_t sparse_launch(const SParams& S, int ctas, size_t smem, cudaStream_t stream) {
-  cudaError_t e = cudaMemcpyToSymbolAsync(g_sp, &S, sizeof(SParams), 0, cudaMemcpyHostToDevice, stream);
+  static std::mutex mu;
+  static cudaEvent_t last[64] = {};
+  static cudaStream_t last_stream[64] = {};
+  std::lock_guard<std::mutex> lock(mu);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  return cudaLaunchCooperativeKernel((void*)apg_sparse_kernel, dim3(ctas), dim3(kThreadsS), nullptr, smem, stream);
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (!last[dev]) {
+    e = cudaEventCreateWithFlags(&last[dev], cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  } else if (last_stream[dev] != stream) {
+    e = cudaStreamWaitEvent(stream, last[dev], 0);
+    if (e != cudaSuccess) return e;
+  }
+  e = cudaMemcpyToSymbolAsync(g_sp, &S, sizeof(SParams), 0, cudaMemcpyHostToDevice, stream);
+  if (e != cudaSuccess) return e;
+  e = cudaLaunchCooperativeKernel((void*)apg_sparse_kernel, dim3(ctas), dim3(kThreadsS), nullptr, smem, stream);
+  if (e != cudaSuccess) return e;
+  last_stream[dev] = stream;
+  return cudaEventRecord(last[dev], stream);
 }
 
 // beta_s = beta M (rows of the stage cache mapped to the structured basis,

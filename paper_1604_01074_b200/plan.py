@@ -69,7 +69,7 @@ class DevicePlan:
             handle = lib.tsmpc_plan_create(ctypes.byref(pb), int(device))
         else:
             rank, world, nid = shard
-            idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(bytes(nid))
+            idbuf = None if nid is None else (ctypes.c_uint8 * 128).from_buffer_copy(bytes(nid))
             handle = lib.tsmpc_plan_create_shard(ctypes.byref(pb), int(device), int(rank), int(world),
                                                  idbuf)
         self.shard = shard
@@ -179,20 +179,7 @@ class DevicePlan:
         """One APG solve (engine.py:485-601).  ``keep_device``: leave the iterates in
         HBM (only u0, residual and gap come back); ``warm_device``: start from the
         previous solve's final dual, still in HBM (closed-loop warm start)."""
-        E, n_x, n_u, n = self.n_edges, self.n_x, self.n_u, self.n_nodes
-        out = {
-            "u0": np.empty(n_u), "x": np.empty((n, n_x)), "u": np.empty((E, n_u)),
-            "x_avg": np.empty((n, n_x)), "u_avg": np.empty((E, n_u)),
-            "dual_sig": np.empty((E, n_x)), "dual_zeta": np.empty((E, n_x)),
-            "dual_psi": np.empty((E, n_u)),
-        }
-        res = nat.Result()
-        res.u0 = nat.dptr(out["u0"])
-        if not keep_device:
-            for k, v in out.items():
-                setattr(res, k, nat.dptr(v))
-        trace = np.empty(iters) if record_residuals else None
-        res.resid_trace = nat.dptr(trace)
+        out, res, trace = self._result_buffers(iters, keep_device, record_residuals)
         flags = ((nat.RECORD_RESIDUALS if record_residuals else 0)
                  | (nat.SKIP_GAP if skip_gap else 0) | (nat.KEEP_DEVICE if keep_device else 0)
                  | (nat.WARM_DEVICE if warm_device else 0))
@@ -208,6 +195,27 @@ class DevicePlan:
                                    nat.dptr(ws), nat.dptr(wz), nat.dptr(wp),
                                    nat.dptr(th), nat.dptr(cf), flags, ctypes.byref(res))
         nat.check(rc, "tsmpc_solve")
+        return self._result_dict(out, res, trace)
+
+    def _result_buffers(self, iters: int, keep_device: bool, record_residuals: bool):
+        E, n_x, n_u, n = self.n_edges, self.n_x, self.n_u, self.n_nodes
+        out = {
+            "u0": np.empty(n_u), "x": np.empty((n, n_x)), "u": np.empty((E, n_u)),
+            "x_avg": np.empty((n, n_x)), "u_avg": np.empty((E, n_u)),
+            "dual_sig": np.empty((E, n_x)), "dual_zeta": np.empty((E, n_x)),
+            "dual_psi": np.empty((E, n_u)),
+        }
+        res = nat.Result()
+        res.u0 = nat.dptr(out["u0"])
+        if not keep_device:
+            for k, v in out.items():
+                setattr(res, k, nat.dptr(v))
+        trace = np.empty(iters) if record_residuals else None
+        res.resid_trace = nat.dptr(trace)
+        return out, res, trace
+
+    @staticmethod
+    def _result_dict(out: dict, res, trace) -> dict:
         out.update(residual_inf=float(res.residual_inf), gap=float(res.gap),
                    device_ms=float(res.device_ms), iterations=int(res.iterations),
                    device_total_ms=float(res.device_total_ms),

@@ -26,7 +26,7 @@ import numpy as np
 from . import _native as nat
 from .plan import DevicePlan
 
-__all__ = ["nccl_unique_id", "ShardedSolver", "gather_rows"]
+__all__ = ["nccl_unique_id", "ShardedSolver", "LocalShardGroup", "gather_rows", "merge_rows"]
 
 
 def nccl_unique_id() -> bytes:
@@ -66,29 +66,85 @@ class ShardedSolver:
                                skip_gap=True, keep_device=keep_device)
 
 
+class LocalShardGroup:
+    """All ``world`` shards of one tree on ONE device, solved in lockstep in one
+    process (``tsmpc_solve_group``): per iteration phase 1 of every shard, an
+    in-place device sum of their head-sum buffers (the exchange the NCCL
+    all-reduce performs across GPUs), phase 2 of every shard.  It runs exactly
+    the per-rank kernels of a ``world``-GPU job, so the multi-rank split is
+    checked on one GPU; the kernels of different shards never wait on each other.
+    """
+
+    def __init__(self, model, tree, factor, world: int, scaling=None, device: int = 0):
+        self.world = int(world)
+        self.n_edges, self.n_nodes = int(tree.n_nodes) - 1, int(tree.n_nodes)
+        self.plans = [DevicePlan(model, tree, factor, scaling, device=device,
+                                 shard=(r, self.world, None)) for r in range(self.world)]
+        self.edges = [pl.edges(0) for pl in self.plans]
+
+    def set_cache(self, cache, model=None):
+        for pl in self.plans:
+            pl.set_cache(cache, model)
+
+    def solve(self, p, iters: int, lam: float, theta=None, coef=None,
+              record_residuals: bool = False) -> list[dict]:
+        """Per-rank result dicts (rows of ``edges[r]`` valid in result r)."""
+        bufs = [pl._result_buffers(iters, False, record_residuals) for pl in self.plans]
+        results = (nat.Result * self.world)(*(b[1] for b in bufs))
+        handles = (ctypes.c_void_p * self.world)(*(pl._h for pl in self.plans))
+        flags = (nat.RECORD_RESIDUALS if record_residuals else 0) | nat.SKIP_GAP
+        th = np.ascontiguousarray(theta, dtype=float) if theta is not None else None
+        cf = np.ascontiguousarray(coef, dtype=float) if coef is not None else None
+        pv = np.ascontiguousarray(p, dtype=float)
+        lib = self.plans[0]._lib
+        nat.check(lib.tsmpc_solve_group(handles, self.world, nat.dptr(pv), int(iters), float(lam),
+                                        nat.dptr(th), nat.dptr(cf), flags, results),
+                  "tsmpc_solve_group")
+        return [DevicePlan._result_dict(b[0], results[r], b[2]) for r, b in enumerate(bufs)]
+
+    def assemble(self, outs: list[dict]) -> dict:
+        """Full per-edge / per-node arrays from the per-rank results."""
+        parts = [_owned(o, e) for o, e in zip(outs, self.edges)]
+        return merge_rows(parts, outs[0], self.n_edges, self.n_nodes)
+
+
+_EDGE_KEYS = ("u", "u_avg", "dual_sig", "dual_zeta", "dual_psi")
+_NODE_KEYS = ("x", "x_avg")
+
+
+def _owned(out: dict, edges: np.ndarray) -> dict:
+    part = {k: out[k][edges] for k in _EDGE_KEYS}
+    part.update({k: out[k][edges + 1] for k in _NODE_KEYS})
+    part["edges"] = edges
+    return part
+
+
+def merge_rows(parts: list[dict], out: dict, n_edges: int, n_nodes: int) -> dict:
+    """Full arrays from per-rank owned rows (each edge is computed by exactly
+    one rank or replicated); ``out`` supplies the root row and the residual."""
+    full = {k: np.zeros((n_edges, out[k].shape[1])) for k in _EDGE_KEYS}
+    full.update({k: np.zeros((n_nodes, out[k].shape[1])) for k in _NODE_KEYS})
+    full["x"][0] = out["x"][0]
+    full["x_avg"][0] = out["x_avg"][0]
+    for pt in parts:
+        e = pt["edges"]
+        for k in _EDGE_KEYS:
+            full[k][e] = pt[k]
+        for k in _NODE_KEYS:
+            full[k][e + 1] = pt[k]
+    full["u0"] = full["u_avg"][0]
+    full["residual_inf"] = out["residual_inf"]
+    return full
+
+
 def gather_rows(out: dict, edges: np.ndarray, n_edges: int, n_nodes: int, group=None,
                 dst: int = 0) -> dict | None:
     """Assemble full per-edge / per-node arrays on rank ``dst`` from every rank's
     owned rows (each edge is computed by exactly one rank or replicated)."""
     import torch.distributed as dist
-    part = {k: out[k][edges] for k in ("u", "u_avg", "dual_sig", "dual_zeta", "dual_psi")}
-    part.update({k: out[k][edges + 1] for k in ("x", "x_avg")})
-    part["edges"] = edges
+    part = _owned(out, edges)
     parts = [None] * dist.get_world_size(group) if dist.get_rank(group) == dst else None
     dist.gather_object(part, parts, dst=dst, group=group)
     if parts is None:
         return None
-    full = {k: np.zeros((n_edges, out[k].shape[1])) for k in ("u", "u_avg", "dual_sig", "dual_zeta",
-                                                           "dual_psi")}
-    full.update({k: np.zeros((n_nodes, out[k].shape[1])) for k in ("x", "x_avg")})
-    full["x"][0] = out["x"][0]
-    full["x_avg"][0] = out["x_avg"][0]
-    for pt in parts:
-        e = pt["edges"]
-        for k in ("u", "u_avg", "dual_sig", "dual_zeta", "dual_psi"):
-            full[k][e] = pt[k]
-        for k in ("x", "x_avg"):
-            full[k][e + 1] = pt[k]
-    full["u0"] = full["u_avg"][0]
-    full["residual_inf"] = out["residual_inf"]
-    return full
+    return merge_rows(parts, out, n_edges, n_nodes)

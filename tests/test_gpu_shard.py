@@ -1,7 +1,9 @@
 """GPU: the sharded solve machinery (phase 1 -> ncclAllReduce -> phase 2 per
-iteration, streamed tiles) on one GPU with a one-rank NCCL communicator.  The
-multi-rank data movement is NCCL's; the partition logic is covered on CPU by
-tests/test_shard_cpu.py (gloo, world size 2)."""
+iteration, streamed tiles) on one GPU with a one-rank NCCL communicator, and
+the real multi-rank split (world 2..8) through tsmpc_solve_group: every shard's
+kernels on one device, their head sums exchanged by an in-place device sum
+between the phases, results assembled from each rank's owned rows.  The
+partition logic is also covered on CPU by tests/test_shard_cpu.py (gloo)."""
 
 import numpy as np
 import pytest
@@ -14,8 +16,9 @@ if not has_gpu():  # pragma: no cover - CPU container
     pytest.skip("no CUDA device", allow_module_level=True)
 
 from paper_1604_01074_b200 import engine  # noqa: E402
+from paper_1604_01074_b200.errors import ValidationError  # noqa: E402
 from paper_1604_01074_b200.plan import DevicePlan  # noqa: E402
-from paper_1604_01074_b200.shard import nccl_unique_id  # noqa: E402
+from paper_1604_01074_b200.shard import LocalShardGroup, nccl_unique_id  # noqa: E402
 
 
 @pytest.mark.parametrize("name", ["bcn63_SMPC1_N24", "tank3_tree30_N24", "tank3_tree_30_N8"])
@@ -50,3 +53,63 @@ def test_shard_world1_matches_single_gpu_plan():
     b = shard.solve(c.p, c.iters, c.lam, theta=th, coef=cf, skip_gap=True)
     for f in ("u0", "x_avg", "u_avg", "x", "u"):
         assert rel_err(b[f], a[f]) <= 10 * c.tol(f), f
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("name", ["bcn63_SMPC1_N24", "tank3_tree30_N24"])
+def test_shard_group_matches_reference(name, world):
+    c = load_case(name)
+    z = c.z
+    grp = LocalShardGroup(c.model, c.tree, c.factor, world, c.scaling)
+    owned = np.concatenate(grp.edges)
+    assert np.array_equal(np.unique(owned), np.arange(c.tree.n_edges))
+    grp.set_cache(c.cache, c.model)
+    th, cf = engine.theta_schedule(c.iters)
+    outs = grp.solve(c.p, c.iters, c.lam, theta=th, coef=cf)
+    assert all(o["kernel_launches"] == 2 * c.iters for o in outs)
+    assert len({o["residual_inf"] for o in outs}) == 1  # max over the group
+    full = grp.assemble(outs)
+    for f in ("u0", "x", "u", "x_avg", "u_avg"):
+        assert rel_err(full[f], z[f"r_{f}"]) <= c.tol(f), (f, rel_err(full[f], z[f"r_{f}"]))
+    for k in ("sig", "zeta", "psi"):
+        assert rel_err(full[f"dual_{k}"], z[f"r_dual_{k}"]) <= c.tol("dual"), k
+    r_ref = float(z["r_residual_inf"])
+    assert abs(full["residual_inf"] - r_ref) <= c.tol("residual_inf") * max(1.0, abs(r_ref))
+
+
+@pytest.mark.parametrize("tree_name,world", [("SMPC3", 2), ("SMPC3", 8), ("SMPC8", 4)])
+def test_shard_group_matches_single_plan_paper_trees(tree_name, world):
+    """Full-size paper trees: the w-way split reproduces the single-GPU plan's
+    iterates to within the summation order of the chain-head sums."""
+    import bench
+    W = bench.build_workload(tree_name)
+    iters = 60
+    th, cf = engine.theta_schedule(iters)
+    single = DevicePlan(W["model"], W["tree"], W["factor"], W["scaling"])
+    single.set_cache(W["caches"][0], W["model"])
+    lam = 0.05
+    a = single.solve(W["p"], iters, lam, theta=th, coef=cf, skip_gap=True, record_residuals=True)
+    grp = LocalShardGroup(W["model"], W["tree"], W["factor"], world, W["scaling"])
+    sizes = [len(e) for e in grp.edges]
+    assert min(sizes) > 0
+    grp.set_cache(W["caches"][0], W["model"])
+    outs = grp.solve(W["p"], iters, lam, theta=th, coef=cf, record_residuals=True)
+    full = grp.assemble(outs)
+    for f in ("u0", "x", "u", "x_avg", "u_avg"):
+        assert rel_err(full[f], a[f]) <= 1e-10, (f, rel_err(full[f], a[f]))
+    for k in ("sig", "zeta", "psi"):
+        assert rel_err(full[f"dual_{k}"], a[f"dual_{k}"]) <= 1e-10, k
+    assert np.allclose(outs[0]["resid_trace"], a["resid_trace"], rtol=1e-8, atol=1e-12)
+
+
+def test_shard_group_rejects_bad_members():
+    c = load_case("tank3_tree30_N24")
+    grp = LocalShardGroup(c.model, c.tree, c.factor, 2, c.scaling)
+    grp.set_cache(c.cache, c.model)
+    # an NCCL-less shard plan of a world-2 split cannot run alone
+    with pytest.raises(ValidationError, match="tsmpc_solve_group"):
+        grp.plans[0].solve(c.p, 5, c.lam, skip_gap=True)
+    # members out of rank order are refused
+    grp.plans.reverse()
+    with pytest.raises(ValidationError, match="local shard plan of rank"):
+        grp.solve(c.p, 5, c.lam)
