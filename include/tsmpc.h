@@ -213,6 +213,12 @@ int tsmpc_describe_tree(const tsmpc_problem* prob, int32_t max_ctas, int32_t col
  * trunk_edges, resident_ctas, max_rows_per_cta, max_needs, smem_bytes}. */
 int tsmpc_describe_sparse(const tsmpc_problem* prob, int32_t max_ctas, int64_t smem_limit,
                           int64_t* info, int32_t n_info);
+/* Page-locked host memory for result buffers (cudaHostAlloc, portable across
+ * devices): tsmpc_solve's device->host copies into such buffers run at DMA speed
+ * (the Python layer returns SolveReport arrays from a pool of these). */
+void* tsmpc_host_alloc(int64_t bytes);
+void tsmpc_host_free(void* ptr);
+
 /* Host-only planning of one shard: info = {ctas, owned_chains, owned_rows,
  * trunk_edges, total_chains, owned_trunk_nodes, smem_bytes}; the owned chain
  * edges go to edges[0..cap) when edges != NULL. */

@@ -12,6 +12,8 @@ import ctypes
 import os
 import pathlib
 import subprocess
+import threading
+import weakref
 
 import numpy as np
 
@@ -90,6 +92,8 @@ SIGNATURES = {
     "tsmpc_describe_sparse": (ctypes.c_int, [ctypes.POINTER(Problem), ctypes.c_int32, ctypes.c_int64,
                                              _ip, ctypes.c_int32]),
     "tsmpc_device_count": (ctypes.c_int, []),
+    "tsmpc_host_alloc": (ctypes.c_void_p, [ctypes.c_int64]),
+    "tsmpc_host_free": (None, [ctypes.c_void_p]),
     "tsmpc_debug_timers": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64),
                                           ctypes.c_int32]),
     "tsmpc_describe_tree": (ctypes.c_int, [ctypes.POINTER(Problem), ctypes.c_int32, ctypes.c_int32,
@@ -171,6 +175,60 @@ def check(rc: int, what: str = "") -> None:
 
 def device_count() -> int:
     return int(load_library().tsmpc_device_count())
+
+
+class _PinnedPool:
+    """Reusable page-locked blocks (``tsmpc_host_alloc``) backing result arrays.
+
+    A block returns to the pool when the last array viewing it is collected, so
+    steady-state solves reuse the same few blocks and their device->host copies
+    run at DMA speed (pageable destinations go through the driver's bounce
+    buffer at a fraction of that).  At most ``keep`` bytes are kept idle.
+    """
+
+    def __init__(self, keep: int = 1 << 30):
+        self.keep = keep
+        self._free: dict[int, list[int]] = {}
+        self._idle = 0
+        self._lock = threading.Lock()
+        self.disabled = bool(os.environ.get("TSMPC_PAGEABLE"))
+
+    def arrays(self, shapes) -> list[np.ndarray] | None:
+        """float64 arrays of the given shapes in one pinned block (None if
+        page-locked memory is unavailable)."""
+        if self.disabled:
+            return None
+        sizes = [int(np.prod(sh)) * 8 for sh in shapes]
+        offs, total = [], 0
+        for n in sizes:
+            offs.append(total)
+            total += (n + 127) // 128 * 128
+        total = max(total, 128)
+        with self._lock:
+            lst = self._free.get(total)
+            ptr = lst.pop() if lst else None
+            if ptr is not None:
+                self._idle -= total
+        if ptr is None:
+            ptr = load_library().tsmpc_host_alloc(total)
+            if not ptr:
+                self.disabled = True  # no device / no page-locked memory: pageable arrays
+                return None
+        buf = (ctypes.c_char * total).from_address(ptr)
+        weakref.finalize(buf, self._release, ptr, total).atexit = False
+        return [np.frombuffer(buf, dtype=np.float64, count=n // 8, offset=o).reshape(sh)
+                if n else np.empty(sh) for sh, n, o in zip(shapes, sizes, offs)]
+
+    def _release(self, ptr: int, nbytes: int) -> None:
+        with self._lock:
+            if self._idle + nbytes <= self.keep:
+                self._free.setdefault(nbytes, []).append(ptr)
+                self._idle += nbytes
+                return
+        load_library().tsmpc_host_free(ptr)
+
+
+PINNED = _PinnedPool()
 
 
 def dptr(a) -> "ctypes._Pointer | None":

@@ -335,6 +335,19 @@ const char* tsmpc_plan_path(const tsmpc_plan* pl) {
   return s.c_str();
 }
 
+void* tsmpc_host_alloc(int64_t bytes) {
+  void* p = nullptr;
+  if (bytes <= 0 || cudaHostAlloc(&p, (size_t)bytes, cudaHostAllocPortable) != cudaSuccess) {
+    fail(TSMPC_ERR_CUDA, "cudaHostAlloc(%lld bytes) failed", (long long)bytes);
+    return nullptr;
+  }
+  return p;
+}
+
+void tsmpc_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 int tsmpc_device_count(void) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;

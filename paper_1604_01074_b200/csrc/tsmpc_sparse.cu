@@ -718,6 +718,8 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
   double* Zs = S.sweep_in_a ? c.A() : c.B();
   double* Xs = Zs + (size_t)T * nc;
   double* Ip = Xs + (size_t)T * nc;  // 1 / (2 p) of each trunk edge
+  long long ts_ = clock64();
+  (void)ts_;
   const int* sch = g;  // schedule: resident / staged in shared memory when it fits, else via L1
   if (S.sched_resident) {
     sch = reinterpret_cast<const int*>(s_dyn + S.O_SCHED);
@@ -736,6 +738,7 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
   const double* Y = P.ybuf[cur];
   const double* Yp = P.ybuf[cur ^ 1];
   const double* adiag = c.adiag();
+  TSMPC_MARK(P, 13, ts_);
   // (1) own terms + chain-head children (one parallel round of loads)
 #pragma unroll 1
   for (int tp = threadIdx.x; tp < T; tp += kThreadsS) Ip[tp] = __ldg(P.inv2p + pos[8 * tp]);
@@ -792,6 +795,7 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
     Xs[idx] = x;
   }
   __syncthreads();
+  TSMPC_MARK(P, 14, ts_);
   if (T <= kSeqTrunk) {
     // small trunk: one thread per component walks the levels (no level barriers)
     if (threadIdx.x < nc) {
@@ -869,6 +873,7 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
     __syncthreads();
   }
   }
+  TSMPC_MARK(P, 15, ts_);
   // (4) KY columns of this slice
 #pragma unroll 1
   for (int idx = threadIdx.x; idx < T * nc; idx += kThreadsS) {

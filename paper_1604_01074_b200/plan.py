@@ -199,12 +199,20 @@ class DevicePlan:
 
     def _result_buffers(self, iters: int, keep_device: bool, record_residuals: bool):
         E, n_x, n_u, n = self.n_edges, self.n_x, self.n_u, self.n_nodes
-        out = {
-            "u0": np.empty(n_u), "x": np.empty((n, n_x)), "u": np.empty((E, n_u)),
-            "x_avg": np.empty((n, n_x)), "u_avg": np.empty((E, n_u)),
-            "dual_sig": np.empty((E, n_x)), "dual_zeta": np.empty((E, n_x)),
-            "dual_psi": np.empty((E, n_u)),
-        }
+        shapes = {"u0": (n_u,)}
+        if not keep_device:
+            shapes.update({"x": (n, n_x), "u": (E, n_u), "x_avg": (n, n_x), "u_avg": (E, n_u),
+                           "dual_sig": (E, n_x), "dual_zeta": (E, n_x), "dual_psi": (E, n_u)})
+        # result arrays in page-locked memory (pooled) when available
+        arrs = nat.PINNED.arrays(list(shapes.values()))
+        if arrs is None:
+            arrs = [np.empty(sh) for sh in shapes.values()]
+        out = dict(zip(shapes, arrs))
+        if keep_device:
+            out.update({"x": np.empty((n, n_x)), "u": np.empty((E, n_u)),
+                        "x_avg": np.empty((n, n_x)), "u_avg": np.empty((E, n_u)),
+                        "dual_sig": np.empty((E, n_x)), "dual_zeta": np.empty((E, n_x)),
+                        "dual_psi": np.empty((E, n_u))})
         res = nat.Result()
         res.u0 = nat.dptr(out["u0"])
         if not keep_device:

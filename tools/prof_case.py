@@ -39,7 +39,7 @@ if os.environ.get("TSMPC_DENSE_NAMES"):
 else:  # sparse kernel marks (tsmpc_sparse.cu)
     names = ["bwd fill", "bwd xiq scan", "bwd h=Ls'z", "bwd g scan", "fwd S scan", "bwd z=B'xiq",
              "fwd bv=B du", "fwd u, x scan", "fwd epilogue", "grid.sync", "trunk sweep", "fwd du=Lt S",
-             "trunk needs+own", " epi pass1", " epi bar", " epi pass2"]
+             "trunk needs+own", " sweep: stage", " sweep: loads", " sweep: levels"]
 tot = float(tm.sum())
 if tot > 0:
     n = a.iters * a.reps
