@@ -443,6 +443,126 @@ __global__ void __launch_bounds__(256) gap_dykstra_pass_kernel(EdgeCtx c, const 
   }
 }
 
+// Dykstra in lockstep (cooperative launch): the same iterates and stopping sweep
+// as the two passes above, without running every edge for all 200 sweeps.  Edges
+// advance kDykBlk sweeps at a time (state round-trips through st, two buffers of
+// [x | inc] rows), recording the per-sweep max change; after each block one grid
+// barrier makes slots[] final, and every thread reads the same stopping sweep K.
+// The edges then restart from the state at the start of K's block and run the
+// K + 1 - blk0 sweeps left before the final affine projection (as pass 2 would).
+constexpr int kDykBlk = 8;
+constexpr int kDykMax = 200;
+
+__global__ void __launch_bounds__(256) gap_dykstra_coop_kernel(EdgeCtx c, const double* __restrict__ u0,
+                                                               unsigned long long* slots, double* st,
+                                                               double* uf) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double dsm[];
+  double* ev = dsm;
+  double* pv = ev + c.er_nnz;
+  double* wsm = pv + c.pc_nnz + (c.pc_nnz + c.er_nnz & 1);
+  int* ep = reinterpret_cast<int*>(wsm + 8 * 448);
+  int* eix = ep + c.ne + 1;
+  int* pp = eix + c.er_nnz;
+  int* pix = pp + c.nu + 1;
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < c.er_nnz; i += blockDim.x) { ev[i] = c.er_val[i]; eix[i] = c.er_idx[i]; }
+  for (int i = threadIdx.x; i < c.pc_nnz; i += blockDim.x) { pv[i] = c.pc_val[i]; pix[i] = c.pc_idx[i]; }
+  for (int i = threadIdx.x; i <= c.ne; i += blockDim.x) ep[i] = c.er_ptr[i];
+  for (int i = threadIdx.x; i <= c.nu; i += blockDim.x) pp[i] = c.pc_ptr[i];
+  __syncthreads();
+  auto project = [&](const double* xx, const double* tgt, double* rr, double* ya) {
+    for (int k = lane; k < c.ne; k += 32) {
+      double s = 0.0;
+      for (int q = ep[k]; q < ep[k + 1]; ++q) s = fma(xx[eix[q]], ev[q], s);
+      rr[k] = s - tgt[k];
+    }
+    __syncwarp();
+    for (int jj = lane; jj < c.nu; jj += 32) {
+      double s = 0.0;
+      for (int q = pp[jj]; q < pp[jj + 1]; ++q) s = fma(rr[pix[q]], pv[q], s);
+      ya[jj] = xx[jj] - s;
+    }
+    __syncwarp();
+  };
+  double* x = wsm + (size_t)wl * 448;
+  double* y = x + 128;
+  double* r = y + 128;
+  double* inc = r + 64;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const size_t SW = 2 * (size_t)c.NUP;  // one [x | inc] state row
+  double* SA = st;                      // state at the start of the current block
+  double* SB = st + (size_t)c.E * SW;   // state at its end
+  // runs sweeps [it0, it1) of edge e from state (x, inc) in shared memory
+  auto sweeps = [&](int e, int it0, int it1, bool record) {
+    const double* tgt = c.jrhs + (size_t)e * c.ne;
+    for (int it = it0; it < it1; ++it) {
+      project(x, tgt, r, y);
+      double mx = 0.0;
+      for (int j = lane; j < c.nu; j += 32) {
+        const double t = y[j] + inc[j];
+        const double xn = clip(t, c.u_min[j], c.u_max[j]);
+        inc[j] = t - xn;
+        mx = fmax(mx, fabs(xn - x[j]));
+        x[j] = xn;
+      }
+      __syncwarp();
+      if (record) {
+        mx = warp_max(mx);
+        if (lane == 0 && mx > 0.0) atomicMax(slots + it, (unsigned long long)__double_as_longlong(mx));
+      }
+    }
+  };
+  int K = -1, blk0 = 0;
+  for (int blk = 0; blk < kDykMax; blk += kDykBlk) {
+    const int it1 = min(blk + kDykBlk, kDykMax);
+    for (int e = gw; e < c.E; e += nw) {
+      const double* sa = SA + (size_t)e * SW;
+      for (int j = lane; j < c.nu; j += 32) {
+        x[j] = blk == 0 ? u0[(size_t)e * c.NUP + j] : __ldcg(sa + j);
+        inc[j] = blk == 0 ? 0.0 : __ldcg(sa + c.NUP + j);
+      }
+      __syncwarp();
+      sweeps(e, blk, it1, true);
+      double* sb = SB + (size_t)e * SW;
+      for (int j = lane; j < c.nu; j += 32) {
+        __stcg(sb + j, x[j]);
+        __stcg(sb + c.NUP + j, inc[j]);
+      }
+      if (blk == 0) {  // the block-start state of block 0, for a restart
+        for (int j = lane; j < c.nu; j += 32) {
+          __stcg(SA + (size_t)e * SW + j, u0[(size_t)e * c.NUP + j]);
+          __stcg(SA + (size_t)e * SW + c.NUP + j, 0.0);
+        }
+      }
+      __syncwarp();
+    }
+    grid.sync();
+    for (int it = blk; it < it1; ++it) {
+      const double g = __longlong_as_double((long long)*((volatile unsigned long long*)(slots + it)));
+      if (g < 1e-13) { K = it; break; }
+    }
+    if (K >= 0) { blk0 = blk; break; }
+    double* t = SA; SA = SB; SB = t;
+  }
+  // K found: restart K's block and stop after sweep K; else SA holds the state
+  // after all kDykMax sweeps
+  const int n_left = K >= 0 ? K + 1 - blk0 : 0;
+  for (int e = gw; e < c.E; e += nw) {
+    const double* sa = SA + (size_t)e * SW;
+    for (int j = lane; j < c.nu; j += 32) {
+      x[j] = __ldcg(sa + j);
+      inc[j] = __ldcg(sa + c.NUP + j);
+    }
+    __syncwarp();
+    sweeps(e, 0, n_left, false);
+    project(x, c.jrhs + (size_t)e * c.ne, r, y);
+    for (int j = lane; j < c.nu; j += 32) uf[(size_t)e * c.NUP + j] = y[j];
+    __syncwarp();
+  }
+}
+
 // ub_e = u_feas_e B'   (E x NXP)
 __global__ void gap_ub_kernel(EdgeCtx c, const double* __restrict__ uf, double* ub) {
   __shared__ double shm[8][128];

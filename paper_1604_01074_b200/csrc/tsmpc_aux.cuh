@@ -55,6 +55,8 @@ __global__ void gap_project_dykstra_kernel(EdgeCtx c, double* xit, double* inc, 
                                            unsigned long long* slots);
 __global__ void gap_dykstra_pass_kernel(EdgeCtx c, const double* __restrict__ u0,
                                         unsigned long long* slots, int pass, double* uf);
+__global__ void gap_dykstra_coop_kernel(EdgeCtx c, const double* __restrict__ u0,
+                                        unsigned long long* slots, double* st, double* uf);
 __global__ void gap_ub_kernel(EdgeCtx c, const double* uf, double* ub);
 __global__ void gap_propagate_stage_kernel(EdgeCtx c, int n0, int n1, double* xf, const double* ub);
 __global__ void gap_primal_terms_kernel(EdgeCtx c, const double* uf, const double* xf, double* cols);

@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -98,6 +99,8 @@ struct tsmpc_plan {
   const NcclApi* nccl = nullptr;
   void* comm = nullptr;
   double* HS = nullptr;
+  double* DYKST = nullptr;  // lockstep Dykstra state (2 x E x [x | inc])
+  bool dyk_two_pass = std::getenv("TSMPC_DYKSTRA_TWO_PASS") != nullptr;
   std::vector<int> owned_edges, trunk_edges;
   // plan stats
   int n_levels = 0, n_tiles = 0, n_segs = 0, n_ctas = 0, n_trunk = 0;
@@ -783,6 +786,8 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
 
   cudaFuncSetAttribute(gap_dykstra_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(sizeof(double) * (2 * 64 * 128 + 8 * 448 + 1) + sizeof(int) * (2 * 64 * 128 + 200)));
+  cudaFuncSetAttribute(gap_dykstra_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(sizeof(double) * (2 * 64 * 128 + 8 * 448 + 1) + sizeof(int) * (2 * 64 * 128 + 200)));
   {  // sparse junction operators for the gap's Dykstra projection
     std::vector<int> erp{0}, eri, pcp{0}, pci;
     std::vector<double> erv, pcv;
@@ -1105,12 +1110,27 @@ static int compute_gap(tsmpc_plan* pl, const double* yfinal, double* gap) {
     CU(cudaMemsetAsync(pl->DYK, 0, sizeof(unsigned long long) * 256, pl->stream));
     const size_t dsm = sizeof(double) * ((size_t)c.er_nnz + c.pc_nnz + 1 + 8 * 448) +
                        sizeof(int) * ((size_t)pl->ne + 1 + c.er_nnz + pl->nu + 1 + c.pc_nnz);
-    const int gblk = std::max(1, std::min((E + 7) / 8, pl->sm_count * 8));
-    gap_dykstra_pass_kernel<<<gblk, 256, dsm, pl->stream>>>(c, pl->UAVG, pl->DYK, 1, pl->UF);
-    CU(cudaGetLastError());
-    gap_dykstra_pass_kernel<<<gblk, 256, dsm, pl->stream>>>(c, pl->UAVG, pl->DYK, 2, pl->UF);
-    CU(cudaGetLastError());
-    pl->launches += 1;
+    // lockstep cooperative Dykstra when its grid is co-resident, else two passes
+    int occ = 0;
+    if (!pl->dyk_two_pass &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gap_dykstra_coop_kernel, 256, dsm) == cudaSuccess &&
+        occ > 0) {
+      if (!pl->DYKST && pl->alloc(&pl->DYKST, 4 * (size_t)E * pl->NUP)) return TSMPC_ERR_CUDA;
+      const int gblk = std::max(1, std::min((E + 7) / 8, occ * pl->sm_count));
+      double* u0 = pl->UAVG;
+      unsigned long long* slots = pl->DYK;
+      double* st = pl->DYKST;
+      double* uf = pl->UF;
+      void* args[] = {&c, &u0, &slots, &st, &uf};
+      CU(cudaLaunchCooperativeKernel((void*)gap_dykstra_coop_kernel, dim3(gblk), dim3(256), args, dsm, pl->stream));
+    } else {
+      const int gblk = std::max(1, std::min((E + 7) / 8, pl->sm_count * 8));
+      gap_dykstra_pass_kernel<<<gblk, 256, dsm, pl->stream>>>(c, pl->UAVG, pl->DYK, 1, pl->UF);
+      CU(cudaGetLastError());
+      gap_dykstra_pass_kernel<<<gblk, 256, dsm, pl->stream>>>(c, pl->UAVG, pl->DYK, 2, pl->UF);
+      CU(cudaGetLastError());
+      pl->launches += 1;
+    }
   }
   gap_ub_kernel<<<G, 256, 0, pl->stream>>>(c, pl->UF, pl->UB);
   CU(cudaGetLastError());

@@ -154,3 +154,20 @@ def test_residual_stopping_matches_fixed_iteration_solve(name):
     assert a["gap"] == b["gap"]
     never = plan.solve(c.p, n, c.lam, theta=th, coef=cf, tol=1e-300)
     assert never["iterations"] == n
+
+
+@pytest.mark.parametrize("tree_name", ["SMPC1", "SMPC3"])
+def test_lockstep_dykstra_gap_equals_two_pass(tree_name, monkeypatch):
+    """The cooperative lockstep Dykstra (default) runs the same per-edge sweeps
+    and stops at the same global sweep as the two-pass form: bitwise-equal gap."""
+    import bench
+    W = bench.build_workload(tree_name)
+    th, cf = engine.theta_schedule(120)
+    gaps = []
+    for two_pass in (False, True):
+        if two_pass:
+            monkeypatch.setenv("TSMPC_DYKSTRA_TWO_PASS", "1")
+        plan = DevicePlan(W["model"], W["tree"], W["factor"], W["scaling"])
+        plan.set_cache(W["caches"][0], W["model"])
+        gaps.append(plan.solve(W["p"], 120, 0.05, theta=th, coef=cf, keep_device=True)["gap"])
+    assert np.isfinite(gaps[0]) and gaps[0] == gaps[1]
