@@ -563,6 +563,120 @@ __global__ void __launch_bounds__(256) gap_dykstra_coop_kernel(EdgeCtx c, const 
   }
 }
 
+// The lockstep Dykstra above with one thread per (edge, junction row): when the
+// junction rows touch disjoint flows, the projection onto {E u = d} splits into
+// independent rows, so a thread keeps its row's flows, Dykstra increments and
+// block-start state in registers.  Per element the operations and their order
+// are those of the warp kernels (row dot in ascending flow order, fma(r, p, 0)),
+// so the result is bitwise the same.  Flows no junction touches settle after one
+// sweep at clip(x0) (projection = identity) and only feed the sweep-0 maximum.
+__global__ void __launch_bounds__(256) gap_dykstra_comp_kernel(EdgeCtx c, const DykComp* __restrict__ comps,
+                                                                  int ncomp, const int* __restrict__ free_u,
+                                                                  int nfree, const double* __restrict__ u0,
+                                                                  unsigned long long* slots, double* uf) {
+  cg::grid_group grid = cg::this_grid();
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  {
+    double m0 = 0.0;
+    for (int i = tid; i < c.E * nfree; i += nth) {
+      const int e = i / nfree, j = free_u[i - e * nfree];
+      const double x0 = u0[(size_t)e * c.NUP + j];
+      const double t = (x0 - 0.0) + 0.0;
+      const double xn = clip(t, c.u_min[j], c.u_max[j]);
+      m0 = fmax(m0, fabs(xn - x0));
+      uf[(size_t)e * c.NUP + j] = xn - 0.0;
+    }
+    m0 = warp_max(m0);
+    if (lane == 0 && m0 > 0.0) atomicMax(slots, (unsigned long long)__double_as_longlong(m0));
+  }
+  const bool active = tid < c.E * ncomp;
+  int e = 0, n = 0, emask = 0, pmask = 0;
+  double x[kDykCU], inc[kDykCU], lo[kDykCU], hi[kDykCU], ce[kDykCU], cp[kDykCU], xs[kDykCU], is[kDykCU];
+  int ui[kDykCU];
+  double tg = 0.0;
+  if (active) {
+    e = tid / ncomp;
+    const DykComp& q = comps[tid - e * ncomp];
+    n = q.n;
+    emask = q.emask;
+    pmask = q.pmask;
+    tg = c.jrhs[(size_t)e * c.ne + q.row];
+#pragma unroll
+    for (int i = 0; i < kDykCU; ++i) {
+      ui[i] = i < n ? q.u[i] : 0;
+      ce[i] = q.e[i];
+      cp[i] = q.p[i];
+      x[i] = i < n ? u0[(size_t)e * c.NUP + ui[i]] : 0.0;
+      lo[i] = c.u_min[ui[i]];
+      hi[i] = c.u_max[ui[i]];
+      inc[i] = 0.0;
+    }
+  }
+  auto project_row = [&](double* y) {
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < kDykCU; ++i)
+      if (i < n && (emask >> i & 1)) s = fma(x[i], ce[i], s);
+    const double rr = s - tg;
+#pragma unroll
+    for (int i = 0; i < kDykCU; ++i) y[i] = x[i] - ((pmask >> i & 1) ? fma(rr, cp[i], 0.0) : 0.0);
+  };
+  auto sweep = [&]() -> double {
+    double y[kDykCU], mx = 0.0;
+    project_row(y);
+#pragma unroll
+    for (int i = 0; i < kDykCU; ++i)
+      if (i < n) {
+        const double t = y[i] + inc[i];
+        const double xn = clip(t, lo[i], hi[i]);
+        inc[i] = t - xn;
+        mx = fmax(mx, fabs(xn - x[i]));
+        x[i] = xn;
+      }
+    return mx;
+  };
+  int K = -1, blk0 = 0;
+  for (int blk = 0; blk < kDykMax; blk += kDykBlk) {
+#pragma unroll
+    for (int i = 0; i < kDykCU; ++i) {
+      xs[i] = x[i];
+      is[i] = inc[i];
+    }
+    double mxs[kDykBlk];
+#pragma unroll
+    for (int s = 0; s < kDykBlk; ++s) mxs[s] = (active && blk + s < kDykMax) ? sweep() : 0.0;
+#pragma unroll
+    for (int s = 0; s < kDykBlk; ++s) {
+      const double m = warp_max(mxs[s]);
+      if (lane == 0 && m > 0.0 && blk + s < kDykMax)
+        atomicMax(slots + blk + s, (unsigned long long)__double_as_longlong(m));
+    }
+    grid.sync();
+    const int it1 = min(blk + kDykBlk, kDykMax);
+    for (int it = blk; it < it1; ++it) {
+      const double g = __longlong_as_double((long long)*((volatile unsigned long long*)(slots + it)));
+      if (g < 1e-13) { K = it; break; }
+    }
+    if (K >= 0) { blk0 = blk; break; }
+  }
+  if (!active) return;
+  if (K >= 0) {  // restart K's block, stop after sweep K
+#pragma unroll
+    for (int i = 0; i < kDykCU; ++i) {
+      x[i] = xs[i];
+      inc[i] = is[i];
+    }
+#pragma unroll 1
+    for (int s = 0; s < K + 1 - blk0; ++s) (void)sweep();
+  }
+  double y[kDykCU];
+  project_row(y);
+#pragma unroll
+  for (int i = 0; i < kDykCU; ++i)
+    if (i < n) uf[(size_t)e * c.NUP + ui[i]] = y[i];
+}
+
 // ub_e = u_feas_e B'   (E x NXP)
 __global__ void gap_ub_kernel(EdgeCtx c, const double* __restrict__ uf, double* ub) {
   __shared__ double shm[8][128];

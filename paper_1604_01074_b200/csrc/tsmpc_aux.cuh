@@ -55,6 +55,20 @@ __global__ void gap_project_dykstra_kernel(EdgeCtx c, double* xit, double* inc, 
                                            unsigned long long* slots);
 __global__ void gap_dykstra_pass_kernel(EdgeCtx c, const double* __restrict__ u0,
                                         unsigned long long* slots, int pass, double* uf);
+// One junction row of the gap's Dykstra projection with the flows it touches
+// (E row k and the E_pinv^T entries of row k), when the junction rows have
+// disjoint flow supports (gap_dykstra_comp_kernel).
+constexpr int kDykCU = 4;
+struct DykComp {
+  int n, row, emask, pmask;  // flows, junction row, which E / E_pinv^T entries exist
+  int u[kDykCU];             // flow indices, ascending
+  double e[kDykCU];          // E[row, u[i]]
+  double p[kDykCU];          // E_pinv^T[row, u[i]]
+};
+__global__ void gap_dykstra_comp_kernel(EdgeCtx c, const DykComp* __restrict__ comps, int ncomp,
+                                        const int* __restrict__ free_u, int nfree,
+                                        const double* __restrict__ u0, unsigned long long* slots,
+                                        double* uf);
 __global__ void gap_dykstra_coop_kernel(EdgeCtx c, const double* __restrict__ u0,
                                         unsigned long long* slots, double* st, double* uf);
 __global__ void gap_ub_kernel(EdgeCtx c, const double* uf, double* ub);

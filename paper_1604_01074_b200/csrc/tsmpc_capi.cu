@@ -100,6 +100,10 @@ struct tsmpc_plan {
   void* comm = nullptr;
   double* HS = nullptr;
   double* DYKST = nullptr;  // lockstep Dykstra state (2 x E x [x | inc])
+  DykComp* DYKC = nullptr;  // per-junction-row components (disjoint flow supports)
+  int* DYKF = nullptr;      // flows no junction touches
+  int dyk_ncomp = -1, dyk_nfree = 0;  // dyk_ncomp < 0: components not usable
+  bool dyk_warp = std::getenv("TSMPC_DYKSTRA_WARP") != nullptr;
   bool dyk_two_pass = std::getenv("TSMPC_DYKSTRA_TWO_PASS") != nullptr;
   std::vector<int> owned_edges, trunk_edges;
   // plan stats
@@ -812,6 +816,48 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
     if (rc) return bail(0);
     c.er_ptr = d_erp; c.er_idx = d_eri; c.er_val = d_erv; c.er_nnz = (int)eri.size();
     c.pc_ptr = d_pcp; c.pc_idx = d_pci; c.pc_val = d_pcv; c.pc_nnz = (int)pci.size();
+    // junction rows with disjoint flow supports -> one Dykstra component per row
+    std::vector<int> owner(nu, -1);
+    bool disjoint = ne > 0;
+    for (int k = 0; k < ne && disjoint; ++k)
+      for (int j = 0; j < nu; ++j)
+        if (pb->E[(size_t)k * nu + j] != 0.0 || pb->E_pinvT[(size_t)k * nu + j] != 0.0) {
+          if (owner[j] >= 0 && owner[j] != k) disjoint = false;
+          owner[j] = k;
+        }
+    std::vector<DykComp> comps;
+    std::vector<int> freeu;
+    for (int k = 0; k < ne && disjoint; ++k) {
+      DykComp q{};
+      q.row = k;
+      for (int j = 0; j < nu; ++j) {
+        if (owner[j] != k) continue;
+        if (q.n == kDykCU) { disjoint = false; break; }
+        q.u[q.n] = j;
+        q.e[q.n] = pb->E[(size_t)k * nu + j];
+        q.p[q.n] = pb->E_pinvT[(size_t)k * nu + j];
+        if (q.e[q.n] != 0.0) q.emask |= 1 << q.n;
+        if (q.p[q.n] != 0.0) q.pmask |= 1 << q.n;
+        ++q.n;
+      }
+      if (q.n > 0) comps.push_back(q);
+    }
+    for (int j = 0; j < nu; ++j)
+      if (owner[j] < 0) freeu.push_back(j);
+    if (disjoint && !comps.empty()) {
+      const int nfree = (int)freeu.size();
+      if (freeu.empty()) freeu.push_back(0);  // keep the device array non-empty
+      rc |= pl->alloc(&pl->DYKC, comps.size());
+      rc |= pl->upload(&pl->DYKF, freeu.data(), freeu.size());
+      if (rc) return bail(0);
+      if (cudaMemcpyAsync(pl->DYKC, comps.data(), sizeof(DykComp) * comps.size(), cudaMemcpyHostToDevice,
+                          pl->stream) != cudaSuccess) {
+        fail(TSMPC_ERR_CUDA, "upload of the Dykstra components failed");
+        return bail(0);
+      }
+      pl->dyk_ncomp = (int)comps.size();
+      pl->dyk_nfree = nfree;
+    }
   }
 
   int occ_d = 0;
@@ -1110,9 +1156,23 @@ static int compute_gap(tsmpc_plan* pl, const double* yfinal, double* gap) {
     CU(cudaMemsetAsync(pl->DYK, 0, sizeof(unsigned long long) * 256, pl->stream));
     const size_t dsm = sizeof(double) * ((size_t)c.er_nnz + c.pc_nnz + 1 + 8 * 448) +
                        sizeof(int) * ((size_t)pl->ne + 1 + c.er_nnz + pl->nu + 1 + c.pc_nnz);
-    // lockstep cooperative Dykstra when its grid is co-resident, else two passes
-    int occ = 0;
-    if (!pl->dyk_two_pass &&
+    // lockstep cooperative Dykstra when its grid is co-resident: a thread per (edge,
+    // junction row) when the rows have disjoint flows, else a warp per edge; else
+    // the two-pass form
+    int occ = 0, occ_c = 0;
+    if (!pl->dyk_two_pass && !pl->dyk_warp && pl->dyk_ncomp > 0 &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, gap_dykstra_comp_kernel, 256, 0) == cudaSuccess &&
+        (long long)E * pl->dyk_ncomp <= (long long)occ_c * pl->sm_count * 256) {
+      const int gblk = std::max(1, (int)(((long long)E * pl->dyk_ncomp + 255) / 256));
+      const DykComp* comps = pl->DYKC;
+      int ncomp = pl->dyk_ncomp, nfree = pl->dyk_nfree;
+      const int* freeu = pl->DYKF;
+      double* u0 = pl->UAVG;
+      unsigned long long* slots = pl->DYK;
+      double* uf = pl->UF;
+      void* args[] = {&c, &comps, &ncomp, &freeu, &nfree, &u0, &slots, &uf};
+      CU(cudaLaunchCooperativeKernel((void*)gap_dykstra_comp_kernel, dim3(gblk), dim3(256), args, 0, pl->stream));
+    } else if (!pl->dyk_two_pass &&
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gap_dykstra_coop_kernel, 256, dsm) == cudaSuccess &&
         occ > 0) {
       if (!pl->DYKST && pl->alloc(&pl->DYKST, 4 * (size_t)E * pl->NUP)) return TSMPC_ERR_CUDA;
@@ -1123,6 +1183,18 @@ static int compute_gap(tsmpc_plan* pl, const double* yfinal, double* gap) {
       double* uf = pl->UF;
       void* args[] = {&c, &u0, &slots, &st, &uf};
       CU(cudaLaunchCooperativeKernel((void*)gap_dykstra_coop_kernel, dim3(gblk), dim3(256), args, dsm, pl->stream));
+      if (std::getenv("TSMPC_DEBUG_DYKSTRA")) {
+        std::vector<unsigned long long> sl(200);
+        CU(cudaMemcpyAsync(sl.data(), pl->DYK, sizeof(unsigned long long) * 200, cudaMemcpyDeviceToHost, pl->stream));
+        CU(cudaStreamSynchronize(pl->stream));
+        int K = -1;
+        for (int it = 0; it < 200 && K < 0; ++it) {
+          double g;
+          std::memcpy(&g, &sl[it], sizeof g);
+          if (g < 1e-13) K = it;
+        }
+        std::fprintf(stderr, "[tsmpc] dykstra: grid %d x 256 (occupancy %d/SM), stopping sweep K = %d\n", gblk, occ, K);
+      }
     } else {
       const int gblk = std::max(1, std::min((E + 7) / 8, pl->sm_count * 8));
       gap_dykstra_pass_kernel<<<gblk, 256, dsm, pl->stream>>>(c, pl->UAVG, pl->DYK, 1, pl->UF);

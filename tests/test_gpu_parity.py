@@ -158,16 +158,18 @@ def test_residual_stopping_matches_fixed_iteration_solve(name):
 
 @pytest.mark.parametrize("tree_name", ["SMPC1", "SMPC3"])
 def test_lockstep_dykstra_gap_equals_two_pass(tree_name, monkeypatch):
-    """The cooperative lockstep Dykstra (default) runs the same per-edge sweeps
-    and stops at the same global sweep as the two-pass form: bitwise-equal gap."""
+    """The cooperative lockstep Dykstra forms (a thread per junction row, a warp
+    per edge) run the same per-element sweeps and stop at the same global sweep
+    as the two-pass form: bitwise-equal gap."""
     import bench
     W = bench.build_workload(tree_name)
     th, cf = engine.theta_schedule(120)
     gaps = []
-    for two_pass in (False, True):
-        if two_pass:
-            monkeypatch.setenv("TSMPC_DYKSTRA_TWO_PASS", "1")
+    # per-junction threads (default for bcn63), warp per edge, two passes
+    for env in (None, "TSMPC_DYKSTRA_WARP", "TSMPC_DYKSTRA_TWO_PASS"):
+        if env:
+            monkeypatch.setenv(env, "1")
         plan = DevicePlan(W["model"], W["tree"], W["factor"], W["scaling"])
         plan.set_cache(W["caches"][0], W["model"])
         gaps.append(plan.solve(W["p"], 120, 0.05, theta=th, coef=cf, keep_device=True)["gap"])
-    assert np.isfinite(gaps[0]) and gaps[0] == gaps[1]
+    assert np.isfinite(gaps[0]) and gaps[0] == gaps[1] == gaps[2], gaps
