@@ -458,6 +458,7 @@ __global__ void __launch_bounds__(256) gap_dykstra_coop_kernel(EdgeCtx c, const 
                                                                double* uf) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double dsm[];
+  __shared__ double wmax[8][kDykBlk];
   double* ev = dsm;
   double* pv = ev + c.er_nnz;
   double* wsm = pv + c.pc_nnz + (c.pc_nnz + c.er_nnz & 1);
@@ -508,15 +509,17 @@ __global__ void __launch_bounds__(256) gap_dykstra_coop_kernel(EdgeCtx c, const 
         x[j] = xn;
       }
       __syncwarp();
-      if (record) {
+      if (record) {  // per-warp maxima over its edges; reduced per CTA below
         mx = warp_max(mx);
-        if (lane == 0 && mx > 0.0) atomicMax(slots + it, (unsigned long long)__double_as_longlong(mx));
+        if (lane == 0) wmax[wl][it - it0] = fmax(wmax[wl][it - it0], mx);
       }
     }
   };
   int K = -1, blk0 = 0;
   for (int blk = 0; blk < kDykMax; blk += kDykBlk) {
     const int it1 = min(blk + kDykBlk, kDykMax);
+    if (lane < kDykBlk) wmax[wl][lane] = 0.0;
+    __syncwarp();
     for (int e = gw; e < c.E; e += nw) {
       const double* sa = SA + (size_t)e * SW;
       for (int j = lane; j < c.nu; j += 32) {
@@ -537,6 +540,14 @@ __global__ void __launch_bounds__(256) gap_dykstra_coop_kernel(EdgeCtx c, const 
         }
       }
       __syncwarp();
+    }
+    // one global atomic per CTA and sweep (same-address global atomics from every
+    // warp serialise in L2)
+    __syncthreads();
+    if (threadIdx.x < it1 - blk) {
+      double m = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, wmax[w][threadIdx.x]);
+      if (m > 0.0) atomicMax(slots + blk + threadIdx.x, (unsigned long long)__double_as_longlong(m));
     }
     grid.sync();
     for (int it = blk; it < it1; ++it) {
@@ -575,6 +586,7 @@ __global__ void __launch_bounds__(256) gap_dykstra_comp_kernel(EdgeCtx c, const 
                                                                   int nfree, const double* __restrict__ u0,
                                                                   unsigned long long* slots, double* uf) {
   cg::grid_group grid = cg::this_grid();
+  __shared__ unsigned long long cta_max[kDykBlk];
   const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
   const int lane = threadIdx.x & 31;
   {
@@ -646,12 +658,18 @@ __global__ void __launch_bounds__(256) gap_dykstra_comp_kernel(EdgeCtx c, const 
     double mxs[kDykBlk];
 #pragma unroll
     for (int s = 0; s < kDykBlk; ++s) mxs[s] = (active && blk + s < kDykMax) ? sweep() : 0.0;
+    // per-sweep maxima: warp, then CTA (shared atomics), then one global atomic
+    // per CTA and sweep (thousands of same-address global atomics serialise in L2)
+    if (threadIdx.x < kDykBlk) cta_max[threadIdx.x] = 0ull;
+    __syncthreads();
 #pragma unroll
     for (int s = 0; s < kDykBlk; ++s) {
       const double m = warp_max(mxs[s]);
-      if (lane == 0 && m > 0.0 && blk + s < kDykMax)
-        atomicMax(slots + blk + s, (unsigned long long)__double_as_longlong(m));
+      if (lane == 0 && m > 0.0) atomicMax(cta_max + s, (unsigned long long)__double_as_longlong(m));
     }
+    __syncthreads();
+    if (threadIdx.x < kDykBlk && blk + threadIdx.x < kDykMax && cta_max[threadIdx.x] != 0ull)
+      atomicMax(slots + blk + threadIdx.x, cta_max[threadIdx.x]);
     grid.sync();
     const int it1 = min(blk + kDykBlk, kDykMax);
     for (int it = blk; it < it1; ++it) {
