@@ -711,8 +711,11 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
     else {
       SparseTreeIn ti{N, n_nodes, pb->stage_starts, pb->anc, pb->child_start, pb->child_stop, pb->prob};
       SparseOpsIn oi{nx, nu, nv, pb->B, pb->Ls, pb->lam_s};
-      SparseHostPlan hp = plan_sparse(ti, oi, NXP, NUP, NVP, pl->sm_count, (size_t)prop.sharedMemPerBlockOptin,
-                                      shard, shard ? srank : 0, shard ? sworld : 1);
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, apg_sparse_kernel);  // static shared memory counts against the opt-in limit
+      SparseHostPlan hp = plan_sparse(ti, oi, NXP, NUP, NVP, pl->sm_count,
+                                      (size_t)prop.sharedMemPerBlockOptin - fa.sharedSizeBytes, shard,
+                                      shard ? srank : 0, shard ? sworld : 1);
       int occ_s = 0;
       if (hp.ok) {
         if (cudaFuncSetAttribute(apg_sparse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hp.smem) !=

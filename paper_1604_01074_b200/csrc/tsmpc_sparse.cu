@@ -1222,11 +1222,20 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
       for (int t = 0; t < nt; ++t)
         fwd_tile(t, nu, cf, th, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur, &rmax);
       if (nu == P.iters - 1 || P.record_all || is_check(P, nu)) {
+        // warp, then CTA, then one global atomic per CTA (same-address global
+        // atomics from every warp serialise in L2)
+        __shared__ double s_rmax[kThreadsS / 32];
         for (int off = 16; off > 0; off >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, off));
-        if ((threadIdx.x & 31) == 0 && rmax > 0.0) {
-          const unsigned long long b = (unsigned long long)__double_as_longlong(rmax);
-          if (nu == P.iters - 1 || P.record_all) atomicMax(P.resid + (P.record_all ? nu : 0), b);
-          if (is_check(P, nu)) atomicMax(P.resid_chk + nu / P.check_every, b);
+        if ((threadIdx.x & 31) == 0) s_rmax[threadIdx.x >> 5] = rmax;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          double m = 0.0;
+          for (int w = 0; w < kThreadsS / 32; ++w) m = fmax(m, s_rmax[w]);
+          if (m > 0.0) {
+            const unsigned long long b = (unsigned long long)__double_as_longlong(m);
+            if (nu == P.iters - 1 || P.record_all) atomicMax(P.resid + (P.record_all ? nu : 0), b);
+            if (is_check(P, nu)) atomicMax(P.resid_chk + nu / P.check_every, b);
+          }
         }
         rmax = 0.0;
       }
