@@ -99,6 +99,8 @@ struct tsmpc_plan {
   const NcclApi* nccl = nullptr;
   void* comm = nullptr;
   double* HS = nullptr;
+  double* TR = nullptr;            // split mode: [du | B du | x] per trunk position
+  unsigned int* SUBCTR = nullptr;  // split mode: trunk-CTA barrier counter
   double* DYKST = nullptr;  // lockstep Dykstra state (2 x E x [x | inc])
   DykComp* DYKC = nullptr;  // per-junction-row components (disjoint flow supports)
   int* DYKF = nullptr;      // flows no junction touches
@@ -687,6 +689,7 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
   P.xavg = pl->XAVG; P.uavg = pl->UAVG; P.X = pl->X; P.U = pl->U; P.T = pl->T;
   P.XIQG = pl->XIQG; P.GG = pl->GG; P.p = pl->P;
   P.timers = pl->TIMERS;
+  P.timer_cta = std::getenv("TSMPC_TIMER_CTA") ? std::atoi(std::getenv("TSMPC_TIMER_CTA")) : 0;
 
   pl->d_est_c = d_est; pl->d_anc_c = d_anc; pl->d_cs_c = d_cs; pl->d_ce_c = d_ce;
   pl->d_pe_c = d_pe; pl->d_B_c = d_B;
@@ -746,6 +749,13 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
         S.spi = d_spi; S.spv = d_spv; S.meta = d_meta; S.meta_ptr = d_mptr; S.tsched = d_ts;
         S.beta_s = pl->BETA_S; S.TG = pl->TG;
         S.HS_LD = NVP + NXP;
+        if (S.split) {
+          rc |= pl->alloc(&pl->TR, (size_t)std::max(1, hp.n_trunk) * S.TR_LD);
+          rc |= pl->alloc(&pl->SUBCTR, 1);
+          if (rc) return bail(0);
+          S.TR = pl->TR;
+          S.sub_ctr = pl->SUBCTR;
+        }
         if (shard) {
           unsigned char* d_tow;
           rc |= pl->upload(&d_tow, hp.towned.data(), std::max<size_t>(1, hp.towned.size()));
@@ -1423,6 +1433,7 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
       S.nu0 = 0;
       S.nu1 = iters;
       S.phase = 3;
+      if (pl->SUBCTR) CU(cudaMemsetAsync(pl->SUBCTR, 0, sizeof(unsigned int), pl->stream));
       CU(sparse_launch(S, pl->sp_ctas, pl->sp_smem, pl->stream));
       ++pl->launches;
     } else {

@@ -99,7 +99,8 @@ struct Params {
   int check_every;
   unsigned long long* resid_chk;
   int* iters_done;
-  unsigned long long* timers;   // phase cycle counters of CTA 0 (TSMPC_TIMERS builds only)
+  unsigned long long* timers;   // phase cycle counters of CTA timer_cta (TSMPC_TIMERS builds only)
+  int timer_cta;
 };
 
 // ---------------------------------------------------------------------------
@@ -116,6 +117,7 @@ struct Params {
 constexpr int kThreadsS = 512;
 constexpr int kWarpsS = kThreadsS / 32;
 constexpr int kTileS = 24;         // rows per chain tile (a leaf chain never spans tiles)
+constexpr int kMinTrunkCtas = 8;   // split mode needs at least this many spare CTAs for the trunk
 
 struct SParams {
   Params P;                     // dims, model vectors, scaling, tree, state, loop control, KY
@@ -160,6 +162,15 @@ struct SParams {
   double* HS;                   // T x HS_LD
   int HS_LD;                    // NVP + NXP
   const unsigned char* towned;  // T: this rank owns the heads of the node below
+  // split mode (single GPU, one tile per chain CTA, spare CTAs): CTAs >= split_c0
+  // ("trunk CTAs") run the trunk sweep, then -- after a barrier among themselves --
+  // the trunk forward of their trunk rows, exporting per trunk position
+  // [du | B du | x] to TR; meanwhile the chain CTAs run their chains' forward with
+  // zero trunk input, then add the affine trunk terms from TR after the grid barrier.
+  int split, split_c0, split_n;
+  double* TR;                   // T x TR_LD
+  int TR_LD;                    // NUP + 2 NXP
+  unsigned int* sub_ctr;        // arrival counter of the trunk-CTA barrier (zeroed per launch)
 };
 
 // Phase timers (profiling builds: -DTSMPC_TIMERS).  Slot k accumulates the cycles
@@ -168,7 +179,7 @@ struct SParams {
 #define TSMPC_MARK(P, k, t)                                                   \
   do {                                                                        \
     __syncthreads();                                                          \
-    if (blockIdx.x == 0 && threadIdx.x == 0 && (P).timers) {                  \
+    if (blockIdx.x == (P).timer_cta && threadIdx.x == 0 && (P).timers) {      \
       const long long now_ = clock64();                                       \
       atomicAdd((P).timers + (k), (unsigned long long)(now_ - (t)));          \
       (t) = now_;                                                             \

@@ -616,7 +616,7 @@ __device__ __noinline__ void fwd_tile(int ti, int nu_it, double cf, double th, i
     double* scol = RA + lo * LA + kk;
     const double* tcol = tmode == 1 ? slot_row(c, srow0 + lo) + 2 * c.YW + c.NXP + c.NUP + kk : scol;
     const int tld = tmode == 1 ? c.SL : LA;
-    double Sv = pn >= 0 ? c.need[(size_t)pn * S.need_ld + kk] : 0.0;
+    double Sv = pn >= 0 && !S.split ? c.need[(size_t)pn * S.need_ld + kk] : 0.0;  // split: added later
 #pragma unroll 1
     for (int j0 = 0; j0 < n; j0 += kCh) {
       double v[kCh];
@@ -666,7 +666,8 @@ __device__ __noinline__ void fwd_tile(int ti, int nu_it, double cf, double th, i
     }
   }
   // the thread reads back only its own u entries: no barrier needed
-  epi_psi_rows(nu_it, cf, th, nrows, ysm, !resident || nu_it == P.iters - 1 || is_check(P, nu_it), cur ^ 1, rmax);
+  if (!S.split)
+    epi_psi_rows(nu_it, cf, th, nrows, ysm, !resident || nu_it == P.iters - 1 || is_check(P, nu_it), cur ^ 1, rmax);
   {
     const double* adiag = c.adiag();
     const double* pr = c.proot();
@@ -676,7 +677,7 @@ __device__ __noinline__ void fwd_tile(int ti, int nu_it, double cf, double th, i
       const int* sg = c.mt.segs + 4 * (seg0 + s);
       const int lo = sg[0], n = sg[1] - lo, pn = sg[2];
       double* col = RA + lo * LA + i;
-      double x = pn >= 0 ? c.need[(size_t)pn * S.need_ld + c.NVP + i] : pr[i];
+      double x = pn >= 0 ? (S.split ? 0.0 : c.need[(size_t)pn * S.need_ld + c.NVP + i]) : pr[i];
       const double a = adiag[i];
 #pragma unroll 1
       for (int j0 = 0; j0 < n; j0 += kCh) {
@@ -694,6 +695,7 @@ __device__ __noinline__ void fwd_tile(int ti, int nu_it, double cf, double th, i
   }
   __syncthreads();
   TSMPC_MARK(P, 7, tm_);
+  if (S.split) return;  // trunk terms and epilogue: fwd_finish, after the grid barrier
   // (5) epilogue, state blocks (warp per row)
   epi_state(nu_it, cf, th, nrows, ysm, !resident || nu_it == P.iters - 1 || is_check(P, nu_it), cur ^ 1, rmax);
   __syncthreads();
@@ -701,6 +703,81 @@ __device__ __noinline__ void fwd_tile(int ti, int nu_it, double cf, double th, i
 }
 
 // ----------------------------------------------------------------------------
+// ----------------------------------------------------------------------------
+// split mode, after the grid barrier: the chain's forward ran with zero trunk
+// input; S, du, bv, x are affine in the trunk parent's values, so
+//   u_e += du_tp                                   (du = Lt S, S_e = S_tp + local)
+//   x_e += G_d .* (B du_tp) + a^(d+1) .* x_tp       (d = depth below the head,
+//                                                    G_d = 1 + a + ... + a^d)
+// with [du_tp | B du_tp | x_tp] read from TR.  Then the prox / dual epilogue.
+// ----------------------------------------------------------------------------
+__device__ __noinline__ void fwd_finish(int ti, int nu_it, double cf, double th, int ysm, bool resident, int cur,
+                                        double* rmax) {
+  const SParams& S = g_sp;
+  const Ctx c = ctx_of();
+  const Params& P = S.P;
+  const int* td = c.mt.tiles + 4 * ti;
+  const int nrows = td[1], seg0 = td[2], nsegs = td[3];
+  const int tid = threadIdx.x, k = tid & (kKW - 1), g = tid / kKW;
+  const int nx = c.nx, nu = c.nu, LA = c.LA;
+  double* RA = c.A();
+  double* RB = c.B();
+  long long tm_ = clock64();
+  (void)tm_;
+  const bool last = nu_it == P.iters - 1 || is_check(P, nu_it);
+  // one chain per tile in split mode
+  const int pn = c.mt.segs[4 * seg0 + 2];
+  if (pn >= 0 && k < nu) {
+    const double d = ldcg(S.TR + (size_t)pn * S.TR_LD + k);
+#pragma unroll
+    for (int m = 0; m < kRowsPT; ++m) {
+      const int r = g + kGroups * m;
+      if (r < nrows) RB[r * c.NUP + k] = __dadd_rn(RB[r * c.NUP + k], d);
+    }
+  }
+  // the thread reads back only its own u entries: no barrier needed
+  epi_psi_rows(nu_it, cf, th, nrows, ysm, !resident || last, cur ^ 1, rmax);
+  TSMPC_MARK(P, 13, tm_);
+  if (pn >= 0) {
+    const double* adiag = c.adiag();
+#pragma unroll 1
+    for (int idx = tid; idx < nsegs * nx; idx += kThreadsS) {
+      const int s = idx / nx, i = idx - s * nx;
+      const int* sg = c.mt.segs + 4 * (seg0 + s);
+      const int lo = sg[0], n = sg[1] - lo;
+      const double* tr = S.TR + (size_t)sg[2] * S.TR_LD;
+      const double bt = ldcg(tr + c.NUP + i), xt = ldcg(tr + c.NUP + c.NXP + i);
+      const double a = adiag[i];
+      double* col = RA + lo * LA + i;
+      double gs = 1.0, pw = a;
+#pragma unroll 4
+      for (int j = 0; j < n; ++j) {
+        col[j * LA] = __dadd_rn(col[j * LA], __dadd_rn(__dmul_rn(gs, bt), __dmul_rn(pw, xt)));
+        gs = __dadd_rn(__dmul_rn(gs, a), 1.0);
+        pw = __dmul_rn(pw, a);
+      }
+    }
+  }
+  __syncthreads();
+  TSMPC_MARK(P, 14, tm_);
+  epi_state(nu_it, cf, th, nrows, ysm, !resident || last, cur ^ 1, rmax);
+  __syncthreads();
+  TSMPC_MARK(P, 8, tm_);
+}
+
+// barrier among the trunk CTAs of split mode (arrival counter zeroed per launch)
+__device__ __forceinline__ void trunk_barrier(unsigned int* ctr, unsigned int n, unsigned int& target) {
+  __syncthreads();
+  target += n;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    while (*((volatile unsigned int*)ctr) < target) __nanosleep(32);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 // phase B: component-sliced trunk sweep -> KY (see tsmpc_apg.cu trunk_sweep_smem
 // for the recursion; here the schedule is staged in shared memory first)
 // ----------------------------------------------------------------------------
@@ -709,8 +786,11 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
   const Ctx c = ctx_of();
   const Params& P = S.P;
   const int ncomp = c.nv + c.nx + c.nu;
-  const int c_lo = (int)((long long)ncomp * blockIdx.x / gridDim.x);
-  const int c_hi = (int)((long long)ncomp * (blockIdx.x + 1) / gridDim.x);
+  // component slice of this CTA (split mode: among the trunk CTAs)
+  const int si = S.split ? (int)blockIdx.x - S.split_c0 : (int)blockIdx.x;
+  const int ns = S.split ? S.split_n : (int)gridDim.x;
+  const int c_lo = (int)((long long)ncomp * si / ns);
+  const int c_hi = (int)((long long)ncomp * (si + 1) / ns);
   const int nc = c_hi - c_lo;
   if (nc <= 0) return;
   const int* g = S.tsched;
@@ -1002,6 +1082,7 @@ __device__ __noinline__ void trunk_needs() {
 #pragma unroll 1
       for (int q = rp[j]; q < rp[j + 1]; ++q) d = fma(rv[q], ND[(size_t)n * LD + ri[q]], d);
       ND[(size_t)n * LD + UO + j] = d;
+      if (S.split) stcg(S.TR + (size_t)nd[4 * n] * S.TR_LD + j, d);  // du of the trunk row
     }
   }
   __syncthreads();
@@ -1016,6 +1097,7 @@ __device__ __noinline__ void trunk_needs() {
       double b = 0.0;
 #pragma unroll 1
       for (int q = rp[i]; q < rp[i + 1]; ++q) b = fma(rv[q], ND[(size_t)n * LD + UO + ri[q]], b);
+      if (S.split) stcg(S.TR + (size_t)nd[4 * n] * S.TR_LD + c.NUP + i, b);  // B du of the trunk row
       ND[(size_t)n * LD + c.NVP + i] = __dadd_rn(b, evec_n(n, i));
     }
     __syncthreads();
@@ -1051,6 +1133,7 @@ __device__ __noinline__ void trunk_needs() {
       for (int idx = threadIdx.x; idx < nn * nx; idx += kThreadsS) {
         const int n = idx / nx, i = idx - n * nx;
         ND[(size_t)n * LD + c.NVP + i] = xo[(size_t)n * SLD + i];
+        if (S.split) stcg(S.TR + (size_t)nd[4 * n] * S.TR_LD + c.NUP + c.NXP + i, xo[(size_t)n * SLD + i]);
       }
       __syncthreads();
     } else {
@@ -1064,6 +1147,7 @@ __device__ __noinline__ void trunk_needs() {
           const double xp = pn >= 0 ? ND[(size_t)pn * LD + c.NVP + i] : c.proot()[i];
           double* xv = ND + (size_t)n * LD + c.NVP + i;
           *xv = __dadd_rn(__dmul_rn(xp, adiag[i]), *xv);
+          if (S.split) stcg(S.TR + (size_t)nd[4 * n] * S.TR_LD + c.NUP + c.NXP + i, *xv);
         }
         __syncthreads();
       }
@@ -1176,6 +1260,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
     __syncthreads();
   }
   double rmax = 0.0;
+  unsigned int sub_target = 0;  // trunk-CTA barrier episodes x split_n (split mode)
   double cf = P.coef[S.nu0], th = P.theta[S.nu0];
   for (int nu = S.nu0; nu < S.nu1; ++nu) {
     const int cur = (P.slot0 + nu) & 1;
@@ -1201,7 +1286,31 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
       }
     }
     if (do_b) {
-      if (trunk) {
+      long long tb_s = 0;
+      (void)tb_s;
+      if (trunk && S.split) {
+        // trunk CTAs: sweep, barrier among themselves, trunk forward (-> TR) and
+        // trunk-row epilogues; chain CTAs meanwhile: forward with zero trunk input
+        long long tb_ = clock64();
+        (void)tb_;
+        grid.sync();
+        TSMPC_MARK(P, 9, tb_);
+        if ((int)blockIdx.x >= S.split_c0) {
+          trunk_sweep(cf, cur);
+          TSMPC_MARK(P, 10, tb_);
+          trunk_barrier(S.sub_ctr, (unsigned)S.split_n, sub_target);
+          TSMPC_MARK(P, 11, tb_);
+          trunk_needs();
+          TSMPC_MARK(P, 12, tb_);
+        } else {
+          for (int t = 0; t < nt; ++t)
+            fwd_tile(t, nu, cf, th, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur, &rmax);
+        }
+        TSMPC_MARK(P, 10, tb_);
+        grid.sync();
+        TSMPC_MARK(P, 9, tb_);
+        tb_s = tb_;
+      } else if (trunk) {
         long long tb_ = clock64();
         (void)tb_;
         if (!S.sharded) grid.sync();
@@ -1219,8 +1328,15 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
         for (int i = threadIdx.x; i < c.nx; i += kThreadsS)
           P.xavg[i] = __dadd_rn(__dmul_rn(P.xavg[i], om), __dmul_rn(th, c.proot()[i]));
       }
-      for (int t = 0; t < nt; ++t)
-        fwd_tile(t, nu, cf, th, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur, &rmax);
+      if (trunk && S.split) {
+        // trunk-row epilogues (trunk CTAs) overlap the chain CTAs' trunk terms + epilogue
+        if ((int)blockIdx.x >= S.split_c0) trunk_own_rows(nu, cf, th, cur, &rmax);
+        for (int t = 0; t < nt; ++t) fwd_finish(t, nu, cf, th, ysm, resident, cur, &rmax);
+        TSMPC_MARK(P, 3, tb_s);
+      } else {
+        for (int t = 0; t < nt; ++t)
+          fwd_tile(t, nu, cf, th, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur, &rmax);
+      }
       if (nu == P.iters - 1 || P.record_all || is_check(P, nu)) {
         // warp, then CTA, then one global atomic per CTA (same-address global
         // atomics from every warp serialise in L2)

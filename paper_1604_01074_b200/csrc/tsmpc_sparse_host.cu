@@ -43,7 +43,8 @@ void csr(int rows, int cols, const std::vector<double>& dense, bool by_col, std:
 }  // namespace
 
 SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NXP, int NUP, int NVP,
-                           int max_ctas, size_t smem_limit, bool sharded, int rank, int world, bool psi_in_smem) {
+                           int max_ctas, size_t smem_limit, bool sharded, int rank, int world, bool psi_in_smem,
+                           bool allow_split) {
   SparseHostPlan out;
   out.rank = rank;
   out.world = world;
@@ -131,13 +132,26 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
   }
   std::sort(out.owned_edges.begin(), out.owned_edges.end());
 
+  // ---- split mode: a CTA per chain, the trunk on split_n further CTAs
+  int split_n = 0;
+  const int ncomp_all = nv + nx + nu;
+  if (allow_split && !sharded && T > 0 && !chains.empty() && !std::getenv("TSMPC_NO_SPLIT")) {
+    const int spare = max_ctas - (int)chains.size();
+    // enough trunk CTAs that one sweep slice (T x components) fits one pass of the CTA
+    const int want = std::max(kMinTrunkCtas, (int)(((long long)ncomp_all * T + 383) / 384));
+    if (spare >= kMinTrunkCtas) split_n = std::min(spare, want);
+  }
+  const int nch_split = split_n ? (int)chains.size() : 0;
   // ---- CTA count and chain assignment (contiguous, balanced by rows)
   long long R = 0;
   for (auto& ch : chains) R += (long long)ch.size();
   int C = T > 0 ? max_ctas : std::max(1, std::min(max_ctas, (int)chains.size()));
   if (T > 0) C = std::max(1, std::min(max_ctas, (int)chains.size() + T));
+  if (split_n) C = nch_split + split_n;
   std::vector<std::vector<int>> cta_chains(C);
-  {
+  if (split_n) {
+    for (int i = 0; i < nch_split; ++i) cta_chains[i].push_back(i);
+  } else {
     long long pre = 0;
     for (int i = 0; i < (int)chains.size(); ++i) {
       const long long mid2 = 2 * pre + (long long)chains[i].size();
@@ -153,7 +167,9 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
   // This keeps each CTA's needs close to its chains' root paths (also on shards,
   // where many trunk edges have no owned chains below them).
   std::vector<std::vector<int>> cta_own(C);
-  {
+  if (split_n) {  // trunk rows round-robin over the trunk CTAs
+    for (int tp = 0; tp < T; ++tp) cta_own[nch_split + tp % split_n].push_back(tp);
+  } else {
     std::vector<long long> load(C, 0);
     std::vector<std::set<int>> need(C);
     for (int c = 0; c < C; ++c)
@@ -253,10 +269,11 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
     auto add_path = [&](int e) {
       for (; e >= 0; e = (int)t.anc[e + 1] - 1) need_set.insert({depth[tpos[e]], tpos[e]});
     };
-    for (int i : cta_chains[c]) {
-      const int pa = (int)t.anc[chains[i][0] + 1] - 1;
-      if (pa >= 0) add_path(pa);
-    }
+    if (!split_n)  // split mode: chain CTAs read their trunk parents from TR
+      for (int i : cta_chains[c]) {
+        const int pa = (int)t.anc[chains[i][0] + 1] - 1;
+        if (pa >= 0) add_path(pa);
+      }
     for (int tp : cta_own[c]) add_path(out.trunk_edge[tp]);
     std::vector<int> need_tp;
     std::map<int, int> need_idx;
@@ -284,7 +301,8 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
       for (int i : tl) {
         const auto& ch = chains[i];
         const int pa = (int)t.anc[ch[0] + 1] - 1;
-        segs.insert(segs.end(), {lo, lo + (int)ch.size(), pa >= 0 ? need_idx[tpos[pa]] : -1, 0});
+        const int pref = pa < 0 ? -1 : (split_n ? tpos[pa] : need_idx[tpos[pa]]);
+        segs.insert(segs.end(), {lo, lo + (int)ch.size(), pref, 0});
         for (int e : ch) {
           const double inv2p = 1.0 / (2.0 * t.prob[e + 1]);
           int w[2];
@@ -443,7 +461,8 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
     bool any_t0 = false;
     for (int c = 0; c < C; ++c) any_t0 |= metas[c][7] == 0;
     const int ncomp = nv + nx + nu;
-    const long long nc_max = (ncomp + C - 1) / C;
+    const int nsl = split_n ? split_n : C;  // CTAs sharing the sweep
+    const long long nc_max = (ncomp + nsl - 1) / nsl;
     const long long regB = (long long)kTileS * NUP;
     const long long cap = any_t0 ? regB : (long long)S.n_work;
     const long long zx = 2LL * T * nc_max + T;  // Zs, Xs, 1/(2p) per trunk edge
@@ -467,6 +486,14 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
   }
   S.O_INT = (int)off;
   off += ints_d;
+  S.split = split_n ? 1 : 0;
+  S.split_c0 = nch_split;
+  S.split_n = split_n;
+  S.TR_LD = NUP + 2 * NXP;
+  if (split_n)  // the chain CTAs keep their one tile resident (else no split)
+    for (int c = 0; c < nch_split; ++c)
+      if (metas[c][6] == 0 || metas[c][0] != 1)
+        return plan_sparse(t, ops, NXP, NUP, NVP, max_ctas, smem_limit, sharded, rank, world, psi_in_smem, false);
   S.meta_max = meta_max;
   out.smem = (size_t)off * sizeof(double);
   out.meta.clear();

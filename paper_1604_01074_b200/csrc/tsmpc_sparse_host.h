@@ -50,8 +50,10 @@ struct SparseHostPlan {
 // sharded: split the leaf chains across `world` ranks by the trunk node they hang
 // from (all chain heads of a node go to one rank), keep this rank's share, stream
 // every tile (state lives in HBM between the two launches of an iteration).
+// allow_split: use split mode (SParams::split) when every chain gets its own CTA
+// and enough CTAs are left for the trunk.
 SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NXP, int NUP, int NVP,
                            int max_ctas, size_t smem_limit, bool sharded = false, int rank = 0,
-                           int world = 1, bool psi_in_smem = true);
+                           int world = 1, bool psi_in_smem = true, bool allow_split = true);
 
 }  // namespace tsmpc
