@@ -200,7 +200,10 @@ int tsmpc_dual_operator_set_ones(tsmpc_plan* plan);
 int tsmpc_dual_operator_step(tsmpc_plan* plan, double* y_dot_dy, double* dy_dot_dy,
                              double* y_dot_y);
 
-/* Introspection (tests / bench). */
+/* Introspection (tests / bench): info = {levels, ctas, tiles, segments,
+ * smem_bytes, diag_A, threads, tile_rows, sms, collapsed, trunk_edges, sparse,
+ * resident_ctas, sharded, rank, world, owned_chain_edges, total_chains,
+ * trunk_ctas}. */
 int tsmpc_plan_info(const tsmpc_plan* plan, int64_t* info, int32_t n_info);
 
 /* Host-only planning (no device needed): the segment / level / tile / trunk
@@ -210,7 +213,8 @@ int tsmpc_plan_info(const tsmpc_plan* plan, int64_t* info, int32_t n_info);
 int tsmpc_describe_tree(const tsmpc_problem* prob, int32_t max_ctas, int32_t collapse,
                         int64_t* info, int32_t n_info);
 /* Host-only planning of the sparse kernel: info = {ctas, tiles, chains,
- * trunk_edges, resident_ctas, max_rows_per_cta, max_needs, smem_bytes}. */
+ * trunk_edges, resident_ctas, max_rows_per_cta, max_needs, smem_bytes,
+ * trunk_ctas (split mode: spare CTAs running the trunk; 0 otherwise)}. */
 int tsmpc_describe_sparse(const tsmpc_problem* prob, int32_t max_ctas, int64_t smem_limit,
                           int64_t* info, int32_t n_info);
 /* Page-locked host memory for result buffers (cudaHostAlloc, portable across

@@ -972,7 +972,7 @@ int tsmpc_describe_sparse(const tsmpc_problem* pb, int32_t max_ctas, int64_t sme
                                   (size_t)smem_limit);
   if (!hp.ok) return fail(TSMPC_ERR_VALIDATION, "%s", hp.why.c_str());
   const int64_t vals[] = {hp.n_ctas, hp.n_tiles, hp.n_chains, hp.n_trunk, hp.resident_ctas, hp.max_rows,
-                          hp.max_needs, (int64_t)hp.smem};
+                          hp.max_needs, (int64_t)hp.smem, hp.S.split_n};
   for (int i = 0; i < n && i < (int)(sizeof(vals) / sizeof(vals[0])); ++i) info[i] = vals[i];
   return TSMPC_OK;
 }
@@ -1005,7 +1005,7 @@ int tsmpc_plan_info(const tsmpc_plan* pl, int64_t* info, int32_t n) {
                           sp ? kThreadsS : kThreads, sp ? kTileS : kTileM, pl->sm_count, pl->base.collapsed,
                           sp ? pl->sp_trunk : pl->n_trunk, sp ? 1 : 0, pl->sp_resident,
                           pl->sharded ? 1 : 0, pl->rank, pl->world, (int64_t)pl->owned_edges.size(),
-                          pl->total_chains};
+                          pl->total_chains, sp ? pl->sbase.split_n : 0};
   for (int i = 0; i < n && i < (int)(sizeof(vals) / sizeof(vals[0])); ++i) info[i] = vals[i];
   return TSMPC_OK;
 }

@@ -88,7 +88,7 @@ class DevicePlan:
     def info(self) -> dict:
         keys = ("levels", "ctas", "tiles", "segments", "smem_bytes", "diag_A", "threads",
                 "tile_rows", "sms", "collapsed", "trunk_edges", "sparse", "resident_ctas",
-                "sharded", "rank", "world", "owned_chain_edges", "total_chains")
+                "sharded", "rank", "world", "owned_chain_edges", "total_chains", "trunk_ctas")
         buf = np.zeros(len(keys), dtype=np.int64)
         nat.check(self._lib.tsmpc_plan_info(self._h, nat.iptr(buf), len(keys)), "tsmpc_plan_info")
         d = dict(zip(keys, (int(v) for v in buf)))
@@ -311,7 +311,7 @@ def describe_sparse(model, tree, factor, max_ctas: int = 148, smem_limit: int = 
     for name, arr in keep.items():
         setattr(pb, name, nat.iptr(arr) if arr.dtype == np.int64 else nat.dptr(arr))
     keys = ("ctas", "tiles", "chains", "trunk_edges", "resident_ctas", "max_rows", "max_needs",
-            "smem_bytes")
+            "smem_bytes", "trunk_ctas")
     buf = np.zeros(len(keys), dtype=np.int64)
     nat.check(lib.tsmpc_describe_sparse(ctypes.byref(pb), int(max_ctas), int(smem_limit),
                                         nat.iptr(buf), len(keys)), "tsmpc_describe_sparse")

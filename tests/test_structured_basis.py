@@ -88,12 +88,16 @@ def test_sparse_planner_paper_trees():
         assert d["chains"] + d["trunk_edges"] <= t.n_edges
         got[name] = d
     assert got["CE"]["ctas"] == 1 and got["CE"]["trunk_edges"] == 0
-    # SMPC3 (configs[1]): one scenario chain per CTA, everything SMEM-resident
+    # SMPC3 (configs[1]): one scenario chain per CTA, everything SMEM-resident;
+    # split mode: the trunk (37 edges) on spare CTAs
     assert got["SMPC3"]["chains"] == 114 and got["SMPC3"]["trunk_edges"] == 37
-    assert got["SMPC3"]["resident_ctas"] == got["SMPC3"]["ctas"] == 148
+    assert got["SMPC3"]["trunk_ctas"] == 27
+    assert got["SMPC3"]["resident_ctas"] == got["SMPC3"]["ctas"] == 114 + 27
+    assert got["SMPC1"]["trunk_ctas"] == 8 and got["SMPC1"]["ctas"] == 6 + 8
     assert got["SMPC3"]["max_rows"] == 21
-    # SMPC8: 3-4 chains per CTA -> streamed tile slots
+    # SMPC8: 3-4 chains per CTA -> streamed tile slots, no split
     assert got["SMPC8"]["chains"] == 493 and got["SMPC8"]["resident_ctas"] == 0
+    assert got["SMPC8"]["trunk_ctas"] == 0 and got["CE"]["trunk_ctas"] == 0
 
 
 def test_sparse_planner_rejects_long_chains():
