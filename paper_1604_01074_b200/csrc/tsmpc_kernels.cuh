@@ -168,6 +168,8 @@ struct SParams {
   // [du | B du | x] to TR; meanwhile the chain CTAs run their chains' forward with
   // zero trunk input, then add the affine trunk terms from TR after the grid barrier.
   int split, split_c0, split_n;
+  int split_local;              // trunk CTAs sweep their own trunk subtrees in shared memory
+                                // (all components; no trunk-CTA barrier, KY stays on chip)
   double* TR;                   // T x TR_LD
   int TR_LD;                    // NUP + 2 NXP
   unsigned int* sub_ctr;        // arrival counter of the trunk-CTA barrier (zeroed per launch)

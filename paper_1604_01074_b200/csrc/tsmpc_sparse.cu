@@ -964,6 +964,135 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
 }
 
 // ----------------------------------------------------------------------------
+// split mode, trunk CTA: the sweep of trunk_sweep restricted to the trunk
+// subtrees holding this CTA's rows, for ALL components, in shared memory (the
+// slot region is unused on trunk CTAs).  Every trunk CTA of a subtree repeats
+// it, which replaces a barrier among the trunk CTAs and the KY round trip
+// through L2; the KY rows of the CTA's needs go straight to the staging rows of
+// trunk_needs (region B, pitch KY_LD + NUP + NXP).
+// Meta section after `own`: {nsub, nslev, slev[nslev+1], sub tp[nsub], local index[T]}.
+// ----------------------------------------------------------------------------
+__device__ __noinline__ void trunk_sweep_local(double cf, int cur) {
+  const SParams& S = g_sp;
+  const Ctx c = ctx_of();
+  const Params& P = S.P;
+  const int* sb = c.mt.own + c.mt.nown;
+  const int nsub = sb[0], nsl = sb[1];
+  const int* slev = sb + 2;
+  const int* stp = slev + nsl + 1;
+  const int* lio = stp + nsub;
+  const int ncomp = c.nv + c.nx + c.nu;
+  double* Zs = s_dyn + S.O_SLOT;
+  double* Xs = Zs + (size_t)nsub * ncomp;
+  double* Ip = Xs + (size_t)nsub * ncomp;
+  const int* g = S.tsched;
+  const int T = __ldg(g), nlev = __ldg(g + 1);
+  const int* sch = S.sched_resident ? reinterpret_cast<const int*>(s_dyn + S.O_SCHED) : g;
+  const int* pos = sch + 4 + nlev + 1;
+  const int* tch = pos + 8 * T;
+  const int* hch = tch + sch[2];
+  const size_t E = (size_t)c.E;
+  const double* Y = P.ybuf[cur];
+  const double* Yp = P.ybuf[cur ^ 1];
+  const double* adiag = c.adiag();
+#pragma unroll 1
+  for (int li = threadIdx.x; li < nsub; li += kThreadsS) Ip[li] = __ldg(P.inv2p + pos[8 * stp[li]]);
+  // (1) own terms + chain-head children
+#pragma unroll 1
+  for (int idx = threadIdx.x; idx < nsub * ncomp; idx += kThreadsS) {
+    const int li = idx / ncomp, q = idx - li * ncomp;
+    const int* ps = pos + 8 * stp[li];
+    const int a = ps[0], st = ps[1], h0 = ps[5], nh = ps[6];
+    double z = 0.0, x = 0.0;
+    if (q < c.nv) {
+      z = ldcg(S.beta_s + (size_t)a * c.NVP + q);
+#pragma unroll 1
+      for (int m0 = 0; m0 < nh; m0 += kCh) {
+        double v[kCh];
+#pragma unroll
+        for (int u = 0; u < kCh; ++u) v[u] = m0 + u < nh ? ldcg(P.GG + (size_t)hch[h0 + m0 + u] * c.NVP + q) : 0.0;
+#pragma unroll
+        for (int u = 0; u < kCh; ++u)
+          if (m0 + u < nh) z = __dadd_rn(z, v[u]);
+      }
+    } else if (q < c.nv + c.nx) {
+      const int i = q - c.nv;
+      const size_t o = (size_t)a * c.NXP + i;
+      const double ws = extrap(ldcg(Y + o), ldcg(Yp + o), cf);
+      const double wz = extrap(ldcg(Y + E * c.NXP + o), ldcg(Yp + E * c.NXP + o), cf);
+      const double s = __dadd_rn(__dmul_rn(ws, c.scl[st]), __dmul_rn(wz, c.scl[c.N + st]));
+      double h = 0.0;
+#pragma unroll 1
+      for (int m0 = 0; m0 < nh; m0 += kCh) {
+        double v[kCh];
+#pragma unroll
+        for (int u = 0; u < kCh; ++u) v[u] = m0 + u < nh ? ldcg(P.XIQG + (size_t)hch[h0 + m0 + u] * c.NXP + i) : 0.0;
+#pragma unroll
+        for (int u = 0; u < kCh; ++u)
+          if (m0 + u < nh) h = __dadd_rn(h, v[u]);
+      }
+      x = __dadd_rn(s, __dmul_rn(h, adiag[i]));
+    } else {
+      const int j = q - c.nv - c.nx;
+      const size_t o = 2 * E * c.NXP + (size_t)a * c.NUP + j;
+      const double wp = extrap(ldcg(Y + o), ldcg(Yp + o), cf);
+      z = c.scaled() ? __dmul_rn(wp, c.dpsi(st, j)) : wp;
+    }
+    Zs[idx] = z;
+    Xs[idx] = x;
+  }
+  __syncthreads();
+  // (2) bottom-up over the subtree levels: add trunk children
+#pragma unroll 1
+  for (int l = nsl - 1; l >= 0; --l) {
+#pragma unroll 1
+    for (int idx = slev[l] * ncomp + threadIdx.x; idx < slev[l + 1] * ncomp; idx += kThreadsS) {
+      const int li = idx / ncomp, q = idx - li * ncomp;
+      const int* ps = pos + 8 * stp[li];
+      const int c0 = ps[3], n = ps[4];
+      double zs = 0.0, xs = 0.0;
+#pragma unroll 1
+      for (int m = 0; m < n; ++m) {
+        const int lc = lio[tch[c0 + m]];
+        zs = __dadd_rn(zs, Zs[lc * ncomp + q]);
+        xs = __dadd_rn(xs, Xs[lc * ncomp + q]);
+      }
+      if (q >= c.nv && q < c.nv + c.nx) {
+        const double xiq = __dadd_rn(Xs[idx], __dmul_rn(xs, adiag[q - c.nv]));
+        Xs[idx] = xiq;
+        Zs[idx] = __dadd_rn(xiq, zs);
+      } else {
+        Zs[idx] = __dadd_rn(Zs[idx], zs);
+      }
+    }
+    __syncthreads();
+  }
+  // (3) top-down: K_a, Y_a = own * inv2p_a + parent's
+#pragma unroll 1
+  for (int l = 0; l < nsl; ++l) {
+#pragma unroll 1
+    for (int idx = slev[l] * ncomp + threadIdx.x; idx < slev[l + 1] * ncomp; idx += kThreadsS) {
+      const int li = idx / ncomp, q = idx - li * ncomp;
+      const int pp = pos[8 * stp[li] + 2];
+      double v = __dmul_rn(Zs[idx], Ip[li]);
+      if (pp >= 0) v = __dadd_rn(v, Zs[lio[pp] * ncomp + q]);
+      Zs[idx] = v;
+    }
+    __syncthreads();
+  }
+  // (4) KY rows of the needs -> staging rows of trunk_needs
+  const int SLD = P.KY_LD + c.NUP + c.NXP;
+  const int* nd = c.mt.needs;
+#pragma unroll 1
+  for (int idx = threadIdx.x; idx < c.mt.nneed * ncomp; idx += kThreadsS) {
+    const int n = idx / ncomp, q = idx - n * ncomp;
+    const int col = q < c.nv ? q : (q < c.nv + c.nx ? c.NVP + (q - c.nv) : c.NVP + c.NXP + (q - c.nv - c.nx));
+    c.B()[(size_t)n * SLD + col] = Zs[lio[nd[4 * n]] * ncomp + q];
+  }
+  // (trunk_needs starts with a barrier-protected staging round)
+}
+
+// ----------------------------------------------------------------------------
 // sharded plans, end of phase 1: per trunk position, the sums over the chain heads
 // hanging from its node (same order as the single-GPU sweep: children in node
 // order) -> HS; zero where another rank owns those heads.  Grid-strided.
@@ -1023,7 +1152,9 @@ __device__ __noinline__ void trunk_needs() {
     for (int idx = threadIdx.x; idx < nn * per; idx += kThreadsS) {
       const int n = idx / per, q = idx - n * per;
       double* dst = c.B() + (size_t)n * SLD;
-      if (q < hk) cp16(dst + 2 * q, P.KY + (size_t)nd[4 * n] * P.KY_LD + 2 * q);
+      if (q < hk) {
+        if (!S.split_local) cp16(dst + 2 * q, P.KY + (size_t)nd[4 * n] * P.KY_LD + 2 * q);
+      }
       else if (q < hk + hu) cp16(dst + P.KY_LD + 2 * (q - hk), P.uhat + (size_t)nd[4 * n + 2] * c.NUP + 2 * (q - hk));
       else cp16(dst + P.KY_LD + c.NUP + 2 * (q - hk - hu), P.evec + (size_t)nd[4 * n + 2] * c.NXP + 2 * (q - hk - hu));
     }
@@ -1296,10 +1427,15 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
         grid.sync();
         TSMPC_MARK(P, 9, tb_);
         if ((int)blockIdx.x >= S.split_c0) {
-          trunk_sweep(cf, cur);
-          TSMPC_MARK(P, 10, tb_);
-          trunk_barrier(S.sub_ctr, (unsigned)S.split_n, sub_target);
-          TSMPC_MARK(P, 11, tb_);
+          if (S.split_local) {
+            trunk_sweep_local(cf, cur);
+            TSMPC_MARK(P, 10, tb_);
+          } else {
+            trunk_sweep(cf, cur);
+            TSMPC_MARK(P, 10, tb_);
+            trunk_barrier(S.sub_ctr, (unsigned)S.split_n, sub_target);
+            TSMPC_MARK(P, 11, tb_);
+          }
           trunk_needs();
           TSMPC_MARK(P, 12, tb_);
         } else {

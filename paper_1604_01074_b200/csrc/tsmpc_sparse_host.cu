@@ -167,8 +167,18 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
   // This keeps each CTA's needs close to its chains' root paths (also on shards,
   // where many trunk edges have no owned chains below them).
   std::vector<std::vector<int>> cta_own(C);
-  if (split_n) {  // trunk rows round-robin over the trunk CTAs
-    for (int tp = 0; tp < T; ++tp) cta_own[nch_split + tp % split_n].push_back(tp);
+  // depth-0 ancestor (trunk subtree root) of every trunk position
+  std::vector<int> troot(T, -1);
+  for (int tp = 0; tp < T; ++tp) {
+    int e = out.trunk_edge[tp];
+    while ((int)t.anc[e + 1] - 1 >= 0) e = (int)t.anc[e + 1] - 1;
+    troot[tp] = tpos[e];
+  }
+  if (split_n) {  // trunk rows in contiguous runs of (subtree, position) order
+    std::vector<int> order(T);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return troot[a] < troot[b]; });
+    for (int i = 0; i < T; ++i) cta_own[nch_split + (int)((long long)i * split_n / T)].push_back(order[i]);
   } else {
     std::vector<long long> load(C, 0);
     std::vector<std::set<int>> need(C);
@@ -249,6 +259,7 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
     depth[tp] = d;
   }
   std::vector<int> cta_rows(C, 0), cta_needs(C, 0);
+  int sub_max = 0;  // largest trunk-subtree set of a split-mode trunk CTA
   std::vector<std::vector<int>> metas(C);
   int total_tiles = 0;
   for (int c = 0; c < C; ++c) {
@@ -323,6 +334,29 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
     }
     m.insert(m.end(), lev.begin(), lev.end());
     for (int tp : cta_own[c]) m.push_back(need_idx[tp]);
+    if (split_n && c >= nch_split) {
+      // the trunk subtrees of the owned rows: {nsub, nslev, slev[nslev+1], sub tp[nsub], local index of tp[T]}
+      std::set<int> roots;
+      for (int tp : cta_own[c]) roots.insert(troot[tp]);
+      std::vector<std::pair<int, int>> sub;  // (depth, tp)
+      for (int tp = 0; tp < T; ++tp)
+        if (roots.count(troot[tp])) sub.push_back({depth[tp], tp});
+      std::sort(sub.begin(), sub.end());
+      std::vector<int> slev{0}, stp, lio(T, -1);
+      for (size_t i = 0; i < sub.size(); ++i) {
+        if (i > 0 && sub[i].first != sub[i - 1].first) slev.push_back((int)i);
+        lio[sub[i].second] = (int)i;
+        stp.push_back(sub[i].second);
+      }
+      slev.push_back((int)sub.size());
+      if (sub.empty()) slev = {0};
+      m.push_back((int)sub.size());
+      m.push_back((int)slev.size() - 1);
+      m.insert(m.end(), slev.begin(), slev.end());
+      m.insert(m.end(), stp.begin(), stp.end());
+      m.insert(m.end(), lio.begin(), lio.end());
+      sub_max = std::max(sub_max, (int)sub.size());
+    }
     cta_rows[c] = nrows;
     cta_needs[c] = (int)need_tp.size();
     total_tiles += (int)tiles.size();
@@ -490,6 +524,18 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
   S.split_c0 = nch_split;
   S.split_n = split_n;
   S.TR_LD = NUP + 2 * NXP;
+  {
+    // local subtree sweeps: [Z | X] x all components + 1/(2p) per subtree position in
+    // the (unused) slot region of the trunk CTAs; needs staged on chip (trunk_needs)
+    const long long KY_LD = (long long)NVP + NXP + NUP;
+    const long long sld = KY_LD + NUP + NXP;
+    const bool fits = (long long)sub_max * (2LL * ncomp_all + 1) <= (long long)S.slot_rows * S.slot_ld &&
+                      (long long)need_max * sld <= (long long)kTileS * NUP;
+    S.split_local = (split_n && fits && !std::getenv("TSMPC_SPLIT_GLOBAL_SWEEP")) ? 1 : 0;
+    if (std::getenv("TSMPC_PLAN_DEBUG"))
+      std::fprintf(stderr, "plan_sparse: split %d (trunk CTAs %d from %d) local %d sub_max %d need_max %d\n",
+                   S.split, split_n, nch_split, S.split_local, sub_max, need_max);
+  }
   if (split_n)  // the chain CTAs keep their one tile resident (else no split)
     for (int c = 0; c < nch_split; ++c)
       if (metas[c][6] == 0 || metas[c][0] != 1)
