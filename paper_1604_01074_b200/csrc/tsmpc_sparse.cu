@@ -772,7 +772,8 @@ __device__ __forceinline__ void trunk_barrier(unsigned int* ctr, unsigned int n,
   if (threadIdx.x == 0) {
     __threadfence();
     atomicAdd(ctr, 1u);
-    while (*((volatile unsigned int*)ctr) < target) __nanosleep(32);
+    while (*((volatile unsigned int*)ctr) < target) {
+    }
     __threadfence();
   }
   __syncthreads();
@@ -871,6 +872,14 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
       const double wp = extrap(ldcg(Y + o), ldcg(Yp + o), cf);
       z = c.scaled() ? __dmul_rn(wp, c.dpsi(st, j)) : wp;
     }
+    if (ps[4] == 0) {  // no trunk children: the bottom-up step (children sums 0) here
+      if (q >= c.nv && q < c.nv + c.nx) {
+        x = __dadd_rn(x, __dmul_rn(0.0, adiag[q - c.nv]));
+        z = __dadd_rn(x, 0.0);
+      } else {
+        z = __dadd_rn(z, 0.0);
+      }
+    }
     Zs[idx] = z;
     Xs[idx] = x;
   }
@@ -913,9 +922,10 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
     }
     __syncthreads();
   } else {
-  // (2) bottom-up over edge-stage levels: add trunk children
+  // (2) bottom-up over edge-stage levels: add trunk children (the deepest level
+  // has none: done above); level 0 also takes its top-down step (no parent)
 #pragma unroll 1
-  for (int l = nlev - 1; l >= 0; --l) {
+  for (int l = nlev - 2; l >= 0; --l) {
 #pragma unroll 1
     for (int idx = lev[l] * nc + threadIdx.x; idx < lev[l + 1] * nc; idx += kThreadsS) {
       const int tp = idx / nc, k = idx - tp * nc, q = c_lo + k;
@@ -928,19 +938,21 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
         zs = __dadd_rn(zs, Zs[cp * nc + k]);
         xs = __dadd_rn(xs, Xs[cp * nc + k]);
       }
+      double zn;
       if (q >= c.nv && q < c.nv + c.nx) {
         const double xiq = __dadd_rn(Xs[idx], __dmul_rn(xs, adiag[q - c.nv]));
         Xs[idx] = xiq;
-        Zs[idx] = __dadd_rn(xiq, zs);
+        zn = __dadd_rn(xiq, zs);
       } else {
-        Zs[idx] = __dadd_rn(Zs[idx], zs);
+        zn = __dadd_rn(Zs[idx], zs);
       }
+      Zs[idx] = l == 0 ? __dmul_rn(zn, Ip[tp]) : zn;
     }
     __syncthreads();
   }
   // (3) top-down: K_a, Y_a = own * inv2p_a + parent's
 #pragma unroll 1
-  for (int l = 0; l < nlev; ++l) {
+  for (int l = nlev >= 2 ? 1 : 0; l < nlev; ++l) {
 #pragma unroll 1
     for (int idx = lev[l] * nc + threadIdx.x; idx < lev[l + 1] * nc; idx += kThreadsS) {
       const int tp = idx / nc, k = idx - tp * nc;
@@ -1038,13 +1050,22 @@ __device__ __noinline__ void trunk_sweep_local(double cf, int cur) {
       const double wp = extrap(ldcg(Y + o), ldcg(Yp + o), cf);
       z = c.scaled() ? __dmul_rn(wp, c.dpsi(st, j)) : wp;
     }
+    if (ps[4] == 0) {  // no trunk children: the bottom-up step (children sums 0) here
+      if (q >= c.nv && q < c.nv + c.nx) {
+        x = __dadd_rn(x, __dmul_rn(0.0, adiag[q - c.nv]));
+        z = __dadd_rn(x, 0.0);
+      } else {
+        z = __dadd_rn(z, 0.0);
+      }
+    }
     Zs[idx] = z;
     Xs[idx] = x;
   }
   __syncthreads();
-  // (2) bottom-up over the subtree levels: add trunk children
+  // (2) bottom-up over the subtree levels: add trunk children (the deepest level
+  // has none: done above); level 0 also takes its top-down step (no parent)
 #pragma unroll 1
-  for (int l = nsl - 1; l >= 0; --l) {
+  for (int l = nsl - 2; l >= 0; --l) {
 #pragma unroll 1
     for (int idx = slev[l] * ncomp + threadIdx.x; idx < slev[l + 1] * ncomp; idx += kThreadsS) {
       const int li = idx / ncomp, q = idx - li * ncomp;
@@ -1057,19 +1078,21 @@ __device__ __noinline__ void trunk_sweep_local(double cf, int cur) {
         zs = __dadd_rn(zs, Zs[lc * ncomp + q]);
         xs = __dadd_rn(xs, Xs[lc * ncomp + q]);
       }
+      double zn;
       if (q >= c.nv && q < c.nv + c.nx) {
         const double xiq = __dadd_rn(Xs[idx], __dmul_rn(xs, adiag[q - c.nv]));
         Xs[idx] = xiq;
-        Zs[idx] = __dadd_rn(xiq, zs);
+        zn = __dadd_rn(xiq, zs);
       } else {
-        Zs[idx] = __dadd_rn(Zs[idx], zs);
+        zn = __dadd_rn(Zs[idx], zs);
       }
+      Zs[idx] = l == 0 ? __dmul_rn(zn, Ip[li]) : zn;
     }
     __syncthreads();
   }
   // (3) top-down: K_a, Y_a = own * inv2p_a + parent's
 #pragma unroll 1
-  for (int l = 0; l < nsl; ++l) {
+  for (int l = nsl >= 2 ? 1 : 0; l < nsl; ++l) {
 #pragma unroll 1
     for (int idx = slev[l] * ncomp + threadIdx.x; idx < slev[l + 1] * ncomp; idx += kThreadsS) {
       const int li = idx / ncomp, q = idx - li * ncomp;
