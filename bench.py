@@ -242,16 +242,22 @@ def run_ours(args, ws, rank, local):
         if rank == 0:
             line["sharded"] = sh
     if rank == 0:
-        # configs[1] "solve to the reference residual tolerance": the residual_inf the
-        # 500-iteration solve reaches (the reference's, within the parity tolerance),
-        # tested on the device every 25 iterations
-        r_ref = step()["residual_inf"]
-        rt = [plan.solve(W["p"], args.iters, lam, theta=th, coef=cf, keep_device=True, tol=r_ref,
-                         check_every=25) for _ in range(3)]
-        line["to_tolerance"] = {"tol": r_ref, "check_every": 25, "iterations": rt[-1]["iterations"],
-                                "solve_ms": statistics.median(r["device_total_ms"] for r in rt),
-                                "loop_ms": statistics.median(r["device_ms"] for r in rt),
-                                "residual_inf": rt[-1]["residual_inf"]}
+        # SolverConfig(tol=...): the device tests residual_inf every 25 iterations.
+        # The APG dual residual is not monotone on this workload (the 500-iteration
+        # value is already reached within the first checks), so the line reports the
+        # residual at every check and what the test costs: the same 500-iteration
+        # solve with a tolerance that is never met vs without the test
+        tr = plan.solve(W["p"], args.iters, lam, theta=th, coef=cf, keep_device=True, skip_gap=True,
+                        record_residuals=True)["resid_trace"]
+        plain = [plan.solve(W["p"], args.iters, lam, theta=th, coef=cf, keep_device=True,
+                            skip_gap=True)["device_ms"] for _ in range(3)]
+        chk = [plan.solve(W["p"], args.iters, lam, theta=th, coef=cf, keep_device=True, skip_gap=True,
+                          tol=1e-300, check_every=25)["device_ms"] for _ in range(3)]
+        line["stopping_test"] = {
+            "check_every": 25,
+            "residual_at_checks": [float(tr[j]) for j in range(24, args.iters, 25)],
+            "loop_ms_without": statistics.median(plain), "loop_ms_with": statistics.median(chk),
+            "us_per_check": 1e3 * (statistics.median(chk) - statistics.median(plain)) / (args.iters // 25)}
     if not args.no_sweep and rank == 0:
         line["sweep"] = sweep(args, lam_cache={args.tree: lam}, local=local)
     if rank == 0 and not args.no_cpu:
