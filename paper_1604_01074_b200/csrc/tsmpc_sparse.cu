@@ -1158,6 +1158,8 @@ __device__ __noinline__ void trunk_needs() {
   const Params& P = S.P;
   const int nn = c.mt.nneed;
   if (nn == 0) return;
+  long long tn_ = clock64();
+  (void)tn_;
   const int nx = c.nx, nu = c.nu, nv = c.nv;
   const int LD = S.need_ld;
   const int* nd = c.mt.needs;
@@ -1185,6 +1187,7 @@ __device__ __noinline__ void trunk_needs() {
     cp_wait<0>();
     __syncthreads();
   }
+  TSMPC_MARK(P, 4, tn_);
   auto ky = [&](int n, int col) -> double {
     return staged ? KYs[(size_t)n * SLD + col] : ldcg(P.KY + (size_t)nd[4 * n] * P.KY_LD + col);
   };
@@ -1194,52 +1197,92 @@ __device__ __noinline__ void trunk_needs() {
   auto evec_n = [&](int n, int i) -> double {
     return staged ? KYs[(size_t)n * SLD + P.KY_LD + c.NUP + i] : ldcg(P.evec + (size_t)nd[4 * n + 2] * c.NXP + i);
   };
-  // (1) Yz = Ypsi + B' Yx
-  {
-    const int* cp = c.spi + S.Bc_ptr;
-    const int* ci = c.spi + S.Bc_idx;
-    const double* cv = c.spv + S.Bc_val;
-#pragma unroll 1
-    for (int idx = threadIdx.x; idx < nn * nu; idx += kThreadsS) {
-      const int n = idx / nu, j = idx - n * nu;
-      double z = ky(n, c.NVP + c.NXP + j);
-#pragma unroll 1
-      for (int q = cp[j]; q < cp[j + 1]; ++q) z = fma(cv[q], ky(n, c.NVP + ci[q]), z);
-      ND[(size_t)n * LD + UO + j] = z;
-    }
-  }
-  __syncthreads();
-  // (2) S = K + Ls' Yz
-  {
-    const int* cp = c.spi + S.Lc_ptr;
-    const int* ci = c.spi + S.Lc_idx;
-    const double* cv = c.spv + S.Lc_val;
-#pragma unroll 1
-    for (int idx = threadIdx.x; idx < nn * nv; idx += kThreadsS) {
-      const int n = idx / nv, k = idx - n * nv;
-      double h = 0.0;
-#pragma unroll 1
-      for (int q = cp[k]; q < cp[k + 1]; ++q) h = fma(cv[q], ND[(size_t)n * LD + UO + ci[q]], h);
-      ND[(size_t)n * LD + k] = __dadd_rn(ky(n, k), h);
-    }
-  }
-  __syncthreads();
-  // (3) du = Lt S
-  {
-    const int* rp = c.spi + S.Lr_ptr;
-    const int* ri = c.spi + S.Lr_idx;
-    const double* rv = c.spv + S.Lr_val;
+  if (S.split && staged) {
+    // split mode: S is only an intermediate (the chains get du / B du / x from TR),
+    // so each du_j is evaluated in one pass, re-deriving the Yz_j' and S_k it needs
+    // with the same operations in the same order as the three passes below
+    const int* lp = c.spi + S.Lr_ptr;
+    const int* lq = c.spi + S.Lr_idx;
+    const double* lv = c.spv + S.Lr_val;
+    const int* sp = c.spi + S.Lc_ptr;
+    const int* sq = c.spi + S.Lc_idx;
+    const double* sv = c.spv + S.Lc_val;
+    const int* bp = c.spi + S.Bc_ptr;
+    const int* bq = c.spi + S.Bc_idx;
+    const double* bv = c.spv + S.Bc_val;
 #pragma unroll 1
     for (int idx = threadIdx.x; idx < nn * nu; idx += kThreadsS) {
       const int n = idx / nu, j = idx - n * nu;
       double d = 0.0;
 #pragma unroll 1
-      for (int q = rp[j]; q < rp[j + 1]; ++q) d = fma(rv[q], ND[(size_t)n * LD + ri[q]], d);
+      for (int q = lp[j]; q < lp[j + 1]; ++q) {
+        const int k = lq[q];
+        double h = 0.0;
+#pragma unroll 1
+        for (int q2 = sp[k]; q2 < sp[k + 1]; ++q2) {
+          const int j2 = sq[q2];
+          double z = ky(n, c.NVP + c.NXP + j2);
+#pragma unroll 1
+          for (int q3 = bp[j2]; q3 < bp[j2 + 1]; ++q3) z = fma(bv[q3], ky(n, c.NVP + bq[q3]), z);
+          h = fma(sv[q2], z, h);
+        }
+        d = fma(lv[q], __dadd_rn(ky(n, k), h), d);
+      }
       ND[(size_t)n * LD + UO + j] = d;
-      if (S.split) stcg(S.TR + (size_t)nd[4 * n] * S.TR_LD + j, d);  // du of the trunk row
+      stcg(S.TR + (size_t)nd[4 * n] * S.TR_LD + j, d);  // du of the trunk row
     }
+    __syncthreads();
+  } else {
+  // (1) Yz = Ypsi + B' Yx
+    {
+      const int* cp = c.spi + S.Bc_ptr;
+      const int* ci = c.spi + S.Bc_idx;
+      const double* cv = c.spv + S.Bc_val;
+  #pragma unroll 1
+      for (int idx = threadIdx.x; idx < nn * nu; idx += kThreadsS) {
+        const int n = idx / nu, j = idx - n * nu;
+        double z = ky(n, c.NVP + c.NXP + j);
+  #pragma unroll 1
+        for (int q = cp[j]; q < cp[j + 1]; ++q) z = fma(cv[q], ky(n, c.NVP + ci[q]), z);
+        ND[(size_t)n * LD + UO + j] = z;
+      }
+    }
+    __syncthreads();
+    TSMPC_MARK(P, 5, tn_);
+    // (2) S = K + Ls' Yz
+    {
+      const int* cp = c.spi + S.Lc_ptr;
+      const int* ci = c.spi + S.Lc_idx;
+      const double* cv = c.spv + S.Lc_val;
+  #pragma unroll 1
+      for (int idx = threadIdx.x; idx < nn * nv; idx += kThreadsS) {
+        const int n = idx / nv, k = idx - n * nv;
+        double h = 0.0;
+  #pragma unroll 1
+        for (int q = cp[k]; q < cp[k + 1]; ++q) h = fma(cv[q], ND[(size_t)n * LD + UO + ci[q]], h);
+        ND[(size_t)n * LD + k] = __dadd_rn(ky(n, k), h);
+      }
+    }
+    __syncthreads();
+    TSMPC_MARK(P, 6, tn_);
+    // (3) du = Lt S
+    {
+      const int* rp = c.spi + S.Lr_ptr;
+      const int* ri = c.spi + S.Lr_idx;
+      const double* rv = c.spv + S.Lr_val;
+  #pragma unroll 1
+      for (int idx = threadIdx.x; idx < nn * nu; idx += kThreadsS) {
+        const int n = idx / nu, j = idx - n * nu;
+        double d = 0.0;
+  #pragma unroll 1
+        for (int q = rp[j]; q < rp[j + 1]; ++q) d = fma(rv[q], ND[(size_t)n * LD + ri[q]], d);
+        ND[(size_t)n * LD + UO + j] = d;
+        if (S.split) stcg(S.TR + (size_t)nd[4 * n] * S.TR_LD + j, d);  // du of the trunk row
+      }
+    }
+    __syncthreads();
+    TSMPC_MARK(P, 7, tn_);
   }
-  __syncthreads();
   // (4) bv + e ; then u = uhat + du ; then x level by level (parents first)
   {
     const int* rp = c.spi + S.Br_ptr;
@@ -1252,9 +1295,12 @@ __device__ __noinline__ void trunk_needs() {
 #pragma unroll 1
       for (int q = rp[i]; q < rp[i + 1]; ++q) b = fma(rv[q], ND[(size_t)n * LD + UO + ri[q]], b);
       if (S.split) stcg(S.TR + (size_t)nd[4 * n] * S.TR_LD + c.NUP + i, b);  // B du of the trunk row
-      ND[(size_t)n * LD + c.NVP + i] = __dadd_rn(b, evec_n(n, i));
+      // split + staged: bv + e in the (free) S columns, so the x walk below can
+      // write x in place without a copy-back pass
+      ND[(size_t)n * LD + (S.split && staged ? 0 : c.NVP) + i] = __dadd_rn(b, evec_n(n, i));
     }
     __syncthreads();
+    TSMPC_MARK(P, 13, tn_);
     // u = uhat + du (independent of the x pass below: no barrier in between)
 #pragma unroll 1
     for (int idx = threadIdx.x; idx < nn * nu; idx += kThreadsS) {
@@ -1270,26 +1316,34 @@ __device__ __noinline__ void trunk_needs() {
       // ancestors' (bv + e) by powers of a; the result goes to the staged KY
       // columns (no longer read) and is copied back after a barrier
       double* xo = c.B();
+      const int bo = S.split ? 0 : c.NVP;  // where bv + e is
 #pragma unroll 1
       for (int idx = threadIdx.x; idx < nn * nx; idx += kThreadsS) {
         const int n = idx / nx, i = idx - n * nx;
         const double a = adiag[i];
-        double xv = ND[(size_t)n * LD + c.NVP + i], m = a;
+        double xv = ND[(size_t)n * LD + bo + i], m = a;
 #pragma unroll 1
         for (int anc = nd[4 * n + 1]; anc >= 0; anc = nd[4 * anc + 1]) {
-          xv = __dadd_rn(xv, __dmul_rn(m, ND[(size_t)anc * LD + c.NVP + i]));
+          xv = __dadd_rn(xv, __dmul_rn(m, ND[(size_t)anc * LD + bo + i]));
           m = __dmul_rn(m, a);
         }
-        xo[(size_t)n * SLD + i] = __dadd_rn(xv, __dmul_rn(m, c.proot()[i]));
+        xv = __dadd_rn(xv, __dmul_rn(m, c.proot()[i]));
+        if (S.split) {
+          ND[(size_t)n * LD + c.NVP + i] = xv;
+          stcg(S.TR + (size_t)nd[4 * n] * S.TR_LD + c.NUP + c.NXP + i, xv);
+        } else {
+          xo[(size_t)n * SLD + i] = xv;
+        }
       }
       __syncthreads();
+      if (!S.split) {
 #pragma unroll 1
-      for (int idx = threadIdx.x; idx < nn * nx; idx += kThreadsS) {
-        const int n = idx / nx, i = idx - n * nx;
-        ND[(size_t)n * LD + c.NVP + i] = xo[(size_t)n * SLD + i];
-        if (S.split) stcg(S.TR + (size_t)nd[4 * n] * S.TR_LD + c.NUP + c.NXP + i, xo[(size_t)n * SLD + i]);
+        for (int idx = threadIdx.x; idx < nn * nx; idx += kThreadsS) {
+          const int n = idx / nx, i = idx - n * nx;
+          ND[(size_t)n * LD + c.NVP + i] = xo[(size_t)n * SLD + i];
+        }
+        __syncthreads();
       }
-      __syncthreads();
     } else {
 #pragma unroll 1
       for (int l = 0; l < c.mt.nlev; ++l) {
