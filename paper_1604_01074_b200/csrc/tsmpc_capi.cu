@@ -751,7 +751,8 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
         S.HS_LD = NVP + NXP;
         if (S.split) {
           rc |= pl->alloc(&pl->TR, (size_t)std::max(1, hp.n_trunk) * S.TR_LD);
-          rc |= pl->alloc(&pl->SUBCTR, 1);
+          rc |= pl->alloc(&pl->SUBCTR, 4);
+          S.split_flags = std::getenv("TSMPC_SPLIT_GRID") ? 0 : 1;
           if (rc) return bail(0);
           S.TR = pl->TR;
           S.sub_ctr = pl->SUBCTR;
@@ -1433,7 +1434,7 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
       S.nu0 = 0;
       S.nu1 = iters;
       S.phase = 3;
-      if (pl->SUBCTR) CU(cudaMemsetAsync(pl->SUBCTR, 0, sizeof(unsigned int), pl->stream));
+      if (pl->SUBCTR) CU(cudaMemsetAsync(pl->SUBCTR, 0, 4 * sizeof(unsigned int), pl->stream));
       CU(sparse_launch(S, pl->sp_ctas, pl->sp_smem, pl->stream));
       ++pl->launches;
     } else {

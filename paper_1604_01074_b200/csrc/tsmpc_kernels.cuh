@@ -172,7 +172,10 @@ struct SParams {
                                 // (all components; no trunk-CTA barrier, KY stays on chip)
   double* TR;                   // T x TR_LD
   int TR_LD;                    // NUP + 2 NXP
-  unsigned int* sub_ctr;        // arrival counter of the trunk-CTA barrier (zeroed per launch)
+  unsigned int* sub_ctr;        // [trunk-CTA barrier, heads published, TR published] (zeroed per launch)
+  int split_flags;              // directed signals between chain and trunk CTAs instead of grid barriers
+  int split_heads, O_HSUM;      // chain CTAs publish their head values right after the fill, by
+                                // reductions ([sum beta_s | sum psi^ | sum G_d s | sum z] at O_HSUM)
 };
 
 // Phase timers (profiling builds: -DTSMPC_TIMERS).  Slot k accumulates the cycles

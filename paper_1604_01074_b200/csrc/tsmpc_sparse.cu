@@ -101,6 +101,25 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+// directed signals of split mode (counters zeroed per launch): a CTA publishes
+// its writes (arrive) / waits until `target` arrivals (wait)
+__device__ __forceinline__ void signal_arrive(unsigned int* ctr) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+  }
+}
+__device__ __forceinline__ void signal_wait(unsigned int* ctr, unsigned int target) {
+  if (threadIdx.x == 0) {
+    while (*((volatile unsigned int*)ctr) < target) {
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+
 
 // Element phases map threads component-major: thread = (row group g, component
 // k), g = tid / kKW, rows r = g, g + kGroups, ...  The per-component sparse
@@ -459,6 +478,67 @@ __device__ __noinline__ void bwd_tile(int ti, double cf, int ysm, int srow0, boo
   }
   __syncthreads();
   TSMPC_MARK(P, 0, tm_);
+  if (S.split_heads && S.split_flags) {
+    // split mode: the trunk needs only this chain's head values, which are linear in
+    // the fill:  xiq_head = sum_d a^d s_d,  g_head = sum beta_s + Ls'(sum psi^ + B' sum_d G_d s_d)
+    // (d = depth below the head, G_d = 1 + a + ... + a^d).  Publish them now; the
+    // scans below produce the per-row t for this CTA's own forward.
+    double* hb = s_dyn + S.O_HSUM;  // sum beta_s (NVP), set at launch start
+    double* hp = hb + c.NVP;        // sum psi^ (NUP)
+    double* hx = hp + c.NUP;        // sum_d G_d s_d (NXP)
+    double* hz = hx + c.NXP;        // sum z (NUP)
+    const int* sg = c.mt.segs + 4 * seg0;  // one chain per tile in split mode
+    const int lo = sg[0], n = sg[1] - lo, head = c.mt.edge(row0 + lo);
+    const bool pub = sg[2] >= 0;
+    const double* adiag = c.adiag();
+    if (pub) {
+#pragma unroll 1
+      for (int idx = tid; idx < nx + nu; idx += kThreadsS) {
+        if (idx < nx) {
+          const int i = idx;
+          const double a = adiag[i];
+          double xh = 0.0, xs = 0.0, pw = 1.0, gw = 1.0;
+#pragma unroll 4
+          for (int d = 0; d < n; ++d) {
+            const double sv = RA[(lo + d) * LA + i];
+            xh = fma(pw, sv, xh);
+            xs = fma(gw, sv, xs);
+            pw = __dmul_rn(pw, a);
+            gw = __dadd_rn(gw, pw);
+          }
+          stcg(P.XIQG + (size_t)head * c.NXP + i, xh);
+          hx[i] = xs;
+        } else {
+          const int j = idx - nx;
+          double ps = 0.0;
+#pragma unroll 4
+          for (int d = 0; d < n; ++d) ps = __dadd_rn(ps, RB[(lo + d) * c.NUP + j]);
+          hp[j] = ps;
+        }
+      }
+      __syncthreads();
+      if (tid < nu) {
+        const int* cp = c.spi + S.Bc_ptr;
+        const int* ci = c.spi + S.Bc_idx;
+        const double* cv = c.spv + S.Bc_val;
+        double z = hp[tid];
+#pragma unroll 1
+        for (int q = cp[tid]; q < cp[tid + 1]; ++q) z = fma(cv[q], hx[ci[q]], z);
+        hz[tid] = z;
+      }
+      __syncthreads();
+      if (tid < nv) {
+        const int* cp = c.spi + S.Lc_ptr;
+        const int* ci = c.spi + S.Lc_idx;
+        const double* cv = c.spv + S.Lc_val;
+        double h = 0.0;
+#pragma unroll 1
+        for (int q = cp[tid]; q < cp[tid + 1]; ++q) h = fma(cv[q], hz[ci[q]], h);
+        stcg(P.GG + (size_t)head * c.NVP + tid, __dadd_rn(hb[tid], h));
+      }
+    }
+    signal_arrive(S.sub_ctr + 1);
+  }
   // streamed CTAs: the slot is free again -> prefetch the next tile's dual rows
   // (or, after the last backward tile, the ergodic rows the forward sweep needs)
   if (!resident) {
@@ -490,7 +570,7 @@ __device__ __noinline__ void bwd_tile(int ti, double cf, int ysm, int srow0, boo
           col[(j1 - 1 - u) * LA] = x;
         }
     }
-    if (sg[2] >= 0) stcg(P.XIQG + (size_t)c.mt.edge(row0 + lo) * c.NXP + i, x);
+    if (sg[2] >= 0 && !(S.split_heads && S.split_flags)) stcg(P.XIQG + (size_t)c.mt.edge(row0 + lo) * c.NXP + i, x);
   }
   __syncthreads();
   TSMPC_MARK(P, 1, tm_);
@@ -546,7 +626,7 @@ __device__ __noinline__ void bwd_tile(int ti, double cf, int ysm, int srow0, boo
         }
       }
     }
-    if (sg[2] >= 0) stcg(P.GG + (size_t)c.mt.edge(row0 + lo) * c.NVP + kk, gv);
+    if (sg[2] >= 0 && !(S.split_heads && S.split_flags)) stcg(P.GG + (size_t)c.mt.edge(row0 + lo) * c.NVP + kk, gv);
   }
   __syncthreads();
   TSMPC_MARK(P, 3, tm_);
@@ -1467,6 +1547,20 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
     cp_wait<0>();
     __syncthreads();
   }
+  if (S.split && S.split_heads && (int)blockIdx.x < S.split_c0 && nt == 1) {
+    // sum of beta_s over the chain (static during the launch), chain order
+    double* hb = s_dyn + S.O_HSUM;
+    const int* sg = c.mt.segs + 4 * c.mt.tiles[2];
+    const int lo = sg[0], n = sg[1] - lo;
+#pragma unroll 1
+    for (int k = threadIdx.x; k < c.nv; k += kThreadsS) {
+      double b = 0.0;
+#pragma unroll 1
+      for (int d = 0; d < n; ++d) b = __dadd_rn(b, ldcg(S.beta_s + (size_t)c.mt.edge(c.mt.tiles[0] + lo + d) * c.NVP + k));
+      hb[k] = b;
+    }
+    __syncthreads();
+  }
   double rmax = 0.0;
   unsigned int sub_target = 0;  // trunk-CTA barrier episodes x split_n (split mode)
   double cf = P.coef[S.nu0], th = P.theta[S.nu0];
@@ -1493,7 +1587,49 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
         head_prereduce();
       }
     }
-    if (do_b) {
+    if (do_b && trunk && S.split && S.split_flags) {
+      // split mode with directed signals instead of grid barriers: chain CTAs
+      // publish their chain heads and run the zero-input forward at once; trunk
+      // CTAs wait for every chain's heads, sweep, run the trunk forward and
+      // publish TR; chain CTAs wait for TR only before their trunk terms.
+      long long tb_ = clock64();
+      (void)tb_;
+      const unsigned it = (unsigned)(nu - S.nu0 + 1);
+      if ((int)blockIdx.x < S.split_c0) {
+        if (!S.split_heads) signal_arrive(S.sub_ctr + 1);  // else published inside bwd_tile
+        for (int t = 0; t < nt; ++t)
+          fwd_tile(t, nu, cf, th, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur, &rmax);
+        TSMPC_MARK(P, 10, tb_);
+        signal_wait(S.sub_ctr + 2, it * (unsigned)S.split_n);
+        TSMPC_MARK(P, 9, tb_);
+        if (blockIdx.x == 0) {
+          const double om = __dsub_rn(1.0, th);
+          for (int i = threadIdx.x; i < c.nx; i += kThreadsS)
+            P.xavg[i] = __dadd_rn(__dmul_rn(P.xavg[i], om), __dmul_rn(th, c.proot()[i]));
+        }
+        for (int t = 0; t < nt; ++t) fwd_finish(t, nu, cf, th, ysm, resident, cur, &rmax);
+        TSMPC_MARK(P, 3, tb_);
+      } else {
+        // the previous iteration's trunk-row epilogues (dual rows the sweep reads)
+        if (nu > S.nu0) trunk_barrier(S.sub_ctr, (unsigned)S.split_n, sub_target);
+        signal_wait(S.sub_ctr + 1, it * (unsigned)S.split_c0);
+        TSMPC_MARK(P, 9, tb_);
+        if (S.split_local) {
+          trunk_sweep_local(cf, cur);
+          TSMPC_MARK(P, 10, tb_);
+        } else {
+          trunk_sweep(cf, cur);
+          TSMPC_MARK(P, 10, tb_);
+          trunk_barrier(S.sub_ctr, (unsigned)S.split_n, sub_target);
+          TSMPC_MARK(P, 11, tb_);
+        }
+        trunk_needs();
+        signal_arrive(S.sub_ctr + 2);
+        TSMPC_MARK(P, 12, tb_);
+        trunk_own_rows(nu, cf, th, cur, &rmax);
+        TSMPC_MARK(P, 3, tb_);
+      }
+    } else if (do_b) {
       long long tb_s = 0;
       (void)tb_s;
       if (trunk && S.split) {
@@ -1550,6 +1686,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
         for (int t = 0; t < nt; ++t)
           fwd_tile(t, nu, cf, th, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur, &rmax);
       }
+    }
+    if (do_b) {
       if (nu == P.iters - 1 || P.record_all || is_check(P, nu)) {
         // warp, then CTA, then one global atomic per CTA (same-address global
         // atomics from every warp serialise in L2)

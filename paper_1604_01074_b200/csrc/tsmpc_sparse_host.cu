@@ -520,6 +520,14 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
   }
   S.O_INT = (int)off;
   off += ints_d;
+  // split mode: per-chain head sums (early head publication, tsmpc_sparse.cu bwd_tile)
+  S.O_HSUM = (int)off;
+  S.split_heads = 0;
+  if (split_n && off + even((long long)NVP + 2LL * NUP + NXP) <= (long long)(smem_limit / sizeof(double)) &&
+      !std::getenv("TSMPC_NO_EARLY_HEADS")) {
+    S.split_heads = 1;
+    off += even((long long)NVP + 2LL * NUP + NXP);
+  }
   S.split = split_n ? 1 : 0;
   S.split_c0 = nch_split;
   S.split_n = split_n;
