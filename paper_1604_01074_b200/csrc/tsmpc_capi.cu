@@ -748,6 +748,9 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
         S = hp.S;
         S.spi = d_spi; S.spv = d_spv; S.meta = d_meta; S.meta_ptr = d_mptr; S.tsched = d_ts;
         S.beta_s = pl->BETA_S; S.TG = pl->TG;
+        S.a_unit = 1;
+        for (int i = 0; i < nx; ++i)
+          if (pb->A[(size_t)i * nx + i] != 1.0) S.a_unit = 0;
         S.HS_LD = NVP + NXP;
         if (S.split) {
           rc |= pl->alloc(&pl->TR, (size_t)std::max(1, hp.n_trunk) * S.TR_LD);

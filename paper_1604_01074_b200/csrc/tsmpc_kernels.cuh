@@ -174,6 +174,7 @@ struct SParams {
   int TR_LD;                    // NUP + 2 NXP
   unsigned int* sub_ctr;        // [trunk-CTA barrier, heads published, TR published] (zeroed per launch)
   int split_flags;              // directed signals between chain and trunk CTAs instead of grid barriers
+  int a_unit;                   // A = I (a = 1 in every state component): chain recursions are plain sums
   int split_heads, O_HSUM;      // chain CTAs publish their head values right after the fill, by
                                 // reductions ([sum beta_s | sum psi^ | sum G_d s | sum z] at O_HSUM)
 };

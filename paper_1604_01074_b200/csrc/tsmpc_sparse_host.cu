@@ -138,7 +138,8 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
   if (allow_split && !sharded && T > 0 && !chains.empty() && !std::getenv("TSMPC_NO_SPLIT")) {
     const int spare = max_ctas - (int)chains.size();
     // enough trunk CTAs that one sweep slice (T x components) fits one pass of the CTA
-    const int want = std::max(kMinTrunkCtas, (int)(((long long)ncomp_all * T + 383) / 384));
+    int want = std::max(kMinTrunkCtas, (int)(((long long)ncomp_all * T + 383) / 384));
+    if (const char* e = std::getenv("TSMPC_TRUNK_CTAS")) want = std::max(kMinTrunkCtas, std::atoi(e));
     if (spare >= kMinTrunkCtas) split_n = std::min(spare, want);
   }
   const int nch_split = split_n ? (int)chains.size() : 0;
@@ -523,10 +524,13 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
   // split mode: per-chain head sums (early head publication, tsmpc_sparse.cu bwd_tile)
   S.O_HSUM = (int)off;
   S.split_heads = 0;
-  if (split_n && off + even((long long)NVP + 2LL * NUP + NXP) <= (long long)(smem_limit / sizeof(double)) &&
+  // [sum beta_s (NVP) | scratch: head sums 2 NUP + NXP during the backward, the
+  // parent's TR row NUP + 2 NXP during fwd_finish]
+  const long long hsum = NVP + std::max(2LL * NUP + NXP, (long long)NUP + 2LL * NXP);
+  if (split_n && off + even(hsum) <= (long long)(smem_limit / sizeof(double)) &&
       !std::getenv("TSMPC_NO_EARLY_HEADS")) {
     S.split_heads = 1;
-    off += even((long long)NVP + 2LL * NUP + NXP);
+    off += even(hsum);
   }
   S.split = split_n ? 1 : 0;
   S.split_c0 = nch_split;
