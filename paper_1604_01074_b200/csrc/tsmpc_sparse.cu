@@ -824,8 +824,6 @@ __device__ __noinline__ void fwd_finish(int ti, int nu_it, double cf, double th,
       if (r < nrows) RB[r * c.NUP + k] = __dadd_rn(RB[r * c.NUP + k], d);
     }
   }
-  // the thread reads back only its own u entries: no barrier needed
-  epi_psi_rows(nu_it, cf, th, nrows, ysm, !resident || last, cur ^ 1, rmax);
   TSMPC_MARK(P, 13, tm_);
   if (pn >= 0 && S.a_unit) {
     // a = 1: G_d = d + 1 and a^(d+1) = 1 exactly, so every row is independent
@@ -859,6 +857,8 @@ __device__ __noinline__ void fwd_finish(int ti, int nu_it, double cf, double th,
   }
   __syncthreads();
   TSMPC_MARK(P, 14, tm_);
+  // psi and state blocks back to back: they write disjoint columns of the rows
+  epi_psi_rows(nu_it, cf, th, nrows, ysm, !resident || last, cur ^ 1, rmax);
   epi_state(nu_it, cf, th, nrows, ysm, !resident || last, cur ^ 1, rmax);
   __syncthreads();
   TSMPC_MARK(P, 8, tm_);
