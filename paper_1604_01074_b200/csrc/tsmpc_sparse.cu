@@ -881,7 +881,10 @@ __device__ __forceinline__ void trunk_barrier(unsigned int* ctr, unsigned int n,
 // phase B: component-sliced trunk sweep -> KY (see tsmpc_apg.cu trunk_sweep_smem
 // for the recursion; here the schedule is staged in shared memory first)
 // ----------------------------------------------------------------------------
-__device__ __noinline__ void trunk_sweep(double cf, int cur) {
+__device__ __noinline__ void trunk_sweep(double cf, int cur, int part) {
+  // part 1: own terms (no chain heads needed: run while waiting for them);
+  // part 2: chain-head sums, levels, KY; part 3: both.  Each (edge, component)
+  // element stays with the same thread across the parts.
   const SParams& S = g_sp;
   const Ctx c = ctx_of();
   const Params& P = S.P;
@@ -905,11 +908,13 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
     sch = reinterpret_cast<const int*>(s_dyn + S.O_SCHED);
   } else if (S.sched_smem) {
     int* ss = reinterpret_cast<int*>(Ip + T);
+    if (part & 1) {
 #pragma unroll 1
-    for (int i = threadIdx.x; i < S.n_tsched; i += kThreadsS) ss[i] = __ldg(g + i);
+      for (int i = threadIdx.x; i < S.n_tsched; i += kThreadsS) ss[i] = __ldg(g + i);
+      __syncthreads();
+    }
     sch = ss;
   }
-  __syncthreads();
   const int* lev = sch + 4;
   const int* pos = lev + nlev + 1;
   const int* tch = pos + 8 * T;
@@ -919,17 +924,44 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
   const double* Yp = P.ybuf[cur ^ 1];
   const double* adiag = c.adiag();
   TSMPC_MARK(P, 13, ts_);
-  // (1) own terms + chain-head children (one parallel round of loads)
+  if (part & 1) {
+    // (1a) own terms: beta (v), s = D_sig w_sig + D_zeta w_zeta (x), D_psi w_psi (u)
 #pragma unroll 1
-  for (int tp = threadIdx.x; tp < T; tp += kThreadsS) Ip[tp] = __ldg(P.inv2p + pos[8 * tp]);
+    for (int tp = threadIdx.x; tp < T; tp += kThreadsS) Ip[tp] = __ldg(P.inv2p + pos[8 * tp]);
+#pragma unroll 1
+    for (int idx = threadIdx.x; idx < T * nc; idx += kThreadsS) {
+      const int tp = idx / nc, k = idx - tp * nc, q = c_lo + k;
+      const int* ps = pos + 8 * tp;
+      const int a = ps[0], st = ps[1];
+      double z = 0.0, x = 0.0;
+      if (q < c.nv) {
+        z = ldcg(S.beta_s + (size_t)a * c.NVP + q);
+      } else if (q < c.nv + c.nx) {
+        const int i = q - c.nv;
+        const size_t o = (size_t)a * c.NXP + i;
+        const double ws = extrap(ldcg(Y + o), ldcg(Yp + o), cf);
+        const double wz = extrap(ldcg(Y + E * c.NXP + o), ldcg(Yp + E * c.NXP + o), cf);
+        const double ds = c.scl[st], dz = c.scl[c.N + st];
+        x = __dadd_rn(__dmul_rn(ws, ds), __dmul_rn(wz, dz));
+      } else {
+        const int j = q - c.nv - c.nx;
+        const size_t o = 2 * E * c.NXP + (size_t)a * c.NUP + j;
+        const double wp = extrap(ldcg(Y + o), ldcg(Yp + o), cf);
+        z = c.scaled() ? __dmul_rn(wp, c.dpsi(st, j)) : wp;
+      }
+      Zs[idx] = z;
+      Xs[idx] = x;
+    }
+  }
+  if (!(part & 2)) return;
+  // (1b) chain-head children (one parallel round of loads), childless fold
 #pragma unroll 1
   for (int idx = threadIdx.x; idx < T * nc; idx += kThreadsS) {
     const int tp = idx / nc, k = idx - tp * nc, q = c_lo + k;
     const int* ps = pos + 8 * tp;
-    const int a = ps[0], st = ps[1], h0 = ps[5], nh = ps[6];
-    double z = 0.0, x = 0.0;
+    const int h0 = ps[5], nh = ps[6];
+    double z = Zs[idx], x = Xs[idx];
     if (q < c.nv) {
-      z = ldcg(S.beta_s + (size_t)a * c.NVP + q);
       if (S.sharded) {
         if (nh > 0) z = __dadd_rn(z, ldcg(S.HS + (size_t)tp * S.HS_LD + q));
       } else {
@@ -945,11 +977,6 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
       }
     } else if (q < c.nv + c.nx) {
       const int i = q - c.nv;
-      const size_t o = (size_t)a * c.NXP + i;
-      const double ws = extrap(ldcg(Y + o), ldcg(Yp + o), cf);
-      const double wz = extrap(ldcg(Y + E * c.NXP + o), ldcg(Yp + E * c.NXP + o), cf);
-      const double ds = c.scl[st], dz = c.scl[c.N + st];
-      const double s = __dadd_rn(__dmul_rn(ws, ds), __dmul_rn(wz, dz));
       double h = 0.0;
       if (S.sharded) {
         if (nh > 0) h = ldcg(S.HS + (size_t)tp * S.HS_LD + c.NVP + i);
@@ -964,12 +991,7 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur) {
             if (m0 + u < nh) h = __dadd_rn(h, v[u]);
         }
       }
-      x = __dadd_rn(s, __dmul_rn(h, adiag[i]));
-    } else {
-      const int j = q - c.nv - c.nx;
-      const size_t o = 2 * E * c.NXP + (size_t)a * c.NUP + j;
-      const double wp = extrap(ldcg(Y + o), ldcg(Yp + o), cf);
-      z = c.scaled() ? __dmul_rn(wp, c.dpsi(st, j)) : wp;
+      x = __dadd_rn(x, __dmul_rn(h, adiag[i]));
     }
     if (ps[4] == 0) {  // no trunk children: the bottom-up step (children sums 0) here
       if (q >= c.nv && q < c.nv + c.nx) {
@@ -1631,13 +1653,14 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
       } else {
         // the previous iteration's trunk-row epilogues (dual rows the sweep reads)
         if (nu > S.nu0) trunk_barrier(S.sub_ctr, (unsigned)S.split_n, sub_target);
+        if (!S.split_local) trunk_sweep(cf, cur, 1);  // own terms, before the heads arrive
         signal_wait(S.sub_ctr + 1, it * (unsigned)S.split_c0);
         TSMPC_MARK(P, 9, tb_);
         if (S.split_local) {
           trunk_sweep_local(cf, cur);
           TSMPC_MARK(P, 10, tb_);
         } else {
-          trunk_sweep(cf, cur);
+          trunk_sweep(cf, cur, 2);
           TSMPC_MARK(P, 10, tb_);
           trunk_barrier(S.sub_ctr, (unsigned)S.split_n, sub_target);
           TSMPC_MARK(P, 11, tb_);
@@ -1663,7 +1686,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
             trunk_sweep_local(cf, cur);
             TSMPC_MARK(P, 10, tb_);
           } else {
-            trunk_sweep(cf, cur);
+            trunk_sweep(cf, cur, 3);
             TSMPC_MARK(P, 10, tb_);
             trunk_barrier(S.sub_ctr, (unsigned)S.split_n, sub_target);
             TSMPC_MARK(P, 11, tb_);
@@ -1683,7 +1706,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
         (void)tb_;
         if (!S.sharded) grid.sync();
         TSMPC_MARK(P, 9, tb_);
-        trunk_sweep(cf, cur);
+        trunk_sweep(cf, cur, 3);
         TSMPC_MARK(P, 10, tb_);
         grid.sync();
         TSMPC_MARK(P, 9, tb_);
