@@ -281,10 +281,15 @@ struct EpiConst {
   double cf, th, om, lam, ilam, lam_p;
   bool last, want, wt;
   double* Yn;
+  bool pre;      // also leave the next iteration's fill (s -> x slot, psi^ -> u slot)
+  double cfn;    // momentum coefficient of the next iteration
 };
 
-__device__ __forceinline__ EpiConst epi_const(const Params& P, int nu_it, double cf, double th, bool wt, int ncur) {
+__device__ __forceinline__ EpiConst epi_const(const Params& P, int nu_it, double cf, double th, bool wt, int ncur,
+                                              bool pre = false, double cfn = 0.0) {
   EpiConst k;
+  k.pre = pre;
+  k.cfn = cfn;
   k.cf = cf;
   k.th = th;
   k.om = __dsub_rn(1.0, th);
@@ -312,6 +317,10 @@ __device__ __forceinline__ void epi_psi_elem(const Ctx& c, const Params& P, cons
   const double t = fmin(fmax(a, __dmul_rn(dp, c.bnd[3 * c.NXP + k])), __dmul_rn(dp, c.bnd[3 * c.NXP + c.NUP + k]));
   const double ny = __dadd_rn(w, __dmul_rn(q.lam, __dsub_rn(hp, t)));
   yp[k] = ny;
+  if (q.pre) {  // the next backward's fill of this element (bwd_tile step 1)
+    const double wn = extrap(ny, yc[k], q.cfn);
+    s_dyn[d[3] + k] = c.scaled() ? __dmul_rn(wn, dp) : wn;
+  }
   if (q.want) rmax = fmax(rmax, fabs(__dsub_rn(u, __ddiv_rn(t, dp))));
   double* ua = row + 2 * c.YW + c.NXP;
   const double na = __dadd_rn(__dmul_rn(ua[k], q.om), __dmul_rn(q.th, u));
@@ -325,11 +334,11 @@ __device__ __forceinline__ void epi_psi_elem(const Ctx& c, const Params& P, cons
 
 // state blocks of rows described by rdesc, one warp per row
 __device__ __noinline__ void epi_state(int nu_it, double cf, double th, int nrows, int ysm, bool wt, int ncur,
-                                       double* rmax_io) {
+                                       double* rmax_io, bool pre = false, double cfn = 0.0) {
   const SParams& S = g_sp;
   const Ctx c = ctx_of();
   const Params& P = S.P;
-  const EpiConst q = epi_const(P, nu_it, cf, th, wt, ncur);
+  const EpiConst q = epi_const(P, nu_it, cf, th, wt, ncur, pre, cfn);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const size_t E = (size_t)c.E;
   const double* xs_s = c.bnd;
@@ -403,6 +412,10 @@ __device__ __noinline__ void epi_state(int nu_it, double cf, double th, int nrow
           stcg(P.xavg + (size_t)(e + 1) * c.NXP + i, na);
         }
         if (q.last) stcg(P.X + (size_t)(e + 1) * c.NXP + i, xi);
+        if (q.pre) {  // the next backward's fill of this element (bwd_tile step 1)
+          const double wsn = extrap(ns, yc[i], q.cfn), wzn = extrap(nz, yc[c.NXP + i], q.cfn);
+          const_cast<double*>(x)[i] = __dadd_rn(__dmul_rn(wsn, ds), __dmul_rn(wzn, dz));
+        }
       }
     }
   }
@@ -411,11 +424,11 @@ __device__ __noinline__ void epi_state(int nu_it, double cf, double th, int nrow
 
 // psi block of rows described by rdesc (component-major), u read from the rows
 __device__ __noinline__ void epi_psi_rows(int nu_it, double cf, double th, int nrows, int ysm, bool wt, int ncur,
-                                          double* rmax_io) {
+                                          double* rmax_io, bool pre = false, double cfn = 0.0) {
   const SParams& S = g_sp;
   const Ctx c = ctx_of();
   const Params& P = S.P;
-  const EpiConst q = epi_const(P, nu_it, cf, th, wt, ncur);
+  const EpiConst q = epi_const(P, nu_it, cf, th, wt, ncur, pre, cfn);
   const int k = threadIdx.x & (kKW - 1), g = threadIdx.x / kKW;
   double rmax = *rmax_io;
   if (k < c.nu) {
@@ -433,7 +446,8 @@ __device__ __noinline__ void epi_psi_rows(int nu_it, double cf, double th, int n
 // A in place (tmode 0: the CTA's only tile stays in shared memory), to the
 // tile's slot rows (tmode 1) or to HBM (tmode 2, streamed CTAs).
 // ----------------------------------------------------------------------------
-__device__ __noinline__ void bwd_tile(int ti, double cf, int ysm, int srow0, bool resident, int cur) {
+__device__ __noinline__ void bwd_tile(int ti, double cf, int ysm, int srow0, bool resident, int cur,
+                                      bool prefilled = false) {
   const SParams& S = g_sp;
   const Ctx c = ctx_of();
   const Params& P = S.P;
@@ -459,8 +473,9 @@ __device__ __noinline__ void bwd_tile(int ti, double cf, int ysm, int srow0, boo
     __syncthreads();
   }
   // (1) fill: s = D_sig w_sig + D_zeta w_zeta -> A ; psi^ = D_psi w_psi -> B
+  // (prefilled: the previous iteration's epilogue left exactly these values)
 #pragma unroll 1
-  for (int m = 0; m < kRowsPT; ++m) {
+  for (int m = 0; m < (prefilled ? 0 : kRowsPT); ++m) {
     const int r = g + kGroups * m;
     if (r >= nrows) break;
     const double* yc = slot_row(c, srow0 + r) + (size_t)ysm * c.YW;
@@ -858,8 +873,11 @@ __device__ __noinline__ void fwd_finish(int ti, int nu_it, double cf, double th,
   __syncthreads();
   TSMPC_MARK(P, 14, tm_);
   // psi and state blocks back to back: they write disjoint columns of the rows
-  epi_psi_rows(nu_it, cf, th, nrows, ysm, !resident || last, cur ^ 1, rmax);
-  epi_state(nu_it, cf, th, nrows, ysm, !resident || last, cur ^ 1, rmax);
+  // prefill: the next iteration of this launch starts its backward without the fill
+  const bool pre = S.split_heads && S.split_flags && nu_it + 1 < S.nu1;
+  const double cfn = pre ? P.coef[nu_it + 1] : 0.0;
+  epi_psi_rows(nu_it, cf, th, nrows, ysm, !resident || last, cur ^ 1, rmax, pre, cfn);
+  epi_state(nu_it, cf, th, nrows, ysm, !resident || last, cur ^ 1, rmax, pre, cfn);
   __syncthreads();
   TSMPC_MARK(P, 8, tm_);
 }
@@ -1622,7 +1640,9 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
     const int nn = nu + 1 < P.iters ? nu + 1 : nu;
     const double cf_n = P.coef[nn], th_n = P.theta[nn];
     if (do_a) {
-      for (int t = nt - 1; t >= 0; --t) bwd_tile(t, cf, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur);
+      for (int t = nt - 1; t >= 0; --t)
+        bwd_tile(t, cf, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur,
+                 S.split && S.split_heads && S.split_flags && nu > S.nu0);
       if (S.sharded && trunk) {
         grid.sync();
         head_prereduce();
