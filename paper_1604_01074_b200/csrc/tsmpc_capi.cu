@@ -753,6 +753,12 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
           if (pb->A[(size_t)i * nx + i] != 1.0) S.a_unit = 0;
         S.HS_LD = NVP + NXP;
         if (S.split) {
+          int* d_tpi;
+          double* d_tpv;
+          rc |= pl->upload(&d_tpi, hp.tpi.data(), hp.tpi.size());
+          rc |= pl->upload(&d_tpv, hp.tpv.data(), hp.tpv.size());
+          S.tpi = d_tpi;
+          S.tpv = d_tpv;
           rc |= pl->alloc(&pl->TR, (size_t)std::max(1, hp.n_trunk) * S.TR_LD);
           rc |= pl->alloc(&pl->SUBCTR, 4);
           S.split_flags = std::getenv("TSMPC_SPLIT_GRID") ? 0 : 1;

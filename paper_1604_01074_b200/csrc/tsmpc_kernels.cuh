@@ -175,6 +175,12 @@ struct SParams {
   unsigned int* sub_ctr;        // [trunk-CTA barrier, heads published, TR published] (zeroed per launch)
   int split_flags;              // directed signals between chain and trunk CTAs instead of grid barriers
   int a_unit;                   // A = I (a = 1 in every state component): chain recursions are plain sums
+  const int* tpi;               // split mode: combined trunk-forward operators (SparseHostPlan::tpi/tpv)
+  const double* tpv;
+  int M1_ptr, M1_col, M2_ptr, M2_col, M1_val, M2_val;
+  int n_tpi, n_tpv;
+  int tops;                     // 1: trunk CTAs stage tpv | tpi in their slot region at O_SLOT + O_TOPS
+  int O_TOPS;
   int split_heads, O_HSUM;      // chain CTAs publish their head values right after the fill, by
                                 // reductions ([sum beta_s | sum psi^ | sum G_d s | sum z] at O_HSUM)
 };

@@ -1336,39 +1336,36 @@ __device__ __noinline__ void trunk_needs() {
   auto evec_n = [&](int n, int i) -> double {
     return staged ? KYs[(size_t)n * SLD + P.KY_LD + c.NUP + i] : ldcg(P.evec + (size_t)nd[4 * n + 2] * c.NXP + i);
   };
-  if (S.split && staged) {
-    // split mode: S is only an intermediate (the chains get du / B du / x from TR),
-    // so each du_j is evaluated in one pass, re-deriving the Yz_j' and S_k it needs
-    // with the same operations in the same order as the three passes below
-    const int* lp = c.spi + S.Lr_ptr;
-    const int* lq = c.spi + S.Lr_idx;
-    const double* lv = c.spv + S.Lr_val;
-    const int* sp = c.spi + S.Lc_ptr;
-    const int* sq = c.spi + S.Lc_idx;
-    const double* sv = c.spv + S.Lc_val;
-    const int* bp = c.spi + S.Bc_ptr;
-    const int* bq = c.spi + S.Bc_idx;
-    const double* bv = c.spv + S.Bc_val;
+  if (S.split && staged && S.tops) {
+    // split mode: S is only an intermediate (the chains get du / B du / x from TR).
+    // du = M1 KY and B du = M2 KY with the combined operators of the planner
+    // (staged in this trunk CTA's slot region at launch), one pass; bv + e goes to
+    // the (free) S columns for the x walk below
+    const double* tv = s_dyn + S.O_SLOT + S.O_TOPS;
+    const int* ti = reinterpret_cast<const int*>(tv + S.n_tpv);
+    const int* m1p = ti + S.M1_ptr;
+    const int* m1c = ti + S.M1_col;
+    const double* m1v = tv + S.M1_val;
+    const int* m2p = ti + S.M2_ptr;
+    const int* m2c = ti + S.M2_col;
+    const double* m2v = tv + S.M2_val;
 #pragma unroll 1
-    for (int idx = threadIdx.x; idx < nn * nu; idx += kThreadsS) {
-      const int n = idx / nu, j = idx - n * nu;
-      double d = 0.0;
-#pragma unroll 1
-      for (int q = lp[j]; q < lp[j + 1]; ++q) {
-        const int k = lq[q];
-        double h = 0.0;
-#pragma unroll 1
-        for (int q2 = sp[k]; q2 < sp[k + 1]; ++q2) {
-          const int j2 = sq[q2];
-          double z = ky(n, c.NVP + c.NXP + j2);
-#pragma unroll 1
-          for (int q3 = bp[j2]; q3 < bp[j2 + 1]; ++q3) z = fma(bv[q3], ky(n, c.NVP + bq[q3]), z);
-          h = fma(sv[q2], z, h);
-        }
-        d = fma(lv[q], __dadd_rn(ky(n, k), h), d);
+    for (int idx = threadIdx.x; idx < nn * (nu + nx); idx += kThreadsS) {
+      const int n = idx / (nu + nx), r = idx - n * (nu + nx);
+      const double* kyr = KYs + (size_t)n * SLD;
+      double acc = 0.0;
+      if (r < nu) {
+#pragma unroll 4
+        for (int q = m1p[r]; q < m1p[r + 1]; ++q) acc = fma(m1v[q], kyr[m1c[q]], acc);
+        ND[(size_t)n * LD + UO + r] = acc;
+        stcg(S.TR + (size_t)nd[4 * n] * S.TR_LD + r, acc);  // du of the trunk row
+      } else {
+        const int i = r - nu;
+#pragma unroll 4
+        for (int q = m2p[i]; q < m2p[i + 1]; ++q) acc = fma(m2v[q], kyr[m2c[q]], acc);
+        stcg(S.TR + (size_t)nd[4 * n] * S.TR_LD + c.NUP + i, acc);  // B du of the trunk row
+        ND[(size_t)n * LD + i] = __dadd_rn(acc, evec_n(n, i));
       }
-      ND[(size_t)n * LD + UO + j] = d;
-      stcg(S.TR + (size_t)nd[4 * n] * S.TR_LD + j, d);  // du of the trunk row
     }
     __syncthreads();
   } else {
@@ -1428,7 +1425,7 @@ __device__ __noinline__ void trunk_needs() {
     const int* ri = c.spi + S.Br_idx;
     const double* rv = c.spv + S.Br_val;
 #pragma unroll 1
-    for (int idx = threadIdx.x; idx < nn * nx; idx += kThreadsS) {
+    for (int idx = threadIdx.x; idx < (S.split && staged && S.tops ? 0 : nn * nx); idx += kThreadsS) {
       const int n = idx / nx, i = idx - n * nx;
       double b = 0.0;
 #pragma unroll 1
@@ -1438,7 +1435,7 @@ __device__ __noinline__ void trunk_needs() {
       // write x in place without a copy-back pass
       ND[(size_t)n * LD + (S.split && staged ? 0 : c.NVP) + i] = __dadd_rn(b, evec_n(n, i));
     }
-    __syncthreads();
+    if (!(S.split && staged && S.tops)) __syncthreads();
     TSMPC_MARK(P, 13, tn_);
     // u = uhat + du (independent of the x pass below: no barrier in between)
 #pragma unroll 1
@@ -1604,6 +1601,15 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
     }
     cp_commit();
     cp_wait<0>();
+    __syncthreads();
+  }
+  if (S.split && S.tops && (int)blockIdx.x >= S.split_c0) {
+    double* tv = s_dyn + S.O_SLOT + S.O_TOPS;
+    int* ti = reinterpret_cast<int*>(tv + S.n_tpv);
+#pragma unroll 1
+    for (int i = threadIdx.x; i < S.n_tpv; i += kThreadsS) tv[i] = __ldg(S.tpv + i);
+#pragma unroll 1
+    for (int i = threadIdx.x; i < S.n_tpi; i += kThreadsS) ti[i] = __ldg(S.tpi + i);
     __syncthreads();
   }
   if (S.split && S.split_heads && (int)blockIdx.x < S.split_c0 && nt == 1) {

@@ -389,6 +389,42 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
     S.Lr_ptr = put(p4); S.Lr_idx = put(i4); S.Lr_val = putv(v4);
     S.n_spi = (int)out.spi.size();
     S.n_spv = (int)out.spv.size();
+    // combined trunk-forward operators on a KY row (split mode):
+    //   du = Lt (K + Ls'(Ypsi + B' Yx)) = M1 [K | Yx | Ypsi],  B du = (B M1) [K | Yx | Ypsi]
+    {
+      const int KY_LD = NVP + NXP + NUP;
+      std::vector<double> M1((size_t)nu * KY_LD, 0.0), M2((size_t)nx * KY_LD, 0.0);
+      std::vector<double> LsB((size_t)nv * nx, 0.0);  // Ls' B' (nv x nx)
+      for (int k = 0; k < nv; ++k)
+        for (int i = 0; i < nx; ++i) {
+          double a = 0.0;
+          for (int j = 0; j < nu; ++j) a += Lsd[(size_t)j * nv + k] * Bd[(size_t)i * nu + j];
+          LsB[(size_t)k * nx + i] = a;
+        }
+      for (int j = 0; j < nu; ++j)
+        for (int k = 0; k < nv; ++k) {
+          const double l = Lt[(size_t)j * nv + k];
+          if (l == 0.0) continue;
+          M1[(size_t)j * KY_LD + k] += l;
+          for (int i = 0; i < nx; ++i) M1[(size_t)j * KY_LD + NVP + i] += l * LsB[(size_t)k * nx + i];
+          for (int j2 = 0; j2 < nu; ++j2) M1[(size_t)j * KY_LD + NVP + NXP + j2] += l * Lsd[(size_t)j2 * nv + k];
+        }
+      for (int i = 0; i < nx; ++i)
+        for (int j = 0; j < nu; ++j) {
+          const double b = Bd[(size_t)i * nu + j];
+          if (b == 0.0) continue;
+          for (int col = 0; col < KY_LD; ++col) M2[(size_t)i * KY_LD + col] += b * M1[(size_t)j * KY_LD + col];
+        }
+      std::vector<int> q1, c1, q2, c2;
+      std::vector<double> w1, w2;
+      csr(nu, KY_LD, M1, false, q1, c1, w1);
+      csr(nx, KY_LD, M2, false, q2, c2, w2);
+      auto tput = [&](const std::vector<int>& v) { int o = (int)out.tpi.size(); out.tpi.insert(out.tpi.end(), v.begin(), v.end()); return o; };
+      auto tputv = [&](const std::vector<double>& v) { int o = (int)out.tpv.size(); out.tpv.insert(out.tpv.end(), v.begin(), v.end()); return o; };
+      S.M1_ptr = tput(q1); S.M1_col = tput(c1); S.M1_val = tputv(w1);
+      S.M2_ptr = tput(q2); S.M2_col = tput(c2); S.M2_val = tputv(w2);
+      if (out.tpv.empty()) out.tpv.push_back(0.0);
+    }
   }
 
   // ---- shared-memory layout (doubles)
@@ -544,6 +580,12 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
     const bool fits = (long long)sub_max * (2LL * ncomp_all + 1) <= (long long)S.slot_rows * S.slot_ld &&
                       (long long)need_max * sld <= (long long)kTileS * NUP;
     S.split_local = (split_n && fits && !std::getenv("TSMPC_SPLIT_GLOBAL_SWEEP")) ? 1 : 0;
+    // combined trunk-forward operators staged in the trunk CTAs' slot region
+    S.n_tpi = (int)out.tpi.size();
+    S.n_tpv = (int)out.tpv.size();
+    S.O_TOPS = S.split_local ? (int)even((long long)sub_max * (2LL * ncomp_all + 1)) : 0;
+    S.tops = (split_n && (long long)S.O_TOPS + S.n_tpv + (S.n_tpi + 1) / 2 + 1 <= (long long)S.slot_rows * S.slot_ld &&
+              (long long)need_max * sld <= (long long)kTileS * NUP && !std::getenv("TSMPC_NO_TOPS")) ? 1 : 0;
     if (std::getenv("TSMPC_PLAN_DEBUG"))
       std::fprintf(stderr, "plan_sparse: split %d (trunk CTAs %d from %d) local %d sub_max %d need_max %d\n",
                    S.split, split_n, nch_split, S.split_local, sub_max, need_max);

@@ -37,6 +37,11 @@ struct SparseHostPlan {
   std::vector<int> trunk_edge;      // trunk position -> edge
   std::vector<int> spi;             // sparse index pool
   std::vector<double> spv;          // sparse value pool
+  // split mode: trunk forward operators on a KY row [K | Yx | Ypsi] (pitch KY_LD),
+  // du = M1 KY and B du = M2 KY, CSR by row: tpi = [M1 ptr (nu+1) | M1 col | M2 ptr
+  // (nx+1) | M2 col], tpv = [M1 val | M2 val] (offsets in SParams)
+  std::vector<int> tpi;
+  std::vector<double> tpv;
   // sharding (rank of world): chains owned, per trunk position ownership of the heads
   int rank = 0, world = 1, owned_rows = 0, total_chains = 0;
   std::vector<unsigned char> towned;
