@@ -305,7 +305,7 @@ __device__ __forceinline__ EpiConst epi_const(const Params& P, int nu_it, double
 
 // psi block of row r, component k (k < n_u); u = the row's control component
 __device__ __forceinline__ void epi_psi_elem(const Ctx& c, const Params& P, const EpiConst& q, const int* d,
-                                             int ysm, int k, double u, double& rmax) {
+                                             int ysm, int k, double u, double& rmax, double ulo, double uhi) {
   const int e = d[0], st = d[1];
   double* row = s_dyn + d[4];
   const double* yc = row + (size_t)ysm * c.YW + 2 * c.NXP;
@@ -314,7 +314,7 @@ __device__ __forceinline__ void epi_psi_elem(const Ctx& c, const Params& P, cons
   const double w = extrap(yc[k], yp[k], q.cf);
   const double hp = __dmul_rn(u, dp);
   const double a = __dadd_rn(__dmul_rn(w, q.ilam), hp);
-  const double t = fmin(fmax(a, __dmul_rn(dp, c.bnd[3 * c.NXP + k])), __dmul_rn(dp, c.bnd[3 * c.NXP + c.NUP + k]));
+  const double t = fmin(fmax(a, __dmul_rn(dp, ulo)), __dmul_rn(dp, uhi));
   const double ny = __dadd_rn(w, __dmul_rn(q.lam, __dsub_rn(hp, t)));
   yp[k] = ny;
   if (q.pre) {  // the next backward's fill of this element (bwd_tile step 1)
@@ -346,6 +346,15 @@ __device__ __noinline__ void epi_state(int nu_it, double cf, double th, int nrow
   const double* xmx_s = c.bnd + 2 * c.NXP;
   const int N = c.N;
   double rmax = *rmax_io;
+  // the lane's bounds, hoisted (the row stores could alias them for the compiler)
+  double bxs[4], bmn[4], bmx[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int i = lane + 32 * m;
+    bxs[m] = i < c.nx ? xs_s[i] : 0.0;
+    bmn[m] = i < c.nx ? xmn_s[i] : 0.0;
+    bmx[m] = i < c.nx ? xmx_s[i] : 0.0;
+  }
 #pragma unroll 1
   for (int r = warp; r < nrows; r += kWarpsS) {
     const int* d = c.rdesc() + 5 * r;
@@ -368,8 +377,8 @@ __device__ __noinline__ void epi_state(int nu_it, double cf, double th, int nrow
         const double xi = x[i];
         ts[m] = __dadd_rn(__dmul_rn(ws[m], q.ilam), __dmul_rn(xi, ds));
         tz[m] = __dadd_rn(__dmul_rn(wz[m], q.ilam), __dmul_rn(xi, dz));
-        const double gs_ = __dsub_rn(fmax(ts[m], __dmul_rn(ds, xs_s[i])), ts[m]);
-        const double gz = __dsub_rn(fmin(fmax(tz[m], __dmul_rn(dz, xmn_s[i])), __dmul_rn(dz, xmx_s[i])), tz[m]);
+        const double gs_ = __dsub_rn(fmax(ts[m], __dmul_rn(ds, bxs[m])), ts[m]);
+        const double gz = __dsub_rn(fmin(fmax(tz[m], __dmul_rn(dz, bmn[m])), __dmul_rn(dz, bmx[m])), tz[m]);
         ss = fma(gs_, gs_, ss);
         sz = fma(gz, gz, sz);
       }
@@ -392,8 +401,8 @@ __device__ __noinline__ void epi_state(int nu_it, double cf, double th, int nrow
       if (i < c.nx) {
         const double xi = x[i];
         const double hs = __dmul_rn(xi, ds), hz = __dmul_rn(xi, dz);
-        const double ps = fmax(ts[m], __dmul_rn(ds, xs_s[i]));
-        const double pz = fmin(fmax(tz[m], __dmul_rn(dz, xmn_s[i])), __dmul_rn(dz, xmx_s[i]));
+        const double ps = fmax(ts[m], __dmul_rn(ds, bxs[m]));
+        const double pz = fmin(fmax(tz[m], __dmul_rn(dz, bmn[m])), __dmul_rn(dz, bmx[m]));
         const double t_s = __dadd_rn(ts[m], __dmul_rn(fs, __dsub_rn(ps, ts[m])));
         const double t_z = __dadd_rn(tz[m], __dmul_rn(fz, __dsub_rn(pz, tz[m])));
         const double ns = __dadd_rn(ws[m], __dmul_rn(q.lam, __dsub_rn(hs, t_s)));
@@ -432,10 +441,12 @@ __device__ __noinline__ void epi_psi_rows(int nu_it, double cf, double th, int n
   const int k = threadIdx.x & (kKW - 1), g = threadIdx.x / kKW;
   double rmax = *rmax_io;
   if (k < c.nu) {
+    // the component's bounds, hoisted (the row stores could alias them for the compiler)
+    const double ulo = c.bnd[3 * c.NXP + k], uhi = c.bnd[3 * c.NXP + c.NUP + k];
 #pragma unroll 1
     for (int r = g; r < nrows; r += kGroups) {
       const int* d = c.rdesc() + 5 * r;
-      epi_psi_elem(c, P, q, d, ysm, k, s_dyn[d[3] + k], rmax);
+      epi_psi_elem(c, P, q, d, ysm, k, s_dyn[d[3] + k], rmax, ulo, uhi);
     }
   }
   *rmax_io = rmax;
@@ -877,6 +888,7 @@ __device__ __noinline__ void fwd_finish(int ti, int nu_it, double cf, double th,
   const bool pre = S.split_heads && S.split_flags && nu_it + 1 < S.nu1;
   const double cfn = pre ? P.coef[nu_it + 1] : 0.0;
   epi_psi_rows(nu_it, cf, th, nrows, ysm, !resident || last, cur ^ 1, rmax, pre, cfn);
+  TSMPC_MARK(P, 15, tm_);
   epi_state(nu_it, cf, th, nrows, ysm, !resident || last, cur ^ 1, rmax, pre, cfn);
   __syncthreads();
   TSMPC_MARK(P, 8, tm_);
