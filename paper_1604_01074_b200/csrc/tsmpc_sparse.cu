@@ -110,9 +110,15 @@ __device__ __forceinline__ void signal_arrive(unsigned int* ctr) {
     atomicAdd(ctr, 1u);
   }
 }
+// spin-waits give up after ~2 s (a plan inconsistency must fail the launch, not
+// hang the GPU)
+constexpr long long kSpinLimit = 4000000000LL;
+
 __device__ __forceinline__ void signal_wait(unsigned int* ctr, unsigned int target) {
   if (threadIdx.x == 0) {
+    const long long t0 = clock64();
     while (*((volatile unsigned int*)ctr) < target) {
+      if (clock64() - t0 > kSpinLimit) __trap();
     }
     __threadfence();
   }
@@ -901,7 +907,9 @@ __device__ __forceinline__ void trunk_barrier(unsigned int* ctr, unsigned int n,
   if (threadIdx.x == 0) {
     __threadfence();
     atomicAdd(ctr, 1u);
+    const long long t0 = clock64();
     while (*((volatile unsigned int*)ctr) < target) {
+      if (clock64() - t0 > kSpinLimit) __trap();
     }
     __threadfence();
   }
