@@ -173,3 +173,28 @@ def test_lockstep_dykstra_gap_equals_two_pass(tree_name, monkeypatch):
         plan.set_cache(W["caches"][0], W["model"])
         gaps.append(plan.solve(W["p"], 120, 0.05, theta=th, coef=cf, keep_device=True)["gap"])
     assert np.isfinite(gaps[0]) and gaps[0] == gaps[1] == gaps[2], gaps
+
+
+@pytest.mark.parametrize("tree_name", ["SMPC1", "SMPC3"])
+def test_split_mode_matches_grid_barrier_mode(tree_name, monkeypatch):
+    """Split mode (trunk on spare CTAs, directed signals, heads published from
+    the fill, affine trunk terms, prefilled backward, combined trunk operators)
+    against the two-grid-barrier plan of the same tree: same iterates up to
+    summation order."""
+    import bench
+    W = bench.build_workload(tree_name)
+    th, cf = engine.theta_schedule(200)
+    outs = []
+    for env in (None, "TSMPC_NO_SPLIT"):
+        if env:
+            monkeypatch.setenv(env, "1")
+        plan = DevicePlan(W["model"], W["tree"], W["factor"], W["scaling"])
+        assert plan.info()["trunk_ctas"] == (0 if env else plan.info()["trunk_ctas"])
+        plan.set_cache(W["caches"][0], W["model"])
+        outs.append(plan.solve(W["p"], 200, 0.05, theta=th, coef=cf, record_residuals=True))
+    a, b = outs
+    assert a["kernel_launches"] >= 1
+    for f in ("u0", "x", "u", "x_avg", "u_avg", "dual_sig", "dual_zeta", "dual_psi"):
+        assert rel_err(a[f], b[f]) <= 1e-9, (f, rel_err(a[f], b[f]))
+    np.testing.assert_allclose(a["resid_trace"], b["resid_trace"], rtol=1e-8, atol=1e-9)
+    assert abs(a["gap"] - b["gap"]) <= 1e-8 * max(1.0, abs(b["gap"]))
