@@ -135,7 +135,6 @@ __device__ __forceinline__ void signal_wait(unsigned int* ctr, unsigned int targ
 constexpr int kKW = 128;                    // component lanes per row group (n_x, n_u <= 128)
 constexpr int kGroups = kThreadsS / kKW;    // 4 row groups
 constexpr int kRowsPT = kTileS / kGroups;   // rows per thread in a full tile
-constexpr int kSeqTrunk = 0;                // trunks up to this size are swept by one thread per component (slower on B200: off)
 constexpr int kCh = 8;                      // rows per register chunk of the chain scans
 
 struct Ctx {
@@ -992,10 +991,10 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur, int part) {
     }
   }
   if (!(part & 2)) return;
-  // (1b) chain-head children (one parallel round of loads), childless fold
-#pragma unroll 1
-  for (int idx = threadIdx.x; idx < T * nc; idx += kThreadsS) {
-    const int tp = idx / nc, k = idx - tp * nc, q = c_lo + k;
+  if (part & 1) __syncthreads();  // the steps below map elements to threads differently
+  // per (trunk position, component) steps of the recursion
+  auto heads = [&](int tp, int k) {  // (1b) chain-head children, childless fold
+    const int q = c_lo + k, idx = tp * nc + k;
     const int* ps = pos + 8 * tp;
     const int h0 = ps[5], nh = ps[6];
     double z = Zs[idx], x = Xs[idx];
@@ -1041,97 +1040,84 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur, int part) {
     }
     Zs[idx] = z;
     Xs[idx] = x;
-  }
+  };
+  auto up = [&](int tp, int k, int l) {  // (2) add trunk children; level 0 also scales
+    const int q = c_lo + k, idx = tp * nc + k;
+    const int* ps = pos + 8 * tp;
+    const int c0 = ps[3], n = ps[4];
+    double zs = 0.0, xs = 0.0;
+#pragma unroll 1
+    for (int m = 0; m < n; ++m) {
+      const int cp = tch[c0 + m];
+      zs = __dadd_rn(zs, Zs[cp * nc + k]);
+      xs = __dadd_rn(xs, Xs[cp * nc + k]);
+    }
+    double zn;
+    if (q >= c.nv && q < c.nv + c.nx) {
+      const double xiq = __dadd_rn(Xs[idx], __dmul_rn(xs, adiag[q - c.nv]));
+      Xs[idx] = xiq;
+      zn = __dadd_rn(xiq, zs);
+    } else {
+      zn = __dadd_rn(Zs[idx], zs);
+    }
+    Zs[idx] = l == 0 ? __dmul_rn(zn, Ip[tp]) : zn;
+  };
+  auto down = [&](int tp, int k) {  // (3) K_a, Y_a = own * inv2p_a + parent's
+    const int idx = tp * nc + k;
+    const int pp = pos[8 * tp + 2];
+    double v = __dmul_rn(Zs[idx], Ip[tp]);
+    if (pp >= 0) v = __dadd_rn(v, Zs[pp * nc + k]);
+    Zs[idx] = v;
+  };
+  auto store = [&](int tp, int k) {  // (4) KY column
+    const int q = c_lo + k;
+    const int col = q < c.nv ? q : (q < c.nv + c.nx ? c.NVP + (q - c.nv) : c.NVP + c.NXP + (q - c.nv - c.nx));
+    stcg(P.KY + (size_t)tp * P.KY_LD + col, Zs[tp * nc + k]);
+  };
+#pragma unroll 1
+  for (int idx = threadIdx.x; idx < T * nc; idx += kThreadsS) heads(idx / nc, idx % nc);
   __syncthreads();
   TSMPC_MARK(P, 14, ts_);
-  if (T <= kSeqTrunk) {
-    // small trunk: one thread per component walks the levels (no level barriers)
-    if (threadIdx.x < nc) {
-      const int k = threadIdx.x, q = c_lo + k;
-      const bool xq = q >= c.nv && q < c.nv + c.nx;
-      const double aq = xq ? adiag[q - c.nv] : 0.0;
+  if (S.split) {
+    // levels: a warp per component (lanes over trunk positions), so every level
+    // step of one component's recursion stays inside the warp (no block barriers)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll 1
-      for (int tp = T - 1; tp >= 0; --tp) {  // children have larger positions
-        const int* ps = pos + 8 * tp;
-        const int c0 = ps[3], n = ps[4];
-        double zs = 0.0, xs = 0.0;
+    for (int k = warp; k < nc; k += kWarpsS) {
 #pragma unroll 1
-        for (int m = 0; m < n; ++m) {
-          const int cp = tch[c0 + m];
-          zs = __dadd_rn(zs, Zs[cp * nc + k]);
-          xs = __dadd_rn(xs, Xs[cp * nc + k]);
-        }
-        const int idx = tp * nc + k;
-        if (xq) {
-          const double xiq = __dadd_rn(Xs[idx], __dmul_rn(xs, aq));
-          Xs[idx] = xiq;
-          Zs[idx] = __dadd_rn(xiq, zs);
-        } else {
-          Zs[idx] = __dadd_rn(Zs[idx], zs);
-        }
+      for (int l = nlev - 2; l >= 0; --l) {
+#pragma unroll 1
+        for (int tp = lev[l] + lane; tp < lev[l + 1]; tp += 32) up(tp, k, l);
+        __syncwarp();
       }
 #pragma unroll 1
-      for (int tp = 0; tp < T; ++tp) {  // parents have smaller positions
-        const int pp = pos[8 * tp + 2];
-        const int idx = tp * nc + k;
-        double v = __dmul_rn(Zs[idx], Ip[tp]);
-        if (pp >= 0) v = __dadd_rn(v, Zs[pp * nc + k]);
-        Zs[idx] = v;
+      for (int l = nlev >= 2 ? 1 : 0; l < nlev; ++l) {
+#pragma unroll 1
+        for (int tp = lev[l] + lane; tp < lev[l + 1]; tp += 32) down(tp, k);
+        __syncwarp();
       }
+#pragma unroll 1
+      for (int tp = lane; tp < T; tp += 32) store(tp, k);
     }
-    __syncthreads();
-  } else {
-  // (2) bottom-up over edge-stage levels: add trunk children (the deepest level
-  // has none: done above); level 0 also takes its top-down step (no parent)
+    return;
+  }
+  // bottom-up over edge-stage levels (the deepest level has no trunk children:
+  // done above); level 0 also takes its top-down step (no parent)
 #pragma unroll 1
   for (int l = nlev - 2; l >= 0; --l) {
 #pragma unroll 1
-    for (int idx = lev[l] * nc + threadIdx.x; idx < lev[l + 1] * nc; idx += kThreadsS) {
-      const int tp = idx / nc, k = idx - tp * nc, q = c_lo + k;
-      const int* ps = pos + 8 * tp;
-      const int c0 = ps[3], n = ps[4];
-      double zs = 0.0, xs = 0.0;
-#pragma unroll 1
-      for (int m = 0; m < n; ++m) {
-        const int cp = tch[c0 + m];
-        zs = __dadd_rn(zs, Zs[cp * nc + k]);
-        xs = __dadd_rn(xs, Xs[cp * nc + k]);
-      }
-      double zn;
-      if (q >= c.nv && q < c.nv + c.nx) {
-        const double xiq = __dadd_rn(Xs[idx], __dmul_rn(xs, adiag[q - c.nv]));
-        Xs[idx] = xiq;
-        zn = __dadd_rn(xiq, zs);
-      } else {
-        zn = __dadd_rn(Zs[idx], zs);
-      }
-      Zs[idx] = l == 0 ? __dmul_rn(zn, Ip[tp]) : zn;
-    }
+    for (int idx = lev[l] * nc + threadIdx.x; idx < lev[l + 1] * nc; idx += kThreadsS) up(idx / nc, idx % nc, l);
     __syncthreads();
   }
-  // (3) top-down: K_a, Y_a = own * inv2p_a + parent's
 #pragma unroll 1
   for (int l = nlev >= 2 ? 1 : 0; l < nlev; ++l) {
 #pragma unroll 1
-    for (int idx = lev[l] * nc + threadIdx.x; idx < lev[l + 1] * nc; idx += kThreadsS) {
-      const int tp = idx / nc, k = idx - tp * nc;
-      const int* ps = pos + 8 * tp;
-      const int pp = ps[2];
-      double v = __dmul_rn(Zs[idx], Ip[tp]);
-      if (pp >= 0) v = __dadd_rn(v, Zs[pp * nc + k]);
-      Zs[idx] = v;
-    }
+    for (int idx = lev[l] * nc + threadIdx.x; idx < lev[l + 1] * nc; idx += kThreadsS) down(idx / nc, idx % nc);
     __syncthreads();
   }
-  }
   TSMPC_MARK(P, 15, ts_);
-  // (4) KY columns of this slice
 #pragma unroll 1
-  for (int idx = threadIdx.x; idx < T * nc; idx += kThreadsS) {
-    const int tp = idx / nc, k = idx - tp * nc, q = c_lo + k;
-    const int col = q < c.nv ? q : (q < c.nv + c.nx ? c.NVP + (q - c.nv) : c.NVP + c.NXP + (q - c.nv - c.nx));
-    stcg(P.KY + (size_t)tp * P.KY_LD + col, Zs[idx]);
-  }
+  for (int idx = threadIdx.x; idx < T * nc; idx += kThreadsS) store(idx / nc, idx % nc);
 }
 
 // ----------------------------------------------------------------------------
