@@ -53,7 +53,8 @@ struct tsmpc_plan {
   Params base{};
   EdgeCtx ctx{};
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
+  cudaStream_t stream2 = nullptr;   // result read-back, overlapping the duality gap
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev_out = nullptr;
   long long launches = 0;  // kernels launched by the current API call
   std::vector<void*> allocs;
   std::vector<int64_t> stage_starts;
@@ -139,10 +140,10 @@ struct tsmpc_plan {
                          cudaMemcpyHostToDevice, stream));
     return TSMPC_OK;
   }
-  int get_rows(double* dst, int w, const double* src, int ld, int rows) {
+  int get_rows(double* dst, int w, const double* src, int ld, int rows, cudaStream_t s = nullptr) {
     if (rows == 0 || w == 0 || dst == nullptr) return TSMPC_OK;
     CU(cudaMemcpy2DAsync(dst, w * sizeof(double), src, ld * sizeof(double), w * sizeof(double), rows,
-                         cudaMemcpyDeviceToHost, stream));
+                         cudaMemcpyDeviceToHost, s ? s : stream));
     return TSMPC_OK;
   }
   ~tsmpc_plan() {
@@ -152,6 +153,11 @@ struct tsmpc_plan {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (ev2) cudaEventDestroy(ev2);
+    if (ev_out) cudaEventDestroy(ev_out);
+    if (stream2) {
+      cudaStreamSynchronize(stream2);
+      cudaStreamDestroy(stream2);
+    }
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -401,8 +407,10 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
   pl->device = device;
   if (cudaSetDevice(device) != cudaSuccess) { fail(TSMPC_ERR_CUDA, "cudaSetDevice failed"); return bail(0); }
   if (cudaStreamCreateWithFlags(&pl->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&pl->stream2, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&pl->ev0) != cudaSuccess || cudaEventCreate(&pl->ev1) != cudaSuccess ||
-      cudaEventCreate(&pl->ev2) != cudaSuccess) {
+      cudaEventCreate(&pl->ev2) != cudaSuccess ||
+      cudaEventCreateWithFlags(&pl->ev_out, cudaEventDisableTiming) != cudaSuccess) {
     fail(TSMPC_ERR_CUDA, "stream/event creation failed");
     return bail(0);
   }
@@ -1388,28 +1396,37 @@ int solve_finish(tsmpc_plan* pl, const SolveState& st, int32_t flags, tsmpc_resu
   // keep the last iterate before the gap's solve step reuses X / U
   CU(cudaMemcpyAsync(pl->XL, pl->X, sizeof(double) * (size_t)pl->n_nodes * NXP, cudaMemcpyDeviceToDevice, pl->stream));
   CU(cudaMemcpyAsync(pl->UL, pl->U, sizeof(double) * (size_t)E * NUP, cudaMemcpyDeviceToDevice, pl->stream));
+  // the results are final here (the gap only reads them): read them back on the
+  // copy stream while the gap runs
+  CU(cudaEventRecord(pl->ev_out, pl->stream));
+  CU(cudaStreamWaitEvent(pl->stream2, pl->ev_out, 0));
+  cudaStream_t cs = pl->stream2;
+  std::vector<unsigned long long> rbits(nres);
+  CU(cudaMemcpyAsync(rbits.data(), pl->RESID, sizeof(unsigned long long) * nres, cudaMemcpyDeviceToHost, cs));
+  if (pl->get_rows(out->u0, nu, pl->UAVG, NUP, 1, cs)) return TSMPC_ERR_CUDA;
+  if (!(flags & TSMPC_KEEP_DEVICE)) {
+    int rc = 0;
+    rc |= pl->get_rows(out->x, nx, pl->XL, NXP, pl->n_nodes, cs);
+    rc |= pl->get_rows(out->u, nu, pl->UL, NUP, E, cs);
+    rc |= pl->get_rows(out->x_avg, nx, pl->XAVG, NXP, pl->n_nodes, cs);
+    rc |= pl->get_rows(out->u_avg, nu, pl->UAVG, NUP, E, cs);
+    rc |= pl->get_rows(out->dual_sig, nx, yfin, NXP, E, cs);
+    rc |= pl->get_rows(out->dual_zeta, nx, yfin + (size_t)E * NXP, NXP, E, cs);
+    rc |= pl->get_rows(out->dual_psi, nu, yfin + 2 * (size_t)E * NXP, NUP, E, cs);
+    if (rc) return rc;
+  }
   double gap = NAN;
   if (!(flags & TSMPC_SKIP_GAP) && !pl->sharded) {
     int rc = compute_gap(pl, yfin, &gap);
-    if (rc) return rc;
+    if (rc) {
+      cudaStreamSynchronize(cs);
+      return rc;
+    }
   }
   CU(cudaEventRecord(pl->ev2, pl->stream));
   out->gap = gap;
   out->iterations = done;
-  std::vector<unsigned long long> rbits(nres);
-  CU(cudaMemcpyAsync(rbits.data(), pl->RESID, sizeof(unsigned long long) * nres, cudaMemcpyDeviceToHost, pl->stream));
-  if (pl->get_rows(out->u0, nu, pl->UAVG, NUP, 1)) return TSMPC_ERR_CUDA;
-  if (!(flags & TSMPC_KEEP_DEVICE)) {
-    int rc = 0;
-    rc |= pl->get_rows(out->x, nx, pl->XL, NXP, pl->n_nodes);
-    rc |= pl->get_rows(out->u, nu, pl->UL, NUP, E);
-    rc |= pl->get_rows(out->x_avg, nx, pl->XAVG, NXP, pl->n_nodes);
-    rc |= pl->get_rows(out->u_avg, nu, pl->UAVG, NUP, E);
-    rc |= pl->get_rows(out->dual_sig, nx, yfin, NXP, E);
-    rc |= pl->get_rows(out->dual_zeta, nx, yfin + (size_t)E * NXP, NXP, E);
-    rc |= pl->get_rows(out->dual_psi, nu, yfin + 2 * (size_t)E * NXP, NUP, E);
-    if (rc) return rc;
-  }
+  CU(cudaStreamSynchronize(cs));
   CU(cudaStreamSynchronize(pl->stream));
   float ms = 0.f;
   CU(cudaEventElapsedTime(&ms, pl->ev0, pl->ev1));
