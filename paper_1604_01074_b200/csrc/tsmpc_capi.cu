@@ -580,11 +580,9 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
   P.scaled = scaled ? 1 : 0;
 
   int rc = 0;
-  const double* d_c = nullptr;
   double *d_W1f, *d_W2f, *d_adiag, *d_A, *d_xs, *d_xmin, *d_xmax, *d_umin, *d_umax, *d_sig, *d_zeta, *d_psi,
       *d_inv2p, *d_pe, *d_Wu, *d_E, *d_EpinvT, *d_B;
   int *d_anc, *d_cs, *d_ce, *d_est, *d_lt, *d_ts, *d_sr, *d_re;
-  (void)d_c;
   rc |= pl->upload(&d_W1f, W1f.data(), W1f.size());
   rc |= pl->upload(&d_W2f, W2f.data(), W2f.size());
   rc |= pl->upload(&d_adiag, adiag.data(), adiag.size());

@@ -157,7 +157,6 @@ struct Ctx {
   __device__ double* B() const { return work + kTileS * LA; }
   __device__ const double* adiag() const { return bnd + 3 * NXP + 2 * NUP; }
   __device__ const double* proot() const { return bnd + 4 * NXP + 2 * NUP; }
-  __device__ double* fac() const { return red + kTileS * 8; }
   __device__ int* rdesc() const { return reinterpret_cast<int*>(red + kTileS * 10); }
   const double* psi_g;  // psi_stage in HBM when the table does not fit shared memory
   __device__ double dpsi(int st, int k) const {
@@ -1756,6 +1755,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
         if ((int)blockIdx.x >= S.split_c0) trunk_own_rows(nu, cf, th, cur, &rmax);
         for (int t = 0; t < nt; ++t) fwd_finish(t, nu, cf, th, ysm, resident, cur, &rmax);
         TSMPC_MARK(P, 3, tb_s);
+        (void)tb_s;
       } else {
         for (int t = 0; t < nt; ++t)
           fwd_tile(t, nu, cf, th, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur, &rmax);
