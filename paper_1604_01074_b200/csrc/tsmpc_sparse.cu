@@ -1703,8 +1703,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
         TSMPC_MARK(P, 3, tb_);
       }
     } else if (do_b) {
-      long long tb_s = 0;
-      (void)tb_s;
+      [[maybe_unused]] long long tb_s = 0;  // phase timers only
       if (trunk && S.split) {
         // trunk CTAs: sweep, barrier among themselves, trunk forward (-> TR) and
         // trunk-row epilogues; chain CTAs meanwhile: forward with zero trunk input
@@ -1755,7 +1754,6 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
         if ((int)blockIdx.x >= S.split_c0) trunk_own_rows(nu, cf, th, cur, &rmax);
         for (int t = 0; t < nt; ++t) fwd_finish(t, nu, cf, th, ysm, resident, cur, &rmax);
         TSMPC_MARK(P, 3, tb_s);
-        (void)tb_s;
       } else {
         for (int t = 0; t < nt; ++t)
           fwd_tile(t, nu, cf, th, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur, &rmax);
