@@ -297,14 +297,7 @@ __device__ __noinline__ void bwd_tile(const Params& P, int tile, int nu) {
   const int* const edge = SM_EDGE(P);
   const int* const slo = SM_LO(P);
   const int* const shi = SM_HI(P);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int E = P.n_edges;
-  const int cur = (P.slot0 + nu) & 1;
-  const double* __restrict__ Y = P.ybuf[cur];
-  const double* __restrict__ Yp = P.ybuf[cur ^ 1];
-  const bool apg = P.mode == kModeApg;
-  const double c = apg ? P.coef[nu] : 0.0;
-  const size_t zoff = (size_t)E * P.NXP, poff = 2 * (size_t)E * P.NXP;
+  const int tid = threadIdx.x;
 
   // (1) operand rows [s | psi^] + GEMM-1 bias beta (warp per row)
   fill_rows(P, nu, nrows);
