@@ -38,18 +38,24 @@ def test_solve_step_matches_reference(name):
     assert rel_err(out.u, z["s_u"]) <= 1e-11
 
 
-@pytest.mark.parametrize("path", ["sparse", "dense"])
+@pytest.mark.parametrize("path", ["sparse", "sparse-nosplit", "dense"])
 @pytest.mark.parametrize("name", ALL_CASES)
 def test_apg_solve_matches_reference(name, path, monkeypatch):
-    """Both persistent kernels: the structured-basis sparse kernel (default when A
-    is diagonal) and the dense fused-operator DMMA kernel (TSMPC_FORCE_DENSE)."""
+    """Every persistent-kernel path: the structured-basis sparse kernel (default
+    when A is diagonal; split mode where the plan allows it), the same kernel with
+    split mode off (two grid barriers per iteration), and the dense fused-operator
+    DMMA kernel (TSMPC_FORCE_DENSE)."""
     c = load_case(name)
     z = c.z
     monkeypatch.setenv("TSMPC_FORCE_DENSE", "1" if path == "dense" else "0")
+    if path == "sparse-nosplit":
+        monkeypatch.setenv("TSMPC_NO_SPLIT", "1")
     plan = _plan(c)
     info = plan.info()
     diag = np.count_nonzero(c.model.A - np.diag(np.diag(c.model.A))) == 0
-    assert info["sparse"] == (1 if (path == "sparse" and diag) else 0), info["path"]
+    assert info["sparse"] == (1 if (path != "dense" and diag) else 0), info["path"]
+    if path == "sparse-nosplit":
+        assert info["trunk_ctas"] == 0
     th, cf = engine.theta_schedule(c.iters)
     out = plan.solve(c.p, c.iters, c.lam, theta=th, coef=cf)
     for f in ("u0", "x", "u", "x_avg", "u_avg"):
