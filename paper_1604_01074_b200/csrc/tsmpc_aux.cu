@@ -214,8 +214,8 @@ __device__ double smooth_term(const EdgeCtx& c, int e, const double* U, int ldu,
   __syncwarp();
   double quad = 0.0;
   for (int j = lane; j < c.nu; j += 32) {
-    double wd = 0.0;
-    for (int k = 0; k < c.nu; ++k) wd = fma(c.Wu[(size_t)j * c.nu + k], sh[k], wd);
+    double wd = 0.0;  // non-zeros of row j of Wu, ascending columns (diagonal for water networks)
+    for (int q = c.wu_ptr[j]; q < c.wu_ptr[j + 1]; ++q) wd = fma(c.wu_val[q], sh[c.wu_idx[q]], wd);
     quad = fma(sh[j], wd, quad);
   }
   __syncwarp();

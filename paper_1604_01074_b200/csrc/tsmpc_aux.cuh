@@ -29,6 +29,8 @@ struct EdgeCtx {
   const int *er_ptr, *er_idx, *pc_ptr, *pc_idx;
   const double *er_val, *pc_val;
   int er_nnz, pc_nnz;
+  const int *wu_ptr, *wu_idx;   // Wu by row (CSR): the smooth cost's quadratic form
+  const double* wu_val;
 };
 
 struct ProxArgs {

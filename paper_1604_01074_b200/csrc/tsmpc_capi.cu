@@ -845,6 +845,23 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
     if (rc) return bail(0);
     c.er_ptr = d_erp; c.er_idx = d_eri; c.er_val = d_erv; c.er_nnz = (int)eri.size();
     c.pc_ptr = d_pcp; c.pc_idx = d_pci; c.pc_val = d_pcv; c.pc_nnz = (int)pci.size();
+    {  // Wu by row for the gap's smooth cost
+      std::vector<int> wp{0}, wi;
+      std::vector<double> wv;
+      for (int j = 0; j < nu; ++j) {
+        for (int k = 0; k < nu; ++k)
+          if (pb->Wu[(size_t)j * nu + k] != 0.0) { wi.push_back(k); wv.push_back(pb->Wu[(size_t)j * nu + k]); }
+        wp.push_back((int)wi.size());
+      }
+      if (wi.empty()) { wi.push_back(0); wv.push_back(0.0); }
+      int *d_wp, *d_wi;
+      double* d_wv;
+      rc |= pl->upload(&d_wp, wp.data(), wp.size());
+      rc |= pl->upload(&d_wi, wi.data(), wi.size());
+      rc |= pl->upload(&d_wv, wv.data(), wv.size());
+      if (rc) return bail(0);
+      c.wu_ptr = d_wp; c.wu_idx = d_wi; c.wu_val = d_wv;
+    }
     // junction rows with disjoint flow supports -> one Dykstra component per row
     std::vector<int> owner(nu, -1);
     bool disjoint = ne > 0;
