@@ -732,6 +732,26 @@ __global__ void gap_propagate_stage_kernel(EdgeCtx c, int n0, int n1, double* xf
   }
 }
 
+// All stages at once when A is diagonal: each (node, component) replays its root
+// path top-down with the operations of gap_propagate_stage_kernel, in the same
+// order (identical values), so one launch replaces N stage launches.
+__global__ void gap_propagate_paths_kernel(EdgeCtx c, int n_nodes, double* xf, const double* __restrict__ ub) {
+  const int total = (n_nodes - 1) * c.nx;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
+    const int n = 1 + k / c.nx, i = k % c.nx;
+    int path[kPropMaxDepth];
+    int m = 0;
+    for (int v = n; v > 0 && m < kPropMaxDepth; v = c.anc[v]) path[m++] = v;
+    const double a = c.a_diag[i];
+    double x = xf[i];  // root row (the initial state)
+    for (int j = m - 1; j >= 0; --j) {
+      const size_t oe = (size_t)(path[j] - 1) * c.NXP + i;
+      x = (x * a + ub[oe]) + c.gdd[oe];
+    }
+    xf[(size_t)n * c.NXP + i] = x;
+  }
+}
+
 // Primal side, part 2: smooth cost of u_feas and soft state cost (engine.py:347-364).
 __global__ void gap_primal_terms_kernel(EdgeCtx c, const double* __restrict__ uf,
                                         const double* __restrict__ xf, double* cols) {

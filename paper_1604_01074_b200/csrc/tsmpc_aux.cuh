@@ -75,6 +75,8 @@ __global__ void gap_dykstra_coop_kernel(EdgeCtx c, const double* __restrict__ u0
                                         unsigned long long* slots, double* st, double* uf);
 __global__ void gap_ub_kernel(EdgeCtx c, const double* uf, double* ub);
 __global__ void gap_propagate_stage_kernel(EdgeCtx c, int n0, int n1, double* xf, const double* ub);
+constexpr int kPropMaxDepth = 64;  // deepest tree for gap_propagate_paths_kernel
+__global__ void gap_propagate_paths_kernel(EdgeCtx c, int n_nodes, double* xf, const double* ub);
 __global__ void gap_primal_terms_kernel(EdgeCtx c, const double* uf, const double* xf, double* cols);
 
 __global__ void apg_persistent_kernel(const __grid_constant__ Params P);

@@ -1253,11 +1253,18 @@ static int compute_gap(tsmpc_plan* pl, const double* yfinal, double* gap) {
   gap_ub_kernel<<<G, 256, 0, pl->stream>>>(c, pl->UF, pl->UB);
   CU(cudaGetLastError());
   CU(cudaMemcpyAsync(pl->XF, pl->P, sizeof(double) * pl->NXP, cudaMemcpyDeviceToDevice, pl->stream));
-  for (int j = 0; j < pl->N; ++j) {
-    const int n0 = (int)pl->stage_starts[j + 1], n1 = (int)pl->stage_starts[j + 2];
-    const int total = (n1 - n0) * pl->nx;
-    gap_propagate_stage_kernel<<<std::max(1, std::min((total + 255) / 256, 4096)), 256, 0, pl->stream>>>(
-        c, n0, n1, pl->XF, pl->UB);
+  if (c.a_diag && pl->N <= kPropMaxDepth) {  // every stage in one launch (root paths)
+    const int total = (pl->n_nodes - 1) * pl->nx;
+    gap_propagate_paths_kernel<<<std::max(1, std::min((total + 255) / 256, 4096)), 256, 0, pl->stream>>>(
+        c, pl->n_nodes, pl->XF, pl->UB);
+    pl->launches -= pl->N - 1;
+  } else {
+    for (int j = 0; j < pl->N; ++j) {
+      const int n0 = (int)pl->stage_starts[j + 1], n1 = (int)pl->stage_starts[j + 2];
+      const int total = (n1 - n0) * pl->nx;
+      gap_propagate_stage_kernel<<<std::max(1, std::min((total + 255) / 256, 4096)), 256, 0, pl->stream>>>(
+          c, n0, n1, pl->XF, pl->UB);
+    }
   }
   CU(cudaGetLastError());
   gap_primal_terms_kernel<<<G, 256, 0, pl->stream>>>(c, pl->UF, pl->XF, pl->COLS);
