@@ -705,8 +705,8 @@ __global__ void gap_ub_kernel(EdgeCtx c, const double* __restrict__ uf, double* 
     for (int j = lane; j < c.nu; j += 32) shm[wl][j] = uf[(size_t)e * c.NUP + j];
     __syncwarp();
     for (int i = lane; i < c.nx; i += 32) {
-      double s = 0.0;
-      for (int j = 0; j < c.nu; ++j) s = fma(shm[wl][j], c.B[(size_t)i * c.nu + j], s);
+      double s = 0.0;  // non-zeros of row i of B, ascending columns
+      for (int q = c.bq_ptr[i]; q < c.bq_ptr[i + 1]; ++q) s = fma(shm[wl][c.bq_idx[q]], c.bq_val[q], s);
       ub[(size_t)e * c.NXP + i] = s;
     }
     __syncwarp();

@@ -31,6 +31,8 @@ struct EdgeCtx {
   int er_nnz, pc_nnz;
   const int *wu_ptr, *wu_idx;   // Wu by row (CSR): the smooth cost's quadratic form
   const double* wu_val;
+  const int *bq_ptr, *bq_idx;   // B by row (CSR): ub = u B'
+  const double* bq_val;
 };
 
 struct ProxArgs {

@@ -862,6 +862,23 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
       if (rc) return bail(0);
       c.wu_ptr = d_wp; c.wu_idx = d_wi; c.wu_val = d_wv;
     }
+    {  // B by row for the gap's ub = u B'
+      std::vector<int> bp{0}, bi;
+      std::vector<double> bv;
+      for (int i = 0; i < nx; ++i) {
+        for (int j = 0; j < nu; ++j)
+          if (pb->B[(size_t)i * nu + j] != 0.0) { bi.push_back(j); bv.push_back(pb->B[(size_t)i * nu + j]); }
+        bp.push_back((int)bi.size());
+      }
+      if (bi.empty()) { bi.push_back(0); bv.push_back(0.0); }
+      int *d_bp, *d_bi;
+      double* d_bv;
+      rc |= pl->upload(&d_bp, bp.data(), bp.size());
+      rc |= pl->upload(&d_bi, bi.data(), bi.size());
+      rc |= pl->upload(&d_bv, bv.data(), bv.size());
+      if (rc) return bail(0);
+      c.bq_ptr = d_bp; c.bq_idx = d_bi; c.bq_val = d_bv;
+    }
     // junction rows with disjoint flow supports -> one Dykstra component per row
     std::vector<int> owner(nu, -1);
     bool disjoint = ne > 0;
