@@ -441,10 +441,20 @@ def run_reference(args, ws, rank):
     scal = O.scaling_tuple(W["scaling"])
     it = args.ref_iters
     times = []
+    # the reference's own knob: SolverConfig.threads runs each stage's chunks on a
+    # worker pool (engine.py:47, 536; BLAS stays pinned to one thread, engine.py:535).
+    # Probe 1 and min(8 chunks, nproc) threads briefly and time the faster one.
+    probe = {}
     with threadpool_limits(limits=1):
+        for thr in sorted({1, max(1, min(O.CHUNKS, os.cpu_count() or 1))}):
+            O.apg(fac, cache, tree, mdl, W["p"], lam, 2, scal, threads=thr)
+            t0 = time.perf_counter()
+            O.apg(fac, cache, tree, mdl, W["p"], lam, 8, scal, threads=thr)
+            probe[thr] = 8 / (time.perf_counter() - t0)
+        threads = max(probe, key=probe.get)
         for k in range(args.warmup + args.steps):
             t0 = time.perf_counter()
-            O.apg(fac, cache, tree, mdl, W["p"], lam, it, scal)
+            O.apg(fac, cache, tree, mdl, W["p"], lam, it, scal, threads=threads)
             if k >= args.warmup:
                 times.append(time.perf_counter() - t0)
     total = float(sum(times))
@@ -460,10 +470,13 @@ def run_reference(args, ws, rank):
                                f"{W['tree'].n_edges} edges), {args.iters}-iteration APG solve",
                    "tree": args.tree, "edges": W["tree"].n_edges, "iters": args.iters,
                    "sample_iters_per_step": it},
-        "cpu_baseline": {"value": value, "unit": "APG iter/s", "cores": 1, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "APG iter/s", "cores": threads, "kind": "port",
                          "sample": f"{it} APG iterations per step (reference algorithm restated "
-                                   "in oracle/tsmpc_oracle.py; BLAS pinned to 1 thread as the "
-                                   "reference does, engine.py:535)",
+                                   f"in oracle/tsmpc_oracle.py) with {threads} solve-step "
+                                   "thread(s), the faster of the probed SolverConfig.threads "
+                                   "values; BLAS pinned to 1 thread as the reference does "
+                                   "(engine.py:535)",
+                         "thread_probe_iters_per_s": {str(k): v for k, v in probe.items()},
                          "host": _cpu_model(), "nproc": os.cpu_count()},
         "e2e": {"value": value, "unit": "APG iter/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},

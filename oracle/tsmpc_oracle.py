@@ -29,10 +29,24 @@ def _chunks(n, k=CHUNKS):
     return [(i, min(i + size, n)) for i in range(0, n, size)]
 
 
-def solve_step(fac, beta, uhat, evec, tree, w_sig, w_zeta, w_psi, p):
+def _run(pool, fn, tasks):
+    """Run one stage's chunk tasks: in order, or on the worker pool with a barrier at
+    the end (the reference's ``WorkerPool.run``, ``_parallel.py``; chunks of a stage
+    write disjoint rows, so the result does not depend on the thread count)."""
+    if pool is None:
+        for t in tasks:
+            fn(*t)
+    else:
+        for f in [pool.submit(fn, *t) for t in tasks]:
+            f.result()
+
+
+def solve_step(fac, beta, uhat, evec, tree, w_sig, w_zeta, w_psi, p, pool=None):
     """Backward + forward stage sweep (factor.py:142-185).
 
     ``fac`` provides A, Bbar, L, Rbar_chol.  Returns (x (n_nodes, n_x), u (E, n_u)).
+    ``pool`` (a ``concurrent.futures`` executor) runs each stage's chunks in
+    parallel, as ``SolveContext(threads > 1)`` does (factor.py:176-185).
     """
     A, Bbar, L, chol = fac["A"], fac["Bbar"], fac["L"], fac["Rbar_chol"]
     A_T, Bbar_T, L_T = A.T.copy(), Bbar.T.copy(), L.T.copy()   # factor.py:100-102
@@ -48,37 +62,41 @@ def solve_step(fac, beta, uhat, evec, tree, w_sig, w_zeta, w_psi, p):
     v = np.empty((E, n_v))
     x = np.empty((n_nodes, n_x))
     u = np.empty((E, n_u))
+
+    def backward_chunk(pa_, pb_):                           # factor.py:142-156
+        ea, eb = int(cs[pa_]) - 1, int(ce[pb_ - 1]) - 1
+        rows, nodes = slice(ea, eb), slice(ea + 1, eb + 1)
+        xiq = w_sig[rows] + w_zeta[rows]                   # factor.py:147-148
+        xiq += q_node[nodes]
+        g = beta[rows] + r_node[nodes]                     # factor.py:149-151
+        g += xiq @ Bbar
+        g += w_psi[rows] @ L
+        lam_g = -scipy.linalg.cho_solve((chol, True), g.T, check_finite=False).T
+        delta[rows] = lam_g * inv2p[rows, None]            # factor.py:153
+        offs = (cs[pa_:pb_] - (ea + 1)).astype(np.intp)
+        r_node[pa_:pb_] = np.add.reduceat(g, offs, axis=0)        # factor.py:155
+        q_node[pa_:pb_] = np.add.reduceat(xiq, offs, axis=0) @ A  # factor.py:156
+
+    def forward_chunk(j, ea, eb):                           # factor.py:158-170
+        rows = slice(ea, eb)
+        nodes = slice(ea + 1, eb + 1)
+        if j == 0:
+            v[rows] = delta[rows]
+        else:
+            v[rows] = delta[rows] + v[pa_edge[rows]]
+        u[rows] = v[rows] @ L_T + uhat[rows]
+        xs = x[anc[nodes]] @ A_T
+        xs += v[rows] @ Bbar_T
+        xs += evec[rows]
+        x[nodes] = xs
+
     for j in range(N - 1, -1, -1):                         # factor.py:110-119, 179-180
         ps, pe = int(ss[j]), int(ss[j + 1])
-        for a, b in _chunks(pe - ps):
-            pa_, pb_ = ps + a, ps + b
-            ea, eb = int(cs[pa_]) - 1, int(ce[pb_ - 1]) - 1
-            rows, nodes = slice(ea, eb), slice(ea + 1, eb + 1)
-            xiq = w_sig[rows] + w_zeta[rows]               # factor.py:147-148
-            xiq += q_node[nodes]
-            g = beta[rows] + r_node[nodes]                 # factor.py:149-151
-            g += xiq @ Bbar
-            g += w_psi[rows] @ L
-            lam_g = -scipy.linalg.cho_solve((chol, True), g.T, check_finite=False).T
-            delta[rows] = lam_g * inv2p[rows, None]        # factor.py:153
-            offs = (cs[pa_:pb_] - (ea + 1)).astype(np.intp)
-            r_node[pa_:pb_] = np.add.reduceat(g, offs, axis=0)        # factor.py:155
-            q_node[pa_:pb_] = np.add.reduceat(xiq, offs, axis=0) @ A  # factor.py:156
+        _run(pool, backward_chunk, [(ps + a, ps + b) for a, b in _chunks(pe - ps)])
     x[0] = p                                               # factor.py:181
-    for j in range(N):                                     # factor.py:158-170, 182-184
+    for j in range(N):                                     # factor.py:121-126, 182-184
         es, ee = int(ss[j + 1]) - 1, int(ss[j + 2]) - 1
-        for a, b in _chunks(ee - es):
-            rows = slice(es + a, es + b)
-            nodes = slice(es + a + 1, es + b + 1)
-            if j == 0:
-                v[rows] = delta[rows]
-            else:
-                v[rows] = delta[rows] + v[pa_edge[rows]]
-            u[rows] = v[rows] @ L_T + uhat[rows]
-            xs = x[anc[nodes]] @ A_T
-            xs += v[rows] @ Bbar_T
-            xs += evec[rows]
-            x[nodes] = xs
+        _run(pool, forward_chunk, [(j, es + a, es + b) for a, b in _chunks(ee - es)])
     return x, u
 
 
@@ -119,12 +137,21 @@ def expand_scaling(scaling, edge_stage):
     return s[edge_stage][:, None], z[edge_stage][:, None], p[edge_stage]
 
 
-def apg(fac, cache, tree, mdl, p, lam, iters, scaling=None, warm=None, record=False):
+def apg(fac, cache, tree, mdl, p, lam, iters, scaling=None, warm=None, record=False, threads=1):
     """Fixed-iteration APG loop (engine.py:519-600), without the final gap.
 
     Returns a dict with u0, x, u, x_avg, u_avg, residual_inf, dual (scaled), and
-    residual_trace when ``record``.
+    residual_trace when ``record``.  ``threads`` > 1 runs the solve step's stage
+    chunks on a thread pool (``SolverConfig.threads``, engine.py:47, 536).
     """
+    if threads > 1:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=threads) as pool:
+            return _apg(fac, cache, tree, mdl, p, lam, iters, scaling, warm, record, pool)
+    return _apg(fac, cache, tree, mdl, p, lam, iters, scaling, warm, record, None)
+
+
+def _apg(fac, cache, tree, mdl, p, lam, iters, scaling, warm, record, pool):
     E = tree["n_nodes"] - 1
     n_x, n_u = fac["A"].shape[0], fac["L"].shape[0]
     edges = expand_scaling(scaling, tree["edge_stage"])
@@ -143,7 +170,7 @@ def apg(fac, cache, tree, mdl, p, lam, iters, scaling=None, warm=None, record=Fa
         c = theta * (1.0 / theta_prev - 1.0)                      # engine.py:198
         w = [a + c * (a - b) for a, b in zip(y, y_prev)]
         w_orig = w if edges is None else [w[k] * edges[k] for k in range(3)]
-        x, u = solve_step(fac, cache["beta"], cache["uhat"], cache["evec"], tree, *w_orig, p)
+        x, u = solve_step(fac, cache["beta"], cache["uhat"], cache["evec"], tree, *w_orig, p, pool=pool)
         Hz = [x[1:].copy(), x[1:].copy(), u.copy()]              # engine.py:106-108
         Hz_s = Hz if edges is None else [Hz[k] * edges[k] for k in range(3)]
         t_arg = [w[k] / lam + Hz_s[k] for k in range(3)]          # engine.py:552-554

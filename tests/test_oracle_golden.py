@@ -57,6 +57,21 @@ def test_oracle_apg_matches_reference(name):
         + c.tol("gap", 0.0) * max(1.0, abs(float(z["r_gap"])))
 
 
+@pytest.mark.parametrize("name", ["tank3_tree_30_N8", "bcn63_SMPC1_N24"])
+def test_oracle_threaded_chunks_are_bitwise_equal(name):
+    """The thread-pool form of the solve step (the reference's SolverConfig.threads,
+    used by bench.py's reference arm) gives the sequential result bit for bit, as the
+    reference guarantees for its own threads (t/test_factor_solve.py:165-185)."""
+    c = load_case(name)
+    fac, cache, tree, mdl, scal = _inputs(c)
+    a = O.apg(fac, cache, tree, mdl, c.p, c.lam, 30, scal, threads=1)
+    b = O.apg(fac, cache, tree, mdl, c.p, c.lam, 30, scal, threads=4)
+    for f in ("x", "u", "x_avg", "u_avg"):
+        assert np.array_equal(a[f], b[f]), f
+    for ya, yb in zip(a["dual"], b["dual"]):
+        assert np.array_equal(ya, yb)
+
+
 @pytest.mark.parametrize("name", ["tank3_tree_6_N8", "small_s0", "small_s4", "small_denseA",
                                   "bcn63_CE_N24"])
 def test_oracle_power_iteration_matches_reference(name):
