@@ -268,7 +268,7 @@ def run_ours(args, ws, rank, local):
         dist.barrier()
         dist.destroy_process_group()
     if rank == 0:
-        print(json.dumps(line))
+        emit(line)
 
 
 def sharded_measure(args, ws, rank, local, dist):
@@ -481,10 +481,33 @@ def run_reference(args, ws, rank):
         "e2e": {"value": value, "unit": "APG iter/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    emit(line)
+
+
+_RESULT_FD = None
+
+
+def _reserve_stdout():
+    """Route fd 1 to stderr for the whole run so that native libraries printing to
+    stdout (NCCL's version banner, driver messages) cannot break the one-JSON-line
+    contract; the result line goes to the original stdout via ``emit``."""
+    global _RESULT_FD
+    sys.stdout.flush()
+    _RESULT_FD = os.dup(1)
+    os.dup2(2, 1)
+
+
+def emit(line):
+    text = json.dumps(line) + "\n"
+    if _RESULT_FD is None:
+        sys.stdout.write(text)
+        sys.stdout.flush()
+    else:
+        os.write(_RESULT_FD, text.encode())
 
 
 def main():
+    _reserve_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -499,7 +522,7 @@ def main():
     ap.add_argument("--no-shard", action="store_true")
     ap.add_argument("--no-closed-loop", action="store_true")
     ap.add_argument("--cl-steps", type=int, default=24)
-    ap.add_argument("--shard-tree", default="SMPC8", choices=("SMPC3", "SMPC8", "W4k"))
+    ap.add_argument("--shard-tree", default="W4k", choices=("SMPC3", "SMPC8", "W4k"))
     args = ap.parse_args()
     ws, rank, local = dist_env()
     if args.impl == "reference":
