@@ -521,7 +521,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-shard", action="store_true")
     ap.add_argument("--no-closed-loop", action="store_true")
-    ap.add_argument("--cl-steps", type=int, default=24)
+    ap.add_argument("--cl-steps", type=int, default=168)  # one week
     ap.add_argument("--shard-tree", default="W4k", choices=("SMPC3", "SMPC8", "W4k"))
     args = ap.parse_args()
     ws, rank, local = dist_env()
