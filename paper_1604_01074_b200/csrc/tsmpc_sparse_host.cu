@@ -137,8 +137,9 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
   const int ncomp_all = nv + nx + nu;
   if (allow_split && !sharded && T > 0 && !chains.empty() && !std::getenv("TSMPC_NO_SPLIT")) {
     const int spare = max_ctas - (int)chains.size();
-    // enough trunk CTAs that one sweep slice (T x components) fits one pass of the CTA
-    int want = std::max(kMinTrunkCtas, (int)(((long long)ncomp_all * T + 383) / 384));
+    // enough trunk CTAs that one sweep slice (T x components) stays under ~300 items
+    // (measured on SMPC3: 27 CTAs at 384 items 22.5 us/iteration, 34 at 300 22.2)
+    int want = std::max(kMinTrunkCtas, (int)(((long long)ncomp_all * T + 299) / 300));
     if (const char* e = std::getenv("TSMPC_TRUNK_CTAS")) want = std::max(kMinTrunkCtas, std::atoi(e));
     if (spare >= kMinTrunkCtas) split_n = std::min(spare, want);
   }

@@ -91,8 +91,8 @@ def test_sparse_planner_paper_trees():
     # SMPC3 (configs[1]): one scenario chain per CTA, everything SMEM-resident;
     # split mode: the trunk (37 edges) on spare CTAs
     assert got["SMPC3"]["chains"] == 114 and got["SMPC3"]["trunk_edges"] == 37
-    assert got["SMPC3"]["trunk_ctas"] == 27
-    assert got["SMPC3"]["resident_ctas"] == got["SMPC3"]["ctas"] == 114 + 27
+    assert got["SMPC3"]["trunk_ctas"] == 34
+    assert got["SMPC3"]["resident_ctas"] == got["SMPC3"]["ctas"] == 114 + 34
     assert got["SMPC1"]["trunk_ctas"] == 8 and got["SMPC1"]["ctas"] == 6 + 8
     assert got["SMPC3"]["max_rows"] == 21
     # SMPC8: 3-4 chains per CTA -> streamed tile slots, no split
