@@ -359,8 +359,11 @@ __device__ __noinline__ void epi_state(int nu_it, double cf, double th, int nrow
     bmn[m] = i < c.nx ? xmn_s[i] : 0.0;
     bmx[m] = i < c.nx ? xmx_s[i] : 0.0;
   }
+  // rows from the last warp down: the first warps carry the extra psi rows
+  // (epi_psi_rows: row group g = warp / 4), so the warps with a second state row
+  // are the ones with one psi row fewer
 #pragma unroll 1
-  for (int r = warp; r < nrows; r += kWarpsS) {
+  for (int r = kWarpsS - 1 - warp; r < nrows; r += kWarpsS) {
     const int* d = c.rdesc() + 5 * r;
     const int e = d[0], st = d[1];
     double* row = s_dyn + d[4];
