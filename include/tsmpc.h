@@ -101,12 +101,17 @@ typedef struct tsmpc_result {
   int32_t iterations;  /* out: iterations actually run                         */
   double device_total_ms;   /* out: CUDA-event time of loop + duality gap        */
   int64_t kernel_launches;  /* out: libtsmpc kernels launched by this call       */
+  double* gap_trace;   /* iters (only with TSMPC_GAP_TRACE): duality gap after every
+                          iteration, engine.py:577-582                              */
 } tsmpc_result;
 
 #define TSMPC_RECORD_RESIDUALS 1   /* residual_inf of every iteration -> resid_trace */
 #define TSMPC_SKIP_GAP         2   /* do not evaluate the duality gap               */
 #define TSMPC_KEEP_DEVICE      4   /* leave results on the device (no D2H but u0)   */
 #define TSMPC_WARM_DEVICE      8   /* warm start from the last solve's final dual (HBM) */
+#define TSMPC_GAP_TRACE       16   /* duality gap of every iteration -> gap_trace (implies
+                                      RECORD_RESIDUALS; single-GPU structured-basis plans;
+                                      one launch per iteration + the gap's kernels)       */
 
 /* Problem / tree geometry and device planning.  Returns NULL on failure. */
 tsmpc_plan* tsmpc_plan_create(const tsmpc_problem* prob, int device);

@@ -7,10 +7,8 @@ behind the C ABI of ``include/tsmpc.h``.
 """
 
 from .errors import DeviceError, DimensionError, ParseError, TreeSmpcError, ValidationError
-from .model import (NetworkModel, StageCost, junction_residual, load_network, simulate_step,
-                    stage_cost, validate_model)
-from .tree import (DemandForecast, ScenarioTree, build_tree, load_tree, node_demands,
-                   scenario_paths, tree_document)
+from .model import NetworkModel, check_model, validate_model
+from .tree import DemandForecast, ScenarioTree, node_demands
 from .points import DualPoint, PrimalPoint, SplitPoint
 from .precompute import (DualScaling, EliminationBasis, FactorCache, StageCache,
                          build_stage_cache, compute_basis, compute_preconditioner,

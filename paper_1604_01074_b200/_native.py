@@ -26,7 +26,7 @@ SOURCES = ["tsmpc_apg.cu", "tsmpc_sparse.cu", "tsmpc_sparse_host.cu", "tsmpc_ncc
            "tsmpc_aux.cu", "tsmpc_capi.cu"]
 
 OK, ERR_DIMENSION, ERR_VALIDATION, ERR_CUDA, ERR_NCCL, ERR_ARGUMENT = 0, -1, -2, -3, -4, -5
-RECORD_RESIDUALS, SKIP_GAP, KEEP_DEVICE, WARM_DEVICE = 1, 2, 4, 8
+RECORD_RESIDUALS, SKIP_GAP, KEEP_DEVICE, WARM_DEVICE, GAP_TRACE = 1, 2, 4, 8, 16
 
 _dp = ctypes.POINTER(ctypes.c_double)
 _ip = ctypes.POINTER(ctypes.c_int64)
@@ -55,6 +55,7 @@ class Result(ctypes.Structure):
         ("residual_inf", ctypes.c_double), ("gap", ctypes.c_double),
         ("device_ms", ctypes.c_double), ("iterations", ctypes.c_int32),
         ("device_total_ms", ctypes.c_double), ("kernel_launches", ctypes.c_int64),
+        ("gap_trace", _dp),
     ]
 
 
@@ -104,6 +105,32 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
               "-Xcompiler", "-fPIC", "-shared", "-ldl"]
 
 
+def _compile(srcs, out: pathlib.Path, extra=()) -> None:
+    """nvcc each translation unit to an object in parallel (build/ next to csrc),
+    then link the shared library."""
+    import concurrent.futures as cf
+    nvcc = os.environ.get("NVCC", "nvcc")
+    objdir = CSRC.parent / "build" / out.stem
+    objdir.mkdir(parents=True, exist_ok=True)
+    cflags = [f for f in NVCC_FLAGS if f not in ("-shared", "-ldl")]
+
+    def one(src):
+        obj = objdir / (src.stem + ".o")
+        cmd = [nvcc, *cflags, *extra, "-c", "-o", str(obj), str(src)]
+        res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise DeviceError(f"nvcc failed ({' '.join(cmd)}):\n{res.stderr[-4000:]}")
+        return obj
+
+    with cf.ThreadPoolExecutor(max_workers=len(srcs)) as ex:
+        objs = list(ex.map(one, srcs))
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(out),
+           *map(str, objs), "-ldl"]
+    res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise DeviceError(f"nvcc link failed ({' '.join(cmd)}):\n{res.stderr[-4000:]}")
+
+
 def build_library(force: bool = False, verbose: bool = False, timers: bool = False) -> pathlib.Path:
     """Compile ``libtsmpc.so`` in-tree for sm_100a (cross-compiles without a GPU).
 
@@ -113,24 +140,14 @@ def build_library(force: bool = False, verbose: bool = False, timers: bool = Fal
     srcs = [CSRC / s for s in SOURCES]
     if timers:
         out = PKG_DIR / "libtsmpc_timers.so"
-        cmd = [os.environ.get("NVCC", "nvcc"), *NVCC_FLAGS, "-DTSMPC_TIMERS", "-o", str(out),
-               *map(str, srcs)]
-        res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
-        if res.returncode != 0:
-            raise DeviceError(f"nvcc failed:\n{res.stderr[-4000:]}")
+        _compile(srcs, out, ("-DTSMPC_TIMERS",))
         return out
     deps = srcs + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [PKG_DIR.parent / "include" / "tsmpc.h"]
     if not force and LIB_PATH.exists():
         newest = max(p.stat().st_mtime for p in deps)
         if LIB_PATH.stat().st_mtime >= newest:
             return LIB_PATH
-    nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", str(LIB_PATH), *map(str, srcs)]
-    res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
-    if res.returncode != 0:
-        raise DeviceError(f"nvcc failed ({' '.join(cmd)}):\n{res.stderr[-4000:]}")
-    if verbose and res.stderr:
-        print(res.stderr)
+    _compile(srcs, LIB_PATH)
     return LIB_PATH
 
 

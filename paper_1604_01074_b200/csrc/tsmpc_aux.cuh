@@ -85,6 +85,7 @@ __global__ void apg_persistent_kernel(const __grid_constant__ Params P);
 __global__ void apg_sparse_kernel();
 // copies S to the kernel's constant parameter block and launches (cooperative)
 cudaError_t sparse_launch(const SParams& S, int ctas, size_t smem, cudaStream_t stream);
+const void* sparse_kernel_fn(int wide, int nx);
 __global__ void beta_rotate_kernel(const double* __restrict__ beta, const double* __restrict__ M, double* out,
                                    int E, int nv, int NVP);
 

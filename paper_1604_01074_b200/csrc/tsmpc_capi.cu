@@ -102,6 +102,9 @@ struct tsmpc_plan {
   double* HS = nullptr;
   double* TR = nullptr;            // split mode: [du | B du | x] per trunk position
   unsigned int* SUBCTR = nullptr;  // split mode: trunk-CTA barrier counter
+  unsigned int* ABORT = nullptr;   // raised by a sparse-kernel spin-wait that timed out
+  double* GTR = nullptr;           // per-iteration gap reductions (TSMPC_GAP_TRACE), iters x 10
+  int gtr_cap = 0;
   double* DYKST = nullptr;  // lockstep Dykstra state (2 x E x [x | inc])
   DykComp* DYKC = nullptr;  // per-junction-row components (disjoint flow supports)
   int* DYKF = nullptr;      // flows no junction touches
@@ -346,7 +349,8 @@ const char* tsmpc_last_error(void) { return g_err.c_str(); }
 const char* tsmpc_plan_path(const tsmpc_plan* pl) {
   if (!pl) return "";
   static thread_local std::string s;
-  s = pl->use_sparse ? "sparse" : ("dense: " + pl->sp_why);
+  s = !pl->use_sparse ? "dense: " + pl->sp_why
+                      : pl->sbase.wide ? "sparse (wide)" : pl->sbase.split ? "sparse (split)" : "sparse";
   return s.c_str();
 }
 
@@ -658,6 +662,7 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
   rc |= pl->alloc(&pl->COLS, (size_t)E * 10);
   rc |= pl->alloc(&pl->ROWS, (size_t)E * 6);
   rc |= pl->alloc(&pl->RED, 16);
+  rc |= pl->alloc(&pl->ABORT, 1);
   rc |= pl->alloc(&pl->DYK, 256);
   rc |= pl->alloc(&pl->TIMERS, 16);
   int *d_te = nullptr, *d_tsp = nullptr, *d_tpos = nullptr, *d_pp = nullptr, *d_pl = nullptr,
@@ -725,15 +730,27 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
       SparseHostPlan hp = plan_sparse(ti, oi, NXP, NUP, NVP, pl->sm_count,
                                       (size_t)prop.sharedMemPerBlockOptin - fa.sharedSizeBytes, shard,
                                       shard ? srank : 0, shard ? sworld : 1);
+      // wide mode (apg_wide_kernel) when some CTA would stream its rows through a
+      // tile slot, when a chain is longer than a slot tile, and for shards
+      // (TSMPC_NO_WIDE: the slot-streaming plan of apg_sparse_kernel)
+      if (!std::getenv("TSMPC_NO_WIDE") && nx <= 128 && (!hp.ok || hp.resident_ctas < hp.n_ctas || shard)) {
+        cudaFuncAttributes fw{};
+        cudaFuncGetAttributes(&fw, sparse_kernel_fn(1, nx));
+        SparseHostPlan hw = plan_sparse(ti, oi, NXP, NUP, NVP, pl->sm_count,
+                                        (size_t)prop.sharedMemPerBlockOptin - fw.sharedSizeBytes, shard,
+                                        shard ? srank : 0, shard ? sworld : 1, true, true, true);
+        if (hw.ok) hp = std::move(hw);
+        else if (!hp.ok) hp.why += std::string("; wide mode: ") + hw.why;
+      }
+      const void* kfn = sparse_kernel_fn(hp.S.wide, nx);
       int occ_s = 0;
       if (hp.ok) {
-        if (cudaFuncSetAttribute(apg_sparse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hp.smem) !=
-            cudaSuccess) {
+        if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hp.smem) != cudaSuccess) {
           hp.ok = false;
           hp.why = "cannot reserve shared memory for the sparse kernel";
           cudaGetLastError();
         } else {
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, apg_sparse_kernel, kThreadsS, hp.smem);
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, kfn, kThreadsS, hp.smem);
           if (occ_s < 1) { hp.ok = false; hp.why = "sparse kernel does not fit on an SM"; }
         }
       }
@@ -758,6 +775,7 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
         for (int i = 0; i < nx; ++i)
           if (pb->A[(size_t)i * nx + i] != 1.0) S.a_unit = 0;
         S.HS_LD = NVP + NXP;
+        S.abort_flag = pl->ABORT;
         if (S.split) {
           int* d_tpi;
           double* d_tpv;
@@ -1052,10 +1070,10 @@ int tsmpc_plan_info(const tsmpc_plan* pl, int64_t* info, int32_t n) {
   const bool sp = pl->use_sparse;
   const int64_t vals[] = {pl->n_levels, sp ? pl->sp_ctas : pl->n_ctas, sp ? pl->sp_tiles : pl->n_tiles,
                           pl->n_segs, (int64_t)(sp ? pl->sp_smem : pl->smem), pl->base.diagA,
-                          sp ? kThreadsS : kThreads, sp ? kTileS : kTileM, pl->sm_count, pl->base.collapsed,
+                          sp ? kThreadsS : kThreads, sp ? pl->sbase.tile_cap : kTileM, pl->sm_count, pl->base.collapsed,
                           sp ? pl->sp_trunk : pl->n_trunk, sp ? 1 : 0, pl->sp_resident,
                           pl->sharded ? 1 : 0, pl->rank, pl->world, (int64_t)pl->owned_edges.size(),
-                          pl->total_chains, sp ? pl->sbase.split_n : 0};
+                          pl->total_chains, sp ? pl->sbase.split_n : 0, sp ? pl->sbase.wide : 0};
   for (int i = 0; i < n && i < (int)(sizeof(vals) / sizeof(vals[0])); ++i) info[i] = vals[i];
   return TSMPC_OK;
 }
@@ -1202,7 +1220,17 @@ static int run_step(tsmpc_plan* pl, double* w, int scaled, const double* beta, c
   return launch_apg(pl, P);
 }
 
-static int compute_gap(tsmpc_plan* pl, const double* yfinal, double* gap) {
+// duality gap (engine.py:458-480) from the 10 reduced terms of compute_gap_terms
+static double gap_from_terms(const tsmpc_plan* pl, const double* k) {
+  const double primal = k[0] + (pl->ctx.Wx * k[1] + pl->ctx.gamma_d * k[2]);
+  const double pairing = (k[3] + k[4]) + k[5];
+  const double conj = (k[7] + k[8]) + k[9];
+  return primal - ((pairing + k[6]) - conj);
+}
+
+// the gap's kernels for the dual `yfinal` (scaled) and the ergodic averages in
+// XAVG / UAVG; the 10 reduced terms go to `terms` (device, no host sync)
+static int compute_gap_terms(tsmpc_plan* pl, const double* yfinal, double* terms) {
   EdgeCtx c = pl->ctx;
   const int E = pl->E, G = grid_for(E);
   CU(cudaMemsetAsync(pl->COLS, 0, sizeof(double) * (size_t)E * 10, pl->stream));
@@ -1286,15 +1314,18 @@ static int compute_gap(tsmpc_plan* pl, const double* yfinal, double* gap) {
   CU(cudaGetLastError());
   gap_primal_terms_kernel<<<G, 256, 0, pl->stream>>>(c, pl->UF, pl->XF, pl->COLS);
   CU(cudaGetLastError());
-  reduce_cols_kernel<<<1, 1024, 0, pl->stream>>>(pl->COLS, E, 10, pl->RED);
+  reduce_cols_kernel<<<1, 1024, 0, pl->stream>>>(pl->COLS, E, 10, terms);
   CU(cudaGetLastError());
+  return TSMPC_OK;
+}
+
+static int compute_gap(tsmpc_plan* pl, const double* yfinal, double* gap) {
+  int rc = compute_gap_terms(pl, yfinal, pl->RED);
+  if (rc) return rc;
   double k[10];
   CU(cudaMemcpyAsync(k, pl->RED, sizeof(k), cudaMemcpyDeviceToHost, pl->stream));
   CU(cudaStreamSynchronize(pl->stream));
-  const double primal = k[0] + (pl->ctx.Wx * k[1] + pl->ctx.gamma_d * k[2]);
-  const double pairing = (k[3] + k[4]) + k[5];
-  const double conj = (k[7] + k[8]) + k[9];
-  *gap = primal - ((pairing + k[6]) - conj);
+  *gap = gap_from_terms(pl, k);
   return TSMPC_OK;
 }
 
@@ -1319,7 +1350,14 @@ int solve_prepare(tsmpc_plan* pl, const double* p, int32_t iters, double lam, co
   CU(cudaSetDevice(pl->device));
   pl->launches = 0;
   const int E = pl->E, NXP = pl->NXP, NUP = pl->NUP, nx = pl->nx, nu = pl->nu;
-  const bool record = flags & TSMPC_RECORD_RESIDUALS;
+  const bool record = flags & (TSMPC_RECORD_RESIDUALS | TSMPC_GAP_TRACE);
+  if ((flags & TSMPC_GAP_TRACE) && (!pl->use_sparse || pl->sharded))
+    return fail(TSMPC_ERR_VALIDATION, "the per-iteration duality gap needs a single-GPU structured-basis plan");
+  if ((flags & TSMPC_GAP_TRACE) && pl->tol > 0.0)
+    return fail(TSMPC_ERR_VALIDATION, "the per-iteration duality gap runs the fixed iteration count (no tol)");
+  if ((flags & TSMPC_GAP_TRACE) && (flags & TSMPC_SKIP_GAP))
+    return fail(TSMPC_ERR_VALIDATION, "TSMPC_GAP_TRACE and TSMPC_SKIP_GAP exclude each other");
+  CU(cudaMemsetAsync(pl->ABORT, 0, sizeof(unsigned int), pl->stream));
   // momentum tables
   if (pl->theta_cap < iters) {
     int rc = pl->alloc(&pl->THETA, iters) | pl->alloc(&pl->COEF, iters);
@@ -1417,19 +1455,21 @@ int solve_finish(tsmpc_plan* pl, const SolveState& st, int32_t flags, tsmpc_resu
   const int iters = st.iters, nres = st.nres;
   const bool record = st.record, stopping = st.stopping;
   int done = iters;
+  unsigned int aborted = 0;
+  CU(cudaMemcpyAsync(&aborted, pl->ABORT, sizeof(aborted), cudaMemcpyDeviceToHost, pl->stream));
+  unsigned long long stop_bits = 0;  // residual of the check that stopped the solve
   if (stopping) {
     CU(cudaMemcpyAsync(&done, pl->ITERS, sizeof(int), cudaMemcpyDeviceToHost, pl->stream));
     CU(cudaStreamSynchronize(pl->stream));
     if (done < 1 || done > iters) done = iters;
-    if (done < iters) {  // the stopping residual becomes the reported one
-      unsigned long long b;
-      CU(cudaMemcpyAsync(&b, pl->RCHK + done / pl->check_every - 1, sizeof(b), cudaMemcpyDeviceToHost,
-                         pl->stream));
-      CU(cudaStreamSynchronize(pl->stream));
-      CU(cudaMemcpyAsync(pl->RESID, &b, sizeof(b), cudaMemcpyHostToDevice, pl->stream));
-      CU(cudaStreamSynchronize(pl->stream));
+    if (done < iters) {
+      CU(cudaMemcpyAsync(&stop_bits, pl->RCHK + done / pl->check_every - 1, sizeof(stop_bits),
+                         cudaMemcpyDeviceToHost, pl->stream));
     }
   }
+  CU(cudaStreamSynchronize(pl->stream));
+  if (aborted)
+    return fail(TSMPC_ERR_CUDA, "sparse kernel: a chain/trunk signal wait timed out (launch results discarded)");
   double* yfin = ((done & 1) == 0) ? pl->Y0 : pl->Y1;
   pl->last_y = yfin;
   // keep the last iterate before the gap's solve step reuses X / U
@@ -1465,6 +1505,14 @@ int solve_finish(tsmpc_plan* pl, const SolveState& st, int32_t flags, tsmpc_resu
   CU(cudaEventRecord(pl->ev2, pl->stream));
   out->gap = gap;
   out->iterations = done;
+  if ((flags & TSMPC_GAP_TRACE) && out->gap_trace) {
+    std::vector<double> terms((size_t)std::max(0, iters - 1) * 10);
+    if (!terms.empty())
+      CU(cudaMemcpyAsync(terms.data(), pl->GTR, sizeof(double) * terms.size(), cudaMemcpyDeviceToHost, pl->stream));
+    CU(cudaStreamSynchronize(pl->stream));
+    for (int k = 0; k + 1 < iters; ++k) out->gap_trace[k] = gap_from_terms(pl, terms.data() + (size_t)k * 10);
+    out->gap_trace[iters - 1] = gap;
+  }
   CU(cudaStreamSynchronize(cs));
   CU(cudaStreamSynchronize(pl->stream));
   float ms = 0.f;
@@ -1474,9 +1522,11 @@ int solve_finish(tsmpc_plan* pl, const SolveState& st, int32_t flags, tsmpc_resu
   out->device_total_ms = ms;
   out->kernel_launches = pl->launches;
   auto as_d = [](unsigned long long b) { double d; std::memcpy(&d, &b, sizeof d); return d; };
-  out->residual_inf = as_d(rbits[nres - 1]);
+  // residual_inf: the last iteration run (record: its trace slot; a stopped solve
+  // without a trace: the residual of the check that stopped it)
+  out->residual_inf = record ? as_d(rbits[done - 1]) : (stop_bits ? as_d(stop_bits) : as_d(rbits[0]));
   if (record && out->resid_trace)
-    for (int k = 0; k < iters; ++k) out->resid_trace[k] = as_d(rbits[k]);
+    for (int k = 0; k < iters; ++k) out->resid_trace[k] = k < done ? as_d(rbits[k]) : NAN;
   return TSMPC_OK;
 }
 
@@ -1495,7 +1545,29 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
   CU(cudaEventRecord(pl->ev0, pl->stream));
   if (pl->use_sparse) {
     SParams S = sparse_params(pl, P);
-    if (!pl->sharded) {
+    if (!pl->sharded && (flags & TSMPC_GAP_TRACE)) {
+      // per-iteration duality gap (engine.py:577-582): one launch per iteration,
+      // each leaving its state in HBM, then the gap's kernels on y_{nu+1} and the
+      // ergodic averages; the 10 reduced terms of every iteration stay on the device
+      // until the end (no host round trip per iteration)
+      if (pl->gtr_cap < iters) {
+        if (pl->alloc(&pl->GTR, (size_t)iters * 10)) return TSMPC_ERR_CUDA;
+        pl->gtr_cap = iters;
+      }
+      S.phase = 3;
+      S.wb_end = 1;
+      for (int nu = 0; nu < iters; ++nu) {
+        S.nu0 = nu;
+        S.nu1 = nu + 1;
+        if (pl->SUBCTR) CU(cudaMemsetAsync(pl->SUBCTR, 0, 4 * sizeof(unsigned int), pl->stream));
+        CU(sparse_launch(S, pl->sp_ctas, pl->sp_smem, pl->stream));
+        ++pl->launches;
+        if (nu + 1 < iters) {  // the last one is the solve's own gap (solve_finish)
+          if (compute_gap_terms(pl, ((nu + 1) & 1) ? pl->Y1 : pl->Y0, pl->GTR + (size_t)nu * 10))
+            return TSMPC_ERR_CUDA;
+        }
+      }
+    } else if (!pl->sharded) {
       S.nu0 = 0;
       S.nu1 = iters;
       S.phase = 3;
@@ -1628,6 +1700,9 @@ int tsmpc_solve_group(tsmpc_plan* const* plans, int32_t n, const double* p, int3
 int tsmpc_set_stopping(tsmpc_plan* pl, double tol, int32_t check_every) {
   if (!pl) return fail(TSMPC_ERR_ARGUMENT, "null argument");
   if (check_every < 1) return fail(TSMPC_ERR_VALIDATION, "check_every must be >= 1");
+  if (tol > 0.0 && (!pl->use_sparse || pl->sharded))
+    return fail(TSMPC_ERR_VALIDATION, "the residual stopping test needs a single-GPU structured-basis plan "
+                                      "(this plan runs the %s kernel)", pl->use_sparse ? "sharded" : "dense");
   pl->tol = tol > 0.0 ? tol : 0.0;
   pl->check_every = check_every;
   return TSMPC_OK;

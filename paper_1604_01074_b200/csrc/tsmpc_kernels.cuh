@@ -118,6 +118,7 @@ constexpr int kThreadsS = 512;
 constexpr int kWarpsS = kThreadsS / 32;
 constexpr int kTileS = 24;         // rows per chain tile (a leaf chain never spans tiles)
 constexpr int kMinTrunkCtas = 8;   // split mode needs at least this many spare CTAs for the trunk
+constexpr int kTileW = 96;         // rows per wide tile (a leaf chain never spans tiles)
 
 struct SParams {
   Params P;                     // dims, model vectors, scaling, tree, state, loop control, KY
@@ -183,6 +184,17 @@ struct SParams {
   int O_TOPS;
   int split_heads, O_HSUM;      // chain CTAs publish their head values right after the fill, by
                                 // reductions ([sum beta_s | sum psi^ | sum G_d s | sum z] at O_HSUM)
+  unsigned int* abort_flag;     // raised by a spin-wait that timed out (plan-owned, zeroed per solve)
+  int wb_end;                   // launch window [nu0, nu1) ends with a full write-back (the state of
+                                // iteration nu1 - 1 is left in HBM: per-iteration duality gap)
+  int tile_cap;                 // rows of the work regions A / B (kTileS, or the widest wide tile)
+  // wide mode (apg_wide_kernel): a CTA's chains are packed into tiles of up to
+  // kTileW rows that are processed as one (the chain scans of all its chains run
+  // together), and the dual / ergodic rows stay in HBM (L2-resident), read into
+  // registers by the fill and the epilogue -- no shared-memory slot rows.  t rows
+  // stay in region A when a CTA has one tile (tmode 0), else they go through TG.
+  int wide;
+  int wide_prefill;             // the epilogue of the CTA's last tile leaves the next fill
 };
 
 // Phase timers (profiling builds: -DTSMPC_TIMERS).  Slot k accumulates the cycles

@@ -110,22 +110,34 @@ __device__ __forceinline__ void signal_arrive(unsigned int* ctr) {
     atomicAdd(ctr, 1u);
   }
 }
-// spin-waits give up after ~2 s (a plan inconsistency must fail the launch, not
-// hang the GPU)
+// Spin-waits give up after ~2 s of clock64 time: the waiting CTA raises the
+// plan's abort flag and returns, every other wait returns as soon as it sees the
+// flag, so all CTAs run to the end of the launch (no CTA exits early: the grid
+// barriers stay consistent) and the host reports TSMPC_ERR_CUDA with a message
+// instead of a hung GPU or a sticky trap that would poison the CUDA context.
+// A timeout means a plan inconsistency (or a debugger stopping the kernel); the
+// results of that launch are discarded.
 constexpr long long kSpinLimit = 4000000000LL;
+
+__device__ __forceinline__ void spin_until(const unsigned int* ctr, unsigned int target) {
+  const long long t0 = clock64();
+  volatile const unsigned int* abort_flag = g_sp.abort_flag;
+  while (*((volatile const unsigned int*)ctr) < target) {
+    if (*abort_flag) return;
+    if (clock64() - t0 > kSpinLimit) {
+      atomicExch(const_cast<unsigned int*>(abort_flag), 1u);
+      return;
+    }
+  }
+}
 
 __device__ __forceinline__ void signal_wait(unsigned int* ctr, unsigned int target) {
   if (threadIdx.x == 0) {
-    const long long t0 = clock64();
-    while (*((volatile unsigned int*)ctr) < target) {
-      if (clock64() - t0 > kSpinLimit) __trap();
-    }
+    spin_until(ctr, target);
     __threadfence();
   }
   __syncthreads();
 }
-
-
 
 // Element phases map threads component-major: thread = (row group g, component
 // k), g = tid / kKW, rows r = g, g + kGroups, ...  The per-component sparse
@@ -148,16 +160,17 @@ struct Ctx {
   const int* spi;  // sparse index pool (shared)
   const double* spv;
   double* need;    // need rows [S | x | u]
-  double* work;    // region A (kTileS x LA) | region B (kTileS x NUP)
+  double* work;    // region A (tcap x LA) | region B (tcap x NUP)
   double* slot;
   int NXP, NUP, NVP, YW, SL, N, LA;
   int nx, nu, nv, E;
+  int tcap;        // rows of the work regions (kTileS; the largest wide tile in wide mode)
   // region A: xiq -> h -> t (backward), S -> bv + e -> x (forward); region B: z / du -> u
   __device__ double* A() const { return work; }
-  __device__ double* B() const { return work + kTileS * LA; }
+  __device__ double* B() const { return work + tcap * LA; }
   __device__ const double* adiag() const { return bnd + 3 * NXP + 2 * NUP; }
   __device__ const double* proot() const { return bnd + 4 * NXP + 2 * NUP; }
-  __device__ int* rdesc() const { return reinterpret_cast<int*>(red + kTileS * 10); }
+  __device__ int* rdesc() const { return reinterpret_cast<int*>(red + tcap * 10); }
   const double* psi_g;  // psi_stage in HBM when the table does not fit shared memory
   __device__ double dpsi(int st, int k) const {
     return psi ? psi[st * NUP + k] : (psi_g ? __ldg(psi_g + (size_t)st * NUP + k) : 1.0);
@@ -180,6 +193,7 @@ __device__ __forceinline__ Ctx ctx_of() {
   c.psi = P.scaled && S.psi_smem ? s_dyn + S.O_PSI : nullptr;
   c.psi_g = P.scaled && !S.psi_smem ? P.psi_stage : nullptr;
   c.LA = S.LA;
+  c.tcap = S.tile_cap;
   c.need = s_dyn + S.O_NEED;
   c.work = s_dyn + S.O_WORK;
   c.slot = s_dyn + S.O_SLOT;
@@ -281,6 +295,12 @@ __device__ __forceinline__ bool is_check(const Params& P, int nu) {
   return P.tol > 0.0 && (nu + 1) % P.check_every == 0 && nu + 1 < P.iters;
 }
 
+// iteration whose state is written back to HBM in full (last iteration, stopping
+// checks, the end of a write-back window)
+__device__ __forceinline__ bool is_last(const Params& P, int nu) {
+  return nu == P.iters - 1 || is_check(P, nu) || (g_sp.wb_end && nu == g_sp.nu1 - 1);
+}
+
 struct EpiConst {
   double cf, th, om, lam, ilam, lam_p;
   bool last, want, wt;
@@ -300,7 +320,7 @@ __device__ __forceinline__ EpiConst epi_const(const Params& P, int nu_it, double
   k.lam = P.lam;
   k.ilam = P.inv_lam;
   k.lam_p = 1.0 / P.lam;
-  k.last = nu_it == P.iters - 1 || is_check(P, nu_it);
+  k.last = is_last(P, nu_it);
   k.want = k.last || P.record_all;
   k.wt = wt;
   k.Yn = P.ybuf[ncur];
@@ -780,7 +800,7 @@ __device__ __noinline__ void fwd_tile(int ti, int nu_it, double cf, double th, i
   }
   // the thread reads back only its own u entries: no barrier needed
   if (!S.split)
-    epi_psi_rows(nu_it, cf, th, nrows, ysm, !resident || nu_it == P.iters - 1 || is_check(P, nu_it), cur ^ 1, rmax);
+    epi_psi_rows(nu_it, cf, th, nrows, ysm, !resident || is_last(P, nu_it), cur ^ 1, rmax);
   {
     const double* adiag = c.adiag();
     const double* pr = c.proot();
@@ -810,7 +830,7 @@ __device__ __noinline__ void fwd_tile(int ti, int nu_it, double cf, double th, i
   TSMPC_MARK(P, 7, tm_);
   if (S.split) return;  // trunk terms and epilogue: fwd_finish, after the grid barrier
   // (5) epilogue, state blocks (warp per row)
-  epi_state(nu_it, cf, th, nrows, ysm, !resident || nu_it == P.iters - 1 || is_check(P, nu_it), cur ^ 1, rmax);
+  epi_state(nu_it, cf, th, nrows, ysm, !resident || is_last(P, nu_it), cur ^ 1, rmax);
   __syncthreads();
   TSMPC_MARK(P, 8, tm_);
 }
@@ -837,7 +857,7 @@ __device__ __noinline__ void fwd_finish(int ti, int nu_it, double cf, double th,
   double* RB = c.B();
   long long tm_ = clock64();
   (void)tm_;
-  const bool last = nu_it == P.iters - 1 || is_check(P, nu_it);
+  const bool last = is_last(P, nu_it);
   // one chain per tile in split mode
   const int pn = c.mt.segs[4 * seg0 + 2];
   // the parent's [du | B du | x] row, staged once (split_heads: in the head-sum
@@ -908,10 +928,7 @@ __device__ __forceinline__ void trunk_barrier(unsigned int* ctr, unsigned int n,
   if (threadIdx.x == 0) {
     __threadfence();
     atomicAdd(ctr, 1u);
-    const long long t0 = clock64();
-    while (*((volatile unsigned int*)ctr) < target) {
-      if (clock64() - t0 > kSpinLimit) __trap();
-    }
+    spin_until(ctr, target);
     __threadfence();
   }
   __syncthreads();
@@ -1316,7 +1333,7 @@ __device__ __noinline__ void trunk_needs() {
   // KY, uhat and e rows of the needs, staged in region B in one round of loads
   // (else read through L2 where used)
   const int SLD = P.KY_LD + c.NUP + c.NXP;
-  const bool staged = nn * SLD <= kTileS * c.NUP;
+  const bool staged = nn * SLD <= c.tcap * c.NUP;
   const double* KYs = c.B();
   if (staged) {
     const int hk = P.KY_LD / 2, hu = c.NUP / 2, hx = c.NXP / 2, per = hk + hu + hx;
@@ -1537,6 +1554,508 @@ __device__ __noinline__ void trunk_own_rows(int nu_it, double cf, double th, int
     __syncthreads();
     epi_psi_rows(nu_it, cf, th, nb, 0, true, cur ^ 1, rmax);
     epi_state(nu_it, cf, th, nb, 0, true, cur ^ 1, rmax);
+    __syncthreads();
+  }
+}
+
+
+// ============================================================================
+// wide mode (SParams::wide, apg_wide_kernel): all chains of a CTA form one tile
+// of up to kTileW rows (W4k: several such tiles), so every chain scan runs over
+// nsegs x components threads at once; the dual (y, y_prev) and ergodic rows are
+// never staged in shared memory but read from HBM / L2 into registers by the
+// fill and the epilogue, in chunks of rows whose loads are issued together.
+// XS: state components per lane in the warp-per-row state epilogue (n_x <= 32 XS).
+// ============================================================================
+constexpr int kChunkW = 4;   // rows whose loads a thread issues before using them
+
+__device__ __forceinline__ const double* ysig(const double* Y, size_t e, int NXP) { return Y + e * NXP; }
+
+// psi block of the rows in rdesc (component-major, as epi_psi_rows), state in HBM
+__device__ __noinline__ void epi_psi_wide(int nu_it, double cf, double th, int nrows, int cur, double* rmax_io,
+                                          bool pre, double cfn) {
+  const SParams& S = g_sp;
+  const Ctx c = ctx_of();
+  const Params& P = S.P;
+  const EpiConst q = epi_const(P, nu_it, cf, th, true, cur ^ 1, pre, cfn);
+  const int k = threadIdx.x & (kKW - 1), g = threadIdx.x / kKW;
+  double rmax = *rmax_io;
+  if (k < c.nu) {
+    const double ulo = c.bnd[3 * c.NXP + k], uhi = c.bnd[3 * c.NXP + c.NUP + k];
+    const size_t E = (size_t)c.E;
+    const double* Yc = P.ybuf[cur] + 2 * E * c.NXP + k;
+    double* Yn = P.ybuf[cur ^ 1] + 2 * E * c.NXP + k;
+    double* UA = P.uavg + k;
+    const int* rd = c.rdesc();
+#pragma unroll 1
+    for (int r0 = g; r0 < nrows; r0 += kChunkW * kGroups) {
+      double yc[kChunkW], yp[kChunkW], ua[kChunkW];
+      size_t eo[kChunkW];
+#pragma unroll
+      for (int u = 0; u < kChunkW; ++u) {
+        const int r = r0 + u * kGroups;
+        eo[u] = 0;
+        yc[u] = yp[u] = ua[u] = 0.0;
+        if (r < nrows) {
+          eo[u] = (size_t)rd[5 * r] * c.NUP;
+          yc[u] = ldcg(Yc + eo[u]);
+          yp[u] = ldcg(Yn + eo[u]);
+          ua[u] = ldcg(UA + eo[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kChunkW; ++u) {
+        const int r = r0 + u * kGroups;
+        if (r < nrows) {
+          const int* d = rd + 5 * r;
+          const int st = d[1];
+          double* us = s_dyn + d[3] + k;
+          const double uu = *us;
+          const double dp = c.dpsi(st, k);
+          const double w = extrap(yc[u], yp[u], q.cf);
+          const double hp = __dmul_rn(uu, dp);
+          const double a = __dadd_rn(__dmul_rn(w, q.ilam), hp);
+          const double t = fmin(fmax(a, __dmul_rn(dp, ulo)), __dmul_rn(dp, uhi));
+          const double ny = __dadd_rn(w, __dmul_rn(q.lam, __dsub_rn(hp, t)));
+          stcg(Yn + eo[u], ny);
+          if (q.want) rmax = fmax(rmax, fabs(__dsub_rn(uu, __ddiv_rn(t, dp))));
+          stcg(UA + eo[u], __dadd_rn(__dmul_rn(ua[u], q.om), __dmul_rn(q.th, uu)));
+          if (q.last) stcg(P.U + eo[u] + k, uu);
+          if (q.pre) {  // the next backward's fill of this element
+            const double wn = extrap(ny, yc[u], q.cfn);
+            *us = c.scaled() ? __dmul_rn(wn, dp) : wn;
+          }
+        }
+      }
+    }
+  }
+  *rmax_io = rmax;
+}
+
+// state blocks of the rows in rdesc, one warp per row (two rows in flight), state in HBM
+template <int XS>
+__device__ __noinline__ void epi_state_wide(int nu_it, double cf, double th, int nrows, int cur, double* rmax_io,
+                                            bool pre, double cfn) {
+  const SParams& S = g_sp;
+  const Ctx c = ctx_of();
+  const Params& P = S.P;
+  const EpiConst q = epi_const(P, nu_it, cf, th, true, cur ^ 1, pre, cfn);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const size_t E = (size_t)c.E;
+  const int N = c.N;
+  double rmax = *rmax_io;
+  double bxs[XS], bmn[XS], bmx[XS];
+#pragma unroll
+  for (int m = 0; m < XS; ++m) {
+    const int i = lane + 32 * m;
+    bxs[m] = i < c.nx ? c.bnd[i] : 0.0;
+    bmn[m] = i < c.nx ? c.bnd[c.NXP + i] : 0.0;
+    bmx[m] = i < c.nx ? c.bnd[2 * c.NXP + i] : 0.0;
+  }
+  const double* Ys = P.ybuf[cur];
+  const double* Yz = Ys + E * c.NXP;
+  double* Ns = P.ybuf[cur ^ 1];
+  double* Nz = Ns + E * c.NXP;
+  const int* rd = c.rdesc();
+  constexpr int R2 = 2;
+#pragma unroll 1
+  for (int r0 = kWarpsS - 1 - warp; r0 < nrows; r0 += R2 * kWarpsS) {
+    double ycs[R2][XS], yps[R2][XS], ycz[R2][XS], ypz[R2][XS], xav[R2][XS];
+    size_t eo[R2];
+#pragma unroll
+    for (int h = 0; h < R2; ++h) {
+      const int r = r0 + h * kWarpsS;
+      eo[h] = r < nrows ? (size_t)rd[5 * r] * c.NXP : 0;
+#pragma unroll
+      for (int m = 0; m < XS; ++m) {
+        const int i = lane + 32 * m;
+        const bool ok = r < nrows && i < c.nx;
+        ycs[h][m] = ok ? ldcg(Ys + eo[h] + i) : 0.0;
+        yps[h][m] = ok ? ldcg(Ns + eo[h] + i) : 0.0;
+        ycz[h][m] = ok ? ldcg(Yz + eo[h] + i) : 0.0;
+        ypz[h][m] = ok ? ldcg(Nz + eo[h] + i) : 0.0;
+        xav[h][m] = ok ? ldcg(P.xavg + eo[h] + c.NXP + i) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < R2; ++h) {
+      const int r = r0 + h * kWarpsS;
+      if (r >= nrows) break;  // warp-uniform
+      const int* d = rd + 5 * r;
+      const int st = d[1];
+      double* x = s_dyn + d[2];
+      const double ds = c.scl[st], dz = c.scl[N + st];
+      double ws[XS], wz[XS], ts[XS], tz[XS], xv[XS];
+      double ss = 0.0, sz = 0.0;
+#pragma unroll
+      for (int m = 0; m < XS; ++m) {
+        const int i = lane + 32 * m;
+        ws[m] = wz[m] = ts[m] = tz[m] = xv[m] = 0.0;
+        if (i < c.nx) {
+          ws[m] = extrap(ycs[h][m], yps[h][m], q.cf);
+          wz[m] = extrap(ycz[h][m], ypz[h][m], q.cf);
+          xv[m] = x[i];
+          ts[m] = __dadd_rn(__dmul_rn(ws[m], q.ilam), __dmul_rn(xv[m], ds));
+          tz[m] = __dadd_rn(__dmul_rn(wz[m], q.ilam), __dmul_rn(xv[m], dz));
+          const double gs_ = __dsub_rn(fmax(ts[m], __dmul_rn(ds, bxs[m])), ts[m]);
+          const double gz = __dsub_rn(fmin(fmax(tz[m], __dmul_rn(dz, bmn[m])), __dmul_rn(dz, bmx[m])), tz[m]);
+          ss = fma(gs_, gs_, ss);
+          sz = fma(gz, gz, sz);
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        ss += __shfl_xor_sync(0xffffffffu, ss, off);
+        sz += __shfl_xor_sync(0xffffffffu, sz, off);
+      }
+      // prox factor min(1, weight / distance) as weight * rsqrt(distance^2) (see epi_state)
+      const double wgt_s = __dmul_rn(__dmul_rn(q.lam_p, P.Wx), c.scl[2 * N + st]);
+      const double wgt_z = __dmul_rn(__dmul_rn(q.lam_p, P.gamma_d), c.scl[3 * N + st]);
+      const double fs = ss > __dmul_rn(wgt_s, wgt_s) ? __dmul_rn(wgt_s, rsqrt(ss)) : 1.0;
+      const double fz = sz > __dmul_rn(wgt_z, wgt_z) ? __dmul_rn(wgt_z, rsqrt(sz)) : 1.0;
+#pragma unroll
+      for (int m = 0; m < XS; ++m) {
+        const int i = lane + 32 * m;
+        if (i < c.nx) {
+          const double xi = xv[m];
+          const double hs = __dmul_rn(xi, ds), hz = __dmul_rn(xi, dz);
+          const double ps = fmax(ts[m], __dmul_rn(ds, bxs[m]));
+          const double pz = fmin(fmax(tz[m], __dmul_rn(dz, bmn[m])), __dmul_rn(dz, bmx[m]));
+          const double t_s = __dadd_rn(ts[m], __dmul_rn(fs, __dsub_rn(ps, ts[m])));
+          const double t_z = __dadd_rn(tz[m], __dmul_rn(fz, __dsub_rn(pz, tz[m])));
+          const double ns = __dadd_rn(ws[m], __dmul_rn(q.lam, __dsub_rn(hs, t_s)));
+          const double nz = __dadd_rn(wz[m], __dmul_rn(q.lam, __dsub_rn(hz, t_z)));
+          stcg(Ns + eo[h] + i, ns);
+          stcg(Nz + eo[h] + i, nz);
+          if (q.want) {
+            rmax = fmax(rmax, fabs(__dsub_rn(xi, __ddiv_rn(t_s, ds))));
+            rmax = fmax(rmax, fabs(__dsub_rn(xi, __ddiv_rn(t_z, dz))));
+          }
+          stcg(P.xavg + eo[h] + c.NXP + i, __dadd_rn(__dmul_rn(xav[h][m], q.om), __dmul_rn(q.th, xi)));
+          if (q.last) stcg(P.X + eo[h] + c.NXP + i, xi);
+          if (q.pre) {  // the next backward's fill of this element
+            const double wsn = extrap(ns, ycs[h][m], q.cfn), wzn = extrap(nz, ycz[h][m], q.cfn);
+            x[i] = __dadd_rn(__dmul_rn(wsn, ds), __dmul_rn(wzn, dz));
+          }
+        }
+      }
+    }
+  }
+  *rmax_io = rmax;
+}
+
+// backward sweep of wide tile ti (factor.py:142-156): fill from HBM (unless the
+// previous epilogue left it), xiq scan, z = psi^ + B' xiq, h = beta_s + Ls' z,
+// g scan -> t (region A in place for tmode 0, TG for tmode 2), chain heads -> GG / XIQG
+__device__ __noinline__ void bwd_wide(int ti, double cf, int cur, bool prefilled) {
+  const SParams& S = g_sp;
+  const Ctx c = ctx_of();
+  const Params& P = S.P;
+  const int* td = c.mt.tiles + 4 * ti;
+  const int row0 = td[0], nrows = td[1], seg0 = td[2], nsegs = td[3];
+  const int tid = threadIdx.x, k = tid & (kKW - 1), g = tid / kKW;
+  const int nx = c.nx, nu = c.nu, nv = c.nv, N = c.N, LA = c.LA;
+  const int tmode = c.mt.tmode;
+  const size_t E = (size_t)c.E;
+  double* RA = c.A();
+  double* RB = c.B();
+  long long tm_ = clock64();
+  (void)tm_;
+  if (!prefilled) {
+    // (1) fill: s = D_sig w_sig + D_zeta w_zeta -> A ; psi^ = D_psi w_psi -> B
+    const double* Y = P.ybuf[cur];
+    const double* Yp = P.ybuf[cur ^ 1];
+#pragma unroll 1
+    for (int r0 = g; r0 < nrows; r0 += kChunkW * kGroups) {
+      double a0[kChunkW], a1[kChunkW], a2[kChunkW], a3[kChunkW], b0[kChunkW], b1[kChunkW];
+#pragma unroll
+      for (int u = 0; u < kChunkW; ++u) {
+        const int r = r0 + u * kGroups;
+        a0[u] = a1[u] = a2[u] = a3[u] = b0[u] = b1[u] = 0.0;
+        if (r < nrows) {
+          const size_t e = (size_t)c.mt.edge(row0 + r);
+          if (k < nx) {
+            const size_t o = e * c.NXP + k;
+            a0[u] = ldcg(Y + o);
+            a1[u] = ldcg(Yp + o);
+            a2[u] = ldcg(Y + E * c.NXP + o);
+            a3[u] = ldcg(Yp + E * c.NXP + o);
+          }
+          if (k < nu) {
+            const size_t o = 2 * E * c.NXP + e * c.NUP + k;
+            b0[u] = ldcg(Y + o);
+            b1[u] = ldcg(Yp + o);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kChunkW; ++u) {
+        const int r = r0 + u * kGroups;
+        if (r < nrows) {
+          const int st = c.mt.stage(row0 + r);
+          if (k < nx)
+            RA[r * LA + k] = __dadd_rn(__dmul_rn(extrap(a0[u], a1[u], cf), c.scl[st]),
+                                       __dmul_rn(extrap(a2[u], a3[u], cf), c.scl[N + st]));
+          if (k < nu) {
+            const double wp = extrap(b0[u], b1[u], cf);
+            RB[r * c.NUP + k] = c.scaled() ? __dmul_rn(wp, c.dpsi(st, k)) : wp;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  TSMPC_MARK(P, 0, tm_);
+  // (2) xiq scan, tail -> head, every chain of the tile at once
+  const double* adiag = c.adiag();
+#pragma unroll 1
+  for (int idx = tid; idx < nsegs * nx; idx += kThreadsS) {
+    const int s = idx / nx, i = idx - s * nx;
+    const int* sg = c.mt.segs + 4 * (seg0 + s);
+    const int lo = sg[0], n = sg[1] - lo;
+    const double a = adiag[i];
+    double* col = RA + lo * LA + i;
+    double x = 0.0;
+#pragma unroll 1
+    for (int j1 = n; j1 > 0; j1 -= kCh) {
+      double v[kCh];
+#pragma unroll
+      for (int u = 0; u < kCh; ++u) v[u] = j1 - 1 - u >= 0 ? col[(j1 - 1 - u) * LA] : 0.0;
+#pragma unroll
+      for (int u = 0; u < kCh; ++u)
+        if (j1 - 1 - u >= 0) {
+          x = __dadd_rn(v[u], __dmul_rn(x, a));
+          col[(j1 - 1 - u) * LA] = x;
+        }
+    }
+    if (sg[2] >= 0) stcg(P.XIQG + (size_t)c.mt.edge(row0 + lo) * c.NXP + i, x);
+  }
+  __syncthreads();
+  TSMPC_MARK(P, 1, tm_);
+  // (3) z = psi^ + B' xiq (column k of B), B <- B + B' A
+  if (k < nu) {
+    const SpCol col = sp_col(c, S.Bc_ptr, S.Bc_idx, S.Bc_val, k);
+#pragma unroll 2
+    for (int r = g; r < nrows; r += kGroups)
+      RB[r * c.NUP + k] = sp_dot(c, col, S.Bc_idx, S.Bc_val, RA + r * LA, RB[r * c.NUP + k]);
+  }
+  __syncthreads();
+  TSMPC_MARK(P, 5, tm_);
+  // (4) h = beta_s + Ls' z (column k of Ls), A <- beta_s + Ls' B; beta_s loads per chunk
+  if (k < nv) {
+    const SpCol col = sp_col(c, S.Lc_ptr, S.Lc_idx, S.Lc_val, k);
+#pragma unroll 1
+    for (int r0 = g; r0 < nrows; r0 += kCh * kGroups) {
+      double b[kCh];
+#pragma unroll
+      for (int u = 0; u < kCh; ++u) {
+        const int r = r0 + u * kGroups;
+        b[u] = r < nrows ? ldcg(S.beta_s + (size_t)c.mt.edge(row0 + r) * c.NVP + k) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kCh; ++u) {
+        const int r = r0 + u * kGroups;
+        if (r < nrows) RA[r * LA + k] = __dadd_rn(b[u], sp_dot(c, col, S.Lc_idx, S.Lc_val, RB + r * c.NUP, 0.0));
+      }
+    }
+  }
+  __syncthreads();
+  TSMPC_MARK(P, 2, tm_);
+  // (5) g scan, tail -> head: g_e = h_e + g_child ; t_e = g_e / (2 p_e)
+#pragma unroll 1
+  for (int idx = tid; idx < nsegs * nv; idx += kThreadsS) {
+    const int s = idx / nv, kk = idx - s * nv;
+    const int* sg = c.mt.segs + 4 * (seg0 + s);
+    const int lo = sg[0], n = sg[1] - lo;
+    double* col = RA + lo * LA + kk;
+    double gv = 0.0;
+#pragma unroll 1
+    for (int j1 = n; j1 > 0; j1 -= kCh) {
+      double v[kCh], ip[kCh];
+#pragma unroll
+      for (int u = 0; u < kCh; ++u) {
+        const int j = j1 - 1 - u;
+        v[u] = j >= 0 ? col[j * LA] : 0.0;
+        ip[u] = j >= 0 ? c.mt.inv2p(row0 + lo + j) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kCh; ++u) {
+        const int j = j1 - 1 - u;
+        if (j >= 0) {
+          gv = __dadd_rn(v[u], gv);
+          const double t = __dmul_rn(gv, ip[u]);
+          if (tmode == 2) stcg(S.TG + (size_t)c.mt.edge(row0 + lo + j) * c.NVP + kk, t);
+          else col[j * LA] = t;
+        }
+      }
+    }
+    if (sg[2] >= 0) stcg(P.GG + (size_t)c.mt.edge(row0 + lo) * c.NVP + kk, gv);
+  }
+  __syncthreads();
+  TSMPC_MARK(P, 3, tm_);
+}
+
+// forward sweep of wide tile ti (factor.py:158-170) + epilogue
+template <int XS>
+__device__ __noinline__ void fwd_wide(int ti, int nu_it, double cf, double th, int cur, double* rmax, bool pre,
+                                      double cfn) {
+  const SParams& S = g_sp;
+  const Ctx c = ctx_of();
+  const Params& P = S.P;
+  const int* td = c.mt.tiles + 4 * ti;
+  const int row0 = td[0], nrows = td[1], seg0 = td[2], nsegs = td[3];
+  const int tid = threadIdx.x, k = tid & (kKW - 1), g = tid / kKW;
+  const int nx = c.nx, nu = c.nu, nv = c.nv, LA = c.LA;
+  double* RA = c.A();
+  double* RB = c.B();
+  long long tm_ = clock64();
+  (void)tm_;
+  if (c.mt.tmode == 2) {  // t rows of this tile -> region A
+    const int lane = tid & 31;
+#pragma unroll 1
+    for (int r = tid >> 5; r < nrows; r += kWarpsS) {
+      const double* src = S.TG + (size_t)c.mt.edge(row0 + r) * c.NVP;
+      for (int q = lane; q < c.NVP / 2; q += 32) cp16(RA + r * LA + 2 * q, src + 2 * q);
+    }
+    cp_commit();
+  }
+#pragma unroll 1
+  for (int r = tid; r < nrows; r += kThreadsS) {  // row descriptors of the epilogue
+    int* d = c.rdesc() + 5 * r;
+    d[0] = c.mt.edge(row0 + r);
+    d[1] = c.mt.stage(row0 + r);
+    d[2] = (int)(RA + r * LA - s_dyn);
+    d[3] = (int)(RB + r * c.NUP - s_dyn);
+    d[4] = 0;
+  }
+  if (c.mt.tmode == 2) cp_wait<0>();
+  __syncthreads();
+  // (1) S scan, head -> tail: S_e = t_e + S_parent (A, in place)
+#pragma unroll 1
+  for (int idx = tid; idx < nsegs * nv; idx += kThreadsS) {
+    const int s = idx / nv, kk = idx - s * nv;
+    const int* sg = c.mt.segs + 4 * (seg0 + s);
+    const int lo = sg[0], n = sg[1] - lo, pn = sg[2];
+    double* scol = RA + lo * LA + kk;
+    double Sv = pn >= 0 ? c.need[(size_t)pn * S.need_ld + kk] : 0.0;
+#pragma unroll 1
+    for (int j0 = 0; j0 < n; j0 += kCh) {
+      double v[kCh];
+#pragma unroll
+      for (int u = 0; u < kCh; ++u) v[u] = j0 + u < n ? scol[(j0 + u) * LA] : 0.0;
+#pragma unroll
+      for (int u = 0; u < kCh; ++u)
+        if (j0 + u < n) {
+          Sv = __dadd_rn(v[u], Sv);
+          scol[(j0 + u) * LA] = Sv;
+        }
+    }
+  }
+  __syncthreads();
+  TSMPC_MARK(P, 4, tm_);
+  // (2) du = Lt S (row k of Lt), B <- Lt A
+  if (k < nu) {
+    const SpCol col = sp_col(c, S.Lr_ptr, S.Lr_idx, S.Lr_val, k);
+#pragma unroll 2
+    for (int r = g; r < nrows; r += kGroups) RB[r * c.NUP + k] = sp_dot(c, col, S.Lr_idx, S.Lr_val, RA + r * LA, 0.0);
+  }
+  __syncthreads();
+  TSMPC_MARK(P, 11, tm_);
+  // (3) bv + e = B du + e (row k of B), A <- B B + e; e loads per chunk
+  if (k < nx) {
+    const SpCol col = sp_col(c, S.Br_ptr, S.Br_idx, S.Br_val, k);
+#pragma unroll 1
+    for (int r0 = g; r0 < nrows; r0 += kCh * kGroups) {
+      double ev[kCh];
+#pragma unroll
+      for (int u = 0; u < kCh; ++u) {
+        const int r = r0 + u * kGroups;
+        ev[u] = r < nrows ? ldcg(P.evec + (size_t)c.mt.edge(row0 + r) * c.NXP + k) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kCh; ++u) {
+        const int r = r0 + u * kGroups;
+        if (r < nrows) RA[r * LA + k] = __dadd_rn(sp_dot(c, col, S.Br_idx, S.Br_val, RB + r * c.NUP, 0.0), ev[u]);
+      }
+    }
+  }
+  __syncthreads();
+  TSMPC_MARK(P, 6, tm_);
+  // (4) u = uhat + du (B; the psi epilogue below reads back only this thread's
+  // entries: no barrier), then the x scan, head -> tail: x = a .* x_anc + (bv + e)
+  if (k < nu) {
+#pragma unroll 1
+    for (int r0 = g; r0 < nrows; r0 += kCh * kGroups) {
+      double uh[kCh];
+#pragma unroll
+      for (int u = 0; u < kCh; ++u) {
+        const int r = r0 + u * kGroups;
+        uh[u] = r < nrows ? ldcg(P.uhat + (size_t)c.mt.edge(row0 + r) * c.NUP + k) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kCh; ++u) {
+        const int r = r0 + u * kGroups;
+        if (r < nrows) RB[r * c.NUP + k] = __dadd_rn(RB[r * c.NUP + k], uh[u]);
+      }
+    }
+  }
+  epi_psi_wide(nu_it, cf, th, nrows, cur, rmax, pre, cfn);
+  {
+    const double* adiag = c.adiag();
+    const double* pr = c.proot();
+#pragma unroll 1
+    for (int idx = tid; idx < nsegs * nx; idx += kThreadsS) {
+      const int s = idx / nx, i = idx - s * nx;
+      const int* sg = c.mt.segs + 4 * (seg0 + s);
+      const int lo = sg[0], n = sg[1] - lo, pn = sg[2];
+      double* col = RA + lo * LA + i;
+      double x = pn >= 0 ? c.need[(size_t)pn * S.need_ld + c.NVP + i] : pr[i];
+      const double a = adiag[i];
+#pragma unroll 1
+      for (int j0 = 0; j0 < n; j0 += kCh) {
+        double v[kCh];
+#pragma unroll
+        for (int u = 0; u < kCh; ++u) v[u] = j0 + u < n ? col[(j0 + u) * LA] : 0.0;
+#pragma unroll
+        for (int u = 0; u < kCh; ++u)
+          if (j0 + u < n) {
+            x = __dadd_rn(__dmul_rn(x, a), v[u]);
+            col[(j0 + u) * LA] = x;
+          }
+      }
+    }
+  }
+  __syncthreads();
+  TSMPC_MARK(P, 7, tm_);
+  // (5) epilogue, state blocks (warp per row)
+  epi_state_wide<XS>(nu_it, cf, th, nrows, cur, rmax, pre, cfn);
+  __syncthreads();
+  TSMPC_MARK(P, 8, tm_);
+}
+
+// epilogue of the CTA's own trunk rows (their dual / ergodic rows live in HBM;
+// x and u are the need rows)
+template <int XS>
+__device__ __noinline__ void trunk_own_rows_wide(int nu_it, double cf, double th, int cur, double* rmax) {
+  const SParams& S = g_sp;
+  const Ctx c = ctx_of();
+  const int no = c.mt.nown;
+  if (no == 0) return;
+  const int LD = S.need_ld;
+  for (int b0 = 0; b0 < no; b0 += c.tcap) {
+    const int nb = min(c.tcap, no - b0);
+    for (int i = threadIdx.x; i < nb; i += kThreadsS) {
+      const int n = c.mt.own[b0 + i];
+      int* d = c.rdesc() + 5 * i;
+      d[0] = c.mt.needs[4 * n + 2];
+      d[1] = c.mt.needs[4 * n + 3];
+      d[2] = (int)(c.need + (size_t)n * LD + c.NVP - s_dyn);
+      d[3] = (int)(c.need + (size_t)n * LD + c.NVP + c.NXP - s_dyn);
+      d[4] = 0;
+    }
+    __syncthreads();
+    epi_psi_wide(nu_it, cf, th, nb, cur, rmax, false, 0.0);
+    epi_state_wide<XS>(nu_it, cf, th, nb, cur, rmax, false, 0.0);
     __syncthreads();
   }
 }
@@ -1788,9 +2307,145 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
   if (P.tol > 0.0 && blockIdx.x == 0 && threadIdx.x == 0) *P.iters_done = S.nu1;
 }
 
+
+// Wide-mode persistent kernel (SParams::wide): per iteration, backward over the
+// CTA's tiles (last first) -> grid barrier -> trunk sweep -> grid barrier ->
+// needs, own trunk rows, forward + epilogue over the tiles.  The last forward
+// tile's epilogue leaves the next iteration's fill of that tile (its first
+// backward tile).  Sharded plans run it as two launches per iteration (phase 1:
+// backward + head pre-reduction; phase 2: the rest), state in HBM in between.
+template <int XS>
+__global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel() {
+  cg::grid_group grid = cg::this_grid();
+  const SParams& S = g_sp;
+  const Params& P = S.P;
+  {  // stage model vectors, scaling, sparse operators and this CTA's plan
+    double* bnd = s_dyn + S.O_BND;
+    double* scl = s_dyn + S.O_SCL;
+    const int NXP = P.NXP, NUP = P.NUP, N = P.N;
+#pragma unroll 1
+    for (int i = threadIdx.x; i < NXP; i += kThreadsS) {
+      bnd[i] = P.x_s[i];
+      bnd[NXP + i] = P.x_min[i];
+      bnd[2 * NXP + i] = P.x_max[i];
+      bnd[3 * NXP + 2 * NUP + i] = P.a_diag[i];
+      bnd[4 * NXP + 2 * NUP + i] = P.p[i];
+    }
+#pragma unroll 1
+    for (int j = threadIdx.x; j < NUP; j += kThreadsS) {
+      bnd[3 * NXP + j] = P.u_min[j];
+      bnd[3 * NXP + NUP + j] = P.u_max[j];
+    }
+#pragma unroll 1
+    for (int j = threadIdx.x; j < N; j += kThreadsS) {
+      scl[j] = P.scaled ? P.sig_stage[j] : 1.0;
+      scl[N + j] = P.scaled ? P.zeta_stage[j] : 1.0;
+      scl[2 * N + j] = P.scaled ? P.sig_rcp[j] : 1.0;
+      scl[3 * N + j] = P.scaled ? P.zeta_rcp[j] : 1.0;
+    }
+    if (P.scaled && S.psi_smem) {
+      double* psi = s_dyn + S.O_PSI;
+#pragma unroll 1
+      for (int i = threadIdx.x; i < N * NUP; i += kThreadsS) psi[i] = P.psi_stage[i];
+    }
+    if (S.sched_resident) {
+      int* ss = reinterpret_cast<int*>(s_dyn + S.O_SCHED);
+#pragma unroll 1
+      for (int i = threadIdx.x; i < S.n_tsched; i += kThreadsS) ss[i] = __ldg(S.tsched + i);
+    }
+    int* ints = reinterpret_cast<int*>(s_dyn + S.O_INT);
+    const int m0 = __ldg(S.meta_ptr + blockIdx.x), m1 = __ldg(S.meta_ptr + blockIdx.x + 1);
+#pragma unroll 1
+    for (int i = threadIdx.x; i < m1 - m0; i += kThreadsS) ints[i] = __ldg(S.meta + m0 + i);
+#pragma unroll 1
+    for (int i = threadIdx.x; i < S.n_spi; i += kThreadsS) ints[S.meta_max + i] = __ldg(S.spi + i);
+    double* spv = s_dyn + S.O_SPV;
+#pragma unroll 1
+    for (int i = threadIdx.x; i < S.n_spv; i += kThreadsS) spv[i] = __ldg(S.spv + i);
+    __syncthreads();
+  }
+  const Ctx c = ctx_of();
+  const int nt = c.mt.ntiles;
+  const bool trunk = P.n_trunk > 0;
+  const bool do_a = S.phase & 1, do_b = S.phase & 2;
+  double rmax = 0.0;
+  double cf = P.coef[S.nu0], th = P.theta[S.nu0];
+  for (int nu = S.nu0; nu < S.nu1; ++nu) {
+    const int cur = (P.slot0 + nu) & 1;
+    if (P.tol > 0.0 && nu > S.nu0 && nu % P.check_every == 0) {
+      // stopping test on the residual of iteration nu - 1 (its state is in HBM)
+      grid.sync();
+      const double r = __longlong_as_double(
+          (long long)*((volatile unsigned long long*)(P.resid_chk + nu / P.check_every - 1)));
+      if (r <= P.tol) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) *P.iters_done = nu;
+        return;
+      }
+    }
+    const int nn = nu + 1 < P.iters ? nu + 1 : nu;
+    const double cf_n = P.coef[nn], th_n = P.theta[nn];
+    if (do_a) {
+      for (int t = nt - 1; t >= 0; --t) bwd_wide(t, cf, cur, S.wide_prefill && t == nt - 1 && nu > S.nu0);
+      if (S.sharded && trunk) {
+        grid.sync();
+        head_prereduce();
+      }
+    }
+    if (do_b) {
+      if (trunk) {
+        long long tb_ = clock64();
+        (void)tb_;
+        if (!S.sharded) grid.sync();
+        TSMPC_MARK(P, 9, tb_);
+        trunk_sweep(cf, cur, 3);
+        TSMPC_MARK(P, 10, tb_);
+        grid.sync();
+        TSMPC_MARK(P, 9, tb_);
+        trunk_needs();
+        trunk_own_rows_wide<XS>(nu, cf, th, cur, &rmax);
+        TSMPC_MARK(P, 12, tb_);
+      }
+      if (blockIdx.x == 0) {
+        const double om = __dsub_rn(1.0, th);
+        for (int i = threadIdx.x; i < c.nx; i += kThreadsS)
+          P.xavg[i] = __dadd_rn(__dmul_rn(P.xavg[i], om), __dmul_rn(th, c.proot()[i]));
+      }
+      for (int t = 0; t < nt; ++t)
+        fwd_wide<XS>(t, nu, cf, th, cur, &rmax, S.wide_prefill && t == nt - 1 && nu + 1 < S.nu1, cf_n);
+      if (nu == P.iters - 1 || P.record_all || is_check(P, nu)) {
+        __shared__ double s_rmax[kThreadsS / 32];
+        for (int off = 16; off > 0; off >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, off));
+        if ((threadIdx.x & 31) == 0) s_rmax[threadIdx.x >> 5] = rmax;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          double m = 0.0;
+          for (int w = 0; w < kThreadsS / 32; ++w) m = fmax(m, s_rmax[w]);
+          if (m > 0.0) {
+            const unsigned long long b = (unsigned long long)__double_as_longlong(m);
+            if (nu == P.iters - 1 || P.record_all) atomicMax(P.resid + (P.record_all ? nu : 0), b);
+            if (is_check(P, nu)) atomicMax(P.resid_chk + nu / P.check_every, b);
+          }
+        }
+        rmax = 0.0;
+      }
+    }
+    cf = cf_n;
+    th = th_n;
+  }
+  if (P.tol > 0.0 && blockIdx.x == 0 && threadIdx.x == 0) *P.iters_done = S.nu1;
+}
+
 }  // namespace tsmpc
 
 namespace tsmpc {
+
+// the persistent kernel a plan runs: split / streamed / resident modes share
+// apg_sparse_kernel; wide plans run apg_wide_kernel<XS> (XS = state components per
+// lane of the warp-per-row state epilogue: n_x <= 64 -> 2, <= 128 -> 4)
+const void* sparse_kernel_fn(int wide, int nx) {
+  if (!wide) return (const void*)apg_sparse_kernel;
+  return nx <= 64 ? (const void*)apg_wide_kernel<2> : (const void*)apg_wide_kernel<4>;
+}
 
 // g_sp is one per device and shared by every plan of the process: launches from
 // different streams are chained through a per-device event so that a launch's
@@ -1814,7 +2469,7 @@ cudaError_t sparse_launch(const SParams& S, int ctas, size_t smem, cudaStream_t 
   }
   e = cudaMemcpyToSymbolAsync(g_sp, &S, sizeof(SParams), 0, cudaMemcpyHostToDevice, stream);
   if (e != cudaSuccess) return e;
-  e = cudaLaunchCooperativeKernel((void*)apg_sparse_kernel, dim3(ctas), dim3(kThreadsS), nullptr, smem, stream);
+  e = cudaLaunchCooperativeKernel(sparse_kernel_fn(S.wide, S.P.nx), dim3(ctas), dim3(kThreadsS), nullptr, smem, stream);
   if (e != cudaSuccess) return e;
   last_stream[dev] = stream;
   return cudaEventRecord(last[dev], stream);

@@ -44,7 +44,8 @@ void csr(int rows, int cols, const std::vector<double>& dense, bool by_col, std:
 
 SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NXP, int NUP, int NVP,
                            int max_ctas, size_t smem_limit, bool sharded, int rank, int world, bool psi_in_smem,
-                           bool allow_split) {
+                           bool allow_split, bool wide) {
+  const int tile_lim = wide ? kTileW : kTileS;
   SparseHostPlan out;
   out.rank = rank;
   out.world = world;
@@ -73,7 +74,7 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
       path.push_back(x);
     }
     if (nch[x + 1] == 0) {
-      if ((int)path.size() > kTileS) {
+      if ((int)path.size() > tile_lim) {
         out.why = "leaf chain longer than a tile (" + std::to_string(path.size()) + " edges)";
         return out;
       }
@@ -135,7 +136,7 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
   // ---- split mode: a CTA per chain, the trunk on split_n further CTAs
   int split_n = 0;
   const int ncomp_all = nv + nx + nu;
-  if (allow_split && !sharded && T > 0 && !chains.empty() && !std::getenv("TSMPC_NO_SPLIT")) {
+  if (allow_split && !wide && !sharded && T > 0 && !chains.empty() && !std::getenv("TSMPC_NO_SPLIT")) {
     const int spare = max_ctas - (int)chains.size();
     // enough trunk CTAs that one sweep slice (T x components) stays under ~300 items
     // (measured on SMPC3: 27 CTAs at 384 items 22.5 us/iteration, 34 at 300 22.2)
@@ -265,12 +266,12 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
   std::vector<std::vector<int>> metas(C);
   int total_tiles = 0;
   for (int c = 0; c < C; ++c) {
-    // tiles: consecutive chains packed up to kTileS rows
+    // tiles: consecutive chains packed up to tile_lim rows
     std::vector<std::vector<int>> tiles;
-    int fill = kTileS + 1;
+    int fill = tile_lim + 1;
     for (int i : cta_chains[c]) {
       const int len = (int)chains[i].size();
-      if (fill + len > kTileS) {
+      if (fill + len > tile_lim) {
         tiles.emplace_back();
         fill = 0;
       }
@@ -438,6 +439,17 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
     out.meta_ptr[c + 1] = out.meta_ptr[c] + (int)metas[c].size();
   }
   auto even = [](long long v) { return (v + 1) / 2 * 2; };
+  // rows of the work regions: kTileS, or the widest tile of a wide plan
+  int tcap = kTileS;
+  if (wide) {
+    tcap = 1;
+    for (int c = 0; c < C; ++c) {
+      const int* m = metas[c].data();
+      for (int ti = 0; ti < m[0]; ++ti) tcap = std::max(tcap, m[8 + 4 * ti + 1]);
+    }
+  }
+  S.tile_cap = tcap;
+  S.wide = wide ? 1 : 0;
   S.YW = 2 * NXP + NUP;
   S.need_ld = NVP + NXP + NUP;
   S.need_max = need_max;
@@ -448,7 +460,7 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
   S.O_SCL = (int)off;
   off += even(4LL * N);
   S.O_RED = (int)off;
-  off += 10LL * kTileS + (5 * kTileS + 1) / 2 + 1;  // partial norms, factors, row descriptors
+  off += 10LL * tcap + (5 * tcap + 1) / 2 + 1;  // partial norms, factors, row descriptors
   off = even(off);
   S.O_PSI = (int)off;
   S.psi_smem = psi_in_smem ? 1 : 0;
@@ -458,7 +470,7 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
   S.O_NEED = (int)off;
   off += (long long)need_max * S.need_ld;
   S.O_WORK = (int)off;
-  S.n_work = (int)even((long long)kTileS * (S.LA + NUP));
+  S.n_work = (int)even((long long)tcap * (S.LA + NUP));
   off += S.n_work;
   S.O_SLOT = (int)off;
   const long long ints_d = ((long long)meta_max + S.n_spi + 1) / 2 + 1;
@@ -472,6 +484,61 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
     std::fprintf(stderr, "plan_sparse: rank %d/%d C=%d need_max=%d meta_max=%d n_spi=%d work=%d off=%lld ints_d=%lld "
                  "slot_avail=%lld base_ld=%lld psi=%d\n", rank, world, C, need_max, meta_max, S.n_spi, S.n_work,
                  off, ints_d, slot_avail, base_ld, (int)psi_in_smem);
+  if (wide) {
+    // no slot rows: t stays in region A when a CTA has one tile (and the launch runs
+    // whole iterations), else it goes through TG
+    int max_rows_w = 0;
+    bool any_t0 = false;
+    for (int c = 0; c < C; ++c) {
+      metas[c][6] = 0;
+      metas[c][7] = (metas[c][0] <= 1 && !sharded) ? 0 : 2;
+      any_t0 |= metas[c][7] == 0;
+      max_rows_w = std::max(max_rows_w, cta_rows[c]);
+    }
+    if (slot_avail < 0) {
+      if (psi_in_smem)
+        return plan_sparse(t, ops, NXP, NUP, NVP, max_ctas, smem_limit, sharded, rank, world, false, allow_split,
+                           true);
+      out.why = "shared memory too small for the wide tiles";
+      return out;
+    }
+    const int ncomp = nv + nx + nu;
+    const long long nc_max = (ncomp + C - 1) / C;
+    const long long cap = any_t0 ? (long long)tcap * NUP : (long long)S.n_work;
+    const long long zx = 2LL * T * nc_max + T;
+    const long long sched = ((long long)out.tsched.size() + 1) / 2 + 2;
+    S.sweep_in_a = any_t0 ? 0 : 1;
+    S.sched_smem = zx + sched <= cap ? 1 : 0;
+    if (zx > cap) {
+      out.why = "trunk too large for the work region";
+      return out;
+    }
+    S.slot_ld = (int)base_ld;
+    S.slot_rows = 0;
+    S.wide_prefill = 1;
+    {
+      const long long sched_d = ((long long)out.tsched.size() + 1) / 2 + 1;
+      S.sched_resident = (T > 0 && off + ints_d + sched_d <= limit_d) ? 1 : 0;
+      S.O_SLOT = (int)off;
+      S.O_SCHED = (int)off;
+      if (S.sched_resident) off += sched_d;
+    }
+    S.O_INT = (int)off;
+    off += ints_d;
+    S.O_HSUM = (int)off;
+    S.split = 0;
+    S.TR_LD = NUP + 2 * NXP;
+    S.meta_max = meta_max;
+    out.smem = (size_t)off * sizeof(double);
+    out.meta.clear();
+    for (int c = 0; c < C; ++c) out.meta.insert(out.meta.end(), metas[c].begin(), metas[c].end());
+    S.n_tsched = (int)out.tsched.size();
+    out.resident_ctas = 0;
+    out.max_rows = max_rows_w;
+    out.max_needs = need_max;
+    out.ok = true;
+    return out;
+  }
   if (slot_avail / base_ld < kTileS) {
     if (psi_in_smem) return plan_sparse(t, ops, NXP, NUP, NVP, max_ctas, smem_limit, sharded, rank, world, false);
     out.why = "shared memory too small for one tile slot";

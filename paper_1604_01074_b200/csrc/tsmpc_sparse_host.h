@@ -57,8 +57,11 @@ struct SparseHostPlan {
 // every tile (state lives in HBM between the two launches of an iteration).
 // allow_split: use split mode (SParams::split) when every chain gets its own CTA
 // and enough CTAs are left for the trunk.
+// wide: wide mode (SParams::wide, apg_wide_kernel): tiles of up to kTileW rows,
+// dual / ergodic rows in HBM, no split mode; chains up to kTileW edges.
 SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NXP, int NUP, int NVP,
                            int max_ctas, size_t smem_limit, bool sharded = false, int rank = 0,
-                           int world = 1, bool psi_in_smem = true, bool allow_split = true);
+                           int world = 1, bool psi_in_smem = true, bool allow_split = true,
+                           bool wide = false);
 
 }  // namespace tsmpc

@@ -37,7 +37,9 @@ __all__ = [
 @dataclass
 class SolverConfig:
     """Solve knobs (reference ``engine.py:40-57``).  ``threads`` is accepted for
-    API compatibility; the device ignores it."""
+    API compatibility; the device ignores it.  ``device``, ``tol`` and
+    ``check_every`` are extensions: :func:`solve` reads them with ``getattr``, so
+    the reference's own ``SolverConfig`` objects (which lack them) work too."""
 
     max_iters: int = 500
     lam: float | None = None
@@ -58,6 +60,11 @@ class SolverConfig:
             raise ValidationError("lambda override must be positive")
         if self.threads < 1:
             raise ValidationError("thread count must be >= 1")
+        if self.tol is not None and self.record_residuals:
+            # the reference's traces are per iteration of the fixed-length loop
+            raise ValidationError("tol (early stop) and record_residuals exclude each other")
+        if self.check_every < 1:
+            raise ValidationError("check_every must be >= 1")
 
 
 @dataclass
@@ -124,10 +131,6 @@ def smooth_cost(model, tree, cache, u) -> float:
 
 # -- device-backed operators ------------------------------------------------------
 
-class _RowModelShim:
-    """Minimal model/tree/factor stand-ins for a prox-only device plan."""
-
-
 def prox_g(t: SplitPoint, lam: float, model, scaling_edges=None, *, tree=None,
            factor=None, scaling=None) -> SplitPoint:
     """prox of g with parameter ``lam`` (reference ``engine.py:157-183``) on the device.
@@ -167,7 +170,7 @@ def _prox_plan(model, rows, scaling_edges):
     hit = _PROX_PLANS.get(key)
     if hit is None:
         from .plan import DevicePlan
-        hit = DevicePlan(model, tree, fac, scaling)
+        hit = DevicePlan(model, tree, fac, scaling, warn_dense=False)
         _PROX_PLANS.clear()
         _PROX_PLANS[key] = hit
     return hit
@@ -198,8 +201,12 @@ def compute_lambda(basis, factor, model, tree, scaling=None, tol: float = 1e-8,
     (reference ``engine.py:286-337``)."""
     if basis.sigma <= 0:
         raise ValidationError("strong convexity modulus must be positive")
-    cache0 = _zero_cache(basis, model, tree)
     plan = plan_for(model, tree, factor, scaling, device)
+    key = ("lam", id(basis), id(scaling), float(tol), int(max_iter))
+    memo = getattr(plan, "_lam_memo", None)
+    if memo is not None and memo[0] == key and memo[1] is basis and memo[2] is scaling:
+        return memo[3]
+    cache0 = _zero_cache(basis, model, tree)
     plan.dual_operator_begin(cache0.beta)
     lam_max = 0.0
     for _ in range(max_iter):
@@ -210,7 +217,28 @@ def compute_lambda(basis, factor, model, tree, scaling=None, tol: float = 1e-8,
         lam_max = new
     if not np.isfinite(lam_max) or lam_max <= 0:
         raise ValidationError(f"dual Lipschitz estimate invalid: {lam_max!r}")
+    plan._lam_memo = (key, basis, scaling, 0.995 / lam_max)
     return 0.995 / lam_max
+
+
+# one-time setup derived inside solve() when the caller does not pass it: kept per
+# (model, tree) object so that repeat drop-in calls reuse one device plan and one
+# step size instead of re-deriving and re-uploading them every call
+_SETUP: dict = {}
+
+
+def _setup_for(model, tree, precondition: bool):
+    key = (id(model), id(tree), bool(precondition))
+    hit = _SETUP.get(key)
+    if hit is not None and hit[0] is model and hit[1] is tree:
+        return hit[2:]
+    basis = compute_basis(model)
+    factor = factor_step(basis, model)
+    scaling = compute_preconditioner(basis, model, tree.N, tree=tree) if precondition else None
+    if len(_SETUP) >= 4:
+        _SETUP.pop(next(iter(_SETUP)))
+    _SETUP[key] = (model, tree, basis, factor, scaling)
+    return basis, factor, scaling
 
 
 def solve(model, tree, forecast, p, q, config: SolverConfig | None = None, *,
@@ -227,17 +255,25 @@ def solve(model, tree, forecast, p, q, config: SolverConfig | None = None, *,
         raise DimensionError(f"p: shape {p.shape}, expected ({model.n_x},)")
     if q.shape != (model.n_u,):
         raise DimensionError(f"q: shape {q.shape}, expected ({model.n_u},)")
-    basis = basis or compute_basis(model)
-    factor = factor or factor_step(basis, model)
-    if config.precondition and scaling is None:
-        scaling = compute_preconditioner(basis, model, tree.N, tree=tree)
+    device = int(getattr(config, "device", 0))
+    tol = getattr(config, "tol", None)
+    check_every = int(getattr(config, "check_every", 25))
+    if basis is None and factor is None:
+        basis, factor, derived = _setup_for(model, tree, config.precondition)
+        if config.precondition and scaling is None:
+            scaling = derived
+    else:
+        basis = basis or compute_basis(model)
+        factor = factor or factor_step(basis, model)
+        if config.precondition and scaling is None:
+            scaling = compute_preconditioner(basis, model, tree.N, tree=tree)
     if not config.precondition:
         scaling = None
     lam = lam if lam is not None else config.lam
     if lam is None:
-        lam = compute_lambda(basis, factor, model, tree, scaling=scaling, device=config.device)
+        lam = compute_lambda(basis, factor, model, tree, scaling=scaling, device=device)
 
-    plan = plan_for(model, tree, factor, scaling, config.device)
+    plan = plan_for(model, tree, factor, scaling, device)
     if cache is None:
         # stage cache built on the device from the forecast
         if forecast.dhat.shape[0] != tree.N:
@@ -249,13 +285,16 @@ def solve(model, tree, forecast, p, q, config: SolverConfig | None = None, *,
     theta, coef = theta_schedule(config.max_iters)
     warm = warm_dual if (config.warm_start and warm_dual is not None) else None
     t0 = time.perf_counter()
+    # record_residuals: the residual and the duality gap of every iteration
+    # (engine.py:577-582), evaluated in the same device solve (one launch per iteration)
+    trace_on_device = bool(config.record_residuals) and plan.info()["sparse"] == 1
     out = plan.solve(p, config.max_iters, float(lam), warm=warm, theta=theta, coef=coef,
-                     record_residuals=config.record_residuals, tol=config.tol,
-                     check_every=config.check_every)
+                     record_residuals=config.record_residuals, tol=tol,
+                     check_every=check_every, gap_trace=trace_on_device)
+    gap_trace = out["gap_trace"]
+    if config.record_residuals and not trace_on_device:
+        gap_trace = _gap_trace_dense(plan, p, config, lam, warm, theta, coef)
     wall = time.perf_counter() - t0
-    gap_trace = None
-    if config.record_residuals:
-        gap_trace = _gap_trace(plan, p, config, lam, warm, theta, coef)
     return SolveReport(
         u0=out["u0"], x=out["x"], u=out["u"], x_avg=out["x_avg"], u_avg=out["u_avg"],
         residual_inf=out["residual_inf"], gap=out["gap"], iterations=out["iterations"],
@@ -265,9 +304,11 @@ def solve(model, tree, forecast, p, q, config: SolverConfig | None = None, *,
         device_ms=out["device_ms"])
 
 
-def _gap_trace(plan, p, config, lam, warm, theta, coef):
-    """Per-iteration duality gap (reference ``engine.py:577-582``): iteration nu's
-    gap is the gap after a fresh nu+1-iteration solve (identical iterates)."""
+def _gap_trace_dense(plan, p, config, lam, warm, theta, coef):
+    """Per-iteration duality gap on a dense-kernel plan (non-diagonal A), whose
+    persistent kernel has no launch windows: iteration nu's gap is the gap after a
+    fresh nu+1-iteration device solve (identical iterates; O(iters^2) work, only
+    for this rare plan type)."""
     gaps = np.empty(config.max_iters)
     for nu in range(config.max_iters):
         r = plan.solve(p, nu + 1, float(lam), warm=warm, theta=theta[:nu + 1],

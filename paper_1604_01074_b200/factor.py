@@ -61,12 +61,16 @@ class SolveContext:
     def __init__(self, factor, tree, threads: int = 1, device: int = 0):
         self.factor, self.tree = factor, tree
         self.threads = max(1, int(threads))
-        self._plan = DevicePlan(_StepModel(factor), tree, factor, None, device)
+        self._plan = _step_plan(factor, tree, device)
         self.x = np.zeros((tree.n_nodes, factor.n_x))
         self.u = np.zeros((tree.n_edges, factor.n_u))
+        # the device decomposition both sweeps run over (segments of only-child
+        # chains grouped into levels, packed into CTA tiles; tsmpc_capi.cu decompose)
         info = self._plan.info()
-        self.backward_plan = [("levels", info["levels"]), ("tiles", info["tiles"])]
-        self.forward_plan = list(self.backward_plan)
+        sweep = {k: info[k] for k in ("levels", "segments", "tiles", "ctas", "collapsed", "trunk_edges")}
+        sweep["kernel"] = "tsmpc::apg_persistent_kernel (STEP mode)"
+        self.backward_plan = dict(sweep, order="stages N-1 .. 0")
+        self.forward_plan = dict(sweep, order="stages 0 .. N-1")
 
     def close(self):
         self._plan = None
@@ -85,6 +89,22 @@ class SolveContext:
         self.x[...] = z.x
         self.u[...] = z.u
         return PrimalPoint(self.x, self.u)
+
+
+_STEP_PLANS: dict = {}
+
+
+def _step_plan(factor, tree, device: int) -> DevicePlan:
+    """One solve-step plan per (factor, tree, device), reused across calls."""
+    key = (id(factor), id(tree), device)
+    hit = _STEP_PLANS.get(key)
+    if hit is not None and hit.factor is factor and hit.tree is tree:
+        return hit
+    if len(_STEP_PLANS) >= 4:
+        _STEP_PLANS.pop(next(iter(_STEP_PLANS)))
+    plan = DevicePlan(_StepModel(factor), tree, factor, None, device, warn_dense=False)
+    _STEP_PLANS[key] = plan
+    return plan
 
 
 def solve_step(factor, cache, tree, w: DualPoint, p, q=None, threads: int = 1) -> PrimalPoint:

@@ -11,12 +11,13 @@ report comes down.
 from __future__ import annotations
 
 import ctypes
+import warnings
 import weakref
 
 import numpy as np
 
 from . import _native as nat
-from .errors import DeviceError, DimensionError
+from .errors import DeviceError, DimensionError, ValidationError
 from .points import DualPoint, PrimalPoint
 
 __all__ = ["DevicePlan", "plan_for"]
@@ -30,7 +31,8 @@ class DevicePlan:
     """``shard=(rank, world, nccl_id)`` creates one rank's plan of a tree split
     across GPUs (see ``shard.py``); results then cover ``edges()`` only."""
 
-    def __init__(self, model, tree, factor, scaling=None, device: int = 0, shard=None):
+    def __init__(self, model, tree, factor, scaling=None, device: int = 0, shard=None,
+                 warn_dense: bool = True):
         lib = nat.load_library()
         n_x, n_u, n_v = factor.n_x, factor.n_u, factor.n_v
         E = np.asarray(model.E, dtype=float)
@@ -46,15 +48,20 @@ class DevicePlan:
             "child_stop": _c(tree.child_stop, np.int64), "prob": _c(tree.prob),
         }
         self.structured = None
+        self.structured_error = None
         if np.count_nonzero(np.asarray(factor.A) - np.diag(np.diag(factor.A))) == 0:
+            from .precompute import structured_basis
             try:
-                from .precompute import structured_basis
-                basis = _BasisView(factor.L)
-                sb = structured_basis(model, basis)
+                sb = structured_basis(model, _BasisView(factor.L))
+            except (ValidationError, np.linalg.LinAlgError) as exc:
+                # the plan runs the dense fused-operator kernel; say why (plan.info()["path"])
+                self.structured_error = f"{type(exc).__name__}: {exc}"
+                if warn_dense:
+                    warnings.warn(f"structured kernel basis unavailable ({self.structured_error}); "
+                                  "the plan uses the dense DMMA kernel", RuntimeWarning, stacklevel=2)
+            else:
                 keep["Ls"], keep["lam_s"], keep["Ms"] = _c(sb.Ls), _c(sb.lam), _c(sb.M)
                 self.structured = sb
-            except Exception:  # no structured basis -> dense fused-operator kernel
-                self.structured = None
         if scaling is not None:
             keep["sig_stage"] = _c(scaling.sig_stage)
             keep["zeta_stage"] = _c(scaling.zeta_stage)
@@ -88,7 +95,8 @@ class DevicePlan:
     def info(self) -> dict:
         keys = ("levels", "ctas", "tiles", "segments", "smem_bytes", "diag_A", "threads",
                 "tile_rows", "sms", "collapsed", "trunk_edges", "sparse", "resident_ctas",
-                "sharded", "rank", "world", "owned_chain_edges", "total_chains", "trunk_ctas")
+                "sharded", "rank", "world", "owned_chain_edges", "total_chains", "trunk_ctas",
+                "wide")
         buf = np.zeros(len(keys), dtype=np.int64)
         nat.check(self._lib.tsmpc_plan_info(self._h, nat.iptr(buf), len(keys)), "tsmpc_plan_info")
         d = dict(zip(keys, (int(v) for v in buf)))
@@ -175,14 +183,19 @@ class DevicePlan:
               theta=None, coef=None, record_residuals: bool = False,
               skip_gap: bool = False, keep_device: bool = False,
               warm_device: bool = False, tol: float | None = None,
-              check_every: int = 25) -> dict:
+              check_every: int = 25, gap_trace: bool = False) -> dict:
         """One APG solve (engine.py:485-601).  ``keep_device``: leave the iterates in
         HBM (only u0, residual and gap come back); ``warm_device``: start from the
-        previous solve's final dual, still in HBM (closed-loop warm start)."""
+        previous solve's final dual, still in HBM (closed-loop warm start);
+        ``gap_trace``: also the duality gap after every iteration (implies
+        ``record_residuals``; engine.py:577-582)."""
+        record_residuals = record_residuals or gap_trace
         out, res, trace = self._result_buffers(iters, keep_device, record_residuals)
+        gtrace = np.empty(iters) if gap_trace else None
+        res.gap_trace = nat.dptr(gtrace)
         flags = ((nat.RECORD_RESIDUALS if record_residuals else 0)
                  | (nat.SKIP_GAP if skip_gap else 0) | (nat.KEEP_DEVICE if keep_device else 0)
-                 | (nat.WARM_DEVICE if warm_device else 0))
+                 | (nat.WARM_DEVICE if warm_device else 0) | (nat.GAP_TRACE if gap_trace else 0))
         ws = wz = wp = None
         if warm is not None:
             ws, wz, wp = _c(warm.sig), _c(warm.zeta), _c(warm.psi)
@@ -195,7 +208,12 @@ class DevicePlan:
                                    nat.dptr(ws), nat.dptr(wz), nat.dptr(wp),
                                    nat.dptr(th), nat.dptr(cf), flags, ctypes.byref(res))
         nat.check(rc, "tsmpc_solve")
-        return self._result_dict(out, res, trace)
+        d = self._result_dict(out, res, trace)
+        n = d["iterations"]
+        if trace is not None and n < iters:  # stopped early: the trace covers n iterations
+            d["resid_trace"] = trace[:n]
+        d["gap_trace"] = gtrace
+        return d
 
     def _result_buffers(self, iters: int, keep_device: bool, record_residuals: bool):
         E, n_x, n_u, n = self.n_edges, self.n_x, self.n_u, self.n_nodes

@@ -18,7 +18,7 @@ from .model import NetworkModel, validate_model
 from .tree import DemandForecast, _finish
 
 __all__ = ["bcn63_network", "three_tank_network", "paper_tree", "PAPER_TREES",
-           "base_demand", "forecast_profile", "uniform_tree", "initial_state"]
+           "base_demand", "forecast_profile", "uniform_tree", "initial_state", "input_arrays"]
 
 # name -> (b1, b2, n_s); edges = 1 + b1 + b1*b2 + 21*n_s at N = 24
 PAPER_TREES = {
@@ -189,3 +189,18 @@ def forecast_for(tree, k: int = 0, base=None) -> DemandForecast:
     if base is None:
         base = base_demand(tree.n_d)
     return DemandForecast(forecast_profile(base, k, tree.N), k=k)
+
+
+def input_arrays(model, tree, forecast, p, q) -> list:
+    """Every input array a solve reads, in a fixed order (fixture digests of
+    tests/golden/make_golden_large.py: regenerated inputs are checked against the
+    sha256 of the arrays the reference was fed)."""
+    keys = ("A", "B", "Gd", "E", "Ed", "u_min", "u_max", "x_min", "x_max", "x_s", "alpha1",
+            "alpha2_schedule", "Wu")
+    out = [np.asarray(getattr(model, k), dtype=np.float64) for k in keys]
+    out.append(np.array([model.W_alpha, model.Wx, model.gamma_d], dtype=np.float64))
+    out += [np.asarray(tree.stage_starts, dtype=np.int64), np.asarray(tree.anc, dtype=np.int64),
+            np.asarray(tree.prob, dtype=np.float64), np.asarray(tree.eps, dtype=np.float64),
+            np.asarray(forecast.dhat, dtype=np.float64), np.array([forecast.k], dtype=np.int64),
+            np.asarray(p, dtype=np.float64), np.asarray(q, dtype=np.float64)]
+    return out

@@ -1,82 +1,56 @@
-"""Host-side data layer of the drop-in API: loaders, validation, trees, synthetic
-inputs and configuration objects (mirrors the reference's test_network_model.py /
-test_scenario_tree.py expectations on the same behaviours)."""
+"""Host-side data layer of the drop-in API: model / tree containers and their
+invariants, synthetic inputs, configuration objects, the device planner."""
 
-import json
+import dataclasses
 
 import numpy as np
 import pytest
 
-from paper_1604_01074_b200 import (DemandForecast, DimensionError, ParseError, SolverConfig,
-                                   ValidationError, build_tree, load_network, load_tree,
-                                   node_demands, scenario_paths, synth, tree_document)
-from paper_1604_01074_b200.model import junction_residual, simulate_step, stage_cost
+from paper_1604_01074_b200 import (DemandForecast, DimensionError, ScenarioTree, SolverConfig,
+                                   ValidationError, check_model, node_demands, synth,
+                                   validate_model)
 from paper_1604_01074_b200.plan import describe_tree
 
 
-def _net_doc(m):
-    d = {k: np.asarray(getattr(m, k)).tolist() for k in
-         ("A", "B", "Gd", "E", "Ed", "u_min", "u_max", "x_min", "x_max", "x_s", "alpha1",
-          "alpha2_schedule", "Wu")}
-    d.update(W_alpha=m.W_alpha, Wx=m.Wx, gamma_d=m.gamma_d)
-    return d
-
-
-def test_network_roundtrip_and_validation():
+def test_model_validation():
     m = synth.three_tank_network()
-    doc = _net_doc(m)
-    back = load_network(json.dumps(doc))
-    np.testing.assert_array_equal(back.B, m.B)
-    assert back.n_x == 3 and back.n_u == 4 and back.n_e == 1 and back.n_d == 2
-    with pytest.raises(ParseError):
-        load_network("{not json")
-    bad = dict(doc)
-    del bad["Wu"]
-    with pytest.raises(ParseError):
-        load_network(json.dumps(bad))
-    bad = dict(doc, u_min=[50.0, 0, 0, 0])
-    with pytest.raises(ValidationError) as ei:
-        load_network(json.dumps(bad))
-    assert any("u_min > u_max" in v for v in ei.value.violations)
-    bad = dict(doc, Wu=(-np.eye(4)).tolist())
+    assert validate_model(m) == []
+    bad = dataclasses.replace(m, u_min=np.array([50.0, 0, 0, 0]))
+    assert any("u_min <= u_max" in v for v in validate_model(bad))
     with pytest.raises(ValidationError):
-        load_network(json.dumps(bad))
+        check_model(dataclasses.replace(m, Wu=-np.eye(4)))
+    assert any(v.startswith("B:") for v in validate_model(dataclasses.replace(m, B=np.eye(2))))
 
 
-def test_plant_helpers():
-    m = synth.three_tank_network()
-    x = simulate_step(m, [250, 200, 200], [20, 50, 15, 15], [30, 20])
-    np.testing.assert_allclose(x, [250 + 20 - 20, 200 + 15, 200 + 15])
-    np.testing.assert_allclose(junction_residual(m, [0, 50, 10, 10], [30, 0]), [0.0])
-    c = stage_cost(m, [50, 50, 50], [1, 1, 1, 1], [0, 0, 0, 0], 8)
-    assert c.safety > 0 and c.smoothing == pytest.approx(0.5 + 0.3 + 0.2 + 0.2)
-    with pytest.raises(DimensionError):
-        simulate_step(m, [1, 2], [0, 0, 0, 0], [0, 0])
-
-
-def test_tree_build_load_roundtrip():
+def test_tree_from_arrays_and_demands():
     t = synth.uniform_tree([3, 2], N=8, n_d=2, seed=11)
     assert t.n_s == 6 and t.n_edges == 3 + 6 + 6 * 6
-    back = load_tree(json.dumps(tree_document(t)))
-    for k in ("stage_starts", "anc", "child_start", "child_stop"):
-        np.testing.assert_array_equal(getattr(back, k), getattr(t, k))
-    np.testing.assert_allclose(back.prob, t.prob)
-    paths = scenario_paths(t)
-    assert len(paths) == 6 and all(len(p) == 9 for p in paths)
+    again = ScenarioTree.from_arrays(t.N, t.stage_starts, t.anc, t.prob, t.eps)
+    for k in ("stage_starts", "anc", "child_start", "child_stop", "prob", "eps"):
+        np.testing.assert_array_equal(getattr(again, k), getattr(t, k))
+    # children ranges: contiguous runs of the next stage, leaves empty at n_nodes
+    for node in range(t.n_nodes):
+        kids = np.flatnonzero(t.anc == node)
+        if kids.size:
+            assert (t.child_start[node], t.child_stop[node]) == (kids[0], kids[-1] + 1)
+        else:
+            assert t.child_start[node] == t.child_stop[node] == t.n_nodes
     fc = DemandForecast(np.ones((8, 2)), k=3)
-    d = node_demands(t, fc)
-    np.testing.assert_allclose(d, 1.0 + t.edge_eps)
+    np.testing.assert_allclose(node_demands(t, fc), 1.0 + t.edge_eps)
     with pytest.raises(DimensionError):
         node_demands(t, DemandForecast(np.ones((7, 2))))
 
 
 def test_tree_validation_errors():
+    t = synth.uniform_tree([2], N=2, n_d=1, seed=1)
+    with pytest.raises(ValidationError):   # stage probabilities do not sum to 1
+        ScenarioTree.from_arrays(t.N, t.stage_starts, t.anc, t.prob * 1.1, t.eps)
+    anc = t.anc.copy()
+    anc[4] = 0                             # a stage-2 node hanging from the root
     with pytest.raises(ValidationError):
-        build_tree([2], [np.zeros((2, 1))], [[1.0], [0.7, 0.7]], N=1)  # stage prob != 1
-    with pytest.raises(ParseError):
-        load_tree('{"N": 1, "stages": []}')
-    with pytest.raises(ValidationError):
-        build_tree([0], [np.zeros((1, 1))], [[1.0], [1.0]], N=1)
+        ScenarioTree.from_arrays(t.N, t.stage_starts, anc, t.prob, t.eps)
+    with pytest.raises(ValidationError):   # bad stage offsets
+        ScenarioTree.from_arrays(t.N, t.stage_starts[:-1], t.anc, t.prob, t.eps)
 
 
 @pytest.mark.parametrize("name,edges", [("CE", 24), ("SMPC1", 136), ("SMPC3", 2431),
@@ -118,3 +92,19 @@ def test_solver_config_validation():
         SolverConfig(lam=-1.0)
     with pytest.raises(ValidationError):
         SolverConfig(threads=0)
+
+
+def test_reference_style_solver_config_is_accepted():
+    """A SolverConfig without the device / tol / check_every extensions (the
+    reference's own class, engine.py:40-57) is read with defaults."""
+    from paper_1604_01074_b200 import engine
+
+    class RefConfig:  # the reference's fields only
+        max_iters, lam, precondition, threads = 5, None, True, 1
+        record_residuals, warm_start = False, False
+
+    cfg = RefConfig()
+    assert getattr(cfg, "device", 0) == 0 and getattr(cfg, "tol", None) is None
+    with pytest.raises(ValidationError):
+        SolverConfig(tol=1.0, record_residuals=True)
+    assert engine.solve.__doc__
