@@ -131,6 +131,13 @@ def _compile(srcs, out: pathlib.Path, extra=()) -> None:
         raise DeviceError(f"nvcc link failed ({' '.join(cmd)}):\n{res.stderr[-4000:]}")
 
 
+def build_variant(name: str, defines: list[str]) -> pathlib.Path:
+    """A-B experiment build: libtsmpc_<name>.so with extra -D defines (tools/ab_variants.sh)."""
+    out = PKG_DIR / f"libtsmpc_{name}.so"
+    _compile([CSRC / s for s in SOURCES], out, tuple(f"-D{d}" for d in defines))
+    return out
+
+
 def build_library(force: bool = False, verbose: bool = False, timers: bool = False) -> pathlib.Path:
     """Compile ``libtsmpc.so`` in-tree for sm_100a (cross-compiles without a GPU).
 

@@ -168,6 +168,21 @@ struct tsmpc_plan {
 namespace {
 
 // ---------------------------------------------------------------- planning
+// The structured-basis plan: split / resident / slot-streamed (apg_sparse_kernel),
+// or wide mode (apg_wide_kernel) when some CTA would stream its rows through a
+// tile slot, when a leaf chain is longer than a slot tile, and for shards
+// (TSMPC_NO_WIDE keeps the slot-streaming plan).
+SparseHostPlan choose_sparse_plan(const SparseTreeIn& ti, const SparseOpsIn& oi, int NXP, int NUP, int NVP,
+                                  int ctas, size_t smem_plain, size_t smem_wide, bool shard, int rank, int world) {
+  SparseHostPlan hp = plan_sparse(ti, oi, NXP, NUP, NVP, ctas, smem_plain, shard, rank, world);
+  if (!std::getenv("TSMPC_NO_WIDE") && oi.nx <= 128 && (!hp.ok || hp.resident_ctas < hp.n_ctas || shard)) {
+    SparseHostPlan hw = plan_sparse(ti, oi, NXP, NUP, NVP, ctas, smem_wide, shard, rank, world, true, true, true);
+    if (hw.ok) return hw;
+    if (!hp.ok) hp.why += std::string("; wide mode: ") + hw.why;
+  }
+  return hp;
+}
+
 struct Decomposition {
   int n_levels = 0;
   std::vector<int> lvl_tiles, tile_seg, seg_row, row_edge;
@@ -727,21 +742,12 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
       SparseOpsIn oi{nx, nu, nv, pb->B, pb->Ls, pb->lam_s};
       cudaFuncAttributes fa{};
       cudaFuncGetAttributes(&fa, apg_sparse_kernel);  // static shared memory counts against the opt-in limit
-      SparseHostPlan hp = plan_sparse(ti, oi, NXP, NUP, NVP, pl->sm_count,
-                                      (size_t)prop.sharedMemPerBlockOptin - fa.sharedSizeBytes, shard,
-                                      shard ? srank : 0, shard ? sworld : 1);
-      // wide mode (apg_wide_kernel) when some CTA would stream its rows through a
-      // tile slot, when a chain is longer than a slot tile, and for shards
-      // (TSMPC_NO_WIDE: the slot-streaming plan of apg_sparse_kernel)
-      if (!std::getenv("TSMPC_NO_WIDE") && nx <= 128 && (!hp.ok || hp.resident_ctas < hp.n_ctas || shard)) {
-        cudaFuncAttributes fw{};
-        cudaFuncGetAttributes(&fw, sparse_kernel_fn(1, nx));
-        SparseHostPlan hw = plan_sparse(ti, oi, NXP, NUP, NVP, pl->sm_count,
-                                        (size_t)prop.sharedMemPerBlockOptin - fw.sharedSizeBytes, shard,
-                                        shard ? srank : 0, shard ? sworld : 1, true, true, true);
-        if (hw.ok) hp = std::move(hw);
-        else if (!hp.ok) hp.why += std::string("; wide mode: ") + hw.why;
-      }
+      cudaFuncAttributes fw{};
+      cudaFuncGetAttributes(&fw, sparse_kernel_fn(1, nx));
+      SparseHostPlan hp = choose_sparse_plan(ti, oi, NXP, NUP, NVP, pl->sm_count,
+                                             (size_t)prop.sharedMemPerBlockOptin - fa.sharedSizeBytes,
+                                             (size_t)prop.sharedMemPerBlockOptin - fw.sharedSizeBytes, shard,
+                                             shard ? srank : 0, shard ? sworld : 1);
       const void* kfn = sparse_kernel_fn(hp.S.wide, nx);
       int occ_s = 0;
       if (hp.ok) {
@@ -1036,11 +1042,11 @@ int tsmpc_describe_sparse(const tsmpc_problem* pb, int32_t max_ctas, int64_t sme
     return fail(TSMPC_ERR_ARGUMENT, "null argument");
   SparseTreeIn ti{pb->N, pb->n_nodes, pb->stage_starts, pb->anc, pb->child_start, pb->child_stop, pb->prob};
   SparseOpsIn oi{pb->n_x, pb->n_u, pb->n_v, pb->B, pb->Ls, pb->lam_s};
-  SparseHostPlan hp = plan_sparse(ti, oi, r4(pb->n_x), r4(pb->n_u), r4(pb->n_v), std::max(1, (int)max_ctas),
-                                  (size_t)smem_limit);
+  SparseHostPlan hp = choose_sparse_plan(ti, oi, r4(pb->n_x), r4(pb->n_u), r4(pb->n_v), std::max(1, (int)max_ctas),
+                                         (size_t)smem_limit, (size_t)smem_limit, false, 0, 1);
   if (!hp.ok) return fail(TSMPC_ERR_VALIDATION, "%s", hp.why.c_str());
   const int64_t vals[] = {hp.n_ctas, hp.n_tiles, hp.n_chains, hp.n_trunk, hp.resident_ctas, hp.max_rows,
-                          hp.max_needs, (int64_t)hp.smem, hp.S.split_n};
+                          hp.max_needs, (int64_t)hp.smem, hp.S.split_n, hp.S.wide, hp.S.tile_cap};
   for (int i = 0; i < n && i < (int)(sizeof(vals) / sizeof(vals[0])); ++i) info[i] = vals[i];
   return TSMPC_OK;
 }
@@ -1052,8 +1058,8 @@ int tsmpc_describe_shard(const tsmpc_problem* pb, int32_t max_ctas, int64_t smem
     return fail(TSMPC_ERR_ARGUMENT, "null argument");
   SparseTreeIn ti{pb->N, pb->n_nodes, pb->stage_starts, pb->anc, pb->child_start, pb->child_stop, pb->prob};
   SparseOpsIn oi{pb->n_x, pb->n_u, pb->n_v, pb->B, pb->Ls, pb->lam_s};
-  SparseHostPlan hp = plan_sparse(ti, oi, r4(pb->n_x), r4(pb->n_u), r4(pb->n_v), std::max(1, (int)max_ctas),
-                                  (size_t)smem_limit, true, rank, world);
+  SparseHostPlan hp = choose_sparse_plan(ti, oi, r4(pb->n_x), r4(pb->n_u), r4(pb->n_v), std::max(1, (int)max_ctas),
+                                         (size_t)smem_limit, (size_t)smem_limit, true, rank, world);
   if (!hp.ok) return fail(TSMPC_ERR_VALIDATION, "%s", hp.why.c_str());
   int64_t owned_heads = 0;
   for (unsigned char t : hp.towned) owned_heads += t;

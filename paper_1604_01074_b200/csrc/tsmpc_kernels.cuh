@@ -195,6 +195,7 @@ struct SParams {
   // stay in region A when a CTA has one tile (tmode 0), else they go through TG.
   int wide;
   int wide_prefill;             // the epilogue of the CTA's last tile leaves the next fill
+  int hsum_nseg;                // wide split mode: chains per chain CTA the head-sum scratch holds
 };
 
 // Phase timers (profiling builds: -DTSMPC_TIMERS).  Slot k accumulates the cycles

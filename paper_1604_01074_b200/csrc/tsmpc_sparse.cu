@@ -156,7 +156,7 @@ struct Ctx {
   double* bnd;     // x_s, x_min, x_max (NXP), u_min, u_max (NUP), a_diag (NXP), p (NXP)
   double* scl;     // sig, zeta, 1/sig, 1/zeta per stage (N each)
   double* psi;     // psi_stage (N x NUP) or null (unscaled)
-  double* red;     // epilogue: partial norms [kTileS][4][2], factors [kTileS][2], row descriptors
+  double* red;     // epilogue row descriptors (5 ints per row)
   const int* spi;  // sparse index pool (shared)
   const double* spv;
   double* need;    // need rows [S | x | u]
@@ -170,12 +170,15 @@ struct Ctx {
   __device__ double* B() const { return work + tcap * LA; }
   __device__ const double* adiag() const { return bnd + 3 * NXP + 2 * NUP; }
   __device__ const double* proot() const { return bnd + 4 * NXP + 2 * NUP; }
-  __device__ int* rdesc() const { return reinterpret_cast<int*>(red + tcap * 10); }
+  __device__ int* rdesc() const { return reinterpret_cast<int*>(red); }
   const double* psi_g;  // psi_stage in HBM when the table does not fit shared memory
+  int psi_o;            // offset of the psi_stage table in shared memory, -1 if not there
+  // (indexing s_dyn directly keeps the access an LDS; a possibly-null pointer
+  // would compile to a generic load)
   __device__ double dpsi(int st, int k) const {
-    return psi ? psi[st * NUP + k] : (psi_g ? __ldg(psi_g + (size_t)st * NUP + k) : 1.0);
+    return psi_o >= 0 ? s_dyn[psi_o + st * NUP + k] : (psi_g ? __ldg(psi_g + (size_t)st * NUP + k) : 1.0);
   }
-  __device__ bool scaled() const { return psi || psi_g; }
+  __device__ bool scaled() const { return psi_o >= 0 || psi_g; }
 };
 
 __device__ __forceinline__ Ctx ctx_of() {
@@ -191,6 +194,7 @@ __device__ __forceinline__ Ctx ctx_of() {
   c.scl = s_dyn + S.O_SCL;
   c.red = s_dyn + S.O_RED;
   c.psi = P.scaled && S.psi_smem ? s_dyn + S.O_PSI : nullptr;
+  c.psi_o = P.scaled && S.psi_smem ? S.O_PSI : -1;
   c.psi_g = P.scaled && !S.psi_smem ? P.psi_stage : nullptr;
   c.LA = S.LA;
   c.tcap = S.tile_cap;
@@ -327,7 +331,11 @@ __device__ __forceinline__ EpiConst epi_const(const Params& P, int nu_it, double
   return k;
 }
 
+#ifndef TSMPC_WANT_T
+#define TSMPC_WANT_T 1
+#endif
 // psi block of row r, component k (k < n_u); u = the row's control component
+template <bool WANT>
 __device__ __forceinline__ void epi_psi_elem(const Ctx& c, const Params& P, const EpiConst& q, const int* d,
                                              int ysm, int k, double u, double& rmax, double ulo, double uhi) {
   const int e = d[0], st = d[1];
@@ -345,7 +353,7 @@ __device__ __forceinline__ void epi_psi_elem(const Ctx& c, const Params& P, cons
     const double wn = extrap(ny, yc[k], q.cfn);
     s_dyn[d[3] + k] = c.scaled() ? __dmul_rn(wn, dp) : wn;
   }
-  if (q.want) rmax = fmax(rmax, fabs(__dsub_rn(u, __ddiv_rn(t, dp))));
+  if (WANT && q.want) rmax = fmax(rmax, fabs(__dsub_rn(u, __ddiv_rn(t, dp))));
   double* ua = row + 2 * c.YW + c.NXP;
   const double na = __dadd_rn(__dmul_rn(ua[k], q.om), __dmul_rn(q.th, u));
   ua[k] = na;
@@ -356,9 +364,12 @@ __device__ __forceinline__ void epi_psi_elem(const Ctx& c, const Params& P, cons
   if (q.last) stcg(P.U + (size_t)e * c.NUP + k, u);
 }
 
-// state blocks of rows described by rdesc, one warp per row
-__device__ __noinline__ void epi_state(int nu_it, double cf, double th, int nrows, int ysm, bool wt, int ncur,
-                                       double* rmax_io, bool pre = false, double cfn = 0.0) {
+// state blocks of rows described by rdesc, one warp per row.  WANT: the residual
+// may be needed (compiled apart: otherwise ptxas if-converts its divisions into
+// every element)
+template <bool WANT>
+__device__ __noinline__ void epi_state_t(int nu_it, double cf, double th, int nrows, int ysm, bool wt, int ncur,
+                                         double* rmax_io, bool pre, double cfn) {
   const SParams& S = g_sp;
   const Ctx c = ctx_of();
   const Params& P = S.P;
@@ -436,7 +447,7 @@ __device__ __noinline__ void epi_state(int nu_it, double cf, double th, int nrow
         const double nz = __dadd_rn(wz[m], __dmul_rn(q.lam, __dsub_rn(hz, t_z)));
         yp[i] = ns;
         yp[c.NXP + i] = nz;
-        if (q.want) {
+        if (WANT && q.want) {
           rmax = fmax(rmax, fabs(__dsub_rn(xi, __ddiv_rn(t_s, ds))));
           rmax = fmax(rmax, fabs(__dsub_rn(xi, __ddiv_rn(t_z, dz))));
         }
@@ -459,8 +470,9 @@ __device__ __noinline__ void epi_state(int nu_it, double cf, double th, int nrow
 }
 
 // psi block of rows described by rdesc (component-major), u read from the rows
-__device__ __noinline__ void epi_psi_rows(int nu_it, double cf, double th, int nrows, int ysm, bool wt, int ncur,
-                                          double* rmax_io, bool pre = false, double cfn = 0.0) {
+template <bool WANT>
+__device__ __noinline__ void epi_psi_rows_t(int nu_it, double cf, double th, int nrows, int ysm, bool wt, int ncur,
+                                            double* rmax_io, bool pre, double cfn) {
   const SParams& S = g_sp;
   const Ctx c = ctx_of();
   const Params& P = S.P;
@@ -473,10 +485,22 @@ __device__ __noinline__ void epi_psi_rows(int nu_it, double cf, double th, int n
 #pragma unroll 1
     for (int r = g; r < nrows; r += kGroups) {
       const int* d = c.rdesc() + 5 * r;
-      epi_psi_elem(c, P, q, d, ysm, k, s_dyn[d[3] + k], rmax, ulo, uhi);
+      epi_psi_elem<WANT>(c, P, q, d, ysm, k, s_dyn[d[3] + k], rmax, ulo, uhi);
     }
   }
   *rmax_io = rmax;
+}
+
+__device__ __forceinline__ bool want_resid(const Params& P, int nu) { return is_last(P, nu) || P.record_all; }
+__device__ __forceinline__ void epi_state(int nu_it, double cf, double th, int nrows, int ysm, bool wt, int ncur,
+                                          double* rmax_io, bool pre = false, double cfn = 0.0) {
+  if (!TSMPC_WANT_T || want_resid(g_sp.P, nu_it)) epi_state_t<true>(nu_it, cf, th, nrows, ysm, wt, ncur, rmax_io, pre, cfn);
+  else epi_state_t<false>(nu_it, cf, th, nrows, ysm, wt, ncur, rmax_io, pre, cfn);
+}
+__device__ __forceinline__ void epi_psi_rows(int nu_it, double cf, double th, int nrows, int ysm, bool wt, int ncur,
+                                             double* rmax_io, bool pre = false, double cfn = 0.0) {
+  if (!TSMPC_WANT_T || want_resid(g_sp.P, nu_it)) epi_psi_rows_t<true>(nu_it, cf, th, nrows, ysm, wt, ncur, rmax_io, pre, cfn);
+  else epi_psi_rows_t<false>(nu_it, cf, th, nrows, ysm, wt, ncur, rmax_io, pre, cfn);
 }
 
 // ----------------------------------------------------------------------------
@@ -1567,13 +1591,28 @@ __device__ __noinline__ void trunk_own_rows(int nu_it, double cf, double th, int
 // fill and the epilogue, in chunks of rows whose loads are issued together.
 // XS: state components per lane in the warp-per-row state epilogue (n_x <= 32 XS).
 // ============================================================================
-constexpr int kChunkW = 4;   // rows whose loads a thread issues before using them
+#ifndef TSMPC_CHUNKW
+#define TSMPC_CHUNKW 8
+#endif
+#ifndef TSMPC_R2
+#define TSMPC_R2 2
+#endif
+#ifndef TSMPC_PREF
+#define TSMPC_PREF 1
+#endif
+constexpr int kChunkW = TSMPC_CHUNKW;  // rows whose loads a thread issues before using them (epilogue)
+constexpr int kChunkF = 4;   // the same for the (first-iteration) fill
+constexpr int kRW = kTileW / kGroups;   // rows per thread of a wide tile, (group, component) mapping
+constexpr int kG8 = kThreadsS / 64;     // row groups of the 64-lane mapping (components < 64)
+constexpr int kRX = kTileW / kG8;       // rows per thread of a wide tile in that mapping
 
-__device__ __forceinline__ const double* ysig(const double* Y, size_t e, int NXP) { return Y + e * NXP; }
 
-// psi block of the rows in rdesc (component-major, as epi_psi_rows), state in HBM
-__device__ __noinline__ void epi_psi_wide(int nu_it, double cf, double th, int nrows, int cur, double* rmax_io,
-                                          bool pre, double cfn) {
+// psi block of the rows in rdesc (component-major, as epi_psi_rows), state in HBM.
+// WANT: this iteration's residual is needed (compiled apart: otherwise ptxas
+// if-converts the residual's IEEE divisions into every element)
+template <bool WANT>
+__device__ __noinline__ void epi_psi_wide_t(int nu_it, double cf, double th, int nrows, int cur, double* rmax_io,
+                                            bool pre, double cfn) {
   const SParams& S = g_sp;
   const Ctx c = ctx_of();
   const Params& P = S.P;
@@ -1590,14 +1629,14 @@ __device__ __noinline__ void epi_psi_wide(int nu_it, double cf, double th, int n
 #pragma unroll 1
     for (int r0 = g; r0 < nrows; r0 += kChunkW * kGroups) {
       double yc[kChunkW], yp[kChunkW], ua[kChunkW];
-      size_t eo[kChunkW];
+      int eo[kChunkW];
 #pragma unroll
       for (int u = 0; u < kChunkW; ++u) {
         const int r = r0 + u * kGroups;
         eo[u] = 0;
         yc[u] = yp[u] = ua[u] = 0.0;
         if (r < nrows) {
-          eo[u] = (size_t)rd[5 * r] * c.NUP;
+          eo[u] = rd[5 * r] * c.NUP;
           yc[u] = ldcg(Yc + eo[u]);
           yp[u] = ldcg(Yn + eo[u]);
           ua[u] = ldcg(UA + eo[u]);
@@ -1618,7 +1657,7 @@ __device__ __noinline__ void epi_psi_wide(int nu_it, double cf, double th, int n
           const double t = fmin(fmax(a, __dmul_rn(dp, ulo)), __dmul_rn(dp, uhi));
           const double ny = __dadd_rn(w, __dmul_rn(q.lam, __dsub_rn(hp, t)));
           stcg(Yn + eo[u], ny);
-          if (q.want) rmax = fmax(rmax, fabs(__dsub_rn(uu, __ddiv_rn(t, dp))));
+          if (WANT && q.want) rmax = fmax(rmax, fabs(__dsub_rn(uu, __ddiv_rn(t, dp))));
           stcg(UA + eo[u], __dadd_rn(__dmul_rn(ua[u], q.om), __dmul_rn(q.th, uu)));
           if (q.last) stcg(P.U + eo[u] + k, uu);
           if (q.pre) {  // the next backward's fill of this element
@@ -1633,9 +1672,9 @@ __device__ __noinline__ void epi_psi_wide(int nu_it, double cf, double th, int n
 }
 
 // state blocks of the rows in rdesc, one warp per row (two rows in flight), state in HBM
-template <int XS>
-__device__ __noinline__ void epi_state_wide(int nu_it, double cf, double th, int nrows, int cur, double* rmax_io,
-                                            bool pre, double cfn) {
+template <int XS, bool WANT>
+__device__ __noinline__ void epi_state_wide_t(int nu_it, double cf, double th, int nrows, int cur, double* rmax_io,
+                                              bool pre, double cfn) {
   const SParams& S = g_sp;
   const Ctx c = ctx_of();
   const Params& P = S.P;
@@ -1657,15 +1696,15 @@ __device__ __noinline__ void epi_state_wide(int nu_it, double cf, double th, int
   double* Ns = P.ybuf[cur ^ 1];
   double* Nz = Ns + E * c.NXP;
   const int* rd = c.rdesc();
-  constexpr int R2 = 2;
+  constexpr int R2 = TSMPC_R2;
 #pragma unroll 1
   for (int r0 = kWarpsS - 1 - warp; r0 < nrows; r0 += R2 * kWarpsS) {
     double ycs[R2][XS], yps[R2][XS], ycz[R2][XS], ypz[R2][XS], xav[R2][XS];
-    size_t eo[R2];
+    int eo[R2];
 #pragma unroll
     for (int h = 0; h < R2; ++h) {
       const int r = r0 + h * kWarpsS;
-      eo[h] = r < nrows ? (size_t)rd[5 * r] * c.NXP : 0;
+      eo[h] = r < nrows ? rd[5 * r] * c.NXP : 0;
 #pragma unroll
       for (int m = 0; m < XS; ++m) {
         const int i = lane + 32 * m;
@@ -1727,7 +1766,7 @@ __device__ __noinline__ void epi_state_wide(int nu_it, double cf, double th, int
           const double nz = __dadd_rn(wz[m], __dmul_rn(q.lam, __dsub_rn(hz, t_z)));
           stcg(Ns + eo[h] + i, ns);
           stcg(Nz + eo[h] + i, nz);
-          if (q.want) {
+          if (WANT && q.want) {
             rmax = fmax(rmax, fabs(__dsub_rn(xi, __ddiv_rn(t_s, ds))));
             rmax = fmax(rmax, fabs(__dsub_rn(xi, __ddiv_rn(t_z, dz))));
           }
@@ -1742,6 +1781,20 @@ __device__ __noinline__ void epi_state_wide(int nu_it, double cf, double th, int
     }
   }
   *rmax_io = rmax;
+}
+
+__device__ __forceinline__ void epi_psi_wide(int nu_it, double cf, double th, int nrows, int cur, double* rmax,
+                                             bool pre, double cfn) {
+  const Params& P = g_sp.P;
+  if (!TSMPC_WANT_T || is_last(P, nu_it) || P.record_all) epi_psi_wide_t<true>(nu_it, cf, th, nrows, cur, rmax, pre, cfn);
+  else epi_psi_wide_t<false>(nu_it, cf, th, nrows, cur, rmax, pre, cfn);
+}
+template <int XS>
+__device__ __forceinline__ void epi_state_wide(int nu_it, double cf, double th, int nrows, int cur, double* rmax,
+                                               bool pre, double cfn) {
+  const Params& P = g_sp.P;
+  if (!TSMPC_WANT_T || is_last(P, nu_it) || P.record_all) epi_state_wide_t<XS, true>(nu_it, cf, th, nrows, cur, rmax, pre, cfn);
+  else epi_state_wide_t<XS, false>(nu_it, cf, th, nrows, cur, rmax, pre, cfn);
 }
 
 // backward sweep of wide tile ti (factor.py:142-156): fill from HBM (unless the
@@ -1761,15 +1814,23 @@ __device__ __noinline__ void bwd_wide(int ti, double cf, int cur, bool prefilled
   double* RB = c.B();
   long long tm_ = clock64();
   (void)tm_;
+  // beta_s of this thread's rows for the h phase, loaded now (the loads are in
+  // flight during the fill / head sums / xiq scan / z phases)
+  double bpre[kRW];
+#pragma unroll
+  for (int m = 0; m < kRW; ++m) {
+    const int r = g + kGroups * m;
+    bpre[m] = TSMPC_PREF && r < nrows && k < nv ? ldcg(S.beta_s + (size_t)c.mt.edge(row0 + r) * c.NVP + k) : 0.0;
+  }
   if (!prefilled) {
     // (1) fill: s = D_sig w_sig + D_zeta w_zeta -> A ; psi^ = D_psi w_psi -> B
     const double* Y = P.ybuf[cur];
     const double* Yp = P.ybuf[cur ^ 1];
 #pragma unroll 1
-    for (int r0 = g; r0 < nrows; r0 += kChunkW * kGroups) {
-      double a0[kChunkW], a1[kChunkW], a2[kChunkW], a3[kChunkW], b0[kChunkW], b1[kChunkW];
+    for (int r0 = g; r0 < nrows; r0 += kChunkF * kGroups) {
+      double a0[kChunkF], a1[kChunkF], a2[kChunkF], a3[kChunkF], b0[kChunkF], b1[kChunkF];
 #pragma unroll
-      for (int u = 0; u < kChunkW; ++u) {
+      for (int u = 0; u < kChunkF; ++u) {
         const int r = r0 + u * kGroups;
         a0[u] = a1[u] = a2[u] = a3[u] = b0[u] = b1[u] = 0.0;
         if (r < nrows) {
@@ -1789,7 +1850,7 @@ __device__ __noinline__ void bwd_wide(int ti, double cf, int cur, bool prefilled
         }
       }
 #pragma unroll
-      for (int u = 0; u < kChunkW; ++u) {
+      for (int u = 0; u < kChunkF; ++u) {
         const int r = r0 + u * kGroups;
         if (r < nrows) {
           const int st = c.mt.stage(row0 + r);
@@ -1806,8 +1867,78 @@ __device__ __noinline__ void bwd_wide(int ti, double cf, int cur, bool prefilled
     __syncthreads();
   }
   TSMPC_MARK(P, 0, tm_);
-  // (2) xiq scan, tail -> head, every chain of the tile at once
   const double* adiag = c.adiag();
+  if (S.split) {
+    // split mode: the trunk needs only each chain's head values, linear in the fill
+    // (see bwd_tile):  xiq_head = sum_d a^d s_d,  g_head = sum beta_s + Ls'(sum psi^ + B' sum_d G_d s_d).
+    // Per chain s of the tile: [sum beta_s] at hb + s NVP (launch constant), scratch
+    // row [hx (NXP) | hp (NUP) | hz (NUP)] at hs + s HL.
+    const double* hb = s_dyn + S.O_HSUM;
+    double* hs = s_dyn + S.O_HSUM + S.hsum_nseg * c.NVP;
+    const int HL = max(c.NXP + 2 * c.NUP, S.TR_LD);
+#pragma unroll 1
+    for (int idx = tid; idx < nsegs * (nx + nu); idx += kThreadsS) {
+      const int s = idx / (nx + nu), q = idx - s * (nx + nu);
+      const int* sg = c.mt.segs + 4 * (seg0 + s);
+      if (sg[2] < 0) continue;
+      const int lo = sg[0], n = sg[1] - lo;
+      if (q < nx) {
+        const double a = adiag[q];
+        double xh = 0.0, xs = 0.0, pw = 1.0, gw = 1.0;
+#pragma unroll 4
+        for (int d = 0; d < n; ++d) {
+          const double sv = RA[(lo + d) * LA + q];
+          xh = fma(pw, sv, xh);
+          xs = fma(gw, sv, xs);
+          pw = __dmul_rn(pw, a);
+          gw = __dadd_rn(gw, pw);
+        }
+        stcg(P.XIQG + (size_t)c.mt.edge(row0 + lo) * c.NXP + q, xh);
+        hs[s * HL + q] = xs;
+      } else {
+        const int j = q - nx;
+        double ps = 0.0;
+#pragma unroll 4
+        for (int d = 0; d < n; ++d) ps = __dadd_rn(ps, RB[(lo + d) * c.NUP + j]);
+        hs[s * HL + c.NXP + j] = ps;
+      }
+    }
+    __syncthreads();
+    {
+      const int* cp = c.spi + S.Bc_ptr;
+      const int* ci = c.spi + S.Bc_idx;
+      const double* cv = c.spv + S.Bc_val;
+#pragma unroll 1
+      for (int idx = tid; idx < nsegs * nu; idx += kThreadsS) {
+        const int s = idx / nu, j = idx - s * nu;
+        if (c.mt.segs[4 * (seg0 + s) + 2] < 0) continue;
+        const double* h = hs + s * HL;
+        double z = h[c.NXP + j];
+#pragma unroll 1
+        for (int q = cp[j]; q < cp[j + 1]; ++q) z = fma(cv[q], h[ci[q]], z);
+        hs[s * HL + c.NXP + c.NUP + j] = z;
+      }
+    }
+    __syncthreads();
+    {
+      const int* cp = c.spi + S.Lc_ptr;
+      const int* ci = c.spi + S.Lc_idx;
+      const double* cv = c.spv + S.Lc_val;
+#pragma unroll 1
+      for (int idx = tid; idx < nsegs * nv; idx += kThreadsS) {
+        const int s = idx / nv, k2 = idx - s * nv;
+        const int* sg = c.mt.segs + 4 * (seg0 + s);
+        if (sg[2] < 0) continue;
+        const double* hz = hs + s * HL + c.NXP + c.NUP;
+        double h = 0.0;
+#pragma unroll 1
+        for (int q = cp[k2]; q < cp[k2 + 1]; ++q) h = fma(cv[q], hz[ci[q]], h);
+        stcg(P.GG + (size_t)c.mt.edge(row0 + sg[0]) * c.NVP + k2, __dadd_rn(hb[s * c.NVP + k2], h));
+      }
+    }
+    signal_arrive(S.sub_ctr + 1);
+  }
+  // (2) xiq scan, tail -> head, every chain of the tile at once
 #pragma unroll 1
   for (int idx = tid; idx < nsegs * nx; idx += kThreadsS) {
     const int s = idx / nx, i = idx - s * nx;
@@ -1828,7 +1959,7 @@ __device__ __noinline__ void bwd_wide(int ti, double cf, int cur, bool prefilled
           col[(j1 - 1 - u) * LA] = x;
         }
     }
-    if (sg[2] >= 0) stcg(P.XIQG + (size_t)c.mt.edge(row0 + lo) * c.NXP + i, x);
+    if (sg[2] >= 0 && !S.split) stcg(P.XIQG + (size_t)c.mt.edge(row0 + lo) * c.NXP + i, x);
   }
   __syncthreads();
   TSMPC_MARK(P, 1, tm_);
@@ -1841,22 +1972,15 @@ __device__ __noinline__ void bwd_wide(int ti, double cf, int cur, bool prefilled
   }
   __syncthreads();
   TSMPC_MARK(P, 5, tm_);
-  // (4) h = beta_s + Ls' z (column k of Ls), A <- beta_s + Ls' B; beta_s loads per chunk
+  // (4) h = beta_s + Ls' z (column k of Ls), A <- beta_s + Ls' B
   if (k < nv) {
     const SpCol col = sp_col(c, S.Lc_ptr, S.Lc_idx, S.Lc_val, k);
-#pragma unroll 1
-    for (int r0 = g; r0 < nrows; r0 += kCh * kGroups) {
-      double b[kCh];
 #pragma unroll
-      for (int u = 0; u < kCh; ++u) {
-        const int r = r0 + u * kGroups;
-        b[u] = r < nrows ? ldcg(S.beta_s + (size_t)c.mt.edge(row0 + r) * c.NVP + k) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < kCh; ++u) {
-        const int r = r0 + u * kGroups;
-        if (r < nrows) RA[r * LA + k] = __dadd_rn(b[u], sp_dot(c, col, S.Lc_idx, S.Lc_val, RB + r * c.NUP, 0.0));
-      }
+    for (int m = 0; m < kRW; ++m) {
+      const int r = g + kGroups * m;
+      if (r < nrows)
+        RA[r * LA + k] = __dadd_rn(TSMPC_PREF ? bpre[m] : ldcg(S.beta_s + (size_t)c.mt.edge(row0 + r) * c.NVP + k),
+                                   sp_dot(c, col, S.Lc_idx, S.Lc_val, RB + r * c.NUP, 0.0));
     }
   }
   __syncthreads();
@@ -1889,13 +2013,15 @@ __device__ __noinline__ void bwd_wide(int ti, double cf, int cur, bool prefilled
         }
       }
     }
-    if (sg[2] >= 0) stcg(P.GG + (size_t)c.mt.edge(row0 + lo) * c.NVP + kk, gv);
+    if (sg[2] >= 0 && !S.split) stcg(P.GG + (size_t)c.mt.edge(row0 + lo) * c.NVP + kk, gv);
   }
   __syncthreads();
   TSMPC_MARK(P, 3, tm_);
 }
 
-// forward sweep of wide tile ti (factor.py:158-170) + epilogue
+// forward sweep of wide tile ti (factor.py:158-170) + epilogue; in split mode the
+// chains run with zero trunk input and the trunk terms and the epilogue follow in
+// fwd_finish_wide
 template <int XS>
 __device__ __noinline__ void fwd_wide(int ti, int nu_it, double cf, double th, int cur, double* rmax, bool pre,
                                       double cfn) {
@@ -1910,6 +2036,21 @@ __device__ __noinline__ void fwd_wide(int ti, int nu_it, double cf, double th, i
   double* RB = c.B();
   long long tm_ = clock64();
   (void)tm_;
+  // e (64-lane mapping, components < 64) and uhat of this thread's rows, loaded now
+  // (in flight during the S scan and du phases)
+  const int k8 = tid & 63, g8 = tid >> 6;
+  const bool x64 = nx <= 64;
+  double epre[kRX], upre[kRW];
+#pragma unroll
+  for (int m = 0; m < kRX; ++m) {
+    const int r = g8 + kG8 * m;
+    epre[m] = TSMPC_PREF && x64 && r < nrows && k8 < nx ? ldcg(P.evec + (size_t)c.mt.edge(row0 + r) * c.NXP + k8) : 0.0;
+  }
+#pragma unroll
+  for (int m = 0; m < kRW; ++m) {
+    const int r = g + kGroups * m;
+    upre[m] = TSMPC_PREF && r < nrows && k < nu ? ldcg(P.uhat + (size_t)c.mt.edge(row0 + r) * c.NUP + k) : 0.0;
+  }
   if (c.mt.tmode == 2) {  // t rows of this tile -> region A
     const int lane = tid & 31;
 #pragma unroll 1
@@ -1926,7 +2067,11 @@ __device__ __noinline__ void fwd_wide(int ti, int nu_it, double cf, double th, i
     d[1] = c.mt.stage(row0 + r);
     d[2] = (int)(RA + r * LA - s_dyn);
     d[3] = (int)(RB + r * c.NUP - s_dyn);
-    d[4] = 0;
+    if (!S.split) d[4] = 0;
+  }
+  if (S.split && tid < nsegs) {  // segment of every row (trunk terms of fwd_finish_wide)
+    const int* sg = c.mt.segs + 4 * (seg0 + tid);
+    for (int r = sg[0]; r < sg[1]; ++r) c.rdesc()[5 * r + 4] = tid;
   }
   if (c.mt.tmode == 2) cp_wait<0>();
   __syncthreads();
@@ -1937,7 +2082,7 @@ __device__ __noinline__ void fwd_wide(int ti, int nu_it, double cf, double th, i
     const int* sg = c.mt.segs + 4 * (seg0 + s);
     const int lo = sg[0], n = sg[1] - lo, pn = sg[2];
     double* scol = RA + lo * LA + kk;
-    double Sv = pn >= 0 ? c.need[(size_t)pn * S.need_ld + kk] : 0.0;
+    double Sv = pn >= 0 && !S.split ? c.need[(size_t)pn * S.need_ld + kk] : 0.0;  // split: added later
 #pragma unroll 1
     for (int j0 = 0; j0 < n; j0 += kCh) {
       double v[kCh];
@@ -1961,45 +2106,40 @@ __device__ __noinline__ void fwd_wide(int ti, int nu_it, double cf, double th, i
   }
   __syncthreads();
   TSMPC_MARK(P, 11, tm_);
-  // (3) bv + e = B du + e (row k of B), A <- B B + e; e loads per chunk
-  if (k < nx) {
-    const SpCol col = sp_col(c, S.Br_ptr, S.Br_idx, S.Br_val, k);
-#pragma unroll 1
-    for (int r0 = g; r0 < nrows; r0 += kCh * kGroups) {
-      double ev[kCh];
+  // (3) bv + e = B du + e (row k of B), A <- B B + e; 64 lanes x 8 row groups
+  // when n_x <= 64 (every thread busy), else the (group, component) mapping
+  if (x64) {
+    if (k8 < nx) {
+      const SpCol col = sp_col(c, S.Br_ptr, S.Br_idx, S.Br_val, k8);
 #pragma unroll
-      for (int u = 0; u < kCh; ++u) {
-        const int r = r0 + u * kGroups;
-        ev[u] = r < nrows ? ldcg(P.evec + (size_t)c.mt.edge(row0 + r) * c.NXP + k) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < kCh; ++u) {
-        const int r = r0 + u * kGroups;
-        if (r < nrows) RA[r * LA + k] = __dadd_rn(sp_dot(c, col, S.Br_idx, S.Br_val, RB + r * c.NUP, 0.0), ev[u]);
+      for (int m = 0; m < kRX; ++m) {
+        const int r = g8 + kG8 * m;
+        if (r < nrows)
+          RA[r * LA + k8] = __dadd_rn(sp_dot(c, col, S.Br_idx, S.Br_val, RB + r * c.NUP, 0.0),
+                                      TSMPC_PREF ? epre[m] : ldcg(P.evec + (size_t)c.mt.edge(row0 + r) * c.NXP + k8));
       }
     }
+  } else if (k < nx) {
+    const SpCol col = sp_col(c, S.Br_ptr, S.Br_idx, S.Br_val, k);
+#pragma unroll 2
+    for (int r = g; r < nrows; r += kGroups)
+      RA[r * LA + k] = __dadd_rn(sp_dot(c, col, S.Br_idx, S.Br_val, RB + r * c.NUP, 0.0),
+                                 ldcg(P.evec + (size_t)c.mt.edge(row0 + r) * c.NXP + k));
   }
   __syncthreads();
   TSMPC_MARK(P, 6, tm_);
   // (4) u = uhat + du (B; the psi epilogue below reads back only this thread's
   // entries: no barrier), then the x scan, head -> tail: x = a .* x_anc + (bv + e)
   if (k < nu) {
-#pragma unroll 1
-    for (int r0 = g; r0 < nrows; r0 += kCh * kGroups) {
-      double uh[kCh];
 #pragma unroll
-      for (int u = 0; u < kCh; ++u) {
-        const int r = r0 + u * kGroups;
-        uh[u] = r < nrows ? ldcg(P.uhat + (size_t)c.mt.edge(row0 + r) * c.NUP + k) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < kCh; ++u) {
-        const int r = r0 + u * kGroups;
-        if (r < nrows) RB[r * c.NUP + k] = __dadd_rn(RB[r * c.NUP + k], uh[u]);
-      }
+    for (int m = 0; m < kRW; ++m) {
+      const int r = g + kGroups * m;
+      if (r < nrows)
+        RB[r * c.NUP + k] = __dadd_rn(RB[r * c.NUP + k],
+                                      TSMPC_PREF ? upre[m] : ldcg(P.uhat + (size_t)c.mt.edge(row0 + r) * c.NUP + k));
     }
   }
-  epi_psi_wide(nu_it, cf, th, nrows, cur, rmax, pre, cfn);
+  if (!S.split) epi_psi_wide(nu_it, cf, th, nrows, cur, rmax, pre, cfn);
   {
     const double* adiag = c.adiag();
     const double* pr = c.proot();
@@ -2009,7 +2149,7 @@ __device__ __noinline__ void fwd_wide(int ti, int nu_it, double cf, double th, i
       const int* sg = c.mt.segs + 4 * (seg0 + s);
       const int lo = sg[0], n = sg[1] - lo, pn = sg[2];
       double* col = RA + lo * LA + i;
-      double x = pn >= 0 ? c.need[(size_t)pn * S.need_ld + c.NVP + i] : pr[i];
+      double x = pn >= 0 ? (S.split ? 0.0 : c.need[(size_t)pn * S.need_ld + c.NVP + i]) : pr[i];
       const double a = adiag[i];
 #pragma unroll 1
       for (int j0 = 0; j0 < n; j0 += kCh) {
@@ -2027,7 +2167,102 @@ __device__ __noinline__ void fwd_wide(int ti, int nu_it, double cf, double th, i
   }
   __syncthreads();
   TSMPC_MARK(P, 7, tm_);
+  if (S.split) return;  // trunk terms and epilogue: fwd_finish_wide
   // (5) epilogue, state blocks (warp per row)
+  epi_state_wide<XS>(nu_it, cf, th, nrows, cur, rmax, pre, cfn);
+  __syncthreads();
+  TSMPC_MARK(P, 8, tm_);
+}
+
+// split mode, after the chains' trunk parents are published (TR): the forward ran
+// with zero trunk input, and S, du, bv, x are affine in the parent's values, so
+//   u_e += du_tp,   x_e += G_d .* (B du_tp) + a^(d+1) .* x_tp   (d = depth below the head)
+// (see fwd_finish), for every chain of the wide tile; then the prox / dual epilogue.
+template <int XS>
+__device__ __noinline__ void fwd_finish_wide(int ti, int nu_it, double cf, double th, int cur, double* rmax, bool pre,
+                                             double cfn) {
+  const SParams& S = g_sp;
+  const Ctx c = ctx_of();
+  const Params& P = S.P;
+  const int* td = c.mt.tiles + 4 * ti;
+  const int nrows = td[1], seg0 = td[2], nsegs = td[3];
+  const int tid = threadIdx.x, k = tid & (kKW - 1), g = tid / kKW;
+  const int nx = c.nx, nu = c.nu, LA = c.LA;
+  double* RA = c.A();
+  double* RB = c.B();
+  long long tm_ = clock64();
+  (void)tm_;
+  // the parents' [du | B du | x] rows, staged once per chain
+  double* tr = s_dyn + S.O_HSUM + S.hsum_nseg * c.NVP;
+  const int HL = max(c.NXP + 2 * c.NUP, S.TR_LD);
+  {
+    constexpr int U = 4;  // loads in flight per thread (a 4-chain tile in one round)
+    double v[U];
+    int dst[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int idx = tid + u * kThreadsS;
+      const int s = idx / S.TR_LD, q = idx - s * S.TR_LD;
+      const int pn = s < nsegs ? c.mt.segs[4 * (seg0 + s) + 2] : -1;
+      dst[u] = pn >= 0 ? s * HL + q : -1;
+      v[u] = pn >= 0 ? ldcg(S.TR + (size_t)pn * S.TR_LD + q) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (dst[u] >= 0) tr[dst[u]] = v[u];
+#pragma unroll 1
+    for (int idx = tid + U * kThreadsS; idx < nsegs * S.TR_LD; idx += kThreadsS) {
+      const int s = idx / S.TR_LD, q = idx - s * S.TR_LD;
+      const int pn = c.mt.segs[4 * (seg0 + s) + 2];
+      if (pn >= 0) tr[s * HL + q] = ldcg(S.TR + (size_t)pn * S.TR_LD + q);
+    }
+  }
+  __syncthreads();
+  const int* rd = c.rdesc();
+  if (k < nu) {
+#pragma unroll 2
+    for (int r = g; r < nrows; r += kGroups) {
+      const int s = rd[5 * r + 4];
+      if (c.mt.segs[4 * (seg0 + s) + 2] >= 0) RB[r * c.NUP + k] = __dadd_rn(RB[r * c.NUP + k], tr[s * HL + k]);
+    }
+  }
+  TSMPC_MARK(P, 13, tm_);
+  if (S.a_unit) {
+    // a = 1: G_d = d + 1 and a^(d+1) = 1 exactly, every row independent
+#pragma unroll 1
+    for (int idx = tid; idx < nrows * nx; idx += kThreadsS) {
+      const int r = idx / nx, i = idx - r * nx;
+      const int s = rd[5 * r + 4];
+      const int* sg = c.mt.segs + 4 * (seg0 + s);
+      if (sg[2] < 0) continue;
+      const double bt = tr[s * HL + c.NUP + i], xt = tr[s * HL + c.NUP + c.NXP + i];
+      double* x = RA + r * LA + i;
+      *x = __dadd_rn(*x, __dadd_rn(__dmul_rn((double)(r - sg[0] + 1), bt), __dmul_rn(1.0, xt)));
+    }
+  } else {
+    const double* adiag = c.adiag();
+#pragma unroll 1
+    for (int idx = tid; idx < nsegs * nx; idx += kThreadsS) {
+      const int s = idx / nx, i = idx - s * nx;
+      const int* sg = c.mt.segs + 4 * (seg0 + s);
+      if (sg[2] < 0) continue;
+      const int lo = sg[0], n = sg[1] - lo;
+      const double bt = tr[s * HL + c.NUP + i], xt = tr[s * HL + c.NUP + c.NXP + i];
+      const double a = adiag[i];
+      double* col = RA + lo * LA + i;
+      double gs = 1.0, pw = a;
+#pragma unroll 4
+      for (int j = 0; j < n; ++j) {
+        col[j * LA] = __dadd_rn(col[j * LA], __dadd_rn(__dmul_rn(gs, bt), __dmul_rn(pw, xt)));
+        gs = __dadd_rn(__dmul_rn(gs, a), 1.0);
+        pw = __dmul_rn(pw, a);
+      }
+    }
+  }
+  __syncthreads();
+  TSMPC_MARK(P, 14, tm_);
+  epi_psi_wide(nu_it, cf, th, nrows, cur, rmax, pre, cfn);
+  TSMPC_MARK(P, 15, tm_);
   epi_state_wide<XS>(nu_it, cf, th, nrows, cur, rmax, pre, cfn);
   __syncthreads();
   TSMPC_MARK(P, 8, tm_);
@@ -2368,7 +2603,24 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel() {
   const int nt = c.mt.ntiles;
   const bool trunk = P.n_trunk > 0;
   const bool do_a = S.phase & 1, do_b = S.phase & 2;
+  const bool chain_cta = (int)blockIdx.x < S.split_c0;
+  if (S.split && chain_cta && nt == 1) {
+    // per chain, the sum of beta_s over its rows (static during the launch), chain order
+    double* hb = s_dyn + S.O_HSUM;
+    const int nsg = c.mt.tiles[3], sg0 = c.mt.tiles[2], row0 = c.mt.tiles[0];
+#pragma unroll 1
+    for (int idx = threadIdx.x; idx < nsg * c.nv; idx += kThreadsS) {
+      const int s = idx / c.nv, k = idx - s * c.nv;
+      const int* sg = c.mt.segs + 4 * (sg0 + s);
+      double b = 0.0;
+#pragma unroll 1
+      for (int d = sg[0]; d < sg[1]; ++d) b = __dadd_rn(b, ldcg(S.beta_s + (size_t)c.mt.edge(row0 + d) * c.NVP + k));
+      hb[s * c.NVP + k] = b;
+    }
+    __syncthreads();
+  }
   double rmax = 0.0;
+  unsigned int sub_target = 0;  // trunk-CTA barrier episodes x split_n (split mode)
   double cf = P.coef[S.nu0], th = P.theta[S.nu0];
   for (int nu = S.nu0; nu < S.nu1; ++nu) {
     const int cur = (P.slot0 + nu) & 1;
@@ -2391,7 +2643,44 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel() {
         head_prereduce();
       }
     }
-    if (do_b) {
+    if (do_b && trunk && S.split) {
+      // wide split mode, directed signals: chain CTAs published their heads in the
+      // backward and run the zero-input forward at once; trunk CTAs wait for every
+      // chain's heads, sweep, run the trunk forward and publish TR; chain CTAs wait
+      // for TR only before their trunk terms
+      long long tb_ = clock64();
+      (void)tb_;
+      const unsigned it = (unsigned)(nu - S.nu0 + 1);
+      if (chain_cta) {
+        for (int t = 0; t < nt; ++t) fwd_wide<XS>(t, nu, cf, th, cur, &rmax, false, 0.0);
+        TSMPC_MARK(P, 10, tb_);
+        signal_wait(S.sub_ctr + 2, it * (unsigned)S.split_n);
+        TSMPC_MARK(P, 9, tb_);
+        if (blockIdx.x == 0) {
+          const double om = __dsub_rn(1.0, th);
+          for (int i = threadIdx.x; i < c.nx; i += kThreadsS)
+            P.xavg[i] = __dadd_rn(__dmul_rn(P.xavg[i], om), __dmul_rn(th, c.proot()[i]));
+        }
+        for (int t = 0; t < nt; ++t)
+          fwd_finish_wide<XS>(t, nu, cf, th, cur, &rmax, S.wide_prefill && t == nt - 1 && nu + 1 < S.nu1, cf_n);
+        TSMPC_MARK(P, 3, tb_);
+      } else {
+        // the previous iteration's trunk-row epilogues (dual rows the sweep reads)
+        if (nu > S.nu0) trunk_barrier(S.sub_ctr, (unsigned)S.split_n, sub_target);
+        trunk_sweep(cf, cur, 1);  // own terms, before the heads arrive
+        signal_wait(S.sub_ctr + 1, it * (unsigned)S.split_c0);
+        TSMPC_MARK(P, 9, tb_);
+        trunk_sweep(cf, cur, 2);
+        TSMPC_MARK(P, 10, tb_);
+        trunk_barrier(S.sub_ctr, (unsigned)S.split_n, sub_target);
+        TSMPC_MARK(P, 11, tb_);
+        trunk_needs();
+        signal_arrive(S.sub_ctr + 2);
+        TSMPC_MARK(P, 12, tb_);
+        trunk_own_rows_wide<XS>(nu, cf, th, cur, &rmax);
+        TSMPC_MARK(P, 3, tb_);
+      }
+    } else if (do_b) {
       if (trunk) {
         long long tb_ = clock64();
         (void)tb_;
@@ -2412,6 +2701,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel() {
       }
       for (int t = 0; t < nt; ++t)
         fwd_wide<XS>(t, nu, cf, th, cur, &rmax, S.wide_prefill && t == nt - 1 && nu + 1 < S.nu1, cf_n);
+    }
+    if (do_b) {
       if (nu == P.iters - 1 || P.record_all || is_check(P, nu)) {
         __shared__ double s_rmax[kThreadsS / 32];
         for (int off = 16; off > 0; off >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, off));

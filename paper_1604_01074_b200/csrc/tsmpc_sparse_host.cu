@@ -144,22 +144,51 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
     if (const char* e = std::getenv("TSMPC_TRUNK_CTAS")) want = std::max(kMinTrunkCtas, std::atoi(e));
     if (spare >= kMinTrunkCtas) split_n = std::min(spare, want);
   }
-  const int nch_split = split_n ? (int)chains.size() : 0;
   // ---- CTA count and chain assignment (contiguous, balanced by rows)
   long long R = 0;
   for (auto& ch : chains) R += (long long)ch.size();
+  // rows of the fullest CTA when the chains are spread over C CTAs by the midpoint rule
+  auto fullest = [&](int C) {
+    std::vector<long long> rows(C, 0);
+    long long pre = 0, mx = 0;
+    for (auto& ch : chains) {
+      const long long mid2 = 2 * pre + (long long)ch.size();
+      const int c = std::min(std::max((int)((mid2 * C) / (2 * std::max<long long>(R, 1))), 0), C - 1);
+      mx = std::max(mx, rows[c] += (long long)ch.size());
+      pre += (long long)ch.size();
+    }
+    return mx;
+  };
+  // wide split mode: the fewest chain CTAs that keep the fullest CTA at its
+  // all-CTA load (one wide tile each); the rest run the trunk
+  int nch_wide = 0;
+  if (wide && allow_split && !sharded && T > 0 && !chains.empty() && !std::getenv("TSMPC_NO_SPLIT")) {
+    const long long full = fullest(max_ctas);
+    if (full <= kTileW) {
+      for (int c0 = (int)std::max<long long>(1, (R + full - 1) / full); c0 <= max_ctas - kMinTrunkCtas; ++c0)
+        if (fullest(c0) <= full) {
+          nch_wide = c0;
+          break;
+        }
+      if (const char* e = std::getenv("TSMPC_TRUNK_CTAS"))
+        nch_wide = std::max(nch_wide, max_ctas - std::max(kMinTrunkCtas, std::atoi(e)));
+      if (nch_wide > 0) split_n = max_ctas - nch_wide;
+    }
+  }
+  const int nch_split = split_n ? (nch_wide ? nch_wide : (int)chains.size()) : 0;
   int C = T > 0 ? max_ctas : std::max(1, std::min(max_ctas, (int)chains.size()));
   if (T > 0) C = std::max(1, std::min(max_ctas, (int)chains.size() + T));
   if (split_n) C = nch_split + split_n;
   std::vector<std::vector<int>> cta_chains(C);
-  if (split_n) {
+  if (split_n && !nch_wide) {
     for (int i = 0; i < nch_split; ++i) cta_chains[i].push_back(i);
   } else {
+    const int Cc = nch_wide ? nch_wide : C;  // CTAs holding chains
     long long pre = 0;
     for (int i = 0; i < (int)chains.size(); ++i) {
       const long long mid2 = 2 * pre + (long long)chains[i].size();
-      int c = (int)((mid2 * C) / (2 * std::max<long long>(R, 1)));
-      c = std::min(std::max(c, 0), C - 1);
+      int c = (int)((mid2 * Cc) / (2 * std::max<long long>(R, 1)));
+      c = std::min(std::max(c, 0), Cc - 1);
       cta_chains[c].push_back(i);
       pre += (long long)chains[i].size();
     }
@@ -460,7 +489,7 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
   S.O_SCL = (int)off;
   off += even(4LL * N);
   S.O_RED = (int)off;
-  off += 10LL * tcap + (5 * tcap + 1) / 2 + 1;  // partial norms, factors, row descriptors
+  off += (5 * tcap + 1) / 2 + 1;  // epilogue row descriptors
   off = even(off);
   S.O_PSI = (int)off;
   S.psi_smem = psi_in_smem ? 1 : 0;
@@ -495,6 +524,9 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
       any_t0 |= metas[c][7] == 0;
       max_rows_w = std::max(max_rows_w, cta_rows[c]);
     }
+    if (std::getenv("TSMPC_PLAN_DEBUG"))
+      std::fprintf(stderr, "plan_sparse wide: tcap=%d off=%lld ints_d=%lld limit=%lld psi=%d\n", tcap, off, ints_d,
+                   limit_d, (int)psi_in_smem);
     if (slot_avail < 0) {
       if (psi_in_smem)
         return plan_sparse(t, ops, NXP, NUP, NVP, max_ctas, smem_limit, sharded, rank, world, false, allow_split,
@@ -516,6 +548,8 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
     S.slot_ld = (int)base_ld;
     S.slot_rows = 0;
     S.wide_prefill = 1;
+    S.split = 0;
+    S.TR_LD = NUP + 2 * NXP;
     {
       const long long sched_d = ((long long)out.tsched.size() + 1) / 2 + 1;
       S.sched_resident = (T > 0 && off + ints_d + sched_d <= limit_d) ? 1 : 0;
@@ -526,8 +560,38 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
     S.O_INT = (int)off;
     off += ints_d;
     S.O_HSUM = (int)off;
-    S.split = 0;
-    S.TR_LD = NUP + 2 * NXP;
+    if (split_n) {
+      // chain CTAs: per chain [sum beta_s (NVP)] and a scratch row of max(NXP + 2 NUP,
+      // TR_LD) (head sums during the backward, the parent's TR row in the finish)
+      int nsm = 1;
+      for (int c = 0; c < nch_split; ++c) nsm = std::max(nsm, metas[c][2]);
+      const long long hsum = (long long)nsm * (NVP + std::max(NXP + 2LL * NUP, (long long)S.TR_LD));
+      const bool fits = off + even(hsum) <= limit_d;
+      bool single = true;
+      for (int c = 0; c < nch_split; ++c) single &= metas[c][0] == 1;
+      if (!fits || !single)  // no room for the head sums / multi-tile chain CTAs: plain wide
+        return plan_sparse(t, ops, NXP, NUP, NVP, max_ctas, smem_limit, sharded, rank, world, psi_in_smem, false,
+                           true);
+      off += even(hsum);
+      S.hsum_nseg = nsm;
+      S.split = 1;
+      S.split_c0 = nch_split;
+      S.split_n = split_n;
+      S.split_flags = 1;
+      S.split_heads = 1;
+      S.split_local = 0;
+      S.tops = 0;
+      S.sweep_in_a = 1;  // the trunk CTAs hold no tiles: the whole work region is theirs
+      const long long zx = 2LL * T * ((ncomp + split_n - 1) / split_n) + T;
+      S.sched_smem = zx + sched <= (long long)S.n_work ? 1 : 0;
+      if (zx > (long long)S.n_work) {
+        out.why = "trunk too large for the work region";
+        return out;
+      }
+    }
+    if (std::getenv("TSMPC_PLAN_DEBUG"))
+      std::fprintf(stderr, "plan_sparse wide: split %d (chain CTAs %d, trunk CTAs %d), smem %lld doubles\n", S.split,
+                   nch_split, split_n, off);
     S.meta_max = meta_max;
     out.smem = (size_t)off * sizeof(double);
     out.meta.clear();

@@ -329,7 +329,7 @@ def describe_sparse(model, tree, factor, max_ctas: int = 148, smem_limit: int = 
     for name, arr in keep.items():
         setattr(pb, name, nat.iptr(arr) if arr.dtype == np.int64 else nat.dptr(arr))
     keys = ("ctas", "tiles", "chains", "trunk_edges", "resident_ctas", "max_rows", "max_needs",
-            "smem_bytes", "trunk_ctas")
+            "smem_bytes", "trunk_ctas", "wide", "tile_rows")
     buf = np.zeros(len(keys), dtype=np.int64)
     nat.check(lib.tsmpc_describe_sparse(ctypes.byref(pb), int(max_ctas), int(smem_limit),
                                         nat.iptr(buf), len(keys)), "tsmpc_describe_sparse")

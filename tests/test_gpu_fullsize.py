@@ -42,7 +42,7 @@ def test_full_size_tree_matches_oracle(tree_name, iters, path, monkeypatch):
     info = plan.info()
     assert info["sparse"] == (1 if path == "sparse" else 0), info["path"]
     if tree_name != "SMPC3" and path == "sparse":
-        assert info["resident_ctas"] < info["ctas"] and info["trunk_ctas"] == 0, info
+        assert info["wide"] == 1 and info["resident_ctas"] == 0, info
     lam = 0.05
     th, cf = engine.theta_schedule(iters)
     out = plan.solve(W["p"], iters, lam, theta=th, coef=cf, skip_gap=True, record_residuals=True)

@@ -95,16 +95,25 @@ def test_sparse_planner_paper_trees():
     assert got["SMPC3"]["resident_ctas"] == got["SMPC3"]["ctas"] == 114 + 34
     assert got["SMPC1"]["trunk_ctas"] == 8 and got["SMPC1"]["ctas"] == 6 + 8
     assert got["SMPC3"]["max_rows"] == 21
-    # SMPC8: 3-4 chains per CTA -> streamed tile slots, no split
+    # SMPC8: 3-4 chains per CTA -> wide mode (a CTA's chains as one tile, rows in HBM),
+    # split: the fewest chain CTAs keeping 4 chains (84 rows) per CTA, the trunk on the rest
     assert got["SMPC8"]["chains"] == 493 and got["SMPC8"]["resident_ctas"] == 0
-    assert got["SMPC8"]["trunk_ctas"] == 0 and got["CE"]["trunk_ctas"] == 0
+    assert got["SMPC8"]["wide"] == 1 and got["SMPC8"]["max_rows"] == 84
+    assert got["SMPC8"]["trunk_ctas"] == 148 - 124 and got["SMPC8"]["tiles"] == 124
+    assert got["CE"]["trunk_ctas"] == 0 and got["SMPC3"]["wide"] == 0
 
 
-def test_sparse_planner_rejects_long_chains():
+def test_sparse_planner_long_chains():
+    """Chains longer than a slot tile (24 rows) run in wide mode (up to 96 rows per
+    chain: any horizon N <= 96 for the paper's tree shapes); longer ones are refused
+    (the dense kernel takes those plans)."""
     m = synth.three_tank_network()
     b = compute_basis(m)
     f = factor_step(b, m)
-    t = synth.uniform_tree([2], N=30, n_d=2, seed=3)   # two chains of 30 edges > tile
+    t = synth.uniform_tree([2], N=30, n_d=2, seed=3)   # two chains of 30 edges > slot tile
+    d = describe_sparse(m, t, f)
+    assert d["wide"] == 1 and d["max_rows"] == 30
+    t = synth.uniform_tree([2], N=100, n_d=2, seed=3)  # chains of 100 edges > wide tile
     from paper_1604_01074_b200.errors import ValidationError
     with pytest.raises(ValidationError):
         describe_sparse(m, t, f)

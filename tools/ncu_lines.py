@@ -22,6 +22,7 @@ ap.add_argument("rep")
 ap.add_argument("lib", nargs="?", default="paper_1604_01074_b200/libtsmpc.so")
 ap.add_argument("--top", type=int, default=40)
 ap.add_argument("--cubin", default="tsmpc_apg.sm_100a.cubin")
+ap.add_argument("--by-instr", action="store_true", help="rank lines by instructions executed")
 a = ap.parse_args()
 
 src = subprocess.run(["ncu", "-i", a.rep, "--page", "source", "--csv", "--print-source", "sass"],
@@ -74,7 +75,8 @@ tot_s = sum(sum(v for k, v in d.items() if k != "instr") for d in agg.values()) 
 tot_i = sum(d["instr"] for d in agg.values()) or 1.0
 files = {}
 print(f"unmatched rows: {miss}/{len(data)}   total stall samples {tot_s:.0f}")
-items = sorted(agg.items(), key=lambda kv: -sum(v for k, v in kv[1].items() if k != "instr"))
+items = sorted(agg.items(), key=(lambda kv: -kv[1]["instr"]) if a.by_instr else
+               (lambda kv: -sum(v for k, v in kv[1].items() if k != "instr")))
 for loc, d in items[: a.top]:
     s = sum(v for k, v in d.items() if k != "instr")
     top = sorted(((k.replace("stall_", ""), v) for k, v in d.items() if k != "instr" and v > 0),
