@@ -82,9 +82,11 @@ __global__ void gap_propagate_paths_kernel(EdgeCtx c, int n_nodes, double* xf, c
 __global__ void gap_primal_terms_kernel(EdgeCtx c, const double* uf, const double* xf, double* cols);
 
 __global__ void apg_persistent_kernel(const __grid_constant__ Params P);
-__global__ void apg_sparse_kernel();
+__global__ void apg_sparse_kernel(LaunchWin win);
 // copies S to the kernel's constant parameter block and launches (cooperative)
-cudaError_t sparse_launch(const SParams& S, int ctas, size_t smem, cudaStream_t stream);
+cudaError_t sparse_launch(const SParams& S, LaunchWin w, int ctas, size_t smem, cudaStream_t stream);
+cudaError_t sparse_params_upload(const SParams& S, cudaStream_t stream);
+cudaError_t sparse_note_launch(cudaStream_t stream);
 const void* sparse_kernel_fn(int wide, int nx);
 __global__ void beta_rotate_kernel(const double* __restrict__ beta, const double* __restrict__ M, double* out,
                                    int E, int nv, int NVP);

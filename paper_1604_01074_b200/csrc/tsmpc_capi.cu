@@ -112,6 +112,10 @@ struct tsmpc_plan {
   bool dyk_warp = std::getenv("TSMPC_DYKSTRA_WARP") != nullptr;
   bool dyk_two_pass = std::getenv("TSMPC_DYKSTRA_TWO_PASS") != nullptr;
   std::vector<int> owned_edges, trunk_edges;
+  int* d_trunk = nullptr;           // shard plans: trunk edge ids (device), for the gap's assembly
+  cudaGraphExec_t gexec = nullptr;  // sharded solve: the captured launches + all-reduces
+  int g_iters = 0;
+  std::string graph_why;
   // plan stats
   int n_levels = 0, n_tiles = 0, n_segs = 0, n_ctas = 0, n_trunk = 0;
   int dyk_blocks = 0;
@@ -151,6 +155,7 @@ struct tsmpc_plan {
   }
   ~tsmpc_plan() {
     if (stream) cudaStreamSynchronize(stream);
+    if (gexec) cudaGraphExecDestroy(gexec);
     if (comm && nccl) nccl->CommDestroy(comm);
     for (void* p : allocs) cudaFree(p);
     if (ev0) cudaEventDestroy(ev0);
@@ -810,6 +815,8 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
           pl->total_chains = hp.total_chains;
           pl->owned_edges = hp.owned_edges;
           pl->trunk_edges = hp.trunk_edge;
+          rc |= pl->upload(&pl->d_trunk, hp.trunk_edge.data(), std::max<size_t>(1, hp.trunk_edge.size()));
+          if (rc) return bail(0);
         }
         pl->use_sparse = true;
         pl->sp_ctas = hp.n_ctas;
@@ -1448,6 +1455,49 @@ int solve_prepare(tsmpc_plan* pl, const double* p, int32_t iters, double lam, co
   return TSMPC_OK;
 }
 
+// Shard plans hold their owned chain rows and the replicated trunk rows; the other
+// rows are zero.  Before the duality gap every rank assembles the full ergodic
+// averages and final dual by a sum over ranks, with the replicated rows (trunk edges
+// and the root's x_avg) counted on rank 0 only: exact, each entry has one
+// non-zero contributor.
+__global__ void zero_trunk_rows_kernel(const int* te, int T, int E, int NXP, int NUP, double* xavg, double* uavg,
+                                       double* y) {
+  const int b = blockIdx.x;
+  if (b == T) {
+    for (int i = threadIdx.x; i < NXP; i += blockDim.x) xavg[i] = 0.0;
+    return;
+  }
+  const size_t e = (size_t)te[b];
+  for (int i = threadIdx.x; i < NXP; i += blockDim.x) {
+    xavg[(e + 1) * NXP + i] = 0.0;
+    y[e * NXP + i] = 0.0;
+    y[(size_t)E * NXP + e * NXP + i] = 0.0;
+  }
+  for (int j = threadIdx.x; j < NUP; j += blockDim.x) {
+    uavg[e * NUP + j] = 0.0;
+    y[2 * (size_t)E * NXP + e * NUP + j] = 0.0;
+  }
+}
+
+int zero_replicated_rows(tsmpc_plan* pl, double* yfin, cudaStream_t s) {
+  const int T = (int)pl->trunk_edges.size();
+  zero_trunk_rows_kernel<<<T + 1, 128, 0, s>>>(pl->d_trunk, T, pl->E, pl->NXP, pl->NUP, pl->XAVG, pl->UAVG, yfin);
+  CU(cudaGetLastError());
+  return TSMPC_OK;
+}
+
+int assemble_shard_state(tsmpc_plan* pl, double* yfin) {
+  if (pl->rank != 0 && zero_replicated_rows(pl, yfin, pl->stream)) return TSMPC_ERR_CUDA;
+  const size_t yblk = 2 * (size_t)pl->E * pl->NXP + (size_t)pl->E * pl->NUP;
+  struct { double* p; size_t n; } bufs[] = {{pl->XAVG, (size_t)pl->n_nodes * pl->NXP},
+                                            {pl->UAVG, (size_t)pl->E * pl->NUP}, {yfin, yblk}};
+  for (auto& b : bufs) {
+    const int nr = pl->nccl->AllReduce(b.p, b.p, b.n, NcclApi::kFloat64, NcclApi::kSum, pl->comm, pl->stream);
+    if (nr != 0) return fail(TSMPC_ERR_NCCL, "ncclAllReduce: %s", pl->nccl->GetErrorString(nr));
+  }
+  return TSMPC_OK;
+}
+
 SParams sparse_params(const tsmpc_plan* pl, const Params& P) {
   SParams S = pl->sbase;
   S.P = P;
@@ -1456,7 +1506,8 @@ SParams sparse_params(const tsmpc_plan* pl, const Params& P) {
   return S;
 }
 
-int solve_finish(tsmpc_plan* pl, const SolveState& st, int32_t flags, tsmpc_result* out) {
+int solve_finish(tsmpc_plan* pl, const SolveState& st, int32_t flags, tsmpc_result* out,
+                 bool assembled = false) {
   const int E = pl->E, NXP = pl->NXP, NUP = pl->NUP, nx = pl->nx, nu = pl->nu;
   const int iters = st.iters, nres = st.nres;
   const bool record = st.record, stopping = st.stopping;
@@ -1478,6 +1529,11 @@ int solve_finish(tsmpc_plan* pl, const SolveState& st, int32_t flags, tsmpc_resu
     return fail(TSMPC_ERR_CUDA, "sparse kernel: a chain/trunk signal wait timed out (launch results discarded)");
   double* yfin = ((done & 1) == 0) ? pl->Y0 : pl->Y1;
   pl->last_y = yfin;
+  const bool want_gap = !(flags & TSMPC_SKIP_GAP) && (!pl->sharded || pl->comm || assembled);
+  if (want_gap && pl->sharded && pl->comm && !assembled) {
+    int rc = assemble_shard_state(pl, yfin);
+    if (rc) return rc;
+  }
   // keep the last iterate before the gap's solve step reuses X / U
   CU(cudaMemcpyAsync(pl->XL, pl->X, sizeof(double) * (size_t)pl->n_nodes * NXP, cudaMemcpyDeviceToDevice, pl->stream));
   CU(cudaMemcpyAsync(pl->UL, pl->U, sizeof(double) * (size_t)E * NUP, cudaMemcpyDeviceToDevice, pl->stream));
@@ -1501,7 +1557,7 @@ int solve_finish(tsmpc_plan* pl, const SolveState& st, int32_t flags, tsmpc_resu
     if (rc) return rc;
   }
   double gap = NAN;
-  if (!(flags & TSMPC_SKIP_GAP) && !pl->sharded) {
+  if (want_gap) {
     int rc = compute_gap(pl, yfin, &gap);
     if (rc) {
       cudaStreamSynchronize(cs);
@@ -1560,13 +1616,9 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
         if (pl->alloc(&pl->GTR, (size_t)iters * 10)) return TSMPC_ERR_CUDA;
         pl->gtr_cap = iters;
       }
-      S.phase = 3;
-      S.wb_end = 1;
       for (int nu = 0; nu < iters; ++nu) {
-        S.nu0 = nu;
-        S.nu1 = nu + 1;
         if (pl->SUBCTR) CU(cudaMemsetAsync(pl->SUBCTR, 0, 4 * sizeof(unsigned int), pl->stream));
-        CU(sparse_launch(S, pl->sp_ctas, pl->sp_smem, pl->stream));
+        CU(sparse_launch(S, LaunchWin{nu, nu + 1, 3, 1}, pl->sp_ctas, pl->sp_smem, pl->stream));
         ++pl->launches;
         if (nu + 1 < iters) {  // the last one is the solve's own gap (solve_finish)
           if (compute_gap_terms(pl, ((nu + 1) & 1) ? pl->Y1 : pl->Y0, pl->GTR + (size_t)nu * 10))
@@ -1574,29 +1626,64 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
         }
       }
     } else if (!pl->sharded) {
-      S.nu0 = 0;
-      S.nu1 = iters;
-      S.phase = 3;
       if (pl->SUBCTR) CU(cudaMemsetAsync(pl->SUBCTR, 0, 4 * sizeof(unsigned int), pl->stream));
-      CU(sparse_launch(S, pl->sp_ctas, pl->sp_smem, pl->stream));
+      CU(sparse_launch(S, LaunchWin{0, iters, 3, 0}, pl->sp_ctas, pl->sp_smem, pl->stream));
       ++pl->launches;
     } else {
       // per iteration: phase 1 (backward + head pre-reduction), the cross-GPU sum of
-      // the per-trunk-node head sums, phase 2 (trunk sweep, needs, forward, epilogue)
+      // the per-trunk-node head sums, phase 2 (trunk sweep, needs, forward, epilogue).
+      // With a communicator the 2 x iters launches and the all-reduces are captured
+      // once per iteration count into a CUDA graph and replayed (the launch windows
+      // are kernel arguments; the plan's parameters are uploaded before each replay)
       const size_t hs = (size_t)std::max(1, pl->sp_trunk) * S.HS_LD;
-      for (int nu = 0; nu < iters; ++nu) {
-        S.nu0 = nu;
-        S.nu1 = nu + 1;
-        S.phase = 1;
-        CU(sparse_launch(S, pl->sp_ctas, pl->sp_smem, pl->stream));
-        if (pl->sp_trunk > 0 && pl->comm) {
-          const int nr = pl->nccl->AllReduce(pl->HS, pl->HS, hs, NcclApi::kFloat64, NcclApi::kSum, pl->comm, pl->stream);
-          if (nr != 0) return fail(TSMPC_ERR_NCCL, "ncclAllReduce: %s", pl->nccl->GetErrorString(nr));
+      auto issue = [&]() -> int {
+        for (int nu = 0; nu < iters; ++nu) {
+          CU(sparse_launch(S, LaunchWin{nu, nu + 1, 1, 0}, pl->sp_ctas, pl->sp_smem, pl->stream));
+          if (pl->sp_trunk > 0 && pl->comm) {
+            const int nr = pl->nccl->AllReduce(pl->HS, pl->HS, hs, NcclApi::kFloat64, NcclApi::kSum, pl->comm,
+                                               pl->stream);
+            if (nr != 0) return fail(TSMPC_ERR_NCCL, "ncclAllReduce: %s", pl->nccl->GetErrorString(nr));
+          }
+          CU(sparse_launch(S, LaunchWin{nu, nu + 1, 2, 0}, pl->sp_ctas, pl->sp_smem, pl->stream));
         }
-        S.phase = 2;
-        CU(sparse_launch(S, pl->sp_ctas, pl->sp_smem, pl->stream));
-        pl->launches += 2;
+        return TSMPC_OK;
+      };
+      bool graphed = false;
+      if (pl->comm && !std::getenv("TSMPC_NO_GRAPH")) {
+        if (pl->gexec && pl->g_iters == iters) {
+          graphed = true;
+        } else {
+          if (pl->gexec) {
+            cudaGraphExecDestroy(pl->gexec);
+            pl->gexec = nullptr;
+          }
+          CU(sparse_params_upload(S, pl->stream));  // g_sp holds this plan's parameters
+          cudaGraph_t g = nullptr;
+          if (cudaStreamBeginCapture(pl->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+            const int irc = issue();
+            const cudaError_t ce = cudaStreamEndCapture(pl->stream, &g);
+            if (irc == TSMPC_OK && ce == cudaSuccess && g &&
+                cudaGraphInstantiate(&pl->gexec, g, 0) == cudaSuccess) {
+              pl->g_iters = iters;
+              graphed = true;
+            } else {
+              pl->gexec = nullptr;
+              pl->graph_why = irc != TSMPC_OK ? g_err : std::string(cudaGetErrorString(ce));
+            }
+            if (g) cudaGraphDestroy(g);
+          }
+          cudaGetLastError();  // a failed capture falls back to direct launches
+        }
       }
+      if (graphed) {
+        CU(sparse_params_upload(S, pl->stream));
+        CU(cudaGraphLaunch(pl->gexec, pl->stream));
+        CU(sparse_note_launch(pl->stream));
+      } else {
+        const int irc = issue();
+        if (irc) return irc;
+      }
+      pl->launches += 2 * (long long)iters;
       if (pl->comm) {
         // residual: max over ranks (non-negative doubles order like their bit patterns)
         const int nr = pl->nccl->AllReduce(pl->RESID, pl->RESID, (size_t)st.nres, NcclApi::kUint64, NcclApi::kMax,
@@ -1677,26 +1764,41 @@ int tsmpc_solve_group(tsmpc_plan* const* plans, int32_t n, const double* p, int3
   const size_t hs = (size_t)std::max(1, plans[0]->sp_trunk) * plans[0]->sbase.HS_LD;
   for (int nu = 0; nu < iters; ++nu) {
     for (int r = 0; r < n; ++r) {
-      S[r].nu0 = nu;
-      S[r].nu1 = nu + 1;
-      S[r].phase = 1;
-      CU(sparse_launch(S[r], plans[r]->sp_ctas, plans[r]->sp_smem, s0));
+      CU(sparse_launch(S[r], LaunchWin{nu, nu + 1, 1, 0}, plans[r]->sp_ctas, plans[r]->sp_smem, s0));
     }
     if (plans[0]->sp_trunk > 0) {
       group_sum_kernel<<<(unsigned)std::min<size_t>(256, (hs + 255) / 256), 256, 0, s0>>>(g, n, hs);
       CU(cudaGetLastError());
     }
     for (int r = 0; r < n; ++r) {
-      S[r].phase = 2;
-      CU(sparse_launch(S[r], plans[r]->sp_ctas, plans[r]->sp_smem, s0));
+      CU(sparse_launch(S[r], LaunchWin{nu, nu + 1, 2, 0}, plans[r]->sp_ctas, plans[r]->sp_smem, s0));
       plans[r]->launches += 2;
     }
   }
   group_max_kernel<<<(st[0].nres + 255) / 256, 256, 0, s0>>>(g, n, st[0].nres);
   CU(cudaGetLastError());
   for (int r = 0; r < n; ++r) CU(cudaEventRecord(plans[r]->ev1, s0));
+  const bool gap = !(flags & TSMPC_SKIP_GAP);
+  if (gap) {
+    // the exchange assemble_shard_state does across GPUs: every shard's averages and
+    // final dual become the full arrays (replicated rows counted once)
+    const size_t yblk = 2 * (size_t)plans[0]->E * plans[0]->NXP + (size_t)plans[0]->E * plans[0]->NUP;
+    GroupBufs gx{}, gu{}, gy{};
+    for (int r = 0; r < n; ++r) {
+      double* yfin = (iters & 1) == 0 ? plans[r]->Y0 : plans[r]->Y1;
+      if (r > 0 && zero_replicated_rows(plans[r], yfin, s0)) return TSMPC_ERR_CUDA;
+      gx.hs[r] = plans[r]->XAVG;
+      gu.hs[r] = plans[r]->UAVG;
+      gy.hs[r] = yfin;
+    }
+    const size_t nx_ = (size_t)plans[0]->n_nodes * plans[0]->NXP, nu_ = (size_t)plans[0]->E * plans[0]->NUP;
+    group_sum_kernel<<<(unsigned)std::min<size_t>(1024, (nx_ + 255) / 256), 256, 0, s0>>>(gx, n, nx_);
+    group_sum_kernel<<<(unsigned)std::min<size_t>(1024, (nu_ + 255) / 256), 256, 0, s0>>>(gu, n, nu_);
+    group_sum_kernel<<<(unsigned)std::min<size_t>(1024, (yblk + 255) / 256), 256, 0, s0>>>(gy, n, yblk);
+    CU(cudaGetLastError());
+  }
   for (int r = 0; r < n; ++r) {
-    int rc = solve_finish(plans[r], st[r], flags, outs + r);
+    int rc = solve_finish(plans[r], st[r], flags, outs + r, gap);
     if (rc) return rc;
   }
   return TSMPC_OK;

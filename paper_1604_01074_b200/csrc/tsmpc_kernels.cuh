@@ -150,10 +150,8 @@ struct SParams {
   int slot_rows;                // resident capacity of the slot region (rows)
   const double* beta_s;         // E x NVP  beta in the structured basis (beta M)
   double* TG;                   // E x NVP  t rows of streamed CTAs
-  // launch window: iterations [nu0, nu1) and phases (1: backward (+ head pre-reduction
-  // when sharded), 2: trunk sweep, needs, forward + epilogue).  Single-GPU plans run
-  // every iteration with both phases in one launch.
-  int nu0, nu1, phase;
+  // (the launch window -- iterations and phases -- is a kernel argument, LaunchWin,
+  // so that consecutive launches of one plan reuse the uploaded parameters)
   // subtree sharding across GPUs (one process per GPU): the trunk is replicated, the
   // leaf chains are split by the trunk node they hang from; HS holds, per trunk
   // position, [sum of the chain-head g | sum of the chain-head xiq] of the heads
@@ -185,8 +183,6 @@ struct SParams {
   int split_heads, O_HSUM;      // chain CTAs publish their head values right after the fill, by
                                 // reductions ([sum beta_s | sum psi^ | sum G_d s | sum z] at O_HSUM)
   unsigned int* abort_flag;     // raised by a spin-wait that timed out (plan-owned, zeroed per solve)
-  int wb_end;                   // launch window [nu0, nu1) ends with a full write-back (the state of
-                                // iteration nu1 - 1 is left in HBM: per-iteration duality gap)
   int tile_cap;                 // rows of the work regions A / B (kTileS, or the widest wide tile)
   // wide mode (apg_wide_kernel): a CTA's chains are packed into tiles of up to
   // kTileW rows that are processed as one (the chain scans of all its chains run
@@ -196,6 +192,15 @@ struct SParams {
   int wide;
   int wide_prefill;             // the epilogue of the CTA's last tile leaves the next fill
   int hsum_nseg;                // wide split mode: chains per chain CTA the head-sum scratch holds
+};
+
+// Launch window of the structured-basis kernels (a kernel argument): iterations
+// [nu0, nu1) and phases (1: backward (+ head pre-reduction when sharded), 2: trunk
+// sweep, needs, forward + epilogue).  Single-GPU plans run every iteration with
+// both phases in one launch.  wb_end: the window ends with a full write-back (the
+// state of iteration nu1 - 1 is left in HBM: per-iteration duality gap).
+struct LaunchWin {
+  int nu0, nu1, phase, wb_end;
 };
 
 // Phase timers (profiling builds: -DTSMPC_TIMERS).  Slot k accumulates the cycles

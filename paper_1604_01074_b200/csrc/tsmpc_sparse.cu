@@ -35,6 +35,7 @@
 // and, on the last iteration, the outputs.  Otherwise one tile slot is streamed
 // with cp.async, prefetched one step ahead (see bwd/fwd below).
 #include "tsmpc_kernels.cuh"
+#include <cstring>
 #include <mutex>
 
 namespace cg = cooperative_groups;
@@ -47,6 +48,8 @@ extern __shared__ __align__(16) double s_dyn[];
 // launching stream): every field access is a uniform constant-bank load that
 // the compiler may hoist freely, also inside the __noinline__ phase functions.
 __constant__ SParams g_sp;
+// the launch window of the running kernel (set from the kernel argument at entry)
+__shared__ LaunchWin s_win;
 
 namespace {
 
@@ -302,7 +305,7 @@ __device__ __forceinline__ bool is_check(const Params& P, int nu) {
 // iteration whose state is written back to HBM in full (last iteration, stopping
 // checks, the end of a write-back window)
 __device__ __forceinline__ bool is_last(const Params& P, int nu) {
-  return nu == P.iters - 1 || is_check(P, nu) || (g_sp.wb_end && nu == g_sp.nu1 - 1);
+  return nu == P.iters - 1 || is_check(P, nu) || (s_win.wb_end && nu == s_win.nu1 - 1);
 }
 
 struct EpiConst {
@@ -936,7 +939,7 @@ __device__ __noinline__ void fwd_finish(int ti, int nu_it, double cf, double th,
   TSMPC_MARK(P, 14, tm_);
   // psi and state blocks back to back: they write disjoint columns of the rows
   // prefill: the next iteration of this launch starts its backward without the fill
-  const bool pre = S.split_heads && S.split_flags && nu_it + 1 < S.nu1;
+  const bool pre = S.split_heads && S.split_flags && nu_it + 1 < s_win.nu1;
   const double cfn = pre ? P.coef[nu_it + 1] : 0.0;
   epi_psi_rows(nu_it, cf, th, nrows, ysm, !resident || last, cur ^ 1, rmax, pre, cfn);
   TSMPC_MARK(P, 15, tm_);
@@ -1600,6 +1603,22 @@ __device__ __noinline__ void trunk_own_rows(int nu_it, double cf, double th, int
 #ifndef TSMPC_PREF
 #define TSMPC_PREF 1
 #endif
+#ifndef TSMPC_WEAK
+#define TSMPC_WEAK 0
+#endif
+#ifndef TSMPC_FASTEPI
+#define TSMPC_FASTEPI 1
+#endif
+// state loads / stores of the wide epilogues: the rows are this CTA's own (or, for
+// trunk rows, read by other CTAs only after a fenced barrier through L2)
+__device__ __forceinline__ double epi_ld(const double* p) {
+  if (TSMPC_WEAK & 1) return *p;
+  return __ldcg(p);
+}
+__device__ __forceinline__ void epi_st(double* p, double v) {
+  if (TSMPC_WEAK & 2) *p = v;
+  else __stcg(p, v);
+}
 constexpr int kChunkW = TSMPC_CHUNKW;  // rows whose loads a thread issues before using them (epilogue)
 constexpr int kChunkF = 4;   // the same for the (first-iteration) fill
 constexpr int kRW = kTileW / kGroups;   // rows per thread of a wide tile, (group, component) mapping
@@ -1609,14 +1628,23 @@ constexpr int kRX = kTileW / kG8;       // rows per thread of a wide tile in tha
 
 // psi block of the rows in rdesc (component-major, as epi_psi_rows), state in HBM.
 // WANT: this iteration's residual is needed (compiled apart: otherwise ptxas
-// if-converts the residual's IEEE divisions into every element)
-template <bool WANT>
+// if-converts the residual's IEEE divisions into every element).  MODE 0: general
+// (every condition tested at run time); MODE 1 / 2: the steady-state iteration
+// (prefill, no output write-back, psi table in shared memory), without / with the
+// split-mode trunk term folded in -- straight-line code over a full chunk of rows,
+// so the elements' dependency chains interleave.
+// trb_o (split mode): shared-memory offset of the tile's staged parent rows
+// [du | B du | x] (stride trl), -1 if none; u += du_tp is folded in here.
+template <bool WANT, int MODE>
 __device__ __noinline__ void epi_psi_wide_t(int nu_it, double cf, double th, int nrows, int cur, double* rmax_io,
-                                            bool pre, double cfn) {
+                                            bool pre, double cfn, int trb_o, int trl, int seg0) {
   const SParams& S = g_sp;
   const Ctx c = ctx_of();
   const Params& P = S.P;
   const EpiConst q = epi_const(P, nu_it, cf, th, true, cur ^ 1, pre, cfn);
+  constexpr bool FAST = MODE != 0;
+  const bool do_pre = FAST || q.pre, do_last = !FAST && q.last;
+  const bool fold = MODE == 2 || (MODE == 0 && trb_o >= 0);
   const int k = threadIdx.x & (kKW - 1), g = threadIdx.x / kKW;
   double rmax = *rmax_io;
   if (k < c.nu) {
@@ -1626,6 +1654,7 @@ __device__ __noinline__ void epi_psi_wide_t(int nu_it, double cf, double th, int
     double* Yn = P.ybuf[cur ^ 1] + 2 * E * c.NXP + k;
     double* UA = P.uavg + k;
     const int* rd = c.rdesc();
+    const int psio = c.psi_o + k;
 #pragma unroll 1
     for (int r0 = g; r0 < nrows; r0 += kChunkW * kGroups) {
       double yc[kChunkW], yp[kChunkW], ua[kChunkW];
@@ -1637,48 +1666,62 @@ __device__ __noinline__ void epi_psi_wide_t(int nu_it, double cf, double th, int
         yc[u] = yp[u] = ua[u] = 0.0;
         if (r < nrows) {
           eo[u] = rd[5 * r] * c.NUP;
-          yc[u] = ldcg(Yc + eo[u]);
-          yp[u] = ldcg(Yn + eo[u]);
-          ua[u] = ldcg(UA + eo[u]);
+          yc[u] = epi_ld(Yc + eo[u]);
+          yp[u] = epi_ld(Yn + eo[u]);
+          ua[u] = epi_ld(UA + eo[u]);
         }
       }
-#pragma unroll
-      for (int u = 0; u < kChunkW; ++u) {
-        const int r = r0 + u * kGroups;
-        if (r < nrows) {
-          const int* d = rd + 5 * r;
-          const int st = d[1];
-          double* us = s_dyn + d[3] + k;
-          const double uu = *us;
-          const double dp = c.dpsi(st, k);
-          const double w = extrap(yc[u], yp[u], q.cf);
-          const double hp = __dmul_rn(uu, dp);
-          const double a = __dadd_rn(__dmul_rn(w, q.ilam), hp);
-          const double t = fmin(fmax(a, __dmul_rn(dp, ulo)), __dmul_rn(dp, uhi));
-          const double ny = __dadd_rn(w, __dmul_rn(q.lam, __dsub_rn(hp, t)));
-          stcg(Yn + eo[u], ny);
-          if (WANT && q.want) rmax = fmax(rmax, fabs(__dsub_rn(uu, __ddiv_rn(t, dp))));
-          stcg(UA + eo[u], __dadd_rn(__dmul_rn(ua[u], q.om), __dmul_rn(q.th, uu)));
-          if (q.last) stcg(P.U + eo[u] + k, uu);
-          if (q.pre) {  // the next backward's fill of this element
-            const double wn = extrap(ny, yc[u], q.cfn);
-            *us = c.scaled() ? __dmul_rn(wn, dp) : wn;
-          }
+      auto elem = [&](int u, int r) {
+        const int* d = rd + 5 * r;
+        const int st = d[1];
+        double* us = s_dyn + d[3] + k;
+        double uu = *us;
+        if (fold) {
+          const int sg = d[4];
+          const double du = s_dyn[trb_o + sg * trl + k];
+          uu = c.mt.segs[4 * (seg0 + sg) + 2] >= 0 ? __dadd_rn(uu, du) : uu;
         }
+        const double dp = FAST ? s_dyn[psio + st * c.NUP] : c.dpsi(st, k);
+        const double w = extrap(yc[u], yp[u], q.cf);
+        const double hp = __dmul_rn(uu, dp);
+        const double a = __dadd_rn(__dmul_rn(w, q.ilam), hp);
+        const double t = fmin(fmax(a, __dmul_rn(dp, ulo)), __dmul_rn(dp, uhi));
+        const double ny = __dadd_rn(w, __dmul_rn(q.lam, __dsub_rn(hp, t)));
+        epi_st(Yn + eo[u], ny);
+        if (WANT && q.want) rmax = fmax(rmax, fabs(__dsub_rn(uu, __ddiv_rn(t, dp))));
+        epi_st(UA + eo[u], __dadd_rn(__dmul_rn(ua[u], q.om), __dmul_rn(q.th, uu)));
+        if (do_last) epi_st(P.U + eo[u] + k, uu);
+        if (do_pre) {  // the next backward's fill of this element
+          const double wn = extrap(ny, yc[u], q.cfn);
+          *us = (FAST || c.scaled()) ? __dmul_rn(wn, dp) : wn;
+        }
+      };
+      if (FAST && r0 + (kChunkW - 1) * kGroups < nrows) {
+#pragma unroll
+        for (int u = 0; u < kChunkW; ++u) elem(u, r0 + u * kGroups);
+      } else {
+#pragma unroll
+        for (int u = 0; u < kChunkW; ++u)
+          if (r0 + u * kGroups < nrows) elem(u, r0 + u * kGroups);
       }
     }
   }
   *rmax_io = rmax;
 }
 
-// state blocks of the rows in rdesc, one warp per row (two rows in flight), state in HBM
-template <int XS, bool WANT>
+// state blocks of the rows in rdesc, one warp per row (R2 rows in flight), state in
+// HBM.  WANT / MODE as for epi_psi_wide_t; the fold (split mode, A = I) adds
+// x += (d + 1) B du_tp + x_tp.
+template <int XS, bool WANT, int MODE>
 __device__ __noinline__ void epi_state_wide_t(int nu_it, double cf, double th, int nrows, int cur, double* rmax_io,
-                                              bool pre, double cfn) {
+                                              bool pre, double cfn, int trb_o, int trl, int seg0) {
   const SParams& S = g_sp;
   const Ctx c = ctx_of();
   const Params& P = S.P;
   const EpiConst q = epi_const(P, nu_it, cf, th, true, cur ^ 1, pre, cfn);
+  constexpr bool FAST = MODE != 0;
+  const bool do_pre = FAST || q.pre, do_last = !FAST && q.last;
+  const bool fold = MODE == 2 || (MODE == 0 && trb_o >= 0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const size_t E = (size_t)c.E;
   const int N = c.N;
@@ -1709,23 +1752,27 @@ __device__ __noinline__ void epi_state_wide_t(int nu_it, double cf, double th, i
       for (int m = 0; m < XS; ++m) {
         const int i = lane + 32 * m;
         const bool ok = r < nrows && i < c.nx;
-        ycs[h][m] = ok ? ldcg(Ys + eo[h] + i) : 0.0;
-        yps[h][m] = ok ? ldcg(Ns + eo[h] + i) : 0.0;
-        ycz[h][m] = ok ? ldcg(Yz + eo[h] + i) : 0.0;
-        ypz[h][m] = ok ? ldcg(Nz + eo[h] + i) : 0.0;
-        xav[h][m] = ok ? ldcg(P.xavg + eo[h] + c.NXP + i) : 0.0;
+        ycs[h][m] = ok ? epi_ld(Ys + eo[h] + i) : 0.0;
+        yps[h][m] = ok ? epi_ld(Ns + eo[h] + i) : 0.0;
+        ycz[h][m] = ok ? epi_ld(Yz + eo[h] + i) : 0.0;
+        ypz[h][m] = ok ? epi_ld(Nz + eo[h] + i) : 0.0;
+        xav[h][m] = ok ? epi_ld(P.xavg + eo[h] + c.NXP + i) : 0.0;
       }
     }
-#pragma unroll
-    for (int h = 0; h < R2; ++h) {
-      const int r = r0 + h * kWarpsS;
-      if (r >= nrows) break;  // warp-uniform
+    auto row = [&](int h, int r) {
       const int* d = rd + 5 * r;
       const int st = d[1];
       double* x = s_dyn + d[2];
       const double ds = c.scl[st], dz = c.scl[N + st];
       double ws[XS], wz[XS], ts[XS], tz[XS], xv[XS];
       double ss = 0.0, sz = 0.0;
+      int tpo = -1;        // the parent's [du | B du | x] row (split mode)
+      double dep1 = 0.0;   // depth below the chain head + 1
+      if (fold) {
+        const int* sg = c.mt.segs + 4 * (seg0 + d[4]);
+        tpo = sg[2] >= 0 ? trb_o + d[4] * trl : -1;
+        dep1 = (double)(r - sg[0] + 1);
+      }
 #pragma unroll
       for (int m = 0; m < XS; ++m) {
         const int i = lane + 32 * m;
@@ -1734,6 +1781,9 @@ __device__ __noinline__ void epi_state_wide_t(int nu_it, double cf, double th, i
           ws[m] = extrap(ycs[h][m], yps[h][m], q.cf);
           wz[m] = extrap(ycz[h][m], ypz[h][m], q.cf);
           xv[m] = x[i];
+          if (fold && tpo >= 0)
+            xv[m] = __dadd_rn(xv[m], __dadd_rn(__dmul_rn(dep1, s_dyn[tpo + c.NUP + i]),
+                                               __dmul_rn(1.0, s_dyn[tpo + c.NUP + c.NXP + i])));
           ts[m] = __dadd_rn(__dmul_rn(ws[m], q.ilam), __dmul_rn(xv[m], ds));
           tz[m] = __dadd_rn(__dmul_rn(wz[m], q.ilam), __dmul_rn(xv[m], dz));
           const double gs_ = __dsub_rn(fmax(ts[m], __dmul_rn(ds, bxs[m])), ts[m]);
@@ -1764,37 +1814,64 @@ __device__ __noinline__ void epi_state_wide_t(int nu_it, double cf, double th, i
           const double t_z = __dadd_rn(tz[m], __dmul_rn(fz, __dsub_rn(pz, tz[m])));
           const double ns = __dadd_rn(ws[m], __dmul_rn(q.lam, __dsub_rn(hs, t_s)));
           const double nz = __dadd_rn(wz[m], __dmul_rn(q.lam, __dsub_rn(hz, t_z)));
-          stcg(Ns + eo[h] + i, ns);
-          stcg(Nz + eo[h] + i, nz);
+          epi_st(Ns + eo[h] + i, ns);
+          epi_st(Nz + eo[h] + i, nz);
           if (WANT && q.want) {
             rmax = fmax(rmax, fabs(__dsub_rn(xi, __ddiv_rn(t_s, ds))));
             rmax = fmax(rmax, fabs(__dsub_rn(xi, __ddiv_rn(t_z, dz))));
           }
-          stcg(P.xavg + eo[h] + c.NXP + i, __dadd_rn(__dmul_rn(xav[h][m], q.om), __dmul_rn(q.th, xi)));
-          if (q.last) stcg(P.X + eo[h] + c.NXP + i, xi);
-          if (q.pre) {  // the next backward's fill of this element
+          epi_st(P.xavg + eo[h] + c.NXP + i, __dadd_rn(__dmul_rn(xav[h][m], q.om), __dmul_rn(q.th, xi)));
+          if (do_last) epi_st(P.X + eo[h] + c.NXP + i, xi);
+          if (do_pre) {  // the next backward's fill of this element
             const double wsn = extrap(ns, ycs[h][m], q.cfn), wzn = extrap(nz, ycz[h][m], q.cfn);
             x[i] = __dadd_rn(__dmul_rn(wsn, ds), __dmul_rn(wzn, dz));
           }
         }
       }
+    };
+    if (FAST && r0 + (R2 - 1) * kWarpsS < nrows) {
+#pragma unroll
+      for (int h = 0; h < R2; ++h) row(h, r0 + h * kWarpsS);
+    } else {
+#pragma unroll
+      for (int h = 0; h < R2; ++h)
+        if (r0 + h * kWarpsS < nrows) row(h, r0 + h * kWarpsS);  // warp-uniform
     }
   }
   *rmax_io = rmax;
 }
 
+__device__ __forceinline__ bool epi_fast(const Params& P, int nu_it, bool pre) {
+  return pre && !is_last(P, nu_it) && !P.record_all && P.scaled && g_sp.psi_smem;
+}
 __device__ __forceinline__ void epi_psi_wide(int nu_it, double cf, double th, int nrows, int cur, double* rmax,
-                                             bool pre, double cfn) {
+                                             bool pre, double cfn, int trb_o = -1, int trl = 0, int seg0 = 0) {
   const Params& P = g_sp.P;
-  if (!TSMPC_WANT_T || is_last(P, nu_it) || P.record_all) epi_psi_wide_t<true>(nu_it, cf, th, nrows, cur, rmax, pre, cfn);
-  else epi_psi_wide_t<false>(nu_it, cf, th, nrows, cur, rmax, pre, cfn);
+#ifdef TSMPC_KO
+  if (TSMPC_KO & 1) return;  // timing experiment only: results are wrong
+#endif
+  if (!TSMPC_WANT_T || is_last(P, nu_it) || P.record_all)
+    epi_psi_wide_t<true, 0>(nu_it, cf, th, nrows, cur, rmax, pre, cfn, trb_o, trl, seg0);
+  else if (TSMPC_FASTEPI && epi_fast(P, nu_it, pre))
+    trb_o >= 0 ? epi_psi_wide_t<false, 2>(nu_it, cf, th, nrows, cur, rmax, pre, cfn, trb_o, trl, seg0)
+               : epi_psi_wide_t<false, 1>(nu_it, cf, th, nrows, cur, rmax, pre, cfn, trb_o, trl, seg0);
+  else
+    epi_psi_wide_t<false, 0>(nu_it, cf, th, nrows, cur, rmax, pre, cfn, trb_o, trl, seg0);
 }
 template <int XS>
 __device__ __forceinline__ void epi_state_wide(int nu_it, double cf, double th, int nrows, int cur, double* rmax,
-                                               bool pre, double cfn) {
+                                               bool pre, double cfn, int trb_o = -1, int trl = 0, int seg0 = 0) {
   const Params& P = g_sp.P;
-  if (!TSMPC_WANT_T || is_last(P, nu_it) || P.record_all) epi_state_wide_t<XS, true>(nu_it, cf, th, nrows, cur, rmax, pre, cfn);
-  else epi_state_wide_t<XS, false>(nu_it, cf, th, nrows, cur, rmax, pre, cfn);
+#ifdef TSMPC_KO
+  if (TSMPC_KO & 2) return;  // timing experiment only: results are wrong
+#endif
+  if (!TSMPC_WANT_T || is_last(P, nu_it) || P.record_all)
+    epi_state_wide_t<XS, true, 0>(nu_it, cf, th, nrows, cur, rmax, pre, cfn, trb_o, trl, seg0);
+  else if (TSMPC_FASTEPI && epi_fast(P, nu_it, pre))
+    trb_o >= 0 ? epi_state_wide_t<XS, false, 2>(nu_it, cf, th, nrows, cur, rmax, pre, cfn, trb_o, trl, seg0)
+               : epi_state_wide_t<XS, false, 1>(nu_it, cf, th, nrows, cur, rmax, pre, cfn, trb_o, trl, seg0);
+  else
+    epi_state_wide_t<XS, false, 0>(nu_it, cf, th, nrows, cur, rmax, pre, cfn, trb_o, trl, seg0);
 }
 
 // backward sweep of wide tile ti (factor.py:142-156): fill from HBM (unless the
@@ -2184,12 +2261,12 @@ __device__ __noinline__ void fwd_finish_wide(int ti, int nu_it, double cf, doubl
   const SParams& S = g_sp;
   const Ctx c = ctx_of();
   const Params& P = S.P;
+  (void)P;
   const int* td = c.mt.tiles + 4 * ti;
   const int nrows = td[1], seg0 = td[2], nsegs = td[3];
-  const int tid = threadIdx.x, k = tid & (kKW - 1), g = tid / kKW;
-  const int nx = c.nx, nu = c.nu, LA = c.LA;
+  const int tid = threadIdx.x;
+  const int nx = c.nx, LA = c.LA;
   double* RA = c.A();
-  double* RB = c.B();
   long long tm_ = clock64();
   (void)tm_;
   // the parents' [du | B du | x] rows, staged once per chain
@@ -2218,28 +2295,10 @@ __device__ __noinline__ void fwd_finish_wide(int ti, int nu_it, double cf, doubl
     }
   }
   __syncthreads();
-  const int* rd = c.rdesc();
-  if (k < nu) {
-#pragma unroll 2
-    for (int r = g; r < nrows; r += kGroups) {
-      const int s = rd[5 * r + 4];
-      if (c.mt.segs[4 * (seg0 + s) + 2] >= 0) RB[r * c.NUP + k] = __dadd_rn(RB[r * c.NUP + k], tr[s * HL + k]);
-    }
-  }
   TSMPC_MARK(P, 13, tm_);
-  if (S.a_unit) {
-    // a = 1: G_d = d + 1 and a^(d+1) = 1 exactly, every row independent
-#pragma unroll 1
-    for (int idx = tid; idx < nrows * nx; idx += kThreadsS) {
-      const int r = idx / nx, i = idx - r * nx;
-      const int s = rd[5 * r + 4];
-      const int* sg = c.mt.segs + 4 * (seg0 + s);
-      if (sg[2] < 0) continue;
-      const double bt = tr[s * HL + c.NUP + i], xt = tr[s * HL + c.NUP + c.NXP + i];
-      double* x = RA + r * LA + i;
-      *x = __dadd_rn(*x, __dadd_rn(__dmul_rn((double)(r - sg[0] + 1), bt), __dmul_rn(1.0, xt)));
-    }
-  } else {
+  if (!S.a_unit) {
+    // general diagonal A: x_e += G_d .* (B du_tp) + a^(d+1) .* x_tp by the recursion over
+    // each chain (A = I: folded into the state epilogue below)
     const double* adiag = c.adiag();
 #pragma unroll 1
     for (int idx = tid; idx < nsegs * nx; idx += kThreadsS) {
@@ -2258,12 +2317,14 @@ __device__ __noinline__ void fwd_finish_wide(int ti, int nu_it, double cf, doubl
         pw = __dmul_rn(pw, a);
       }
     }
+    __syncthreads();
   }
-  __syncthreads();
   TSMPC_MARK(P, 14, tm_);
-  epi_psi_wide(nu_it, cf, th, nrows, cur, rmax, pre, cfn);
+  // u += du_tp folded into the psi epilogue, x += (d+1) B du_tp + x_tp (A = I) into the state one
+  const int tro = (int)(tr - s_dyn);
+  epi_psi_wide(nu_it, cf, th, nrows, cur, rmax, pre, cfn, tro, HL, seg0);
   TSMPC_MARK(P, 15, tm_);
-  epi_state_wide<XS>(nu_it, cf, th, nrows, cur, rmax, pre, cfn);
+  epi_state_wide<XS>(nu_it, cf, th, nrows, cur, rmax, pre, cfn, S.a_unit ? tro : -1, HL, seg0);
   __syncthreads();
   TSMPC_MARK(P, 8, tm_);
 }
@@ -2297,10 +2358,11 @@ __device__ __noinline__ void trunk_own_rows_wide(int nu_it, double cf, double th
 
 }  // namespace
 
-__global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
+__global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel(LaunchWin win) {
   cg::grid_group grid = cg::this_grid();
   const SParams& S = g_sp;
   const Params& P = S.P;
+  if (threadIdx.x == 0) s_win = win;  // visible after the staging barrier below
   {  // stage model vectors, scaling, sparse operators and this CTA's plan
     double* bnd = s_dyn + S.O_BND;
     double* scl = s_dyn + S.O_SCL;
@@ -2350,9 +2412,9 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
   const bool resident = c.mt.resident != 0;
   const int nt = c.mt.ntiles;
   const bool trunk = P.n_trunk > 0;
-  const bool do_a = S.phase & 1, do_b = S.phase & 2;
+  const bool do_a = win.phase & 1, do_b = win.phase & 2;
   {  // initial dual / ergodic rows
-    const int cur0 = (P.slot0 + S.nu0) & 1, ysm0 = S.nu0 & 1;
+    const int cur0 = (P.slot0 + win.nu0) & 1, ysm0 = win.nu0 & 1;
     if (resident) {
       if (nt > 0) load_rows(c.mt.rows, 4, c.mt.nrows, c.slot, 3, cur0, ysm0);
     } else if (nt > 0) {
@@ -2390,11 +2452,11 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
   }
   double rmax = 0.0;
   unsigned int sub_target = 0;  // trunk-CTA barrier episodes x split_n (split mode)
-  double cf = P.coef[S.nu0], th = P.theta[S.nu0];
-  for (int nu = S.nu0; nu < S.nu1; ++nu) {
+  double cf = P.coef[win.nu0], th = P.theta[win.nu0];
+  for (int nu = win.nu0; nu < win.nu1; ++nu) {
     const int cur = (P.slot0 + nu) & 1;
     const int ysm = nu & 1;
-    if (P.tol > 0.0 && nu > S.nu0 && nu % P.check_every == 0) {
+    if (P.tol > 0.0 && nu > win.nu0 && nu % P.check_every == 0) {
       // stopping test on the residual of iteration nu - 1 (its state is in HBM)
       grid.sync();
       const double r = __longlong_as_double(
@@ -2410,7 +2472,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
     if (do_a) {
       for (int t = nt - 1; t >= 0; --t)
         bwd_tile(t, cf, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur,
-                 S.split && S.split_heads && S.split_flags && nu > S.nu0);
+                 S.split && S.split_heads && S.split_flags && nu > win.nu0);
       if (S.sharded && trunk) {
         grid.sync();
         head_prereduce();
@@ -2423,7 +2485,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
       // publish TR; chain CTAs wait for TR only before their trunk terms.
       long long tb_ = clock64();
       (void)tb_;
-      const unsigned it = (unsigned)(nu - S.nu0 + 1);
+      const unsigned it = (unsigned)(nu - win.nu0 + 1);
       if ((int)blockIdx.x < S.split_c0) {
         if (!S.split_heads) signal_arrive(S.sub_ctr + 1);  // else published inside bwd_tile
         for (int t = 0; t < nt; ++t)
@@ -2440,7 +2502,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
         TSMPC_MARK(P, 3, tb_);
       } else {
         // the previous iteration's trunk-row epilogues (dual rows the sweep reads)
-        if (nu > S.nu0) trunk_barrier(S.sub_ctr, (unsigned)S.split_n, sub_target);
+        if (nu > win.nu0) trunk_barrier(S.sub_ctr, (unsigned)S.split_n, sub_target);
         if (!S.split_local) trunk_sweep(cf, cur, 1);  // own terms, before the heads arrive
         signal_wait(S.sub_ctr + 1, it * (unsigned)S.split_c0);
         TSMPC_MARK(P, 9, tb_);
@@ -2539,7 +2601,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
     cf = cf_n;
     th = th_n;
   }
-  if (P.tol > 0.0 && blockIdx.x == 0 && threadIdx.x == 0) *P.iters_done = S.nu1;
+  if (P.tol > 0.0 && blockIdx.x == 0 && threadIdx.x == 0) *P.iters_done = win.nu1;
 }
 
 
@@ -2550,10 +2612,11 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel() {
 // backward tile).  Sharded plans run it as two launches per iteration (phase 1:
 // backward + head pre-reduction; phase 2: the rest), state in HBM in between.
 template <int XS>
-__global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel() {
+__global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
   cg::grid_group grid = cg::this_grid();
   const SParams& S = g_sp;
   const Params& P = S.P;
+  if (threadIdx.x == 0) s_win = win;  // visible after the staging barrier below
   {  // stage model vectors, scaling, sparse operators and this CTA's plan
     double* bnd = s_dyn + S.O_BND;
     double* scl = s_dyn + S.O_SCL;
@@ -2602,7 +2665,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel() {
   const Ctx c = ctx_of();
   const int nt = c.mt.ntiles;
   const bool trunk = P.n_trunk > 0;
-  const bool do_a = S.phase & 1, do_b = S.phase & 2;
+  const bool do_a = win.phase & 1, do_b = win.phase & 2;
   const bool chain_cta = (int)blockIdx.x < S.split_c0;
   if (S.split && chain_cta && nt == 1) {
     // per chain, the sum of beta_s over its rows (static during the launch), chain order
@@ -2621,10 +2684,10 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel() {
   }
   double rmax = 0.0;
   unsigned int sub_target = 0;  // trunk-CTA barrier episodes x split_n (split mode)
-  double cf = P.coef[S.nu0], th = P.theta[S.nu0];
-  for (int nu = S.nu0; nu < S.nu1; ++nu) {
+  double cf = P.coef[win.nu0], th = P.theta[win.nu0];
+  for (int nu = win.nu0; nu < win.nu1; ++nu) {
     const int cur = (P.slot0 + nu) & 1;
-    if (P.tol > 0.0 && nu > S.nu0 && nu % P.check_every == 0) {
+    if (P.tol > 0.0 && nu > win.nu0 && nu % P.check_every == 0) {
       // stopping test on the residual of iteration nu - 1 (its state is in HBM)
       grid.sync();
       const double r = __longlong_as_double(
@@ -2637,7 +2700,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel() {
     const int nn = nu + 1 < P.iters ? nu + 1 : nu;
     const double cf_n = P.coef[nn], th_n = P.theta[nn];
     if (do_a) {
-      for (int t = nt - 1; t >= 0; --t) bwd_wide(t, cf, cur, S.wide_prefill && t == nt - 1 && nu > S.nu0);
+      for (int t = nt - 1; t >= 0; --t) bwd_wide(t, cf, cur, S.wide_prefill && t == nt - 1 && nu > win.nu0);
       if (S.sharded && trunk) {
         grid.sync();
         head_prereduce();
@@ -2650,7 +2713,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel() {
       // for TR only before their trunk terms
       long long tb_ = clock64();
       (void)tb_;
-      const unsigned it = (unsigned)(nu - S.nu0 + 1);
+      const unsigned it = (unsigned)(nu - win.nu0 + 1);
       if (chain_cta) {
         for (int t = 0; t < nt; ++t) fwd_wide<XS>(t, nu, cf, th, cur, &rmax, false, 0.0);
         TSMPC_MARK(P, 10, tb_);
@@ -2662,11 +2725,11 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel() {
             P.xavg[i] = __dadd_rn(__dmul_rn(P.xavg[i], om), __dmul_rn(th, c.proot()[i]));
         }
         for (int t = 0; t < nt; ++t)
-          fwd_finish_wide<XS>(t, nu, cf, th, cur, &rmax, S.wide_prefill && t == nt - 1 && nu + 1 < S.nu1, cf_n);
+          fwd_finish_wide<XS>(t, nu, cf, th, cur, &rmax, S.wide_prefill && t == nt - 1 && nu + 1 < win.nu1, cf_n);
         TSMPC_MARK(P, 3, tb_);
       } else {
         // the previous iteration's trunk-row epilogues (dual rows the sweep reads)
-        if (nu > S.nu0) trunk_barrier(S.sub_ctr, (unsigned)S.split_n, sub_target);
+        if (nu > win.nu0) trunk_barrier(S.sub_ctr, (unsigned)S.split_n, sub_target);
         trunk_sweep(cf, cur, 1);  // own terms, before the heads arrive
         signal_wait(S.sub_ctr + 1, it * (unsigned)S.split_c0);
         TSMPC_MARK(P, 9, tb_);
@@ -2700,7 +2763,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel() {
           P.xavg[i] = __dadd_rn(__dmul_rn(P.xavg[i], om), __dmul_rn(th, c.proot()[i]));
       }
       for (int t = 0; t < nt; ++t)
-        fwd_wide<XS>(t, nu, cf, th, cur, &rmax, S.wide_prefill && t == nt - 1 && nu + 1 < S.nu1, cf_n);
+        fwd_wide<XS>(t, nu, cf, th, cur, &rmax, S.wide_prefill && t == nt - 1 && nu + 1 < win.nu1, cf_n);
     }
     if (do_b) {
       if (nu == P.iters - 1 || P.record_all || is_check(P, nu)) {
@@ -2723,7 +2786,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel() {
     cf = cf_n;
     th = th_n;
   }
-  if (P.tol > 0.0 && blockIdx.x == 0 && threadIdx.x == 0) *P.iters_done = S.nu1;
+  if (P.tol > 0.0 && blockIdx.x == 0 && threadIdx.x == 0) *P.iters_done = win.nu1;
 }
 
 }  // namespace tsmpc
@@ -2742,28 +2805,72 @@ const void* sparse_kernel_fn(int wide, int nx) {
 // different streams are chained through a per-device event so that a launch's
 // parameter upload cannot land while another plan's kernel still reads g_sp
 // (the kernel occupies the whole GPU anyway, so nothing is lost).
-cudaError_t sparse_launch(const SParams& S, int ctas, size_t smem, cudaStream_t stream) {
-  static std::mutex mu;
-  static cudaEvent_t last[64] = {};
-  static cudaStream_t last_stream[64] = {};
-  std::lock_guard<std::mutex> lock(mu);
+namespace {
+struct DevParams {  // what g_sp holds on a device, and the last launch that reads it
+  std::mutex mu;
+  bool valid = false;
+  SParams cur{};
+  cudaEvent_t last = nullptr;
+  cudaStream_t last_stream = nullptr;
+};
+DevParams g_dev[64];
+}  // namespace
+
+// Upload S into g_sp unless it already holds exactly these bytes.  An upload
+// waits for the last launch (on another stream) that may still read g_sp.
+cudaError_t sparse_params_upload(const SParams& S, cudaStream_t stream) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-  if (!last[dev]) {
-    e = cudaEventCreateWithFlags(&last[dev], cudaEventDisableTiming);
-    if (e != cudaSuccess) return e;
-  } else if (last_stream[dev] != stream) {
-    e = cudaStreamWaitEvent(stream, last[dev], 0);
+  DevParams& d = g_dev[dev];
+  std::lock_guard<std::mutex> lock(d.mu);
+  if (!d.last) {
+    e = cudaEventCreateWithFlags(&d.last, cudaEventDisableTiming);
     if (e != cudaSuccess) return e;
   }
-  e = cudaMemcpyToSymbolAsync(g_sp, &S, sizeof(SParams), 0, cudaMemcpyHostToDevice, stream);
+  if (d.valid && std::memcmp(&d.cur, &S, sizeof(SParams)) == 0) return cudaSuccess;
+  if (d.last_stream && d.last_stream != stream) {
+    e = cudaStreamWaitEvent(stream, d.last, 0);
+    if (e != cudaSuccess) return e;
+  }
+  d.cur = S;  // stable host copy: the async copy reads it
+  d.valid = true;
+  return cudaMemcpyToSymbolAsync(g_sp, &d.cur, sizeof(SParams), 0, cudaMemcpyHostToDevice, stream);
+}
+
+// Bookkeeping after launches that did not go through sparse_launch (a graph
+// replay): later uploads from other streams wait for them.
+cudaError_t sparse_note_launch(cudaStream_t stream) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  e = cudaLaunchCooperativeKernel(sparse_kernel_fn(S.wide, S.P.nx), dim3(ctas), dim3(kThreadsS), nullptr, smem, stream);
+  DevParams& d = g_dev[dev];
+  std::lock_guard<std::mutex> lock(d.mu);
+  if (!d.last) {
+    e = cudaEventCreateWithFlags(&d.last, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  }
+  d.last_stream = stream;
+  return cudaEventRecord(d.last, stream);
+}
+
+// One cooperative launch of the plan's persistent kernel over the window `w`.
+cudaError_t sparse_launch(const SParams& S, LaunchWin w, int ctas, size_t smem, cudaStream_t stream) {
+  cudaError_t e = sparse_params_upload(S, stream);
   if (e != cudaSuccess) return e;
-  last_stream[dev] = stream;
-  return cudaEventRecord(last[dev], stream);
+  void* args[] = {&w};
+  e = cudaLaunchCooperativeKernel(sparse_kernel_fn(S.wide, S.P.nx), dim3(ctas), dim3(kThreadsS), args, smem, stream);
+  if (e != cudaSuccess) return e;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  DevParams& d = g_dev[dev];
+  std::lock_guard<std::mutex> lock(d.mu);
+  d.last_stream = stream;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(stream, &cs);
+  if (cs != cudaStreamCaptureStatusNone) return cudaSuccess;  // graph capture: no event record
+  return cudaEventRecord(d.last, stream);
 }
 
 // beta_s = beta M (rows of the stage cache mapped to the structured basis,

@@ -14,7 +14,11 @@ parallelism is the per-stage thread pool (``pkg/src/treesmpc/_parallel.py``,
 
 The cross-rank sum is exact (one non-zero contributor per entry), so a shard
 solve reproduces the single-GPU iterates up to the summation order of the
-chain-head sums (ulp level).  The duality gap is not evaluated by shard plans.
+chain-head sums (ulp level).  The duality gap (engine.py:458-480) is evaluated
+after the loop: every rank assembles the full ergodic averages and final dual by
+an all-reduce sum (replicated trunk rows counted on rank 0 only; exact) and
+evaluates the same gap as a single-GPU plan.  With a communicator the
+2 x iters launches and all-reduces are replayed from a CUDA graph.
 """
 
 from __future__ import annotations
@@ -61,9 +65,9 @@ class ShardedSolver:
         self.plan.set_cache(cache, model)
 
     def solve(self, p, iters: int, lam: float, theta=None, coef=None, warm=None,
-              keep_device: bool = False) -> dict:
+              keep_device: bool = False, skip_gap: bool = False) -> dict:
         return self.plan.solve(p, iters, lam, warm=warm, theta=theta, coef=coef,
-                               skip_gap=True, keep_device=keep_device)
+                               skip_gap=skip_gap, keep_device=keep_device)
 
 
 class LocalShardGroup:
@@ -87,12 +91,13 @@ class LocalShardGroup:
             pl.set_cache(cache, model)
 
     def solve(self, p, iters: int, lam: float, theta=None, coef=None,
-              record_residuals: bool = False) -> list[dict]:
-        """Per-rank result dicts (rows of ``edges[r]`` valid in result r)."""
+              record_residuals: bool = False, skip_gap: bool = True) -> list[dict]:
+        """Per-rank result dicts (rows of ``edges[r]`` valid in result r; with
+        ``skip_gap=False`` every result carries the duality gap of the whole tree)."""
         bufs = [pl._result_buffers(iters, False, record_residuals) for pl in self.plans]
         results = (nat.Result * self.world)(*(b[1] for b in bufs))
         handles = (ctypes.c_void_p * self.world)(*(pl._h for pl in self.plans))
-        flags = (nat.RECORD_RESIDUALS if record_residuals else 0) | nat.SKIP_GAP
+        flags = (nat.RECORD_RESIDUALS if record_residuals else 0) | (nat.SKIP_GAP if skip_gap else 0)
         th = np.ascontiguousarray(theta, dtype=float) if theta is not None else None
         cf = np.ascontiguousarray(coef, dtype=float) if coef is not None else None
         pv = np.ascontiguousarray(p, dtype=float)

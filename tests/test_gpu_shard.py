@@ -31,15 +31,38 @@ def test_shard_world1_matches_reference(name):
     assert np.array_equal(plan.edges(0), np.arange(c.tree.n_edges))
     plan.set_cache(c.cache, c.model)
     th, cf = engine.theta_schedule(c.iters)
-    out = plan.solve(c.p, c.iters, c.lam, theta=th, coef=cf, skip_gap=True)
-    assert out["kernel_launches"] == 2 * c.iters
+    assert plan.solve(c.p, c.iters, c.lam, theta=th, coef=cf, skip_gap=True)["kernel_launches"] == 2 * c.iters
+    out = plan.solve(c.p, c.iters, c.lam, theta=th, coef=cf)
     for f in ("u0", "x", "u", "x_avg", "u_avg"):
         assert rel_err(out[f], z[f"r_{f}"]) <= c.tol(f), (f, rel_err(out[f], z[f"r_{f}"]))
     for k in ("sig", "zeta", "psi"):
         assert rel_err(out[f"dual_{k}"], z[f"r_dual_{k}"]) <= c.tol("dual"), k
     r_ref = float(z["r_residual_inf"])
     assert abs(out["residual_inf"] - r_ref) <= c.tol("residual_inf") * max(1.0, abs(r_ref))
-    assert np.isnan(out["gap"])
+    # duality gap of the shard solve (assembled state, engine.py:458-480)
+    g_ref = float(z["r_gap"])
+    assert abs(out["gap"] - g_ref) <= c.tol("gap") * max(1.0, abs(g_ref)), (out["gap"], g_ref)
+
+
+def test_shard_graph_replay_equals_direct_launches(monkeypatch):
+    """The CUDA-graph replay of the 2 x iters launches + all-reduces gives the same
+    bits as issuing them one by one (TSMPC_NO_GRAPH), twice in a row."""
+    c = load_case("bcn63_SMPC1_N24")
+    th, cf = engine.theta_schedule(c.iters)
+    res = []
+    for env in ("0", "1", "0"):
+        if env == "1":
+            monkeypatch.setenv("TSMPC_NO_GRAPH", "1")
+        else:
+            monkeypatch.delenv("TSMPC_NO_GRAPH", raising=False)
+        plan = DevicePlan(c.model, c.tree, c.factor, c.scaling, shard=(0, 1, nccl_unique_id()))
+        plan.set_cache(c.cache, c.model)
+        res.append(plan.solve(c.p, c.iters, c.lam, theta=th, coef=cf))
+        res.append(plan.solve(c.p, c.iters, c.lam, theta=th, coef=cf))
+    for r in res[1:]:
+        for f in ("u0", "x_avg", "u_avg", "dual_psi"):
+            assert np.array_equal(r[f], res[0][f]), f
+        assert r["gap"] == res[0]["gap"]
 
 
 def test_shard_world1_matches_single_gpu_plan():
@@ -65,8 +88,11 @@ def test_shard_group_matches_reference(name, world):
     assert np.array_equal(np.unique(owned), np.arange(c.tree.n_edges))
     grp.set_cache(c.cache, c.model)
     th, cf = engine.theta_schedule(c.iters)
-    outs = grp.solve(c.p, c.iters, c.lam, theta=th, coef=cf)
-    assert all(o["kernel_launches"] == 2 * c.iters for o in outs)
+    outs = grp.solve(c.p, c.iters, c.lam, theta=th, coef=cf, skip_gap=False)
+    assert all(o["kernel_launches"] >= 2 * c.iters for o in outs)
+    g_ref = float(z["r_gap"])
+    for o in outs:  # every rank evaluates the gap of the whole tree
+        assert abs(o["gap"] - g_ref) <= c.tol("gap") * max(1.0, abs(g_ref)), (o["gap"], g_ref)
     assert len({o["residual_inf"] for o in outs}) == 1  # max over the group
     full = grp.assemble(outs)
     for f in ("u0", "x", "u", "x_avg", "u_avg"):
@@ -88,13 +114,14 @@ def test_shard_group_matches_single_plan_paper_trees(tree_name, world):
     single = DevicePlan(W["model"], W["tree"], W["factor"], W["scaling"])
     single.set_cache(W["caches"][0], W["model"])
     lam = 0.05
-    a = single.solve(W["p"], iters, lam, theta=th, coef=cf, skip_gap=True, record_residuals=True)
+    a = single.solve(W["p"], iters, lam, theta=th, coef=cf, record_residuals=True)
     grp = LocalShardGroup(W["model"], W["tree"], W["factor"], world, W["scaling"])
     sizes = [len(e) for e in grp.edges]
     assert min(sizes) > 0
     grp.set_cache(W["caches"][0], W["model"])
-    outs = grp.solve(W["p"], iters, lam, theta=th, coef=cf, record_residuals=True)
+    outs = grp.solve(W["p"], iters, lam, theta=th, coef=cf, record_residuals=True, skip_gap=False)
     full = grp.assemble(outs)
+    assert abs(outs[0]["gap"] - a["gap"]) <= 1e-9 * max(1.0, abs(a["gap"])), (outs[0]["gap"], a["gap"])
     for f in ("u0", "x", "u", "x_avg", "u_avg"):
         assert rel_err(full[f], a[f]) <= 1e-10, (f, rel_err(full[f], a[f]))
     for k in ("sig", "zeta", "psi"):
