@@ -81,9 +81,9 @@ def dev_metrics(a: np.ndarray, b: np.ndarray) -> tuple[float, float, float]:
     return blk, col, cs
 
 
-def make_case(name, tree_name, iters, record=False, calibrate=True, tree_kw=None):
+def make_case(name, tree_name, iters, record=False, calibrate=True, tree_kw=None, paper_weights=False):
     from paper_1604_01074_b200 import synth
-    model = synth.bcn63_network()
+    model = synth.bcn63_network(paper_weights=paper_weights)
     tree = synth.paper_tree(*synth.PAPER_TREES[tree_name], **(tree_kw or {}))
     fc = synth.forecast_for(tree, k=0)
     p, q = synth.initial_state(model)
@@ -106,7 +106,8 @@ def make_case(name, tree_name, iters, record=False, calibrate=True, tree_kw=None
          "input_sha256": np.array(input_digest(model, tree, fc, p, q)),
          "lam": np.array(lam), "r_u0": rep.u0, "r_residual_inf": np.array(rep.residual_inf),
          "r_gap": np.array(rep.gap), "ref_lambda_s": np.array(t_lam),
-         "ref_solve_s": np.array(t_solve), "edges": np.array(rt.n_edges)}
+         "ref_solve_s": np.array(t_solve), "edges": np.array(rt.n_edges),
+         "paper_weights": np.array(bool(paper_weights))}
     if tree_kw:
         d["tree_kw"] = np.array(repr(tree_kw))
     rows_e, rows_n = sample_rows(rt.n_edges), sample_rows(rt.n_nodes)
@@ -149,6 +150,8 @@ CASES = {
     # record_residuals=True: per-iteration residual and duality gap (engine.py:577-582)
     "L_bcn63_CE_trace_i150": ("CE", 150, True),
     "L_bcn63_SMPC1_trace_i60": ("SMPC1", 60, True),
+    # the paper's cost weights: W_alpha=2e4, Wu=1e5 I, Wx=1e7, gamma_d=5e7
+    "L_bcn63pw_SMPC3_i500": ("SMPC3", 500, False, True),
 }
 
 
@@ -158,7 +161,7 @@ def recalibrate(name, seeds):
     from paper_1604_01074_b200 import synth
     z = dict(np.load(HERE / f"{name}.npz"))
     tree_name, iters = str(z["tree_name"]), int(z["iters"])
-    model = synth.bcn63_network()
+    model = synth.bcn63_network(paper_weights=bool(z.get("paper_weights", False)))
     tree = synth.paper_tree(*synth.PAPER_TREES[tree_name])
     fc = synth.forecast_for(tree, k=0)
     p, q = synth.initial_state(model)
@@ -201,8 +204,8 @@ def main():
         return
     only = args or list(CASES)
     for name in only:
-        tree_name, iters, record = CASES[name]
-        make_case(name, tree_name, iters, record=record)
+        tree_name, iters, record, *pw = CASES[name]
+        make_case(name, tree_name, iters, record=record, paper_weights=bool(pw and pw[0]))
 
 
 if __name__ == "__main__":

@@ -19,7 +19,7 @@ import numpy as np
 GOLDEN = pathlib.Path(__file__).resolve().parent / "golden"
 FIELDS = ("x", "u", "x_avg", "u_avg", "dual_sig", "dual_zeta", "dual_psi")
 LARGE_CASES = ["L_bcn63_CE_i500", "L_bcn63_CE_i2000", "L_bcn63_SMPC1_i2000", "L_bcn63_SMPC3_i500",
-               "L_bcn63_SMPC3_i2000", "L_bcn63_SMPC8_i500", "L_bcn63_W4k_i100"]
+               "L_bcn63_SMPC3_i2000", "L_bcn63_SMPC8_i500", "L_bcn63_W4k_i100", "L_bcn63pw_SMPC3_i500"]
 TRACE_CASES = ["L_bcn63_CE_trace_i150", "L_bcn63_SMPC1_trace_i60"]
 FLOOR = 1e-11
 
@@ -33,7 +33,7 @@ def workload(z: dict) -> dict:
     """Regenerate the inputs the reference was fed and check their digest."""
     from paper_1604_01074_b200 import (build_stage_cache, compute_basis, compute_preconditioner,
                                        factor_step, node_demands, synth)
-    model = synth.bcn63_network()
+    model = synth.bcn63_network(paper_weights=bool(z.get("paper_weights", False)))
     tree = synth.paper_tree(*synth.PAPER_TREES[str(z["tree_name"])])
     fc = synth.forecast_for(tree, k=0)
     p, q = synth.initial_state(model)

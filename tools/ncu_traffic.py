@@ -25,6 +25,9 @@ scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 for r in rows[2:]:
     name = r[hdr.index("Kernel Name")]
     kern = name.split("(")[0].strip()
+    if kern.startswith("void "):
+        kern = kern[5:]
+    kern = kern.split("<")[0]  # template arguments (apg_wide_kernel<2>)
     kern = kern if kern.startswith("tsmpc::") else "tsmpc::" + kern
     tot = 0.0
     for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
