@@ -116,10 +116,10 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def build_workload(tree_name: str, seed_offset: int = 0):
+def build_workload(tree_name: str, seed_offset: int = 0, paper_weights: bool = False):
     from paper_1604_01074_b200 import (build_stage_cache, compute_basis, compute_preconditioner,
                                        factor_step, node_demands, synth)
-    model = synth.bcn63_network()
+    model = synth.bcn63_network(paper_weights=paper_weights)
     tree = synth.paper_tree(*synth.PAPER_TREES[tree_name], seed=seed_offset)
     basis = compute_basis(model)
     fac = factor_step(basis, model)
@@ -299,12 +299,23 @@ def residual_target(args, local):
     engine.solve).  The device checks residual_inf every 25 iterations and stops at
     the first check <= r_ref (SolverConfig.tol); the APG dual residual is not
     monotone, so the line also reports the first iteration after which every
-    check stays <= r_ref, and the same 500-iteration solve without the test."""
+    check stays <= r_ref, and the same 500-iteration solve without the test.  Also
+    run with the paper's cost weights, where the residual
+    decreases steadily and the criterion is not met early by a dip."""
+    out = {}
+    for key, pw, gname in (("bcn63", False, "L_bcn63_SMPC3_i500"), ("bcn63_paper_weights", True,
+                                                                     "L_bcn63pw_SMPC3_i500")):
+        g = golden(gname)
+        if g is not None:
+            out[key] = _residual_target_one(local, g, gname, pw)
+    return out
+
+
+def _residual_target_one(local, g, gname, paper_weights):
     import torch
     from paper_1604_01074_b200 import theta_schedule
     from paper_1604_01074_b200.plan import DevicePlan
-    g = golden("L_bcn63_SMPC3_i500")
-    W = build_workload("SMPC3")
+    W = build_workload("SMPC3", paper_weights=paper_weights)
     plan = DevicePlan(W["model"], W["tree"], W["factor"], W["scaling"], device=local)
     plan.set_cache(W["caches"][0], W["model"])
     lam = float(g["lam"])
@@ -313,27 +324,27 @@ def residual_target(args, local):
     tr = plan.solve(W["p"], 500, lam, theta=th, coef=cf, keep_device=True, skip_gap=True,
                     record_residuals=True)["resid_trace"]
     checks = list(range(24, 500, 25))
-    stay = next((k for k in checks if all(tr[j] <= r_ref for j in checks if j >= k)), None)
+    stay = next((k for k in checks if all(tr[j] <= r_ref * (1 + 1e-9) for j in checks if j >= k)), None)
     runs = []
     for _ in range(5):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        r = plan.solve(W["p"], 500, lam, theta=th, coef=cf, keep_device=True, tol=r_ref, check_every=25)
+        r = plan.solve(W["p"], 500, lam, theta=th, coef=cf, keep_device=True, tol=r_ref * (1 + 1e-9),
+                       check_every=25)
         runs.append((r["iterations"], r["device_ms"], r["device_total_ms"], (time.perf_counter() - t0) * 1e3,
                      r["residual_inf"]))
     full = [plan.solve(W["p"], 500, lam, theta=th, coef=cf, keep_device=True)["device_total_ms"]
             for _ in range(3)]
     it, loop_ms, tot_ms, wall_ms, res = runs[len(runs) // 2]
-    return {"tree": "SMPC3", "r_ref": r_ref, "r_ref_source": "reference engine.solve residual_inf at "
-            "500 iterations (tests/golden/L_bcn63_SMPC3_i500.npz)", "check_every": 25,
+    return {"tree": "SMPC3", "r_ref": r_ref, "r_ref_source": f"reference engine.solve residual_inf at 500 "
+            f"iterations (tests/golden/{gname}.npz)", "check_every": 25,
             "iterations_to_first_check_below": it, "loop_ms": loop_ms, "loop_plus_gap_ms": tot_ms,
             "call_wall_ms": wall_ms, "residual_at_stop": res,
             "first_iteration_staying_below": None if stay is None else stay + 1,
             "residual_at_checks": [float(tr[j]) for j in checks],
             "fixed_500_loop_plus_gap_ms": statistics.median(full),
-            "note": "residual_inf of the APG iterate is not monotone on this problem: it dips below "
-                    "r_ref within the first checks and rises again; both stopping definitions are "
-                    "reported"}
+            "note": "tolerance r_ref (1 + 1e-9): the device residual at 500 iterations equals the reference's "
+                    "to ~1e-9 relative; the APG residual is not monotone, both stopping definitions are reported"}
 
 
 def sharded_measure(args, ws, rank, local, dist):
