@@ -29,7 +29,7 @@ _W = {}
 
 def _work(name):
     z = load(name)
-    key = str(z["tree_name"])
+    key = (str(z["tree_name"]), bool(z.get("paper_weights", False)))
     if key not in _W:
         _W.clear()
         _W[key] = workload(z)
