@@ -17,13 +17,14 @@ ap.add_argument("--tree", default="SMPC8")
 ap.add_argument("--iters", type=int, default=60)
 ap.add_argument("--out", required=True)
 ap.add_argument("--ref")
+ap.add_argument("--record", action="store_true", help="record the residual trace (disables some fast paths)")
 a = ap.parse_args()
 W = bench.build_workload(a.tree)
 plan = DevicePlan(W["model"], W["tree"], W["factor"], W["scaling"])
 plan.set_cache(W["caches"][0], W["model"])
 th, cf = theta_schedule(a.iters)
-r = plan.solve(W["p"], a.iters, 0.4797, theta=th, coef=cf, record_residuals=True)
-keys = ("u0", "x", "u", "x_avg", "u_avg", "dual_sig", "dual_zeta", "dual_psi", "resid_trace")
+r = plan.solve(W["p"], a.iters, 0.4797, theta=th, coef=cf, record_residuals=a.record)
+keys = ("u0", "x", "u", "x_avg", "u_avg", "dual_sig", "dual_zeta", "dual_psi") + (("resid_trace",) if a.record else ())
 np.savez(a.out, **{k: r[k] for k in keys}, gap=r["gap"])
 if a.ref:
     z = np.load(a.ref)
