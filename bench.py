@@ -186,7 +186,7 @@ def time_loop(torch, dev, plan, W, lam, iters, steps, warmup, flush=True):
 def run_ours(args, ws, rank, local):
     import torch
     from paper_1604_01074_b200 import engine, theta_schedule
-    from paper_1604_01074_b200.plan import DevicePlan
+    from paper_1604_01074_b200.plan import plan_for
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
@@ -203,7 +203,11 @@ def run_ours(args, ws, rank, local):
     W = build_workload(args.tree)
     tree, model = W["tree"], W["model"]
     E = tree.n_edges
-    plan = DevicePlan(model, tree, W["factor"], W["scaling"], device=local)
+    # the drop-in's own plan (engine.solve's plan_for: a wide plan gets its buffer
+    # placement picked by short timing trials, plan.tuned_plan); setup timed
+    t0 = time.perf_counter()
+    plan = plan_for(model, tree, W["factor"], W["scaling"], device=local)
+    plan_ms = (time.perf_counter() - t0) * 1e3
     plan.set_cache(W["caches"][0], model)
     lam, lam_ms = device_lambda(W, local)
     info = plan.info()
@@ -218,13 +222,17 @@ def run_ours(args, ws, rank, local):
             for _ in range(3)]
 
     # ---- e2e through the public API (host buffers: forecast H2D + full report D2H per step)
-    e2e_ms = []
+    e2e_ms, e2e_dev = [], []
     for k in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        engine.solve(model, tree, W["forecasts"][k % 2], W["p"], W["q"],
-                     engine.SolverConfig(max_iters=args.iters), basis=W["basis"],
-                     factor=W["factor"], scaling=W["scaling"], lam=lam)
+        rep = engine.solve(model, tree, W["forecasts"][k % 2], W["p"], W["q"],
+                           engine.SolverConfig(max_iters=args.iters), basis=W["basis"],
+                           factor=W["factor"], scaling=W["scaling"], lam=lam)
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        e2e_dev.append(rep.device_ms)
+        assert rep.iterations == args.iters
+    print("e2e per call (ms):", [round(v, 2) for v in e2e_ms], "device loop:", [round(v, 2) for v in e2e_dev],
+          file=sys.stderr)
     e2e_ms = e2e_ms[args.warmup:]
     e2e_total = float(sum(e2e_ms))
     e2e_value = args.steps * args.iters / (e2e_total / 1e3)
@@ -264,7 +272,8 @@ def run_ours(args, ws, rank, local):
         "solve_ms": {"loop": ms_per_step,
                      "loop_plus_gap": statistics.median(r["device_total_ms"] for r in full),
                      "gap": statistics.median(r["device_total_ms"] - r["device_ms"] for r in full)},
-        "setup": {"device_lambda_ms": lam_ms},
+        "setup": {"device_lambda_ms": lam_ms, "plan_create_ms": plan_ms,
+                  "layout_trials_ms": getattr(plan, "layout_trials_ms", None)},
         "clocks": clk.summary(),
     }
     g = golden(f"L_bcn63_{args.tree}_i500")
@@ -491,7 +500,7 @@ def sweep(args, local, have, cpu=True):
     """The paper's scenario-count sweep: device loop time per tree, and the reference
     algorithm's CPU time per iteration on the same host (oracle port, short sample)."""
     import torch
-    from paper_1604_01074_b200.plan import DevicePlan
+    from paper_1604_01074_b200.plan import tuned_plan
     out = {}
     hbm_peak, _ = peaks()
     dev = torch.device("cuda", local)
@@ -500,7 +509,7 @@ def sweep(args, local, have, cpu=True):
             W, plan, lam = have[name]
         else:
             W = build_workload(name)
-            plan = DevicePlan(W["model"], W["tree"], W["factor"], W["scaling"], device=local)
+            plan = tuned_plan(W["model"], W["tree"], W["factor"], W["scaling"], device=local)
             plan.set_cache(W["caches"][0], W["model"])
             g = golden(f"L_bcn63_{name}_i500") or golden(f"L_bcn63_{name}_i100")
             lam = float(g["lam"]) if g is not None else device_lambda(W, local)[0]

@@ -185,6 +185,12 @@ int tsmpc_solve(tsmpc_plan* plan, const double* p, int32_t iters, double lam,
  * result.residual_inf the stopping residual.  Honoured by the structured-basis
  * kernel of single-GPU plans; other plans run max_iters. */
 int tsmpc_set_stopping(tsmpc_plan* plan, double tol, int32_t check_every);
+/* Timing trial (extension, no reference counterpart): `iters` iterations of the
+ * plan's persistent kernel on whatever its buffers hold (zero right after
+ * creation; the loop's cost does not depend on the data), CUDA-event time in *ms.
+ * The Python layer uses it to pick the fastest of a few placements of a large
+ * plan's buffers in device memory (plan.tuned_plan).  Single-GPU plans. */
+int tsmpc_plan_trial(tsmpc_plan* plan, int32_t iters, double* ms);
 
 /* factor.solve_step: z = argmin <z, H'w> + f(z) for an unscaled dual w. */
 int tsmpc_solve_step(tsmpc_plan* plan, const double* w_sig, const double* w_zeta,

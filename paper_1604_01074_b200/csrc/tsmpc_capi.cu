@@ -40,6 +40,7 @@ int fail(int code, const char* fmt, ...) {
   } while (0)
 
 inline int r4(int v) { return (v + 3) / 4 * 4; }
+constexpr size_t kArenaPad = 0;  // TSMPC_ARENA_PAD overrides (bytes)
 inline int r8(int v) { return (v + 7) / 8 * 8; }
 
 }  // namespace
@@ -648,31 +649,47 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
   rc |= pl->upload(&d_ts, dec.tile_seg.data(), dec.tile_seg.size());
   rc |= pl->upload(&d_sr, dec.seg_row.data(), dec.seg_row.size());
   rc |= pl->upload(&d_re, dec.row_edge.data(), dec.row_edge.size());
-  // state
+  // state.  The buffers the persistent kernels touch every iteration (both dual
+  // slots, the ergodic averages, the static per-edge vectors) come from one arena
+  // with a skew between consecutive buffers: the kernel reads the same row of
+  // several of them back to back, and buffer bases that map those rows onto the
+  // same L2 sets / DRAM banks measurably slow it down (identical SMPC8 plans at
+  // different cudaMalloc addresses ran 58-67 us/iteration; tools/layout_probe.py)
   const size_t yblk = 2 * (size_t)E * NXP + (size_t)E * NUP;
-  rc |= pl->alloc(&pl->Y0, yblk);
-  rc |= pl->alloc(&pl->Y1, yblk);
+  {
+    const char* pe = std::getenv("TSMPC_ARENA_PAD");
+    const size_t pad = pe ? (size_t)std::atoll(pe) : kArenaPad;  // bytes, skew per buffer
+    const size_t sizes[] = {yblk, yblk, (size_t)n_nodes * NXP, (size_t)E * NUP, (size_t)E * NUP,
+                            (size_t)E * NXP, (size_t)E * NVP};
+    double** dst[] = {&pl->Y0, &pl->Y1, &pl->XAVG, &pl->UAVG, &pl->UHAT, &pl->EVEC, &pl->BETA_S};
+    size_t total = 0;
+    std::vector<size_t> off;
+    for (size_t i = 0; i < sizeof(sizes) / sizeof(sizes[0]); ++i) {
+      off.push_back(total);
+      total += ((sizes[i] * sizeof(double) + 255) / 256) * 256 + (i + 1) * pad;
+    }
+    char* arena = nullptr;
+    rc |= pl->alloc(&arena, total);
+    if (rc) return bail(0);
+    for (size_t i = 0; i < off.size(); ++i) *dst[i] = reinterpret_cast<double*>(arena + off[i] + (i + 1) * pad);
+  }
   rc |= pl->alloc(&pl->WB, yblk);
   rc |= pl->alloc(&pl->PY, yblk);
-  rc |= pl->alloc(&pl->XAVG, (size_t)n_nodes * NXP);
   rc |= pl->alloc(&pl->X, (size_t)n_nodes * NXP);
   rc |= pl->alloc(&pl->XL, (size_t)n_nodes * NXP);
   rc |= pl->alloc(&pl->XF, (size_t)n_nodes * NXP);
   rc |= pl->alloc(&pl->Z0X, (size_t)n_nodes * NXP);
-  rc |= pl->alloc(&pl->UAVG, (size_t)E * NUP);
   rc |= pl->alloc(&pl->U, (size_t)E * NUP);
   rc |= pl->alloc(&pl->UL, (size_t)E * NUP);
   rc |= pl->alloc(&pl->Z0U, (size_t)E * NUP);
   rc |= pl->alloc(&pl->UF, (size_t)E * NUP);
   rc |= pl->alloc(&pl->XIT, (size_t)E * NUP);
   rc |= pl->alloc(&pl->INC, (size_t)E * NUP);
-  rc |= pl->alloc(&pl->UHAT, (size_t)E * NUP);
   rc |= pl->alloc(&pl->T, (size_t)E * NVP);
   rc |= pl->alloc(&pl->GG, (size_t)E * NVP);
   rc |= pl->alloc(&pl->BETA, (size_t)E * NVP);
   rc |= pl->alloc(&pl->BETA0, (size_t)E * NVP);
   rc |= pl->alloc(&pl->XIQG, (size_t)E * NXP);
-  rc |= pl->alloc(&pl->EVEC, (size_t)E * NXP);
   rc |= pl->alloc(&pl->GDD, (size_t)E * NXP);
   rc |= pl->alloc(&pl->UB, (size_t)E * NXP);
   rc |= pl->alloc(&pl->JRHS, (size_t)E * ne);
@@ -774,7 +791,6 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
         rc |= pl->upload(&d_spi, hp.spi.data(), hp.spi.size());
         rc |= pl->upload(&d_spv, hp.spv.data(), hp.spv.size());
         rc |= pl->upload(&pl->MS, pb->Ms, (size_t)nv * nv);
-        rc |= pl->alloc(&pl->BETA_S, (size_t)E * NVP);
         rc |= pl->alloc(&pl->TG, (size_t)E * NVP);
         rc |= pl->alloc(&pl->KY_S, (size_t)std::max(1, hp.n_trunk) * P.KY_LD);
         if (rc) return bail(0);
@@ -1804,6 +1820,38 @@ int tsmpc_solve_group(tsmpc_plan* const* plans, int32_t n, const double* p, int3
   return TSMPC_OK;
 }
 
+
+int tsmpc_plan_trial(tsmpc_plan* pl, int32_t iters, double* ms) {
+  if (!pl || !ms || iters < 1) return fail(TSMPC_ERR_ARGUMENT, "null argument or iters < 1");
+  // a timing trial of the persistent kernel on whatever the plan's buffers hold
+  // (zero after creation): the loop's cost does not depend on the data
+  const bool had = pl->has_cache;
+  const double tol = pl->tol;
+  pl->has_cache = true;
+  pl->tol = 0.0;
+  std::vector<double> p(pl->nx, 0.0);
+  SolveState st;
+  int rc = solve_prepare(pl, p.data(), iters, 1.0, nullptr, nullptr, nullptr, nullptr, nullptr,
+                         TSMPC_SKIP_GAP | TSMPC_KEEP_DEVICE, st);
+  pl->has_cache = had;
+  pl->tol = tol;
+  if (rc) return rc;
+  if (pl->sharded) return fail(TSMPC_ERR_VALIDATION, "timing trials are for single-GPU plans");
+  CU(cudaEventRecord(pl->ev0, pl->stream));
+  if (pl->use_sparse) {
+    SParams S = sparse_params(pl, st.P);
+    if (pl->SUBCTR) CU(cudaMemsetAsync(pl->SUBCTR, 0, 4 * sizeof(unsigned int), pl->stream));
+    CU(sparse_launch(S, LaunchWin{0, iters, 3, 0}, pl->sp_ctas, pl->sp_smem, pl->stream));
+  } else if (launch_apg(pl, st.P)) {
+    return TSMPC_ERR_CUDA;
+  }
+  CU(cudaEventRecord(pl->ev1, pl->stream));
+  CU(cudaEventSynchronize(pl->ev1));
+  float f = 0.f;
+  CU(cudaEventElapsedTime(&f, pl->ev0, pl->ev1));
+  *ms = f;
+  return TSMPC_OK;
+}
 
 int tsmpc_set_stopping(tsmpc_plan* pl, double tol, int32_t check_every) {
   if (!pl) return fail(TSMPC_ERR_ARGUMENT, "null argument");

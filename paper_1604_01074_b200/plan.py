@@ -20,7 +20,7 @@ from . import _native as nat
 from .errors import DeviceError, DimensionError, ValidationError
 from .points import DualPoint, PrimalPoint
 
-__all__ = ["DevicePlan", "plan_for"]
+__all__ = ["DevicePlan", "plan_for", "tuned_plan"]
 
 
 def _c(a, dtype=np.float64):
@@ -111,6 +111,12 @@ class DevicePlan:
         buf = np.zeros(max(n, 1), dtype=np.int64)
         self._lib.tsmpc_plan_edges(self._h, int(which), nat.iptr(buf), n)
         return buf[:n]
+
+    def trial(self, iters: int = 40) -> float:
+        """CUDA-event ms of `iters` iterations of the plan's kernel (timing trial)."""
+        ms = ctypes.c_double()
+        nat.check(self._lib.tsmpc_plan_trial(self._h, int(iters), ctypes.byref(ms)), "tsmpc_plan_trial")
+        return ms.value
 
     def debug_timers(self) -> np.ndarray:
         """Phase cycle counters of CTA 0 since the last call (timer builds only)."""
@@ -363,6 +369,36 @@ def describe_shard(model, tree, factor, rank: int, world: int, max_ctas: int = 1
     return d
 
 
+def tuned_plan(model, tree, factor, scaling=None, device: int = 0, candidates: int = 4,
+               trial_iters: int = 40) -> DevicePlan:
+    """A plan whose device buffers sit at a fast placement.
+
+    The wide kernels' iteration time depends on where the plan's buffers land in
+    device memory (identical SMPC8 plans at different addresses ran 57-70
+    us/iteration, reproducibly per plan: L2 set / DRAM bank conflicts between rows
+    read back to back; tools/layout_probe.py).  For wide plans this creates
+    `candidates` plans (kept alive together, so each lands elsewhere), times a short
+    trial of each (tsmpc_plan_trial; the cost does not depend on the data) and keeps
+    the fastest.  Other plans are returned as created.  TSMPC_NO_LAYOUT_TUNE=1
+    disables the search."""
+    import os
+    first = DevicePlan(model, tree, factor, scaling, device)
+    info = first.info()
+    if not (info["sparse"] and info["wide"]) or info["sharded"] or candidates <= 1 \
+            or os.environ.get("TSMPC_NO_LAYOUT_TUNE"):
+        return first
+    plans = [first] + [DevicePlan(model, tree, factor, scaling, device) for _ in range(candidates - 1)]
+    times = []
+    for pl in plans:
+        pl.trial(trial_iters)  # warm-up
+        times.append(min(pl.trial(trial_iters) for _ in range(2)))
+    best = int(np.argmin(times))
+    keep = plans[best]
+    keep.layout_trials_ms = times
+    del plans
+    return keep
+
+
 def plan_for(model, tree, factor, scaling=None, device: int = 0) -> DevicePlan:
     """Cached plan per (model, tree, factor, scaling) object identity."""
     key = (id(model), id(tree), id(factor), id(scaling), device)
@@ -373,7 +409,7 @@ def plan_for(model, tree, factor, scaling=None, device: int = 0) -> DevicePlan:
         return hit
     if len(_PLANS) >= _MAX_PLANS:
         _PLANS.pop(next(iter(_PLANS)))
-    plan = DevicePlan(model, tree, factor, scaling, device)
+    plan = tuned_plan(model, tree, factor, scaling, device)
     _PLANS[key] = plan
     return plan
 
