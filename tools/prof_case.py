@@ -1,5 +1,6 @@
 """Run one solve of a synthetic bcn63 case (profiling driver; no timing claims)."""
 import argparse
+import os
 import pathlib
 import sys
 
@@ -7,7 +8,7 @@ sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))
 
 from paper_1604_01074_b200 import (build_stage_cache, compute_basis, compute_preconditioner,  # noqa: E402
                                    factor_step, node_demands, synth, theta_schedule)
-from paper_1604_01074_b200.plan import DevicePlan  # noqa: E402
+from paper_1604_01074_b200.plan import DevicePlan, tuned_plan  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--tree", default="CE")
@@ -24,7 +25,7 @@ s = compute_preconditioner(b, m, t.N, tree=t)
 p, q = synth.initial_state(m)
 fc = synth.forecast_for(t)
 c = build_stage_cache(b, m, t, node_demands(t, fc), k=0, q=q)
-plan = DevicePlan(m, t, f, None if a.plain else s)
+plan = (DevicePlan if os.environ.get("PROF_UNTUNED") else tuned_plan)(m, t, f, None if a.plain else s)
 plan.set_cache(c, m)
 th, cf = theta_schedule(a.iters)
 for _ in range(a.reps):

@@ -2,11 +2,11 @@
 # (ours + reference arm), ncu launch list of the bench command, full captures of
 # the headline kernel (wide, SMPC8) and of the SMPC3 kernel, DRAM traffic, phase timers.
 set -u
-E=gpurun_out/ev2
+E=gpurun_out/ev3
 mkdir -p $E
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $E/smi.txt 2>&1
 python tools/prof_case.py --tree SMPC8 --iters 50 --skip-gap > $E/plain8.log 2>&1 && \
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:apg_wide_kernel -c 1 -f \
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:apg_wide_kernel -s 12 -c 1 -f \
   -o $E/wide_smpc8 python tools/prof_case.py --tree SMPC8 --iters 50 --skip-gap > $E/ncu_smpc8.log 2>&1
 python tools/prof_case.py --tree SMPC3 --iters 50 --skip-gap > $E/plain3.log 2>&1 && \
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:apg_sparse_kernel -c 1 -f \
