@@ -142,6 +142,19 @@ tsmpc_plan* tsmpc_plan_create_shard(const tsmpc_problem* prob, int device, int32
 int tsmpc_solve_group(tsmpc_plan* const* plans, int32_t n, const double* p, int32_t iters,
                       double lam, const double* theta, const double* coef, int32_t flags,
                       tsmpc_result* outs);
+/* Single-process multi-GPU (one host thread drives n GPUs): n shard plans of one
+ * tree, rank r on devices[r], with communicators from ncclCommInitAll;
+ * plans_out[r] receives rank r's plan (destroy each with tsmpc_plan_destroy).
+ * tsmpc_solve_multi runs one solve over all of them -- per iteration phase 1 on
+ * every GPU, the head-sum all-reduces inside one NCCL group, phase 2 on every
+ * GPU -- and fills outs[r] as tsmpc_solve fills a shard plan's result (the
+ * duality gap on the assembled state).  This is what engine.solve runs for
+ * SolverConfig(devices=(...)): the sharded solve behind the reference API. */
+int tsmpc_plans_create_multi(const tsmpc_problem* prob, const int32_t* devices, int32_t n,
+                             tsmpc_plan** plans_out);
+int tsmpc_solve_multi(tsmpc_plan* const* plans, int32_t n, const double* p, int32_t iters,
+                      double lam, const double* theta, const double* coef, int32_t flags,
+                      tsmpc_result* outs);
 /* Edges whose rows a plan computes (which = 0: all for a single-GPU plan, owned
  * chains + trunk for a shard plan; which = 1: trunk edges).  Writes up to cap
  * edge ids to out (may be NULL) and returns the count (or a negative status). */

@@ -78,6 +78,10 @@ SIGNATURES = {
     "tsmpc_plan_path": (ctypes.c_char_p, [ctypes.c_void_p]),
     "tsmpc_set_stopping": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, ctypes.c_int32]),
     "tsmpc_plan_trial": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]),
+    "tsmpc_plans_create_multi": (ctypes.c_int, [ctypes.POINTER(Problem), ctypes.POINTER(ctypes.c_int32),
+                                                ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p)]),
+    "tsmpc_solve_multi": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32, _dp, ctypes.c_int32,
+                                         ctypes.c_double, _dp, _dp, ctypes.c_int32, ctypes.POINTER(Result)]),
     "tsmpc_set_cache_operators": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, _dp, _dp, _dp, _dp, _dp,
                                                  _dp]),
     "tsmpc_set_forecast": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, _dp, _dp]),

@@ -114,6 +114,7 @@ struct tsmpc_plan {
   bool dyk_two_pass = std::getenv("TSMPC_DYKSTRA_TWO_PASS") != nullptr;
   std::vector<int> owned_edges, trunk_edges;
   int* d_trunk = nullptr;           // shard plans: trunk edge ids (device), for the gap's assembly
+  bool multi = false;               // one of the plans of tsmpc_plans_create_multi
   cudaGraphExec_t gexec = nullptr;  // sharded solve: the captured launches + all-reduces
   int g_iters = 0;
   std::string graph_why;
@@ -1524,6 +1525,7 @@ SParams sparse_params(const tsmpc_plan* pl, const Params& P) {
 
 int solve_finish(tsmpc_plan* pl, const SolveState& st, int32_t flags, tsmpc_result* out,
                  bool assembled = false) {
+  CU(cudaSetDevice(pl->device));
   const int E = pl->E, NXP = pl->NXP, NUP = pl->NUP, nx = pl->nx, nu = pl->nu;
   const int iters = st.iters, nres = st.nres;
   const bool record = st.record, stopping = st.stopping;
@@ -1616,6 +1618,8 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
   if (!pl || !p || !out) return fail(TSMPC_ERR_ARGUMENT, "null argument");
   if (pl->sharded && !pl->comm && pl->world > 1)
     return fail(TSMPC_ERR_VALIDATION, "shard plan without a communicator: run it through tsmpc_solve_group");
+  if (pl->multi && pl->world > 1)
+    return fail(TSMPC_ERR_VALIDATION, "plan of a multi-GPU set: run it through tsmpc_solve_multi");
   SolveState st;
   int rc = solve_prepare(pl, p, iters, lam, warm_sig, warm_zeta, warm_psi, theta, coef, flags, st);
   if (rc) return rc;
@@ -1974,3 +1978,119 @@ int tsmpc_dual_operator_step(tsmpc_plan* pl, double* y_dot_dy, double* dy_dot_dy
 }
 
 }  // extern "C"
+
+int tsmpc_plans_create_multi(const tsmpc_problem* pb, const int32_t* devices, int32_t n, tsmpc_plan** out) {
+  if (!pb || !devices || !out) return fail(TSMPC_ERR_ARGUMENT, "null argument");
+  if (n < 1 || n > 64) return fail(TSMPC_ERR_ARGUMENT, "device count %d outside 1..64", n);
+  std::string why;
+  const NcclApi* api = nccl_api(why);
+  if (!api) return fail(TSMPC_ERR_NCCL, "%s", why.c_str());
+  std::vector<tsmpc_plan*> plans(n, nullptr);
+  auto cleanup = [&]() {
+    for (tsmpc_plan* p : plans) delete p;
+  };
+  for (int r = 0; r < n; ++r) {
+    plans[r] = plan_create_impl(pb, devices[r], r, n, nullptr);  // local shard plan of rank r
+    if (!plans[r]) {
+      const std::string e = g_err;
+      cleanup();
+      return fail(TSMPC_ERR_VALIDATION, "rank %d: %s", r, e.c_str());
+    }
+  }
+  std::vector<NcclApi::Comm> comms(n, nullptr);
+  std::vector<int> devs(devices, devices + n);
+  const int nr = api->CommInitAll(comms.data(), n, devs.data());
+  if (nr != 0) {
+    cleanup();
+    return fail(TSMPC_ERR_NCCL, "ncclCommInitAll(%d devices): %s", n, api->GetErrorString(nr));
+  }
+  for (int r = 0; r < n; ++r) {
+    plans[r]->nccl = api;
+    plans[r]->comm = comms[r];
+    plans[r]->multi = true;
+    out[r] = plans[r];
+  }
+  return TSMPC_OK;
+}
+
+int tsmpc_solve_multi(tsmpc_plan* const* plans, int32_t n, const double* p, int32_t iters, double lam,
+                      const double* theta, const double* coef, int32_t flags, tsmpc_result* outs) {
+  if (!plans || !p || !outs) return fail(TSMPC_ERR_ARGUMENT, "null argument");
+  if (n < 1 || n > 64) return fail(TSMPC_ERR_ARGUMENT, "plan count %d outside 1..64", n);
+  for (int r = 0; r < n; ++r) {
+    const tsmpc_plan* pl = plans[r];
+    if (!pl || !pl->multi || pl->world != n || pl->rank != r || !pl->comm)
+      return fail(TSMPC_ERR_VALIDATION, "member %d must be rank %d of a tsmpc_plans_create_multi set of %d", r, r, n);
+  }
+  if (flags & TSMPC_GAP_TRACE) return fail(TSMPC_ERR_VALIDATION, "no per-iteration gap on multi-GPU solves");
+  const NcclApi* api = plans[0]->nccl;
+  std::vector<SolveState> st(n);
+  std::vector<SParams> S(n);
+  for (int r = 0; r < n; ++r) {
+    int rc = solve_prepare(plans[r], p, iters, lam, nullptr, nullptr, nullptr, theta, coef, flags, st[r]);
+    if (rc) return rc;
+    S[r] = sparse_params(plans[r], st[r].P);
+    CU(cudaEventRecord(plans[r]->ev0, plans[r]->stream));
+  }
+  auto nccl = [&](int nr) -> int {
+    return nr == 0 ? TSMPC_OK : fail(TSMPC_ERR_NCCL, "NCCL: %s", api->GetErrorString(nr));
+  };
+  const size_t hs = (size_t)std::max(1, plans[0]->sp_trunk) * S[0].HS_LD;
+  for (int nu = 0; nu < iters; ++nu) {
+    for (int r = 0; r < n; ++r) {
+      CU(cudaSetDevice(plans[r]->device));
+      CU(sparse_launch(S[r], LaunchWin{nu, nu + 1, 1, 0}, plans[r]->sp_ctas, plans[r]->sp_smem, plans[r]->stream));
+    }
+    if (plans[0]->sp_trunk > 0) {
+      if (nccl(api->GroupStart())) return TSMPC_ERR_NCCL;
+      for (int r = 0; r < n; ++r)
+        if (nccl(api->AllReduce(plans[r]->HS, plans[r]->HS, hs, NcclApi::kFloat64, NcclApi::kSum, plans[r]->comm,
+                                plans[r]->stream)))
+          return TSMPC_ERR_NCCL;
+      if (nccl(api->GroupEnd())) return TSMPC_ERR_NCCL;
+    }
+    for (int r = 0; r < n; ++r) {
+      CU(cudaSetDevice(plans[r]->device));
+      CU(sparse_launch(S[r], LaunchWin{nu, nu + 1, 2, 0}, plans[r]->sp_ctas, plans[r]->sp_smem, plans[r]->stream));
+      plans[r]->launches += 2;
+    }
+  }
+  // residual: max over ranks
+  if (nccl(api->GroupStart())) return TSMPC_ERR_NCCL;
+  for (int r = 0; r < n; ++r)
+    if (nccl(api->AllReduce(plans[r]->RESID, plans[r]->RESID, (size_t)st[r].nres, NcclApi::kUint64, NcclApi::kMax,
+                            plans[r]->comm, plans[r]->stream)))
+      return TSMPC_ERR_NCCL;
+  if (nccl(api->GroupEnd())) return TSMPC_ERR_NCCL;
+  for (int r = 0; r < n; ++r) {
+    CU(cudaSetDevice(plans[r]->device));
+    CU(cudaEventRecord(plans[r]->ev1, plans[r]->stream));
+  }
+  const bool gap = !(flags & TSMPC_SKIP_GAP);
+  if (gap) {
+    // the full averages and final dual on every GPU (replicated rows counted on rank 0)
+    for (int r = 1; r < n; ++r) {
+      CU(cudaSetDevice(plans[r]->device));
+      double* yfin = (iters & 1) == 0 ? plans[r]->Y0 : plans[r]->Y1;
+      if (zero_replicated_rows(plans[r], yfin, plans[r]->stream)) return TSMPC_ERR_CUDA;
+    }
+    const size_t yblk = 2 * (size_t)plans[0]->E * plans[0]->NXP + (size_t)plans[0]->E * plans[0]->NUP;
+    if (nccl(api->GroupStart())) return TSMPC_ERR_NCCL;
+    for (int r = 0; r < n; ++r) {
+      tsmpc_plan* pl = plans[r];
+      double* yfin = (iters & 1) == 0 ? pl->Y0 : pl->Y1;
+      if (nccl(api->AllReduce(pl->XAVG, pl->XAVG, (size_t)pl->n_nodes * pl->NXP, NcclApi::kFloat64, NcclApi::kSum,
+                              pl->comm, pl->stream)) ||
+          nccl(api->AllReduce(pl->UAVG, pl->UAVG, (size_t)pl->E * pl->NUP, NcclApi::kFloat64, NcclApi::kSum, pl->comm,
+                              pl->stream)) ||
+          nccl(api->AllReduce(yfin, yfin, yblk, NcclApi::kFloat64, NcclApi::kSum, pl->comm, pl->stream)))
+        return TSMPC_ERR_NCCL;
+    }
+    if (nccl(api->GroupEnd())) return TSMPC_ERR_NCCL;
+  }
+  for (int r = 0; r < n; ++r) {
+    int rc = solve_finish(plans[r], st[r], flags, outs + r, gap);
+    if (rc) return rc;
+  }
+  return TSMPC_OK;
+}

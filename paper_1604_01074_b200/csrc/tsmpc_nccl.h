@@ -19,6 +19,9 @@ struct NcclApi {
   int (*CommDestroy)(Comm) = nullptr;
   int (*AllReduce)(const void*, void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(int) = nullptr;
+  int (*CommInitAll)(Comm*, int, const int*) = nullptr;  // single-process multi-GPU
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
   static constexpr int kUint64 = 5, kFloat64 = 8, kSum = 0, kMax = 2;
 };
 

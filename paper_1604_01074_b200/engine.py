@@ -52,6 +52,9 @@ class SolverConfig:
     # residual_inf checked every `check_every` iterations on the device is <= tol
     tol: float | None = None
     check_every: int = 25
+    # extension: split the tree by subtree over these GPUs of this process (one
+    # NCCL all-reduce of chain-head sums per iteration; shard.MultiDeviceSolver)
+    devices: tuple | None = None
 
     def __post_init__(self):
         if self.max_iters < 1:
@@ -273,6 +276,10 @@ def solve(model, tree, forecast, p, q, config: SolverConfig | None = None, *,
     if lam is None:
         lam = compute_lambda(basis, factor, model, tree, scaling=scaling, device=device)
 
+    devices = getattr(config, "devices", None)
+    if devices:
+        return _solve_multi(model, tree, forecast, p, q, config, basis, factor, cache, scaling,
+                            float(lam), tuple(devices), warm_dual)
     plan = plan_for(model, tree, factor, scaling, device)
     if cache is None:
         # stage cache built on the device from the forecast
@@ -302,6 +309,46 @@ def solve(model, tree, forecast, p, q, config: SolverConfig | None = None, *,
         residual_trace=out["resid_trace"], gap_trace=gap_trace,
         dual=DualPoint(out["dual_sig"], out["dual_zeta"], out["dual_psi"]),
         device_ms=out["device_ms"])
+
+
+_MULTI: dict = {}
+
+
+def _solve_multi(model, tree, forecast, p, q, config, basis, factor, cache, scaling, lam, devices,
+                 warm_dual):
+    """engine.solve over several GPUs of this process (SolverConfig.devices)."""
+    from .shard import MultiDeviceSolver
+    if config.warm_start and warm_dual is not None:
+        raise ValidationError("warm_dual is not supported with SolverConfig.devices")
+    if config.tol is not None:
+        raise ValidationError("tol (early stop) is not supported with SolverConfig.devices")
+    key = (id(model), id(tree), id(factor), id(scaling), devices)
+    hit = _MULTI.get(key)
+    if hit is None or hit.model is not model or hit.tree is not tree or hit.factor is not factor \
+            or hit.scaling is not scaling:
+        _MULTI.clear()
+        hit = MultiDeviceSolver(model, tree, factor, scaling, devices)
+        _MULTI[key] = hit
+    if cache is None:
+        if forecast.dhat.shape[0] != tree.N:
+            raise DimensionError(
+                f"forecast horizon {forecast.dhat.shape[0]} does not match tree horizon {tree.N}")
+        hit.set_forecast(forecast, q, basis, model)
+    else:
+        hit.set_cache(cache, model)
+    theta, coef = theta_schedule(config.max_iters)
+    t0 = time.perf_counter()
+    outs = hit.solve(p, config.max_iters, lam, theta=theta, coef=coef,
+                     record_residuals=config.record_residuals)
+    full = hit.assemble(outs)
+    wall = time.perf_counter() - t0
+    return SolveReport(
+        u0=full["u0"], x=full["x"], u=full["u"], x_avg=full["x_avg"], u_avg=full["u_avg"],
+        residual_inf=full["residual_inf"], gap=full["gap"], iterations=full["iterations"],
+        wall_time_s=wall, lam=lam, preconditioned=scaling is not None,
+        residual_trace=full["resid_trace"], gap_trace=None,
+        dual=DualPoint(full["dual_sig"], full["dual_zeta"], full["dual_psi"]),
+        device_ms=full["device_ms"])
 
 
 def _gap_trace_dense(plan, p, config, lam, warm, theta, coef):

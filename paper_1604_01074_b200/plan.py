@@ -34,6 +34,21 @@ class DevicePlan:
     def __init__(self, model, tree, factor, scaling=None, device: int = 0, shard=None,
                  warn_dense: bool = True):
         lib = nat.load_library()
+        pb, keep = self._problem(model, tree, factor, scaling, warn_dense)
+        if shard is None:
+            handle = lib.tsmpc_plan_create(ctypes.byref(pb), int(device))
+        else:
+            rank, world, nid = shard
+            idbuf = None if nid is None else (ctypes.c_uint8 * 128).from_buffer_copy(bytes(nid))
+            handle = lib.tsmpc_plan_create_shard(ctypes.byref(pb), int(device), int(rank), int(world),
+                                                 idbuf)
+        if not handle:
+            nat.check(nat.ERR_CUDA if "CUDA" in nat.last_error() or "device" in nat.last_error()
+                      else nat.ERR_VALIDATION, "tsmpc_plan_create")
+        self._bind(lib, handle, model, tree, factor, scaling, shard)
+
+    def _problem(self, model, tree, factor, scaling, warn_dense=True):
+        """The tsmpc_problem of (model, tree, factor, scaling) and the arrays it points at."""
         n_x, n_u, n_v = factor.n_x, factor.n_u, factor.n_v
         E = np.asarray(model.E, dtype=float)
         n_e = E.shape[0]
@@ -58,7 +73,7 @@ class DevicePlan:
                 self.structured_error = f"{type(exc).__name__}: {exc}"
                 if warn_dense:
                     warnings.warn(f"structured kernel basis unavailable ({self.structured_error}); "
-                                  "the plan uses the dense DMMA kernel", RuntimeWarning, stacklevel=2)
+                                  "the plan uses the dense DMMA kernel", RuntimeWarning, stacklevel=3)
             else:
                 keep["Ls"], keep["lam_s"], keep["Ms"] = _c(sb.Ls), _c(sb.lam), _c(sb.M)
                 self.structured = sb
@@ -72,24 +87,37 @@ class DevicePlan:
         pb.W_alpha, pb.Wx, pb.gamma_d = float(model.W_alpha), float(model.Wx), float(model.gamma_d)
         for name, arr in keep.items():
             setattr(pb, name, nat.iptr(arr) if arr.dtype == np.int64 else nat.dptr(arr))
-        if shard is None:
-            handle = lib.tsmpc_plan_create(ctypes.byref(pb), int(device))
-        else:
-            rank, world, nid = shard
-            idbuf = None if nid is None else (ctypes.c_uint8 * 128).from_buffer_copy(bytes(nid))
-            handle = lib.tsmpc_plan_create_shard(ctypes.byref(pb), int(device), int(rank), int(world),
-                                                 idbuf)
+        return pb, keep
+
+    def _bind(self, lib, handle, model, tree, factor, scaling, shard):
         self.shard = shard
-        if not handle:
-            nat.check(nat.ERR_CUDA if "CUDA" in nat.last_error() or "device" in nat.last_error()
-                      else nat.ERR_VALIDATION, "tsmpc_plan_create")
         self._lib = lib
         self._h = ctypes.c_void_p(handle)
         self._fin = weakref.finalize(self, lib.tsmpc_plan_destroy, ctypes.c_void_p(handle))
         self.model, self.tree, self.factor, self.scaling = model, tree, factor, scaling
-        self.n_x, self.n_u, self.n_v = n_x, n_u, n_v
+        self.n_x, self.n_u, self.n_v = factor.n_x, factor.n_u, factor.n_v
         self.n_nodes, self.n_edges = int(tree.n_nodes), int(tree.n_edges)
         self._cache_key = None
+
+    @classmethod
+    def create_multi(cls, model, tree, factor, scaling, devices) -> list["DevicePlan"]:
+        """Rank r's shard plan on devices[r] for every r, NCCL communicators from
+        ncclCommInitAll (one process drives all GPUs; tsmpc_plans_create_multi)."""
+        lib = nat.load_library()
+        head = cls.__new__(cls)
+        pb, keep = head._problem(model, tree, factor, scaling)
+        n = len(devices)
+        devs = (ctypes.c_int32 * n)(*[int(d) for d in devices])
+        handles = (ctypes.c_void_p * n)()
+        nat.check(lib.tsmpc_plans_create_multi(ctypes.byref(pb), devs, n, handles), "tsmpc_plans_create_multi")
+        plans = []
+        for r in range(n):
+            pl = head if r == 0 else cls.__new__(cls)
+            if r:
+                pl.structured, pl.structured_error = head.structured, head.structured_error
+            pl._bind(lib, handles[r], model, tree, factor, scaling, (r, n, None))
+            plans.append(pl)
+        return plans
 
     # -- introspection -------------------------------------------------------
     def info(self) -> dict:

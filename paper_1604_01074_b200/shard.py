@@ -30,7 +30,8 @@ import numpy as np
 from . import _native as nat
 from .plan import DevicePlan
 
-__all__ = ["nccl_unique_id", "ShardedSolver", "LocalShardGroup", "gather_rows", "merge_rows"]
+__all__ = ["nccl_unique_id", "ShardedSolver", "LocalShardGroup", "MultiDeviceSolver", "gather_rows",
+           "merge_rows"]
 
 
 def nccl_unique_id() -> bytes:
@@ -111,6 +112,50 @@ class LocalShardGroup:
         """Full per-edge / per-node arrays from the per-rank results."""
         parts = [_owned(o, e) for o, e in zip(outs, self.edges)]
         return merge_rows(parts, outs[0], self.n_edges, self.n_nodes)
+
+
+class MultiDeviceSolver:
+    """Every shard of one tree, each on its own GPU of THIS process
+    (``tsmpc_plans_create_multi`` / ``tsmpc_solve_multi``: one host thread drives
+    all GPUs, the per-iteration all-reduces go out as one NCCL group).  This is
+    what ``engine.solve`` runs for ``SolverConfig(devices=(...))``."""
+
+    def __init__(self, model, tree, factor, scaling=None, devices=(0,)):
+        self.devices = tuple(int(d) for d in devices)
+        self.world = len(self.devices)
+        self.n_edges, self.n_nodes = int(tree.n_nodes) - 1, int(tree.n_nodes)
+        self.plans = DevicePlan.create_multi(model, tree, factor, scaling, self.devices)
+        self.edges = [pl.edges(0) for pl in self.plans]
+        self.model, self.tree, self.factor, self.scaling = model, tree, factor, scaling
+
+    def set_cache(self, cache, model=None):
+        for pl in self.plans:
+            pl.set_cache(cache, model)
+
+    def set_forecast(self, forecast, q, basis, model=None):
+        for pl in self.plans:
+            pl.set_forecast(forecast, q, basis, model)
+
+    def solve(self, p, iters: int, lam: float, theta=None, coef=None, record_residuals: bool = False,
+              skip_gap: bool = False) -> list[dict]:
+        bufs = [pl._result_buffers(iters, False, record_residuals) for pl in self.plans]
+        results = (nat.Result * self.world)(*(b[1] for b in bufs))
+        handles = (ctypes.c_void_p * self.world)(*(pl._h for pl in self.plans))
+        flags = (nat.RECORD_RESIDUALS if record_residuals else 0) | (nat.SKIP_GAP if skip_gap else 0)
+        th = np.ascontiguousarray(theta, dtype=float) if theta is not None else None
+        cf = np.ascontiguousarray(coef, dtype=float) if coef is not None else None
+        pv = np.ascontiguousarray(p, dtype=float)
+        nat.check(self.plans[0]._lib.tsmpc_solve_multi(handles, self.world, nat.dptr(pv), int(iters),
+                                                       float(lam), nat.dptr(th), nat.dptr(cf), flags,
+                                                       results), "tsmpc_solve_multi")
+        return [DevicePlan._result_dict(b[0], results[r], b[2]) for r, b in enumerate(bufs)]
+
+    def assemble(self, outs: list[dict]) -> dict:
+        parts = [_owned(o, e) for o, e in zip(outs, self.edges)]
+        full = merge_rows(parts, outs[0], self.n_edges, self.n_nodes)
+        full.update(gap=outs[0]["gap"], iterations=outs[0]["iterations"],
+                    device_ms=max(o["device_ms"] for o in outs), resid_trace=outs[0]["resid_trace"])
+        return full
 
 
 _EDGE_KEYS = ("u", "u_avg", "dual_sig", "dual_zeta", "dual_psi")

@@ -140,3 +140,20 @@ def test_shard_group_rejects_bad_members():
     grp.plans.reverse()
     with pytest.raises(ValidationError, match="local shard plan of rank"):
         grp.solve(c.p, 5, c.lam)
+
+
+def test_engine_solve_over_devices_matches_reference():
+    """engine.solve(SolverConfig(devices=...)): the sharded solve behind the reference
+    API (tsmpc_plans_create_multi + tsmpc_solve_multi; one GPU here, so one rank)."""
+    c = load_case("bcn63_SMPC1_N24")
+    z = c.z
+    rep = engine.solve(c.model, c.tree, c.forecast, c.p, c.q,
+                       engine.SolverConfig(max_iters=c.iters, devices=(0,)), basis=c.basis,
+                       factor=c.factor, cache=c.cache, scaling=c.scaling, lam=c.lam)
+    for f in ("u0", "x", "u", "x_avg", "u_avg"):
+        assert rel_err(getattr(rep, f), z[f"r_{f}"]) <= c.tol(f), (f, rel_err(getattr(rep, f), z[f"r_{f}"]))
+    for k in ("sig", "zeta", "psi"):
+        assert rel_err(getattr(rep.dual, k), z[f"r_dual_{k}"]) <= c.tol("dual"), k
+    g_ref = float(z["r_gap"])
+    assert abs(rep.gap - g_ref) <= c.tol("gap") * max(1.0, abs(g_ref)), (rep.gap, g_ref)
+    assert rep.iterations == c.iters
