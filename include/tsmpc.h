@@ -120,11 +120,15 @@ void tsmpc_plan_destroy(tsmpc_plan* plan);
 /* Subtree sharding across the GPUs of one node (one process per GPU).  Rank 0
  * creates an NCCL unique id (128 bytes) with tsmpc_nccl_unique_id and shares it
  * (e.g. torch.distributed broadcast); every rank then creates its shard plan.
- * The trunk (edges above the leaf chains) is replicated; the leaf chains are
- * split by the trunk node they hang from.  tsmpc_solve on a shard plan runs, per
- * iteration, phase 1 -> ncclAllReduce of the per-trunk-node chain-head sums ->
- * phase 2, and returns results for tsmpc_plan_edges(plan, 0, ...) only; the
- * residual is the max over ranks; the duality gap is not evaluated (NaN).
+ * The leaf chains are split by the trunk node they hang from; a trunk position
+ * with one rank's chains below is computed by that rank only, the positions with
+ * several ranks' chains below ("mixed", the top of the tree) are replicated.
+ * tsmpc_solve on a shard plan runs, per iteration, phase 1 (backward, bottom-up
+ * sums below the cut) -> ncclAllReduce of the cut exchange rows (per cut
+ * position its bottom-up sums, per mixed position its chain-head sums; one
+ * contributor per entry: exact) -> phase 2, and returns results for
+ * tsmpc_plan_edges(plan, 0, ...) only; the residual is the max over ranks; the
+ * duality gap is evaluated on the state assembled across ranks.
  * Replaces the reference's intra-stage thread pool (pkg/src/treesmpc/_parallel.py,
  * factor.py:107-128) at the node level.  Requires the structured-basis kernel. */
 int tsmpc_nccl_unique_id(uint8_t* out128);
@@ -133,7 +137,7 @@ tsmpc_plan* tsmpc_plan_create_shard(const tsmpc_problem* prob, int device, int32
 /* Several shard plans of one tree on ONE device, created with nccl_id128 = NULL
  * (local shard plans, ranks 0..n-1 of world n, plans[r] = rank r), solved in
  * lockstep in one process: per iteration, phase 1 of every shard, an in-place
- * device sum of their head-sum buffers (the exchange ncclAllReduce performs
+ * device sum of their cut exchange rows (the exchange ncclAllReduce performs
  * across GPUs), phase 2 of every shard; residuals are max-reduced the same way.
  * outs[r] receives rank r's rows, as tsmpc_solve on an NCCL shard plan would.
  * Exercises the multi-rank split on a single GPU (the kernels of different
@@ -146,7 +150,7 @@ int tsmpc_solve_group(tsmpc_plan* const* plans, int32_t n, const double* p, int3
  * tree, rank r on devices[r], with communicators from ncclCommInitAll;
  * plans_out[r] receives rank r's plan (destroy each with tsmpc_plan_destroy).
  * tsmpc_solve_multi runs one solve over all of them -- per iteration phase 1 on
- * every GPU, the head-sum all-reduces inside one NCCL group, phase 2 on every
+ * every GPU, the cut-row all-reduces inside one NCCL group, phase 2 on every
  * GPU -- and fills outs[r] as tsmpc_solve fills a shard plan's result (the
  * duality gap on the assembled state).  This is what engine.solve runs for
  * SolverConfig(devices=(...)): the sharded solve behind the reference API. */
@@ -156,7 +160,8 @@ int tsmpc_solve_multi(tsmpc_plan* const* plans, int32_t n, const double* p, int3
                       double lam, const double* theta, const double* coef, int32_t flags,
                       tsmpc_result* outs);
 /* Edges whose rows a plan computes (which = 0: all for a single-GPU plan, owned
- * chains + trunk for a shard plan; which = 1: trunk edges).  Writes up to cap
+ * chains + own and mixed trunk positions for a shard plan; which = 1: trunk
+ * edges).  Writes up to cap
  * edge ids to out (may be NULL) and returns the count (or a negative status). */
 int tsmpc_plan_edges(const tsmpc_plan* plan, int32_t which, int64_t* out, int64_t cap);
 
@@ -248,8 +253,13 @@ void* tsmpc_host_alloc(int64_t bytes);
 void tsmpc_host_free(void* ptr);
 
 /* Host-only planning of one shard: info = {ctas, owned_chains, owned_rows,
- * trunk_edges, total_chains, owned_trunk_nodes, smem_bytes}; the owned chain
- * edges go to edges[0..cap) when edges != NULL. */
+ * trunk_edges, total_chains, owned_trunk_nodes (chain-head groups), smem_bytes,
+ * own_trunk_positions (only this rank's chains below), mixed_positions (several
+ * ranks' chains below: replicated), cut_positions (single-rank subtrees hanging
+ * from a mixed position), exchange_rows, exchange_doubles (per iteration, the
+ * count every rank sums: SURVEY §8e's cut), result_rows}; the edges whose rows
+ * the shard computes (tsmpc_plan_edges(plan, 0)) go to edges[0..cap) when
+ * edges != NULL. */
 int tsmpc_describe_shard(const tsmpc_problem* prob, int32_t max_ctas, int64_t smem_limit,
                          int32_t rank, int32_t world, int64_t* info, int32_t n_info,
                          int64_t* edges, int64_t cap);

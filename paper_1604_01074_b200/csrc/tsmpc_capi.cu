@@ -101,6 +101,7 @@ struct tsmpc_plan {
   const NcclApi* nccl = nullptr;
   void* comm = nullptr;
   double* HS = nullptr;
+  double* XCH = nullptr;            // shard plans: the cut exchange rows (summed across ranks)
   double* TR = nullptr;            // split mode: [du | B du | x] per trunk position
   unsigned int* SUBCTR = nullptr;  // split mode: trunk-CTA barrier counter
   unsigned int* ABORT = nullptr;   // raised by a sparse-kernel spin-wait that timed out
@@ -113,7 +114,9 @@ struct tsmpc_plan {
   bool dyk_warp = std::getenv("TSMPC_DYKSTRA_WARP") != nullptr;
   bool dyk_two_pass = std::getenv("TSMPC_DYKSTRA_TWO_PASS") != nullptr;
   std::vector<int> owned_edges, trunk_edges;
-  int* d_trunk = nullptr;           // shard plans: trunk edge ids (device), for the gap's assembly
+  std::vector<int> result_edges;    // shard plans: rows this rank computes (chains + own / mixed trunk)
+  std::vector<int> zero_edges;      // shard plans: rows zeroed before the cross-rank assembly
+  int* d_zero = nullptr;
   bool multi = false;               // one of the plans of tsmpc_plans_create_multi
   cudaGraphExec_t gexec = nullptr;  // sharded solve: the captured launches + all-reduces
   int g_iters = 0;
@@ -478,8 +481,10 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
          (size_t)prop.sharedMemPerBlockOptin);
     return bail(0);
   }
+  cudaFuncAttributes fp{};
+  cudaFuncGetAttributes(&fp, apg_persistent_kernel);
   if (cudaFuncSetAttribute(apg_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)pl->smem) != cudaSuccess) {
+                           (int)(prop.sharedMemPerBlockOptin - fp.sharedSizeBytes)) != cudaSuccess) {
     fail(TSMPC_ERR_CUDA, "cannot reserve %zu bytes of shared memory", pl->smem);
     return bail(0);
   }
@@ -774,7 +779,12 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
       const void* kfn = sparse_kernel_fn(hp.S.wide, nx);
       int occ_s = 0;
       if (hp.ok) {
-        if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hp.smem) != cudaSuccess) {
+        // the attribute is per kernel, shared by every plan of the process: the
+        // opt-in maximum (not this plan's size, which a plan needing more would trip on)
+        cudaFuncAttributes fk{};
+        cudaFuncGetAttributes(&fk, kfn);
+        const int smem_max = (int)(prop.sharedMemPerBlockOptin - fk.sharedSizeBytes);
+        if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max) != cudaSuccess) {
           hp.ok = false;
           hp.why = "cannot reserve shared memory for the sparse kernel";
           cudaGetLastError();
@@ -822,9 +832,15 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
           unsigned char* d_tow;
           rc |= pl->upload(&d_tow, hp.towned.data(), std::max<size_t>(1, hp.towned.size()));
           rc |= pl->alloc(&pl->HS, (size_t)std::max(1, hp.n_trunk) * S.HS_LD);
+          S.cut = hp.cut ? 1 : 0;
+          S.n_xch = hp.n_xch;
+          S.XCH_LD = hp.cut ? P.KY_LD + NXP : S.HS_LD;
+          if (hp.cut) rc |= pl->alloc(&pl->XCH, (size_t)std::max(1, hp.n_xch) * S.XCH_LD);
+          else pl->XCH = pl->HS;  // every position's head sums, exchanged in place
           if (rc) return bail(0);
           S.sharded = 1;
           S.HS = pl->HS;
+          S.XCH = pl->XCH;
           S.towned = d_tow;
           pl->sharded = true;
           pl->rank = srank;
@@ -832,7 +848,21 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
           pl->total_chains = hp.total_chains;
           pl->owned_edges = hp.owned_edges;
           pl->trunk_edges = hp.trunk_edge;
-          rc |= pl->upload(&pl->d_trunk, hp.trunk_edge.data(), std::max<size_t>(1, hp.trunk_edge.size()));
+          pl->result_edges = hp.result_edges;
+          // rows another rank computes (or, replicated, rank 0 counts): zeroed before
+          // the cross-rank assembly of the averages and the dual
+          {
+            std::vector<char> keep(E, 0);
+            for (int e : hp.result_edges) keep[e] = 1;
+            if (srank != 0)
+              for (size_t tp = 0; tp < hp.trunk_edge.size(); ++tp)
+                if (hp.trole[tp] == kRoleMixed) keep[hp.trunk_edge[tp]] = 0;
+            for (int e = 0; e < E; ++e)
+              if (!keep[e]) pl->zero_edges.push_back(e);
+          }
+          if (pl->zero_edges.empty()) pl->zero_edges.push_back(-1);  // (a valid upload; never read)
+          rc |= pl->upload(&pl->d_zero, pl->zero_edges.data(), pl->zero_edges.size());
+          if (pl->zero_edges[0] < 0) pl->zero_edges.clear();
           if (rc) return bail(0);
         }
         pl->use_sparse = true;
@@ -1014,9 +1044,7 @@ int tsmpc_plan_edges(const tsmpc_plan* pl, int32_t which, int64_t* out, int64_t 
     if (!pl->sharded) {
       for (int e = 0; e < pl->E; ++e) all.push_back(e);
     } else {
-      all = pl->owned_edges;
-      all.insert(all.end(), pl->trunk_edges.begin(), pl->trunk_edges.end());
-      std::sort(all.begin(), all.end());
+      all = pl->result_edges;  // own chains, own and mixed trunk positions
     }
   } else if (which == 1) {
     v = &pl->trunk_edges;
@@ -1087,11 +1115,20 @@ int tsmpc_describe_shard(const tsmpc_problem* pb, int32_t max_ctas, int64_t smem
   if (!hp.ok) return fail(TSMPC_ERR_VALIDATION, "%s", hp.why.c_str());
   int64_t owned_heads = 0;
   for (unsigned char t : hp.towned) owned_heads += t;
+  int64_t own_trunk = 0, mixed = 0, cut = 0;
+  for (signed char r : hp.trole) {
+    own_trunk += r == kRoleOwn || r == kRoleCutOwn;
+    mixed += r == kRoleMixed;
+    cut += r == kRoleCutOwn || r == kRoleCutForeign;
+  }
+  const int64_t xld = hp.cut ? r4(pb->n_x) * 2 + r4(pb->n_v) + r4(pb->n_u) : r4(pb->n_x) + r4(pb->n_v);
   const int64_t vals[] = {hp.n_ctas, hp.n_chains, hp.owned_rows, hp.n_trunk, hp.total_chains, owned_heads,
-                          (int64_t)hp.smem};
+                          (int64_t)hp.smem, own_trunk, mixed, cut, hp.n_xch,
+                          hp.n_xch * xld,
+                          (int64_t)hp.result_edges.size()};
   for (int i = 0; i < n && i < (int)(sizeof(vals) / sizeof(vals[0])); ++i) info[i] = vals[i];
   if (edges)
-    for (int64_t i = 0; i < cap && i < (int64_t)hp.owned_edges.size(); ++i) edges[i] = hp.owned_edges[i];
+    for (int64_t i = 0; i < cap && i < (int64_t)hp.result_edges.size(); ++i) edges[i] = hp.result_edges[i];
   return TSMPC_OK;
 }
 
@@ -1472,19 +1509,21 @@ int solve_prepare(tsmpc_plan* pl, const double* p, int32_t iters, double lam, co
   return TSMPC_OK;
 }
 
-// Shard plans hold their owned chain rows and the replicated trunk rows; the other
-// rows are zero.  Before the duality gap every rank assembles the full ergodic
-// averages and final dual by a sum over ranks, with the replicated rows (trunk edges
-// and the root's x_avg) counted on rank 0 only: exact, each entry has one
-// non-zero contributor.
-__global__ void zero_trunk_rows_kernel(const int* te, int T, int E, int NXP, int NUP, double* xavg, double* uavg,
-                                       double* y) {
+// Shard plans hold the rows of their own chains, of the trunk positions with
+// only their chains below, and of the mixed (replicated) trunk positions; the other
+// rows hold zeros or a warm start.  Before the duality gap every rank assembles the
+// full ergodic averages and final dual by a sum over ranks, after zeroing the rows
+// it does not count (another rank's; mixed rows and the root's x_avg on ranks != 0):
+// exact, each entry has one non-zero contributor.
+__global__ void zero_rows_kernel(const int* rows, int n, bool root, int E, int NXP, int NUP, double* xavg,
+                                 double* uavg, double* y) {
   const int b = blockIdx.x;
-  if (b == T) {
-    for (int i = threadIdx.x; i < NXP; i += blockDim.x) xavg[i] = 0.0;
+  if (b == n) {
+    if (root)
+      for (int i = threadIdx.x; i < NXP; i += blockDim.x) xavg[i] = 0.0;
     return;
   }
-  const size_t e = (size_t)te[b];
+  const size_t e = (size_t)rows[b];
   for (int i = threadIdx.x; i < NXP; i += blockDim.x) {
     xavg[(e + 1) * NXP + i] = 0.0;
     y[e * NXP + i] = 0.0;
@@ -1497,14 +1536,15 @@ __global__ void zero_trunk_rows_kernel(const int* te, int T, int E, int NXP, int
 }
 
 int zero_replicated_rows(tsmpc_plan* pl, double* yfin, cudaStream_t s) {
-  const int T = (int)pl->trunk_edges.size();
-  zero_trunk_rows_kernel<<<T + 1, 128, 0, s>>>(pl->d_trunk, T, pl->E, pl->NXP, pl->NUP, pl->XAVG, pl->UAVG, yfin);
+  const int n = (int)pl->zero_edges.size();
+  zero_rows_kernel<<<n + 1, 128, 0, s>>>(pl->d_zero, n, pl->rank != 0, pl->E, pl->NXP, pl->NUP, pl->XAVG, pl->UAVG,
+                                         yfin);
   CU(cudaGetLastError());
   return TSMPC_OK;
 }
 
 int assemble_shard_state(tsmpc_plan* pl, double* yfin) {
-  if (pl->rank != 0 && zero_replicated_rows(pl, yfin, pl->stream)) return TSMPC_ERR_CUDA;
+  if (zero_replicated_rows(pl, yfin, pl->stream)) return TSMPC_ERR_CUDA;
   const size_t yblk = 2 * (size_t)pl->E * pl->NXP + (size_t)pl->E * pl->NUP;
   struct { double* p; size_t n; } bufs[] = {{pl->XAVG, (size_t)pl->n_nodes * pl->NXP},
                                             {pl->UAVG, (size_t)pl->E * pl->NUP}, {yfin, yblk}};
@@ -1650,17 +1690,18 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
       CU(sparse_launch(S, LaunchWin{0, iters, 3, 0}, pl->sp_ctas, pl->sp_smem, pl->stream));
       ++pl->launches;
     } else {
-      // per iteration: phase 1 (backward + head pre-reduction), the cross-GPU sum of
-      // the per-trunk-node head sums, phase 2 (trunk sweep, needs, forward, epilogue).
+      // per iteration: phase 1 (backward, head pre-reduction, the bottom-up sums below
+      // the cut), the cross-GPU sum of the cut exchange rows XCH, phase 2 (trunk
+      // sweep above the cut, needs, forward, epilogue).
       // With a communicator the 2 x iters launches and the all-reduces are captured
       // once per iteration count into a CUDA graph and replayed (the launch windows
       // are kernel arguments; the plan's parameters are uploaded before each replay)
-      const size_t hs = (size_t)std::max(1, pl->sp_trunk) * S.HS_LD;
+      const size_t xn = (size_t)S.n_xch * S.XCH_LD;
       auto issue = [&]() -> int {
         for (int nu = 0; nu < iters; ++nu) {
           CU(sparse_launch(S, LaunchWin{nu, nu + 1, 1, 0}, pl->sp_ctas, pl->sp_smem, pl->stream));
-          if (pl->sp_trunk > 0 && pl->comm) {
-            const int nr = pl->nccl->AllReduce(pl->HS, pl->HS, hs, NcclApi::kFloat64, NcclApi::kSum, pl->comm,
+          if (pl->sp_trunk > 0 && pl->comm && xn > 0) {
+            const int nr = pl->nccl->AllReduce(pl->XCH, pl->XCH, xn, NcclApi::kFloat64, NcclApi::kSum, pl->comm,
                                                pl->stream);
             if (nr != 0) return fail(TSMPC_ERR_NCCL, "ncclAllReduce: %s", pl->nccl->GetErrorString(nr));
           }
@@ -1756,7 +1797,7 @@ int tsmpc_solve_group(tsmpc_plan* const* plans, int32_t n, const double* p, int3
     if (!pl->sharded || pl->comm || pl->world != n || pl->rank != r)
       return fail(TSMPC_ERR_VALIDATION, "group member %d must be the local shard plan of rank %d of %d", r, r, n);
     if (pl->device != plans[0]->device || pl->sp_trunk != plans[0]->sp_trunk ||
-        pl->sbase.HS_LD != plans[0]->sbase.HS_LD || pl->E != plans[0]->E)
+        pl->sbase.n_xch != plans[0]->sbase.n_xch || pl->E != plans[0]->E)
       return fail(TSMPC_ERR_VALIDATION, "group members must be shards of one tree on one device");
   }
   CU(cudaSetDevice(plans[0]->device));
@@ -1777,16 +1818,16 @@ int tsmpc_solve_group(tsmpc_plan* const* plans, int32_t n, const double* p, int3
     int rc = solve_prepare(plans[r], p, iters, lam, nullptr, nullptr, nullptr, theta, coef, flags, st[r]);
     if (rc) return rc;
     S[r] = sparse_params(plans[r], st[r].P);
-    g.hs[r] = plans[r]->HS;
+    g.hs[r] = plans[r]->XCH;
     g.res[r] = plans[r]->RESID;
     CU(cudaEventRecord(plans[r]->ev0, s0));
   }
-  const size_t hs = (size_t)std::max(1, plans[0]->sp_trunk) * plans[0]->sbase.HS_LD;
+  const size_t hs = (size_t)S[0].n_xch * S[0].XCH_LD;
   for (int nu = 0; nu < iters; ++nu) {
     for (int r = 0; r < n; ++r) {
       CU(sparse_launch(S[r], LaunchWin{nu, nu + 1, 1, 0}, plans[r]->sp_ctas, plans[r]->sp_smem, s0));
     }
-    if (plans[0]->sp_trunk > 0) {
+    if (plans[0]->sp_trunk > 0 && hs > 0) {
       group_sum_kernel<<<(unsigned)std::min<size_t>(256, (hs + 255) / 256), 256, 0, s0>>>(g, n, hs);
       CU(cudaGetLastError());
     }
@@ -1806,7 +1847,7 @@ int tsmpc_solve_group(tsmpc_plan* const* plans, int32_t n, const double* p, int3
     GroupBufs gx{}, gu{}, gy{};
     for (int r = 0; r < n; ++r) {
       double* yfin = (iters & 1) == 0 ? plans[r]->Y0 : plans[r]->Y1;
-      if (r > 0 && zero_replicated_rows(plans[r], yfin, s0)) return TSMPC_ERR_CUDA;
+      if (zero_replicated_rows(plans[r], yfin, s0)) return TSMPC_ERR_CUDA;
       gx.hs[r] = plans[r]->XAVG;
       gu.hs[r] = plans[r]->UAVG;
       gy.hs[r] = yfin;
@@ -2035,16 +2076,16 @@ int tsmpc_solve_multi(tsmpc_plan* const* plans, int32_t n, const double* p, int3
   auto nccl = [&](int nr) -> int {
     return nr == 0 ? TSMPC_OK : fail(TSMPC_ERR_NCCL, "NCCL: %s", api->GetErrorString(nr));
   };
-  const size_t hs = (size_t)std::max(1, plans[0]->sp_trunk) * S[0].HS_LD;
+  const size_t hs = (size_t)S[0].n_xch * S[0].XCH_LD;
   for (int nu = 0; nu < iters; ++nu) {
     for (int r = 0; r < n; ++r) {
       CU(cudaSetDevice(plans[r]->device));
       CU(sparse_launch(S[r], LaunchWin{nu, nu + 1, 1, 0}, plans[r]->sp_ctas, plans[r]->sp_smem, plans[r]->stream));
     }
-    if (plans[0]->sp_trunk > 0) {
+    if (plans[0]->sp_trunk > 0 && hs > 0) {
       if (nccl(api->GroupStart())) return TSMPC_ERR_NCCL;
       for (int r = 0; r < n; ++r)
-        if (nccl(api->AllReduce(plans[r]->HS, plans[r]->HS, hs, NcclApi::kFloat64, NcclApi::kSum, plans[r]->comm,
+        if (nccl(api->AllReduce(plans[r]->XCH, plans[r]->XCH, hs, NcclApi::kFloat64, NcclApi::kSum, plans[r]->comm,
                                 plans[r]->stream)))
           return TSMPC_ERR_NCCL;
       if (nccl(api->GroupEnd())) return TSMPC_ERR_NCCL;
@@ -2068,8 +2109,8 @@ int tsmpc_solve_multi(tsmpc_plan* const* plans, int32_t n, const double* p, int3
   }
   const bool gap = !(flags & TSMPC_SKIP_GAP);
   if (gap) {
-    // the full averages and final dual on every GPU (replicated rows counted on rank 0)
-    for (int r = 1; r < n; ++r) {
+    // the full averages and final dual on every GPU (each row counted once)
+    for (int r = 0; r < n; ++r) {
       CU(cudaSetDevice(plans[r]->device));
       double* yfin = (iters & 1) == 0 ? plans[r]->Y0 : plans[r]->Y1;
       if (zero_replicated_rows(plans[r], yfin, plans[r]->stream)) return TSMPC_ERR_CUDA;

@@ -119,6 +119,12 @@ constexpr int kWarpsS = kThreadsS / 32;
 constexpr int kTileS = 24;         // rows per chain tile (a leaf chain never spans tiles)
 constexpr int kMinTrunkCtas = 8;   // split mode needs at least this many spare CTAs for the trunk
 constexpr int kTileW = 96;         // rows per wide tile (a leaf chain never spans tiles)
+// shard plans: role of a trunk position on this rank (trunk schedule pos[8 tp + 7] & 7;
+// (pos[8 tp + 7] >> 3) - 1 is its row in the cut exchange buffer XCH, -1 if none).
+// Own / foreign: every chain below it belongs to this / another rank; mixed: chains
+// of several ranks (replicated: every rank computes it); cut: a single-rank position
+// whose parent is mixed (its bottom-up sums cross the cut).
+constexpr int kRoleOwn = 0, kRoleForeign = 1, kRoleMixed = 2, kRoleCutOwn = 3, kRoleCutForeign = 4;
 
 struct SParams {
   Params P;                     // dims, model vectors, scaling, tree, state, loop control, KY
@@ -161,6 +167,16 @@ struct SParams {
   double* HS;                   // T x HS_LD
   int HS_LD;                    // NVP + NXP
   const unsigned char* towned;  // T: this rank owns the heads of the node below
+  // cut exchange (world > 1): instead of HS for every trunk position, the ranks sum
+  // only XCH (n_xch x XCH_LD): the head sums of the mixed positions and the bottom-up
+  // sums [Z in KY columns | X] of the cut positions, written by their owning rank at
+  // the end of phase 1 (zero on the others; exact).  Positions foreign to this rank
+  // are skipped by the sweep, the trunk forward and the epilogues.
+  // cut == 0 (small trunks): every position is mixed, XCH is HS itself (HS_LD wide)
+  // and holds every position's head sums.
+  double* XCH;
+  int n_xch, XCH_LD;            // XCH_LD = KY_LD + NXP (cut) or HS_LD
+  int cut;
   // split mode (single GPU, one tile per chain CTA, spare CTAs): CTAs >= split_c0
   // ("trunk CTAs") run the trunk sweep, then -- after a barrier among themselves --
   // the trunk forward of their trunk rows, exporting per trunk position

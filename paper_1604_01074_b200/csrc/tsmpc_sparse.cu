@@ -968,6 +968,11 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur, int part) {
   // part 1: own terms (no chain heads needed: run while waiting for them);
   // part 2: chain-head sums, levels, KY; part 3: both.  Each (edge, component)
   // element stays with the same thread across the parts.
+  // Shard plans with a cut (S.n_xch > 0): part 5 (end of phase 1) runs the bottom-up
+  // sums of the positions below the cut that this rank owns and exports the cut
+  // positions' sums and the mixed positions' head sums to XCH; part 3 (phase 2, after
+  // the cross-rank sum of XCH) imports the other ranks' cut sums instead of
+  // computing them.  Positions foreign to this rank are skipped throughout.
   const SParams& S = g_sp;
   const Ctx c = ctx_of();
   const Params& P = S.P;
@@ -1015,9 +1020,11 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur, int part) {
     for (int idx = threadIdx.x; idx < T * nc; idx += kThreadsS) {
       const int tp = idx / nc, k = idx - tp * nc, q = c_lo + k;
       const int* ps = pos + 8 * tp;
-      const int a = ps[0], st = ps[1];
+      const int a = ps[0], st = ps[1], rl = ps[7] & 7;
       double z = 0.0, x = 0.0;
-      if (q < c.nv) {
+      if (rl == kRoleForeign || rl == kRoleCutForeign) {
+        // another rank's subtree
+      } else if (q < c.nv) {
         z = ldcg(S.beta_s + (size_t)a * c.NVP + q);
       } else if (q < c.nv + c.nx) {
         const int i = q - c.nv;
@@ -1036,17 +1043,32 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur, int part) {
       Xs[idx] = x;
     }
   }
-  if (!(part & 2)) return;
+  if (!(part & 6)) return;
   if (part & 1) __syncthreads();  // the steps below map elements to threads differently
+  const bool exporting = part & 4;
+  auto kycol = [&](int q) {
+    return q < c.nv ? q : (q < c.nv + c.nx ? c.NVP + (q - c.nv) : c.NVP + c.NXP + (q - c.nv - c.nx));
+  };
   // per (trunk position, component) steps of the recursion
   auto heads = [&](int tp, int k) {  // (1b) chain-head children, childless fold
     const int q = c_lo + k, idx = tp * nc + k;
     const int* ps = pos + 8 * tp;
-    const int h0 = ps[5], nh = ps[6];
+    const int h0 = ps[5], nh = ps[6], rl = ps[7] & 7;
+    if (rl == kRoleForeign || (rl == kRoleMixed && exporting)) return;
+    if (rl == kRoleCutForeign) {  // another rank's bottom-up sums (phase 2)
+      if (!exporting) {
+        const double* xr = S.XCH + (size_t)((ps[7] >> 3) - 1) * S.XCH_LD;
+        Zs[idx] = ldcg(xr + kycol(q));
+        Xs[idx] = q >= c.nv && q < c.nv + c.nx ? ldcg(xr + P.KY_LD + (q - c.nv)) : 0.0;
+      }
+      return;
+    }
+    // chain-head sums: this rank's (HS), or all ranks' for a mixed position (XCH)
+    const double* hs = rl == kRoleMixed ? S.XCH + (size_t)((ps[7] >> 3) - 1) * S.XCH_LD : S.HS + (size_t)tp * S.HS_LD;
     double z = Zs[idx], x = Xs[idx];
     if (q < c.nv) {
       if (S.sharded) {
-        if (nh > 0) z = __dadd_rn(z, ldcg(S.HS + (size_t)tp * S.HS_LD + q));
+        if (nh > 0) z = __dadd_rn(z, ldcg(hs + q));
       } else {
 #pragma unroll 1
         for (int m0 = 0; m0 < nh; m0 += kCh) {  // loads of a chunk in flight together
@@ -1062,7 +1084,7 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur, int part) {
       const int i = q - c.nv;
       double h = 0.0;
       if (S.sharded) {
-        if (nh > 0) h = ldcg(S.HS + (size_t)tp * S.HS_LD + c.NVP + i);
+        if (nh > 0) h = ldcg(hs + c.NVP + i);
       } else {
 #pragma unroll 1
         for (int m0 = 0; m0 < nh; m0 += kCh) {
@@ -1090,7 +1112,8 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur, int part) {
   auto up = [&](int tp, int k, int l) {  // (2) add trunk children; level 0 also scales
     const int q = c_lo + k, idx = tp * nc + k;
     const int* ps = pos + 8 * tp;
-    const int c0 = ps[3], n = ps[4];
+    const int c0 = ps[3], n = ps[4], rl = ps[7] & 7;
+    if (rl == kRoleForeign || rl == kRoleCutForeign || (rl == kRoleMixed && exporting)) return;
     double zs = 0.0, xs = 0.0;
 #pragma unroll 1
     for (int m = 0; m < n; ++m) {
@@ -1108,7 +1131,12 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur, int part) {
     }
     Zs[idx] = l == 0 ? __dmul_rn(zn, Ip[tp]) : zn;
   };
+  auto foreign = [&](int tp) {
+    const int rl = pos[8 * tp + 7] & 7;
+    return rl == kRoleForeign || rl == kRoleCutForeign;
+  };
   auto down = [&](int tp, int k) {  // (3) K_a, Y_a = own * inv2p_a + parent's
+    if (foreign(tp)) return;
     const int idx = tp * nc + k;
     const int pp = pos[8 * tp + 2];
     double v = __dmul_rn(Zs[idx], Ip[tp]);
@@ -1116,9 +1144,8 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur, int part) {
     Zs[idx] = v;
   };
   auto store = [&](int tp, int k) {  // (4) KY column
-    const int q = c_lo + k;
-    const int col = q < c.nv ? q : (q < c.nv + c.nx ? c.NVP + (q - c.nv) : c.NVP + c.NXP + (q - c.nv - c.nx));
-    stcg(P.KY + (size_t)tp * P.KY_LD + col, Zs[tp * nc + k]);
+    if (foreign(tp)) return;
+    stcg(P.KY + (size_t)tp * P.KY_LD + kycol(c_lo + k), Zs[tp * nc + k]);
   };
 #pragma unroll 1
   for (int idx = threadIdx.x; idx < T * nc; idx += kThreadsS) heads(idx / nc, idx % nc);
@@ -1154,6 +1181,27 @@ __device__ __noinline__ void trunk_sweep(double cf, int cur, int part) {
 #pragma unroll 1
     for (int idx = lev[l] * nc + threadIdx.x; idx < lev[l + 1] * nc; idx += kThreadsS) up(idx / nc, idx % nc, l);
     __syncthreads();
+  }
+  if (exporting) {
+    // every exchange row of this CTA's components: this rank's cut sums [Z | X] and
+    // mixed-position head sums, zero where another rank contributes
+#pragma unroll 1
+    for (int idx = threadIdx.x; idx < T * nc; idx += kThreadsS) {
+      const int tp = idx / nc, k = idx - tp * nc, q = c_lo + k;
+      const int code = pos[8 * tp + 7], rl = code & 7;
+      if ((code >> 3) == 0) continue;
+      double* xr = S.XCH + (size_t)((code >> 3) - 1) * S.XCH_LD;
+      double z = 0.0, x = 0.0;
+      if (rl == kRoleCutOwn) {
+        z = Zs[idx];
+        x = Xs[idx];
+      } else if (rl == kRoleMixed && q < c.nv + c.nx && S.towned[tp]) {
+        z = ldcg(S.HS + (size_t)tp * S.HS_LD + (q < c.nv ? q : c.NVP + (q - c.nv)));
+      }
+      if (rl != kRoleMixed || q < c.nv + c.nx) stcg(xr + kycol(q), z);
+      if (rl != kRoleMixed && q >= c.nv && q < c.nv + c.nx) stcg(xr + P.KY_LD + (q - c.nv), x);
+    }
+    return;
   }
 #pragma unroll 1
   for (int l = nlev >= 2 ? 1 : 0; l < nlev; ++l) {
@@ -2476,6 +2524,10 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel(LaunchWin win)
       if (S.sharded && trunk) {
         grid.sync();
         head_prereduce();
+        if (S.cut && S.n_xch > 0) {  // the cut: this rank's sums that cross it -> XCH
+          grid.sync();
+          trunk_sweep(cf, cur, 5);
+        }
       }
     }
     if (do_b && trunk && S.split && S.split_flags) {
@@ -2704,6 +2756,10 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
       if (S.sharded && trunk) {
         grid.sync();
         head_prereduce();
+        if (S.cut && S.n_xch > 0) {  // the cut: this rank's sums that cross it -> XCH
+          grid.sync();
+          trunk_sweep(cf, cur, 5);
+        }
       }
     }
     if (do_b && trunk && S.split) {

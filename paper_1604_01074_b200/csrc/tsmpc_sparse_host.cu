@@ -95,6 +95,8 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
   out.total_chains = (int)chains.size();
   // ---- sharding: groups of chains hanging from the same node, split contiguously
   out.towned.assign(T, 1);
+  out.trole.assign(T, kRoleOwn);
+  out.txrow.assign(T, -1);
   if (sharded && world > 1) {
     std::vector<int> gnode;             // group -> parent node
     std::vector<long long> grows;       // group -> rows
@@ -124,6 +126,37 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
     for (int tp = 0; tp < T; ++tp) out.towned[tp] = 0;
     for (size_t gi = 0; gi < gnode.size(); ++gi)
       if (gowner[gi] == rank && gnode[gi] > 0 && tpos[gnode[gi] - 1] >= 0) out.towned[tpos[gnode[gi] - 1]] = 1;
+    // the cut: ranks owning chains below each trunk position
+    std::vector<int> towner(T, -2);  // -2: none yet, -1: several ranks
+    for (size_t i = 0; i < chains.size(); ++i) {
+      const int g = gowner[group_of[i]];
+      for (int e = (int)t.anc[chains[i][0] + 1] - 1; e >= 0; e = (int)t.anc[e + 1] - 1) {
+        int& o = towner[tpos[e]];
+        o = (o == -2 || o == g) ? g : -1;
+      }
+    }
+    std::vector<int> xrow(T, -1);
+    for (int tp = 0; tp < T; ++tp) {
+      const int pa = (int)t.anc[out.trunk_edge[tp] + 1] - 1;
+      const bool cut = pa >= 0 && towner[tpos[pa]] < 0;
+      if (towner[tp] < 0) out.trole[tp] = kRoleMixed;
+      else if (towner[tp] == rank) out.trole[tp] = cut ? kRoleCutOwn : kRoleOwn;
+      else out.trole[tp] = cut ? kRoleCutForeign : kRoleForeign;
+      if (towner[tp] < 0 || cut) xrow[tp] = out.n_xch++;
+    }
+    out.txrow = xrow;
+    out.cut = true;
+    // small trunks (SMPC3 on 8 ranks: 32 cut rows of 344 doubles vs 37 x 164 head
+    // sums): replicate the whole trunk and exchange every position's head sums
+    if ((long long)out.n_xch * (NVP + 2 * NXP + NUP) >= (long long)T * (NVP + NXP) ||
+        std::getenv("TSMPC_SHARD_FULL")) {
+      out.cut = false;
+      out.n_xch = T;
+      for (int tp = 0; tp < T; ++tp) {
+        out.trole[tp] = kRoleMixed;
+        out.txrow[tp] = tp;
+      }
+    }
     chains.swap(kept);
   }
   out.n_chains = (int)chains.size();
@@ -132,6 +165,10 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
     out.owned_edges.insert(out.owned_edges.end(), ch.begin(), ch.end());
   }
   std::sort(out.owned_edges.begin(), out.owned_edges.end());
+  out.result_edges = out.owned_edges;
+  for (int tp = 0; tp < T; ++tp)
+    if (out.trole[tp] != kRoleForeign && out.trole[tp] != kRoleCutForeign) out.result_edges.push_back(out.trunk_edge[tp]);
+  std::sort(out.result_edges.begin(), out.result_edges.end());
 
   // ---- split mode: a CTA per chain, the trunk on split_n further CTAs
   int split_n = 0;
@@ -222,6 +259,7 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
     const int cap_rows = (T + C - 1) / std::max(C, 1) + 1;
     std::vector<int> path;
     for (int tp = 0; tp < T; ++tp) {
+      if (out.trole[tp] == kRoleForeign || out.trole[tp] == kRoleCutForeign) continue;  // another rank's
       path.clear();
       for (int e = out.trunk_edge[tp]; e >= 0; e = (int)t.anc[e + 1] - 1) path.push_back(tpos[e]);
       int best = -1, best_add = 0;
@@ -273,6 +311,7 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
       }
       p[4] = (int)tch.size() - p[3];
       p[6] = (int)hch.size() - p[5];
+      p[7] = out.trole[tp] | ((out.txrow[tp] + 1) << 3);
     }
     out.tsched = {T, nlev, (int)tch.size(), (int)hch.size()};
     if (T == 0) out.tsched[1] = 0;

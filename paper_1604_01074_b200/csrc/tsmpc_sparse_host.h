@@ -46,6 +46,15 @@ struct SparseHostPlan {
   int rank = 0, world = 1, owned_rows = 0, total_chains = 0;
   std::vector<unsigned char> towned;
   std::vector<int> owned_edges;     // edges of the owned chains (ascending)
+  // cut exchange (world > 1): role of every trunk position on this rank (kRole*,
+  // tsmpc_kernels.cuh) and the rows of the per-iteration exchange buffer: one per
+  // mixed position (its chain-head sums) and one per cut position (a single-rank
+  // subtree hanging from a mixed position: its bottom-up sums)
+  std::vector<signed char> trole;
+  std::vector<int> txrow;           // exchange row of each trunk position, -1 if none
+  int n_xch = 0;
+  bool cut = false;                 // false: whole trunk replicated, XCH = every position's head sums
+  std::vector<int> result_edges;    // edges whose rows this rank computes (chains + own / mixed trunk)
   // filled layout / pool offsets (device pointers are set by the caller)
   SParams S{};
 };

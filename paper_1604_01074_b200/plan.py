@@ -372,7 +372,9 @@ def describe_sparse(model, tree, factor, max_ctas: int = 148, smem_limit: int = 
 
 def describe_shard(model, tree, factor, rank: int, world: int, max_ctas: int = 148,
                    smem_limit: int = 232448) -> dict:
-    """Host-only view of one shard of the structured-basis plan (no GPU needed)."""
+    """Host-only view of one shard of the structured-basis plan (no GPU needed):
+    the chain partition, the trunk positions this rank computes, and the size of
+    the per-iteration cut exchange."""
     from .precompute import structured_basis
     lib = nat.load_library()
     sb = structured_basis(model, _BasisView(factor.L))
@@ -386,14 +388,15 @@ def describe_shard(model, tree, factor, rank: int, world: int, max_ctas: int = 1
     for name, arr in keep.items():
         setattr(pb, name, nat.iptr(arr) if arr.dtype == np.int64 else nat.dptr(arr))
     keys = ("ctas", "owned_chains", "owned_rows", "trunk_edges", "total_chains",
-            "owned_trunk_nodes", "smem_bytes")
+            "owned_trunk_nodes", "smem_bytes", "own_trunk_positions", "mixed_positions",
+            "cut_positions", "exchange_rows", "exchange_doubles", "result_rows")
     buf = np.zeros(len(keys), dtype=np.int64)
     edges = np.zeros(max(1, tree.n_edges), dtype=np.int64)
     nat.check(lib.tsmpc_describe_shard(ctypes.byref(pb), int(max_ctas), int(smem_limit), int(rank),
                                        int(world), nat.iptr(buf), len(keys), nat.iptr(edges),
                                        tree.n_edges), "tsmpc_describe_shard")
     d = dict(zip(keys, (int(v) for v in buf)))
-    d["edges"] = edges[:d["owned_rows"]]
+    d["edges"] = edges[:d["result_rows"]]  # rows this shard computes: its chains, own + mixed trunk
     return d
 
 

@@ -5,20 +5,27 @@ host-side rendezvous).  The reference has no multi-process layer — its only
 parallelism is the per-stage thread pool (``pkg/src/treesmpc/_parallel.py``,
 ``factor.py:107-128``); this module is the node-level equivalent:
 
-* the trunk (every edge above the leaf chains) is replicated on every rank,
-* the leaf chains are split by the trunk node they hang from, so every
-  chain-head sum of a trunk node has exactly one owning rank,
-* each APG iteration runs phase 1 (backward over the owned chains + per-node
-  head sums) -> one ``ncclAllReduce`` of T x (n_v + n_x) doubles -> phase 2
-  (replicated trunk sweep, forward, prox / dual update) inside ``libtsmpc``.
+* the leaf chains are split by the trunk node they hang from (all chains of a
+  node go to one rank), contiguously, balanced by rows;
+* a trunk position with only one rank's chains below is computed by that rank
+  alone; the positions with several ranks' chains below ("mixed": the top of
+  the tree, the root edge alone for W4k on 2/4/8 GPUs) are replicated;
+* each APG iteration runs phase 1 (backward over the owned chains, the
+  bottom-up sums of the owned subtrees) -> one ``ncclAllReduce`` of the sums
+  that cross the cut (per cut position -- a single-rank subtree hanging from a
+  mixed position -- its bottom-up sums, per mixed position its chain-head sums:
+  33 rows of 344 doubles for W4k instead of every trunk node's head sums) ->
+  phase 2 (the sweep above the cut, forward, prox / dual update) inside
+  ``libtsmpc``.
 
-The cross-rank sum is exact (one non-zero contributor per entry), so a shard
-solve reproduces the single-GPU iterates up to the summation order of the
-chain-head sums (ulp level).  The duality gap (engine.py:458-480) is evaluated
-after the loop: every rank assembles the full ergodic averages and final dual by
-an all-reduce sum (replicated trunk rows counted on rank 0 only; exact) and
-evaluates the same gap as a single-GPU plan.  With a communicator the
-2 x iters launches and all-reduces are replayed from a CUDA graph.
+The cross-rank sum is exact (one non-zero contributor per entry) and the sums
+above the cut see the cut positions' values in node order, so a shard solve
+reproduces the single-GPU iterates up to the summation order of the chain-head
+sums (ulp level).  The duality gap (engine.py:458-480) is evaluated after the
+loop: every rank assembles the full ergodic averages and final dual by an
+all-reduce sum (each row counted by one rank; exact) and evaluates the same gap
+as a single-GPU plan.  With a communicator the 2 x iters launches and
+all-reduces are replayed from a CUDA graph.
 """
 
 from __future__ import annotations
@@ -74,7 +81,7 @@ class ShardedSolver:
 class LocalShardGroup:
     """All ``world`` shards of one tree on ONE device, solved in lockstep in one
     process (``tsmpc_solve_group``): per iteration phase 1 of every shard, an
-    in-place device sum of their head-sum buffers (the exchange the NCCL
+    in-place device sum of their cut exchange rows (the exchange the NCCL
     all-reduce performs across GPUs), phase 2 of every shard.  It runs exactly
     the per-rank kernels of a ``world``-GPU job, so the multi-rank split is
     checked on one GPU; the kernels of different shards never wait on each other.

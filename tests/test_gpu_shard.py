@@ -103,7 +103,7 @@ def test_shard_group_matches_reference(name, world):
     assert abs(full["residual_inf"] - r_ref) <= c.tol("residual_inf") * max(1.0, abs(r_ref))
 
 
-@pytest.mark.parametrize("tree_name,world", [("SMPC3", 2), ("SMPC3", 8), ("SMPC8", 4)])
+@pytest.mark.parametrize("tree_name,world", [("SMPC3", 2), ("SMPC3", 8), ("SMPC8", 3), ("SMPC8", 4), ("W4k", 8)])
 def test_shard_group_matches_single_plan_paper_trees(tree_name, world):
     """Full-size paper trees: the w-way split reproduces the single-GPU plan's
     iterates to within the summation order of the chain-head sums."""

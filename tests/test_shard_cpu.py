@@ -74,10 +74,12 @@ def test_two_rank_partition_and_gather(tree_name):
     assert all(r[1] for r in res)                         # one NCCL id, 128 bytes, on every rank
     parts = res[0][2]
     owned = [set(pt) for pt in parts]
-    assert not (owned[0] & owned[1])                       # disjoint chain ownership
     t = synth.paper_tree(*synth.PAPER_TREES[tree_name])
     d0, d1 = res[0][3], res[1][3]
-    assert len(owned[0]) + len(owned[1]) + d0["trunk_edges"] == t.n_edges
+    # every row computed by one rank, except the mixed (replicated) trunk positions
+    assert owned[0] | owned[1] == set(range(t.n_edges))
+    assert len(owned[0] & owned[1]) == d0["mixed_positions"] == d1["mixed_positions"] >= 1
+    assert d0["owned_rows"] + d1["owned_rows"] + d0["trunk_edges"] == t.n_edges
     assert d0["owned_chains"] + d1["owned_chains"] == d0["total_chains"]
     assert d0["owned_trunk_nodes"] + d1["owned_trunk_nodes"] <= d0["trunk_edges"]
     # balanced up to one group of sibling chains (SMPC1: 3 groups of 2 chains)
@@ -89,16 +91,50 @@ def test_shard_partition_world8_heads_grouped():
     m = synth.bcn63_network()
     f = factor_step(compute_basis(m), m)
     t = synth.paper_tree(*synth.PAPER_TREES["SMPC8"])
-    owner = {}
+    owner, mixed = {}, set()
     for r in range(8):
         d = describe_shard(m, t, f, r, 8)
         for e in d["edges"]:
-            assert e not in owner
+            if int(e) in owner:
+                mixed.add(int(e))
             owner[int(e)] = r
+        assert d["mixed_positions"] == len(mixed) or r < 7
+    assert len(owner) == t.n_edges
+    for e in mixed:                                       # replicated rows are trunk edges
+        pn = int(t.anc[e + 1])
+        assert int(t.child_stop[e + 1] - t.child_start[e + 1]) > 1 or pn == 0
     # all chain heads hanging from one node are owned by one rank
     heads_by_node = {}
     for e in owner:
         pn = int(t.anc[e + 1])
-        if int(t.child_stop[pn] - t.child_start[pn]) != 1:   # e is a chain head
+        chain = int(t.child_stop[e + 1] - t.child_start[e + 1]) <= 1
+        if chain and int(t.child_stop[pn] - t.child_start[pn]) != 1:   # e is a chain head
             heads_by_node.setdefault(pn, set()).add(owner[e])
     assert heads_by_node and all(len(v) == 1 for v in heads_by_node.values())
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_cut_exchange_w4k(world):
+    """only sums that cross the cut are exchanged.  W4k [32,16,8]: the
+    root edge is the only position with several ranks' chains below when world
+    divides 32 (cut: the 32 stage-2 edges); otherwise a split stage-2 subtree adds
+    its edge to the mixed set and its stage-3 edges to the cut."""
+    m = synth.bcn63_network()
+    f = factor_step(compute_basis(m), m)
+    t = synth.paper_tree(*synth.PAPER_TREES["W4k"])
+    ds = [describe_shard(m, t, f, r, world) for r in range(world)]
+    d0 = ds[0]
+    assert all(d["exchange_rows"] == d0["exchange_rows"] for d in ds)
+    assert d0["exchange_rows"] == d0["mixed_positions"] + d0["cut_positions"]
+    if 32 % world == 0:
+        assert (d0["mixed_positions"], d0["cut_positions"]) == (1, 32)
+    else:
+        assert 1 < d0["mixed_positions"] <= world and d0["cut_positions"] > 32
+    # vs every trunk position's head sums (T x (n_v + n_x) doubles)
+    assert d0["exchange_doubles"] * (7 if 32 % world == 0 else 3) < d0["trunk_edges"] * (100 + 64)
+    # the trunk rows are shared out: own positions are disjoint, mixed are replicated
+    own = sum(d["own_trunk_positions"] for d in ds)
+    assert own + d0["mixed_positions"] == d0["trunk_edges"]
+    rows = [set(map(int, d["edges"])) for d in ds]
+    assert set().union(*rows) == set(range(t.n_edges))
+    assert sum(len(r) for r in rows) == t.n_edges + (world - 1) * d0["mixed_positions"]
