@@ -293,6 +293,10 @@ def run_ours(args, ws, rank, local):
             line["sharded_one_rank"] = sharded_measure(args, 1, 0, local, None)
         except Exception as exc:  # report, never lose the headline line over it
             line["sharded_one_rank"] = {"error": f"{type(exc).__name__}: {exc}"}
+        try:
+            line["sharded_per_rank_compute"] = sharded_estimate(args, local)
+        except Exception as exc:
+            line["sharded_per_rank_compute"] = {"error": f"{type(exc).__name__}: {exc}"}
     emit(line)
 
 
@@ -357,9 +361,10 @@ def _residual_target_one(local, g, gname, paper_weights):
 
 
 def sharded_measure(args, ws, rank, local, dist):
-    """BASELINE configs[3] on the ranks of this job: W4k split by subtree (trunk
-    replicated, chain groups per rank, one all-reduce of the chain-head sums per
-    iteration).  Device time of the loop, max over ranks."""
+    """BASELINE configs[3] on the ranks of this job: W4k split by subtree (chain
+    groups per rank, the trunk positions above them computed by their rank, the
+    top replicated, one all-reduce of the sums crossing that cut per iteration).
+    Device time of the loop, max over ranks."""
     import torch
     from paper_1604_01074_b200 import theta_schedule
     from paper_1604_01074_b200.plan import DevicePlan
@@ -394,8 +399,31 @@ def sharded_measure(args, ws, rank, local, dist):
             "hbm_frac_per_rank": E / ws * BYTES_PER_EDGE * args.iters / (loop / 1e3) / 1e9 / hbm_peak,
             "owned_chain_edges_rank0": info["owned_chain_edges"], "trunk_edges": info["trunk_edges"],
             "ctas": info["ctas"], "wide": info["wide"], "launches_per_iter": 2,
-            "exchange_bytes_per_iter": 8 * info["trunk_edges"] * (97 + 64),
+            "exchange_bytes_per_iter": 8 * info["exchange_doubles"],
             "step_size": lam}
+
+
+def sharded_estimate(args, local, worlds=(2, 4, 8)):
+    """No multi-GPU box: the per-rank compute of a w-GPU W4k solve, measured on
+    this GPU.  Every rank's shard plan runs its two launches per iteration
+    (tsmpc_plan_trial, without the cross-rank exchange); a w-GPU iteration costs
+    the slowest rank's time plus one all-reduce of `exchange_bytes_per_iter`."""
+    from paper_1604_01074_b200.plan import DevicePlan
+    W = build_workload(args.shard_tree)
+    out = {"tree": args.shard_tree, "iters": args.iters,
+           "note": "per-rank compute only (no NCCL on one GPU); not a multi-GPU measurement"}
+    for w in worlds:
+        us, xb = [], 0
+        for r in range(w):
+            plan = DevicePlan(W["model"], W["tree"], W["factor"], W["scaling"], device=local, shard=(r, w, None))
+            plan.set_cache(W["caches"][0], W["model"])
+            plan.trial(5)
+            us.append(min(plan.trial(args.iters) for _ in range(3)) * 1e3 / args.iters)
+            xb = 8 * plan.info()["exchange_doubles"]
+            del plan
+        out[f"w{w}"] = {"per_rank_us_per_iter": [round(u, 1) for u in us], "max_us_per_iter": round(max(us), 1),
+                        "exchange_bytes_per_iter": xb}
+    return out
 
 
 def sharded_headline(args, ws, rank, local, dist):
@@ -411,7 +439,7 @@ def sharded_headline(args, ws, rank, local, dist):
             "config": {"workload": workload_name(args.shard_tree, tree, args.iters),
                        "tree": args.shard_tree, "edges": tree.n_edges, "iters": args.iters,
                        "baseline_config": "BASELINE.json configs[3] (wide tree sharded by subtree)",
-                       "parallelism": f"subtree-sharded x{ws} (NCCL all-reduce of chain-head sums)"},
+                       "parallelism": f"subtree-sharded x{ws} (NCCL all-reduce of the cut sums)"},
             "roofline": {"bound": "hbm", "achieved": sh["hbm_frac_per_rank"] * hbm_peak, "peak": hbm_peak,
                          "unit": "GB/s", "frac": sh["hbm_frac_per_rank"], "traffic": None,
                          "kernel": "tsmpc::apg_wide_kernel (per rank)", "peak_source": peak_kind},

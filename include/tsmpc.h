@@ -207,7 +207,9 @@ int tsmpc_set_stopping(tsmpc_plan* plan, double tol, int32_t check_every);
  * plan's persistent kernel on whatever its buffers hold (zero right after
  * creation; the loop's cost does not depend on the data), CUDA-event time in *ms.
  * The Python layer uses it to pick the fastest of a few placements of a large
- * plan's buffers in device memory (plan.tuned_plan).  Single-GPU plans. */
+ * plan's buffers in device memory (plan.tuned_plan).  On a shard plan: this
+ * rank's two launches per iteration without the cross-rank exchange, i.e. the
+ * per-rank compute time of a multi-GPU solve (bench.py's sharded estimate). */
 int tsmpc_plan_trial(tsmpc_plan* plan, int32_t iters, double* ms);
 
 /* factor.solve_step: z = argmin <z, H'w> + f(z) for an unscaled dual w. */
@@ -232,7 +234,8 @@ int tsmpc_dual_operator_step(tsmpc_plan* plan, double* y_dot_dy, double* dy_dot_
 /* Introspection (tests / bench): info = {levels, ctas, tiles, segments,
  * smem_bytes, diag_A, threads, tile_rows, sms, collapsed, trunk_edges, sparse,
  * resident_ctas, sharded, rank, world, owned_chain_edges, total_chains,
- * trunk_ctas}. */
+ * trunk_ctas, wide, exchange_doubles (shard plans: the doubles every rank sums
+ * per iteration)}. */
 int tsmpc_plan_info(const tsmpc_plan* plan, int64_t* info, int32_t n_info);
 
 /* Host-only planning (no device needed): the segment / level / tile / trunk

@@ -1140,7 +1140,8 @@ int tsmpc_plan_info(const tsmpc_plan* pl, int64_t* info, int32_t n) {
                           sp ? kThreadsS : kThreads, sp ? pl->sbase.tile_cap : kTileM, pl->sm_count, pl->base.collapsed,
                           sp ? pl->sp_trunk : pl->n_trunk, sp ? 1 : 0, pl->sp_resident,
                           pl->sharded ? 1 : 0, pl->rank, pl->world, (int64_t)pl->owned_edges.size(),
-                          pl->total_chains, sp ? pl->sbase.split_n : 0, sp ? pl->sbase.wide : 0};
+                          pl->total_chains, sp ? pl->sbase.split_n : 0, sp ? pl->sbase.wide : 0,
+                          pl->sharded ? (int64_t)pl->sbase.n_xch * pl->sbase.XCH_LD : 0};
   for (int i = 0; i < n && i < (int)(sizeof(vals) / sizeof(vals[0])); ++i) info[i] = vals[i];
   return TSMPC_OK;
 }
@@ -1881,9 +1882,16 @@ int tsmpc_plan_trial(tsmpc_plan* pl, int32_t iters, double* ms) {
   pl->has_cache = had;
   pl->tol = tol;
   if (rc) return rc;
-  if (pl->sharded) return fail(TSMPC_ERR_VALIDATION, "timing trials are for single-GPU plans");
   CU(cudaEventRecord(pl->ev0, pl->stream));
-  if (pl->use_sparse) {
+  if (pl->sharded) {
+    // this rank's share of a sharded solve: its two launches per iteration,
+    // without the cross-rank exchange (the per-rank compute time of a w-GPU job)
+    SParams S = sparse_params(pl, st.P);
+    for (int nu = 0; nu < iters; ++nu) {
+      CU(sparse_launch(S, LaunchWin{nu, nu + 1, 1, 0}, pl->sp_ctas, pl->sp_smem, pl->stream));
+      CU(sparse_launch(S, LaunchWin{nu, nu + 1, 2, 0}, pl->sp_ctas, pl->sp_smem, pl->stream));
+    }
+  } else if (pl->use_sparse) {
     SParams S = sparse_params(pl, st.P);
     if (pl->SUBCTR) CU(cudaMemsetAsync(pl->SUBCTR, 0, 4 * sizeof(unsigned int), pl->stream));
     CU(sparse_launch(S, LaunchWin{0, iters, 3, 0}, pl->sp_ctas, pl->sp_smem, pl->stream));
