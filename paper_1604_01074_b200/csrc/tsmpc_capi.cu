@@ -664,7 +664,8 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
   const size_t yblk = 2 * (size_t)E * NXP + (size_t)E * NUP;
   {
     const char* pe = std::getenv("TSMPC_ARENA_PAD");
-    const size_t pad = pe ? (size_t)std::atoll(pe) : kArenaPad;  // bytes, skew per buffer
+    // bytes, skew per buffer (a multiple of 16: the epilogues use 16-byte accesses)
+    const size_t pad = ((pe ? (size_t)std::atoll(pe) : kArenaPad) + 15) / 16 * 16;
     const size_t sizes[] = {yblk, yblk, (size_t)n_nodes * NXP, (size_t)E * NUP, (size_t)E * NUP,
                             (size_t)E * NXP, (size_t)E * NVP};
     double** dst[] = {&pl->Y0, &pl->Y1, &pl->XAVG, &pl->UAVG, &pl->UHAT, &pl->EVEC, &pl->BETA_S};

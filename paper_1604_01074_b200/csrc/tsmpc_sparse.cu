@@ -1892,6 +1892,97 @@ __device__ __noinline__ void epi_state_wide_t(int nu_it, double cf, double th, i
 __device__ __forceinline__ bool epi_fast(const Params& P, int nu_it, bool pre) {
   return pre && !is_last(P, nu_it) && !P.record_all && P.scaled && g_sp.psi_smem;
 }
+
+#ifndef TSMPC_PSI2
+#define TSMPC_PSI2 1
+#endif
+// The steady-state psi epilogue (MODE 1 / 2 of epi_psi_wide_t) on component pairs:
+// 64-lane groups, 16-byte loads and stores of every array (half the memory
+// instructions and row look-ups), the same operations per element in the same
+// order (bitwise equal).  Needs even n_u and even shared-memory offsets.
+template <int MODE>
+__device__ __noinline__ void epi_psi_wide_v2(int nu_it, double cf, double th, int nrows, int cur, bool pre,
+                                             double cfn, int trb_o, int trl, int seg0) {
+  const SParams& S = g_sp;
+  const Ctx c = ctx_of();
+  const Params& P = S.P;
+  const EpiConst q = epi_const(P, nu_it, cf, th, true, cur ^ 1, pre, cfn);
+  constexpr int CH = 4, NG = kThreadsS / 64;
+  const int k = 2 * (threadIdx.x & 63), g = threadIdx.x >> 6;
+  if (k >= c.nu) return;
+  const double2 ulo = *reinterpret_cast<const double2*>(c.bnd + 3 * c.NXP + k);
+  const double2 uhi = *reinterpret_cast<const double2*>(c.bnd + 3 * c.NXP + c.NUP + k);
+  const size_t E = (size_t)c.E;
+  const double* Yc = P.ybuf[cur] + 2 * E * c.NXP + k;
+  double* Yn = P.ybuf[cur ^ 1] + 2 * E * c.NXP + k;
+  double* UA = P.uavg + k;
+  const int* rd = c.rdesc();
+  const int psio = c.psi_o + k;
+  auto one = [&](double yc, double yp, double ua, double uu, double dp, double lo, double hi, double& ny, double& na,
+                 double& fill) {
+    const double w = extrap(yc, yp, q.cf);
+    const double hp = __dmul_rn(uu, dp);
+    const double a = __dadd_rn(__dmul_rn(w, q.ilam), hp);
+    const double t = fmin(fmax(a, __dmul_rn(dp, lo)), __dmul_rn(dp, hi));
+    ny = __dadd_rn(w, __dmul_rn(q.lam, __dsub_rn(hp, t)));
+    na = __dadd_rn(__dmul_rn(ua, q.om), __dmul_rn(q.th, uu));
+    fill = __dmul_rn(extrap(ny, yc, q.cfn), dp);
+  };
+#pragma unroll 1
+  for (int r0 = g; r0 < nrows; r0 += CH * NG) {
+    double2 yc[CH], yp[CH], ua[CH];
+    int eo[CH];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const int r = r0 + u * NG;
+      eo[u] = 0;
+      yc[u] = yp[u] = ua[u] = make_double2(0.0, 0.0);
+      if (r < nrows) {
+        eo[u] = rd[5 * r] * c.NUP;
+        yc[u] = __ldcg(reinterpret_cast<const double2*>(Yc + eo[u]));
+        yp[u] = __ldcg(reinterpret_cast<const double2*>(Yn + eo[u]));
+        ua[u] = __ldcg(reinterpret_cast<const double2*>(UA + eo[u]));
+      }
+    }
+    auto elem = [&](int u, int r) {
+      const int* d = rd + 5 * r;
+      double2* us = reinterpret_cast<double2*>(s_dyn + d[3] + k);
+      double2 uu = *us;
+      if (MODE == 2) {
+        const int sg = d[4];
+        const double2 du = *reinterpret_cast<const double2*>(s_dyn + trb_o + sg * trl + k);
+        if (c.mt.segs[4 * (seg0 + sg) + 2] >= 0) {
+          uu.x = __dadd_rn(uu.x, du.x);
+          uu.y = __dadd_rn(uu.y, du.y);
+        }
+      }
+      const double2 dp = *reinterpret_cast<const double2*>(s_dyn + psio + d[1] * c.NUP);
+      double2 ny, na, fl;
+      one(yc[u].x, yp[u].x, ua[u].x, uu.x, dp.x, ulo.x, uhi.x, ny.x, na.x, fl.x);
+      one(yc[u].y, yp[u].y, ua[u].y, uu.y, dp.y, ulo.y, uhi.y, ny.y, na.y, fl.y);
+      __stcg(reinterpret_cast<double2*>(Yn + eo[u]), ny);
+      __stcg(reinterpret_cast<double2*>(UA + eo[u]), na);
+      *us = fl;  // the next backward's fill of this element pair
+    };
+    if (r0 + (CH - 1) * NG < nrows) {
+#pragma unroll
+      for (int u = 0; u < CH; ++u) elem(u, r0 + u * NG);
+    } else {
+#pragma unroll
+      for (int u = 0; u < CH; ++u)
+        if (r0 + u * NG < nrows) elem(u, r0 + u * NG);
+    }
+  }
+}
+// epi_psi_wide_v2 applies: even n_u, 16-byte aligned rows in HBM and shared memory
+__device__ __forceinline__ bool psi_pairs(int cur, int trb_o, int trl) {
+  const Ctx c = ctx_of();
+  const Params& P = g_sp.P;
+  const size_t a = reinterpret_cast<size_t>(P.ybuf[cur]) | reinterpret_cast<size_t>(P.ybuf[cur ^ 1]) |
+                   reinterpret_cast<size_t>(P.uavg) | reinterpret_cast<size_t>(s_dyn);
+  const int o = c.nu | c.psi_o | (int)(c.B() - s_dyn) | (trb_o >= 0 ? (trb_o | trl) : 0) | (c.NXP * 2 * c.E);
+  return (a & 15) == 0 && (o & 1) == 0;
+}
 __device__ __forceinline__ void epi_psi_wide(int nu_it, double cf, double th, int nrows, int cur, double* rmax,
                                              bool pre, double cfn, int trb_o = -1, int trl = 0, int seg0 = 0) {
   const Params& P = g_sp.P;
@@ -1900,6 +1991,9 @@ __device__ __forceinline__ void epi_psi_wide(int nu_it, double cf, double th, in
 #endif
   if (!TSMPC_WANT_T || is_last(P, nu_it) || P.record_all)
     epi_psi_wide_t<true, 0>(nu_it, cf, th, nrows, cur, rmax, pre, cfn, trb_o, trl, seg0);
+  else if (TSMPC_FASTEPI && epi_fast(P, nu_it, pre) && TSMPC_PSI2 && psi_pairs(cur, trb_o, trl))
+    trb_o >= 0 ? epi_psi_wide_v2<2>(nu_it, cf, th, nrows, cur, pre, cfn, trb_o, trl, seg0)
+               : epi_psi_wide_v2<1>(nu_it, cf, th, nrows, cur, pre, cfn, trb_o, trl, seg0);
   else if (TSMPC_FASTEPI && epi_fast(P, nu_it, pre))
     trb_o >= 0 ? epi_psi_wide_t<false, 2>(nu_it, cf, th, nrows, cur, rmax, pre, cfn, trb_o, trl, seg0)
                : epi_psi_wide_t<false, 1>(nu_it, cf, th, nrows, cur, rmax, pre, cfn, trb_o, trl, seg0);
