@@ -90,6 +90,13 @@ struct Meta {
 //   pos : T x {edge, stage, parent pos, tch0, ntch, hch0, nhch, 0}
 //   tch : trunk children (positions);  hch : chain-head children (edge ids)
 
+// max / min of the prox projections: a compare and a select (fmax / fmin add NaN
+// handling the iterates never need; TSMPC_FMAX=1 restores them)
+#ifndef TSMPC_FMAX
+#define TSMPC_FMAX 0
+#endif
+__device__ __forceinline__ double dmax(double a, double b) { return TSMPC_FMAX ? fmax(a, b) : (a > b ? a : b); }
+__device__ __forceinline__ double dmin(double a, double b) { return TSMPC_FMAX ? fmin(a, b) : (a < b ? a : b); }
 __device__ __forceinline__ double extrap(double y, double yp, double c) {
   return __dadd_rn(y, __dmul_rn(c, __dsub_rn(y, yp)));
 }
@@ -349,7 +356,7 @@ __device__ __forceinline__ void epi_psi_elem(const Ctx& c, const Params& P, cons
   const double w = extrap(yc[k], yp[k], q.cf);
   const double hp = __dmul_rn(u, dp);
   const double a = __dadd_rn(__dmul_rn(w, q.ilam), hp);
-  const double t = fmin(fmax(a, __dmul_rn(dp, ulo)), __dmul_rn(dp, uhi));
+  const double t = dmin(dmax(a, __dmul_rn(dp, ulo)), __dmul_rn(dp, uhi));
   const double ny = __dadd_rn(w, __dmul_rn(q.lam, __dsub_rn(hp, t)));
   yp[k] = ny;
   if (q.pre) {  // the next backward's fill of this element (bwd_tile step 1)
@@ -418,8 +425,8 @@ __device__ __noinline__ void epi_state_t(int nu_it, double cf, double th, int nr
         const double xi = x[i];
         ts[m] = __dadd_rn(__dmul_rn(ws[m], q.ilam), __dmul_rn(xi, ds));
         tz[m] = __dadd_rn(__dmul_rn(wz[m], q.ilam), __dmul_rn(xi, dz));
-        const double gs_ = __dsub_rn(fmax(ts[m], __dmul_rn(ds, bxs[m])), ts[m]);
-        const double gz = __dsub_rn(fmin(fmax(tz[m], __dmul_rn(dz, bmn[m])), __dmul_rn(dz, bmx[m])), tz[m]);
+        const double gs_ = __dsub_rn(dmax(ts[m], __dmul_rn(ds, bxs[m])), ts[m]);
+        const double gz = __dsub_rn(dmin(dmax(tz[m], __dmul_rn(dz, bmn[m])), __dmul_rn(dz, bmx[m])), tz[m]);
         ss = fma(gs_, gs_, ss);
         sz = fma(gz, gz, sz);
       }
@@ -442,8 +449,8 @@ __device__ __noinline__ void epi_state_t(int nu_it, double cf, double th, int nr
       if (i < c.nx) {
         const double xi = x[i];
         const double hs = __dmul_rn(xi, ds), hz = __dmul_rn(xi, dz);
-        const double ps = fmax(ts[m], __dmul_rn(ds, bxs[m]));
-        const double pz = fmin(fmax(tz[m], __dmul_rn(dz, bmn[m])), __dmul_rn(dz, bmx[m]));
+        const double ps = dmax(ts[m], __dmul_rn(ds, bxs[m]));
+        const double pz = dmin(dmax(tz[m], __dmul_rn(dz, bmn[m])), __dmul_rn(dz, bmx[m]));
         const double t_s = __dadd_rn(ts[m], __dmul_rn(fs, __dsub_rn(ps, ts[m])));
         const double t_z = __dadd_rn(tz[m], __dmul_rn(fz, __dsub_rn(pz, tz[m])));
         const double ns = __dadd_rn(ws[m], __dmul_rn(q.lam, __dsub_rn(hs, t_s)));
@@ -1733,7 +1740,7 @@ __device__ __noinline__ void epi_psi_wide_t(int nu_it, double cf, double th, int
         const double w = extrap(yc[u], yp[u], q.cf);
         const double hp = __dmul_rn(uu, dp);
         const double a = __dadd_rn(__dmul_rn(w, q.ilam), hp);
-        const double t = fmin(fmax(a, __dmul_rn(dp, ulo)), __dmul_rn(dp, uhi));
+        const double t = dmin(dmax(a, __dmul_rn(dp, ulo)), __dmul_rn(dp, uhi));
         const double ny = __dadd_rn(w, __dmul_rn(q.lam, __dsub_rn(hp, t)));
         epi_st(Yn + eo[u], ny);
         if (WANT && q.want) rmax = fmax(rmax, fabs(__dsub_rn(uu, __ddiv_rn(t, dp))));
@@ -1834,8 +1841,10 @@ __device__ __noinline__ void epi_state_wide_t(int nu_it, double cf, double th, i
                                                __dmul_rn(1.0, s_dyn[tpo + c.NUP + c.NXP + i])));
           ts[m] = __dadd_rn(__dmul_rn(ws[m], q.ilam), __dmul_rn(xv[m], ds));
           tz[m] = __dadd_rn(__dmul_rn(wz[m], q.ilam), __dmul_rn(xv[m], dz));
-          const double gs_ = __dsub_rn(fmax(ts[m], __dmul_rn(ds, bxs[m])), ts[m]);
-          const double gz = __dsub_rn(fmin(fmax(tz[m], __dmul_rn(dz, bmn[m])), __dmul_rn(dz, bmx[m])), tz[m]);
+          const double ps = dmax(ts[m], __dmul_rn(ds, bxs[m]));
+          const double pz = dmin(dmax(tz[m], __dmul_rn(dz, bmn[m])), __dmul_rn(dz, bmx[m]));
+          const double gs_ = __dsub_rn(ps, ts[m]);
+          const double gz = __dsub_rn(pz, tz[m]);
           ss = fma(gs_, gs_, ss);
           sz = fma(gz, gz, sz);
         }
@@ -1856,8 +1865,8 @@ __device__ __noinline__ void epi_state_wide_t(int nu_it, double cf, double th, i
         if (i < c.nx) {
           const double xi = xv[m];
           const double hs = __dmul_rn(xi, ds), hz = __dmul_rn(xi, dz);
-          const double ps = fmax(ts[m], __dmul_rn(ds, bxs[m]));
-          const double pz = fmin(fmax(tz[m], __dmul_rn(dz, bmn[m])), __dmul_rn(dz, bmx[m]));
+          const double ps = dmax(ts[m], __dmul_rn(ds, bxs[m]));
+          const double pz = dmin(dmax(tz[m], __dmul_rn(dz, bmn[m])), __dmul_rn(dz, bmx[m]));
           const double t_s = __dadd_rn(ts[m], __dmul_rn(fs, __dsub_rn(ps, ts[m])));
           const double t_z = __dadd_rn(tz[m], __dmul_rn(fz, __dsub_rn(pz, tz[m])));
           const double ns = __dadd_rn(ws[m], __dmul_rn(q.lam, __dsub_rn(hs, t_s)));
@@ -1923,7 +1932,7 @@ __device__ __noinline__ void epi_psi_wide_v2(int nu_it, double cf, double th, in
     const double w = extrap(yc, yp, q.cf);
     const double hp = __dmul_rn(uu, dp);
     const double a = __dadd_rn(__dmul_rn(w, q.ilam), hp);
-    const double t = fmin(fmax(a, __dmul_rn(dp, lo)), __dmul_rn(dp, hi));
+    const double t = dmin(dmax(a, __dmul_rn(dp, lo)), __dmul_rn(dp, hi));
     ny = __dadd_rn(w, __dmul_rn(q.lam, __dsub_rn(hp, t)));
     na = __dadd_rn(__dmul_rn(ua, q.om), __dmul_rn(q.th, uu));
     fill = __dmul_rn(extrap(ny, yc, q.cfn), dp);
