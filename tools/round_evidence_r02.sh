@@ -2,7 +2,7 @@
 # (ours + reference arm), ncu launch list of the bench command, full captures of
 # the headline kernel (wide, SMPC8) and of the SMPC3 kernel, DRAM traffic, phase timers.
 set -u
-E=gpurun_out/ev3
+E=${E:-gpurun_out/ev3}
 mkdir -p $E
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $E/smi.txt 2>&1
 python tools/prof_case.py --tree SMPC8 --iters 50 --skip-gap > $E/plain8.log 2>&1 && \
