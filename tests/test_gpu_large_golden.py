@@ -120,3 +120,22 @@ def test_stopping_with_residual_trace():
     assert got["resid_trace"].shape == (first + 1,)
     np.testing.assert_array_equal(got["resid_trace"], tr[:first + 1])
     assert got["residual_inf"] == tr[first]
+
+
+@pytest.mark.parametrize("name,world", [("L_bcn63_W4k_i100", 8), ("L_bcn63_SMPC8_i500", 4)])
+def test_sharded_cut_matches_reference(name, world):
+    """The w-way split with the cut exchange (each rank computes its own subtrees'
+    trunk positions, the top of the tree is replicated; tsmpc_solve_group on one
+    GPU) against the reference golden of the whole tree, gap included."""
+    from paper_1604_01074_b200.shard import LocalShardGroup
+    z, W = _work(name)
+    grp = LocalShardGroup(W["model"], W["tree"], W["factor"], world, W["scaling"])
+    assert all(pl.info()["exchange_doubles"] < pl.info()["trunk_edges"] * 164 for pl in grp.plans)
+    grp.set_cache(W["cache"], W["model"])
+    iters = int(z["iters"])
+    th, cf = engine.theta_schedule(iters)
+    outs = grp.solve(W["p"], iters, float(z["lam"]), theta=th, coef=cf, skip_gap=False)
+    full = grp.assemble(outs)
+    full["gap"] = outs[0]["gap"]
+    bad = failures(compare(z, full))
+    assert not bad, bad
