@@ -1680,6 +1680,46 @@ constexpr int kRW = kTileW / kGroups;   // rows per thread of a wide tile, (grou
 constexpr int kG8 = kThreadsS / 64;     // row groups of the 64-lane mapping (components < 64)
 constexpr int kRX = kTileW / kG8;       // rows per thread of a wide tile in that mapping
 
+// ---- static per-row vectors in tensor memory (TMEM) ---------------------------
+// A single-tile wide CTA (SMPC8's chain CTAs: 84 rows) reads, every iteration,
+// beta_s (h phase), uhat and e (forward) of its rows: 84 x 280 doubles that do not
+// change during the launch.  They are loaded once into TMEM (188 kB of the SM's
+// 256 kB, unused otherwise: no MMA here) in the layout of the per-thread register
+// prefetches of bwd_wide / fwd_wide, and each iteration reads them back with a
+// few wide tcgen05.ld instead of 60 global loads per thread.  Every thread owns
+// a private 128-column block of one TMEM lane (lane = tid % 128, columns
+// 128 (tid / 128) ...):  beta_s of its kRW rows -> columns 0..47, uhat -> 48..95,
+// e (64-lane mapping, kRX rows) -> 96..119.
+#ifndef TSMPC_TMSTATIC
+#define TSMPC_TMSTATIC 1
+#endif
+constexpr int kTmB = 0, kTmU = 2 * kRW, kTmE = 4 * kRW;
+static_assert(kTmE + 2 * kRX <= 128, "static TMEM block exceeds a thread's 128 columns");
+__shared__ uint32_t s_tmem;  // TMEM base of this CTA (0 is a valid address)
+__shared__ int s_tm_on;      // the static vectors are in TMEM (else read from HBM)
+__device__ __forceinline__ uint32_t tm_addr(int col) {
+  return s_tmem + ((uint32_t)(((threadIdx.x >> 5) & 3) * 32) << 16) + (uint32_t)((threadIdx.x >> 7) * 128 + col);
+}
+__device__ __forceinline__ void tm_st1(uint32_t a, double v) {  // warp-collective
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(a), "r"(__double2loint(v)),
+               "r"(__double2hiint(v))
+               : "memory");
+}
+// 8 doubles (16 columns) from a, warp-collective; the caller waits (tm_wait_ld)
+__device__ __forceinline__ void tm_ld8(uint32_t a, double* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(a));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __hiloint2double((int)r[2 * i + 1], (int)r[2 * i]);
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
 
 // psi block of the rows in rdesc (component-major, as epi_psi_rows), state in HBM.
 // WANT: this iteration's residual is needed (compiled apart: otherwise ptxas
@@ -2028,6 +2068,9 @@ __device__ __forceinline__ void epi_state_wide(int nu_it, double cf, double th, 
 // backward sweep of wide tile ti (factor.py:142-156): fill from HBM (unless the
 // previous epilogue left it), xiq scan, z = psi^ + B' xiq, h = beta_s + Ls' z,
 // g scan -> t (region A in place for tmode 0, TG for tmode 2), chain heads -> GG / XIQG
+// TMS: the CTA's static vectors are resident in TMEM (s_tm_on; compiled apart, so
+// the multi-tile CTAs keep the plain prefetch code and its register allocation)
+template <bool TMS>
 __device__ __noinline__ void bwd_wide(int ti, double cf, int cur, bool prefilled) {
   const SParams& S = g_sp;
   const Ctx c = ctx_of();
@@ -2045,10 +2088,17 @@ __device__ __noinline__ void bwd_wide(int ti, double cf, int cur, bool prefilled
   // beta_s of this thread's rows for the h phase, loaded now (the loads are in
   // flight during the fill / head sums / xiq scan / z phases)
   double bpre[kRW];
+  if (TMS) {  // resident in TMEM for the launch
+    static_assert(kRW % 8 == 0, "");
 #pragma unroll
-  for (int m = 0; m < kRW; ++m) {
-    const int r = g + kGroups * m;
-    bpre[m] = TSMPC_PREF && r < nrows && k < nv ? ldcg(S.beta_s + (size_t)c.mt.edge(row0 + r) * c.NVP + k) : 0.0;
+    for (int m = 0; m < kRW; m += 8) tm_ld8(tm_addr(kTmB + 2 * m), bpre + m);
+    tm_wait_ld();
+  } else {
+#pragma unroll
+    for (int m = 0; m < kRW; ++m) {
+      const int r = g + kGroups * m;
+      bpre[m] = TSMPC_PREF && r < nrows && k < nv ? ldcg(S.beta_s + (size_t)c.mt.edge(row0 + r) * c.NVP + k) : 0.0;
+    }
   }
   if (!prefilled) {
     // (1) fill: s = D_sig w_sig + D_zeta w_zeta -> A ; psi^ = D_psi w_psi -> B
@@ -2250,7 +2300,7 @@ __device__ __noinline__ void bwd_wide(int ti, double cf, int cur, bool prefilled
 // forward sweep of wide tile ti (factor.py:158-170) + epilogue; in split mode the
 // chains run with zero trunk input and the trunk terms and the epilogue follow in
 // fwd_finish_wide
-template <int XS>
+template <int XS, bool TMS>
 __device__ __noinline__ void fwd_wide(int ti, int nu_it, double cf, double th, int cur, double* rmax, bool pre,
                                       double cfn) {
   const SParams& S = g_sp;
@@ -2269,15 +2319,27 @@ __device__ __noinline__ void fwd_wide(int ti, int nu_it, double cf, double th, i
   const int k8 = tid & 63, g8 = tid >> 6;
   const bool x64 = nx <= 64;
   double epre[kRX], upre[kRW];
+  if (TMS) {  // resident in TMEM for the launch
+    static_assert(kRX % 4 == 0 && kRW % 8 == 0, "");
 #pragma unroll
-  for (int m = 0; m < kRX; ++m) {
-    const int r = g8 + kG8 * m;
-    epre[m] = TSMPC_PREF && x64 && r < nrows && k8 < nx ? ldcg(P.evec + (size_t)c.mt.edge(row0 + r) * c.NXP + k8) : 0.0;
-  }
+    for (int m = 0; m < kRW; m += 8) tm_ld8(tm_addr(kTmU + 2 * m), upre + m);
+    double e8[(kRX + 7) / 8 * 8];
 #pragma unroll
-  for (int m = 0; m < kRW; ++m) {
-    const int r = g + kGroups * m;
-    upre[m] = TSMPC_PREF && r < nrows && k < nu ? ldcg(P.uhat + (size_t)c.mt.edge(row0 + r) * c.NUP + k) : 0.0;
+    for (int m = 0; m < kRX; m += 8) tm_ld8(tm_addr(kTmE + 2 * m), e8 + m);
+    tm_wait_ld();
+#pragma unroll
+    for (int m = 0; m < kRX; ++m) epre[m] = e8[m];
+  } else {
+#pragma unroll
+    for (int m = 0; m < kRX; ++m) {
+      const int r = g8 + kG8 * m;
+      epre[m] = TSMPC_PREF && x64 && r < nrows && k8 < nx ? ldcg(P.evec + (size_t)c.mt.edge(row0 + r) * c.NXP + k8) : 0.0;
+    }
+#pragma unroll
+    for (int m = 0; m < kRW; ++m) {
+      const int r = g + kGroups * m;
+      upre[m] = TSMPC_PREF && r < nrows && k < nu ? ldcg(P.uhat + (size_t)c.mt.edge(row0 + r) * c.NUP + k) : 0.0;
+    }
   }
   if (c.mt.tmode == 2) {  // t rows of this tile -> region A
     const int lane = tid & 31;
@@ -2766,12 +2828,60 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel(LaunchWin win)
 // tile's epilogue leaves the next iteration's fill of that tile (its first
 // backward tile).  Sharded plans run it as two launches per iteration (phase 1:
 // backward + head pre-reduction; phase 2: the rest), state in HBM in between.
+// TMEM for the static vectors: 512 columns (all of it; one CTA per SM), allocated
+// by warp 0 and filled by every thread in its prefetch layout (see kTmB)
+__device__ __noinline__ void tm_static_fill() {
+  if ((threadIdx.x >> 5) == 0) {
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&s_tmem);
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(dst) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const SParams& S = g_sp;
+  const Ctx c = ctx_of();
+  const Params& P = S.P;
+  const int row0 = c.mt.tiles[0], nrows = c.mt.tiles[1];
+  const int k = threadIdx.x & (kKW - 1), g = threadIdx.x / kKW;
+  const int k8 = threadIdx.x & 63, g8 = threadIdx.x >> 6;
+#pragma unroll 1
+  for (int m = 0; m < kRW; ++m) {
+    const int r = g + kGroups * m;
+    const size_t e = r < nrows ? (size_t)c.mt.edge(row0 + r) : 0;
+    tm_st1(tm_addr(kTmB + 2 * m), r < nrows && k < c.nv ? ldcg(S.beta_s + e * c.NVP + k) : 0.0);
+    tm_st1(tm_addr(kTmU + 2 * m), r < nrows && k < c.nu ? ldcg(P.uhat + e * c.NUP + k) : 0.0);
+  }
+#pragma unroll 1
+  for (int m = 0; m < (kRX + 7) / 8 * 8; ++m) {
+    const int r = g8 + kG8 * m;
+    const bool ok = m < kRX && c.nx <= 64 && r < nrows && k8 < c.nx;
+    tm_st1(tm_addr(kTmE + 2 * m), ok ? ldcg(P.evec + (size_t)c.mt.edge(row0 + r) * c.NXP + k8) : 0.0);
+  }
+  tm_wait_st();
+  if (threadIdx.x == 0) s_tm_on = 1;
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tm_release() {
+  if (!s_tm_on) return;
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  if ((threadIdx.x >> 5) == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(s_tmem) : "memory");
+}
+
 template <int XS>
 __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
   cg::grid_group grid = cg::this_grid();
   const SParams& S = g_sp;
   const Params& P = S.P;
-  if (threadIdx.x == 0) s_win = win;  // visible after the staging barrier below
+  if (threadIdx.x == 0) {
+    s_win = win;  // visible after the staging barrier below
+    s_tm_on = 0;
+  }
   {  // stage model vectors, scaling, sparse operators and this CTA's plan
     double* bnd = s_dyn + S.O_BND;
     double* scl = s_dyn + S.O_SCL;
@@ -2837,6 +2947,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
     }
     __syncthreads();
   }
+  // static vectors of a single-tile CTA resident in TMEM for the launch
+  if (TSMPC_TMSTATIC && nt == 1 && do_a && do_b && !S.sharded && (!S.split || chain_cta)) tm_static_fill();
   double rmax = 0.0;
   unsigned int sub_target = 0;  // trunk-CTA barrier episodes x split_n (split mode)
   double cf = P.coef[win.nu0], th = P.theta[win.nu0];
@@ -2849,13 +2961,17 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
           (long long)*((volatile unsigned long long*)(P.resid_chk + nu / P.check_every - 1)));
       if (r <= P.tol) {
         if (blockIdx.x == 0 && threadIdx.x == 0) *P.iters_done = nu;
+        tm_release();
         return;
       }
     }
     const int nn = nu + 1 < P.iters ? nu + 1 : nu;
     const double cf_n = P.coef[nn], th_n = P.theta[nn];
     if (do_a) {
-      for (int t = nt - 1; t >= 0; --t) bwd_wide(t, cf, cur, S.wide_prefill && t == nt - 1 && nu > win.nu0);
+      for (int t = nt - 1; t >= 0; --t) {
+        const bool pf = S.wide_prefill && t == nt - 1 && nu > win.nu0;
+        s_tm_on ? bwd_wide<true>(t, cf, cur, pf) : bwd_wide<false>(t, cf, cur, pf);
+      }
       if (S.sharded && trunk) {
         grid.sync();
         head_prereduce();
@@ -2874,7 +2990,9 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
       (void)tb_;
       const unsigned it = (unsigned)(nu - win.nu0 + 1);
       if (chain_cta) {
-        for (int t = 0; t < nt; ++t) fwd_wide<XS>(t, nu, cf, th, cur, &rmax, false, 0.0);
+        for (int t = 0; t < nt; ++t)
+          s_tm_on ? fwd_wide<XS, true>(t, nu, cf, th, cur, &rmax, false, 0.0)
+                  : fwd_wide<XS, false>(t, nu, cf, th, cur, &rmax, false, 0.0);
         TSMPC_MARK(P, 10, tb_);
         signal_wait(S.sub_ctr + 2, it * (unsigned)S.split_n);
         TSMPC_MARK(P, 9, tb_);
@@ -2922,7 +3040,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
           P.xavg[i] = __dadd_rn(__dmul_rn(P.xavg[i], om), __dmul_rn(th, c.proot()[i]));
       }
       for (int t = 0; t < nt; ++t)
-        fwd_wide<XS>(t, nu, cf, th, cur, &rmax, S.wide_prefill && t == nt - 1 && nu + 1 < win.nu1, cf_n);
+        s_tm_on ? fwd_wide<XS, true>(t, nu, cf, th, cur, &rmax, S.wide_prefill && t == nt - 1 && nu + 1 < win.nu1, cf_n)
+                : fwd_wide<XS, false>(t, nu, cf, th, cur, &rmax, S.wide_prefill && t == nt - 1 && nu + 1 < win.nu1, cf_n);
     }
     if (do_b) {
       if (nu == P.iters - 1 || P.record_all || is_check(P, nu)) {
@@ -2945,6 +3064,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
     cf = cf_n;
     th = th_n;
   }
+  tm_release();
   if (P.tol > 0.0 && blockIdx.x == 0 && threadIdx.x == 0) *P.iters_done = win.nu1;
 }
 
