@@ -2947,6 +2947,15 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
     }
     __syncthreads();
   }
+  if (S.split && S.tops && !chain_cta) {  // trunk CTAs: the combined forward operators
+    double* tv = s_dyn + S.O_SLOT + S.O_TOPS;
+    int* ti = reinterpret_cast<int*>(tv + S.n_tpv);
+#pragma unroll 1
+    for (int i = threadIdx.x; i < S.n_tpv; i += kThreadsS) tv[i] = __ldg(S.tpv + i);
+#pragma unroll 1
+    for (int i = threadIdx.x; i < S.n_tpi; i += kThreadsS) ti[i] = __ldg(S.tpi + i);
+    __syncthreads();
+  }
   // static vectors of a single-tile CTA resident in TMEM for the launch
   if (TSMPC_TMSTATIC && nt == 1 && do_a && do_b && !S.sharded && (!S.split || chain_cta)) tm_static_fill();
   double rmax = 0.0;

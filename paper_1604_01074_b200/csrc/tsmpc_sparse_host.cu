@@ -627,10 +627,23 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
         out.why = "trunk too large for the work region";
         return out;
       }
+      // the trunk CTAs' combined forward operators (du = M1 KY, B du = M2 KY: one
+      // pass instead of three) after the sweep buffers in region A, staged at launch;
+      // the needs' KY / uhat / e rows are staged in region B
+      S.n_tpi = (int)out.tpi.size();
+      S.n_tpv = (int)out.tpv.size();
+      const long long sld = (long long)(NVP + NXP + NUP) + NUP + NXP;
+      const long long otops = even(zx + (S.sched_smem && !S.sched_resident ? sched : 0));
+      if (otops + S.n_tpv + (S.n_tpi + 1) / 2 + 1 <= (long long)tcap * S.LA && (long long)need_max * sld <= (long long)tcap * NUP &&
+          !std::getenv("TSMPC_NO_TOPS")) {
+        S.O_SLOT = S.O_WORK;
+        S.O_TOPS = (int)otops;
+        S.tops = 1;
+      }
     }
     if (std::getenv("TSMPC_PLAN_DEBUG"))
-      std::fprintf(stderr, "plan_sparse wide: split %d (chain CTAs %d, trunk CTAs %d), smem %lld doubles\n", S.split,
-                   nch_split, split_n, off);
+      std::fprintf(stderr, "plan_sparse wide: split %d (chain CTAs %d, trunk CTAs %d), smem %lld doubles, tops %d\n",
+                   S.split, nch_split, split_n, off, S.tops);
     S.meta_max = meta_max;
     out.smem = (size_t)off * sizeof(double);
     out.meta.clear();
