@@ -159,6 +159,66 @@ constexpr int kGroups = kThreadsS / kKW;    // 4 row groups
 constexpr int kRowsPT = kTileS / kGroups;   // rows per thread in a full tile
 constexpr int kCh = 8;                      // rows per register chunk of the chain scans
 
+// ---- tensor memory (TMEM) holding static per-row vectors (see kTmB, kTmRB) ----
+// Every thread of a CTA that uses it owns a private 128-column block of one TMEM
+// lane: lane = tid mod 128, columns 128 (tid / 128) .. + 127.  The accesses are
+// warp-collective (.sync.aligned): every lane of a warp takes part.
+__shared__ uint32_t s_tmem;  // TMEM base of this CTA (0 is a valid address)
+__shared__ int s_tm_on;      // the static vectors are in TMEM (else read from HBM)
+__device__ __forceinline__ uint32_t tm_addr(int col) {
+  return s_tmem + ((uint32_t)(((threadIdx.x >> 5) & 3) * 32) << 16) + (uint32_t)((threadIdx.x >> 7) * 128 + col);
+}
+__device__ __forceinline__ void tm_st1(uint32_t a, double v) {  // warp-collective
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(a), "r"(__double2loint(v)),
+               "r"(__double2hiint(v))
+               : "memory");
+}
+// 8 doubles (16 columns) from a, warp-collective; the caller waits (tm_wait_ld)
+__device__ __forceinline__ void tm_ld8(uint32_t a, double* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(a));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __hiloint2double((int)r[2 * i + 1], (int)r[2 * i]);
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+// all 512 columns (one CTA per SM), allocated by warp 0; s_tmem after the barrier
+__device__ __forceinline__ void tm_alloc_all() {
+  if ((threadIdx.x >> 5) == 0) {
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&s_tmem);
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(dst) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+// after this thread's stores: mark the CTA's vectors resident (s_tm_on)
+__device__ __forceinline__ void tm_fill_done() {
+  tm_wait_st();
+  if (threadIdx.x == 0) s_tm_on = 1;
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tm_release() {
+  if (!s_tm_on) return;
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  if ((threadIdx.x >> 5) == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(s_tmem) : "memory");
+}
+// resident one-tile CTAs (apg_sparse_kernel): beta_s, uhat, e of the thread's
+// kRowsPT rows (group mapping) in columns 0.., 16.., 32..
+constexpr int kTmRB = 0, kTmRU = 16, kTmRE = 32;
+static_assert(kRowsPT <= 8, "resident TMEM slots hold 8 rows per thread");
+
 struct Ctx {
   const SParams* S;
   const Params* P;
@@ -518,6 +578,28 @@ __device__ __forceinline__ void epi_psi_rows(int nu_it, double cf, double th, in
 // A in place (tmode 0: the CTA's only tile stays in shared memory), to the
 // tile's slot rows (tmode 1) or to HBM (tmode 2, streamed CTAs).
 // ----------------------------------------------------------------------------
+// the resident one-tile CTA's static vectors -> TMEM (apg_sparse_kernel)
+__device__ __noinline__ void tm_static_fill_res() {
+  tm_alloc_all();
+  const SParams& S = g_sp;
+  const Ctx c = ctx_of();
+  const Params& P = S.P;
+  const int row0 = c.mt.tiles[0], nrows = c.mt.tiles[1];
+  const int k = threadIdx.x & (kKW - 1), g = threadIdx.x / kKW;
+#pragma unroll 1
+  for (int m = 0; m < 8; ++m) {
+    const int r = g + kGroups * m;
+    const bool ok = m < kRowsPT && r < nrows;
+    const size_t e = ok ? (size_t)c.mt.edge(row0 + r) : 0;
+    tm_st1(tm_addr(kTmRB + 2 * m), ok && k < c.nv ? ldcg(S.beta_s + e * c.NVP + k) : 0.0);
+    tm_st1(tm_addr(kTmRU + 2 * m), ok && k < c.nu ? ldcg(P.uhat + e * c.NUP + k) : 0.0);
+    tm_st1(tm_addr(kTmRE + 2 * m), ok && k < c.nx ? ldcg(P.evec + e * c.NXP + k) : 0.0);
+  }
+  tm_fill_done();
+}
+
+// TMS: the tile's static vectors are resident in TMEM (s_tm_on; compiled apart)
+template <bool TMS>
 __device__ __noinline__ void bwd_tile(int ti, double cf, int ysm, int srow0, bool resident, int cur,
                                       bool prefilled = false) {
   const SParams& S = g_sp;
@@ -534,11 +616,19 @@ __device__ __noinline__ void bwd_tile(int ti, double cf, int ysm, int srow0, boo
   (void)tm_;
   // prefetch beta_s (the bias of h) for this thread's rows
   double bpre[kRowsPT];
+  if (TMS) {
+    double b8[8];
+    tm_ld8(tm_addr(kTmRB), b8);
+    tm_wait_ld();
 #pragma unroll
-  for (int m = 0; m < kRowsPT; ++m) {
-    const int r = g + kGroups * m;
-    bpre[m] = 0.0;
-    if (r < nrows && k < nv) bpre[m] = ldcg(S.beta_s + (size_t)c.mt.edge(row0 + r) * c.NVP + k);
+    for (int m = 0; m < kRowsPT; ++m) bpre[m] = b8[m];
+  } else {
+#pragma unroll
+    for (int m = 0; m < kRowsPT; ++m) {
+      const int r = g + kGroups * m;
+      bpre[m] = 0.0;
+      if (r < nrows && k < nv) bpre[m] = ldcg(S.beta_s + (size_t)c.mt.edge(row0 + r) * c.NVP + k);
+    }
   }
   if (!resident) {
     cp_wait<0>();
@@ -722,6 +812,7 @@ __device__ __noinline__ void bwd_tile(int ti, double cf, int ysm, int srow0, boo
 // ----------------------------------------------------------------------------
 // forward sweep of tile ti (factor.py:158-170) + epilogue
 // ----------------------------------------------------------------------------
+template <bool TMS>
 __device__ __noinline__ void fwd_tile(int ti, int nu_it, double cf, double th, int ysm,
                                       int srow0, bool resident, int cur, double* rmax) {
   const SParams& S = g_sp;
@@ -760,14 +851,26 @@ __device__ __noinline__ void fwd_tile(int ti, int nu_it, double cf, double th, i
   }
   // prefetch the static biases: uhat (u = uhat + du) and e (x recursion)
   double upre[kRowsPT], epre[kRowsPT];
+  if (TMS) {
+    double u8[8], e8[8];
+    tm_ld8(tm_addr(kTmRU), u8);
+    tm_ld8(tm_addr(kTmRE), e8);
+    tm_wait_ld();
 #pragma unroll
-  for (int m = 0; m < kRowsPT; ++m) {
-    const int r = g + kGroups * m;
-    upre[m] = epre[m] = 0.0;
-    if (r < nrows) {
-      const int e = c.mt.edge(row0 + r);
-      if (k < nu) upre[m] = ldcg(P.uhat + (size_t)e * c.NUP + k);
-      if (k < nx) epre[m] = ldcg(P.evec + (size_t)e * c.NXP + k);
+    for (int m = 0; m < kRowsPT; ++m) {
+      upre[m] = u8[m];
+      epre[m] = e8[m];
+    }
+  } else {
+#pragma unroll
+    for (int m = 0; m < kRowsPT; ++m) {
+      const int r = g + kGroups * m;
+      upre[m] = epre[m] = 0.0;
+      if (r < nrows) {
+        const int e = c.mt.edge(row0 + r);
+        if (k < nu) upre[m] = ldcg(P.uhat + (size_t)e * c.NUP + k);
+        if (k < nx) epre[m] = ldcg(P.evec + (size_t)e * c.NXP + k);
+      }
     }
   }
   if (!resident) {
@@ -1695,30 +1798,6 @@ constexpr int kRX = kTileW / kG8;       // rows per thread of a wide tile in tha
 #endif
 constexpr int kTmB = 0, kTmU = 2 * kRW, kTmE = 4 * kRW;
 static_assert(kTmE + 2 * kRX <= 128, "static TMEM block exceeds a thread's 128 columns");
-__shared__ uint32_t s_tmem;  // TMEM base of this CTA (0 is a valid address)
-__shared__ int s_tm_on;      // the static vectors are in TMEM (else read from HBM)
-__device__ __forceinline__ uint32_t tm_addr(int col) {
-  return s_tmem + ((uint32_t)(((threadIdx.x >> 5) & 3) * 32) << 16) + (uint32_t)((threadIdx.x >> 7) * 128 + col);
-}
-__device__ __forceinline__ void tm_st1(uint32_t a, double v) {  // warp-collective
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(a), "r"(__double2loint(v)),
-               "r"(__double2hiint(v))
-               : "memory");
-}
-// 8 doubles (16 columns) from a, warp-collective; the caller waits (tm_wait_ld)
-__device__ __forceinline__ void tm_ld8(uint32_t a, double* v) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15}, [%16];\n"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(a));
-#pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] = __hiloint2double((int)r[2 * i + 1], (int)r[2 * i]);
-}
-__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
-__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
 
 // psi block of the rows in rdesc (component-major, as epi_psi_rows), state in HBM.
@@ -2575,7 +2654,10 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel(LaunchWin win)
   cg::grid_group grid = cg::this_grid();
   const SParams& S = g_sp;
   const Params& P = S.P;
-  if (threadIdx.x == 0) s_win = win;  // visible after the staging barrier below
+  if (threadIdx.x == 0) {
+    s_win = win;  // visible after the staging barrier below
+    s_tm_on = 0;
+  }
   {  // stage model vectors, scaling, sparse operators and this CTA's plan
     double* bnd = s_dyn + S.O_BND;
     double* scl = s_dyn + S.O_SCL;
@@ -2663,6 +2745,10 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel(LaunchWin win)
     }
     __syncthreads();
   }
+  // static vectors of a resident one-tile CTA in TMEM for the launch
+  if (TSMPC_TMSTATIC && nt == 1 && resident && do_a && do_b && !S.sharded &&
+      (!S.split || (int)blockIdx.x < S.split_c0))
+    tm_static_fill_res();
   double rmax = 0.0;
   unsigned int sub_target = 0;  // trunk-CTA barrier episodes x split_n (split mode)
   double cf = P.coef[win.nu0], th = P.theta[win.nu0];
@@ -2676,6 +2762,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel(LaunchWin win)
           (long long)*((volatile unsigned long long*)(P.resid_chk + nu / P.check_every - 1)));
       if (r <= P.tol) {
         if (blockIdx.x == 0 && threadIdx.x == 0) *P.iters_done = nu;
+        tm_release();
         return;
       }
     }
@@ -2684,8 +2771,10 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel(LaunchWin win)
     const double cf_n = P.coef[nn], th_n = P.theta[nn];
     if (do_a) {
       for (int t = nt - 1; t >= 0; --t)
-        bwd_tile(t, cf, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur,
-                 S.split && S.split_heads && S.split_flags && nu > win.nu0);
+        s_tm_on ? bwd_tile<true>(t, cf, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur,
+                                 S.split && S.split_heads && S.split_flags && nu > win.nu0)
+                : bwd_tile<false>(t, cf, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur,
+                                  S.split && S.split_heads && S.split_flags && nu > win.nu0);
       if (S.sharded && trunk) {
         grid.sync();
         head_prereduce();
@@ -2706,7 +2795,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel(LaunchWin win)
       if ((int)blockIdx.x < S.split_c0) {
         if (!S.split_heads) signal_arrive(S.sub_ctr + 1);  // else published inside bwd_tile
         for (int t = 0; t < nt; ++t)
-          fwd_tile(t, nu, cf, th, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur, &rmax);
+          (s_tm_on ? fwd_tile<true>(t, nu, cf, th, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur, &rmax)
+                  : fwd_tile<false>(t, nu, cf, th, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur, &rmax));
         TSMPC_MARK(P, 10, tb_);
         signal_wait(S.sub_ctr + 2, it * (unsigned)S.split_n);
         TSMPC_MARK(P, 9, tb_);
@@ -2761,7 +2851,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel(LaunchWin win)
           TSMPC_MARK(P, 12, tb_);
         } else {
           for (int t = 0; t < nt; ++t)
-            fwd_tile(t, nu, cf, th, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur, &rmax);
+            (s_tm_on ? fwd_tile<true>(t, nu, cf, th, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur, &rmax)
+                  : fwd_tile<false>(t, nu, cf, th, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur, &rmax));
         }
         TSMPC_MARK(P, 10, tb_);
         grid.sync();
@@ -2792,7 +2883,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel(LaunchWin win)
         TSMPC_MARK(P, 3, tb_s);
       } else {
         for (int t = 0; t < nt; ++t)
-          fwd_tile(t, nu, cf, th, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur, &rmax);
+          (s_tm_on ? fwd_tile<true>(t, nu, cf, th, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur, &rmax)
+                  : fwd_tile<false>(t, nu, cf, th, ysm, resident ? c.mt.tiles[4 * t] : 0, resident, cur, &rmax));
       }
     }
     if (do_b) {
@@ -2818,6 +2910,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel(LaunchWin win)
     cf = cf_n;
     th = th_n;
   }
+  tm_release();
   if (P.tol > 0.0 && blockIdx.x == 0 && threadIdx.x == 0) *P.iters_done = win.nu1;
 }
 
@@ -2831,14 +2924,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_sparse_kernel(LaunchWin win)
 // TMEM for the static vectors: 512 columns (all of it; one CTA per SM), allocated
 // by warp 0 and filled by every thread in its prefetch layout (see kTmB)
 __device__ __noinline__ void tm_static_fill() {
-  if ((threadIdx.x >> 5) == 0) {
-    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&s_tmem);
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(dst) : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  tm_alloc_all();
   const SParams& S = g_sp;
   const Ctx c = ctx_of();
   const Params& P = S.P;
@@ -2858,19 +2944,7 @@ __device__ __noinline__ void tm_static_fill() {
     const bool ok = m < kRX && c.nx <= 64 && r < nrows && k8 < c.nx;
     tm_st1(tm_addr(kTmE + 2 * m), ok ? ldcg(P.evec + (size_t)c.mt.edge(row0 + r) * c.NXP + k8) : 0.0);
   }
-  tm_wait_st();
-  if (threadIdx.x == 0) s_tm_on = 1;
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-}
-__device__ __forceinline__ void tm_release() {
-  if (!s_tm_on) return;
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  if ((threadIdx.x >> 5) == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(s_tmem) : "memory");
+  tm_fill_done();
 }
 
 template <int XS>
