@@ -1793,6 +1793,9 @@ constexpr int kRX = kTileW / kG8;       // rows per thread of a wide tile in tha
 // a private 128-column block of one TMEM lane (lane = tid % 128, columns
 // 128 (tid / 128) ...):  beta_s of its kRW rows -> columns 0..47, uhat -> 48..95,
 // e (64-lane mapping, kRX rows) -> 96..119.
+#ifndef TSMPC_TMLATE
+#define TSMPC_TMLATE 1
+#endif
 #ifndef TSMPC_TMSTATIC
 #define TSMPC_TMSTATIC 1
 #endif
@@ -2167,11 +2170,13 @@ __device__ __noinline__ void bwd_wide(int ti, double cf, int cur, bool prefilled
   // beta_s of this thread's rows for the h phase, loaded now (the loads are in
   // flight during the fill / head sums / xiq scan / z phases)
   double bpre[kRW];
-  if (TMS) {  // resident in TMEM for the launch
+  if (TMS) {  // resident in TMEM for the launch (read where used with TSMPC_TMLATE)
     static_assert(kRW % 8 == 0, "");
+    if (!TSMPC_TMLATE) {
 #pragma unroll
-    for (int m = 0; m < kRW; m += 8) tm_ld8(tm_addr(kTmB + 2 * m), bpre + m);
-    tm_wait_ld();
+      for (int m = 0; m < kRW; m += 8) tm_ld8(tm_addr(kTmB + 2 * m), bpre + m);
+      tm_wait_ld();
+    }
   } else {
 #pragma unroll
     for (int m = 0; m < kRW; ++m) {
@@ -2330,6 +2335,11 @@ __device__ __noinline__ void bwd_wide(int ti, double cf, int cur, bool prefilled
   __syncthreads();
   TSMPC_MARK(P, 5, tm_);
   // (4) h = beta_s + Ls' z (column k of Ls), A <- beta_s + Ls' B
+  if (TMS && TSMPC_TMLATE) {
+#pragma unroll
+    for (int m = 0; m < kRW; m += 8) tm_ld8(tm_addr(kTmB + 2 * m), bpre + m);
+    tm_wait_ld();
+  }
   if (k < nv) {
     const SpCol col = sp_col(c, S.Lc_ptr, S.Lc_idx, S.Lc_val, k);
 #pragma unroll
@@ -2398,16 +2408,25 @@ __device__ __noinline__ void fwd_wide(int ti, int nu_it, double cf, double th, i
   const int k8 = tid & 63, g8 = tid >> 6;
   const bool x64 = nx <= 64;
   double epre[kRX], upre[kRW];
-  if (TMS) {  // resident in TMEM for the launch
-    static_assert(kRX % 4 == 0 && kRW % 8 == 0, "");
-#pragma unroll
-    for (int m = 0; m < kRW; m += 8) tm_ld8(tm_addr(kTmU + 2 * m), upre + m);
+  auto tm_ld_e = [&]() {
     double e8[(kRX + 7) / 8 * 8];
 #pragma unroll
     for (int m = 0; m < kRX; m += 8) tm_ld8(tm_addr(kTmE + 2 * m), e8 + m);
     tm_wait_ld();
 #pragma unroll
     for (int m = 0; m < kRX; ++m) epre[m] = e8[m];
+  };
+  auto tm_ld_u = [&]() {
+#pragma unroll
+    for (int m = 0; m < kRW; m += 8) tm_ld8(tm_addr(kTmU + 2 * m), upre + m);
+    tm_wait_ld();
+  };
+  if (TMS) {  // resident in TMEM for the launch (read where used with TSMPC_TMLATE)
+    static_assert(kRX % 4 == 0 && kRW % 8 == 0, "");
+    if (!TSMPC_TMLATE) {
+      tm_ld_u();
+      tm_ld_e();
+    }
   } else {
 #pragma unroll
     for (int m = 0; m < kRX; ++m) {
@@ -2477,6 +2496,7 @@ __device__ __noinline__ void fwd_wide(int ti, int nu_it, double cf, double th, i
   TSMPC_MARK(P, 11, tm_);
   // (3) bv + e = B du + e (row k of B), A <- B B + e; 64 lanes x 8 row groups
   // when n_x <= 64 (every thread busy), else the (group, component) mapping
+  if (TMS && TSMPC_TMLATE) tm_ld_e();
   if (x64) {
     if (k8 < nx) {
       const SpCol col = sp_col(c, S.Br_ptr, S.Br_idx, S.Br_val, k8);
@@ -2499,6 +2519,7 @@ __device__ __noinline__ void fwd_wide(int ti, int nu_it, double cf, double th, i
   TSMPC_MARK(P, 6, tm_);
   // (4) u = uhat + du (B; the psi epilogue below reads back only this thread's
   // entries: no barrier), then the x scan, head -> tail: x = a .* x_anc + (bv + e)
+  if (TMS && TSMPC_TMLATE) tm_ld_u();
   if (k < nu) {
 #pragma unroll
     for (int m = 0; m < kRW; ++m) {
