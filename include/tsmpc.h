@@ -235,7 +235,8 @@ int tsmpc_dual_operator_step(tsmpc_plan* plan, double* y_dot_dy, double* dy_dot_
  * smem_bytes, diag_A, threads, tile_rows, sms, collapsed, trunk_edges, sparse,
  * resident_ctas, sharded, rank, world, owned_chain_edges, total_chains,
  * trunk_ctas, wide, exchange_doubles (shard plans: the doubles every rank sums
- * per iteration)}. */
+ * per iteration), fill_rows_hbm (wide plans with multi-tile or sharded CTAs: the
+ * epilogue leaves the next backward's fill rows in HBM)}. */
 int tsmpc_plan_info(const tsmpc_plan* plan, int64_t* info, int32_t n_info);
 
 /* Host-only planning (no device needed): the segment / level / tile / trunk

@@ -85,7 +85,7 @@ struct tsmpc_plan {
   SParams sbase{};
   int sp_ctas = 0, sp_resident = 0, sp_tiles = 0, sp_trunk = 0;
   size_t sp_smem = 0;
-  double *BETA_S = nullptr, *TG = nullptr, *KY_S = nullptr, *MS = nullptr;
+  double *BETA_S = nullptr, *TG = nullptr, *FG = nullptr, *KY_S = nullptr, *MS = nullptr;
   std::string sp_why;
   // device stage cache (tsmpc_set_cache_operators / tsmpc_set_forecast)
   bool has_cache_ops = false;
@@ -771,13 +771,18 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
       SparseOpsIn oi{nx, nu, nv, pb->B, pb->Ls, pb->lam_s};
       cudaFuncAttributes fa{};
       cudaFuncGetAttributes(&fa, apg_sparse_kernel);  // static shared memory counts against the opt-in limit
-      cudaFuncAttributes fw{};
-      cudaFuncGetAttributes(&fw, sparse_kernel_fn(1, nx));
+      cudaFuncAttributes fw{}, fw2{};
+      cudaFuncGetAttributes(&fw, sparse_kernel_fn(1, nx, false));
+      cudaFuncGetAttributes(&fw2, sparse_kernel_fn(1, nx, true));
+      fw.sharedSizeBytes = std::max(fw.sharedSizeBytes, fw2.sharedSizeBytes);
       SparseHostPlan hp = choose_sparse_plan(ti, oi, NXP, NUP, NVP, pl->sm_count,
                                              (size_t)prop.sharedMemPerBlockOptin - fa.sharedSizeBytes,
                                              (size_t)prop.sharedMemPerBlockOptin - fw.sharedSizeBytes, shard,
                                              shard ? srank : 0, shard ? sworld : 1);
-      const void* kfn = sparse_kernel_fn(hp.S.wide, nx);
+      // fill rows through HBM (FG) for multi-tile / sharded wide CTAs: the kernel variant
+      // compiled with them (the others keep the one-tile code as it was)
+      if (!hp.S.wide || std::getenv("TSMPC_NO_FG")) hp.S.FL = 0;
+      const void* kfn = sparse_kernel_fn(hp.S.wide, nx, hp.S.FL > 0);
       int occ_s = 0;
       if (hp.ok) {
         // the attribute is per kernel, shared by every plan of the process: the
@@ -804,12 +809,13 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
         rc |= pl->upload(&d_spv, hp.spv.data(), hp.spv.size());
         rc |= pl->upload(&pl->MS, pb->Ms, (size_t)nv * nv);
         rc |= pl->alloc(&pl->TG, (size_t)E * NVP);
+        if (hp.S.FL > 0) rc |= pl->alloc(&pl->FG, (size_t)E * hp.S.FL);
         rc |= pl->alloc(&pl->KY_S, (size_t)std::max(1, hp.n_trunk) * P.KY_LD);
         if (rc) return bail(0);
         SParams& S = pl->sbase;
         S = hp.S;
         S.spi = d_spi; S.spv = d_spv; S.meta = d_meta; S.meta_ptr = d_mptr; S.tsched = d_ts;
-        S.beta_s = pl->BETA_S; S.TG = pl->TG;
+        S.beta_s = pl->BETA_S; S.TG = pl->TG; S.FG = pl->FG;
         S.a_unit = 1;
         for (int i = 0; i < nx; ++i)
           if (pb->A[(size_t)i * nx + i] != 1.0) S.a_unit = 0;
@@ -1142,7 +1148,8 @@ int tsmpc_plan_info(const tsmpc_plan* pl, int64_t* info, int32_t n) {
                           sp ? pl->sp_trunk : pl->n_trunk, sp ? 1 : 0, pl->sp_resident,
                           pl->sharded ? 1 : 0, pl->rank, pl->world, (int64_t)pl->owned_edges.size(),
                           pl->total_chains, sp ? pl->sbase.split_n : 0, sp ? pl->sbase.wide : 0,
-                          pl->sharded ? (int64_t)pl->sbase.n_xch * pl->sbase.XCH_LD : 0};
+                          pl->sharded ? (int64_t)pl->sbase.n_xch * pl->sbase.XCH_LD : 0,
+                          sp && pl->sbase.FG ? 1 : 0};
   for (int i = 0; i < n && i < (int)(sizeof(vals) / sizeof(vals[0])); ++i) info[i] = vals[i];
   return TSMPC_OK;
 }

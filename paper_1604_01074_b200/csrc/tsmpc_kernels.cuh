@@ -207,6 +207,12 @@ struct SParams {
   // stay in region A when a CTA has one tile (tmode 0), else they go through TG.
   int wide;
   int wide_prefill;             // the epilogue of the CTA's last tile leaves the next fill
+  // fill rows through HBM (multi-tile or sharded wide CTAs): the epilogue of every tile
+  // that cannot leave its next fill in shared memory writes it to FG (E x FL,
+  // [s (NXP) | psi^ (NUP)]), and the next backward copies it in (cp.async) instead of
+  // reading both dual rows and extrapolating
+  double* FG;
+  int FL;                       // NXP + NUP
   int hsum_nseg;                // wide split mode: chains per chain CTA the head-sum scratch holds
 };
 

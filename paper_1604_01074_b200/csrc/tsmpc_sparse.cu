@@ -1814,13 +1814,14 @@ static_assert(kTmE + 2 * kRX <= 128, "static TMEM block exceeds a thread's 128 c
 // [du | B du | x] (stride trl), -1 if none; u += du_tp is folded in here.
 template <bool WANT, int MODE>
 __device__ __noinline__ void epi_psi_wide_t(int nu_it, double cf, double th, int nrows, int cur, double* rmax_io,
-                                            bool pre, double cfn, int trb_o, int trl, int seg0) {
+                                            int pre, double cfn, int trb_o, int trl, int seg0) {
   const SParams& S = g_sp;
   const Ctx c = ctx_of();
   const Params& P = S.P;
-  const EpiConst q = epi_const(P, nu_it, cf, th, true, cur ^ 1, pre, cfn);
+  const EpiConst q = epi_const(P, nu_it, cf, th, true, cur ^ 1, pre != 0, cfn);
   constexpr bool FAST = MODE != 0;
   const bool do_pre = FAST || q.pre, do_last = !FAST && q.last;
+  const bool fgw = pre == 2;  // the next fill goes to FG (HBM), not to shared memory
   const bool fold = MODE == 2 || (MODE == 0 && trb_o >= 0);
   const int k = threadIdx.x & (kKW - 1), g = threadIdx.x / kKW;
   double rmax = *rmax_io;
@@ -1870,7 +1871,9 @@ __device__ __noinline__ void epi_psi_wide_t(int nu_it, double cf, double th, int
         if (do_last) epi_st(P.U + eo[u] + k, uu);
         if (do_pre) {  // the next backward's fill of this element
           const double wn = extrap(ny, yc[u], q.cfn);
-          *us = (FAST || c.scaled()) ? __dmul_rn(wn, dp) : wn;
+          const double fv = (FAST || c.scaled()) ? __dmul_rn(wn, dp) : wn;
+          if (fgw) stcg(S.FG + (size_t)d[0] * S.FL + c.NXP + k, fv);
+          else *us = fv;
         }
       };
       if (FAST && r0 + (kChunkW - 1) * kGroups < nrows) {
@@ -1889,7 +1892,7 @@ __device__ __noinline__ void epi_psi_wide_t(int nu_it, double cf, double th, int
 // state blocks of the rows in rdesc, one warp per row (R2 rows in flight), state in
 // HBM.  WANT / MODE as for epi_psi_wide_t; the fold (split mode, A = I) adds
 // x += (d + 1) B du_tp + x_tp.
-template <int XS, bool WANT, int MODE>
+template <int XS, bool WANT, int MODE, bool FGW>
 __device__ __noinline__ void epi_state_wide_t(int nu_it, double cf, double th, int nrows, int cur, double* rmax_io,
                                               bool pre, double cfn, int trb_o, int trl, int seg0) {
   const SParams& S = g_sp;
@@ -2003,7 +2006,9 @@ __device__ __noinline__ void epi_state_wide_t(int nu_it, double cf, double th, i
           if (do_last) epi_st(P.X + eo[h] + c.NXP + i, xi);
           if (do_pre) {  // the next backward's fill of this element
             const double wsn = extrap(ns, ycs[h][m], q.cfn), wzn = extrap(nz, ycz[h][m], q.cfn);
-            x[i] = __dadd_rn(__dmul_rn(wsn, ds), __dmul_rn(wzn, dz));
+            const double fv = __dadd_rn(__dmul_rn(wsn, ds), __dmul_rn(wzn, dz));
+            if (FGW) stcg(S.FG + (size_t)d[0] * S.FL + i, fv);
+            else x[i] = fv;
           }
         }
       }
@@ -2020,8 +2025,8 @@ __device__ __noinline__ void epi_state_wide_t(int nu_it, double cf, double th, i
   *rmax_io = rmax;
 }
 
-__device__ __forceinline__ bool epi_fast(const Params& P, int nu_it, bool pre) {
-  return pre && !is_last(P, nu_it) && !P.record_all && P.scaled && g_sp.psi_smem;
+__device__ __forceinline__ bool epi_fast(const Params& P, int nu_it, int pre) {
+  return pre != 0 && !is_last(P, nu_it) && !P.record_all && P.scaled && g_sp.psi_smem;
 }
 
 #ifndef TSMPC_PSI2
@@ -2031,7 +2036,7 @@ __device__ __forceinline__ bool epi_fast(const Params& P, int nu_it, bool pre) {
 // 64-lane groups, 16-byte loads and stores of every array (half the memory
 // instructions and row look-ups), the same operations per element in the same
 // order (bitwise equal).  Needs even n_u and even shared-memory offsets.
-template <int MODE>
+template <int MODE, bool FGW>
 __device__ __noinline__ void epi_psi_wide_v2(int nu_it, double cf, double th, int nrows, int cur, bool pre,
                                              double cfn, int trb_o, int trl, int seg0) {
   const SParams& S = g_sp;
@@ -2093,7 +2098,10 @@ __device__ __noinline__ void epi_psi_wide_v2(int nu_it, double cf, double th, in
       one(yc[u].y, yp[u].y, ua[u].y, uu.y, dp.y, ulo.y, uhi.y, ny.y, na.y, fl.y);
       __stcg(reinterpret_cast<double2*>(Yn + eo[u]), ny);
       __stcg(reinterpret_cast<double2*>(UA + eo[u]), na);
-      *us = fl;  // the next backward's fill of this element pair
+      if (FGW)  // the next backward's fill of this element pair
+        __stcg(reinterpret_cast<double2*>(S.FG + (size_t)d[0] * S.FL + c.NXP + k), fl);
+      else
+        *us = fl;
     };
     if (r0 + (CH - 1) * NG < nrows) {
 #pragma unroll
@@ -2114,37 +2122,53 @@ __device__ __forceinline__ bool psi_pairs(int cur, int trb_o, int trl) {
   const int o = c.nu | c.psi_o | (int)(c.B() - s_dyn) | (trb_o >= 0 ? (trb_o | trl) : 0) | (c.NXP * 2 * c.E);
   return (a & 15) == 0 && (o & 1) == 0;
 }
+// pre: 0 no next fill, 1 next fill into shared memory, 2 next fill into FG (HBM).
+// FGD: the caller may ask for 2 (compiled apart: the one-tile CTAs, which never
+// do, keep the dispatch -- and the register allocation -- without the FG variants)
+template <bool FGD>
 __device__ __forceinline__ void epi_psi_wide(int nu_it, double cf, double th, int nrows, int cur, double* rmax,
-                                             bool pre, double cfn, int trb_o = -1, int trl = 0, int seg0 = 0) {
+                                             int pre, double cfn, int trb_o = -1, int trl = 0, int seg0 = 0) {
   const Params& P = g_sp.P;
 #ifdef TSMPC_KO
   if (TSMPC_KO & 1) return;  // timing experiment only: results are wrong
 #endif
+  if (!FGD) pre = pre != 0;
   if (!TSMPC_WANT_T || is_last(P, nu_it) || P.record_all)
     epi_psi_wide_t<true, 0>(nu_it, cf, th, nrows, cur, rmax, pre, cfn, trb_o, trl, seg0);
   else if (TSMPC_FASTEPI && epi_fast(P, nu_it, pre) && TSMPC_PSI2 && psi_pairs(cur, trb_o, trl))
-    trb_o >= 0 ? epi_psi_wide_v2<2>(nu_it, cf, th, nrows, cur, pre, cfn, trb_o, trl, seg0)
-               : epi_psi_wide_v2<1>(nu_it, cf, th, nrows, cur, pre, cfn, trb_o, trl, seg0);
+    FGD && pre == 2
+        ? (trb_o >= 0 ? epi_psi_wide_t<false, 0>(nu_it, cf, th, nrows, cur, rmax, pre, cfn, trb_o, trl, seg0)
+                      : epi_psi_wide_v2<1, FGD>(nu_it, cf, th, nrows, cur, true, cfn, trb_o, trl, seg0))
+        : trb_o >= 0 ? epi_psi_wide_v2<2, false>(nu_it, cf, th, nrows, cur, true, cfn, trb_o, trl, seg0)
+                     : epi_psi_wide_v2<1, false>(nu_it, cf, th, nrows, cur, true, cfn, trb_o, trl, seg0);
   else if (TSMPC_FASTEPI && epi_fast(P, nu_it, pre))
     trb_o >= 0 ? epi_psi_wide_t<false, 2>(nu_it, cf, th, nrows, cur, rmax, pre, cfn, trb_o, trl, seg0)
                : epi_psi_wide_t<false, 1>(nu_it, cf, th, nrows, cur, rmax, pre, cfn, trb_o, trl, seg0);
   else
     epi_psi_wide_t<false, 0>(nu_it, cf, th, nrows, cur, rmax, pre, cfn, trb_o, trl, seg0);
 }
-template <int XS>
+template <int XS, bool FGD>
 __device__ __forceinline__ void epi_state_wide(int nu_it, double cf, double th, int nrows, int cur, double* rmax,
-                                               bool pre, double cfn, int trb_o = -1, int trl = 0, int seg0 = 0) {
+                                               int pre, double cfn, int trb_o = -1, int trl = 0, int seg0 = 0) {
   const Params& P = g_sp.P;
 #ifdef TSMPC_KO
   if (TSMPC_KO & 2) return;  // timing experiment only: results are wrong
 #endif
-  if (!TSMPC_WANT_T || is_last(P, nu_it) || P.record_all)
-    epi_state_wide_t<XS, true, 0>(nu_it, cf, th, nrows, cur, rmax, pre, cfn, trb_o, trl, seg0);
+  const bool pb = pre != 0;
+  if (FGD && pre == 2) {  // next fill into FG
+    if (!TSMPC_WANT_T || is_last(P, nu_it) || P.record_all)
+      epi_state_wide_t<XS, true, 0, true>(nu_it, cf, th, nrows, cur, rmax, pb, cfn, trb_o, trl, seg0);
+    else if (TSMPC_FASTEPI && epi_fast(P, nu_it, pre) && trb_o < 0)
+      epi_state_wide_t<XS, false, 1, true>(nu_it, cf, th, nrows, cur, rmax, pb, cfn, trb_o, trl, seg0);
+    else
+      epi_state_wide_t<XS, false, 0, true>(nu_it, cf, th, nrows, cur, rmax, pb, cfn, trb_o, trl, seg0);
+  } else if (!TSMPC_WANT_T || is_last(P, nu_it) || P.record_all)
+    epi_state_wide_t<XS, true, 0, false>(nu_it, cf, th, nrows, cur, rmax, pb, cfn, trb_o, trl, seg0);
   else if (TSMPC_FASTEPI && epi_fast(P, nu_it, pre))
-    trb_o >= 0 ? epi_state_wide_t<XS, false, 2>(nu_it, cf, th, nrows, cur, rmax, pre, cfn, trb_o, trl, seg0)
-               : epi_state_wide_t<XS, false, 1>(nu_it, cf, th, nrows, cur, rmax, pre, cfn, trb_o, trl, seg0);
+    trb_o >= 0 ? epi_state_wide_t<XS, false, 2, false>(nu_it, cf, th, nrows, cur, rmax, pb, cfn, trb_o, trl, seg0)
+               : epi_state_wide_t<XS, false, 1, false>(nu_it, cf, th, nrows, cur, rmax, pb, cfn, trb_o, trl, seg0);
   else
-    epi_state_wide_t<XS, false, 0>(nu_it, cf, th, nrows, cur, rmax, pre, cfn, trb_o, trl, seg0);
+    epi_state_wide_t<XS, false, 0, false>(nu_it, cf, th, nrows, cur, rmax, pb, cfn, trb_o, trl, seg0);
 }
 
 // backward sweep of wide tile ti (factor.py:142-156): fill from HBM (unless the
@@ -2152,8 +2176,8 @@ __device__ __forceinline__ void epi_state_wide(int nu_it, double cf, double th, 
 // g scan -> t (region A in place for tmode 0, TG for tmode 2), chain heads -> GG / XIQG
 // TMS: the CTA's static vectors are resident in TMEM (s_tm_on; compiled apart, so
 // the multi-tile CTAs keep the plain prefetch code and its register allocation)
-template <bool TMS>
-__device__ __noinline__ void bwd_wide(int ti, double cf, int cur, bool prefilled) {
+template <bool TMS, bool FGK>
+__device__ __noinline__ void bwd_wide(int ti, double cf, int cur, int pf) {
   const SParams& S = g_sp;
   const Ctx c = ctx_of();
   const Params& P = S.P;
@@ -2184,7 +2208,20 @@ __device__ __noinline__ void bwd_wide(int ti, double cf, int cur, bool prefilled
       bpre[m] = TSMPC_PREF && r < nrows && k < nv ? ldcg(S.beta_s + (size_t)c.mt.edge(row0 + r) * c.NVP + k) : 0.0;
     }
   }
-  if (!prefilled) {
+  if (FGK && pf == 2) {
+    // (1) fill rows left in FG by the previous iteration's epilogue: [s | psi^] -> A | B
+    const int hx = c.NXP / 2, per = hx + c.NUP / 2;
+#pragma unroll 1
+    for (int idx = tid; idx < nrows * per; idx += kThreadsS) {
+      const int r = idx / per, q = idx - r * per;
+      const double* src = S.FG + (size_t)c.mt.edge(row0 + r) * S.FL;
+      if (q < hx) cp16(RA + r * LA + 2 * q, src + 2 * q);
+      else cp16(RB + r * c.NUP + 2 * (q - hx), src + c.NXP + 2 * (q - hx));
+    }
+    cp_commit();
+    cp_wait<0>();
+    __syncthreads();
+  } else if (pf == 0) {
     // (1) fill: s = D_sig w_sig + D_zeta w_zeta -> A ; psi^ = D_psi w_psi -> B
     const double* Y = P.ybuf[cur];
     const double* Yp = P.ybuf[cur ^ 1];
@@ -2389,8 +2426,8 @@ __device__ __noinline__ void bwd_wide(int ti, double cf, int cur, bool prefilled
 // forward sweep of wide tile ti (factor.py:158-170) + epilogue; in split mode the
 // chains run with zero trunk input and the trunk terms and the epilogue follow in
 // fwd_finish_wide
-template <int XS, bool TMS>
-__device__ __noinline__ void fwd_wide(int ti, int nu_it, double cf, double th, int cur, double* rmax, bool pre,
+template <int XS, bool TMS, bool FGK>
+__device__ __noinline__ void fwd_wide(int ti, int nu_it, double cf, double th, int cur, double* rmax, int pre,
                                       double cfn) {
   const SParams& S = g_sp;
   const Ctx c = ctx_of();
@@ -2529,7 +2566,7 @@ __device__ __noinline__ void fwd_wide(int ti, int nu_it, double cf, double th, i
                                       TSMPC_PREF ? upre[m] : ldcg(P.uhat + (size_t)c.mt.edge(row0 + r) * c.NUP + k));
     }
   }
-  if (!S.split) epi_psi_wide(nu_it, cf, th, nrows, cur, rmax, pre, cfn);
+  if (!S.split) epi_psi_wide<FGK && !TMS>(nu_it, cf, th, nrows, cur, rmax, pre, cfn);
   {
     const double* adiag = c.adiag();
     const double* pr = c.proot();
@@ -2559,7 +2596,7 @@ __device__ __noinline__ void fwd_wide(int ti, int nu_it, double cf, double th, i
   TSMPC_MARK(P, 7, tm_);
   if (S.split) return;  // trunk terms and epilogue: fwd_finish_wide
   // (5) epilogue, state blocks (warp per row)
-  epi_state_wide<XS>(nu_it, cf, th, nrows, cur, rmax, pre, cfn);
+  epi_state_wide<XS, FGK && !TMS>(nu_it, cf, th, nrows, cur, rmax, pre, cfn);
   __syncthreads();
   TSMPC_MARK(P, 8, tm_);
 }
@@ -2635,9 +2672,9 @@ __device__ __noinline__ void fwd_finish_wide(int ti, int nu_it, double cf, doubl
   TSMPC_MARK(P, 14, tm_);
   // u += du_tp folded into the psi epilogue, x += (d+1) B du_tp + x_tp (A = I) into the state one
   const int tro = (int)(tr - s_dyn);
-  epi_psi_wide(nu_it, cf, th, nrows, cur, rmax, pre, cfn, tro, HL, seg0);
+  epi_psi_wide<false>(nu_it, cf, th, nrows, cur, rmax, pre, cfn, tro, HL, seg0);
   TSMPC_MARK(P, 15, tm_);
-  epi_state_wide<XS>(nu_it, cf, th, nrows, cur, rmax, pre, cfn, S.a_unit ? tro : -1, HL, seg0);
+  epi_state_wide<XS, false>(nu_it, cf, th, nrows, cur, rmax, pre, cfn, S.a_unit ? tro : -1, HL, seg0);
   __syncthreads();
   TSMPC_MARK(P, 8, tm_);
 }
@@ -2663,8 +2700,8 @@ __device__ __noinline__ void trunk_own_rows_wide(int nu_it, double cf, double th
       d[4] = 0;
     }
     __syncthreads();
-    epi_psi_wide(nu_it, cf, th, nb, cur, rmax, false, 0.0);
-    epi_state_wide<XS>(nu_it, cf, th, nb, cur, rmax, false, 0.0);
+    epi_psi_wide<false>(nu_it, cf, th, nb, cur, rmax, 0, 0.0);
+    epi_state_wide<XS, false>(nu_it, cf, th, nb, cur, rmax, 0, 0.0);
     __syncthreads();
   }
 }
@@ -2968,7 +3005,7 @@ __device__ __noinline__ void tm_static_fill() {
   tm_fill_done();
 }
 
-template <int XS>
+template <int XS, bool FGK>
 __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
   cg::grid_group grid = cg::this_grid();
   const SParams& S = g_sp;
@@ -3056,6 +3093,11 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
   double rmax = 0.0;
   unsigned int sub_target = 0;  // trunk-CTA barrier episodes x split_n (split mode)
   double cf = P.coef[win.nu0], th = P.theta[win.nu0];
+  // FG fill rows: the buffer exists, 16-byte copies line up with the work regions,
+  // and the CTA runs the forward of fwd_wide<XS, false> (split-mode and TMEM CTAs
+  // keep every fill in shared memory or take it from the dual rows)
+  const bool fg_ok = FGK && S.FG != nullptr && !S.split && !s_tm_on &&
+                     (((int)(c.A() - s_dyn) | (int)(c.B() - s_dyn) | c.LA | c.NXP | c.NUP | S.FL) & 1) == 0;
   for (int nu = win.nu0; nu < win.nu1; ++nu) {
     const int cur = (P.slot0 + nu) & 1;
     if (P.tol > 0.0 && nu > win.nu0 && nu % P.check_every == 0) {
@@ -3071,10 +3113,18 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
     }
     const int nn = nu + 1 < P.iters ? nu + 1 : nu;
     const double cf_n = P.coef[nn], th_n = P.theta[nn];
+    // where tile t's epilogue leaves the next iteration's fill: shared memory when
+    // this launch runs the next backward and t is the tile it starts with, else FG
+    auto pre_of = [&](int t) -> int {
+      if (S.wide_prefill && t == nt - 1 && nu + 1 < win.nu1 && do_a) return 1;
+      return fg_ok && nu + 1 < P.iters ? 2 : 0;
+    };
     if (do_a) {
       for (int t = nt - 1; t >= 0; --t) {
-        const bool pf = S.wide_prefill && t == nt - 1 && nu > win.nu0;
-        s_tm_on ? bwd_wide<true>(t, cf, cur, pf) : bwd_wide<false>(t, cf, cur, pf);
+        // fill source: 1 left in shared memory by this launch's previous iteration,
+        // 2 left in FG by the previous iteration, 0 the dual rows
+        const int pf = S.wide_prefill && t == nt - 1 && nu > win.nu0 ? 1 : (fg_ok && nu > 0 ? 2 : 0);
+        s_tm_on ? bwd_wide<true, FGK>(t, cf, cur, pf) : bwd_wide<false, FGK>(t, cf, cur, pf);
       }
       if (S.sharded && trunk) {
         grid.sync();
@@ -3095,8 +3145,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
       const unsigned it = (unsigned)(nu - win.nu0 + 1);
       if (chain_cta) {
         for (int t = 0; t < nt; ++t)
-          s_tm_on ? fwd_wide<XS, true>(t, nu, cf, th, cur, &rmax, false, 0.0)
-                  : fwd_wide<XS, false>(t, nu, cf, th, cur, &rmax, false, 0.0);
+          s_tm_on ? fwd_wide<XS, true, FGK>(t, nu, cf, th, cur, &rmax, 0, 0.0)
+                  : fwd_wide<XS, false, FGK>(t, nu, cf, th, cur, &rmax, 0, 0.0);
         TSMPC_MARK(P, 10, tb_);
         signal_wait(S.sub_ctr + 2, it * (unsigned)S.split_n);
         TSMPC_MARK(P, 9, tb_);
@@ -3144,8 +3194,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
           P.xavg[i] = __dadd_rn(__dmul_rn(P.xavg[i], om), __dmul_rn(th, c.proot()[i]));
       }
       for (int t = 0; t < nt; ++t)
-        s_tm_on ? fwd_wide<XS, true>(t, nu, cf, th, cur, &rmax, S.wide_prefill && t == nt - 1 && nu + 1 < win.nu1, cf_n)
-                : fwd_wide<XS, false>(t, nu, cf, th, cur, &rmax, S.wide_prefill && t == nt - 1 && nu + 1 < win.nu1, cf_n);
+        s_tm_on ? fwd_wide<XS, true, FGK>(t, nu, cf, th, cur, &rmax, pre_of(t), cf_n)
+                : fwd_wide<XS, false, FGK>(t, nu, cf, th, cur, &rmax, pre_of(t), cf_n);
     }
     if (do_b) {
       if (nu == P.iters - 1 || P.record_all || is_check(P, nu)) {
@@ -3179,9 +3229,10 @@ namespace tsmpc {
 // the persistent kernel a plan runs: split / streamed / resident modes share
 // apg_sparse_kernel; wide plans run apg_wide_kernel<XS> (XS = state components per
 // lane of the warp-per-row state epilogue: n_x <= 64 -> 2, <= 128 -> 4)
-const void* sparse_kernel_fn(int wide, int nx) {
+const void* sparse_kernel_fn(int wide, int nx, bool fg) {
   if (!wide) return (const void*)apg_sparse_kernel;
-  return nx <= 64 ? (const void*)apg_wide_kernel<2> : (const void*)apg_wide_kernel<4>;
+  if (fg) return nx <= 64 ? (const void*)apg_wide_kernel<2, true> : (const void*)apg_wide_kernel<4, true>;
+  return nx <= 64 ? (const void*)apg_wide_kernel<2, false> : (const void*)apg_wide_kernel<4, false>;
 }
 
 // g_sp is one per device and shared by every plan of the process: launches from
@@ -3243,7 +3294,7 @@ cudaError_t sparse_launch(const SParams& S, LaunchWin w, int ctas, size_t smem, 
   cudaError_t e = sparse_params_upload(S, stream);
   if (e != cudaSuccess) return e;
   void* args[] = {&w};
-  e = cudaLaunchCooperativeKernel(sparse_kernel_fn(S.wide, S.P.nx), dim3(ctas), dim3(kThreadsS), args, smem, stream);
+  e = cudaLaunchCooperativeKernel(sparse_kernel_fn(S.wide, S.P.nx, S.FL > 0), dim3(ctas), dim3(kThreadsS), args, smem, stream);
   if (e != cudaSuccess) return e;
   int dev = 0;
   cudaGetDevice(&dev);

@@ -556,13 +556,15 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
     // no slot rows: t stays in region A when a CTA has one tile (and the launch runs
     // whole iterations), else it goes through TG
     int max_rows_w = 0;
-    bool any_t0 = false;
+    bool any_t0 = false, any_t2 = false;
     for (int c = 0; c < C; ++c) {
       metas[c][6] = 0;
       metas[c][7] = (metas[c][0] <= 1 && !sharded) ? 0 : 2;
       any_t0 |= metas[c][7] == 0;
+      any_t2 |= metas[c][7] == 2;
       max_rows_w = std::max(max_rows_w, cta_rows[c]);
     }
+    S.FL = any_t2 ? NXP + NUP : 0;  // fill rows through HBM (FG) for multi-tile / sharded CTAs
     if (std::getenv("TSMPC_PLAN_DEBUG"))
       std::fprintf(stderr, "plan_sparse wide: tcap=%d off=%lld ints_d=%lld limit=%lld psi=%d\n", tcap, off, ints_d,
                    limit_d, (int)psi_in_smem);

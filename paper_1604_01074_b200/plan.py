@@ -124,7 +124,7 @@ class DevicePlan:
         keys = ("levels", "ctas", "tiles", "segments", "smem_bytes", "diag_A", "threads",
                 "tile_rows", "sms", "collapsed", "trunk_edges", "sparse", "resident_ctas",
                 "sharded", "rank", "world", "owned_chain_edges", "total_chains", "trunk_ctas",
-                "wide", "exchange_doubles")
+                "wide", "exchange_doubles", "fill_rows_hbm")
         buf = np.zeros(len(keys), dtype=np.int64)
         nat.check(self._lib.tsmpc_plan_info(self._h, nat.iptr(buf), len(keys)), "tsmpc_plan_info")
         d = dict(zip(keys, (int(v) for v in buf)))

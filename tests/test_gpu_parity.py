@@ -204,3 +204,34 @@ def test_split_mode_matches_grid_barrier_mode(tree_name, monkeypatch):
         assert rel_err(a[f], b[f]) <= 1e-9, (f, rel_err(a[f], b[f]))
     np.testing.assert_allclose(a["resid_trace"], b["resid_trace"], rtol=1e-8, atol=1e-9)
     assert abs(a["gap"] - b["gap"]) <= 1e-8 * max(1.0, abs(b["gap"]))
+
+
+@pytest.mark.parametrize("tree_name,shard,record", [("W4k", False, False), ("W4k", False, True),
+                                                    ("SMPC8", True, False)])
+def test_fill_rows_through_hbm_equal_dual_row_fill(tree_name, shard, record, monkeypatch):
+    """Multi-tile and sharded wide CTAs take the next backward's fill rows from FG,
+    written by the previous iteration's epilogue (also across launches: per-iteration
+    windows of record_residuals, the two launches of a sharded iteration); the same
+    operations as the fill from both dual rows, so the bits must match TSMPC_NO_FG."""
+    import bench
+    from paper_1604_01074_b200.shard import nccl_unique_id
+    W = bench.build_workload(tree_name)
+    iters = 24
+    th, cf = engine.theta_schedule(iters)
+    outs = []
+    for env in ("0", "1"):
+        if env == "1":
+            monkeypatch.setenv("TSMPC_NO_FG", "1")
+        else:
+            monkeypatch.delenv("TSMPC_NO_FG", raising=False)
+        plan = DevicePlan(W["model"], W["tree"], W["factor"], W["scaling"],
+                          shard=(0, 1, nccl_unique_id()) if shard else None)
+        assert plan.info()["fill_rows_hbm"] == (0 if env == "1" else 1)
+        plan.set_cache(W["caches"][0], W["model"])
+        outs.append(plan.solve(W["p"], iters, 0.05, theta=th, coef=cf, record_residuals=record))
+    a, b = outs
+    for f in ("u0", "x", "u", "x_avg", "u_avg", "dual_sig", "dual_zeta", "dual_psi"):
+        assert np.array_equal(a[f], b[f]), f
+    assert a["gap"] == b["gap"]
+    if record:
+        assert np.array_equal(a["resid_trace"], b["resid_trace"])
