@@ -44,7 +44,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "SMPC solve time (ms) & APG iters/s vs scenario count, Barcelona DWN N=24"
 BYTES_PER_EDGE = 10_784        # compulsory fp64 bytes per edge per iteration
-SWEEP = ("CE", "SMPC1", "SMPC3", "SMPC8", "W4k")
+SWEEP = ("CE", "SMPC1", "SMPC3", "SMPC8", "W4k", "W16k")
 
 
 def workload_name(tree_name: str, tree, iters: int) -> str:
@@ -550,7 +550,7 @@ def sweep(args, local, have, cpu=True):
                "hbm_frac": E * BYTES_PER_EDGE * args.iters / (loop / 1e3) / 1e9 / hbm_peak,
                "ctas": info["ctas"], "path": info["path"], "trunk_ctas": info["trunk_ctas"]}
         if cpu:
-            c = cpu_baseline(W, lam, args, budget_s=3.0 if name != "W4k" else 6.0)
+            c = cpu_baseline(W, lam, args, budget_s=6.0 if name.startswith("W") else 3.0)
             ent["cpu_port_iters_per_s"] = c["value"]
             ent["cpu_sample"] = c["sample"]
             ent["speedup_vs_cpu_port"] = ent["iters_per_s"] / c["value"]

@@ -781,7 +781,7 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
                                              shard ? srank : 0, shard ? sworld : 1);
       // fill rows through HBM (FG) for multi-tile / sharded wide CTAs: the kernel variant
       // compiled with them (the others keep the one-tile code as it was)
-      if (!hp.S.wide || std::getenv("TSMPC_NO_FG")) hp.S.FL = 0;
+      if (!hp.S.wide || (std::getenv("TSMPC_NO_FG") && !hp.S.rows_window)) hp.S.FL = 0;
       const void* kfn = sparse_kernel_fn(hp.S.wide, nx, hp.S.FL > 0);
       int occ_s = 0;
       if (hp.ok) {

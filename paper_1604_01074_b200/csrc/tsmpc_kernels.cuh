@@ -213,6 +213,12 @@ struct SParams {
   // reading both dual rows and extrapolating
   double* FG;
   int FL;                       // NXP + NUP
+  // per-row / per-chain meta windows (CTAs with many tiles whose full meta does not fit
+  // in shared memory, e.g. W16k): only the header, tiles, needs, levels and own rows
+  // are staged at launch; the rows {edge, stage, inv2p} and chain segments of the
+  // tile being processed are copied into a window (O_WIN ints after the staged ints:
+  // rows then, 4 tile_cap ints further, segments) before each tile
+  int rows_window, O_WIN;
   int hsum_nseg;                // wide split mode: chains per chain CTA the head-sum scratch holds
 };
 

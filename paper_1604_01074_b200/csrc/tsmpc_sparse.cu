@@ -50,6 +50,8 @@ extern __shared__ __align__(16) double s_dyn[];
 __constant__ SParams g_sp;
 // the launch window of the running kernel (set from the kernel argument at entry)
 __shared__ LaunchWin s_win;
+// meta windows (SParams::rows_window): first row / segment of the staged tile
+__shared__ int s_row_off, s_seg_off;
 
 namespace {
 
@@ -66,14 +68,15 @@ struct Meta {
   const int* m;
   int ntiles, nrows, nsegs, nneed, nlev, nown, resident, tmode;
   const int *tiles, *rows, *segs, *needs, *lev, *own;
-  __device__ void bind(const int* base) {
+  // rows_w / segs_w: the meta windows of the current tile (SParams::rows_window), else null
+  __device__ void bind(const int* base, const int* rows_w = nullptr, const int* segs_w = nullptr) {
     m = base;
     ntiles = m[0]; nrows = m[1]; nsegs = m[2]; nneed = m[3]; nlev = m[4]; nown = m[5]; resident = m[6];
     tmode = m[7];
     tiles = m + 8;
-    rows = tiles + 4 * ntiles;
-    segs = rows + 4 * nrows;
-    needs = segs + 4 * nsegs;
+    rows = rows_w ? rows_w : tiles + 4 * ntiles;
+    segs = rows_w ? segs_w : rows + 4 * nrows;
+    needs = rows_w ? tiles + 4 * ntiles : segs + 4 * nsegs;
     lev = needs + 4 * nneed;
     own = lev + nlev + 1;
   }
@@ -272,7 +275,10 @@ __device__ __forceinline__ Ctx ctx_of() {
   c.work = s_dyn + S.O_WORK;
   c.slot = s_dyn + S.O_SLOT;
   const int* ints = reinterpret_cast<const int*>(s_dyn + S.O_INT);
-  c.mt.bind(ints);
+  if (S.rows_window)
+    c.mt.bind(ints, ints + S.O_WIN - 4 * s_row_off, ints + S.O_WIN + 4 * S.tile_cap - 4 * s_seg_off);
+  else
+    c.mt.bind(ints);
   c.spi = ints + S.meta_max;
   c.spv = s_dyn + S.O_SPV;
   return c;
@@ -3005,6 +3011,29 @@ __device__ __noinline__ void tm_static_fill() {
   tm_fill_done();
 }
 
+// meta windows (SParams::rows_window): copy tile t's rows and chain segments from the
+// plan's meta in global memory into the window; ctx_of() rebinds to it
+__device__ __noinline__ void win_stage(int t) {
+  const SParams& S = g_sp;
+  int* ints = reinterpret_cast<int*>(s_dyn + S.O_INT);
+  const int* gm = S.meta + __ldg(S.meta_ptr + blockIdx.x);
+  const int ntl = ints[0], nrw = ints[1];
+  const int row0 = ints[8 + 4 * t], nr = ints[8 + 4 * t + 1], seg0 = ints[8 + 4 * t + 2], ns = ints[8 + 4 * t + 3];
+  __syncthreads();  // the previous tile's readers are done with the window
+  int* w = ints + S.O_WIN;
+  const int* grows = gm + 8 + 4 * ntl + 4 * row0;
+  const int* gsegs = gm + 8 + 4 * ntl + 4 * nrw + 4 * seg0;
+#pragma unroll 1
+  for (int i = threadIdx.x; i < 4 * nr; i += kThreadsS) w[i] = __ldg(grows + i);
+#pragma unroll 1
+  for (int i = threadIdx.x; i < 4 * ns; i += kThreadsS) w[4 * S.tile_cap + i] = __ldg(gsegs + i);
+  if (threadIdx.x == 0) {
+    s_row_off = row0;
+    s_seg_off = seg0;
+  }
+  __syncthreads();
+}
+
 template <int XS, bool FGK>
 __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
   cg::grid_group grid = cg::this_grid();
@@ -3051,7 +3080,15 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
     int* ints = reinterpret_cast<int*>(s_dyn + S.O_INT);
     const int m0 = __ldg(S.meta_ptr + blockIdx.x), m1 = __ldg(S.meta_ptr + blockIdx.x + 1);
 #pragma unroll 1
-    for (int i = threadIdx.x; i < m1 - m0; i += kThreadsS) ints[i] = __ldg(S.meta + m0 + i);
+    if (S.rows_window) {  // everything but the rows and segments (staged per tile)
+      const int lo = 8 + 4 * __ldg(S.meta + m0), gap = 4 * (__ldg(S.meta + m0 + 1) + __ldg(S.meta + m0 + 2));
+#pragma unroll 1
+      for (int i = threadIdx.x; i < m1 - m0 - gap; i += kThreadsS) ints[i] = __ldg(S.meta + m0 + (i < lo ? i : i + gap));
+      if (threadIdx.x == 0) s_row_off = s_seg_off = 0;
+    } else {
+#pragma unroll 1
+      for (int i = threadIdx.x; i < m1 - m0; i += kThreadsS) ints[i] = __ldg(S.meta + m0 + i);
+    }
 #pragma unroll 1
     for (int i = threadIdx.x; i < S.n_spi; i += kThreadsS) ints[S.meta_max + i] = __ldg(S.spi + i);
     double* spv = s_dyn + S.O_SPV;
@@ -3124,6 +3161,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
         // fill source: 1 left in shared memory by this launch's previous iteration,
         // 2 left in FG by the previous iteration, 0 the dual rows
         const int pf = S.wide_prefill && t == nt - 1 && nu > win.nu0 ? 1 : (fg_ok && nu > 0 ? 2 : 0);
+        if (FGK && S.rows_window) win_stage(t);
         s_tm_on ? bwd_wide<true, FGK>(t, cf, cur, pf) : bwd_wide<false, FGK>(t, cf, cur, pf);
       }
       if (S.sharded && trunk) {
@@ -3193,9 +3231,11 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
         for (int i = threadIdx.x; i < c.nx; i += kThreadsS)
           P.xavg[i] = __dadd_rn(__dmul_rn(P.xavg[i], om), __dmul_rn(th, c.proot()[i]));
       }
-      for (int t = 0; t < nt; ++t)
+      for (int t = 0; t < nt; ++t) {
+        if (FGK && S.rows_window) win_stage(t);
         s_tm_on ? fwd_wide<XS, true, FGK>(t, nu, cf, th, cur, &rmax, pre_of(t), cf_n)
                 : fwd_wide<XS, false, FGK>(t, nu, cf, th, cur, &rmax, pre_of(t), cf_n);
+      }
     }
     if (do_b) {
       if (nu == P.iters - 1 || P.record_all || is_check(P, nu)) {

@@ -541,9 +541,30 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
   S.n_work = (int)even((long long)tcap * (S.LA + NUP));
   off += S.n_work;
   S.O_SLOT = (int)off;
-  const long long ints_d = ((long long)meta_max + S.n_spi + 1) / 2 + 1;
+  long long ints_d = ((long long)meta_max + S.n_spi + 1) / 2 + 1;
   const long long limit_d = (long long)(smem_limit / sizeof(double));
-  const long long slot_avail = limit_d - off - ints_d;
+  long long slot_avail = limit_d - off - ints_d;
+  S.rows_window = 0;
+  S.O_WIN = 0;
+  if (wide && slot_avail < 0 && !std::getenv("TSMPC_NO_WINDOW")) {
+    // meta windows: the staged ints keep everything but the rows and segments, which
+    // come in per tile (window of 4 tcap row ints + 4 tcap segment ints)
+    int compact = 0;
+    bool multi = false;
+    for (int c = 0; c < C; ++c) {
+      compact = std::max(compact, (int)metas[c].size() - 4 * metas[c][1] - 4 * metas[c][2]);
+      multi |= metas[c][0] > 1;
+    }
+    const int wmeta = (compact + 1) / 2 * 2 + 8 * tcap;
+    const long long ints_w = ((long long)wmeta + S.n_spi + 1) / 2 + 1;
+    if (multi && limit_d - off - ints_w >= 0) {
+      S.rows_window = 1;
+      S.O_WIN = (compact + 1) / 2 * 2;
+      meta_max = wmeta;
+      ints_d = ints_w;
+      slot_avail = limit_d - off - ints_d;
+    }
+  }
   // slot rows: both dual rows + ergodic rows; t rows join them only for resident
   // CTAs with several tiles (tmode 1); a single resident tile keeps t in region A
   const long long base_ld = 2LL * S.YW + NXP + NUP;
@@ -566,8 +587,8 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
     }
     S.FL = any_t2 ? NXP + NUP : 0;  // fill rows through HBM (FG) for multi-tile / sharded CTAs
     if (std::getenv("TSMPC_PLAN_DEBUG"))
-      std::fprintf(stderr, "plan_sparse wide: tcap=%d off=%lld ints_d=%lld limit=%lld psi=%d\n", tcap, off, ints_d,
-                   limit_d, (int)psi_in_smem);
+      std::fprintf(stderr, "plan_sparse wide: tcap=%d off=%lld ints_d=%lld limit=%lld psi=%d window=%d\n", tcap, off,
+                   ints_d, limit_d, (int)psi_in_smem, S.rows_window);
     if (slot_avail < 0) {
       if (psi_in_smem)
         return plan_sparse(t, ops, NXP, NUP, NVP, max_ctas, smem_limit, sharded, rank, world, false, allow_split,

@@ -4,7 +4,9 @@ the CPU oracle, a few APG iterations each.
 The golden fixtures stop at SMPC3; these cases exercise the plans that only the
 large trees produce: SMPC8 runs the streamed tile slots with 3-4 chains per CTA
 and two grid barriers per iteration (no split mode), W4k (86,561 edges) adds
-multi-tile CTAs with trunk rows spread over every CTA.  The oracle
+multi-tile CTAs with trunk rows spread over every CTA, W16k (345,121 edges,
+16,384 scenarios) CTAs of 28 tiles whose per-row meta is staged
+tile by tile.  The oracle
 (`oracle/tsmpc_oracle.py:122-169`, the reference loop `engine.py:519-600`) is
 the checker only.
 
@@ -31,7 +33,8 @@ TOL = 1e-9
 
 
 @pytest.mark.parametrize("tree_name,iters,path", [("SMPC3", 6, "sparse"), ("SMPC8", 6, "sparse"),
-                                                  ("SMPC8", 3, "dense"), ("W4k", 3, "sparse")])
+                                                  ("SMPC8", 3, "dense"), ("W4k", 3, "sparse"),
+                                                  ("W16k", 2, "sparse")])
 def test_full_size_tree_matches_oracle(tree_name, iters, path, monkeypatch):
     import bench
     monkeypatch.setenv("TSMPC_FORCE_DENSE", "1" if path == "dense" else "0")
@@ -43,6 +46,8 @@ def test_full_size_tree_matches_oracle(tree_name, iters, path, monkeypatch):
     assert info["sparse"] == (1 if path == "sparse" else 0), info["path"]
     if tree_name != "SMPC3" and path == "sparse":
         assert info["wide"] == 1 and info["resident_ctas"] == 0, info
+    if tree_name == "W16k":  # 28 tiles per CTA: per-tile meta windows, fill rows through HBM
+        assert info["tiles"] >= 28 * 148 - 148 and info["fill_rows_hbm"] == 1, info
     lam = 0.05
     th, cf = engine.theta_schedule(iters)
     out = plan.solve(W["p"], iters, lam, theta=th, coef=cf, skip_gap=True, record_residuals=True)
