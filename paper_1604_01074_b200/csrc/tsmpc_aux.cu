@@ -695,6 +695,159 @@ __global__ void __launch_bounds__(256) gap_dykstra_comp_kernel(EdgeCtx c, const 
     if (i < n) uf[(size_t)e * c.NUP + ui[i]] = y[i];
 }
 
+// The same per-(edge, junction row) Dykstra in two passes, for grids too large to be
+// co-resident (SMPC8: 178k components): pass 1 runs every component's sweeps and
+// records the per-sweep maxima over all edges (warp, CTA, then one global atomic per
+// CTA and sweep); a component stops at the first sweep that provably leaves its flows
+// unchanged for good (see dyk_item_sweep): that sweep's change and every later one
+// are exactly zero.  Pass 2 reads the
+// stopping sweep K (the first whose maximum is < 1e-13) and reruns every component
+// from its start for K + 1 sweeps (all 200 when none stops) before the final affine
+// projection.  Per element the operations are those of gap_dykstra_comp_kernel, so
+// the result is bitwise the same.
+namespace {
+struct DykItem {
+  int n, emask, pmask;
+  int ui[kDykCU];
+  double x[kDykCU], inc[kDykCU], lo[kDykCU], hi[kDykCU], ce[kDykCU], cp[kDykCU];
+  double tg;
+};
+__device__ __forceinline__ void dyk_item_load(const EdgeCtx& c, const DykComp& q, int e,
+                                              const double* __restrict__ u0, DykItem& it) {
+  it.n = q.n;
+  it.emask = q.emask;
+  it.pmask = q.pmask;
+  it.tg = c.jrhs[(size_t)e * c.ne + q.row];
+#pragma unroll
+  for (int i = 0; i < kDykCU; ++i) {
+    it.ui[i] = i < it.n ? q.u[i] : 0;
+    it.ce[i] = q.e[i];
+    it.cp[i] = q.p[i];
+    it.x[i] = i < it.n ? u0[(size_t)e * c.NUP + it.ui[i]] : 0.0;
+    it.lo[i] = c.u_min[it.ui[i]];
+    it.hi[i] = c.u_max[it.ui[i]];
+    it.inc[i] = 0.0;
+  }
+}
+__device__ __forceinline__ void dyk_item_project(const DykItem& it, double* y) {
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < kDykCU; ++i)
+    if (i < it.n && (it.emask >> i & 1)) s = fma(it.x[i], it.ce[i], s);
+  const double rr = s - it.tg;
+#pragma unroll
+  for (int i = 0; i < kDykCU; ++i) y[i] = it.x[i] - ((it.pmask >> i & 1) ? fma(rr, it.cp[i], 0.0) : 0.0);
+}
+// one sweep; returns the largest flow change.  *fixed: this sweep and every later one
+// leave the flows unchanged, because with y = P(x) (the same in every later sweep
+// while x does not move) each flow satisfies one of
+//   interior:  y == x, inc == 0, lo <= x <= hi   ->  t = x, x' = x, inc' = 0
+//   at hi:     x == hi, y >= hi, inc >= 0        ->  t = y + inc >= hi, x' = hi, inc' >= 0
+//   at lo:     x == lo, y <= lo, inc <= 0        ->  t <= lo, x' = lo, inc' <= 0
+// (IEEE rounding is monotone, so the inequalities survive y + inc and t - x').
+__device__ __forceinline__ double dyk_item_sweep(DykItem& it, bool* fixed) {
+  double y[kDykCU], mx = 0.0;
+  bool fx = true;
+  dyk_item_project(it, y);
+#pragma unroll
+  for (int i = 0; i < kDykCU; ++i)
+    if (i < it.n) {
+      const double x = it.x[i], c = it.inc[i];
+      fx = fx && ((y[i] == x && c == 0.0 && it.lo[i] <= x && x <= it.hi[i]) ||
+                  (x == it.hi[i] && y[i] >= x && c >= 0.0) || (x == it.lo[i] && y[i] <= x && c <= 0.0));
+      const double t = y[i] + c;
+      const double xn = clip(t, it.lo[i], it.hi[i]);
+      it.inc[i] = t - xn;
+      mx = fmax(mx, fabs(xn - x));
+      it.x[i] = xn;
+    }
+  *fixed = fx;
+  return mx;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(256) gap_dykstra_comp_pass1_kernel(EdgeCtx c, const DykComp* __restrict__ comps,
+                                                                     int ncomp, const int* __restrict__ free_u,
+                                                                     int nfree, const double* __restrict__ u0,
+                                                                     unsigned long long* slots, double* uf) {
+  __shared__ unsigned long long cta_max[kDykMax];
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < kDykMax; i += blockDim.x) cta_max[i] = 0ull;
+  __syncthreads();
+  {  // flows no junction touches: clip(x0) after one sweep (sweep-0 maximum only)
+    double m0 = 0.0;
+    for (int i = tid; i < c.E * nfree; i += nth) {
+      const int e = i / nfree, j = free_u[i - e * nfree];
+      const double x0 = u0[(size_t)e * c.NUP + j];
+      const double t = (x0 - 0.0) + 0.0;
+      const double xn = clip(t, c.u_min[j], c.u_max[j]);
+      m0 = fmax(m0, fabs(xn - x0));
+      uf[(size_t)e * c.NUP + j] = xn - 0.0;
+    }
+    m0 = warp_max(m0);
+    if (lane == 0 && m0 > 0.0) atomicMax(cta_max, (unsigned long long)__double_as_longlong(m0));
+  }
+  const long long total = (long long)c.E * ncomp;
+  // warp-uniform trip count: every lane of a warp runs the same number of items
+  const long long warp0 = (long long)(tid - lane), nwarps_th = nth;
+  for (long long base = warp0; base < total; base += nwarps_th) {
+    const long long item = base + lane;
+    const bool active = item < total;
+    DykItem it;
+    it.n = 0;
+    if (active) {
+      const int e = (int)(item / ncomp);
+      dyk_item_load(c, comps[item - (long long)e * ncomp], e, u0, it);
+    }
+    bool done = !active;
+    for (int s = 0; s < kDykMax; ++s) {
+      if (__all_sync(0xffffffffu, done)) break;  // later sweeps repeat with zero change
+      double mx = 0.0;
+      if (!done) {
+        bool fixed;
+        mx = dyk_item_sweep(it, &fixed);
+        done = fixed;
+      }
+      mx = warp_max(mx);
+      if (lane == 0 && mx > 0.0) atomicMax(cta_max + s, (unsigned long long)__double_as_longlong(mx));
+    }
+  }
+  __syncthreads();
+  for (int s = threadIdx.x; s < kDykMax; s += blockDim.x)
+    if (cta_max[s] != 0ull) atomicMax(slots + s, cta_max[s]);
+}
+
+__global__ void __launch_bounds__(256) gap_dykstra_comp_pass2_kernel(EdgeCtx c, const DykComp* __restrict__ comps,
+                                                                     int ncomp, const double* __restrict__ u0,
+                                                                     const unsigned long long* __restrict__ slots,
+                                                                     double* uf) {
+  __shared__ int s_sweeps;
+  if (threadIdx.x == 0) {
+    int K = -1;
+    for (int it = 0; it < kDykMax && K < 0; ++it)
+      if (__longlong_as_double((long long)slots[it]) < 1e-13) K = it;
+    s_sweeps = K >= 0 ? K + 1 : kDykMax;
+  }
+  __syncthreads();
+  const int nsw = s_sweeps;
+  const long long total = (long long)c.E * ncomp;
+  for (long long item = blockIdx.x * (long long)blockDim.x + threadIdx.x; item < total;
+       item += (long long)gridDim.x * blockDim.x) {
+    const int e = (int)(item / ncomp);
+    DykItem it;
+    dyk_item_load(c, comps[item - (long long)e * ncomp], e, u0, it);
+    bool fixed;
+#pragma unroll 1
+    for (int s = 0; s < nsw; ++s) (void)dyk_item_sweep(it, &fixed);
+    double y[kDykCU];
+    dyk_item_project(it, y);
+#pragma unroll
+    for (int i = 0; i < kDykCU; ++i)
+      if (i < it.n) uf[(size_t)e * c.NUP + it.ui[i]] = y[i];
+  }
+}
+
 // ub_e = u_feas_e B'   (E x NXP)
 __global__ void gap_ub_kernel(EdgeCtx c, const double* __restrict__ uf, double* ub) {
   __shared__ double shm[8][128];

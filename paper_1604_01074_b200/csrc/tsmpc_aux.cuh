@@ -73,6 +73,13 @@ __global__ void gap_dykstra_comp_kernel(EdgeCtx c, const DykComp* __restrict__ c
                                         const int* __restrict__ free_u, int nfree,
                                         const double* __restrict__ u0, unsigned long long* slots,
                                         double* uf);
+__global__ void gap_dykstra_comp_pass1_kernel(EdgeCtx c, const DykComp* __restrict__ comps, int ncomp,
+                                              const int* __restrict__ free_u, int nfree,
+                                              const double* __restrict__ u0, unsigned long long* slots,
+                                              double* uf);
+__global__ void gap_dykstra_comp_pass2_kernel(EdgeCtx c, const DykComp* __restrict__ comps, int ncomp,
+                                              const double* __restrict__ u0,
+                                              const unsigned long long* __restrict__ slots, double* uf);
 __global__ void gap_dykstra_coop_kernel(EdgeCtx c, const double* __restrict__ u0,
                                         unsigned long long* slots, double* st, double* uf);
 __global__ void gap_ub_kernel(EdgeCtx c, const double* uf, double* ub);

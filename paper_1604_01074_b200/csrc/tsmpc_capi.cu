@@ -1327,9 +1327,24 @@ static int compute_gap_terms(tsmpc_plan* pl, const double* yfinal, double* terms
     // junction row) when the rows have disjoint flows, else a warp per edge; else
     // the two-pass form
     int occ = 0, occ_c = 0;
-    if (!pl->dyk_two_pass && !pl->dyk_warp && pl->dyk_ncomp > 0 &&
+    const bool comp_coresident =
+        pl->dyk_ncomp > 0 &&
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, gap_dykstra_comp_kernel, 256, 0) == cudaSuccess &&
-        (long long)E * pl->dyk_ncomp <= (long long)occ_c * pl->sm_count * 256) {
+        (long long)E * pl->dyk_ncomp <= (long long)occ_c * pl->sm_count * 256;
+    if (!pl->dyk_warp && pl->dyk_ncomp > 0 && !pl->dyk_two_pass &&
+        (!comp_coresident || std::getenv("TSMPC_DYKSTRA_COMP2")) && !std::getenv("TSMPC_DYKSTRA_LOCKSTEP")) {
+      // a thread per (edge, junction row) in two passes, when the lockstep grid of
+      // one thread per component cannot be co-resident (SMPC8: 178k components)
+      const long long items = (long long)E * pl->dyk_ncomp;
+      const int gblk = (int)std::max(1LL, std::min((items + 255) / 256, (long long)pl->sm_count * 16));
+      gap_dykstra_comp_pass1_kernel<<<gblk, 256, 0, pl->stream>>>(c, pl->DYKC, pl->dyk_ncomp, pl->DYKF,
+                                                                  pl->dyk_nfree, pl->UAVG, pl->DYK, pl->UF);
+      CU(cudaGetLastError());
+      gap_dykstra_comp_pass2_kernel<<<gblk, 256, 0, pl->stream>>>(c, pl->DYKC, pl->dyk_ncomp, pl->UAVG, pl->DYK,
+                                                                  pl->UF);
+      CU(cudaGetLastError());
+      pl->launches += 1;
+    } else if (!pl->dyk_two_pass && !pl->dyk_warp && comp_coresident) {
       const int gblk = std::max(1, (int)(((long long)E * pl->dyk_ncomp + 255) / 256));
       const DykComp* comps = pl->DYKC;
       int ncomp = pl->dyk_ncomp, nfree = pl->dyk_nfree;

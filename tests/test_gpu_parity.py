@@ -162,23 +162,26 @@ def test_residual_stopping_matches_fixed_iteration_solve(name):
     assert never["iterations"] == n
 
 
-@pytest.mark.parametrize("tree_name", ["SMPC1", "SMPC3"])
+@pytest.mark.parametrize("tree_name", ["SMPC1", "SMPC3", "SMPC8"])
 def test_lockstep_dykstra_gap_equals_two_pass(tree_name, monkeypatch):
-    """The cooperative lockstep Dykstra forms (a thread per junction row, a warp
-    per edge) run the same per-element sweeps and stop at the same global sweep
-    as the two-pass form: bitwise-equal gap."""
+    """The Dykstra forms of the gap's projection -- a thread per (edge, junction
+    row) in cooperative lockstep (default when that grid is co-resident), the same
+    in two passes (the default for SMPC8's 178k components; a component stops once
+    its state repeats), a warp per edge in lockstep, a warp per edge in two
+    passes -- run the same per-element sweeps and stop at the same global sweep:
+    bitwise-equal gap."""
     import bench
     W = bench.build_workload(tree_name)
     th, cf = engine.theta_schedule(120)
     gaps = []
-    # per-junction threads (default for bcn63), warp per edge, two passes
-    for env in (None, "TSMPC_DYKSTRA_WARP", "TSMPC_DYKSTRA_TWO_PASS"):
+    # (the variables accumulate: two-pass components, then warp lockstep, then warp two passes)
+    for env in (None, "TSMPC_DYKSTRA_COMP2", "TSMPC_DYKSTRA_WARP", "TSMPC_DYKSTRA_TWO_PASS"):
         if env:
             monkeypatch.setenv(env, "1")
         plan = DevicePlan(W["model"], W["tree"], W["factor"], W["scaling"])
         plan.set_cache(W["caches"][0], W["model"])
         gaps.append(plan.solve(W["p"], 120, 0.05, theta=th, coef=cf, keep_device=True)["gap"])
-    assert np.isfinite(gaps[0]) and gaps[0] == gaps[1] == gaps[2], gaps
+    assert np.isfinite(gaps[0]) and gaps[0] == gaps[1] == gaps[2] == gaps[3], gaps
 
 
 @pytest.mark.parametrize("tree_name", ["SMPC1", "SMPC3"])

@@ -9,11 +9,12 @@ from paper_1604_01074_b200 import theta_schedule  # noqa: E402
 from paper_1604_01074_b200.plan import DevicePlan  # noqa: E402
 
 tree = sys.argv[1] if len(sys.argv) > 1 else "SMPC3"
+iters = int(sys.argv[2]) if len(sys.argv) > 2 else 500
 W = bench.build_workload(tree)
 plan = DevicePlan(W["model"], W["tree"], W["factor"], W["scaling"])
 plan.set_cache(W["caches"][0], W["model"])
-th, cf = theta_schedule(500)
+th, cf = theta_schedule(iters)
 for _ in range(4):
-    r = plan.solve(W["p"], 500, 0.05, theta=th, coef=cf, keep_device=True)
+    r = plan.solve(W["p"], iters, 0.05, theta=th, coef=cf, keep_device=True)
     print(f"{tree}: loop {r['device_ms']:.3f} ms, loop+gap {r['device_total_ms']:.3f} ms, "
           f"gap {r['device_total_ms'] - r['device_ms']:.3f} ms")
