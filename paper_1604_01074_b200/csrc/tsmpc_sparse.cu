@@ -111,6 +111,57 @@ __device__ __forceinline__ void cp16(double* sdst, const double* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+// bulk (TMA engine) row copies global -> shared completing on an mbarrier (wide
+// kernel's FG fill rows and TG t rows): 16-byte aligned addresses, sizes multiple of 16
+#ifndef TSMPC_BULK
+#define TSMPC_BULK 1
+#endif
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::
+          "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_row(void* sdst, const void* gsrc, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(sdst)),
+               "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// generic-proxy accesses of this thread ordered before later async-proxy (bulk copy) ones
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__shared__ unsigned long long s_bulk_bar;  // bulk row copies of the wide kernel (FGK)
+__shared__ unsigned s_bulk_phase;
+// all threads: arm the bulk barrier for `total` bytes and issue copies 0..n-1
+// (issue(i) calls bulk_row).  The destination's last readers are behind the block
+// barrier that ended the previous phase; the barrier's tx-count may dip below zero
+// while copies complete before thread 0's expect_tx, and its phase cannot complete
+// before that arrival.
+template <class ISSUE>
+__device__ __forceinline__ void bulk_issue(int n, unsigned total, ISSUE issue) {
+  if (TSMPC_BULK & 2) {  // experiment: proxy fence and barriers before the copies
+    fence_proxy_async();
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) mbar_expect_tx(&s_bulk_bar, total);
+  if (TSMPC_BULK & 2) __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) issue(i);
+}
+// all threads: wait for the bytes of the last bulk_issue
+__device__ __forceinline__ void bulk_wait() {
+  mbar_wait(&s_bulk_bar, s_bulk_phase);
+  __syncthreads();
+  if (threadIdx.x == 0) s_bulk_phase ^= 1u;
+}
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
@@ -2214,7 +2265,19 @@ __device__ __noinline__ void bwd_wide(int ti, double cf, int cur, int pf) {
       bpre[m] = TSMPC_PREF && r < nrows && k < nv ? ldcg(S.beta_s + (size_t)c.mt.edge(row0 + r) * c.NVP + k) : 0.0;
     }
   }
-  if (FGK && pf == 2) {
+  if (FGK && pf == 2 && TSMPC_BULK) {
+    // (1) fill rows left in FG by the previous iteration's epilogue: [s | psi^] -> A | B,
+    // two bulk copies per row
+    const double* FG = S.FG;
+    const int FL = S.FL, NXP = c.NXP, NUP = c.NUP;
+    bulk_issue(2 * nrows, 8u * (unsigned)(nrows * FL), [&](int i) {
+      const int r = i >> 1;
+      const double* src = FG + (size_t)c.mt.edge(row0 + r) * FL;
+      if (i & 1) bulk_row(RB + r * NUP, src + NXP, 8u * NUP, &s_bulk_bar);
+      else bulk_row(RA + r * LA, src, 8u * NXP, &s_bulk_bar);
+    });
+    bulk_wait();
+  } else if (FGK && pf == 2) {
     // (1) fill rows left in FG by the previous iteration's epilogue: [s | psi^] -> A | B
     const int hx = c.NXP / 2, per = hx + c.NUP / 2;
 #pragma unroll 1
@@ -2482,7 +2545,12 @@ __device__ __noinline__ void fwd_wide(int ti, int nu_it, double cf, double th, i
       upre[m] = TSMPC_PREF && r < nrows && k < nu ? ldcg(P.uhat + (size_t)c.mt.edge(row0 + r) * c.NUP + k) : 0.0;
     }
   }
-  if (c.mt.tmode == 2) {  // t rows of this tile -> region A
+  const bool tg_bulk = FGK && TSMPC_BULK && c.mt.tmode == 2;
+  if (tg_bulk) {  // t rows of this tile -> region A, a bulk copy per row (waited for below)
+    bulk_issue(nrows, 8u * (unsigned)(nrows * c.NVP), [&](int r) {
+      bulk_row(RA + r * LA, S.TG + (size_t)c.mt.edge(row0 + r) * c.NVP, 8u * c.NVP, &s_bulk_bar);
+    });
+  } else if (c.mt.tmode == 2) {  // t rows of this tile -> region A
     const int lane = tid & 31;
 #pragma unroll 1
     for (int r = tid >> 5; r < nrows; r += kWarpsS) {
@@ -2504,7 +2572,8 @@ __device__ __noinline__ void fwd_wide(int ti, int nu_it, double cf, double th, i
     const int* sg = c.mt.segs + 4 * (seg0 + tid);
     for (int r = sg[0]; r < sg[1]; ++r) c.rdesc()[5 * r + 4] = tid;
   }
-  if (c.mt.tmode == 2) cp_wait<0>();
+  if (tg_bulk) bulk_wait();
+  else if (c.mt.tmode == 2) cp_wait<0>();
   __syncthreads();
   // (1) S scan, head -> tail: S_e = t_e + S_parent (A, in place)
 #pragma unroll 1
@@ -3042,6 +3111,10 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
   if (threadIdx.x == 0) {
     s_win = win;  // visible after the staging barrier below
     s_tm_on = 0;
+    if (FGK && TSMPC_BULK) {
+      mbar_init(&s_bulk_bar, 1);
+      s_bulk_phase = 0;
+    }
   }
   {  // stage model vectors, scaling, sparse operators and this CTA's plan
     double* bnd = s_dyn + S.O_BND;
