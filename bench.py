@@ -297,6 +297,10 @@ def run_ours(args, ws, rank, local):
             line["sharded_per_rank_compute"] = sharded_estimate(args, local)
         except Exception as exc:
             line["sharded_per_rank_compute"] = {"error": f"{type(exc).__name__}: {exc}"}
+        try:  # the largest wide tree of SURVEY section 8d (C4), 16,384 scenarios
+            line["sharded_per_rank_compute_w16k"] = sharded_estimate(args, local, tree="W16k", iters=100)
+        except Exception as exc:
+            line["sharded_per_rank_compute_w16k"] = {"error": f"{type(exc).__name__}: {exc}"}
     emit(line)
 
 
@@ -403,14 +407,18 @@ def sharded_measure(args, ws, rank, local, dist):
             "step_size": lam}
 
 
-def sharded_estimate(args, local, worlds=(2, 4, 8)):
-    """No multi-GPU box: the per-rank compute of a w-GPU W4k solve, measured on
-    this GPU.  Every rank's shard plan runs its two launches per iteration
-    (tsmpc_plan_trial, without the cross-rank exchange); a w-GPU iteration costs
-    the slowest rank's time plus one all-reduce of `exchange_bytes_per_iter`."""
+def sharded_estimate(args, local, worlds=(2, 4, 8), tree=None, iters=None):
+    """No multi-GPU box: the per-rank compute of a w-GPU W4k (or W16k) solve,
+    measured on this GPU.  Every rank's shard plan runs its two launches per
+    iteration (tsmpc_plan_trial, without the cross-rank exchange); a w-GPU
+    iteration costs the slowest rank's time plus one all-reduce of
+    `exchange_bytes_per_iter`."""
     from paper_1604_01074_b200.plan import DevicePlan
-    W = build_workload(args.shard_tree)
-    out = {"tree": args.shard_tree, "iters": args.iters,
+    tree = tree or args.shard_tree
+    iters = iters or args.iters
+    W = build_workload(tree)
+    E = W["tree"].n_edges
+    out = {"tree": tree, "edges": E, "scenarios": W["tree"].n_s, "iters": iters,
            "note": "per-rank compute only (no NCCL on one GPU); not a multi-GPU measurement"}
     for w in worlds:
         us, xb = [], 0
@@ -418,11 +426,12 @@ def sharded_estimate(args, local, worlds=(2, 4, 8)):
             plan = DevicePlan(W["model"], W["tree"], W["factor"], W["scaling"], device=local, shard=(r, w, None))
             plan.set_cache(W["caches"][0], W["model"])
             plan.trial(5)
-            us.append(min(plan.trial(args.iters) for _ in range(3)) * 1e3 / args.iters)
+            us.append(min(plan.trial(iters) for _ in range(3)) * 1e3 / iters)
             xb = 8 * plan.info()["exchange_doubles"]
             del plan
         out[f"w{w}"] = {"per_rank_us_per_iter": [round(u, 1) for u in us], "max_us_per_iter": round(max(us), 1),
-                        "exchange_bytes_per_iter": xb}
+                        "exchange_bytes_per_iter": xb,
+                        "hbm_frac_per_rank": round(E * BYTES_PER_EDGE / w / (max(us) * 1e-6) / 1e9 / peaks()[0], 4)}
     return out
 
 
