@@ -116,6 +116,10 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 #ifndef TSMPC_BULK
 #define TSMPC_BULK 1
 #endif
+#ifndef TSMPC_UNR
+#define TSMPC_UNR 2
+#endif
+constexpr int kUnr = TSMPC_UNR;  // rows in flight per thread in the wide kernel's sparse row phases
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -2434,7 +2438,7 @@ __device__ __noinline__ void bwd_wide(int ti, double cf, int cur, int pf) {
   // (3) z = psi^ + B' xiq (column k of B), B <- B + B' A
   if (k < nu) {
     const SpCol col = sp_col(c, S.Bc_ptr, S.Bc_idx, S.Bc_val, k);
-#pragma unroll 2
+#pragma unroll (kUnr)
     for (int r = g; r < nrows; r += kGroups)
       RB[r * c.NUP + k] = sp_dot(c, col, S.Bc_idx, S.Bc_val, RA + r * LA, RB[r * c.NUP + k]);
   }
@@ -2601,7 +2605,7 @@ __device__ __noinline__ void fwd_wide(int ti, int nu_it, double cf, double th, i
   // (2) du = Lt S (row k of Lt), B <- Lt A
   if (k < nu) {
     const SpCol col = sp_col(c, S.Lr_ptr, S.Lr_idx, S.Lr_val, k);
-#pragma unroll 2
+#pragma unroll (kUnr)
     for (int r = g; r < nrows; r += kGroups) RB[r * c.NUP + k] = sp_dot(c, col, S.Lr_idx, S.Lr_val, RA + r * LA, 0.0);
   }
   __syncthreads();
@@ -2622,7 +2626,7 @@ __device__ __noinline__ void fwd_wide(int ti, int nu_it, double cf, double th, i
     }
   } else if (k < nx) {
     const SpCol col = sp_col(c, S.Br_ptr, S.Br_idx, S.Br_val, k);
-#pragma unroll 2
+#pragma unroll (kUnr)
     for (int r = g; r < nrows; r += kGroups)
       RA[r * LA + k] = __dadd_rn(sp_dot(c, col, S.Br_idx, S.Br_val, RB + r * c.NUP, 0.0),
                                  ldcg(P.evec + (size_t)c.mt.edge(row0 + r) * c.NXP + k));

@@ -117,3 +117,19 @@ def test_sparse_planner_long_chains():
     from paper_1604_01074_b200.errors import ValidationError
     with pytest.raises(ValidationError):
         describe_sparse(m, t, f)
+
+
+def test_sparse_planner_wide_trees():
+    """W4k keeps its whole per-CTA meta in shared memory (7 tiles per CTA); W16k
+    (345,121 edges, 28 tiles and 2,331 rows per CTA) only fits with the per-tile meta
+    windows, and both run wide with fill rows through HBM (multi-tile CTAs)."""
+    m = synth.bcn63_network()
+    b = compute_basis(m)
+    f = factor_step(b, m)
+    for name, tiles_per_cta in (("W4k", 7), ("W16k", 28)):
+        t = synth.paper_tree(*synth.PAPER_TREES[name])
+        d = describe_sparse(m, t, f)
+        assert d["wide"] == 1 and d["ctas"] == 148 and d["smem_bytes"] <= 232448, (name, d)
+        assert d["chains"] == synth.PAPER_TREES[name][2] and d["tile_rows"] == 84
+        assert d["tiles"] >= 148 * (tiles_per_cta - 1), (name, d)
+        assert d["max_rows"] == 21 * -(-d["chains"] // 148), (name, d)
