@@ -3107,6 +3107,23 @@ __device__ __noinline__ void win_stage(int t) {
   __syncthreads();
 }
 
+// block-wide copy of n elements global -> shared, four loads in flight per thread
+template <class T>
+__device__ __forceinline__ void stage_copy(T* dst, const T* __restrict__ src, int n) {
+  int i = threadIdx.x;
+#pragma unroll 1
+  for (; i + 3 * kThreadsS < n; i += 4 * kThreadsS) {
+    const T a = __ldg(src + i), b = __ldg(src + i + kThreadsS), c = __ldg(src + i + 2 * kThreadsS),
+            d = __ldg(src + i + 3 * kThreadsS);
+    dst[i] = a;
+    dst[i + kThreadsS] = b;
+    dst[i + 2 * kThreadsS] = c;
+    dst[i + 3 * kThreadsS] = d;
+  }
+#pragma unroll 1
+  for (; i < n; i += kThreadsS) dst[i] = __ldg(src + i);
+}
+
 template <int XS, bool FGK>
 __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
   cg::grid_group grid = cg::this_grid();
@@ -3144,33 +3161,22 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
       scl[2 * N + j] = P.scaled ? P.sig_rcp[j] : 1.0;
       scl[3 * N + j] = P.scaled ? P.zeta_rcp[j] : 1.0;
     }
-    if (P.scaled && S.psi_smem) {
-      double* psi = s_dyn + S.O_PSI;
-#pragma unroll 1
-      for (int i = threadIdx.x; i < N * NUP; i += kThreadsS) psi[i] = P.psi_stage[i];
-    }
-    if (S.sched_resident) {
-      int* ss = reinterpret_cast<int*>(s_dyn + S.O_SCHED);
-#pragma unroll 1
-      for (int i = threadIdx.x; i < S.n_tsched; i += kThreadsS) ss[i] = __ldg(S.tsched + i);
-    }
+    // the contiguous blocks: four loads in flight per thread (a launch of a shard
+    // plan restages them twice per iteration)
+    if (P.scaled && S.psi_smem) stage_copy(s_dyn + S.O_PSI, P.psi_stage, N * NUP);
+    if (S.sched_resident) stage_copy(reinterpret_cast<int*>(s_dyn + S.O_SCHED), S.tsched, S.n_tsched);
     int* ints = reinterpret_cast<int*>(s_dyn + S.O_INT);
     const int m0 = __ldg(S.meta_ptr + blockIdx.x), m1 = __ldg(S.meta_ptr + blockIdx.x + 1);
-#pragma unroll 1
     if (S.rows_window) {  // everything but the rows and segments (staged per tile)
       const int lo = 8 + 4 * __ldg(S.meta + m0), gap = 4 * (__ldg(S.meta + m0 + 1) + __ldg(S.meta + m0 + 2));
-#pragma unroll 1
-      for (int i = threadIdx.x; i < m1 - m0 - gap; i += kThreadsS) ints[i] = __ldg(S.meta + m0 + (i < lo ? i : i + gap));
+      stage_copy(ints, S.meta + m0, lo);
+      stage_copy(ints + lo, S.meta + m0 + lo + gap, m1 - m0 - gap - lo);
       if (threadIdx.x == 0) s_row_off = s_seg_off = 0;
     } else {
-#pragma unroll 1
-      for (int i = threadIdx.x; i < m1 - m0; i += kThreadsS) ints[i] = __ldg(S.meta + m0 + i);
+      stage_copy(ints, S.meta + m0, m1 - m0);
     }
-#pragma unroll 1
-    for (int i = threadIdx.x; i < S.n_spi; i += kThreadsS) ints[S.meta_max + i] = __ldg(S.spi + i);
-    double* spv = s_dyn + S.O_SPV;
-#pragma unroll 1
-    for (int i = threadIdx.x; i < S.n_spv; i += kThreadsS) spv[i] = __ldg(S.spv + i);
+    stage_copy(ints + S.meta_max, S.spi, S.n_spi);
+    stage_copy(s_dyn + S.O_SPV, S.spv, S.n_spv);
     __syncthreads();
   }
   const Ctx c = ctx_of();
