@@ -291,6 +291,8 @@ def run_ours(args, ws, rank, local):
     if not args.no_shard and not args.quick:
         try:
             line["sharded_one_rank"] = sharded_measure(args, 1, 0, local, None)
+            nccl = sharded_measure(args, 1, 0, local, None, peer=False)
+            line["sharded_one_rank"]["two_launch_nccl_us_per_iter"] = nccl["us_per_iter"]
         except Exception as exc:  # report, never lose the headline line over it
             line["sharded_one_rank"] = {"error": f"{type(exc).__name__}: {exc}"}
         try:
@@ -364,20 +366,23 @@ def _residual_target_one(local, g, gname, paper_weights):
                     "to ~1e-9 relative; the APG residual is not monotone, both stopping definitions are reported"}
 
 
-def sharded_measure(args, ws, rank, local, dist):
+def sharded_measure(args, ws, rank, local, dist, peer=True):
     """BASELINE configs[3] on the ranks of this job: W4k split by subtree (chain
     groups per rank, the trunk positions above them computed by their rank, the
-    top replicated, one all-reduce of the sums crossing that cut per iteration).
-    Device time of the loop, max over ranks."""
+    top replicated, the sums crossing that cut exchanged per iteration: inside the
+    kernel over peer memory when the ranks mapped each other's buffers, else one
+    ncclAllReduce between two launches).  Device time of the loop, max over ranks."""
     import torch
     from paper_1604_01074_b200 import theta_schedule
     from paper_1604_01074_b200.plan import DevicePlan
-    from paper_1604_01074_b200.shard import _broadcast_id, nccl_unique_id
+    from paper_1604_01074_b200.shard import _broadcast_id, nccl_unique_id, open_peer_exchange
     W = build_workload(args.shard_tree)
     nid = _broadcast_id(rank) if dist is not None else nccl_unique_id()
     plan = DevicePlan(W["model"], W["tree"], W["factor"], W["scaling"], device=local,
                       shard=(rank, ws, nid))
     plan.set_cache(W["caches"][0], W["model"])
+    if peer and not os.environ.get("TSMPC_NO_PEER"):
+        open_peer_exchange(plan, ws)
     g = golden(f"L_bcn63_{args.shard_tree}_i100") or golden(f"L_bcn63_{args.shard_tree}_i500")
     lam = float(g["lam"]) if g is not None else 0.4797
     th, cf = theta_schedule(args.iters)
@@ -402,7 +407,10 @@ def sharded_measure(args, ws, rank, local, dist):
             "iters_per_s": args.iters / (loop / 1e3), "us_per_iter": loop * 1e3 / args.iters,
             "hbm_frac_per_rank": E / ws * BYTES_PER_EDGE * args.iters / (loop / 1e3) / 1e9 / hbm_peak,
             "owned_chain_edges_rank0": info["owned_chain_edges"], "trunk_edges": info["trunk_edges"],
-            "ctas": info["ctas"], "wide": info["wide"], "launches_per_iter": 2,
+            "ctas": info["ctas"], "wide": info["wide"],
+            "exchange": ("in-kernel: peer stores + arrival counters, one launch per solve"
+                         if info["peer_exchange"] else "ncclAllReduce between two launches per iteration"),
+            "launches_per_iter": 1.0 / args.iters if info["peer_exchange"] else 2,
             "exchange_bytes_per_iter": 8 * info["exchange_doubles"],
             "step_size": lam}
 
@@ -448,7 +456,7 @@ def sharded_headline(args, ws, rank, local, dist):
             "config": {"workload": workload_name(args.shard_tree, tree, args.iters),
                        "tree": args.shard_tree, "edges": tree.n_edges, "iters": args.iters,
                        "baseline_config": "BASELINE.json configs[3] (wide tree sharded by subtree)",
-                       "parallelism": f"subtree-sharded x{ws} (NCCL all-reduce of the cut sums)"},
+                       "parallelism": f"subtree-sharded x{ws} (cut sums: {sh['exchange']})"},
             "roofline": {"bound": "hbm", "achieved": sh["hbm_frac_per_rank"] * hbm_peak, "peak": hbm_peak,
                          "unit": "GB/s", "frac": sh["hbm_frac_per_rank"], "traffic": None,
                          "kernel": "tsmpc::apg_wide_kernel (per rank)", "peak_source": peak_kind},

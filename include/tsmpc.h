@@ -156,6 +156,25 @@ int tsmpc_solve_group(tsmpc_plan* const* plans, int32_t n, const double* p, int3
  * SolverConfig(devices=(...)): the sharded solve behind the reference API. */
 int tsmpc_plans_create_multi(const tsmpc_problem* prob, const int32_t* devices, int32_t n,
                              tsmpc_plan** plans_out);
+/* The cut exchange inside the persistent kernel, over peer memory (NVLink /
+ * NVSwitch), instead of two launches and an ncclAllReduce per iteration: once
+ * both phases of an iteration are in one launch, each rank's CTAs store their
+ * slice of the exchange rows into every rank's receive rows, fence at system
+ * scope and bump every rank's arrival counter; each rank waits for all arrivals
+ * of the iteration, sums the world rows (one non-zero contributor per entry:
+ * exact) and continues with phase 2 -- one launch per solve, the last tile's fill
+ * kept in shared memory across iterations.  Process per GPU: every rank exports
+ * its blob (tsmpc_plan_peer_handles, CUDA IPC handles of its receive rows and
+ * counter, TSMPC_PEER_BLOB_BYTES), the ranks all-gather them (rank order), and
+ * every rank calls tsmpc_plan_peer_open with the world blobs; all ranks must then
+ * use the exchange (or all call tsmpc_plan_peer_close).  tsmpc_plans_create_multi
+ * enables it itself when every device pair has peer access (TSMPC_NO_PEER=1
+ * keeps the NCCL path).  A rank whose peers do not arrive within ~2 s aborts the
+ * launch (TSMPC_ERR_CUDA) instead of hanging.  Wide shard plans only. */
+#define TSMPC_PEER_BLOB_BYTES 160
+int tsmpc_plan_peer_handles(const tsmpc_plan* plan, uint8_t* blob);
+int tsmpc_plan_peer_open(tsmpc_plan* plan, const uint8_t* blobs, int32_t world);
+int tsmpc_plan_peer_close(tsmpc_plan* plan);
 int tsmpc_solve_multi(tsmpc_plan* const* plans, int32_t n, const double* p, int32_t iters,
                       double lam, const double* theta, const double* coef, int32_t flags,
                       tsmpc_result* outs);
@@ -236,7 +255,8 @@ int tsmpc_dual_operator_step(tsmpc_plan* plan, double* y_dot_dy, double* dy_dot_
  * resident_ctas, sharded, rank, world, owned_chain_edges, total_chains,
  * trunk_ctas, wide, exchange_doubles (shard plans: the doubles every rank sums
  * per iteration), fill_rows_hbm (wide plans with multi-tile or sharded CTAs: the
- * epilogue leaves the next backward's fill rows in HBM)}. */
+ * epilogue leaves the next backward's fill rows in HBM), peer_exchange (shard
+ * plans: the cut exchange runs inside the kernel over peer memory)}. */
 int tsmpc_plan_info(const tsmpc_plan* plan, int64_t* info, int32_t n_info);
 
 /* Host-only planning (no device needed): the segment / level / tile / trunk

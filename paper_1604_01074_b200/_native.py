@@ -87,6 +87,9 @@ SIGNATURES = {
     "tsmpc_set_forecast": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, _dp, _dp]),
     "tsmpc_get_cache": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, _dp]),
     "tsmpc_nccl_unique_id": (ctypes.c_int, [ctypes.POINTER(ctypes.c_uint8)]),
+    "tsmpc_plan_peer_handles": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint8)]),
+    "tsmpc_plan_peer_open": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint8), ctypes.c_int32]),
+    "tsmpc_plan_peer_close": (ctypes.c_int, [ctypes.c_void_p]),
     "tsmpc_plan_create_shard": (ctypes.c_void_p, [ctypes.POINTER(Problem), ctypes.c_int, ctypes.c_int32,
                                                   ctypes.c_int32, ctypes.POINTER(ctypes.c_uint8)]),
     "tsmpc_solve_group": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32, _dp, ctypes.c_int32,

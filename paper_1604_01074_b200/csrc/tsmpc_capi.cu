@@ -102,6 +102,12 @@ struct tsmpc_plan {
   void* comm = nullptr;
   double* HS = nullptr;
   double* XCH = nullptr;            // shard plans: the cut exchange rows (summed across ranks)
+  // shard plans: the cut exchange over peer memory inside the kernel (SParams::peer_rx)
+  double* RX = nullptr;                 // 2 x world x n_xch x XCH_LD receive rows
+  unsigned long long* RXCNT = nullptr;  // arrival counter
+  std::vector<void*> ipc_mapped;        // other ranks' buffers opened with cudaIpcOpenMemHandle
+  bool peer_on = false;
+  unsigned long long xgen = 0;          // exchange generations run so far (the same on every rank)
   double* TR = nullptr;            // split mode: [du | B du | x] per trunk position
   unsigned int* SUBCTR = nullptr;  // split mode: trunk-CTA barrier counter
   unsigned int* ABORT = nullptr;   // raised by a sparse-kernel spin-wait that timed out
@@ -162,6 +168,7 @@ struct tsmpc_plan {
     if (stream) cudaStreamSynchronize(stream);
     if (gexec) cudaGraphExecDestroy(gexec);
     if (comm && nccl) nccl->CommDestroy(comm);
+    for (void* p : ipc_mapped) cudaIpcCloseMemHandle(p);
     for (void* p : allocs) cudaFree(p);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -844,7 +851,15 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
           S.XCH_LD = hp.cut ? P.KY_LD + NXP : S.HS_LD;
           if (hp.cut) rc |= pl->alloc(&pl->XCH, (size_t)std::max(1, hp.n_xch) * S.XCH_LD);
           else pl->XCH = pl->HS;  // every position's head sums, exchanged in place
+          // receive rows and arrival counter of the in-kernel exchange (own allocations:
+          // other ranks map them through CUDA IPC handles)
+          rc |= pl->alloc(&pl->RX, 2 * (size_t)sworld * std::max(1, hp.n_xch) * S.XCH_LD);
+          rc |= pl->alloc(&pl->RXCNT, 1);
           if (rc) return bail(0);
+          S.RX = pl->RX;
+          S.RXCNT = pl->RXCNT;
+          S.rank = srank;
+          S.world = sworld;
           S.sharded = 1;
           S.HS = pl->HS;
           S.XCH = pl->XCH;
@@ -1043,6 +1058,112 @@ tsmpc_plan* tsmpc_plan_create_shard(const tsmpc_problem* pb, int device, int32_t
   return plan_create_impl(pb, device, rank, world, nccl_id);
 }
 
+// ---------------------------------------------------------------- peer exchange
+namespace {
+// the ranks' receive rows / arrival counters as this device sees them -> SParams
+int peer_setup(tsmpc_plan* pl, const std::vector<double*>& rx, const std::vector<unsigned long long*>& cnt,
+               unsigned long long expect) {
+  CU(cudaSetDevice(pl->device));
+  double** d_rx = nullptr;
+  unsigned long long** d_cnt = nullptr;
+  int rc = pl->upload(&d_rx, rx.data(), rx.size());
+  rc |= pl->upload(&d_cnt, cnt.data(), cnt.size());
+  if (rc) return rc;
+  CU(cudaStreamSynchronize(pl->stream));
+  pl->sbase.peer_rx = d_rx;
+  pl->sbase.peer_cnt = d_cnt;
+  pl->sbase.xch_expect = expect;
+  pl->peer_on = true;
+  return TSMPC_OK;
+}
+// peer exchange blob: [RX handle | RXCNT handle | ctas, rank, world, fg | exchange doubles]
+struct PeerBlob {
+  cudaIpcMemHandle_t rx, cnt;
+  int32_t ctas, rank, world, fg;
+  int64_t xn;
+};
+static_assert(sizeof(PeerBlob) <= TSMPC_PEER_BLOB_BYTES, "peer blob size");
+bool peer_capable(const tsmpc_plan* pl) {
+  return pl->sharded && pl->use_sparse && pl->sbase.wide && pl->sbase.FL > 0 && pl->RX && pl->RXCNT;
+}
+}  // namespace
+
+int tsmpc_plan_peer_handles(const tsmpc_plan* pl, uint8_t* blob) {
+  if (!pl || !blob) return fail(TSMPC_ERR_ARGUMENT, "null argument");
+  if (!peer_capable(pl)) return fail(TSMPC_ERR_VALIDATION, "not a wide shard plan: no in-kernel exchange");
+  CU(cudaSetDevice(pl->device));
+  PeerBlob b{};
+  CU(cudaIpcGetMemHandle(&b.rx, pl->RX));
+  CU(cudaIpcGetMemHandle(&b.cnt, pl->RXCNT));
+  b.ctas = pl->sp_ctas;
+  b.rank = pl->rank;
+  b.world = pl->world;
+  b.fg = pl->sbase.FL > 0 ? 1 : 0;
+  b.xn = (int64_t)pl->sbase.n_xch * pl->sbase.XCH_LD;
+  std::memset(blob, 0, TSMPC_PEER_BLOB_BYTES);
+  std::memcpy(blob, &b, sizeof b);
+  return TSMPC_OK;
+}
+
+int tsmpc_plan_peer_open(tsmpc_plan* pl, const uint8_t* blobs, int32_t world) {
+  if (!pl || !blobs) return fail(TSMPC_ERR_ARGUMENT, "null argument");
+  if (!peer_capable(pl)) return fail(TSMPC_ERR_VALIDATION, "not a wide shard plan: no in-kernel exchange");
+  if (world != pl->world) return fail(TSMPC_ERR_ARGUMENT, "%d blobs for a world of %d", world, pl->world);
+  if (pl->peer_on) return TSMPC_OK;
+  CU(cudaSetDevice(pl->device));
+  std::vector<double*> rx(world);
+  std::vector<unsigned long long*> cnt(world);
+  std::vector<void*> opened;
+  auto undo = [&]() {
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
+    cudaGetLastError();
+  };
+  const int64_t xn = (int64_t)pl->sbase.n_xch * pl->sbase.XCH_LD;
+  for (int p = 0; p < world; ++p) {
+    PeerBlob b;
+    std::memcpy(&b, blobs + (size_t)p * TSMPC_PEER_BLOB_BYTES, sizeof b);
+    if (b.rank != p || b.world != world || b.ctas != pl->sp_ctas || b.xn != xn || !b.fg) {
+      undo();
+      return fail(TSMPC_ERR_VALIDATION, "peer %d: plan mismatch (rank %d, world %d, %d CTAs, %lld exchange doubles)",
+                  p, b.rank, b.world, b.ctas, (long long)b.xn);
+    }
+    if (p == pl->rank) {
+      rx[p] = pl->RX;
+      cnt[p] = pl->RXCNT;
+      continue;
+    }
+    void* a = nullptr;
+    void* c = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&a, b.rx, cudaIpcMemLazyEnablePeerAccess);
+    if (e == cudaSuccess) {
+      opened.push_back(a);
+      e = cudaIpcOpenMemHandle(&c, b.cnt, cudaIpcMemLazyEnablePeerAccess);
+      if (e == cudaSuccess) opened.push_back(c);
+    }
+    if (e != cudaSuccess) {
+      undo();
+      return fail(TSMPC_ERR_CUDA, "cudaIpcOpenMemHandle (rank %d's exchange buffers): %s", p, cudaGetErrorString(e));
+    }
+    rx[p] = static_cast<double*>(a);
+    cnt[p] = static_cast<unsigned long long*>(c);
+  }
+  const int rc = peer_setup(pl, rx, cnt, (unsigned long long)world * pl->sp_ctas);
+  if (rc) {
+    undo();
+    return rc;
+  }
+  pl->ipc_mapped.insert(pl->ipc_mapped.end(), opened.begin(), opened.end());
+  return TSMPC_OK;
+}
+
+int tsmpc_plan_peer_close(tsmpc_plan* pl) {
+  if (!pl) return fail(TSMPC_ERR_ARGUMENT, "null argument");
+  pl->peer_on = false;  // back to the two launches + ncclAllReduce per iteration
+  pl->sbase.peer_rx = nullptr;
+  pl->sbase.peer_cnt = nullptr;
+  return TSMPC_OK;
+}
+
 int tsmpc_plan_edges(const tsmpc_plan* pl, int32_t which, int64_t* out, int64_t cap) {
   if (!pl) return fail(TSMPC_ERR_ARGUMENT, "null argument");
   std::vector<int> all;
@@ -1149,7 +1270,7 @@ int tsmpc_plan_info(const tsmpc_plan* pl, int64_t* info, int32_t n) {
                           pl->sharded ? 1 : 0, pl->rank, pl->world, (int64_t)pl->owned_edges.size(),
                           pl->total_chains, sp ? pl->sbase.split_n : 0, sp ? pl->sbase.wide : 0,
                           pl->sharded ? (int64_t)pl->sbase.n_xch * pl->sbase.XCH_LD : 0,
-                          sp && pl->sbase.FG ? 1 : 0};
+                          sp && pl->sbase.FG ? 1 : 0, pl->peer_on ? 1 : 0};
   for (int i = 0; i < n && i < (int)(sizeof(vals) / sizeof(vals[0])); ++i) info[i] = vals[i];
   return TSMPC_OK;
 }
@@ -1734,7 +1855,12 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
         return TSMPC_OK;
       };
       bool graphed = false;
-      if (pl->comm && !std::getenv("TSMPC_NO_GRAPH")) {
+      const bool fused = pl->peer_on && !std::getenv("TSMPC_NO_PEER");
+      if (fused) {
+        // both phases and the cut exchange over peer memory in one launch
+        CU(sparse_launch(S, LaunchWin{0, iters, 7, 0, pl->xgen}, pl->sp_ctas, pl->sp_smem, pl->stream));
+        pl->xgen += (unsigned long long)iters;
+      } else if (pl->comm && !std::getenv("TSMPC_NO_GRAPH")) {
         if (pl->gexec && pl->g_iters == iters) {
           graphed = true;
         } else {
@@ -1760,7 +1886,9 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
           cudaGetLastError();  // a failed capture falls back to direct launches
         }
       }
-      if (graphed) {
+      if (fused) {
+        // (launched above)
+      } else if (graphed) {
         CU(sparse_params_upload(S, pl->stream));
         CU(cudaGraphLaunch(pl->gexec, pl->stream));
         CU(sparse_note_launch(pl->stream));
@@ -1768,7 +1896,7 @@ int tsmpc_solve(tsmpc_plan* pl, const double* p, int32_t iters, double lam, cons
         const int irc = issue();
         if (irc) return irc;
       }
-      pl->launches += 2 * (long long)iters;
+      pl->launches += fused ? 1 : 2 * (long long)iters;
       if (pl->comm) {
         // residual: max over ranks (non-negative doubles order like their bit patterns)
         const int nr = pl->nccl->AllReduce(pl->RESID, pl->RESID, (size_t)st.nres, NcclApi::kUint64, NcclApi::kMax,
@@ -2082,6 +2210,39 @@ int tsmpc_plans_create_multi(const tsmpc_problem* pb, const int32_t* devices, in
     plans[r]->multi = true;
     out[r] = plans[r];
   }
+  // the in-kernel cut exchange when every pair of devices can map each other's memory
+  bool peers = !std::getenv("TSMPC_NO_PEER");
+  for (int r = 0; r < n && peers; ++r) peers = peer_capable(plans[r]) && plans[r]->sp_ctas == plans[0]->sp_ctas;
+  for (int r = 0; r < n && peers; ++r)
+    for (int q = 0; q < n && peers; ++q) {
+      if (q == r || devices[q] == devices[r]) {
+        peers = q == r;
+        continue;
+      }
+      int ok = 0;
+      if (cudaDeviceCanAccessPeer(&ok, devices[r], devices[q]) != cudaSuccess || !ok) {
+        peers = false;
+        break;
+      }
+      cudaSetDevice(devices[r]);
+      const cudaError_t e = cudaDeviceEnablePeerAccess(devices[q], 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) peers = false;
+      cudaGetLastError();
+    }
+  if (peers) {
+    std::vector<double*> rx(n);
+    std::vector<unsigned long long*> cnt(n);
+    for (int r = 0; r < n; ++r) {
+      rx[r] = plans[r]->RX;
+      cnt[r] = plans[r]->RXCNT;
+    }
+    for (int r = 0; r < n; ++r)
+      if (peer_setup(plans[r], rx, cnt, (unsigned long long)n * plans[r]->sp_ctas)) {
+        for (int q = 0; q < n; ++q) tsmpc_plan_peer_close(plans[q]);
+        cudaGetLastError();
+        break;
+      }
+  }
   return TSMPC_OK;
 }
 
@@ -2108,7 +2269,18 @@ int tsmpc_solve_multi(tsmpc_plan* const* plans, int32_t n, const double* p, int3
     return nr == 0 ? TSMPC_OK : fail(TSMPC_ERR_NCCL, "NCCL: %s", api->GetErrorString(nr));
   };
   const size_t hs = (size_t)S[0].n_xch * S[0].XCH_LD;
-  for (int nu = 0; nu < iters; ++nu) {
+  bool fused = !std::getenv("TSMPC_NO_PEER");
+  for (int r = 0; r < n; ++r) fused = fused && plans[r]->peer_on;
+  if (fused) {  // every GPU: both phases and the cut exchange over peer memory, one launch
+    for (int r = 0; r < n; ++r) {
+      CU(cudaSetDevice(plans[r]->device));
+      CU(sparse_launch(S[r], LaunchWin{0, iters, 7, 0, plans[r]->xgen}, plans[r]->sp_ctas, plans[r]->sp_smem,
+                       plans[r]->stream));
+      plans[r]->xgen += (unsigned long long)iters;
+      plans[r]->launches += 1;
+    }
+  }
+  for (int nu = 0; nu < iters && !fused; ++nu) {
     for (int r = 0; r < n; ++r) {
       CU(cudaSetDevice(plans[r]->device));
       CU(sparse_launch(S[r], LaunchWin{nu, nu + 1, 1, 0}, plans[r]->sp_ctas, plans[r]->sp_smem, plans[r]->stream));

@@ -219,16 +219,30 @@ struct SParams {
   // tile being processed are copied into a window (O_WIN ints after the staged ints:
   // rows then, 4 tile_cap ints further, segments) before each tile
   int rows_window, O_WIN;
+  // cut exchange over peer memory inside the persistent kernel (shard plans whose
+  // ranks mapped each other's receive buffers: LaunchWin.phase & 4).  Per iteration
+  // every CTA stores its slice of XCH into slot (generation & 1), sender row `rank`,
+  // of every rank's RX, fences (system scope) and bumps every rank's arrival counter
+  // once; a rank waits until its counter reaches (generation + 1) x xch_expect, then
+  // sums the world sender rows of its slice in rank order back into XCH.
+  double* const* peer_rx;               // world pointers (this device's view of rank p's RX)
+  unsigned long long* const* peer_cnt;  // world pointers (rank p's arrival counter)
+  double* RX;                           // 2 x world x n_xch x XCH_LD
+  unsigned long long* RXCNT;            // this rank's arrival counter (monotone across solves)
+  int rank, world;
+  unsigned long long xch_expect;        // arrivals per iteration: world x CTAs per rank
   int hsum_nseg;                // wide split mode: chains per chain CTA the head-sum scratch holds
 };
 
 // Launch window of the structured-basis kernels (a kernel argument): iterations
 // [nu0, nu1) and phases (1: backward (+ head pre-reduction when sharded), 2: trunk
-// sweep, needs, forward + epilogue).  Single-GPU plans run every iteration with
-// both phases in one launch.  wb_end: the window ends with a full write-back (the
+// sweep, needs, forward + epilogue; 4: shard plans with peer-mapped receive buffers
+// run both phases and the cut exchange in one launch).  Single-GPU plans run every
+// iteration with both phases in one launch.  wb_end: the window ends with a full write-back (the
 // state of iteration nu1 - 1 is left in HBM: per-iteration duality gap).
 struct LaunchWin {
   int nu0, nu1, phase, wb_end;
+  unsigned long long xgen;  // peer exchange (phase & 4): generation of iteration nu0
 };
 
 // Phase timers (profiling builds: -DTSMPC_TIMERS).  Slot k accumulates the cycles

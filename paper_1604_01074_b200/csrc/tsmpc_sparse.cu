@@ -199,6 +199,18 @@ __device__ __forceinline__ void spin_until(const unsigned int* ctr, unsigned int
   }
 }
 
+__device__ __forceinline__ void spin_until64(const unsigned long long* ctr, unsigned long long target) {
+  const long long t0 = clock64();
+  volatile const unsigned int* abort_flag = g_sp.abort_flag;
+  while (*((volatile const unsigned long long*)ctr) < target) {
+    if (*abort_flag) return;
+    if (clock64() - t0 > kSpinLimit) {
+      atomicExch(const_cast<unsigned int*>(abort_flag), 1u);
+      return;
+    }
+  }
+}
+
 __device__ __forceinline__ void signal_wait(unsigned int* ctr, unsigned int target) {
   if (threadIdx.x == 0) {
     spin_until(ctr, target);
@@ -3084,6 +3096,47 @@ __device__ __noinline__ void tm_static_fill() {
   tm_fill_done();
 }
 
+// The cut exchange of a shard plan inside the persistent kernel (SParams::peer_rx,
+// LaunchWin.phase & 4; replaces phase 1 -> ncclAllReduce(XCH, sum) -> phase 2).
+// Called by every CTA after a grid barrier that completed XCH; the caller runs a
+// grid barrier after it before XCH is read.  Every CTA owns the same slice of XCH
+// in both halves: it stores its slice into every rank's RX (over NVLink for the
+// peers), fences at system scope and bumps every rank's arrival counter once; it
+// then waits for world x CTAs arrivals of this generation on its own counter and
+// sums the world sender rows of its slice in rank order.  Each entry has one
+// non-zero contributor (the owning rank), so the sum is exact, as the all-reduce.
+// RX is double-buffered by generation parity: a rank writes generation g + 2 only
+// after its own wait of generation g + 1, which every rank passes only after it
+// has summed generation g.
+__device__ __noinline__ void peer_exchange(unsigned long long gen) {
+  const SParams& S = g_sp;
+  const size_t xn = (size_t)S.n_xch * S.XCH_LD;
+  const int w = S.world;
+  const size_t slot = (size_t)(gen & 1ull) * (size_t)w * xn;
+  const size_t i0 = (size_t)blockIdx.x * kThreadsS + threadIdx.x, step = (size_t)gridDim.x * kThreadsS;
+#pragma unroll 1
+  for (size_t i = i0; i < xn; i += step) {
+    const double v = ldcg(S.XCH + i);
+#pragma unroll 1
+    for (int p = 0; p < w; ++p) __stcg(S.peer_rx[p] + slot + (size_t)S.rank * xn + i, v);
+  }
+  __threadfence_system();
+  __syncthreads();
+  if ((int)threadIdx.x < w) atomicAdd_system(S.peer_cnt[threadIdx.x], 1ull);
+  if (threadIdx.x == 0) {
+    spin_until64(S.RXCNT, (gen + 1ull) * S.xch_expect);
+    __threadfence_system();
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (size_t i = i0; i < xn; i += step) {
+    double s = 0.0;
+#pragma unroll 1
+    for (int p = 0; p < w; ++p) s = __dadd_rn(s, ldcg(S.RX + slot + (size_t)p * xn + i));
+    stcg(S.XCH + i, s);
+  }
+}
+
 // meta windows (SParams::rows_window): copy tile t's rows and chain segments from the
 // plan's meta in global memory into the window; ctx_of() rebinds to it
 __device__ __noinline__ void win_stage(int t) {
@@ -3183,6 +3236,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
   const int nt = c.mt.ntiles;
   const bool trunk = P.n_trunk > 0;
   const bool do_a = win.phase & 1, do_b = win.phase & 2;
+  const bool fused = FGK && S.sharded && (win.phase & 4) && S.peer_rx != nullptr;
   const bool chain_cta = (int)blockIdx.x < S.split_c0;
   if (S.split && chain_cta && nt == 1) {
     // per chain, the sum of beta_s over its rows (static during the launch), chain order
@@ -3220,7 +3274,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
                      (((int)(c.A() - s_dyn) | (int)(c.B() - s_dyn) | c.LA | c.NXP | c.NUP | S.FL) & 1) == 0;
   for (int nu = win.nu0; nu < win.nu1; ++nu) {
     const int cur = (P.slot0 + nu) & 1;
-    if (P.tol > 0.0 && nu > win.nu0 && nu % P.check_every == 0) {
+    if (P.tol > 0.0 && !S.sharded && nu > win.nu0 && nu % P.check_every == 0) {
       // stopping test on the residual of iteration nu - 1 (its state is in HBM)
       grid.sync();
       const double r = __longlong_as_double(
@@ -3254,6 +3308,13 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
           grid.sync();
           trunk_sweep(cf, cur, 5);
         }
+      }
+    }
+    if (fused && trunk) {  // shard plan, both phases in this launch: the cut exchange in between
+      grid.sync();
+      if (S.n_xch > 0) {
+        peer_exchange(win.xgen + (unsigned long long)(nu - win.nu0));
+        grid.sync();
       }
     }
     if (do_b && trunk && S.split) {

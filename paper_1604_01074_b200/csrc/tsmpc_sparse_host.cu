@@ -97,7 +97,9 @@ SparseHostPlan plan_sparse(const SparseTreeIn& t, const SparseOpsIn& ops, int NX
   out.towned.assign(T, 1);
   out.trole.assign(T, kRoleOwn);
   out.txrow.assign(T, -1);
-  if (sharded && world > 1) {
+  // (world 1 with TSMPC_SHARD_FULL: the one rank exchanges every position's head sums
+  // with itself -- exercises the exchange paths on a single GPU)
+  if (sharded && (world > 1 || std::getenv("TSMPC_SHARD_FULL"))) {
     std::vector<int> gnode;             // group -> parent node
     std::vector<long long> grows;       // group -> rows
     std::vector<int> group_of(chains.size());

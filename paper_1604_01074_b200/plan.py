@@ -124,12 +124,33 @@ class DevicePlan:
         keys = ("levels", "ctas", "tiles", "segments", "smem_bytes", "diag_A", "threads",
                 "tile_rows", "sms", "collapsed", "trunk_edges", "sparse", "resident_ctas",
                 "sharded", "rank", "world", "owned_chain_edges", "total_chains", "trunk_ctas",
-                "wide", "exchange_doubles", "fill_rows_hbm")
+                "wide", "exchange_doubles", "fill_rows_hbm", "peer_exchange")
         buf = np.zeros(len(keys), dtype=np.int64)
         nat.check(self._lib.tsmpc_plan_info(self._h, nat.iptr(buf), len(keys)), "tsmpc_plan_info")
         d = dict(zip(keys, (int(v) for v in buf)))
         d["path"] = self._lib.tsmpc_plan_path(self._h).decode()
         return d
+
+    # -- in-kernel cut exchange over peer memory (shard plans) ------------------
+    PEER_BLOB_BYTES = 160  # include/tsmpc.h TSMPC_PEER_BLOB_BYTES
+
+    def peer_handles(self) -> bytes:
+        """This rank's exchange blob (CUDA IPC handles of its receive rows and arrival
+        counter, tsmpc_plan_peer_handles); all-gather it across the ranks."""
+        buf = (ctypes.c_uint8 * self.PEER_BLOB_BYTES)()
+        nat.check(self._lib.tsmpc_plan_peer_handles(self._h, buf), "tsmpc_plan_peer_handles")
+        return bytes(buf)
+
+    def peer_open(self, blobs) -> None:
+        """Map every rank's exchange buffers (blobs in rank order); the solves then run
+        both phases and the cut exchange in one launch (tsmpc_plan_peer_open)."""
+        blob = b"".join(bytes(b) for b in blobs)
+        buf = (ctypes.c_uint8 * len(blob)).from_buffer_copy(blob)
+        nat.check(self._lib.tsmpc_plan_peer_open(self._h, buf, len(blobs)), "tsmpc_plan_peer_open")
+
+    def peer_close(self) -> None:
+        """Back to two launches and an ncclAllReduce per iteration."""
+        nat.check(self._lib.tsmpc_plan_peer_close(self._h), "tsmpc_plan_peer_close")
 
     def edges(self, which: int = 0) -> np.ndarray:
         """Edge ids whose rows this plan computes (which=0) or the trunk edges (1)."""

@@ -55,11 +55,55 @@ def _broadcast_id(rank: int, group=None) -> bytes:
     return obj[0]
 
 
-class ShardedSolver:
-    """This rank's share of a tree solve; construct on every rank collectively."""
+def open_peer_exchange(plan, world: int, group=None) -> bool:
+    """Map every rank's exchange buffers into this rank's shard plan (CUDA IPC
+    handles, all-gathered in rank order) so that each solve runs both phases and
+    the cut exchange over NVLink inside one launch (include/tsmpc.h,
+    tsmpc_plan_peer_open).  Collective over the ranks of ``group``; all ranks end
+    up in the same mode: if any rank cannot map its peers, every rank keeps the
+    two launches + ncclAllReduce per iteration.  ``world == 1`` needs no process
+    group (the plan is its own peer)."""
+    if world == 1:
+        try:
+            plan.peer_open([plan.peer_handles()])
+            return True
+        except Exception:
+            return False
+    import torch.distributed as dist
+    try:
+        blob = plan.peer_handles()
+    except Exception:  # not a wide shard plan: the NCCL path
+        blob = None
+    blobs = [None] * world
+    dist.all_gather_object(blobs, blob, group=group)
+    ok = all(b is not None for b in blobs)
+    if ok:
+        try:
+            plan.peer_open(blobs)
+        except Exception:
+            ok = False
+    flags = [None] * world
+    dist.all_gather_object(flags, ok, group=group)
+    if not all(flags):
+        if ok:
+            plan.peer_close()
+        return False
+    return True
 
-    def __init__(self, model, tree, factor, scaling=None, device: int = 0, group=None):
+
+class ShardedSolver:
+    """This rank's share of a tree solve; construct on every rank collectively.
+    With ``peer`` (default unless TSMPC_NO_PEER is set) the ranks map each other's
+    exchange buffers and every solve is one launch per rank with the cut exchange
+    inside the kernel; otherwise two launches and an ncclAllReduce per iteration."""
+
+    def __init__(self, model, tree, factor, scaling=None, device: int = 0, group=None,
+                 peer: bool | None = None):
+        import os
+
         import torch.distributed as dist
+        if peer is None:
+            peer = not os.environ.get("TSMPC_NO_PEER")
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.group = group
@@ -68,6 +112,10 @@ class ShardedSolver:
                                shard=(self.rank, self.world, nid))
         self.edges = self.plan.edges(0)
         self.trunk = self.plan.edges(1)
+        self.peer_exchange = self._open_peers(group) if peer else False
+
+    def _open_peers(self, group) -> bool:
+        return open_peer_exchange(self.plan, self.world, group)
 
     def set_cache(self, cache, model=None):
         self.plan.set_cache(cache, model)

@@ -157,3 +157,33 @@ def test_engine_solve_over_devices_matches_reference():
     g_ref = float(z["r_gap"])
     assert abs(rep.gap - g_ref) <= c.tol("gap") * max(1.0, abs(g_ref)), (rep.gap, g_ref)
     assert rep.iterations == c.iters
+
+
+@pytest.mark.parametrize("tree_name,full", [("SMPC8", True), ("SMPC8", False), ("W4k", True)])
+def test_peer_exchange_in_kernel_equals_nccl_launches(tree_name, full, monkeypatch):
+    """The cut exchange inside the persistent kernel (tsmpc_plan_peer_open: receive
+    rows and arrival counter mapped for every rank, both phases in one launch) gives
+    the bits of the two-launch + ncclAllReduce path, over repeated solves (the
+    arrival generations carry over).  One GPU: world 1, the plan is its own peer;
+    TSMPC_SHARD_FULL makes every trunk position an exchanged one (n_xch > 0)."""
+    import bench
+    if full:
+        monkeypatch.setenv("TSMPC_SHARD_FULL", "1")
+    W = bench.build_workload(tree_name)
+    iters = 30
+    th, cf = engine.theta_schedule(iters)
+    plan = DevicePlan(W["model"], W["tree"], W["factor"], W["scaling"], shard=(0, 1, nccl_unique_id()))
+    plan.set_cache(W["caches"][0], W["model"])
+    assert (plan.info()["exchange_doubles"] > 0) == full
+    a = plan.solve(W["p"], iters, 0.05, theta=th, coef=cf, record_residuals=True)
+    plan.peer_open([plan.peer_handles()])
+    assert plan.info()["peer_exchange"] == 1
+    outs = [plan.solve(W["p"], iters, 0.05, theta=th, coef=cf, record_residuals=True) for _ in range(2)]
+    for b in outs:
+        assert b["kernel_launches"] < a["kernel_launches"]
+        for f in ("u0", "x", "u", "x_avg", "u_avg", "dual_sig", "dual_zeta", "dual_psi", "resid_trace"):
+            assert np.array_equal(a[f], b[f]), f
+        assert a["gap"] == b["gap"]
+    plan.peer_close()
+    c = plan.solve(W["p"], iters, 0.05, theta=th, coef=cf, record_residuals=True)
+    assert np.array_equal(c["u_avg"], a["u_avg"]) and c["kernel_launches"] == a["kernel_launches"]

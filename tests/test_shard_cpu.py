@@ -138,3 +138,56 @@ def test_cut_exchange_w4k(world):
     rows = [set(map(int, d["edges"])) for d in ds]
     assert set().union(*rows) == set(range(t.n_edges))
     assert sum(len(r) for r in rows) == t.n_edges + (world - 1) * d0["mixed_positions"]
+
+
+class _FakePeerPlan:
+    """Stands in for a shard DevicePlan: records the peer-exchange calls."""
+
+    def __init__(self, rank, fail_open):
+        self.rank, self.fail_open, self.calls = rank, fail_open, []
+
+    def peer_handles(self):
+        self.calls.append("handles")
+        return bytes([self.rank]) * 160
+
+    def peer_open(self, blobs):
+        self.calls.append(("open", [b[0] for b in blobs]))
+        if self.fail_open:
+            raise RuntimeError("cannot map")
+
+    def peer_close(self):
+        self.calls.append("close")
+
+
+def _peer_worker(rank, world, port, fail_rank, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1604_01074_b200.shard import ShardedSolver
+        s = ShardedSolver.__new__(ShardedSolver)
+        s.rank, s.world = rank, world
+        s.plan = _FakePeerPlan(rank, rank == fail_rank)
+        on = s._open_peers(None)
+        q.put((rank, on, s.plan.calls))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_rank", [-1, 1])
+def test_peer_exchange_agreement(fail_rank):
+    """The in-kernel exchange is all-or-nothing across ranks: the blobs are
+    all-gathered in rank order and every rank opens them; if any rank cannot map
+    its peers, the ranks that did close theirs and all keep the NCCL path."""
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, fail_rank, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    for rank, on, calls in res:
+        assert calls[0] == "handles" and calls[1] == ("open", [0, 1])
+        assert on == (fail_rank < 0)
+        assert ("close" in calls) == (fail_rank >= 0 and rank != fail_rank)
