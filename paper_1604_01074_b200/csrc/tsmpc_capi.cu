@@ -2034,7 +2034,15 @@ int tsmpc_plan_trial(tsmpc_plan* pl, int32_t iters, double* ms) {
   pl->tol = tol;
   if (rc) return rc;
   CU(cudaEventRecord(pl->ev0, pl->stream));
-  if (pl->sharded) {
+  if (pl->sharded && pl->sbase.FL > 0 && !std::getenv("TSMPC_NO_PEER")) {
+    // this rank's share of a sharded solve in one launch (both phases per iteration,
+    // as with the in-kernel exchange), without the exchange itself: the per-rank
+    // compute time of a w-GPU job
+    SParams S = sparse_params(pl, st.P);
+    S.peer_rx = nullptr;
+    S.peer_cnt = nullptr;
+    CU(sparse_launch(S, LaunchWin{0, iters, 7, 0, 0}, pl->sp_ctas, pl->sp_smem, pl->stream));
+  } else if (pl->sharded) {
     // this rank's share of a sharded solve: its two launches per iteration,
     // without the cross-rank exchange (the per-rank compute time of a w-GPU job)
     SParams S = sparse_params(pl, st.P);

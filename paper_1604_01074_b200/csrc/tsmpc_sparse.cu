@@ -3236,7 +3236,9 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
   const int nt = c.mt.ntiles;
   const bool trunk = P.n_trunk > 0;
   const bool do_a = win.phase & 1, do_b = win.phase & 2;
-  const bool fused = FGK && S.sharded && (win.phase & 4) && S.peer_rx != nullptr;
+  // shard plan running both phases per iteration in this launch (the cut exchange in
+  // between over peer memory; without peer tables: a compute-only timing trial)
+  const bool fused = FGK && S.sharded && (win.phase & 4);
   const bool chain_cta = (int)blockIdx.x < S.split_c0;
   if (S.split && chain_cta && nt == 1) {
     // per chain, the sum of beta_s over its rows (static during the launch), chain order
@@ -3263,7 +3265,8 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
     __syncthreads();
   }
   // static vectors of a single-tile CTA resident in TMEM for the launch
-  if (TSMPC_TMSTATIC && nt == 1 && do_a && do_b && !S.sharded && (!S.split || chain_cta)) tm_static_fill();
+  if (TSMPC_TMSTATIC && nt == 1 && do_a && do_b && (!S.sharded || fused) && (!S.split || chain_cta))
+    tm_static_fill();
   double rmax = 0.0;
   unsigned int sub_target = 0;  // trunk-CTA barrier episodes x split_n (split mode)
   double cf = P.coef[win.nu0], th = P.theta[win.nu0];
@@ -3312,7 +3315,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
     }
     if (fused && trunk) {  // shard plan, both phases in this launch: the cut exchange in between
       grid.sync();
-      if (S.n_xch > 0) {
+      if (S.n_xch > 0 && S.peer_rx != nullptr) {
         peer_exchange(win.xgen + (unsigned long long)(nu - win.nu0));
         grid.sync();
       }
