@@ -417,17 +417,19 @@ def sharded_measure(args, ws, rank, local, dist, peer=True):
 
 def sharded_estimate(args, local, worlds=(2, 4, 8), tree=None, iters=None):
     """No multi-GPU box: the per-rank compute of a w-GPU W4k (or W16k) solve,
-    measured on this GPU.  Every rank's shard plan runs its two launches per
-    iteration (tsmpc_plan_trial, without the cross-rank exchange); a w-GPU
-    iteration costs the slowest rank's time plus one all-reduce of
-    `exchange_bytes_per_iter`."""
+    measured on this GPU.  Every rank's shard plan runs its solve as one launch
+    (tsmpc_plan_trial: both phases per iteration, without the cross-rank
+    exchange); a w-GPU iteration costs the slowest rank's time plus the in-kernel
+    exchange of `exchange_bytes_per_iter` (peer stores over NVLink, arrival wait)."""
     from paper_1604_01074_b200.plan import DevicePlan
     tree = tree or args.shard_tree
     iters = iters or args.iters
     W = build_workload(tree)
     E = W["tree"].n_edges
     out = {"tree": tree, "edges": E, "scenarios": W["tree"].n_s, "iters": iters,
-           "note": "per-rank compute only (no NCCL on one GPU); not a multi-GPU measurement"}
+           "note": "per-rank compute only: each rank's shard plan runs its whole solve in one launch "
+                   "(both phases per iteration, as with the in-kernel exchange) without the exchange "
+                   "itself; not a multi-GPU measurement"}
     for w in worlds:
         us, xb = [], 0
         for r in range(w):
