@@ -3,8 +3,9 @@
     PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden_large.py [case ...]
 
 Cases: bcn63 CE / SMPC1 / SMPC3 at 500 and 2000 APG iterations, SMPC8
-(configs[2]) at 500 and the wide W4k tree (configs[3]) at 100, all with the
-reference's own step size (``engine.compute_lambda``, ``engine.py:286-337``)
+(configs[2]) at 500, the wide W4k tree (configs[3]) at 100, all with the
+reference's own step size (``engine.compute_lambda``, ``engine.py:286-337``),
+and W16k (345,121 edges) at 20 with SMPC8's step size
 and its own ``engine.solve`` (``engine.py:485-601``), plus two small
 ``record_residuals=True`` runs whose residual and duality-gap traces
 (``engine.py:577-582``) pin ``SolveReport.residual_trace`` / ``gap_trace``.
@@ -81,7 +82,8 @@ def dev_metrics(a: np.ndarray, b: np.ndarray) -> tuple[float, float, float]:
     return blk, col, cs
 
 
-def make_case(name, tree_name, iters, record=False, calibrate=True, tree_kw=None, paper_weights=False):
+def make_case(name, tree_name, iters, record=False, calibrate=True, tree_kw=None, paper_weights=False,
+              lam=None):
     from paper_1604_01074_b200 import synth
     model = synth.bcn63_network(paper_weights=paper_weights)
     tree = synth.paper_tree(*synth.PAPER_TREES[tree_name], **(tree_kw or {}))
@@ -95,7 +97,8 @@ def make_case(name, tree_name, iters, record=False, calibrate=True, tree_kw=None
     cache = treesmpc.build_stage_cache(basis, rm, rt, demands, k=fc.k, q=q)
     scaling = R_engine.compute_preconditioner(basis, rm, rt.N, tree=rt)
     t_l = time.perf_counter()
-    lam = R_engine.compute_lambda(basis, factor, rm, rt, scaling=scaling)
+    if lam is None:
+        lam = R_engine.compute_lambda(basis, factor, rm, rt, scaling=scaling)
     t_lam = time.perf_counter() - t_l
     cfg = R_engine.SolverConfig(max_iters=iters, record_residuals=record)
     t_s = time.perf_counter()
@@ -152,7 +155,11 @@ CASES = {
     "L_bcn63_SMPC1_trace_i60": ("SMPC1", 60, True),
     # the paper's cost weights: W_alpha=2e4, Wu=1e5 I, Wx=1e7, gamma_d=5e7
     "L_bcn63pw_SMPC3_i500": ("SMPC3", 500, False, True),
+    # the largest wide tree (SURVEY §8d C4, 345,121 edges): 20 iterations at SMPC8's
+    # reference step size (the reference's compute_lambda would take ~1 h here)
+    "L_bcn63_W16k_i20": ("W16k", 20, False),
 }
+LAM = {"L_bcn63_W16k_i20": 0.4797702477755166}
 
 
 def recalibrate(name, seeds):
@@ -205,7 +212,7 @@ def main():
     only = args or list(CASES)
     for name in only:
         tree_name, iters, record, *pw = CASES[name]
-        make_case(name, tree_name, iters, record=record, paper_weights=bool(pw and pw[0]))
+        make_case(name, tree_name, iters, record=record, paper_weights=bool(pw and pw[0]), lam=LAM.get(name))
 
 
 if __name__ == "__main__":

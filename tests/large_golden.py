@@ -1,6 +1,6 @@
 """Loader / comparison helpers for the benchmark-tree goldens of
 tests/golden/make_golden_large.py (the real reference's engine.solve on bcn63
-CE / SMPC1 / SMPC3 / SMPC8 / W4k).
+CE / SMPC1 / SMPC3 / SMPC8 / W4k / W16k).
 
 Inputs are regenerated with ``synth`` and checked against the sha256 digest the
 generator stored; results are compared on the stored row sample, on the
@@ -19,7 +19,8 @@ import numpy as np
 GOLDEN = pathlib.Path(__file__).resolve().parent / "golden"
 FIELDS = ("x", "u", "x_avg", "u_avg", "dual_sig", "dual_zeta", "dual_psi")
 LARGE_CASES = ["L_bcn63_CE_i500", "L_bcn63_CE_i2000", "L_bcn63_SMPC1_i2000", "L_bcn63_SMPC3_i500",
-               "L_bcn63_SMPC3_i2000", "L_bcn63_SMPC8_i500", "L_bcn63_W4k_i100", "L_bcn63pw_SMPC3_i500"]
+               "L_bcn63_SMPC3_i2000", "L_bcn63_SMPC8_i500", "L_bcn63_W4k_i100", "L_bcn63pw_SMPC3_i500",
+               "L_bcn63_W16k_i20"]
 TRACE_CASES = ["L_bcn63_CE_trace_i150", "L_bcn63_SMPC1_trace_i60"]
 FLOOR = 1e-11
 

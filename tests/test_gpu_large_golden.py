@@ -122,7 +122,8 @@ def test_stopping_with_residual_trace():
     assert got["residual_inf"] == tr[first]
 
 
-@pytest.mark.parametrize("name,world", [("L_bcn63_W4k_i100", 8), ("L_bcn63_SMPC8_i500", 4)])
+@pytest.mark.parametrize("name,world", [("L_bcn63_W4k_i100", 8), ("L_bcn63_SMPC8_i500", 4),
+                                        ("L_bcn63_W16k_i20", 2), ("L_bcn63_W16k_i20", 8)])
 def test_sharded_cut_matches_reference(name, world):
     """The w-way split with the cut exchange (each rank computes its own subtrees'
     trunk positions, the top of the tree is replicated; tsmpc_solve_group on one
