@@ -1,3 +1,5 @@
+# W4k profiling on one B200 (run under gpurun from the repo root): plain run, phase timers of three CTAs,
+# one ncu --set full capture of the wide kernel (untuned placement) and its summary.
 set -u
 E=gpurun_out/w4k
 mkdir -p $E
