@@ -1076,11 +1076,13 @@ int peer_setup(tsmpc_plan* pl, const std::vector<double*>& rx, const std::vector
   pl->peer_on = true;
   return TSMPC_OK;
 }
-// peer exchange blob: [RX handle | RXCNT handle | ctas, rank, world, fg | exchange doubles]
+// peer exchange blob: [RX handle | RXCNT handle | ctas, rank, world, fg | exchange doubles |
+// exchange generations run so far (the ranks' arrival counters must agree)]
 struct PeerBlob {
   cudaIpcMemHandle_t rx, cnt;
   int32_t ctas, rank, world, fg;
   int64_t xn;
+  uint64_t xgen;
 };
 static_assert(sizeof(PeerBlob) <= TSMPC_PEER_BLOB_BYTES, "peer blob size");
 bool peer_capable(const tsmpc_plan* pl) {
@@ -1100,6 +1102,7 @@ int tsmpc_plan_peer_handles(const tsmpc_plan* pl, uint8_t* blob) {
   b.world = pl->world;
   b.fg = pl->sbase.FL > 0 ? 1 : 0;
   b.xn = (int64_t)pl->sbase.n_xch * pl->sbase.XCH_LD;
+  b.xgen = pl->xgen;
   std::memset(blob, 0, TSMPC_PEER_BLOB_BYTES);
   std::memcpy(blob, &b, sizeof b);
   return TSMPC_OK;
@@ -1122,10 +1125,11 @@ int tsmpc_plan_peer_open(tsmpc_plan* pl, const uint8_t* blobs, int32_t world) {
   for (int p = 0; p < world; ++p) {
     PeerBlob b;
     std::memcpy(&b, blobs + (size_t)p * TSMPC_PEER_BLOB_BYTES, sizeof b);
-    if (b.rank != p || b.world != world || b.ctas != pl->sp_ctas || b.xn != xn || !b.fg) {
+    if (b.rank != p || b.world != world || b.ctas != pl->sp_ctas || b.xn != xn || !b.fg || b.xgen != pl->xgen) {
       undo();
-      return fail(TSMPC_ERR_VALIDATION, "peer %d: plan mismatch (rank %d, world %d, %d CTAs, %lld exchange doubles)",
-                  p, b.rank, b.world, b.ctas, (long long)b.xn);
+      return fail(TSMPC_ERR_VALIDATION,
+                  "peer %d: plan mismatch (rank %d, world %d, %d CTAs, %lld exchange doubles, generation %llu)", p,
+                  b.rank, b.world, b.ctas, (long long)b.xn, (unsigned long long)b.xgen);
     }
     if (p == pl->rank) {
       rx[p] = pl->RX;
