@@ -95,7 +95,7 @@ cudaError_t sparse_launch(const SParams& S, LaunchWin w, int ctas, size_t smem, 
 cudaError_t sparse_params_upload(const SParams& S, cudaStream_t stream);
 cudaError_t sparse_note_launch(cudaStream_t stream);
 const void* sparse_kernel_fn(int wide, int nx, bool fg);
-__global__ void beta_rotate_kernel(const double* __restrict__ beta, const double* __restrict__ M, double* out,
-                                   int E, int nv, int NVP);
+__global__ void beta_rotate_kernel(const double* __restrict__ beta, const int* __restrict__ mc,
+                                   const double* __restrict__ mv, double* out, int E, int nv, int NVP);
 
 }  // namespace tsmpc

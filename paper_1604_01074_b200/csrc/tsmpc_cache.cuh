@@ -22,9 +22,19 @@ struct CacheArgs {
   const double* q;                 // nu
   // outputs
   double *uhat, *evec, *beta, *jrhs, *gdd;
+  // the same operators by row without their zeros (CSR, ascending columns: the
+  // dense summation order), used by cache_rows_sparse_kernel
+  const int *pm_ptr, *pm_idx, *ed_ptr, *ed_idx, *b_ptr, *b_idx, *gd_ptr, *gd_idx;
+  const double *pm_val, *ed_val, *b_val, *gd_val;
 };
 
+#ifndef TSMPC_CB
+#define TSMPC_CB 4
+#endif
+constexpr int kCB = TSMPC_CB;  // edges per pass of cache_beta_kernel
+
 __global__ void cache_rows_kernel(CacheArgs a);
+__global__ void cache_rows_sparse_kernel(CacheArgs a);
 __global__ void cache_beta_kernel(CacheArgs a);
 
 }  // namespace tsmpc

@@ -86,11 +86,16 @@ struct tsmpc_plan {
   int sp_ctas = 0, sp_resident = 0, sp_tiles = 0, sp_trunk = 0;
   size_t sp_smem = 0;
   double *BETA_S = nullptr, *TG = nullptr, *FG = nullptr, *KY_S = nullptr, *MS = nullptr;
+  int* MSC = nullptr;  // the basis rotation M by column without zeros: [ptr (nv+1) | rows], values in MS
   std::string sp_why;
   // device stage cache (tsmpc_set_cache_operators / tsmpc_set_forecast)
   bool has_cache_ops = false;
   int nd_c = 0;
   double *PART_MAP = nullptr, *GD = nullptr, *ED = nullptr, *RHAT = nullptr, *EPS = nullptr, *PBAR = nullptr;
+  // the stage cache operators part_map, Ed, B, Gd in CSR (device): ints, values, offsets
+  int* CSR_I = nullptr;
+  double* CSR_V = nullptr;
+  int csr_oi[8] = {0}, csr_ov[4] = {0};
   double *DHAT = nullptr, *ABAR = nullptr;
   double* last_y = nullptr;  // final dual of the last solve (device warm start)
   int *d_est_c = nullptr, *d_anc_c = nullptr, *d_cs_c = nullptr, *d_ce_c = nullptr;
@@ -814,7 +819,21 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
         rc |= pl->upload(&d_ts, hp.tsched.data(), hp.tsched.size());
         rc |= pl->upload(&d_spi, hp.spi.data(), hp.spi.size());
         rc |= pl->upload(&d_spv, hp.spv.data(), hp.spv.size());
-        rc |= pl->upload(&pl->MS, pb->Ms, (size_t)nv * nv);
+        {  // M (structured basis = L M) by column, zeros dropped: beta_s = beta M per edge
+          std::vector<int> mc(1, 0), mr;
+          std::vector<double> mv;
+          for (int k = 0; k < nv; ++k) {
+            for (int j = 0; j < nv; ++j)
+              if (pb->Ms[(size_t)j * nv + k] != 0.0) {
+                mr.push_back(j);
+                mv.push_back(pb->Ms[(size_t)j * nv + k]);
+              }
+            mc.push_back((int)mr.size());
+          }
+          mc.insert(mc.end(), mr.begin(), mr.end());
+          rc |= pl->upload(&pl->MSC, mc.data(), mc.size());
+          rc |= pl->upload(&pl->MS, mv.data(), std::max<size_t>(1, mv.size()));
+        }
         rc |= pl->alloc(&pl->TG, (size_t)E * NVP);
         if (hp.S.FL > 0) rc |= pl->alloc(&pl->FG, (size_t)E * hp.S.FL);
         rc |= pl->alloc(&pl->KY_S, (size_t)std::max(1, hp.n_trunk) * P.KY_LD);
@@ -1299,8 +1318,8 @@ int tsmpc_set_cache(tsmpc_plan* pl, const double* beta, const double* uhat, cons
   rc |= pl->put_rows(pl->EVEC, pl->NXP, evec, pl->nx, E);
   if (rc) return rc;
   if (pl->use_sparse) {
-    beta_rotate_kernel<<<std::max(1, std::min((E + 7) / 8, 148 * 8)), 256, 0, pl->stream>>>(pl->BETA, pl->MS,
-                                                                                         pl->BETA_S, E, pl->nv, pl->NVP);
+    beta_rotate_kernel<<<std::max(1, std::min((pl->E * pl->nv + 255) / 256, pl->sm_count * 16)), 256, 0,
+                         pl->stream>>>(pl->BETA, pl->MSC, pl->MS, pl->BETA_S, pl->E, pl->nv, pl->NVP);
     CU(cudaGetLastError());
   }
   CU(cudaMemcpyAsync(pl->Q, q, sizeof(double) * pl->nu, cudaMemcpyHostToDevice, pl->stream));
@@ -1343,6 +1362,38 @@ int tsmpc_set_cache_operators(tsmpc_plan* pl, int32_t n_d, const double* part_ma
   CU(up(pl->RHAT, Rhat, (size_t)pl->nu * pl->nv));
   CU(up(pl->EPS, eps_edge, (size_t)pl->E * n_d));
   CU(up(pl->PBAR, pbar, (size_t)pl->E));
+  {
+    // CSR of part_map (nu x nd), Ed (ne x nd), B (nx x nu), Gd (nx x nd), rows in order
+    std::vector<double> Bh((size_t)pl->nx * pl->nu);
+    CU(cudaMemcpyAsync(Bh.data(), pl->d_B_c, Bh.size() * sizeof(double), cudaMemcpyDeviceToHost, pl->stream));
+    CU(cudaStreamSynchronize(pl->stream));
+    std::vector<int> ci;
+    std::vector<double> cv;
+    auto csr = [&](const double* M, int rows, int cols, int slot) {
+      pl->csr_oi[2 * slot] = (int)ci.size();
+      std::vector<int> ptr(rows + 1, 0), idx;
+      for (int r = 0; r < rows; ++r) {
+        for (int k = 0; k < cols; ++k)
+          if (M[(size_t)r * cols + k] != 0.0) {
+            idx.push_back(k);
+            cv.push_back(M[(size_t)r * cols + k]);
+          }
+        ptr[r + 1] = (int)idx.size();
+      }
+      pl->csr_ov[slot] = (int)cv.size() - (int)idx.size();
+      ci.insert(ci.end(), ptr.begin(), ptr.end());
+      pl->csr_oi[2 * slot + 1] = (int)ci.size();
+      ci.insert(ci.end(), idx.begin(), idx.end());
+    };
+    csr(part_map, pl->nu, n_d, 0);
+    csr(Ed, pl->ne, n_d, 1);
+    csr(Bh.data(), pl->nx, pl->nu, 2);
+    csr(Gd, pl->nx, n_d, 3);
+    // (a new upload each call: an earlier pattern may have been smaller)
+    int rc = pl->upload(&pl->CSR_I, ci.data(), ci.size());
+    rc |= pl->upload(&pl->CSR_V, cv.data(), std::max<size_t>(1, cv.size()));
+    if (rc) return rc;
+  }
   CU(cudaStreamSynchronize(pl->stream));
   pl->has_cache_ops = true;
   return TSMPC_OK;
@@ -1367,17 +1418,29 @@ int tsmpc_set_forecast(tsmpc_plan* pl, const double* dhat, const double* q, cons
   a.dhat = pl->DHAT; a.abar = pl->ABAR; a.q = pl->Q;
   a.uhat = pl->UHAT; a.evec = pl->EVEC; a.beta = pl->BETA; a.jrhs = pl->JRHS; a.gdd = pl->GDD;
   const int grid = std::max(1, std::min(pl->E, pl->sm_count * 8));
-  cache_rows_kernel<<<grid, 128, sizeof(double) * (nd + pl->nu), pl->stream>>>(a);
+  if (pl->CSR_I && !std::getenv("TSMPC_DENSE_CACHE")) {
+    const int* I = pl->CSR_I;
+    const double* V = pl->CSR_V;
+    a.pm_ptr = I + pl->csr_oi[0]; a.pm_idx = I + pl->csr_oi[1]; a.pm_val = V + pl->csr_ov[0];
+    a.ed_ptr = I + pl->csr_oi[2]; a.ed_idx = I + pl->csr_oi[3]; a.ed_val = V + pl->csr_ov[1];
+    a.b_ptr = I + pl->csr_oi[4]; a.b_idx = I + pl->csr_oi[5]; a.b_val = V + pl->csr_ov[2];
+    a.gd_ptr = I + pl->csr_oi[6]; a.gd_idx = I + pl->csr_oi[7]; a.gd_val = V + pl->csr_ov[3];
+    const int grid_s = std::max(1, std::min(pl->E, pl->sm_count * 16));
+    cache_rows_sparse_kernel<<<grid_s, 128, sizeof(double) * (nd + pl->nu), pl->stream>>>(a);
+  } else {
+    cache_rows_kernel<<<grid, 128, sizeof(double) * (nd + pl->nu), pl->stream>>>(a);
+  }
   CU(cudaGetLastError());
-  cache_beta_kernel<<<grid, 128, sizeof(double) * pl->nu, pl->stream>>>(a);
+  cache_beta_kernel<<<std::max(1, std::min((pl->E + kCB - 1) / kCB, pl->sm_count * 8)), 128,
+                      sizeof(double) * kCB * pl->nu, pl->stream>>>(a);
   CU(cudaGetLastError());
   if (pl->use_sparse) {
-    beta_rotate_kernel<<<std::max(1, std::min((pl->E + 7) / 8, 148 * 8)), 256, 0, pl->stream>>>(pl->BETA, pl->MS,
-                                                                                              pl->BETA_S, pl->E,
-                                                                                              pl->nv, pl->NVP);
+    beta_rotate_kernel<<<std::max(1, std::min((pl->E * pl->nv + 255) / 256, pl->sm_count * 16)), 256, 0,
+                         pl->stream>>>(pl->BETA, pl->MSC, pl->MS, pl->BETA_S, pl->E, pl->nv, pl->NVP);
     CU(cudaGetLastError());
   }
-  CU(cudaStreamSynchronize(pl->stream));
+  // no host wait: the solve that reads the cache is queued behind it on the same
+  // stream (the pageable inputs are staged before cudaMemcpyAsync returns)
   pl->has_cache = true;
   return TSMPC_OK;
 }

@@ -3495,18 +3495,20 @@ cudaError_t sparse_launch(const SParams& S, LaunchWin w, int ctas, size_t smem, 
 }
 
 // beta_s = beta M (rows of the stage cache mapped to the structured basis,
-// elimination.py:156-157 with L replaced by Ls = L M).  One warp per edge row.
-__global__ void beta_rotate_kernel(const double* __restrict__ beta, const double* __restrict__ M, double* out,
-                                   int E, int nv, int NVP) {
-  const int lane = threadIdx.x & 31;
-  for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < E; e += (gridDim.x * blockDim.x) >> 5) {
+// elimination.py:156-157 with L replaced by Ls = L M).  A thread per (edge, column
+// k); M by column without its zeros (mc = [ptr | rows], mv values, rows ascending:
+// the dense product's order, skipped terms are fma(b, 0, s) = s).
+__global__ void beta_rotate_kernel(const double* __restrict__ beta, const int* __restrict__ mc,
+                                   const double* __restrict__ mv, double* out, int E, int nv, int NVP) {
+  const int* rows = mc + nv + 1;
+  const long long total = (long long)E * nv;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int e = (int)(i / nv), k = (int)(i - (long long)e * nv);
     const double* b = beta + (size_t)e * NVP;
-    for (int k = lane; k < nv; k += 32) {
-      double s = 0.0;
-#pragma unroll 1
-      for (int j = 0; j < nv; ++j) s = fma(b[j], M[(size_t)j * nv + k], s);
-      out[(size_t)e * NVP + k] = s;
-    }
+    double s = 0.0;
+    for (int q = mc[k]; q < mc[k + 1]; ++q) s = fma(b[rows[q]], mv[q], s);
+    out[(size_t)e * NVP + k] = s;
   }
 }
 

@@ -83,3 +83,24 @@ def test_device_stage_cache_matches_host(name):
     host = build_stage_cache(c.basis, c.model, c.tree, node_demands(c.tree, c.forecast),
                              k=c.forecast.k, q=c.q)
     assert rel_err(beta, host.beta) <= 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["bcn63_SMPC1_N24", "small_s4"])
+def test_sparse_stage_cache_equals_dense(name, monkeypatch):
+    """The stage-cache rows with the operators in CSR (cache_rows_sparse_kernel,
+    default) give the dense kernel's bits (TSMPC_DENSE_CACHE): only fma(0, d, s)
+    terms are skipped."""
+    if not has_gpu():
+        pytest.skip("no CUDA device")
+    from paper_1604_01074_b200.plan import DevicePlan
+    c = load_case(name)
+    got = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("TSMPC_DENSE_CACHE", env)
+        plan = DevicePlan(c.model, c.tree, c.factor, c.scaling)
+        plan.set_forecast(c.forecast, c.q, c.basis, c.model)
+        got.append(plan.get_cache())
+    for a, b in zip(*got):
+        assert np.array_equal(a, b)
