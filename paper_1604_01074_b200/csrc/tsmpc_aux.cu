@@ -697,10 +697,8 @@ __global__ void __launch_bounds__(256) gap_dykstra_comp_kernel(EdgeCtx c, const 
 
 // The same per-(edge, junction row) Dykstra in two passes, for grids too large to be
 // co-resident (SMPC8: 178k components): pass 1 runs every component's sweeps and
-// records the per-sweep maxima over all edges (warp, CTA, then one global atomic per
-// CTA and sweep); a component stops at the first sweep that provably leaves its flows
-// unchanged for good (see dyk_item_sweep): that sweep's change and every later one
-// are exactly zero.  Pass 2 reads the
+// records which sweeps change some flow by >= 1e-13 (the stopping criterion needs no
+// more than that).  Pass 2 reads the
 // stopping sweep K (the first whose maximum is < 1e-13) and reruns every component
 // from its start for K + 1 sweeps (all 200 when none stops) before the final affine
 // projection.  Per element the operations are those of gap_dykstra_comp_kernel, so
@@ -766,16 +764,22 @@ __device__ __forceinline__ double dyk_item_sweep(DykItem& it, bool* fixed) {
 }
 }  // namespace
 
+// Pass 1 records only which sweeps have a change >= 1e-13 somewhere (a bit per sweep,
+// OR-reduced per warp every 32 sweeps, then per CTA, then globally in the words after
+// the value slots): the stopping sweep K is the first sweep without one, exactly the
+// first whose maximum over all edges is < 1e-13.
+constexpr int kDykWords = (kDykMax + 31) / 32;
 __global__ void __launch_bounds__(256) gap_dykstra_comp_pass1_kernel(EdgeCtx c, const DykComp* __restrict__ comps,
                                                                      int ncomp, const int* __restrict__ free_u,
                                                                      int nfree, const double* __restrict__ u0,
                                                                      unsigned long long* slots, double* uf) {
-  __shared__ unsigned long long cta_max[kDykMax];
+  __shared__ unsigned cta_bits[kDykWords];
+  unsigned* gbits = reinterpret_cast<unsigned*>(slots + kDykMax);
   const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
   const int lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < kDykMax; i += blockDim.x) cta_max[i] = 0ull;
+  for (int i = threadIdx.x; i < kDykWords; i += blockDim.x) cta_bits[i] = 0u;
   __syncthreads();
-  {  // flows no junction touches: clip(x0) after one sweep (sweep-0 maximum only)
+  {  // flows no junction touches: clip(x0) after one sweep (sweep 0 only)
     double m0 = 0.0;
     for (int i = tid; i < c.E * nfree; i += nth) {
       const int e = i / nfree, j = free_u[i - e * nfree];
@@ -785,8 +789,7 @@ __global__ void __launch_bounds__(256) gap_dykstra_comp_pass1_kernel(EdgeCtx c, 
       m0 = fmax(m0, fabs(xn - x0));
       uf[(size_t)e * c.NUP + j] = xn - 0.0;
     }
-    m0 = warp_max(m0);
-    if (lane == 0 && m0 > 0.0) atomicMax(cta_max, (unsigned long long)__double_as_longlong(m0));
+    if (__any_sync(0xffffffffu, m0 >= 1e-13) && lane == 0) atomicOr(cta_bits, 1u);
   }
   const long long total = (long long)c.E * ncomp;
   // warp-uniform trip count: every lane of a warp runs the same number of items
@@ -800,22 +803,22 @@ __global__ void __launch_bounds__(256) gap_dykstra_comp_pass1_kernel(EdgeCtx c, 
       const int e = (int)(item / ncomp);
       dyk_item_load(c, comps[item - (long long)e * ncomp], e, u0, it);
     }
-    bool done = !active;
+    unsigned bits = 0u;
+#pragma unroll 1
     for (int s = 0; s < kDykMax; ++s) {
-      if (__all_sync(0xffffffffu, done)) break;  // later sweeps repeat with zero change
-      double mx = 0.0;
-      if (!done) {
-        bool fixed;
-        mx = dyk_item_sweep(it, &fixed);
-        done = fixed;
+      bool fixed;
+      const double mx = active ? dyk_item_sweep(it, &fixed) : 0.0;
+      if (mx >= 1e-13) bits |= 1u << (s & 31);
+      if ((s & 31) == 31 || s == kDykMax - 1) {
+        const unsigned w = __reduce_or_sync(0xffffffffu, bits);
+        if (lane == 0 && w) atomicOr(cta_bits + (s >> 5), w);
+        bits = 0u;
       }
-      mx = warp_max(mx);
-      if (lane == 0 && mx > 0.0) atomicMax(cta_max + s, (unsigned long long)__double_as_longlong(mx));
     }
   }
   __syncthreads();
-  for (int s = threadIdx.x; s < kDykMax; s += blockDim.x)
-    if (cta_max[s] != 0ull) atomicMax(slots + s, cta_max[s]);
+  for (int i = threadIdx.x; i < kDykWords; i += blockDim.x)
+    if (cta_bits[i]) atomicOr(gbits + i, cta_bits[i]);
 }
 
 __global__ void __launch_bounds__(256) gap_dykstra_comp_pass2_kernel(EdgeCtx c, const DykComp* __restrict__ comps,
@@ -824,9 +827,10 @@ __global__ void __launch_bounds__(256) gap_dykstra_comp_pass2_kernel(EdgeCtx c, 
                                                                      double* uf) {
   __shared__ int s_sweeps;
   if (threadIdx.x == 0) {
+    const unsigned* gbits = reinterpret_cast<const unsigned*>(slots + kDykMax);
     int K = -1;
     for (int it = 0; it < kDykMax && K < 0; ++it)
-      if (__longlong_as_double((long long)slots[it]) < 1e-13) K = it;
+      if (!((gbits[it >> 5] >> (it & 31)) & 1u)) K = it;
     s_sweeps = K >= 0 ? K + 1 : kDykMax;
   }
   __syncthreads();
