@@ -41,13 +41,12 @@ class _StepModel:
 
 
 def _check_dual_shapes(tree, factor, w):
-    n_e = tree.n_edges
-    if w.sig.shape != (n_e, factor.n_x) or w.zeta.shape != (n_e, factor.n_x):
-        raise DimensionError(
-            f"dual state copies shaped {w.sig.shape}, expected ({n_e}, {factor.n_x})")
-    if w.psi.shape != (n_e, factor.n_u):
-        raise DimensionError(
-            f"dual input copy shaped {w.psi.shape}, expected ({n_e}, {factor.n_u})")
+    """Every block of the dual bundle has one row per edge (DimensionError otherwise)."""
+    widths = {"sig": factor.n_x, "zeta": factor.n_x, "psi": factor.n_u}
+    for block, width in widths.items():
+        got = np.shape(getattr(w, block))
+        if got != (tree.n_edges, width):
+            raise DimensionError(f"dual block {block}: shape {got}, expected ({tree.n_edges}, {width})")
 
 
 class SolveContext:
@@ -110,13 +109,14 @@ def _step_plan(factor, tree, device: int) -> DevicePlan:
 def solve_step(factor, cache, tree, w: DualPoint, p, q=None, threads: int = 1) -> PrimalPoint:
     """Exact minimiser of <z, H'w> + f(z) over the tree, fresh arrays (``factor.py:198-217``)."""
     _check_dual_shapes(tree, factor, w)
-    if cache.beta.shape[0] != tree.n_edges:
-        raise DimensionError("stage cache does not match the tree shape")
     p = np.asarray(p, dtype=float)
-    if p.shape != (factor.n_x,):
-        raise DimensionError(f"p: shape {p.shape}, expected ({factor.n_x},)")
-    if q is not None and not np.array_equal(np.asarray(q, dtype=float), cache.q):
-        raise DimensionError("q differs from the control the cache was built with")
+    checks = ((cache.beta.shape[0] == tree.n_edges, "the stage cache belongs to another tree"),
+              (p.shape == (factor.n_x,), f"initial state of shape {p.shape}, expected ({factor.n_x},)"),
+              (q is None or np.array_equal(np.asarray(q, dtype=float), cache.q),
+               "q is not the control the stage cache was built with"))
+    for ok, msg in checks:
+        if not ok:
+            raise DimensionError(msg)
     with SolveContext(factor, tree, threads=threads) as ctx:
         z = ctx.solve(cache, w, p)
         return PrimalPoint(z.x.copy(), z.u.copy())
