@@ -720,7 +720,7 @@ static tsmpc_plan* plan_create_impl(const tsmpc_problem* pb, int device, int sra
   rc |= pl->alloc(&pl->RED, 16);
   rc |= pl->alloc(&pl->ABORT, 1);
   rc |= pl->alloc(&pl->DYK, 256);
-  rc |= pl->alloc(&pl->TIMERS, 16);
+  rc |= pl->alloc(&pl->TIMERS, 16 + 8 * 256);  // phase timers + timeline stamps (timer builds)
   int *d_te = nullptr, *d_tsp = nullptr, *d_tpos = nullptr, *d_pp = nullptr, *d_pl = nullptr,
       *d_tc0 = nullptr, *d_tpar = nullptr;
   double *d_MTf = nullptr, *d_KY = nullptr, *d_OUT = nullptr;
@@ -1300,10 +1300,10 @@ int tsmpc_plan_info(const tsmpc_plan* pl, int64_t* info, int32_t n) {
 
 int tsmpc_debug_timers(tsmpc_plan* pl, uint64_t* out, int32_t n) {
   if (!pl || !out) return fail(TSMPC_ERR_ARGUMENT, "null argument");
-  unsigned long long t[16];
-  CU(cudaMemcpy(t, pl->TIMERS, sizeof(t), cudaMemcpyDeviceToHost));
-  CU(cudaMemset(pl->TIMERS, 0, sizeof(t)));
-  for (int i = 0; i < n && i < 16; ++i) out[i] = t[i];
+  std::vector<unsigned long long> t(16 + 8 * 256);
+  CU(cudaMemcpy(t.data(), pl->TIMERS, t.size() * sizeof(t[0]), cudaMemcpyDeviceToHost));
+  CU(cudaMemset(pl->TIMERS, 0, t.size() * sizeof(t[0])));
+  for (int i = 0; i < n && i < (int)t.size(); ++i) out[i] = t[i];
   return TSMPC_OK;
 }
 

@@ -257,8 +257,20 @@ struct LaunchWin {
       (t) = now_;                                                             \
     }                                                                         \
   } while (0)
+// Timeline stamps (profiling builds): %globaltimer of point k of every CTA, for the
+// iteration the kernel marks traced (slots 16 + 8 CTA + k of the timer buffer;
+// tools/trace_probe.py).
+#define TSMPC_STAMP(P, k, on)                                                 \
+  do {                                                                        \
+    if ((on) && threadIdx.x == 0 && (P).timers) {                             \
+      unsigned long long g_;                                                  \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_));                 \
+      (P).timers[16 + 8 * blockIdx.x + (k)] = g_;                             \
+    }                                                                         \
+  } while (0)
 #else
 #define TSMPC_MARK(P, k, t) do { } while (0)
+#define TSMPC_STAMP(P, k, on) do { } while (0)
 #endif
 
 }  // namespace tsmpc

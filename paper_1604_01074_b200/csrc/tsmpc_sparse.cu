@@ -50,6 +50,7 @@ extern __shared__ __align__(16) double s_dyn[];
 __constant__ SParams g_sp;
 // the launch window of the running kernel (set from the kernel argument at entry)
 __shared__ LaunchWin s_win;
+__shared__ int s_trace_on;  // timer builds: this iteration is the traced one
 // meta windows (SParams::rows_window): first row / segment of the staged tile
 __shared__ int s_row_off, s_seg_off;
 
@@ -2421,6 +2422,7 @@ __device__ __noinline__ void bwd_wide(int ti, double cf, int cur, int pf) {
       }
     }
     signal_arrive(S.sub_ctr + 1);
+    TSMPC_STAMP(P, 5, s_trace_on);
   }
   // (2) xiq scan, tail -> head, every chain of the tile at once
 #pragma unroll 1
@@ -3277,6 +3279,12 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
                      (((int)(c.A() - s_dyn) | (int)(c.B() - s_dyn) | c.LA | c.NXP | c.NUP | S.FL) & 1) == 0;
   for (int nu = win.nu0; nu < win.nu1; ++nu) {
     const int cur = (P.slot0 + nu) & 1;
+    const bool trace = nu == (win.nu0 + win.nu1) / 2;  // timeline stamps (timer builds)
+    (void)trace;
+#ifdef TSMPC_TIMERS
+    if (threadIdx.x == 0) s_trace_on = trace;  // read after the phases' barriers
+#endif
+    TSMPC_STAMP(P, 0, trace);
     if (P.tol > 0.0 && !S.sharded && nu > win.nu0 && nu % P.check_every == 0) {
       // stopping test on the residual of iteration nu - 1 (its state is in HBM)
       grid.sync();
@@ -3304,6 +3312,7 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
         if (FGK && S.rows_window) win_stage(t);
         s_tm_on ? bwd_wide<true, FGK>(t, cf, cur, pf) : bwd_wide<false, FGK>(t, cf, cur, pf);
       }
+      TSMPC_STAMP(P, 1, trace);
       if (S.sharded && trunk) {
         grid.sync();
         head_prereduce();
@@ -3333,7 +3342,9 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
           s_tm_on ? fwd_wide<XS, true, FGK>(t, nu, cf, th, cur, &rmax, 0, 0.0)
                   : fwd_wide<XS, false, FGK>(t, nu, cf, th, cur, &rmax, 0, 0.0);
         TSMPC_MARK(P, 10, tb_);
+        TSMPC_STAMP(P, 2, trace);
         signal_wait(S.sub_ctr + 2, it * (unsigned)S.split_n);
+        TSMPC_STAMP(P, 3, trace);
         TSMPC_MARK(P, 9, tb_);
         if (blockIdx.x == 0) {
           const double om = __dsub_rn(1.0, th);
@@ -3342,21 +3353,28 @@ __global__ void __launch_bounds__(kThreadsS, 1) apg_wide_kernel(LaunchWin win) {
         }
         for (int t = 0; t < nt; ++t)
           fwd_finish_wide<XS>(t, nu, cf, th, cur, &rmax, S.wide_prefill && t == nt - 1 && nu + 1 < win.nu1, cf_n);
+        TSMPC_STAMP(P, 4, trace);
         TSMPC_MARK(P, 3, tb_);
       } else {
         // the previous iteration's trunk-row epilogues (dual rows the sweep reads)
         if (nu > win.nu0) trunk_barrier(S.sub_ctr, (unsigned)S.split_n, sub_target);
         trunk_sweep(cf, cur, 1);  // own terms, before the heads arrive
+        TSMPC_STAMP(P, 1, trace);
         signal_wait(S.sub_ctr + 1, it * (unsigned)S.split_c0);
+        TSMPC_STAMP(P, 2, trace);
         TSMPC_MARK(P, 9, tb_);
         trunk_sweep(cf, cur, 2);
+        TSMPC_STAMP(P, 3, trace);
         TSMPC_MARK(P, 10, tb_);
         trunk_barrier(S.sub_ctr, (unsigned)S.split_n, sub_target);
+        TSMPC_STAMP(P, 4, trace);
         TSMPC_MARK(P, 11, tb_);
         trunk_needs();
         signal_arrive(S.sub_ctr + 2);
+        TSMPC_STAMP(P, 5, trace);
         TSMPC_MARK(P, 12, tb_);
         trunk_own_rows_wide<XS>(nu, cf, th, cur, &rmax);
+        TSMPC_STAMP(P, 6, trace);
         TSMPC_MARK(P, 3, tb_);
       }
     } else if (do_b) {
