@@ -2353,6 +2353,7 @@ __device__ __noinline__ void bwd_wide(int ti, double cf, int cur, int pf) {
   }
   TSMPC_MARK(P, 0, tm_);
   const double* adiag = c.adiag();
+  TSMPC_STAMP(P, 6, s_trace_on);
   if (S.split) {
     // split mode: the trunk needs only each chain's head values, linear in the fill
     // (see bwd_tile):  xiq_head = sum_d a^d s_d,  g_head = sum beta_s + Ls'(sum psi^ + B' sum_d G_d s_d).
@@ -2389,6 +2390,7 @@ __device__ __noinline__ void bwd_wide(int ti, double cf, int cur, int pf) {
       }
     }
     __syncthreads();
+    TSMPC_STAMP(P, 7, s_trace_on);
     {
       const int* cp = c.spi + S.Bc_ptr;
       const int* ci = c.spi + S.Bc_idx;

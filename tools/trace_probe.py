@@ -32,7 +32,7 @@ st = buf[16:16 + 8 * C].reshape(C, 8).astype(np.float64)
 t0 = st[:, 0][st[:, 0] > 0].min()
 rel = np.where(st > 0, (st - t0) / 1e3, np.nan)
 chain, trunk = rel[:C - tc], rel[C - tc:]
-names_c = {0: "start", 5: "heads published", 1: "backward done", 2: "zero-input fwd done", 3: "TR received",
+names_c = {0: "start", 6: "backward entered", 7: "head sums phase 1", 5: "heads published", 1: "backward done", 2: "zero-input fwd done", 3: "TR received",
            4: "finish done"}
 names_t = {0: "start", 1: "own terms done", 2: "heads received", 3: "sweep done", 4: "trunk barrier",
            5: "TR published", 6: "trunk-row epilogues done"}
